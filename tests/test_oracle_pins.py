@@ -1,0 +1,514 @@
+"""Pins for the CPU oracle (-m "not gpu").
+
+Each test fixes the oracle against something other than itself: values the
+paper / SPEC print (tests/golden/), closed forms derived by hand from the
+statics, textbook identities (RK4 on an LTI system == the polynomial
+propagator; convergence to the matrix-exponential solution), invariants
+(fixed point, linearity in pulse heights, world-size invariance), published
+known-answer vectors (Philox) and brute force on tiny grids.  Pin labels
+P1..P12b follow SURVEY.md 8(c).
+"""
+import math
+
+import numpy as np
+import pytest
+import scipy.linalg
+
+import oracle
+import workloads as W
+from conftest import read_golden_kv, read_golden_table
+
+I = W.IDX
+
+
+def A_and_b(p, n_ag, n_ant, tau_ag, tau_ant):
+    """Continuous-time A, b of the (linear) plant, probed column by column from
+    the oracle RHS: rhs(y) = A y + b.  Independent of the RK4 code."""
+    z = np.zeros(6)
+    b = oracle.rhs(p, z, n_ag, n_ant, tau_ag, tau_ant)
+    A = np.stack([oracle.rhs(p, np.eye(6)[j], n_ag, n_ant, tau_ag, tau_ant) - b for j in range(6)], 1)
+    return A, b
+
+
+def phase_inputs(p, Aprime):
+    lv = oracle.step_levels(p, Aprime)
+    pulse = (p[I["N_SAC_AG"]], p[I["N_SAC_ANT"]], p[I["TAU_AC_AG"]], p[I["TAU_AC_ANT"]])
+    post = (lv[0], lv[1], p[I["TAU_DE_AG"]], p[I["TAU_DE_ANT"]])
+    return pulse, post
+
+
+# --------------------------------------------------------------------------- P1
+def test_p1_table1_defaults_match_paper():
+    rows = read_golden_table("table1_defaults.txt")
+    assert [r[0] for r in rows] == list(W.PARAM_NAMES)
+    for (name, val), d in zip(rows, W.TABLE1_DEFAULTS):
+        if name == "PW":
+            assert math.isnan(d)
+        else:
+            assert float(val) == d, name
+
+
+def test_p1_table2_defaults_match_paper():
+    rows = read_golden_table("table2_defaults.txt")
+    assert tuple(r[0] for r in rows) == W.TABLE2_NAMES
+    assert tuple(float(r[1]) for r in rows) == W.TABLE2_DEFAULTS
+
+
+# --------------------------------------------------------------------------- P2/P3
+def test_p2_symmetric_equilibrium_node_length():
+    g = read_golden_kv("spec_worked_examples.txt")
+    y = oracle.equilibrium(W.truth_opc(), 14.0, 14.0)
+    assert y[0] == 0.0 and y[1] == 0.0
+    assert round(y[2], 6) == g["equilibrium_x_m_defaults"]
+    assert round(y[3], 6) == g["equilibrium_x_m_defaults"]
+    assert y[4] == 14.0 and y[5] == 14.0
+
+
+def test_p3_pulse_onset_activation_slope_units():
+    """df_AG/dt at onset = (55 - 14)/11.7 g/ms: catches ms/s bugs."""
+    g = read_golden_kv("spec_worked_examples.txt")
+    p = W.truth_opc()
+    y = oracle.equilibrium(p, 14.0, 14.0)
+    dy = oracle.rhs(p, y, p[I["N_SAC_AG"]], p[I["N_SAC_ANT"]], p[I["TAU_AC_AG"]], p[I["TAU_AC_ANT"]])
+    # RHS is per second; SPEC quotes g/ms.
+    assert round(dy[4] * 1e-3, 3) == g["onset_dfAG_dt_g_per_ms"]
+    assert dy[4] == pytest.approx(41.0 / 11.7e-3, rel=1e-14)
+    # equilibrium mechanics do not move at the onset instant
+    assert np.all(np.abs(dy[:4]) < 1e-12)
+
+
+def test_activation_eigenvalues_are_minus_one_over_tau():
+    """The f_m rows are first-order lags: eigenvalues -1/tau (s^-1)."""
+    p = W.truth_opc()
+    A, _ = A_and_b(p, 0, 0, p[I["TAU_AC_AG"]], p[I["TAU_AC_ANT"]])
+    ev = np.sort(np.linalg.eigvals(A).real)
+    for tau in (11.7e-3, 2.4e-3):
+        assert np.min(np.abs(ev + 1.0 / tau)) < 1e-6 / tau
+    # defaults: continuous plant is stable (all eigenvalues real and negative)
+    assert np.all(ev < 0)
+
+
+# --------------------------------------------------------------------------- statics
+def _random_physical(n, seed=11):
+    rng = np.random.default_rng(seed)
+    d = W.truth_opc()
+    out = []
+    for _ in range(n):
+        p = d * np.exp(rng.uniform(np.log(0.5), np.log(2.0), size=18))
+        p[I["PW"]] = rng.uniform(5, 60)
+        out.append(p)
+    return out
+
+
+def test_equilibrium_is_zero_of_rhs_for_any_physical_opc_and_drive():
+    """Hand-derived statics: theta_ss = (g_AG n_AG - g_ANT n_ANT)/G
+    makes every derivative vanish, for asymmetric muscles too (Q5)."""
+    rng = np.random.default_rng(3)
+    for p in _random_physical(50):
+        n_ag, n_ant = rng.uniform(0.5, 80, size=2)
+        y = oracle.equilibrium(p, n_ag, n_ant)
+        dy = oracle.rhs(p, y, n_ag, n_ant, 5.0, 3.0)
+        scale = np.abs(np.array([1, 1 / p[I["J"]], 1 / p[I["B_AG"]], 1 / p[I["B_ANT"]], 1, 1])) * 100
+        assert np.all(np.abs(dy) <= 1e-12 * scale)
+        # closed form, derived by hand from D1 with all derivatives zero
+        g_ag = p[0] / (p[2] + p[0])
+        g_ant = p[1] / (p[3] + p[1])
+        G = g_ag * (p[7] + p[2]) + g_ant * (p[8] + p[3])
+        assert y[0] == pytest.approx((g_ag * n_ag - g_ant * n_ant) / G, rel=1e-13, abs=1e-13)
+
+
+# --------------------------------------------------------------------------- P4
+def test_p4_fixed_point_500ms_defaults():
+    """SPEC.md:119 / :550: zero-pulse simulation stays within 1e-9 deg over 500 ms."""
+    p = W.truth_opc()
+    p[I["N_SAC_AG"]] = p[I["N_C_FIX"]]
+    p[I["N_SAC_ANT"]] = p[I["N_C_FIX"]]
+    dth = oracle.simulate(p, 1.0, 500, 0.0, 40.0)
+    assert np.max(np.abs(dth)) < 1e-9
+
+
+def test_p4_fixed_point_any_physical_opc_small_dt():
+    for p in _random_physical(20, seed=5):
+        p[I["N_SAC_AG"]] = p[I["N_C_FIX"]]
+        p[I["N_SAC_ANT"]] = p[I["N_C_FIX"]]
+        dth = oracle.simulate(p, 0.0625, 2000, 0.0, 40.0)
+        assert np.max(np.abs(dth)) < 1e-9
+
+
+# --------------------------------------------------------------------------- P5
+@pytest.mark.parametrize("Aprime", [10.0, 5.0, 20.0])
+def test_p5_steady_state_reaches_target(Aprime):
+    """Long run of the RK4 map settles at theta* + A' (step levels solve the
+    static balance, D4/Q4; both with the 0.01 g antagonist floor active (10, 20)
+    and inactive (5))."""
+    p = W.truth_opc()
+    dth = oracle.simulate(p, 1.0, 3000, Aprime, 40.0)
+    assert dth[-1] == pytest.approx(Aprime, abs=1e-9)
+    lv = oracle.step_levels(p, Aprime)
+    floor_active = lv[1] == 0.01
+    assert floor_active == (Aprime >= 10.0)
+
+
+def test_p5_steady_state_closed_form_random_opcs():
+    """Steady state of the simulated plant == hand-derived closed form, for
+    random physical OPCs integrated with a small step."""
+    for p in _random_physical(10, seed=9):
+        Ap = 8.0
+        dth, st = oracle.simulate(p, 0.0625, 40000, Ap, 40.0, states=True)
+        lv = oracle.step_levels(p, Ap)
+        g_ag = p[0] / (p[2] + p[0])
+        g_ant = p[1] / (p[3] + p[1])
+        G = g_ag * (p[7] + p[2]) + g_ant * (p[8] + p[3])
+        th_ss = (g_ag * lv[0] - g_ant * lv[1]) / G
+        th_star = (g_ag - g_ant) * p[14] / G
+        assert st[-1, 0] == pytest.approx(th_ss, abs=1e-8)
+        assert dth[-1] == pytest.approx(th_ss - th_star, abs=1e-8)
+        assert dth[-1] == pytest.approx(Ap, abs=1e-8)
+        assert st[-1, 4] == pytest.approx(lv[0], rel=1e-10)
+
+
+# --------------------------------------------------------------------------- P6
+def test_p6_linearity_in_pulse_height_and_monotone_amplitude():
+    """The plant is linear in the drive: Delta-theta is affine in N_SAC_AG, so
+    the peak amplitude is monotone in pulse height (north_star pin)."""
+    p = W.truth_opc()
+    trajs = []
+    for h in (40.0, 55.0, 70.0):
+        q = p.copy()
+        q[I["N_SAC_AG"]] = h
+        trajs.append(oracle.simulate(q, 1.0, 100, 10.0, 40.0))
+    t40, t55, t70 = trajs
+    second_diff = t70 - 2 * t55 + t40
+    assert np.max(np.abs(second_diff)) <= 1e-12 * np.max(np.abs(t55))
+    peaks = [t.max() for t in trajs]
+    assert peaks[0] < peaks[1] < peaks[2]
+    # derivative with respect to pulse height is positive during the pulse
+    assert np.all((t70 - t40)[1:41] > 0)
+
+
+def test_directionality():
+    """N_SAC_AG > N_C_FIX > N_SAC_ANT gives a non-negative saccade."""
+    p = W.truth_opc()
+    dth = oracle.simulate(p, 1.0, 100, 10.0, 40.0)
+    assert np.all(dth >= 0)
+    # NOTE: SPEC.md:116 ("J x 10 -> strictly lower peak velocity") does not hold
+    # under D1 (the globe is heavily over-damped; a heavier globe responds
+    # faster here).  It is recorded as reading Q21 in DESIGN.md, not used as a pin.
+
+
+def test_first_step_closed_form_taylor():
+    """From the fixation equilibrium, theta only moves through the chain
+    f -> x -> omega -> theta, so the first RK4 step equals the 4th-order Taylor
+    term of the exact solution, derived by hand from Fig. 1 / D1:
+      dtheta_1 = h^4/24 * (1/J) * [K_SE_AG/B_AG * (N_SAC_AG - F)/tau_AC_AG
+                                   + K_SE_ANT/B_ANT * (F - N_SAC_ANT)/tau_AC_ANT]
+    Pins every sign and coupling on the path, the tau units and the RK4 weight."""
+    for p in [W.truth_opc()] + _random_physical(20, seed=33):
+        F = p[I["N_C_FIX"]]
+        for dt in (1.0, 0.5, 0.1):
+            h = dt * 1e-3
+            expect = h ** 4 / 24 / p[I["J"]] * (
+                p[I["K_SE_AG"]] / p[I["B_AG"]] * (p[I["N_SAC_AG"]] - F) / (1e-3 * p[I["TAU_AC_AG"]])
+                + p[I["K_SE_ANT"]] / p[I["B_ANT"]] * (F - p[I["N_SAC_ANT"]]) / (1e-3 * p[I["TAU_AC_ANT"]]))
+            d1 = oracle.simulate(p, dt, 1, 10.0, 40.0)[1]
+            # abs term: rounding of theta_1 - theta* when theta* != 0 (asymmetric muscles)
+            assert d1 == pytest.approx(expect, rel=1e-9, abs=64 * 2.0 ** -52 * abs(oracle.equilibrium(p, F, F)[0]))
+
+
+# --------------------------------------------------------------------------- P7
+def _rk4_matrix_form(p, dt_ms, n_steps, Aprime):
+    """Textbook identity: classical RK4 on y' = A y + b with constant b is
+    y+ = P(hA) y + h Q(hA) b, P(z) = 1+z+z^2/2+z^3/6+z^4/24, Q(z) = 1+z/2+z^2/6+z^3/24."""
+    h = dt_ms * 1e-3
+    pulse, post = phase_inputs(p, Aprime)
+    mats = []
+    for ph in (pulse, post):
+        A, b = A_and_b(p, *ph)
+        Z = h * A
+        Id = np.eye(6)
+        P = Id + Z + Z @ Z / 2 + Z @ Z @ Z / 6 + Z @ Z @ Z @ Z / 24
+        Q = Id + Z / 2 + Z @ Z / 6 + Z @ Z @ Z / 24
+        mats.append((P, h * Q @ b))
+    npulse = math.ceil(p[I["PW"]] / dt_ms)
+    y = oracle.equilibrium(p, p[I["N_C_FIX"]], p[I["N_C_FIX"]])
+    out = [y.copy()]
+    for k in range(n_steps):
+        P, c = mats[0] if k < npulse else mats[1]
+        y = P @ y + c
+        out.append(y.copy())
+    return np.array(out)
+
+
+def test_p7_rk4_equals_polynomial_propagator():
+    cands = [W.truth_opc()] + _random_physical(10, seed=21)
+    for p in cands:
+        ref = _rk4_matrix_form(p, 1.0, 100, 10.0)
+        dth, st = oracle.simulate(p, 1.0, 100, 10.0, 40.0, states=True)
+        scale = np.maximum(np.abs(ref).max(axis=0), 1.0)
+        assert np.max(np.abs(st - ref) / scale) < 1e-11
+
+
+# --------------------------------------------------------------------------- P8
+def test_p8_rk4_fourth_order_convergence():
+    """SPEC.md:120 / :551: halving dt shrinks the error by >= 12 (theory 16)."""
+    p = W.truth_opc()
+    # steps 1, 1/2, 1/4, 1/8 ms; PW = 40 ms is on every grid so the control
+    # discontinuity is sampled exactly.
+    res = {}
+    for m in (1, 2, 4, 8):
+        res[m] = oracle.simulate(p, 1.0 / m, 100 * m, 10.0, 40.0)[::m]
+    e1 = np.max(np.abs(res[1] - res[8]))
+    e2 = np.max(np.abs(res[2] - res[8]))
+    e4 = np.max(np.abs(res[4] - res[8]))
+    # Richardson: e(h) ~ C h^4 (1 - 1/8^4 ...); ratio of successive errors
+    assert e1 / e2 >= 12
+    assert e2 / e4 >= 12
+
+
+def test_p8_converges_to_matrix_exponential_solution():
+    """dt -> 0 approaches the exact zero-order-hold solution e^{tA} (scipy expm,
+    a library routine independent of the RK4 code)."""
+    p = W.truth_opc()
+    pulse, post = phase_inputs(p, 10.0)
+    h = 1e-3
+    steps = []
+    for ph in (pulse, post):
+        A, b = A_and_b(p, *ph)
+        M = np.zeros((7, 7))
+        M[:6, :6] = A * h
+        M[:6, 6] = b * h
+        steps.append(scipy.linalg.expm(M))
+    y = np.append(oracle.equilibrium(p, 14.0, 14.0), 1.0)
+    th0 = y[0]
+    exact = [0.0]
+    for k in range(100):
+        y = (steps[0] if k < 40 else steps[1]) @ y
+        exact.append(y[0] - th0)
+    exact = np.array(exact)
+    fine = oracle.simulate(p, 1.0 / 64, 6400, 10.0, 40.0)[::64]
+    coarse = oracle.simulate(p, 1.0, 100, 10.0, 40.0)
+    assert np.max(np.abs(fine - exact)) < 1e-8
+    assert np.max(np.abs(coarse - exact)) > 1e-6  # RK4 at 1 ms is not exact
+    assert np.max(np.abs(coarse - exact)) < 1e-2
+
+
+# --------------------------------------------------------------------------- score
+def test_score_spec_examples_and_cap():
+    g = read_golden_kv("spec_worked_examples.txt")
+    a = np.linspace(0, 10, 50)
+    assert oracle.score(a, a, 0) == g["objective_identical"]
+    assert oracle.score(a + 1.0, a, 0) == g["objective_offset1_50samples"]
+    assert oracle.score(a + 1.0, a, 1) == 1.0  # RMS of a unit offset
+    assert oracle.score(a + 3.0, a, 1) == 3.0
+    big = a.copy()
+    big[3] = 1e21
+    assert oracle.score(big, a, 0) == math.inf          # Q10 cap
+    nan = a.copy()
+    nan[5] = math.nan
+    assert oracle.score(nan, a, 0) == math.inf          # NaN -> +inf
+
+
+def test_penalty_spec_example():
+    g = read_golden_kv("spec_worked_examples.txt")
+    p = W.truth_opc()
+    p[I["K_SE_AG"]] = -1.0
+    assert oracle.physical_penalty(p) >= g["penalty_floor"]
+    assert oracle.physical_penalty(p) == 1e10 * 2.0
+    rec = np.zeros(101)
+    assert oracle.objective(p, rec, W.Control()) == 2e10
+    assert oracle.physical_penalty(W.truth_opc()) == 0.0
+    q = W.truth_opc()
+    q[I["J"]] = 0.0
+    assert oracle.physical_penalty(q) == 1e10
+
+
+def test_pulse_window_discretisation():
+    g = read_golden_kv("spec_worked_examples.txt")
+    assert 46.0 - 6.0 == g["pw_placeholder_46ms"]
+    assert oracle.n_pulse(40.0, 1.0) == 40
+    assert oracle.n_pulse(39.21, 1.0) == 40
+    assert oracle.n_pulse(40.0001, 1.0) == 41
+    # NaN PW uses the per-saccade default
+    p = W.truth_opc()
+    q = p.copy()
+    q[I["PW"]] = math.nan
+    assert np.array_equal(oracle.simulate(q, 1.0, 100, 10.0, 40.0), oracle.simulate(p, 1.0, 100, 10.0, 40.0))
+    assert len(oracle.simulate(p, 1.0, 46, 10.0, 40.0)) == int(g["simulate_46ms_samples"])
+
+
+def test_relativize_mirrors_negative_saccades():
+    rec = np.array([3.0, 2.0, 0.0, -5.0])
+    rel, s, Ap = oracle.relativize(rec, math.nan)
+    assert s == -1.0 and Ap == 8.0
+    assert rel.tolist() == [0.0, 1.0, 3.0, 8.0]
+    rel2, s2, Ap2 = oracle.relativize(rec, 4.0)
+    assert s2 == 1.0 and Ap2 == 4.0 and rel2.tolist() == [0.0, -1.0, -3.0, -8.0]
+
+
+# --------------------------------------------------------------------------- P9
+def test_p9_zero_error_on_own_output_and_mirroring():
+    ctl = W.Control()
+    t = W.truth_opc()
+    rec = oracle.positions(t, ctl)
+    rel, s, Ap = oracle.relativize(rec, ctl.amplitude_deg)
+    e = oracle.objective(t, rec, ctl)
+    assert e <= 1e-9 * np.abs(rel).sum()
+    # negative saccade from 3 deg: mirrored estimate gives the same error
+    ctl2 = W.Control(amplitude_deg=-10.0, theta0_deg=3.0)
+    rec2 = oracle.positions(t, ctl2)
+    assert rec2[0] == 3.0 and rec2[-1] < 3.0
+    assert oracle.objective(t, rec2, ctl2) <= 1e-9 * np.abs(rel).sum()
+
+
+def test_p9_planted_grid_argmin_is_truth():
+    ctl = W.Control()
+    rec = oracle.positions(W.truth_opc(), ctl)
+    sp = W.g4_space(per_dim=9)   # 9^4 grid, TRUTH at (4, 4, 4, PW=40 -> digit 39?)
+    # per_dim = 9 puts PW levels 1..9 ms; use a PW grid that contains 40 instead
+    d = W.truth_opc()
+    sp = W.grid_space({
+        "K_SE_AG": (d[0] * 1.01 ** -4, d[0] * 1.01 ** 4, 9, True),
+        "B_AG": (d[4] * 1.01 ** -4, d[4] * 1.01 ** 4, 9, True),
+        "N_SAC_AG": (d[15] * 1.01 ** -4, d[15] * 1.01 ** 4, 9, True),
+        "PW": (36.0, 44.0, 9, False),
+    })
+    n = sp.n_grid()
+    r = oracle.fit(rec, ctl, sp, 0, n, nthreads=4)
+    planted = 4 + 9 * 4 + 81 * 4 + 729 * 4
+    assert r["best_index"] == planted
+    assert r["best_err"] < 1e-9 * 650
+    assert r["n_finite"] == n
+
+
+# --------------------------------------------------------------------------- P10
+def test_p10_bruteforce_argmin_tiny_grid():
+    """3^4 grid over {K_SE_AG, B_AG, N_SAC_AG, PW} (SPEC.md:553 set), noisy trace:
+    the oracle fit == an independent Python brute-force min over objectives."""
+    ctl = W.Control()
+    rec = oracle.positions(W.truth_opc(), ctl) + W.noise(101)
+    d = W.truth_opc()
+    sp = W.grid_space({
+        "K_SE_AG": (d[0] * 0.8, d[0] * 1.2, 3, False),
+        "B_AG": (d[4] * 0.8, d[4] * 1.2, 3, False),
+        "N_SAC_AG": (d[15] * 0.8, d[15] * 1.2, 3, False),
+        "PW": (30.0, 50.0, 3, False),
+    })
+    n = sp.n_grid()
+    errs = []
+    for i in range(n):
+        c = oracle.generate(sp, i)
+        # independent mixed-radix check (dimension 0 fastest)
+        dig = [i % 3, (i // 3) % 3, (i // 9) % 3, (i // 27) % 3]
+        assert c[0] == pytest.approx(d[0] * (0.8 + 0.2 * dig[0]), rel=1e-15)
+        assert c[17] == 30.0 + 10.0 * dig[3]
+        errs.append(oracle.objective(c, rec, ctl))
+    errs = np.array(errs)
+    best = int(np.argmin(errs))
+    r = oracle.fit(rec, ctl, sp, 0, n, nthreads=3, want_err=True)
+    assert r["best_index"] == best
+    assert r["best_err"] == errs[best]
+    assert np.array_equal(r["err"], errs)
+
+
+# --------------------------------------------------------------------------- P11
+def test_p11_philox_known_answers():
+    rows = read_golden_table("philox4x32_10_kat.txt")
+    assert len(rows) == 3
+    for r in rows:
+        v = [int(x, 16) for x in r]
+        out = oracle.philox4x32_10(v[0:4], v[4:6])
+        assert out.tolist() == v[6:10]
+
+
+def test_generator_bounds_and_distribution():
+    sp = W.paper_space()
+    c = oracle.generate_batch(sp, 0, 4000)
+    assert np.all(c >= sp.lo) and np.all(c <= sp.hi)
+    # log-uniform dims: log(v/lo)/log(hi/lo) ~ U(0,1); PW linear ~ U(1, 100)
+    u = np.log(c[:, :17] / sp.lo[:17]) / np.log(sp.hi[:17] / sp.lo[:17])
+    assert np.all(np.abs(u.mean(axis=0) - 0.5) < 0.03)
+    assert np.all(np.abs(u.var(axis=0) - 1 / 12) < 0.01)
+    assert abs(c[:, 17].mean() - 50.5) < 2.0
+    # independent re-derivation of one candidate from the Philox words
+    i = 123456789012
+    words = np.concatenate([oracle.philox4x32_10([i & 0xffffffff, i >> 32, 0, j],
+                                                 [9884, 0]) for j in range(5)])
+    uu = (words[:18].astype(np.float64) + 0.5) / 2.0 ** 32
+    cand = oracle.generate(sp, i)
+    assert cand[17] == pytest.approx(1.0 + uu[17] * 99.0, rel=1e-15)
+    assert cand[3] == pytest.approx(0.12 * 100.0 ** uu[3], rel=1e-14)
+    # saccade field changes the stream
+    assert not np.array_equal(oracle.generate(sp, 5, saccade=1), oracle.generate(sp, 5, saccade=0))
+
+
+# --------------------------------------------------------------------------- P12 / P12b
+def test_p12_shard_invariance():
+    ctl = W.Control()
+    rec = oracle.positions(W.truth_opc(), ctl) + W.noise(101)
+    sp = W.paper_space()
+    N = 3000
+    full = oracle.fit(rec, ctl, sp, 0, N, nthreads=1, want_err=True)
+    for R in (2, 4, 8):
+        parts = []
+        for r in range(R):
+            b, e = N * r // R, N * (r + 1) // R
+            parts.append(oracle.fit(rec, ctl, sp, b, e, nthreads=2))
+        best = min((p["best_err"], p["best_index"]) for p in parts if p["best_index"] >= 0)
+        assert best == (full["best_err"], full["best_index"])
+        assert sum(p["n_finite"] for p in parts) == full["n_finite"]
+    for nt in (3, 8):
+        r = oracle.fit(rec, ctl, sp, 0, N, nthreads=nt)
+        assert (r["best_err"], r["best_index"]) == (full["best_err"], full["best_index"])
+    # the error vector itself is index-deterministic
+    sub = oracle.fit(rec, ctl, sp, 1000, 1100, want_err=True)
+    assert np.array_equal(sub["err"], full["err"][1000:1100])
+
+
+def test_p12b_exact_ties_resolve_to_lowest_index():
+    """PW enters only through ceil(PW/dt): PW in {39.21, 39.6, 40.0} gives
+    bit-identical errors; the lowest index must win (Q12)."""
+    ctl = W.Control()
+    rec = oracle.positions(W.truth_opc(), ctl) + W.noise(101)
+    d = W.truth_opc()
+    sp = W.grid_space({
+        "N_SAC_AG": (d[15] * 0.99, d[15] * 1.01, 3, False),
+        "PW": (39.21, 40.0, 3, False),   # 39.21, 39.605, 40.0 -> n_pulse 40
+    })
+    r = oracle.fit(rec, ctl, sp, 0, 9, want_err=True)
+    e = r["err"].reshape(3, 3)   # [PW digit, N_SAC digit]
+    assert np.all(e[0] == e[1]) and np.all(e[1] == e[2])
+    assert r["best_index"] == int(np.argmin(e[0]))
+    # shard so the tied copies land in different shards: lowest index still wins
+    parts = [oracle.fit(rec, ctl, sp, b, b + 3) for b in (6, 3, 0)]
+    best = min((p["best_err"], p["best_index"]) for p in parts)
+    assert best[1] == r["best_index"]
+
+
+def test_all_diverged_gives_no_finite():
+    ctl = W.Control()
+    rec = oracle.positions(W.truth_opc(), ctl)
+    d = W.truth_opc()
+    # J tiny and B tiny: RK4 at 1 ms blows up for every candidate
+    d[I["J"]] = 1e-9
+    d[I["B_AG"]] = 1e-6
+    d[I["B_ANT"]] = 1e-6
+    sp = W.grid_space({"PW": (10.0, 20.0, 3, False)}, base=d)
+    r = oracle.fit(rec, ctl, sp, 0, 3, want_err=True)
+    assert r["best_index"] == -1 and r["n_finite"] == 0
+    assert np.all(np.isinf(r["err"]))
+
+
+# --------------------------------------------------------------------------- regression (scratch)
+def test_survey_scratch_regression_values():
+    """Values computed during the survey by a separate throwaway script under
+    the same readings (SURVEY 8(c) 'Scratch-derived regression values').
+    Regression only -- not a paper pin."""
+    p = W.truth_opc()
+    d = oracle.simulate(p, 1.0, 100, 10.0, 40.0)
+    ref = [8.039284810329e-04, 0.6438167818780, 2.508462368148, 6.717097214111, 8.175197819521, 9.682190619240]
+    assert np.allclose(d[[1, 10, 20, 40, 50, 100]], ref, rtol=1e-11, atol=1e-15)
+    assert abs(d).sum() == pytest.approx(650.9431611563706, rel=1e-13)
+    d5 = oracle.simulate(p, 1.0, 100, 5.0, 40.0)
+    assert d5[50] == pytest.approx(7.779986704990, rel=1e-11)
+    assert d5[100] == pytest.approx(5.954196963665, rel=1e-11)
+    assert oracle.step_levels(p, 5.0).tolist() == pytest.approx([23.25, 4.75], rel=1e-14)

@@ -1,0 +1,64 @@
+// FMA-pipe microbenchmark for B200 (sm_100a): FP64 / FP32 FMA throughput and
+// dependent-chain latency. Used to derive the ALU roofline denominator.
+#include <cstdio>
+#include <cuda_runtime.h>
+template <typename T, int CH>
+__global__ void thr(T* out, int iters, T a, T b) {
+  T x[CH];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) x[c] = (T)(threadIdx.x + c) * (T)1e-3;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < CH; ++c) x[c] = x[c] * a + b;
+  }
+  T s = 0;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) s += x[c];
+  if (s == (T)12345.678) out[0] = s;
+}
+template <typename T>
+__global__ void lat(T* out, long long* cyc, int iters, T a, T b) {
+  T x = (T)threadIdx.x;
+  long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) { x = x * a + b; x = x * a + b; x = x * a + b; x = x * a + b; }
+  long long t1 = clock64();
+  if (threadIdx.x == 0) { cyc[0] = t1 - t0; }
+  if (x == (T)12345.678) out[0] = x;
+}
+template <typename T, int CH>
+void run_thr(const char* name, int blocks, int threads, int iters) {
+  T* d; cudaMalloc(&d, 64);
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  thr<T, CH><<<blocks, threads>>>(d, iters, (T)0.999999, (T)1e-7);
+  cudaEventRecord(e0);
+  for (int r = 0; r < 5; ++r) thr<T, CH><<<blocks, threads>>>(d, iters, (T)0.999999, (T)1e-7);
+  cudaEventRecord(e1); cudaEventSynchronize(e1);
+  float ms; cudaEventElapsedTime(&ms, e0, e1);
+  double fma = 5.0 * blocks * threads * (double)iters * CH;
+  int clk; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+  printf("%s blocks=%d threads=%d chains=%d: %.3f TFMA/s = %.2f TFLOP/s (%.3f ms)\n", name, blocks, threads, CH,
+         fma / (ms * 1e-3) / 1e12, 2 * fma / (ms * 1e-3) / 1e12, ms);
+  cudaFree(d);
+}
+template <typename T>
+void run_lat(const char* name) {
+  T* d; long long* c; cudaMalloc(&d, 64); cudaMalloc(&c, 8);
+  int iters = 4096;
+  lat<T><<<1, 32>>>(d, c, iters, (T)0.999999, (T)1e-7);
+  lat<T><<<1, 32>>>(d, c, iters, (T)0.999999, (T)1e-7);
+  long long h; cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
+  printf("%s dependent latency: %.2f cycles\n", name, (double)h / (4.0 * iters));
+}
+int main() {
+  cudaDeviceProp p; cudaGetDeviceProperties(&p, 0);
+  printf("%s SMs=%d clock=%d kHz regs/SM=%d smem/SM=%zu\n", p.name, p.multiProcessorCount, p.clockRate,
+         p.regsPerMultiprocessor, p.sharedMemPerMultiprocessor);
+  int sm = p.multiProcessorCount;
+  run_lat<double>("DFMA");
+  run_lat<float>("FFMA");
+  for (int w : {4, 8, 16, 32}) run_thr<double, 8>("DFMA", sm * (w / 4), 128, 20000);
+  run_thr<double, 4>("DFMA", sm * 4, 128, 20000);
+  run_thr<double, 2>("DFMA", sm * 8, 128, 20000);
+  for (int w : {4, 8, 16, 32}) run_thr<float, 8>("FFMA", sm * (w / 4), 128, 40000);
+  return 0;
+}

@@ -1,0 +1,317 @@
+"""bench.py -- OPC candidate-simulation throughput of libopmm on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl libopmm|reference]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 ... bench.py --gpus N
+
+A step = one pass of the whole hot path over one batch:
+opmm_fit of the synthetic 10 deg saccade (1 kHz, 100 ms) over 10^6 random OPC
+candidates per GPU from S_paper (BASELINE.json configs[1]): generate ->
+simulate -> score -> argmin, plus for N > 1 the one NCCL all-gather of the
+per-rank (E, index) pairs.  Candidates are sharded disjointly per rank, so
+per-GPU work is fixed as N grows ("scaling": "weak").
+
+value  : candidates/s over all ranks, inputs resident in HBM (opmm_fit_async),
+         device time from CUDA events on the launching stream, max over ranks;
+         L2 flushed (512 MiB write) between timed steps, outside the events.
+e2e    : the same metric through the synchronous C-ABI call opmm_fit with the
+         trace in pinned HOST memory, H2D + kernel + D2H + CPU_check timed.
+roofline: the fused fit kernel vs the FP64 SIMT peak.
+cpu_baseline: the CPU oracle (oracle/, as it stands) on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+N_STEPS = 100
+PER_GPU = 10**6
+# Algorithmic FP64 work of the fit kernel per candidate:
+# the RK4 map in propagator form is 26 FMA per step (52 flop) + the fused L1
+# score 2 flop per step; per-candidate generation + setup counted separately.
+FLOP_PER_STEP = 54
+FLOP_SETUP = 1800  # per candidate: Philox map (17 exp), statics, P(Z) Horner, X/c build
+SMS, FP64_LANES, SM_MAX_MHZ = 148, 64, 1965.0
+FP64_PEAK_TFLOPS = SMS * FP64_LANES * 2 * SM_MAX_MHZ * 1e6 / 1e12   # 37.23
+FP64_MEASURED_TFLOPS = 33.90   # profiles/r01_fma_peak.txt (DFMA microbenchmark)
+
+
+def workload_name(per_gpu, world):
+    return (f"configs[1]: single synthetic 10 deg horizontal saccade, 1 kHz, 100 ms, "
+            f"{per_gpu:.0e} random OPC candidates per GPU over S_paper (x{world} GPUs)")
+
+
+def make_trace():
+    """Recorded trace: stored fixture written by scripts/make_traces.py from
+    the CPU oracle (TRUTH at A = 10 deg) plus seeded N(0, 0.02 deg) noise."""
+    path = os.path.join(ROOT, "tests", "golden", "trace_truth_A10_dt1_n100.txt")
+    rec = np.loadtxt(path, comments="#")
+    assert rec.shape == (N_STEPS + 1,)
+    return rec + W.noise(N_STEPS + 1)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.3)
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.2)
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline(target_s=12.0, sample_cap=3 * 10**6):
+    """The oracle as it stands, all host cores (OpenMP), on a bounded sample
+    of the same workload (same trace, same candidate stream)."""
+    import oracle
+    ctl = W.Control()
+    rec = make_trace()
+    sp = W.paper_space()
+    cores = len(os.sched_getaffinity(0))
+    t0 = time.perf_counter()
+    oracle.fit(rec, ctl, sp, 0, 20000, nthreads=cores)
+    rate0 = 20000 / (time.perf_counter() - t0)
+    n = int(min(sample_cap, max(20000, rate0 * target_s)))
+    t0 = time.perf_counter()
+    oracle.fit(rec, ctl, sp, 0, n, nthreads=cores)
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": "candidate sims/s", "cores": cores, "kind": "oracle",
+            "sample": f"candidates [0, {n}) of the bench workload (same trace and Philox stream), "
+                      f"{dt:.1f} s, OpenMP static chunks, gcc -O2 -ffp-contract=off"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    ctl = W.Control()
+    rec = make_trace()
+    sp = W.paper_space()
+    cores = len(os.sched_getaffinity(0))
+    sample = 200000
+    for s in range(args.warmup):
+        oracle.fit(rec, ctl, sp, s * sample, (s + 1) * sample, nthreads=cores)
+    times = []
+    for s in range(args.steps):
+        b = (args.warmup + s) * sample
+        t0 = time.perf_counter()
+        oracle.fit(rec, ctl, sp, b, b + sample, nthreads=cores)
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * sum(times) / len(times)
+    value = sample / (ms * 1e-3)
+    line = {"impl": "reference", "metric": "OPC candidate sims/s", "value": value,
+            "unit": "candidate sims/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_name(PER_GPU, args.gpus),
+                       "reference_step": f"{sample} candidates of the workload per step (bounded sample)"},
+            "cpu_baseline": {"value": value, "unit": "candidate sims/s", "cores": cores,
+                             "kind": "oracle",
+                             "sample": f"{sample} candidates per step x {args.steps} steps"},
+            "e2e": {"value": value, "unit": "candidate sims/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2007_09884_b200 import opmm
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        idt = torch.zeros(opmm.NCCL_ID_BYTES, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(opmm.opmm_nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        h = opmm.opmm_create_nccl(local, bytes(idt.cpu().numpy()), rank, world)
+    else:
+        h = opmm.opmm_create(local)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    ctl = W.Control()
+    rec = make_trace()
+    sp = W.paper_space()
+    n_total = args.per_gpu * world
+    stream = torch.cuda.ExternalStream(h.stream)
+    rec_dev = torch.as_tensor(rec, dtype=torch.float64, device="cuda")
+    out_dev = torch.zeros(ctypes.sizeof(opmm.FitResult), dtype=torch.uint8, device="cuda")
+    flush = torch.empty(512 * 2**20, dtype=torch.uint8, device="cuda")
+    torch.cuda.synchronize()
+
+    def device_leg(precision):
+        opts = opmm.fit_options(precision=precision, cpu_check=0)
+        for _ in range(args.warmup):
+            opmm.opmm_fit_async(h, rec_dev, ctl, sp, n_total, out_dev, opts)
+        stream.synchronize()
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        kms = []
+        barrier()
+        torch.cuda.synchronize()
+        with torch.cuda.stream(stream):
+            for s in range(args.steps):
+                flush.fill_(s & 0xff)                 # evict L2 (outside the events)
+                starts[s].record(stream)
+                opmm.opmm_fit_async(h, rec_dev, ctl, sp, n_total, out_dev, opts)
+                ends[s].record(stream)
+                kms.append(opmm.opmm_last_kernel_ms(h))
+        stream.synchronize()
+        torch.cuda.synchronize()
+        barrier()
+        ms = sum(a.elapsed_time(b) for a, b in zip(starts, ends)) / args.steps
+        res = opmm.decode_result(bytes(out_dev.cpu().numpy()))
+        return max_over_ranks(ms), max_over_ranks(sum(kms) / len(kms)), res
+
+    with ClockSampler(local) as clk:
+        ms64, kms64, res64 = device_leg(opmm.FP64)
+    clocks = clk.summary()
+    ms32, kms32, res32 = device_leg(opmm.FP32)
+
+    # e2e: synchronous public call, trace in pinned host memory
+    rec_host = torch.as_tensor(rec, dtype=torch.float64).pin_memory()
+    rec_np = rec_host.numpy()
+    opts = opmm.fit_options(precision=opmm.FP64, cpu_check=1)
+    for _ in range(args.warmup):
+        opmm.opmm_fit(h, rec_np, ctl, sp, n_total, opts)
+    barrier()
+    torch.cuda.synchronize()
+    t_e2e = []
+    for s in range(args.steps):
+        flush.fill_(s & 0xff)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = opmm.opmm_fit(h, rec_np, ctl, sp, n_total, opts)
+        t_e2e.append(time.perf_counter() - t0)
+    barrier()
+    e2e_ms = max_over_ranks(1e3 * sum(t_e2e) / len(t_e2e))
+
+    per_cand_flop = FLOP_PER_STEP * N_STEPS + FLOP_SETUP
+    achieved = per_cand_flop * args.per_gpu / (kms64 * 1e-3) / 1e12
+    line = {
+        "metric": "OPC candidate sims/s", "value": n_total / (ms64 * 1e-3),
+        "unit": "candidate sims/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms64, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_name(args.per_gpu, world), "n_candidates": n_total,
+                   "per_gpu": args.per_gpu, "n_steps": N_STEPS, "dt_ms": 1.0,
+                   "integrator": "rk4-propagator", "metric": "L1",
+                   "l2": "flushed between timed steps (512 MiB write, outside the events)",
+                   "parallelism": f"candidates sharded x{world}, 1 ncclAllGather of 32 B/rank"},
+        "clocks": clocks,
+        "gpu_launches": args.steps * (2 if world > 1 else 1),
+        "e2e": {"value": n_total / (e2e_ms * 1e-3), "unit": "candidate sims/s",
+                "h2d_bytes_per_step": rec_np.nbytes, "d2h_bytes_per_step": ctypes.sizeof(opmm.FitResult),
+                "ms_per_step": e2e_ms, "api": "opmm_fit (sync, host buffers, CPU_check on)"},
+        "roofline": {"bound": "alu", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
+                     "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+                     "kernel": "fit_kernel<double, propagator, L1>", "kernel_ms": kms64,
+                     "flop_per_candidate": per_cand_flop,
+                     "peak_basis": "148 SM x 64 FP64 lanes x 2 x 1965 MHz (DESIGN.md)",
+                     "frac_of_measured_dfma": achieved / FP64_MEASURED_TFLOPS},
+        "fp32": {"value": n_total / (ms32 * 1e-3), "ms_per_step": ms32, "kernel_ms": kms32,
+                 "best_index": res32["best_index"]},
+        "result": {"best_index": res64["best_index"], "opt_err": res64["opt_err"],
+                   "n_finite": res64["n_finite"], "cpu_check": r["cpu_check"]},
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    h.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="libopmm", choices=["libopmm", "reference"])
+    ap.add_argument("--per-gpu", type=int, default=PER_GPU)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,228 @@
+/*
+ * opmm.h -- C ABI of libopmm, the B200 (sm_100a) hot path of the parallel
+ * Oculomotor Plant Mathematical Model (OPMM), arXiv 2007.09884.
+ *
+ * The hot path: for every candidate OPC
+ * vector c_i (Table 1) simulate the
+ * 18-parameter linear homeomorphic plant (Fig. 1; equations
+ * = SPEC D1) under the pulse-step control signal
+ * with fixed-step classical RK4 (SPEC D2),
+ * score it against the recorded saccade ("absolute difference between the
+ * recorded and simulated eye movement trajectories"), and reduce
+ * to the best-fit OPC ("exhaustive search of potential parameter values",
+ * PAPER.md:202; "solutions are sorted for accuracy").
+ *
+ * Conventions (all entry points):
+ *  - Every function returns an opmm_status and never aborts or exits.  On a
+ *    non-OK status a message is available from opmm_last_error() (thread-local).
+ *  - Units: angles in degrees, time arguments in ms, forces in g; internally
+ *    mechanics run in seconds (reading Q2).
+ *  - OPC vectors are 18 doubles in Table-1 order (OPMM_P_* below).  Batches of
+ *    OPC vectors are SoA: element (p, i) at opc[p * ld + i], ld >= n.
+ *  - Trajectories are time-major: sample k of candidate i at traj[k * ld + i]
+ *    (coalesced across candidates).
+ *  - Ownership: the caller owns every buffer passed in or out; the handle owns
+ *    its workspace (block partials, staged trace, NCCL communicator) and frees
+ *    it in opmm_destroy.  A handle is not thread-safe: calls on one handle are
+ *    serialised on its stream.
+ *  - "device" pointers must be CUDA device (or managed) memory on the handle's
+ *    device; "host" pointers are ordinary host memory.  Asynchronous entry
+ *    points (suffix _async, and simulate/score/simulate_score/generate) only
+ *    enqueue work on `stream` (NULL = the handle's own stream) and return.
+ *  - Per-candidate numerical failure is data, not an error:
+ *      non-physical OPC  -> E = 1e10 * (1 + sum of violations)  (D8)
+ *      non-finite or E >= 1e20 accumulated -> E = +inf          (reading Q10)
+ *  - The product never computes on the CPU in place of the GPU: without a
+ *    CUDA device opmm_create fails with OPMM_ERR_CUDA.  The only host
+ *    arithmetic is argument validation, search-space preprocessing, and the
+ *    paper's CPU_check column (a serial re-score of the single returned
+ *    winner), which is validation, not a fallback.
+ */
+#ifndef OPMM_H
+#define OPMM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OPMM_NPARAM 18
+#define OPMM_MAX_STEPS 16384
+#define OPMM_NCCL_ID_BYTES 128
+
+/* Table-1 order. */
+enum {
+  OPMM_P_KSE_AG = 0, OPMM_P_KSE_ANT, OPMM_P_KLT_AG, OPMM_P_KLT_ANT, OPMM_P_B_AG,
+  OPMM_P_B_ANT, OPMM_P_B_P, OPMM_P_NC_AG, OPMM_P_NC_ANT, OPMM_P_J,
+  OPMM_P_TAU_AC_AG, OPMM_P_TAU_AC_ANT, OPMM_P_TAU_DE_AG, OPMM_P_TAU_DE_ANT,
+  OPMM_P_NC_FIX, OPMM_P_NSAC_AG, OPMM_P_NSAC_ANT, OPMM_P_PW
+};
+
+typedef enum {
+  OPMM_OK = 0,
+  OPMM_ERR_INVALID_ARG = 1,  /* argument failed validation; nothing launched   */
+  OPMM_ERR_CUDA = 2,         /* CUDA runtime error or no usable device          */
+  OPMM_ERR_NCCL = 3,         /* NCCL unavailable or a collective failed         */
+  OPMM_ERR_OOM = 4,          /* device allocation failed                        */
+  OPMM_ERR_NO_FINITE = 5,    /* fit: every candidate scored +inf (or N == 0)    */
+  OPMM_ERR_UNSUPPORTED = 6   /* option combination not implemented              */
+} opmm_status;
+
+typedef enum { OPMM_FP64 = 0, OPMM_FP32 = 1 } opmm_precision;
+/* PAPER.md:366 "absolute difference" -> L1 sum over all samples (default);
+ * RMS = sqrt(mean d^2) is the option north_star names (reading Q9). */
+typedef enum { OPMM_METRIC_L1 = 0, OPMM_METRIC_RMS = 1 } opmm_metric;
+/* Both integrators compute the same classical RK4 map (SPEC D2).  PROPAGATOR
+ * applies it as y+ = P(hA) y + hQ(hA) b, built per candidate (DESIGN.md
+ * "Kernels"); RK4_STAGES evaluates the four stages literally. */
+typedef enum { OPMM_INTEG_PROPAGATOR = 0, OPMM_INTEG_RK4_STAGES = 1 } opmm_integrator;
+
+/* Pulse-step control + integration grid of one saccade. */
+typedef struct {
+  double dt_ms;          /* sample interval and RK4 step, > 0 (1.0 at 1 kHz)    */
+  int32_t n_steps;       /* 1..OPMM_MAX_STEPS; trajectories have n_steps+1 samples */
+  int32_t pad_;          /* must be 0                                            */
+  double amplitude_deg;  /* signed target amplitude A; NaN => rec[n]-rec[0] (D5) */
+  double theta0_deg;     /* absolute start position (opmm_simulate output only)  */
+  double pw_default_ms;  /* PW used when a candidate's PW is NaN: "saccade
+                            duration - 6 ms"                      */
+} opmm_control;
+
+/* Candidate generator (PAPER.md:202 exhaustive search; reading Q14/Q15).
+ * mode 0 (random): candidate i uses Philox4x32-10 with key = (seed_lo, seed_hi)
+ *   and counter = (i_lo, i_hi, saccade, j), j = 0..4 -> 20 words; dimension d
+ *   uses word d: u = (w + 0.5) 2^-32; log dims lo*exp(u*log(hi/lo)); linear
+ *   dims lo + u*(hi-lo); lo == hi fixes the dimension.
+ * mode 1 (grid): mixed-radix digits of i (dimension 0 fastest) over levels[d];
+ *   log dims lo*exp(digit*(log(hi/lo)/(L-1))); linear lo + digit*((hi-lo)/(L-1)).
+ *   The product of levels must equal the candidate count of the call. */
+typedef struct {
+  int32_t mode;
+  int32_t pad_;
+  uint64_t seed;
+  double lo[OPMM_NPARAM];
+  double hi[OPMM_NPARAM];
+  uint8_t log_scale[OPMM_NPARAM];  /* 1: log-uniform / geometric; requires lo > 0 */
+  uint8_t pad2_[6];
+  int32_t levels[OPMM_NPARAM];     /* grid mode only, each >= 1                   */
+} opmm_search_space;
+
+typedef struct {
+  int32_t precision;    /* opmm_precision: arithmetic of the integrate+score loop */
+  int32_t metric;       /* opmm_metric                                            */
+  int32_t integrator;   /* opmm_integrator                                        */
+  int32_t block_size;   /* 0 = default (256); else 64..1024, multiple of 32       */
+  int32_t grid_blocks;  /* 0 = default (persistent: SMs x resident blocks)        */
+  int32_t cpu_check;    /* 1 = fill result.cpu_check, 0 = NaN      */
+  double* err_out;      /* optional DEVICE [n]: E_i of every candidate (validation) */
+} opmm_fit_options;
+
+typedef struct {
+  int64_t best_index;            /* global candidate index; -1 if no finite E     */
+  double opt_err;                /* E of the winner as computed by the kernel      */
+  double cpu_check;              /* serial host fp64 re-score (Fig. 4 CPU_check)   */
+  double opc[OPMM_NPARAM];       /* winner's OPC, exactly as evaluated on device   */
+  int64_t n_finite;              /* candidates with finite E (all ranks)           */
+  int64_t n_evaluated;           /* candidates evaluated (all ranks)               */
+} opmm_fit_result;
+
+typedef struct opmm_handle opmm_handle;
+
+/* ---- library / handle --------------------------------------------------- */
+const char* opmm_version(void);
+const char* opmm_last_error(void);
+
+/* Create a handle on CUDA device `device` (single GPU, world = 1). */
+opmm_status opmm_create(opmm_handle** h, int device);
+/* Multi-GPU: one process per GPU.  `nccl_id` is OPMM_NCCL_ID_BYTES produced by
+ * opmm_nccl_unique_id on rank 0 and broadcast by the caller (e.g. through
+ * torch.distributed).  Candidates are sharded disjointly per rank and the
+ * per-rank (E, index) pairs are merged with one ncclAllGather of 24 bytes per
+ * rank.  NCCL is loaded at run time (libnccl.so.2). */
+opmm_status opmm_nccl_unique_id(uint8_t* nccl_id /* host, 128 B */);
+opmm_status opmm_create_nccl(opmm_handle** h, int device, const uint8_t* nccl_id,
+                             int rank, int world);
+opmm_status opmm_destroy(opmm_handle* h);
+/* The handle's own stream (cudaStream_t), for callers that want to order work. */
+opmm_status opmm_get_stream(opmm_handle* h, void** stream);
+/* Device time (ms, CUDA events on the launching stream) of the most recent
+ * fit/simulate kernel launched through this handle (synchronises the handle's
+ * stream). */
+opmm_status opmm_last_kernel_ms(opmm_handle* h, float* ms);
+
+/* ---- host-only helpers (no GPU needed) ----------------------------------- */
+/* Rank r of R owns global candidate indices [floor(rN/R), floor((r+1)N/R)). */
+opmm_status opmm_shard_range(int64_t n, int rank, int world, int64_t* begin, int64_t* end);
+/* Lexicographic (E, index) minimum of `count` partial results (err[i], idx[i]);
+ * idx -1 entries are ignored; +inf never beats a finite E (reading Q12). */
+opmm_status opmm_merge_argmin(const double* err, const int64_t* idx, int count,
+                              double* best_err, int64_t* best_idx);
+/* Validate a control / search space (the same checks every entry point runs). */
+opmm_status opmm_validate(const opmm_control* ctl, const opmm_search_space* space,
+                          int64_t n_candidates);
+
+/* ---- hot path ------------------------------------------------------------- */
+/* Candidates [begin, begin+count) of `space` for saccade `saccade`, written
+ * SoA to DEVICE opc_out[18][ld].  Bit-identical to what the fit kernel
+ * evaluates for the same indices. */
+opmm_status opmm_generate(opmm_handle* h, const opmm_search_space* space, uint32_t saccade,
+                          int64_t begin, int64_t count, double* opc_out, int64_t ld,
+                          void* stream);
+
+/* Simulate n explicit OPC vectors (DEVICE SoA opc[18][ld]) under `ctl`:
+ * DEVICE traj[(n_steps+1) x ld_out] of `precision` (double or float) receives
+ * absolute positions theta0 + s * Delta-theta_k (s = sign(A), D6 mirroring);
+ * optional DEVICE status[n]: 0 ok, 1 non-physical (trajectory NaN), 2 diverged
+ * (non-finite sample).  SPEC simulate. */
+opmm_status opmm_simulate(opmm_handle* h, const double* opc, int64_t n, int64_t ld,
+                          const opmm_control* ctl, int32_t precision, int32_t integrator,
+                          void* traj, int64_t ld_out, uint8_t* status, void* stream);
+
+/* Score n stored trajectories (DEVICE traj[n_samples x ld] of `precision`)
+ * against DEVICE recorded[n_samples] (fp64):  E_i = sum_k |traj_k,i - rec_k|
+ * (L1) or sqrt(mean d^2) (RMS); accumulated >= 1e20 or non-finite -> +inf.
+ * DEVICE err[n] (fp64).  The only HBM-bound entry point. */
+opmm_status opmm_score(opmm_handle* h, const void* traj, int64_t n, int64_t ld,
+                       int32_t n_samples, const double* recorded, int32_t precision,
+                       int32_t metric, double* err, void* stream);
+
+/* Fused simulate + score of n explicit OPC vectors against DEVICE
+ * recorded[n_steps+1]; no trajectory reaches HBM.  E_i as in opmm_fit
+ * (penalty for non-physical).  DEVICE err[n] (fp64). */
+opmm_status opmm_simulate_score(opmm_handle* h, const double* opc, int64_t n, int64_t ld,
+                                const opmm_control* ctl, const double* recorded,
+                                int32_t precision, int32_t metric, int32_t integrator,
+                                double* err, void* stream);
+
+/* Exhaustive fit of one saccade over candidates [0, n_candidates) of `space`:
+ * generate -> simulate -> score -> argmin, in one kernel (plus, for world > 1,
+ * one ncclAllGather and a merge kernel).  `recorded` is HOST or DEVICE
+ * (n_steps+1 fp64 samples, auto-detected); `out` is HOST.  Synchronous.
+ * Returns OPMM_ERR_NO_FINITE (best_index = -1) if no candidate is finite. */
+opmm_status opmm_fit(opmm_handle* h, const double* recorded, const opmm_control* ctl,
+                     const opmm_search_space* space, int64_t n_candidates,
+                     const opmm_fit_options* opts, opmm_fit_result* out);
+
+/* Asynchronous fit for device-resident inputs: DEVICE recorded, DEVICE
+ * out_dev (one opmm_fit_result; cpu_check is NaN).  Enqueues on the handle's
+ * stream; nothing is copied to or from the host. */
+opmm_status opmm_fit_async(opmm_handle* h, const double* recorded_dev, const opmm_control* ctl,
+                           const opmm_search_space* space, int64_t n_candidates,
+                           const opmm_fit_options* opts, opmm_fit_result* out_dev);
+
+/* Population batch: S independent saccades, each
+ * fitted over candidates [0, n_per) of `space` with Philox counter word 2 =
+ * saccade index.  recorded: HOST or DEVICE [S][n_steps+1] (same n_steps and
+ * dt for all, from ctl[0]); ctl: HOST [S] (per-saccade amplitude /
+ * pw_default); out: HOST [S].  On an NCCL handle rank r fits only saccades
+ * [floor(rS/R), floor((r+1)S/R)) and fills only those entries of out: the
+ * saccades are independent problems, so there is no collective. */
+opmm_status opmm_fit_batch(opmm_handle* h, const double* recorded, int64_t S,
+                           const opmm_control* ctl, const opmm_search_space* space,
+                           int64_t n_per, const opmm_fit_options* opts, opmm_fit_result* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OPMM_H */

@@ -3,7 +3,7 @@
  *
  * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
  * cpu_baseline / --impl reference legs of bench.py may load this library.
- * The product library (paper_2007_09884_b200/libopmm.so) never links, calls
+ * The product library (libopmm, paper_2007_09884_b200/) never links, calls
  * or includes anything from here, and nothing here comes from the product:
  * no shared headers, tables, constants or helpers.
  *

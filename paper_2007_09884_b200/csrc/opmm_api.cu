@@ -1,0 +1,753 @@
+// opmm_api.cu -- the C ABI of libopmm (include/opmm.h): argument validation,
+// search-space preprocessing, handle / workspace / stream management, kernel
+// launch configuration, the multi-GPU merge (NCCL, loaded at run time), and
+// the paper's CPU_check column.  Every step of the hot path itself runs in
+// the kernels of opmm_kernels.cu; nothing here computes candidates on the CPU.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <dlfcn.h>
+#include <string>
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include "opmm.h"
+#include "opmm_cpu_check.h"
+#include "opmm_internal.h"
+
+using opmm::Partial;
+
+// ABI layout (mirrored by the ctypes binding; checked by tests/test_abi.py)
+static_assert(sizeof(opmm_control) == 40, "opmm_control layout");
+static_assert(sizeof(opmm_search_space) == 400, "opmm_search_space layout");
+static_assert(sizeof(opmm_fit_options) == 32, "opmm_fit_options layout");
+static_assert(sizeof(opmm_fit_result) == 184, "opmm_fit_result layout");
+static_assert(sizeof(Partial) == 32, "Partial layout");
+
+namespace {
+
+thread_local std::string g_err;
+
+opmm_status fail(opmm_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+#define CK(call)                                                                      \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess)                                                            \
+      return fail(e_ == cudaErrorMemoryAllocation ? OPMM_ERR_OOM : OPMM_ERR_CUDA,     \
+                  "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__,   \
+                  __LINE__);                                                          \
+  } while (0)
+
+#define CKS(expr)                          \
+  do {                                     \
+    opmm_status s_ = (expr);               \
+    if (s_ != OPMM_OK) return s_;          \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// NCCL, resolved at run time (the process normally already has torch's
+// libnccl.so.2 loaded; we reuse it rather than link a second copy).
+// ---------------------------------------------------------------------------
+struct NcclApi {
+  bool loaded = false;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char* (*getErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  if (!api.loaded) {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.getUniqueId = (decltype(api.getUniqueId))dlsym(h, "ncclGetUniqueId");
+      api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
+      api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
+      api.allGather = (decltype(api.allGather))dlsym(h, "ncclAllGather");
+      api.getErrorString = (decltype(api.getErrorString))dlsym(h, "ncclGetErrorString");
+      api.loaded = api.getUniqueId && api.commInitRank && api.commDestroy && api.allGather &&
+                   api.getErrorString;
+    }
+  }
+  return api;
+}
+
+constexpr int kDefaultBlock = 256;
+constexpr size_t kMaxDynSmem = 200 * 1024;
+
+}  // namespace
+
+struct opmm_handle {
+  int device = 0;
+  int rank = 0, world = 1;
+  int num_sms = 0;
+  cudaStream_t stream = nullptr;
+  ncclComm_t comm = nullptr;
+  // workspace
+  Partial* partials = nullptr;
+  size_t partials_cap = 0;
+  unsigned int* counters = nullptr;
+  size_t counters_cap = 0;
+  double* rec = nullptr;
+  size_t rec_cap = 0;
+  double* sacctl = nullptr;
+  size_t sacctl_cap = 0;
+  Partial* rank_part = nullptr;
+  size_t rank_part_cap = 0;
+  Partial* gathered = nullptr;
+  size_t gathered_cap = 0;
+  opmm_fit_result* result = nullptr;
+  size_t result_cap = 0;
+  opmm_fit_result* result_host = nullptr;  // pinned
+  size_t result_host_cap = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  bool timed = false;
+};
+
+namespace {
+
+template <typename P>
+opmm_status ensure(P*& ptr, size_t& cap, size_t n, bool zero = false) {
+  if (n <= cap) return OPMM_OK;
+  if (ptr) cudaFree(ptr);
+  ptr = nullptr;
+  cap = 0;
+  size_t want = n < 64 ? 64 : n;
+  CK(cudaMalloc(reinterpret_cast<void**>(&ptr), want * sizeof(P)));
+  if (zero) CK(cudaMemset(ptr, 0, want * sizeof(P)));
+  cap = want;
+  return OPMM_OK;
+}
+
+opmm_status ensure_host(opmm_fit_result*& ptr, size_t& cap, size_t n) {
+  if (n <= cap) return OPMM_OK;
+  if (ptr) cudaFreeHost(ptr);
+  ptr = nullptr;
+  cap = 0;
+  CK(cudaMallocHost(reinterpret_cast<void**>(&ptr), n * sizeof(opmm_fit_result)));
+  cap = n;
+  return OPMM_OK;
+}
+
+bool is_finite(double x) { return std::isfinite(x); }
+
+opmm_status check_handle(opmm_handle* h) {
+  if (!h) return fail(OPMM_ERR_INVALID_ARG, "handle is NULL");
+  CK(cudaSetDevice(h->device));
+  return OPMM_OK;
+}
+
+opmm_status validate_control(const opmm_control* c, bool need_amplitude) {
+  if (!c) return fail(OPMM_ERR_INVALID_ARG, "control is NULL");
+  if (!(c->dt_ms > 0.0) || !is_finite(c->dt_ms))
+    return fail(OPMM_ERR_INVALID_ARG, "dt_ms must be finite and > 0 (got %g)", c->dt_ms);
+  if (c->n_steps < 1 || c->n_steps > OPMM_MAX_STEPS)
+    return fail(OPMM_ERR_INVALID_ARG, "n_steps must be in [1, %d] (got %d)", OPMM_MAX_STEPS,
+                c->n_steps);
+  if (!is_finite(c->theta0_deg)) return fail(OPMM_ERR_INVALID_ARG, "theta0_deg must be finite");
+  if (std::isinf(c->amplitude_deg)) return fail(OPMM_ERR_INVALID_ARG, "amplitude_deg is infinite");
+  if (need_amplitude && std::isnan(c->amplitude_deg))
+    return fail(OPMM_ERR_INVALID_ARG, "amplitude_deg must be given (no recorded trace here)");
+  if (!(c->pw_default_ms > 0.0) || !is_finite(c->pw_default_ms))
+    return fail(OPMM_ERR_INVALID_ARG, "pw_default_ms must be finite and > 0");
+  return OPMM_OK;
+}
+
+opmm_status validate_space(const opmm_search_space* s, int64_t n) {
+  if (!s) return fail(OPMM_ERR_INVALID_ARG, "search space is NULL");
+  if (s->mode != 0 && s->mode != 1) return fail(OPMM_ERR_INVALID_ARG, "mode must be 0 or 1");
+  for (int d = 0; d < OPMM_NPARAM; ++d) {
+    if (!is_finite(s->lo[d]) || !is_finite(s->hi[d]))
+      return fail(OPMM_ERR_INVALID_ARG, "bounds of dimension %d must be finite", d);
+    if (s->lo[d] > s->hi[d]) return fail(OPMM_ERR_INVALID_ARG, "lo > hi in dimension %d", d);
+    if (s->log_scale[d] > 1) return fail(OPMM_ERR_INVALID_ARG, "log_scale[%d] must be 0/1", d);
+    if (s->log_scale[d] && s->lo[d] != s->hi[d] && !(s->lo[d] > 0.0))
+      return fail(OPMM_ERR_INVALID_ARG, "log dimension %d needs lo > 0", d);
+  }
+  if (s->mode == 1) {
+    long double prod = 1.0L;
+    int64_t p = 1;
+    for (int d = 0; d < OPMM_NPARAM; ++d) {
+      if (s->levels[d] < 1) return fail(OPMM_ERR_INVALID_ARG, "levels[%d] must be >= 1", d);
+      prod *= (long double)s->levels[d];
+      if (prod > 9.2e18L) return fail(OPMM_ERR_INVALID_ARG, "grid too large");
+      p *= s->levels[d];
+    }
+    if (n >= 0 && p != n)
+      return fail(OPMM_ERR_INVALID_ARG, "grid product %lld != n_candidates %lld", (long long)p,
+                  (long long)n);
+  }
+  return OPMM_OK;
+}
+
+// Host preprocessing of the search space: key split, per-dimension kind and
+// span (log(hi/lo) or hi-lo, over (L-1) in grid mode) -- the same
+// expressions the method's generator definition uses (opmm.h).
+opmm::SpaceDev make_space(const opmm_search_space* s) {
+  opmm::SpaceDev d;
+  std::memset(&d, 0, sizeof(d));
+  d.mode = s->mode;
+  d.key0 = (uint32_t)(s->seed & 0xffffffffu);
+  d.key1 = (uint32_t)(s->seed >> 32);
+  for (int k = 0; k < OPMM_NPARAM; ++k) {
+    d.lo[k] = s->lo[k];
+    d.levels[k] = s->mode == 1 ? s->levels[k] : 1;
+    const bool fixed = s->lo[k] == s->hi[k] || (s->mode == 1 && s->levels[k] <= 1);
+    if (fixed) {
+      d.kind[k] = 0;
+      d.span[k] = 0.0;
+    } else if (s->log_scale[k]) {
+      d.kind[k] = 2;
+      const double L = std::log(s->hi[k] / s->lo[k]);
+      d.span[k] = s->mode == 1 ? L / (double)(s->levels[k] - 1) : L;
+    } else {
+      d.kind[k] = 1;
+      const double w = s->hi[k] - s->lo[k];
+      d.span[k] = s->mode == 1 ? w / (double)(s->levels[k] - 1) : w;
+    }
+  }
+  return d;
+}
+
+opmm::CtlDev make_ctl(const opmm_control* c) {
+  opmm::CtlDev d;
+  d.dt_ms = c->dt_ms;
+  d.h = 1e-3 * c->dt_ms;
+  d.n_steps = c->n_steps;
+  d.theta0 = c->theta0_deg;
+  return d;
+}
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+int check_precision(int32_t p) { return p == OPMM_FP64 || p == OPMM_FP32; }
+
+size_t sim_smem(int precision, int32_t n_samples, int block, bool with_rel) {
+  if (precision == OPMM_FP64)
+    return (with_rel ? opmm::rel_bytes<double>(n_samples) : 0) + opmm::stash_bytes<double>(block);
+  return (with_rel ? opmm::rel_bytes<float>(n_samples) : 0) + opmm::stash_bytes<float>(block);
+}
+
+opmm_status grid_for(opmm_handle* h, const void* fn, int block, size_t smem, int64_t work,
+                     int requested, int* grid) {
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, block, smem));
+  if (per_sm < 1) return fail(OPMM_ERR_UNSUPPORTED, "kernel does not fit on an SM (block %d)", block);
+  int64_t g = (int64_t)h->num_sms * per_sm;  // persistent: one wave of resident blocks
+  const int64_t need = (work + block - 1) / block;
+  if (requested > 0) g = requested;
+  if (g > need) g = need;
+  if (g < 1) g = 1;
+  *grid = (int)g;
+  return OPMM_OK;
+}
+
+opmm_status check_block(int block) {
+  if (block < 64 || block > 1024 || block % 32 != 0)
+    return fail(OPMM_ERR_INVALID_ARG, "block_size must be a multiple of 32 in [64, 1024]");
+  return OPMM_OK;
+}
+
+opmm_status record_start(opmm_handle* h, cudaStream_t st) {
+  CK(cudaEventRecord(h->ev0, st));
+  return OPMM_OK;
+}
+opmm_status record_stop(opmm_handle* h, cudaStream_t st) {
+  CK(cudaEventRecord(h->ev1, st));
+  h->timed = true;
+  return OPMM_OK;
+}
+
+opmm_status nccl_fail(ncclResult_t r, const char* what) {
+  return fail(OPMM_ERR_NCCL, "%s failed: %s", what, nccl().getErrorString(r));
+}
+
+// Enqueue one fit (candidates sharded over the handle's ranks) for saccades
+// [s_begin, s_begin + S) of a batch, writing final results to out_dev[S].
+opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_control* ctl,
+                        const double* sacctl_dev, int64_t s_begin, int64_t S,
+                        const opmm_search_space* space, int64_t n_candidates,
+                        const opmm_fit_options* opts, opmm_fit_result* out_dev, bool shard) {
+  const int precision = opts ? opts->precision : OPMM_FP64;
+  const int metric = opts ? opts->metric : OPMM_METRIC_L1;
+  const int integ = opts ? opts->integrator : OPMM_INTEG_PROPAGATOR;
+  const int block = (opts && opts->block_size) ? opts->block_size : kDefaultBlock;
+  if (!check_precision(precision)) return fail(OPMM_ERR_INVALID_ARG, "bad precision %d", precision);
+  if (metric != 0 && metric != 1) return fail(OPMM_ERR_INVALID_ARG, "bad metric %d", metric);
+  if (integ != 0 && integ != 1) return fail(OPMM_ERR_INVALID_ARG, "bad integrator %d", integ);
+  CKS(check_block(block));
+  int64_t b = 0, e = n_candidates;
+  if (shard) opmm_shard_range(n_candidates, h->rank, h->world, &b, &e);
+  const int32_t ns = ctl->n_steps + 1;
+  const size_t smem = sim_smem(precision, ns, block, true);
+  if (smem > kMaxDynSmem) return fail(OPMM_ERR_INVALID_ARG, "trace too long for shared memory");
+  const void* fn = opmm::fit_kernel_ptr(precision, integ, metric);
+  int grid = 1;
+  CKS(grid_for(h, fn, block, smem, e - b, opts ? opts->grid_blocks : 0, &grid));
+  if (e <= b) grid = 1;  // empty shard: one block reports "no candidate"
+  const bool multi = shard && h->world > 1;
+  CKS(ensure(h->partials, h->partials_cap, (size_t)grid * (size_t)(s_begin + S)));
+  CKS(ensure(h->counters, h->counters_cap, (size_t)(s_begin + S), true));
+  if (multi) {
+    CKS(ensure(h->rank_part, h->rank_part_cap, (size_t)(s_begin + S)));
+    CKS(ensure(h->gathered, h->gathered_cap, (size_t)h->world));
+  }
+  opmm::FitArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.rec = rec_dev;
+  a.ctl = make_ctl(ctl);
+  a.space = make_space(space);
+  a.amplitude = ctl->amplitude_deg;
+  a.pw_default = ctl->pw_default_ms;
+  a.sac_ctl = sacctl_dev;
+  a.sac_begin = s_begin;
+  a.begin = b;
+  a.end = e;
+  a.err_out = opts ? opts->err_out : nullptr;
+  a.err_ld = n_candidates;
+  a.partials = h->partials;
+  a.counters = h->counters;
+  a.rank_out = multi ? h->rank_part : nullptr;
+  a.final_out = multi ? nullptr : out_dev;
+  a.out_base = s_begin;
+  CKS(record_start(h, h->stream));
+  for (int64_t s0 = 0; s0 < S; s0 += 65535) {
+    const int64_t sn = (S - s0) < 65535 ? (S - s0) : 65535;
+    a.sac_begin = s_begin + s0;
+    CK(opmm::launch_fit(a, precision, integ, metric, dim3(grid, (unsigned)sn), block, smem,
+                        h->stream));
+  }
+  CKS(record_stop(h, h->stream));
+  if (multi) {
+    // one exchange step: 32-byte (E, index, n_finite, n_evaluated) per rank
+    NcclApi& api = nccl();
+    for (int64_t s = 0; s < S; ++s) {
+      ncclResult_t r = api.allGather(h->rank_part + s_begin + s, h->gathered, sizeof(Partial),
+                                     ncclUint8, h->comm, h->stream);
+      if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather");
+      CK(opmm::launch_merge(h->gathered, h->world, a.space, (uint32_t)(s_begin + s), out_dev + s,
+                            h->stream));
+    }
+  }
+  return OPMM_OK;
+}
+
+opmm_status stage_rec(opmm_handle* h, const double* recorded, size_t count, const double** dev) {
+  if (is_device_ptr(recorded)) {
+    *dev = recorded;
+    return OPMM_OK;
+  }
+  for (size_t k = 0; k < count; ++k)
+    if (!is_finite(recorded[k]))
+      return fail(OPMM_ERR_INVALID_ARG, "recorded sample %zu is not finite", k);
+  CKS(ensure(h->rec, h->rec_cap, count));
+  CK(cudaMemcpyAsync(h->rec, recorded, count * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  *dev = h->rec;
+  return OPMM_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+const char* opmm_version(void) { return "libopmm 0.1.0 (sm_100a)"; }
+
+const char* opmm_last_error(void) { return g_err.c_str(); }
+
+opmm_status opmm_create(opmm_handle** out, int device) {
+  if (!out) return fail(OPMM_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    return fail(OPMM_ERR_CUDA, "no CUDA device available (%s)",
+                e == cudaSuccess ? "0 devices" : cudaGetErrorString(e));
+  }
+  if (device < 0 || device >= count)
+    return fail(OPMM_ERR_INVALID_ARG, "device %d out of range [0, %d)", device, count);
+  CK(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return fail(OPMM_ERR_UNSUPPORTED, "libopmm is built for sm_100a; device is sm_%d%d", prop.major,
+                prop.minor);
+  opmm_handle* h = new opmm_handle();
+  h->device = device;
+  h->num_sms = prop.multiProcessorCount;
+  opmm_status st = OPMM_OK;
+  auto cleanup = [&]() { opmm_destroy(h); };
+  if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreate(&h->ev0) != cudaSuccess || cudaEventCreate(&h->ev1) != cudaSuccess) {
+    st = fail(OPMM_ERR_CUDA, "stream/event creation failed");
+    cleanup();
+    return st;
+  }
+  // allow the largest traces: raise the dynamic shared-memory cap once
+  for (int p = 0; p < 2; ++p)
+    for (int i = 0; i < 2; ++i)
+      for (int m = 0; m < 2; ++m) {
+        cudaFuncSetAttribute(opmm::fit_kernel_ptr(p, i, m),
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDynSmem);
+        cudaFuncSetAttribute(opmm::simscore_kernel_ptr(p, i, m),
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDynSmem);
+      }
+  cudaGetLastError();
+  if ((st = ensure(h->counters, h->counters_cap, 64, true)) != OPMM_OK ||
+      (st = ensure(h->result, h->result_cap, 1)) != OPMM_OK ||
+      (st = ensure_host(h->result_host, h->result_host_cap, 1)) != OPMM_OK) {
+    cleanup();
+    return st;
+  }
+  *out = h;
+  return OPMM_OK;
+}
+
+opmm_status opmm_nccl_unique_id(uint8_t* id) {
+  if (!id) return fail(OPMM_ERR_INVALID_ARG, "id is NULL");
+  NcclApi& api = nccl();
+  if (!api.loaded) return fail(OPMM_ERR_NCCL, "libnccl.so.2 could not be loaded");
+  ncclUniqueId u;
+  ncclResult_t r = api.getUniqueId(&u);
+  if (r != ncclSuccess) return nccl_fail(r, "ncclGetUniqueId");
+  std::memcpy(id, u.internal, OPMM_NCCL_ID_BYTES);
+  return OPMM_OK;
+}
+
+opmm_status opmm_create_nccl(opmm_handle** out, int device, const uint8_t* id, int rank, int world) {
+  if (!id || world < 1 || rank < 0 || rank >= world)
+    return fail(OPMM_ERR_INVALID_ARG, "bad NCCL arguments (rank %d, world %d)", rank, world);
+  CKS(opmm_create(out, device));
+  opmm_handle* h = *out;
+  h->rank = rank;
+  h->world = world;
+  if (world > 1) {
+    NcclApi& api = nccl();
+    if (!api.loaded) {
+      opmm_destroy(h);
+      *out = nullptr;
+      return fail(OPMM_ERR_NCCL, "libnccl.so.2 could not be loaded");
+    }
+    ncclUniqueId u;
+    std::memcpy(u.internal, id, OPMM_NCCL_ID_BYTES);
+    ncclResult_t r = api.commInitRank(&h->comm, world, u, rank);
+    if (r != ncclSuccess) {
+      opmm_destroy(h);
+      *out = nullptr;
+      return nccl_fail(r, "ncclCommInitRank");
+    }
+  }
+  return OPMM_OK;
+}
+
+opmm_status opmm_destroy(opmm_handle* h) {
+  if (!h) return OPMM_OK;
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  if (h->comm && nccl().loaded) nccl().commDestroy(h->comm);
+  cudaFree(h->partials);
+  cudaFree(h->counters);
+  cudaFree(h->rec);
+  cudaFree(h->sacctl);
+  cudaFree(h->rank_part);
+  cudaFree(h->gathered);
+  cudaFree(h->result);
+  if (h->result_host) cudaFreeHost(h->result_host);
+  if (h->ev0) cudaEventDestroy(h->ev0);
+  if (h->ev1) cudaEventDestroy(h->ev1);
+  if (h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+  return OPMM_OK;
+}
+
+opmm_status opmm_get_stream(opmm_handle* h, void** stream) {
+  CKS(check_handle(h));
+  if (!stream) return fail(OPMM_ERR_INVALID_ARG, "stream is NULL");
+  *stream = (void*)h->stream;
+  return OPMM_OK;
+}
+
+opmm_status opmm_last_kernel_ms(opmm_handle* h, float* ms) {
+  CKS(check_handle(h));
+  if (!ms) return fail(OPMM_ERR_INVALID_ARG, "ms is NULL");
+  if (!h->timed) return fail(OPMM_ERR_INVALID_ARG, "no kernel launched yet");
+  CK(cudaEventSynchronize(h->ev1));
+  CK(cudaEventElapsedTime(ms, h->ev0, h->ev1));
+  return OPMM_OK;
+}
+
+opmm_status opmm_shard_range(int64_t n, int rank, int world, int64_t* begin, int64_t* end) {
+  if (!begin || !end || n < 0 || world < 1 || rank < 0 || rank >= world)
+    return fail(OPMM_ERR_INVALID_ARG, "bad shard arguments");
+  // floor(r N / R) without overflow for N < 2^63
+  const __int128 N = n;
+  *begin = (int64_t)(N * rank / world);
+  *end = (int64_t)(N * (rank + 1) / world);
+  return OPMM_OK;
+}
+
+opmm_status opmm_merge_argmin(const double* err, const int64_t* idx, int count, double* best_err,
+                              int64_t* best_idx) {
+  if (!best_err || !best_idx || count < 0 || (count > 0 && (!err || !idx)))
+    return fail(OPMM_ERR_INVALID_ARG, "bad merge arguments");
+  double be = INFINITY;
+  int64_t bi = -1;
+  for (int r = 0; r < count; ++r) {
+    if (idx[r] < 0 || !(err[r] < INFINITY)) continue;
+    if (bi < 0 || err[r] < be || (err[r] == be && idx[r] < bi)) {
+      be = err[r];
+      bi = idx[r];
+    }
+  }
+  *best_err = be;
+  *best_idx = bi;
+  return bi < 0 ? OPMM_ERR_NO_FINITE : OPMM_OK;
+}
+
+opmm_status opmm_validate(const opmm_control* ctl, const opmm_search_space* space,
+                          int64_t n_candidates) {
+  if (n_candidates < 0) return fail(OPMM_ERR_INVALID_ARG, "n_candidates < 0");
+  if (ctl) CKS(validate_control(ctl, false));
+  if (space) CKS(validate_space(space, n_candidates));
+  return OPMM_OK;
+}
+
+opmm_status opmm_generate(opmm_handle* h, const opmm_search_space* space, uint32_t saccade,
+                          int64_t begin, int64_t count, double* opc_out, int64_t ld, void* stream) {
+  CKS(check_handle(h));
+  CKS(validate_space(space, -1));
+  if (begin < 0 || count < 0 || ld < count || (count > 0 && !opc_out))
+    return fail(OPMM_ERR_INVALID_ARG, "bad generate arguments");
+  if (count == 0) return OPMM_OK;
+  cudaStream_t st = stream ? (cudaStream_t)stream : h->stream;
+  int grid = (int)((count + 255) / 256);
+  if (grid > h->num_sms * 8) grid = h->num_sms * 8;
+  CK(opmm::launch_generate(make_space(space), saccade, begin, count, opc_out, ld, grid, st));
+  return OPMM_OK;
+}
+
+opmm_status opmm_simulate(opmm_handle* h, const double* opc, int64_t n, int64_t ld,
+                          const opmm_control* ctl, int32_t precision, int32_t integrator, void* traj,
+                          int64_t ld_out, uint8_t* status, void* stream) {
+  CKS(check_handle(h));
+  CKS(validate_control(ctl, true));
+  if (!check_precision(precision)) return fail(OPMM_ERR_INVALID_ARG, "bad precision");
+  if (integrator != 0 && integrator != 1) return fail(OPMM_ERR_INVALID_ARG, "bad integrator");
+  if (n < 0 || ld < n || ld_out < n || (n > 0 && (!opc || !traj)))
+    return fail(OPMM_ERR_INVALID_ARG, "bad simulate arguments");
+  if (n == 0) return OPMM_OK;
+  cudaStream_t st = stream ? (cudaStream_t)stream : h->stream;
+  const int block = kDefaultBlock;
+  const size_t smem = sim_smem(precision, 0, block, false);
+  const void* fn = opmm::simulate_kernel_ptr(precision, integrator);
+  int grid = 1;
+  CKS(grid_for(h, fn, block, smem, n, 0, &grid));
+  opmm::ExplicitArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.opc = opc;
+  a.n = n;
+  a.ld = ld;
+  a.ctl = make_ctl(ctl);
+  a.amplitude = ctl->amplitude_deg;
+  a.pw_default = ctl->pw_default_ms;
+  a.traj = traj;
+  a.ld_out = ld_out;
+  a.status = status;
+  CKS(record_start(h, st));
+  CK(opmm::launch_explicit(fn, a, dim3(grid), block, smem, st));
+  CKS(record_stop(h, st));
+  return OPMM_OK;
+}
+
+opmm_status opmm_score(opmm_handle* h, const void* traj, int64_t n, int64_t ld, int32_t n_samples,
+                       const double* recorded, int32_t precision, int32_t metric, double* err,
+                       void* stream) {
+  CKS(check_handle(h));
+  if (!check_precision(precision)) return fail(OPMM_ERR_INVALID_ARG, "bad precision");
+  if (metric != 0 && metric != 1) return fail(OPMM_ERR_INVALID_ARG, "bad metric");
+  if (n < 0 || ld < n || n_samples < 1 || n_samples > OPMM_MAX_STEPS + 1 ||
+      (n > 0 && (!traj || !recorded || !err)))
+    return fail(OPMM_ERR_INVALID_ARG, "bad score arguments");
+  if (n == 0) return OPMM_OK;
+  cudaStream_t st = stream ? (cudaStream_t)stream : h->stream;
+  const int block = 256;
+  const size_t smem = (size_t)n_samples * sizeof(double);
+  int grid = 1;
+  CKS(grid_for(h, opmm::score_kernel_ptr(precision, metric), block, smem, n, 0, &grid));
+  opmm::ScoreArgs a{traj, n, ld, n_samples, recorded, err};
+  CKS(record_start(h, st));
+  CK(opmm::launch_score(a, precision, metric, dim3(grid), block, smem, st));
+  CKS(record_stop(h, st));
+  return OPMM_OK;
+}
+
+opmm_status opmm_simulate_score(opmm_handle* h, const double* opc, int64_t n, int64_t ld,
+                                const opmm_control* ctl, const double* recorded, int32_t precision,
+                                int32_t metric, int32_t integrator, double* err, void* stream) {
+  CKS(check_handle(h));
+  CKS(validate_control(ctl, false));
+  if (!check_precision(precision)) return fail(OPMM_ERR_INVALID_ARG, "bad precision");
+  if (metric != 0 && metric != 1) return fail(OPMM_ERR_INVALID_ARG, "bad metric");
+  if (integrator != 0 && integrator != 1) return fail(OPMM_ERR_INVALID_ARG, "bad integrator");
+  if (n < 0 || ld < n || (n > 0 && (!opc || !recorded || !err)))
+    return fail(OPMM_ERR_INVALID_ARG, "bad simulate_score arguments");
+  if (n == 0) return OPMM_OK;
+  cudaStream_t st = stream ? (cudaStream_t)stream : h->stream;
+  const int block = kDefaultBlock;
+  const size_t smem = sim_smem(precision, ctl->n_steps + 1, block, true);
+  if (smem > kMaxDynSmem) return fail(OPMM_ERR_INVALID_ARG, "trace too long for shared memory");
+  const void* fn = opmm::simscore_kernel_ptr(precision, integrator, metric);
+  int grid = 1;
+  CKS(grid_for(h, fn, block, smem, n, 0, &grid));
+  opmm::ExplicitArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.opc = opc;
+  a.n = n;
+  a.ld = ld;
+  a.ctl = make_ctl(ctl);
+  a.amplitude = ctl->amplitude_deg;
+  a.pw_default = ctl->pw_default_ms;
+  a.rec = recorded;
+  a.err = err;
+  CKS(record_start(h, st));
+  CK(opmm::launch_explicit(fn, a, dim3(grid), block, smem, st));
+  CKS(record_stop(h, st));
+  return OPMM_OK;
+}
+
+opmm_status opmm_fit_async(opmm_handle* h, const double* recorded_dev, const opmm_control* ctl,
+                           const opmm_search_space* space, int64_t n_candidates,
+                           const opmm_fit_options* opts, opmm_fit_result* out_dev) {
+  CKS(check_handle(h));
+  CKS(validate_control(ctl, false));
+  if (n_candidates < 0) return fail(OPMM_ERR_INVALID_ARG, "n_candidates < 0");
+  CKS(validate_space(space, n_candidates));
+  if (!recorded_dev || !out_dev) return fail(OPMM_ERR_INVALID_ARG, "NULL recorded/out");
+  return enqueue_fit(h, recorded_dev, ctl, nullptr, 0, 1, space, n_candidates, opts, out_dev, true);
+}
+
+opmm_status opmm_fit(opmm_handle* h, const double* recorded, const opmm_control* ctl,
+                     const opmm_search_space* space, int64_t n_candidates,
+                     const opmm_fit_options* opts, opmm_fit_result* out) {
+  CKS(check_handle(h));
+  CKS(validate_control(ctl, false));
+  if (n_candidates < 0) return fail(OPMM_ERR_INVALID_ARG, "n_candidates < 0");
+  CKS(validate_space(space, n_candidates));
+  if (!recorded || !out) return fail(OPMM_ERR_INVALID_ARG, "NULL recorded/out");
+  const size_t ns = (size_t)ctl->n_steps + 1;
+  const double* rec_dev = nullptr;
+  CKS(stage_rec(h, recorded, ns, &rec_dev));
+  CKS(enqueue_fit(h, rec_dev, ctl, nullptr, 0, 1, space, n_candidates, opts, h->result, true));
+  CK(cudaMemcpyAsync(h->result_host, h->result, sizeof(opmm_fit_result), cudaMemcpyDeviceToHost,
+                     h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  *out = *h->result_host;
+  const bool want_check = !opts || opts->cpu_check;
+  if (want_check && out->best_index >= 0) {
+    // Fig. 4 CPU_check: serial fp64 re-score of the returned OPC on the host
+    if (rec_dev == recorded) {
+      std::string tmp(ns * sizeof(double), '\0');
+      CK(cudaMemcpy(&tmp[0], recorded, ns * sizeof(double), cudaMemcpyDeviceToHost));
+      out->cpu_check = opmm::cpu_check_score(out->opc, reinterpret_cast<const double*>(tmp.data()),
+                                             ctl, opts ? opts->metric : 0);
+    } else {
+      out->cpu_check = opmm::cpu_check_score(out->opc, recorded, ctl, opts ? opts->metric : 0);
+    }
+  }
+  if (out->best_index < 0) return fail(OPMM_ERR_NO_FINITE, "no candidate has a finite error");
+  return OPMM_OK;
+}
+
+opmm_status opmm_fit_batch(opmm_handle* h, const double* recorded, int64_t S,
+                           const opmm_control* ctl, const opmm_search_space* space, int64_t n_per,
+                           const opmm_fit_options* opts, opmm_fit_result* out) {
+  CKS(check_handle(h));
+  if (S < 0 || n_per < 0) return fail(OPMM_ERR_INVALID_ARG, "S and n_per must be >= 0");
+  if (S == 0) return OPMM_OK;
+  if (!recorded || !ctl || !out) return fail(OPMM_ERR_INVALID_ARG, "NULL argument");
+  for (int64_t s = 0; s < S; ++s) {
+    CKS(validate_control(ctl + s, false));
+    if (ctl[s].dt_ms != ctl[0].dt_ms || ctl[s].n_steps != ctl[0].n_steps)
+      return fail(OPMM_ERR_INVALID_ARG, "all saccades of a batch share dt_ms and n_steps");
+  }
+  CKS(validate_space(space, n_per));
+  if (opts && opts->err_out)
+    return fail(OPMM_ERR_UNSUPPORTED, "err_out is not supported by opmm_fit_batch");
+  // saccades are independent problems: rank r takes its contiguous share
+  int64_t sb = 0, se = S;
+  opmm_shard_range(S, h->rank, h->world, &sb, &se);
+  const int64_t Sl = se - sb;
+  if (Sl == 0) return OPMM_OK;
+  const size_t ns = (size_t)ctl[0].n_steps + 1;
+  const double* rec_dev = nullptr;
+  if (is_device_ptr(recorded)) {
+    rec_dev = recorded;
+  } else {
+    for (size_t k = 0; k < (size_t)S * ns; ++k)
+      if (!is_finite(recorded[k])) return fail(OPMM_ERR_INVALID_ARG, "recorded sample not finite");
+    CKS(ensure(h->rec, h->rec_cap, (size_t)S * ns));
+    CK(cudaMemcpyAsync(h->rec, recorded, (size_t)S * ns * sizeof(double), cudaMemcpyHostToDevice,
+                       h->stream));
+    rec_dev = h->rec;
+  }
+  std::string sc((size_t)S * 2 * sizeof(double), '\0');
+  double* scp = reinterpret_cast<double*>(&sc[0]);
+  for (int64_t s = 0; s < S; ++s) {
+    scp[2 * s] = ctl[s].amplitude_deg;
+    scp[2 * s + 1] = ctl[s].pw_default_ms;
+  }
+  CKS(ensure(h->sacctl, h->sacctl_cap, (size_t)S * 2));
+  CK(cudaMemcpyAsync(h->sacctl, scp, (size_t)S * 2 * sizeof(double), cudaMemcpyHostToDevice,
+                     h->stream));
+  CKS(ensure(h->result, h->result_cap, (size_t)Sl));
+  CKS(ensure_host(h->result_host, h->result_host_cap, (size_t)Sl));
+  // candidates are not sharded within a saccade here (shard = false)
+  CKS(enqueue_fit(h, rec_dev, ctl, h->sacctl, sb, Sl, space, n_per, opts, h->result, false));
+  CK(cudaMemcpyAsync(h->result_host, h->result, (size_t)Sl * sizeof(opmm_fit_result),
+                     cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  const bool want_check = !opts || opts->cpu_check;
+  std::string tmp;
+  const double* rec_host = recorded;
+  if (want_check && rec_dev == recorded) {
+    tmp.resize((size_t)S * ns * sizeof(double));
+    CK(cudaMemcpy(&tmp[0], recorded, (size_t)S * ns * sizeof(double), cudaMemcpyDeviceToHost));
+    rec_host = reinterpret_cast<const double*>(tmp.data());
+  }
+  for (int64_t j = 0; j < Sl; ++j) {
+    opmm_fit_result r = h->result_host[j];
+    if (want_check && r.best_index >= 0)
+      r.cpu_check = opmm::cpu_check_score(r.opc, rec_host + (size_t)(sb + j) * ns, ctl + sb + j,
+                                           opts ? opts->metric : 0);
+    out[sb + j] = r;
+  }
+  return OPMM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,471 @@
+// opmm_device.cuh -- device-side building blocks of the libopmm hot path
+// (sm_100a).  Everything here runs per candidate, one candidate per thread,
+// with the OPC vector, the per-candidate propagator and the plant state in
+// registers and the relativized recorded trace in shared memory.
+//
+// Paper / spec anchors (see DESIGN.md for the readings Q1..Q21):
+//   OPC vector, Table-1 order ............ PAPER.md:150-167
+//   pulse-step control signal ............ PAPER.md:106-117 (activation at onset,
+//                                           deactivation at offset), PAPER.md:167 (PW)
+//   plant topology ....................... Fig. 1; equations SPEC D1
+//   integrator: classical RK4, h = dt .... SPEC D2
+//   error = absolute difference .......... PAPER.md:366
+//   exhaustive search / argmin ........... PAPER.md:202
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace opmm {
+
+constexpr int NP = 18;
+constexpr double CAP = 1e20;        // reading Q10
+constexpr double PENALTY = 1e10;    // SPEC D8
+constexpr double NANT_FLOOR = 0.01; // SPEC D4
+
+enum { KSE_AG = 0, KSE_ANT, KLT_AG, KLT_ANT, B_AG, B_ANT, B_P, NC_AG, NC_ANT, J_,
+       TAU_AC_AG, TAU_AC_ANT, TAU_DE_AG, TAU_DE_ANT, NC_FIX, NSAC_AG, NSAC_ANT, PW_ };
+
+// Search space, preprocessed on the host (kernel parameter -> constant bank).
+struct SpaceDev {
+  int32_t mode;          // 0 random (Philox), 1 grid
+  uint32_t key0, key1;   // Philox key = seed
+  uint8_t kind[NP];      // 0 fixed (lo), 1 linear, 2 log
+  double lo[NP];
+  // random: linear hi-lo, log log(hi/lo); grid: linear (hi-lo)/(L-1), log log(hi/lo)/(L-1)
+  double span[NP];
+  int64_t levels[NP];    // grid radices (1 = not a grid dimension)
+};
+
+// Per-launch control (shared by every candidate of a saccade).
+struct CtlDev {
+  double dt_ms;
+  double h;              // dt in seconds
+  int32_t n_steps;
+  double theta0;         // explicit simulate output offset
+};
+
+// ----------------------------------------------------------------------------
+// Philox4x32-10 (Salmon et al. SC'11), reading Q15.
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    k.x += 0x9E3779B9u;
+    k.y += 0xBB67AE85u;
+  }
+  return c;
+}
+
+// u = (w + 0.5) 2^-32 is exact in fp64; the mapping uses explicitly rounded
+// operations so no FMA contraction changes the candidate bits.
+__device__ __forceinline__ double map_word(const SpaceDev& sp, int d, uint32_t w) {
+  const double u = __dmul_rn(__dadd_rn((double)w, 0.5), 2.3283064365386962890625e-10);
+  if (sp.kind[d] == 0) return sp.lo[d];
+  if (sp.kind[d] == 1) return __dadd_rn(sp.lo[d], __dmul_rn(u, sp.span[d]));
+  return __dmul_rn(sp.lo[d], exp(__dmul_rn(u, sp.span[d])));
+}
+
+// Candidate index -> OPC vector (PAPER.md:202 exhaustive search over OPC values).
+// The dimension loops are deliberately not unrolled: the generator runs once
+// per candidate, and a rolled loop keeps the kernel's instruction footprint
+// small (the per-step loop is what must stay resident in the i-cache).
+__device__ __forceinline__ void generate_opc(const SpaceDev& sp, uint32_t saccade, int64_t idx,
+                                             double p[NP]) {
+  if (sp.mode == 0) {
+    const uint2 key = make_uint2(sp.key0, sp.key1);
+    const uint32_t ilo = (uint32_t)((uint64_t)idx & 0xffffffffu);
+    const uint32_t ihi = (uint32_t)((uint64_t)idx >> 32);
+#pragma unroll 1
+    for (int j = 0; j < 5; ++j) {
+      const uint4 w = philox4x32_10(make_uint4(ilo, ihi, saccade, (uint32_t)j), key);
+      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll 1
+      for (int r = 0; r < 4; ++r) {
+        const int d = 4 * j + r;
+        if (d < NP) p[d] = map_word(sp, d, ws[r]);
+      }
+    }
+  } else {
+    uint64_t rem = (uint64_t)idx;
+#pragma unroll 1
+    for (int d = 0; d < NP; ++d) {
+      uint64_t digit = 0;
+      const uint64_t L = (uint64_t)sp.levels[d];
+      if (L > 1) {
+        digit = rem % L;
+        rem = rem / L;
+      }
+      if (sp.kind[d] == 0 || L <= 1) p[d] = sp.lo[d];
+      else if (sp.kind[d] == 1) p[d] = __dadd_rn(sp.lo[d], __dmul_rn((double)digit, sp.span[d]));
+      else p[d] = __dmul_rn(sp.lo[d], exp(__dmul_rn((double)digit, sp.span[d])));
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// Physical check (SPEC D8 SPEC.md:248, reading Q13): 0 if physical, else the
+// penalty 1e10 (1 + sum of violation amounts).  PW NaN is the placeholder.
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ double physical_penalty(const double p[NP]) {
+  bool bad = false;
+  double amount = 0.0;
+#pragma unroll
+  for (int i = 0; i < NP; ++i) {
+    const double v = p[i];
+    const bool strict = (i == KSE_AG || i == KSE_ANT || i == B_AG || i == B_ANT || i == J_ ||
+                         i == TAU_AC_AG || i == TAU_AC_ANT || i == TAU_DE_AG || i == TAU_DE_ANT ||
+                         i == PW_);
+    if (i == PW_ && isnan(v)) continue;
+    if (!isfinite(v)) { bad = true; amount += 1.0; continue; }
+    if (strict ? !(v > 0.0) : !(v >= 0.0)) {
+      bad = true;
+      if (v < 0.0) amount += -v;
+    }
+  }
+  if (!bad) {
+    const double g_ag = p[KSE_AG] / (p[KLT_AG] + p[KSE_AG]);
+    const double g_ant = p[KSE_ANT] / (p[KLT_ANT] + p[KSE_ANT]);
+    const double G = g_ag * (p[NC_AG] + p[KLT_AG]) + g_ant * (p[NC_ANT] + p[KLT_ANT]);
+    if (!(G > 0.0)) bad = true;
+  }
+  return bad ? PENALTY * (1.0 + amount) : 0.0;
+}
+
+// ----------------------------------------------------------------------------
+// Per-candidate setup.  The plant (SPEC D1) is linear and time-invariant
+// within each control phase, so we integrate the deviation from the fixation
+// equilibrium y* (reading Q5): y~ = y - y*, which obeys the same ODE with the
+// drive n replaced by n~ = n - N_C_FIX and starts at 0; theta~ IS Delta-theta.
+//
+// z = (theta, omega, x_AG, x_ANT), f = (f_AG, f_ANT);  Z = h M (dimensionless):
+//   Z01 = h
+//   Z1* = h/J (-(K_SE_AG+K_SE_ANT), -B_P, K_SE_AG, -K_SE_ANT)
+//   Z2* = h/B_AG  (-(N_C_AG - K_SE_AG), 0, -(K_LT_AG + K_SE_AG), 0)
+//   Z3* = h/B_ANT ((N_C_ANT - K_SE_ANT), 0, 0, -(K_LT_ANT + K_SE_ANT))
+//   x_m is driven by f_m / B_m;   f_m' = (n_m - f_m)/tau_m,  zd_m = -dt/tau_m.
+// ----------------------------------------------------------------------------
+struct Mech {
+  double z01, z10, z11, z12, z13, z20, z22, z30, z33;
+  double hb_ag, hb_ant;   // h / B_m
+};
+
+struct Phase {            // control of one phase (pulse or post-pulse step)
+  double zd_ag, zd_ant;   // -dt / tau_m
+  double nt_ag, nt_ant;   // n~_m = n_m - N_C_FIX
+};
+
+struct Setup {
+  Mech m;
+  Phase ph[2];            // 0 = pulse (tau_AC, N_SAC), 1 = step (tau_DE, D4 levels)
+  int32_t n_pulse;        // steps k < n_pulse use phase 0 (reading Q6)
+};
+
+__device__ __forceinline__ void make_setup(const double p_in[NP], double dt_ms, double h,
+                                           int32_t n_steps, double Aprime, double pw_default,
+                                           Setup& s) {
+  const double Kag = p_in[KSE_AG], Kant = p_in[KSE_ANT], Lag = p_in[KLT_AG], Lant = p_in[KLT_ANT];
+  const double Bag = p_in[B_AG], Bant = p_in[B_ANT], Bp = p_in[B_P];
+  const double Ncag = p_in[NC_AG], Ncant = p_in[NC_ANT], J = p_in[J_], F = p_in[NC_FIX];
+  double PW = p_in[PW_];
+  if (isnan(PW)) PW = pw_default;
+  const double hJ = h / J, hBag = h / Bag, hBant = h / Bant;
+  s.m.z01 = h;
+  s.m.z10 = -(Kag + Kant) * hJ;
+  s.m.z11 = -Bp * hJ;
+  s.m.z12 = Kag * hJ;
+  s.m.z13 = -Kant * hJ;
+  s.m.z20 = -(Ncag - Kag) * hBag;
+  s.m.z22 = -(Lag + Kag) * hBag;
+  s.m.z30 = (Ncant - Kant) * hBant;
+  s.m.z33 = -(Lant + Kant) * hBant;
+  s.m.hb_ag = hBag;
+  s.m.hb_ant = hBant;
+  // Post-pulse step levels: static balance at theta* + A' (D4 generalised, Q4).
+  const double g_ag = Kag / (Lag + Kag), g_ant = Kant / (Lant + Kant);
+  const double G = g_ag * (Ncag + Lag) + g_ant * (Ncant + Lant);
+  const double delta = G * Aprime / (g_ag + g_ant);
+  double nt_ag = delta, nt_ant = -delta;
+  if (F - delta < NANT_FLOOR) {
+    const double theta_star = (g_ag * F - g_ant * F) / G;
+    const double n_ag = (G * (theta_star + Aprime) + NANT_FLOOR * g_ant) / g_ag;
+    nt_ag = n_ag - F;
+    nt_ant = NANT_FLOOR - F;
+  }
+  s.ph[0].zd_ag = -dt_ms / p_in[TAU_AC_AG];
+  s.ph[0].zd_ant = -dt_ms / p_in[TAU_AC_ANT];
+  s.ph[0].nt_ag = p_in[NSAC_AG] - F;
+  s.ph[0].nt_ant = p_in[NSAC_ANT] - F;
+  s.ph[1].zd_ag = -dt_ms / p_in[TAU_DE_AG];
+  s.ph[1].zd_ant = -dt_ms / p_in[TAU_DE_ANT];
+  s.ph[1].nt_ag = nt_ag;
+  s.ph[1].nt_ant = nt_ant;
+  // Pulse window: onset at step 0, n_pulse = ceil(PW/dt) (IEEE divide), Q6.
+  const double npd = ceil(PW / dt_ms);
+  s.n_pulse = npd > (double)n_steps ? n_steps + 1 : (int32_t)npd;
+}
+
+// ----------------------------------------------------------------------------
+// Propagator form of the RK4 map: for one phase,
+//   [z; f]+ = P(hA) [z; f] + hQ(hA) b~,  P(x) = 1+x+x^2/2+x^3/6+x^4/24,
+//   Q(x) = 1+x/2+x^2/6+x^3/24 -- exactly the classical RK4 step of the LTI
+// system (textbook identity; pinned in tests as P7).  A is block upper
+// triangular [[M, C],[0, D]], D = diag(-1/tau), C = diag(1/B) on the x rows,
+// so with u_i = Z^i (h c_m) and a_i(zd) = sum_{j>i} zd^(j-1-i)/j!:
+//   mech <- f block  X[:,m] = sum_{i=0..3} u_i a_i(zd_m)
+//   forcing          c      = sum_m (-zd_m n~_m) sum_{i=0..2} u_i a_{i+1}(zd_m)
+//   f update         f_m+   = (1 + zd_m a_0) f_m + (-zd_m a_0 n~_m)
+// The 4x4 mechanical block P(Z) is phase-independent.
+// ----------------------------------------------------------------------------
+template <typename T>
+struct PhaseProp {
+  T X[4][2];
+  T c[4];
+  T pf[2], qf[2];
+};
+
+template <typename T>
+struct Prop {
+  T P[4][4];
+  PhaseProp<T> ph[2];
+};
+
+__device__ __forceinline__ void zmul_vec(const Mech& m, const double v[4], double out[4]) {
+  out[0] = m.z01 * v[1];
+  out[1] = m.z10 * v[0] + m.z11 * v[1] + m.z12 * v[2] + m.z13 * v[3];
+  out[2] = m.z20 * v[0] + m.z22 * v[2];
+  out[3] = m.z30 * v[0] + m.z33 * v[3];
+}
+
+// T <- I + s * Z T   (Horner step for P(Z))
+__device__ __forceinline__ void horner_step(const Mech& m, double s, double Tm[4][4]) {
+  double R[4][4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    double col[4] = {Tm[0][j], Tm[1][j], Tm[2][j], Tm[3][j]}, o[4];
+    zmul_vec(m, col, o);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) R[i][j] = (i == j ? 1.0 : 0.0) + s * o[i];
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) Tm[i][j] = R[i][j];
+}
+
+template <typename T>
+__device__ __forceinline__ void make_prop(const Setup& s, Prop<T>& pr) {
+  const Mech& m = s.m;
+  double Tm[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) Tm[i][j] = (i == j ? 1.0 : 0.0);
+  horner_step(m, 0.25, Tm);              // I + Z/4
+  horner_step(m, 1.0 / 3.0, Tm);         // I + Z/3 (I + Z/4)
+  horner_step(m, 0.5, Tm);               // I + Z/2 (...)
+  horner_step(m, 1.0, Tm);               // I + Z (...) = P(Z)
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) pr.P[i][j] = (T)Tm[i][j];
+  // u_i = Z^i (h c_m): c_AG = e_2 / B_AG, c_ANT = e_3 / B_ANT.
+  double u[2][4][4];
+#pragma unroll
+  for (int mm = 0; mm < 2; ++mm) {
+    u[mm][0][0] = 0.0; u[mm][0][1] = 0.0;
+    u[mm][0][2] = (mm == 0) ? m.hb_ag : 0.0;
+    u[mm][0][3] = (mm == 0) ? 0.0 : m.hb_ant;
+#pragma unroll
+    for (int i = 1; i < 4; ++i) zmul_vec(m, u[mm][i - 1], u[mm][i]);
+  }
+#pragma unroll
+  for (int ph = 0; ph < 2; ++ph) {
+    double c[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int mm = 0; mm < 2; ++mm) {
+      const double zd = mm == 0 ? s.ph[ph].zd_ag : s.ph[ph].zd_ant;
+      const double nt = mm == 0 ? s.ph[ph].nt_ag : s.ph[ph].nt_ant;
+      const double a3 = 1.0 / 24.0;
+      const double a2 = 1.0 / 6.0 + zd * a3;
+      const double a1 = 0.5 + zd * a2;
+      const double a0 = 1.0 + zd * a1;
+      const double g = -zd * nt;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        pr.ph[ph].X[r][mm] = (T)(u[mm][0][r] * a0 + u[mm][1][r] * a1 + u[mm][2][r] * a2 +
+                                 u[mm][3][r] * a3);
+        c[r] += g * (u[mm][0][r] * a1 + u[mm][1][r] * a2 + u[mm][2][r] * a3);
+      }
+      pr.ph[ph].pf[mm] = (T)(1.0 + zd * a0);
+      pr.ph[ph].qf[mm] = (T)(g * a0);
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) pr.ph[ph].c[r] = (T)c[r];
+  }
+}
+
+// ----------------------------------------------------------------------------
+// Trace staging (D5/D6, reading Q7/Q8): s = sign(A) (+1 for A = 0),
+// A' = |A|, rel_k = s (rec_k - rec_0), into shared memory in the loop's type.
+// ----------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ void stage_trace(const double* __restrict__ rec, int32_t n_samples,
+                                            double amplitude, T* rel, double& sgn,
+                                            double& Aprime) {
+  const double r0 = rec[0];
+  const double A = isnan(amplitude) ? rec[n_samples - 1] - r0 : amplitude;
+  sgn = A < 0.0 ? -1.0 : 1.0;
+  Aprime = fabs(A);
+  for (int k = threadIdx.x; k < n_samples; k += blockDim.x) rel[k] = (T)(sgn * (rec[k] - r0));
+}
+
+__device__ __forceinline__ double tabs(double x) { return fabs(x); }
+__device__ __forceinline__ float tabs(float x) { return fabsf(x); }
+
+template <int METRIC, typename T>
+__device__ __forceinline__ void accumulate(T& acc, T d) {
+  if (METRIC == 0) acc += tabs(d);
+  else acc = fma(d, d, acc);
+}
+
+template <int METRIC, typename T>
+__device__ __forceinline__ double finish_error(T acc, int32_t n_samples) {
+  const double a = (double)acc;
+  if (!(a < CAP)) return __longlong_as_double(0x7ff0000000000000LL);  // +inf (Q10)
+  return METRIC == 0 ? a : sqrt(a / (double)n_samples);
+}
+
+// ----------------------------------------------------------------------------
+// Integrate + fused score, PROPAGATOR form: 26 FMA per step for the RK4 map +
+// 2 for the score.  TRAJ (dump mode, no trace): store theta0 + s*Delta-theta_k
+// time-major and accumulate |Delta-theta| instead, to flag divergence.
+// ----------------------------------------------------------------------------
+template <typename T, int METRIC, bool TRAJ>
+__device__ __forceinline__ T run_propagator(const Prop<T>& pr, int32_t n_pulse, int32_t n_steps,
+                                            const T* __restrict__ rel, T* __restrict__ traj,
+                                            int64_t ld_out, T theta0, T sgn,
+                                            T* __restrict__ stash, int stash_ld) {
+  T th = T(0), om = T(0), xa = T(0), xn = T(0), fa = T(0), fn = T(0);
+  T acc = T(0);
+  // The 16 step-phase coefficients wait in a per-thread shared-memory stash
+  // ([16][stash_ld], conflict-free) instead of registers; the 4x4 P stays in
+  // registers for the whole loop.
+  const PhaseProp<T>& q = pr.ph[1];
+  {
+    const T v[16] = {q.X[0][0], q.X[0][1], q.X[1][0], q.X[1][1], q.X[2][0], q.X[2][1], q.X[3][0],
+                     q.X[3][1], q.c[0], q.c[1], q.c[2], q.c[3], q.pf[0], q.pf[1], q.qf[0], q.qf[1]};
+#pragma unroll
+    for (int j = 0; j < 16; ++j) stash[j * stash_ld] = v[j];
+  }
+  T X00 = pr.ph[0].X[0][0], X01 = pr.ph[0].X[0][1], X10 = pr.ph[0].X[1][0], X11 = pr.ph[0].X[1][1];
+  T X20 = pr.ph[0].X[2][0], X21 = pr.ph[0].X[2][1], X30 = pr.ph[0].X[3][0], X31 = pr.ph[0].X[3][1];
+  T c0 = pr.ph[0].c[0], c1 = pr.ph[0].c[1], c2 = pr.ph[0].c[2], c3 = pr.ph[0].c[3];
+  T pa = pr.ph[0].pf[0], pn = pr.ph[0].pf[1], qa = pr.ph[0].qf[0], qn = pr.ph[0].qf[1];
+  const T P00 = pr.P[0][0], P01 = pr.P[0][1], P02 = pr.P[0][2], P03 = pr.P[0][3];
+  const T P10 = pr.P[1][0], P11 = pr.P[1][1], P12 = pr.P[1][2], P13 = pr.P[1][3];
+  const T P20 = pr.P[2][0], P21 = pr.P[2][1], P22 = pr.P[2][2], P23 = pr.P[2][3];
+  const T P30 = pr.P[3][0], P31 = pr.P[3][1], P32 = pr.P[3][2], P33 = pr.P[3][3];
+  if (TRAJ) traj[0] = theta0;
+  // sample 0 contributes |0 - rel_0| = 0 exactly (rel_0 = 0)
+#pragma unroll 2
+  for (int32_t k = 0; k < n_steps; ++k) {
+    const bool sw = (k == n_pulse);
+    // warp-uniform branch: taken only at the steps where some lane's pulse
+    // ends, so the coefficient reload is never predicated into every step
+    if (__any_sync(0xffffffffu, sw)) {  // callers keep all 32 lanes active
+      if (sw) {
+        X00 = stash[0 * stash_ld]; X01 = stash[1 * stash_ld]; X10 = stash[2 * stash_ld];
+        X11 = stash[3 * stash_ld]; X20 = stash[4 * stash_ld]; X21 = stash[5 * stash_ld];
+        X30 = stash[6 * stash_ld]; X31 = stash[7 * stash_ld];
+        c0 = stash[8 * stash_ld]; c1 = stash[9 * stash_ld]; c2 = stash[10 * stash_ld];
+        c3 = stash[11 * stash_ld];
+        pa = stash[12 * stash_ld]; pn = stash[13 * stash_ld];
+        qa = stash[14 * stash_ld]; qn = stash[15 * stash_ld];
+      }
+    }
+    const T r = TRAJ ? T(0) : rel[k + 1];
+    const T nth = fma(P00, th, fma(P01, om, fma(P02, xa, fma(P03, xn, fma(X00, fa, fma(X01, fn, c0))))));
+    const T nom = fma(P10, th, fma(P11, om, fma(P12, xa, fma(P13, xn, fma(X10, fa, fma(X11, fn, c1))))));
+    const T nxa = fma(P20, th, fma(P21, om, fma(P22, xa, fma(P23, xn, fma(X20, fa, fma(X21, fn, c2))))));
+    const T nxn = fma(P30, th, fma(P31, om, fma(P32, xa, fma(P33, xn, fma(X30, fa, fma(X31, fn, c3))))));
+    fa = fma(pa, fa, qa);
+    fn = fma(pn, fn, qn);
+    th = nth; om = nom; xa = nxa; xn = nxn;
+    accumulate<METRIC>(acc, TRAJ ? th : th - r);  // TRAJ: no trace, sum |dtheta|
+    if (TRAJ) traj[(int64_t)(k + 1) * ld_out] = fma(sgn, th, theta0);
+  }
+  return acc;
+}
+
+// ----------------------------------------------------------------------------
+// Integrate + fused score, RK4_STAGES form: the four classical stages
+// evaluated literally (SPEC D2), in deviation coordinates, K_i = h f(Y_i).
+// ----------------------------------------------------------------------------
+template <typename T, int METRIC, bool TRAJ>
+__device__ __forceinline__ T run_rk4_stages(const Setup& s, int32_t n_steps,
+                                            const T* __restrict__ rel, T* __restrict__ traj,
+                                            int64_t ld_out, T theta0, T sgn) {
+  const T z01 = (T)s.m.z01, z10 = (T)s.m.z10, z11 = (T)s.m.z11, z12 = (T)s.m.z12,
+          z13 = (T)s.m.z13, z20 = (T)s.m.z20, z22 = (T)s.m.z22, z30 = (T)s.m.z30,
+          z33 = (T)s.m.z33, hba = (T)s.m.hb_ag, hbn = (T)s.m.hb_ant;
+  T y[6] = {T(0), T(0), T(0), T(0), T(0), T(0)};
+  T acc = T(0);
+  T zda = (T)s.ph[0].zd_ag, zdn = (T)s.ph[0].zd_ant;
+  T zna = (T)(s.ph[0].zd_ag * s.ph[0].nt_ag), znn = (T)(s.ph[0].zd_ant * s.ph[0].nt_ant);
+  if (TRAJ) traj[0] = theta0;
+  const T half = T(0.5), sixth = T(1.0 / 6.0), two = T(2);
+  for (int32_t k = 0; k < n_steps; ++k) {
+    if (k == s.n_pulse) {
+      zda = (T)s.ph[1].zd_ag; zdn = (T)s.ph[1].zd_ant;
+      zna = (T)(s.ph[1].zd_ag * s.ph[1].nt_ag); znn = (T)(s.ph[1].zd_ant * s.ph[1].nt_ant);
+    }
+    T K[4][6];
+    T Y[6];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) Y[i] = y[i];
+#pragma unroll
+    for (int st = 0; st < 4; ++st) {
+      K[st][0] = z01 * Y[1];
+      K[st][1] = fma(z10, Y[0], fma(z11, Y[1], fma(z12, Y[2], z13 * Y[3])));
+      K[st][2] = fma(z20, Y[0], fma(z22, Y[2], hba * Y[4]));
+      K[st][3] = fma(z30, Y[0], fma(z33, Y[3], hbn * Y[5]));
+      K[st][4] = fma(zda, Y[4], -zna);
+      K[st][5] = fma(zdn, Y[5], -znn);
+      if (st < 3) {
+        const T w = st == 2 ? T(1) : half;
+#pragma unroll
+        for (int i = 0; i < 6; ++i) Y[i] = fma(w, K[st][i], y[i]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+      const T t = fma(two, K[2][i], fma(two, K[1][i], K[0][i])) + K[3][i];
+      y[i] = fma(sixth, t, y[i]);
+    }
+    accumulate<METRIC>(acc, TRAJ ? y[0] : y[0] - rel[k + 1]);
+    if (TRAJ) traj[(int64_t)(k + 1) * ld_out] = fma(sgn, y[0], theta0);
+  }
+  return acc;
+}
+
+// ----------------------------------------------------------------------------
+// (E, index) lexicographic order (reading Q12).
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ bool better(double e1, int64_t i1, double e2, int64_t i2) {
+  return e1 < e2 || (e1 == e2 && i1 < i2);
+}
+
+__device__ __forceinline__ void warp_argmin(double& e, int64_t& i) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const double oe = __shfl_xor_sync(0xffffffffu, e, off);
+    const int64_t oi = __shfl_xor_sync(0xffffffffu, i, off);
+    if (better(oe, oi, e, i)) { e = oe; i = oi; }
+  }
+}
+
+}  // namespace opmm

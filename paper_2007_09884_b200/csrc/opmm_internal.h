@@ -1,0 +1,86 @@
+// opmm_internal.h -- launch-argument structs shared by opmm_api.cu (host) and
+// opmm_kernels.cu (device).  Not part of the public ABI.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "opmm.h"
+#include "opmm_device.cuh"
+
+namespace opmm {
+
+// Dynamic shared memory of the simulate kernels: the relativized trace
+// (rel_bytes) followed by the per-thread phase-coefficient stash [16][block].
+template <typename T>
+__host__ __device__ constexpr size_t rel_bytes(int32_t n_samples) {
+  return ((size_t)n_samples * sizeof(T) + 15) & ~(size_t)15;
+}
+template <typename T>
+__host__ __device__ constexpr size_t stash_bytes(int block) {
+  return (size_t)16 * block * sizeof(T);
+}
+
+// Per-block / per-rank (E, index) partial: 32 bytes.
+struct Partial {
+  double e;
+  int64_t i;
+  int64_t nf;     // finite candidates
+  int64_t neval;  // evaluated candidates (rank partials only)
+};
+
+struct FitArgs {
+  const double* rec;        // device [S][n_steps+1]
+  CtlDev ctl;
+  SpaceDev space;
+  double amplitude;         // single fit: signed A (NaN => rec[n]-rec[0])
+  double pw_default;
+  const double* sac_ctl;    // batch: device [S][2] = (amplitude, pw_default); else nullptr
+  int64_t sac_begin;        // first saccade of this launch (blockIdx.y offset)
+  int64_t begin, end;       // candidate range of this rank
+  double* err_out;          // optional device, indexed [sac * err_ld + i]
+  int64_t err_ld;
+  Partial* partials;        // [S][gridDim.x]
+  unsigned int* counters;   // [S], zero between launches
+  Partial* rank_out;        // optional [S]: per-rank result (world > 1)
+  opmm_fit_result* final_out;  // optional: final result of saccade s at [s - out_base]
+  int64_t out_base;
+};
+
+struct ExplicitArgs {
+  const double* opc;        // device SoA [18][ld]
+  int64_t n, ld;
+  CtlDev ctl;
+  double amplitude, pw_default;
+  const double* rec;        // simscore: device [n_steps+1]
+  double* err;              // simscore: device [n]
+  void* traj;               // simulate: device [(n_steps+1) x ld_out]
+  int64_t ld_out;
+  uint8_t* status;          // simulate: optional device [n]
+};
+
+struct ScoreArgs {
+  const void* traj;
+  int64_t n, ld;
+  int32_t n_samples;
+  const double* rec;
+  double* err;
+};
+
+const void* fit_kernel_ptr(int precision, int integrator, int metric);
+const void* simscore_kernel_ptr(int precision, int integrator, int metric);
+const void* simulate_kernel_ptr(int precision, int integrator);
+const void* score_kernel_ptr(int precision, int metric);
+
+cudaError_t launch_fit(const FitArgs& a, int precision, int integrator, int metric, dim3 grid,
+                       int block, size_t smem, cudaStream_t st);
+cudaError_t launch_merge(const Partial* gathered, int world, const SpaceDev& sp, uint32_t saccade,
+                         opmm_fit_result* out, cudaStream_t st);
+cudaError_t launch_explicit(const void* fn, const ExplicitArgs& a, dim3 grid, int block, size_t smem,
+                            cudaStream_t st);
+cudaError_t launch_score(const ScoreArgs& a, int precision, int metric, dim3 grid, int block,
+                         size_t smem, cudaStream_t st);
+cudaError_t launch_generate(const SpaceDev& sp, uint32_t saccade, int64_t begin, int64_t count,
+                            double* out, int64_t ld, int grid, cudaStream_t st);
+
+}  // namespace opmm

@@ -1,0 +1,355 @@
+// opmm_kernels.cu -- sm_100a kernels of the libopmm hot path and their
+// host-side launchers (called only from opmm_api.cu).
+//
+//   fit_kernel         generate -> setup -> integrate+score -> argmin, fused;
+//                      warp shuffle -> shared -> per-block partial -> the last
+//                      block reduces the partials.
+//   merge_kernel       world > 1: lexicographic min of the gathered per-rank
+//                      partials + winner regeneration (a8).
+//   simscore_kernel    explicit OPC batch -> E per candidate (no trajectories).
+//   simulate_kernel    explicit OPC batch -> time-major trajectories (dump mode).
+//   score_kernel       stored trajectories -> E per candidate (HBM-bound).
+//   generate_kernel    candidate dump (SoA), bit-identical to fit_kernel's.
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "opmm.h"
+#include "opmm_device.cuh"
+#include "opmm_internal.h"
+
+namespace opmm {
+
+// ---------------------------------------------------------------------------
+// Evaluate one candidate: physical check, setup, integrate + fused score.
+// ---------------------------------------------------------------------------
+template <typename T, int INTEG, int METRIC, bool TRAJ>
+__device__ __forceinline__ double evaluate(const double p[NP], const CtlDev& c, double Aprime,
+                                           double pw_default, const T* rel, T* traj,
+                                           int64_t ld_out, double sgn, uint8_t* status,
+                                           T* stash) {
+  const double pen = physical_penalty(p);
+  if (pen != 0.0) {
+    if (TRAJ) {
+      const T nanv = (T)__longlong_as_double(0x7ff8000000000000LL);
+      for (int32_t k = 0; k <= c.n_steps; ++k) traj[(int64_t)k * ld_out] = nanv;
+    }
+    if (status) *status = 1;
+    return pen;
+  }
+  Setup s;
+  make_setup(p, c.dt_ms, c.h, c.n_steps, Aprime, pw_default, s);
+  T acc;
+  if (INTEG == 0) {
+    Prop<T> pr;
+    make_prop<T>(s, pr);
+    acc = run_propagator<T, METRIC, TRAJ>(pr, s.n_pulse, c.n_steps, rel, traj, ld_out,
+                                          (T)c.theta0, (T)sgn, stash, blockDim.x);
+  } else {
+    acc = run_rk4_stages<T, METRIC, TRAJ>(s, c.n_steps, rel, traj, ld_out, (T)c.theta0, (T)sgn);
+  }
+  const double E = finish_error<METRIC>(acc, c.n_steps + 1);
+  if (status) *status = isinf(E) ? 2 : 0;
+  return E;
+}
+
+// ---------------------------------------------------------------------------
+// Block-level (E, idx, n_finite) reduction; returns true in thread 0.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void block_argmin(double& e, int64_t& i, int64_t& nf) {
+  __shared__ double se[32];
+  __shared__ int64_t si[32];
+  __shared__ int64_t sn[32];
+  warp_argmin(e, i);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) nf += __shfl_xor_sync(0xffffffffu, nf, off);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  if (lane == 0) { se[wid] = e; si[wid] = i; sn[wid] = nf; }
+  __syncthreads();
+  if (wid == 0) {
+    e = lane < nw ? se[lane] : __longlong_as_double(0x7ff0000000000000LL);
+    i = lane < nw ? si[lane] : INT64_MAX;
+    nf = lane < nw ? sn[lane] : 0;
+    warp_argmin(e, i);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) nf += __shfl_xor_sync(0xffffffffu, nf, off);
+  }
+}
+
+// Write the final result struct (one thread) and the winner's OPC.
+__device__ void write_result(const SpaceDev& sp, uint32_t saccade, double e, int64_t i,
+                             int64_t nf, int64_t neval, opmm_fit_result* out) {
+  const bool ok = i != INT64_MAX && e < __longlong_as_double(0x7ff0000000000000LL);
+  out->best_index = ok ? i : -1;
+  out->opt_err = ok ? e : __longlong_as_double(0x7ff0000000000000LL);
+  out->cpu_check = __longlong_as_double(0x7ff8000000000000LL);
+  out->n_finite = nf;
+  out->n_evaluated = neval;
+  double p[NP];
+  if (ok) generate_opc(sp, saccade, i, p);
+#pragma unroll
+  for (int d = 0; d < NP; ++d) out->opc[d] = ok ? p[d] : __longlong_as_double(0x7ff8000000000000LL);
+}
+
+// ---------------------------------------------------------------------------
+// The fused fit kernel.  gridDim.y = saccades of this launch (1 for a single
+// fit); blockIdx.x strides over the candidate range [begin, end) of each.
+// ---------------------------------------------------------------------------
+template <typename T, int INTEG, int METRIC>
+__global__ void __launch_bounds__(256, 2) fit_kernel(FitArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int32_t ns = a.ctl.n_steps + 1;
+  T* rel = reinterpret_cast<T*>(smem_raw);
+  T* stash = reinterpret_cast<T*>(smem_raw + rel_bytes<T>(ns)) + threadIdx.x;
+  const int64_t sac = (int64_t)blockIdx.y + a.sac_begin;
+  const double amp = a.sac_ctl ? a.sac_ctl[2 * sac] : a.amplitude;
+  const double pwd = a.sac_ctl ? a.sac_ctl[2 * sac + 1] : a.pw_default;
+  double sgn, Aprime;
+  stage_trace<T>(a.rec + sac * (int64_t)ns, ns, amp, rel, sgn, Aprime);
+  __syncthreads();
+
+  double best_e = __longlong_as_double(0x7ff0000000000000LL);
+  int64_t best_i = INT64_MAX;
+  int64_t nf = 0;
+  // Warp-uniform trip count: every lane of a warp runs every iteration (lanes
+  // past `end` evaluate the last candidate again and discard it), so the
+  // per-step warp vote in run_propagator always sees a full warp.
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = a.begin + (int64_t)blockIdx.x * blockDim.x; base < a.end; base += stride) {
+    const int64_t i0 = base + threadIdx.x;
+    const bool valid = i0 < a.end;
+    const int64_t i = valid ? i0 : a.end - 1;
+    double p[NP];
+    generate_opc(a.space, (uint32_t)sac, i, p);
+    const double E = evaluate<T, INTEG, METRIC, false>(p, a.ctl, Aprime, pwd, rel, nullptr, 0,
+                                                       sgn, nullptr, stash);
+    if (valid) {
+      if (a.err_out) a.err_out[sac * a.err_ld + i] = E;
+      nf += E < __longlong_as_double(0x7ff0000000000000LL) ? 1 : 0;
+      if (better(E, i, best_e, best_i)) { best_e = E; best_i = i; }
+    }
+  }
+  block_argmin(best_e, best_i, nf);
+
+  // per-block partial, then the last block of this saccade reduces them
+  __shared__ bool is_last;
+  Partial* parts = a.partials + sac * (int64_t)gridDim.x;
+  if (threadIdx.x == 0) {
+    parts[blockIdx.x] = Partial{best_e, best_i, nf, 0};
+    __threadfence();
+    const unsigned int t = atomicAdd(a.counters + sac, 1u);
+    is_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  double e = __longlong_as_double(0x7ff0000000000000LL);
+  int64_t i = INT64_MAX, n = 0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+    // L2-coherent loads: the partials were written by other blocks
+    const double qe = __ldcg(&parts[b].e);
+    const int64_t qi = __ldcg(reinterpret_cast<const long long*>(&parts[b].i));
+    const int64_t qn = __ldcg(reinterpret_cast<const long long*>(&parts[b].nf));
+    if (better(qe, qi, e, i)) { e = qe; i = qi; }
+    n += qn;
+  }
+  __syncthreads();
+  block_argmin(e, i, n);
+  if (threadIdx.x == 0) {
+    a.counters[sac] = 0;  // re-arm for the next launch (graph-replay safe)
+    const int64_t neval = a.end - a.begin;
+    if (a.rank_out) a.rank_out[sac] = Partial{e, i, n, neval};
+    if (a.final_out)
+      write_result(a.space, (uint32_t)sac, e, i, n, neval, a.final_out + (sac - a.out_base));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// world > 1: merge the gathered per-rank partials (lexicographic) and write
+// the final result with the regenerated winner OPC.  One warp.
+// ---------------------------------------------------------------------------
+__global__ void merge_kernel(const Partial* gathered, int world, SpaceDev sp, uint32_t saccade,
+                             opmm_fit_result* out) {
+  double e = __longlong_as_double(0x7ff0000000000000LL);
+  int64_t i = INT64_MAX, n = 0, ne = 0;
+  for (int r = threadIdx.x; r < world; r += 32) {
+    const Partial q = gathered[r];
+    if (better(q.e, q.i, e, i)) { e = q.e; i = q.i; }
+    n += q.nf;
+    ne += q.neval;
+  }
+  warp_argmin(e, i);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    n += __shfl_xor_sync(0xffffffffu, n, off);
+    ne += __shfl_xor_sync(0xffffffffu, ne, off);
+  }
+  if (threadIdx.x == 0) write_result(sp, saccade, e, i, n, ne, out);
+}
+
+// ---------------------------------------------------------------------------
+// Explicit OPC batch kernels.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void load_opc(const double* __restrict__ opc, int64_t ld, int64_t i,
+                                         double p[NP]) {
+#pragma unroll
+  for (int d = 0; d < NP; ++d) p[d] = __ldg(opc + (int64_t)d * ld + i);
+}
+
+template <typename T, int INTEG, int METRIC>
+__global__ void __launch_bounds__(256, 2) simscore_kernel(ExplicitArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int32_t ns = a.ctl.n_steps + 1;
+  T* rel = reinterpret_cast<T*>(smem_raw);
+  T* stash = reinterpret_cast<T*>(smem_raw + rel_bytes<T>(ns)) + threadIdx.x;
+  double sgn, Aprime;
+  stage_trace<T>(a.rec, ns, a.amplitude, rel, sgn, Aprime);
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < a.n; base += stride) {
+    const int64_t i0 = base + threadIdx.x;
+    const bool valid = i0 < a.n;
+    const int64_t i = valid ? i0 : a.n - 1;
+    double p[NP];
+    load_opc(a.opc, a.ld, i, p);
+    const double E = evaluate<T, INTEG, METRIC, false>(p, a.ctl, Aprime, a.pw_default, rel, nullptr,
+                                                       0, sgn, nullptr, stash);
+    if (valid) a.err[i] = E;
+  }
+}
+
+template <typename T, int INTEG>
+__global__ void __launch_bounds__(256, 2) simulate_kernel(ExplicitArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* stash = reinterpret_cast<T*>(smem_raw) + threadIdx.x;
+  const double A = a.amplitude;  // explicit simulate: A given (NaN rejected on host)
+  const double sgn = A < 0.0 ? -1.0 : 1.0, Aprime = fabs(A);
+  T* traj = reinterpret_cast<T*>(a.traj);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < a.n; base += stride) {
+    const int64_t i0 = base + threadIdx.x;
+    const bool valid = i0 < a.n;
+    // invalid lanes re-integrate candidate n-1 and store the identical values
+    // into its column (benign duplicate writes)
+    const int64_t i = valid ? i0 : a.n - 1;
+    double p[NP];
+    load_opc(a.opc, a.ld, i, p);
+    uint8_t st = 0;
+    // no trace: the accumulator sums |Delta-theta| so that a non-finite (or
+    // >= 1e20) trajectory is flagged as diverged (status 2)
+    (void)evaluate<T, INTEG, 0, true>(p, a.ctl, Aprime, a.pw_default, nullptr, traj + i,
+                                      a.ld_out, sgn, &st, stash);
+    if (valid && a.status) a.status[i] = st;
+  }
+}
+
+// Stored-trajectory score: one candidate per thread, samples streamed
+// time-major (coalesced across the warp), 8 loads in flight per thread.
+template <typename T, int METRIC>
+__global__ void __launch_bounds__(256) score_kernel(ScoreArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* rec = reinterpret_cast<double*>(smem_raw);
+  for (int k = threadIdx.x; k < a.n_samples; k += blockDim.x) rec[k] = a.rec[k];
+  __syncthreads();
+  const T* traj = reinterpret_cast<const T*>(a.traj);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += stride) {
+    double acc = 0.0;
+    int32_t k = 0;
+    for (; k + 8 <= a.n_samples; k += 8) {
+      T v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldcs(traj + (int64_t)(k + u) * a.ld + i);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) accumulate<METRIC>(acc, (double)v[u] - rec[k + u]);
+    }
+    for (; k < a.n_samples; ++k) accumulate<METRIC>(acc, (double)__ldcs(traj + (int64_t)k * a.ld + i) - rec[k]);
+    a.err[i] = finish_error<METRIC>(acc, a.n_samples);
+  }
+}
+
+__global__ void generate_kernel(SpaceDev sp, uint32_t saccade, int64_t begin, int64_t count,
+                                double* out, int64_t ld) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < count; j += stride) {
+    double p[NP];
+    generate_opc(sp, saccade, begin + j, p);
+#pragma unroll
+    for (int d = 0; d < NP; ++d) out[(int64_t)d * ld + j] = p[d];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Launchers.
+// ---------------------------------------------------------------------------
+template <typename T, int INTEG, int METRIC>
+static const void* fit_fn() { return reinterpret_cast<const void*>(&fit_kernel<T, INTEG, METRIC>); }
+
+const void* fit_kernel_ptr(int precision, int integrator, int metric) {
+  if (precision == 0) {
+    if (integrator == 0) return metric == 0 ? fit_fn<double, 0, 0>() : fit_fn<double, 0, 1>();
+    return metric == 0 ? fit_fn<double, 1, 0>() : fit_fn<double, 1, 1>();
+  }
+  if (integrator == 0) return metric == 0 ? fit_fn<float, 0, 0>() : fit_fn<float, 0, 1>();
+  return metric == 0 ? fit_fn<float, 1, 0>() : fit_fn<float, 1, 1>();
+}
+
+cudaError_t launch_fit(const FitArgs& a, int precision, int integrator, int metric, dim3 grid,
+                       int block, size_t smem, cudaStream_t st) {
+  void* args[] = {const_cast<FitArgs*>(&a)};
+  return cudaLaunchKernel(fit_kernel_ptr(precision, integrator, metric), grid, dim3(block), args,
+                          smem, st);
+}
+
+cudaError_t launch_merge(const Partial* gathered, int world, const SpaceDev& sp, uint32_t saccade,
+                         opmm_fit_result* out, cudaStream_t st) {
+  merge_kernel<<<1, 32, 0, st>>>(gathered, world, sp, saccade, out);
+  return cudaGetLastError();
+}
+
+template <typename T, int INTEG, int METRIC>
+static const void* ss_fn() { return reinterpret_cast<const void*>(&simscore_kernel<T, INTEG, METRIC>); }
+
+const void* simscore_kernel_ptr(int precision, int integrator, int metric) {
+  if (precision == 0) {
+    if (integrator == 0) return metric == 0 ? ss_fn<double, 0, 0>() : ss_fn<double, 0, 1>();
+    return metric == 0 ? ss_fn<double, 1, 0>() : ss_fn<double, 1, 1>();
+  }
+  if (integrator == 0) return metric == 0 ? ss_fn<float, 0, 0>() : ss_fn<float, 0, 1>();
+  return metric == 0 ? ss_fn<float, 1, 0>() : ss_fn<float, 1, 1>();
+}
+
+const void* simulate_kernel_ptr(int precision, int integrator) {
+  if (precision == 0)
+    return integrator == 0 ? reinterpret_cast<const void*>(&simulate_kernel<double, 0>)
+                           : reinterpret_cast<const void*>(&simulate_kernel<double, 1>);
+  return integrator == 0 ? reinterpret_cast<const void*>(&simulate_kernel<float, 0>)
+                         : reinterpret_cast<const void*>(&simulate_kernel<float, 1>);
+}
+
+const void* score_kernel_ptr(int precision, int metric) {
+  if (precision == 0)
+    return metric == 0 ? reinterpret_cast<const void*>(&score_kernel<double, 0>)
+                       : reinterpret_cast<const void*>(&score_kernel<double, 1>);
+  return metric == 0 ? reinterpret_cast<const void*>(&score_kernel<float, 0>)
+                     : reinterpret_cast<const void*>(&score_kernel<float, 1>);
+}
+
+cudaError_t launch_explicit(const void* fn, const ExplicitArgs& a, dim3 grid, int block, size_t smem,
+                            cudaStream_t st) {
+  void* args[] = {const_cast<ExplicitArgs*>(&a)};
+  return cudaLaunchKernel(fn, grid, dim3(block), args, smem, st);
+}
+
+cudaError_t launch_score(const ScoreArgs& a, int precision, int metric, dim3 grid, int block,
+                         size_t smem, cudaStream_t st) {
+  void* args[] = {const_cast<ScoreArgs*>(&a)};
+  return cudaLaunchKernel(score_kernel_ptr(precision, metric), grid, dim3(block), args, smem, st);
+}
+
+cudaError_t launch_generate(const SpaceDev& sp, uint32_t saccade, int64_t begin, int64_t count,
+                            double* out, int64_t ld, int grid, cudaStream_t st) {
+  generate_kernel<<<grid, 256, 0, st>>>(sp, saccade, begin, count, out, ld);
+  return cudaGetLastError();
+}
+
+}  // namespace opmm

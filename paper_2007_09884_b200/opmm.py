@@ -1,0 +1,340 @@
+"""Thin ctypes binding of libopmm (include/opmm.h): argument marshalling only.
+
+Every function here has the C name of the entry point it wraps and does
+nothing but convert Python / numpy / torch arguments into the C ABI and turn a
+non-OK status into an exception.  All computation happens in the CUDA kernels
+of libopmm.so; if the library is missing this module raises at import time
+(there is no CPU fallback).  Device buffers are torch CUDA tensors (PyTorch is
+used for device memory and streams only).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libopmm.so")
+
+NPARAM = 18
+MAX_STEPS = 16384
+NCCL_ID_BYTES = 128
+
+OK, ERR_INVALID_ARG, ERR_CUDA, ERR_NCCL, ERR_OOM, ERR_NO_FINITE, ERR_UNSUPPORTED = range(7)
+FP64, FP32 = 0, 1
+METRIC_L1, METRIC_RMS = 0, 1
+INTEG_PROPAGATOR, INTEG_RK4_STAGES = 0, 1
+_STATUS = {0: "OK", 1: "INVALID_ARG", 2: "CUDA", 3: "NCCL", 4: "OOM", 5: "NO_FINITE", 6: "UNSUPPORTED"}
+
+
+class OpmmError(RuntimeError):
+    def __init__(self, status: int, where: str, msg: str):
+        super().__init__(f"{where}: OPMM_ERR_{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Control(C.Structure):
+    _fields_ = [("dt_ms", C.c_double), ("n_steps", C.c_int32), ("pad_", C.c_int32),
+                ("amplitude_deg", C.c_double), ("theta0_deg", C.c_double),
+                ("pw_default_ms", C.c_double)]
+
+
+class SearchSpace(C.Structure):
+    _fields_ = [("mode", C.c_int32), ("pad_", C.c_int32), ("seed", C.c_uint64),
+                ("lo", C.c_double * NPARAM), ("hi", C.c_double * NPARAM),
+                ("log_scale", C.c_uint8 * NPARAM), ("pad2_", C.c_uint8 * 6),
+                ("levels", C.c_int32 * NPARAM)]
+
+
+class FitOptions(C.Structure):
+    _fields_ = [("precision", C.c_int32), ("metric", C.c_int32), ("integrator", C.c_int32),
+                ("block_size", C.c_int32), ("grid_blocks", C.c_int32), ("cpu_check", C.c_int32),
+                ("err_out", C.c_void_p)]
+
+
+class FitResult(C.Structure):
+    _fields_ = [("best_index", C.c_int64), ("opt_err", C.c_double), ("cpu_check", C.c_double),
+                ("opc", C.c_double * NPARAM), ("n_finite", C.c_int64), ("n_evaluated", C.c_int64)]
+
+    def as_dict(self) -> dict:
+        return {"best_index": self.best_index, "opt_err": self.opt_err, "cpu_check": self.cpu_check,
+                "opc": np.array(self.opc[:]), "n_finite": self.n_finite,
+                "n_evaluated": self.n_evaluated}
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2007_09884_b200.build` "
+                          "(libopmm has no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    vp, i64, i32, dp = C.c_void_p, C.c_int64, C.c_int32, C.POINTER(C.c_double)
+    st = C.c_int
+    sig = {
+        "opmm_version": ([], C.c_char_p),
+        "opmm_last_error": ([], C.c_char_p),
+        "opmm_create": ([C.POINTER(vp), C.c_int], st),
+        "opmm_nccl_unique_id": ([C.c_char_p], st),
+        "opmm_create_nccl": ([C.POINTER(vp), C.c_int, C.c_char_p, C.c_int, C.c_int], st),
+        "opmm_destroy": ([vp], st),
+        "opmm_get_stream": ([vp, C.POINTER(vp)], st),
+        "opmm_last_kernel_ms": ([vp, C.POINTER(C.c_float)], st),
+        "opmm_shard_range": ([i64, C.c_int, C.c_int, C.POINTER(i64), C.POINTER(i64)], st),
+        "opmm_merge_argmin": ([dp, C.POINTER(i64), C.c_int, dp, C.POINTER(i64)], st),
+        "opmm_validate": ([C.POINTER(Control), C.POINTER(SearchSpace), i64], st),
+        "opmm_generate": ([vp, C.POINTER(SearchSpace), C.c_uint32, i64, i64, vp, i64, vp], st),
+        "opmm_simulate": ([vp, vp, i64, i64, C.POINTER(Control), i32, i32, vp, i64, vp, vp], st),
+        "opmm_score": ([vp, vp, i64, i64, i32, vp, i32, i32, vp, vp], st),
+        "opmm_simulate_score": ([vp, vp, i64, i64, C.POINTER(Control), vp, i32, i32, i32, vp, vp], st),
+        "opmm_fit": ([vp, vp, C.POINTER(Control), C.POINTER(SearchSpace), i64,
+                      C.POINTER(FitOptions), C.POINTER(FitResult)], st),
+        "opmm_fit_async": ([vp, vp, C.POINTER(Control), C.POINTER(SearchSpace), i64,
+                            C.POINTER(FitOptions), vp], st),
+        "opmm_fit_batch": ([vp, vp, i64, C.POINTER(Control), C.POINTER(SearchSpace), i64,
+                            C.POINTER(FitOptions), C.POINTER(FitResult)], st),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    return L
+
+
+_lib = _load()
+EXPORTED = ("opmm_version", "opmm_last_error", "opmm_create", "opmm_nccl_unique_id",
+            "opmm_create_nccl", "opmm_destroy", "opmm_get_stream", "opmm_last_kernel_ms",
+            "opmm_shard_range", "opmm_merge_argmin", "opmm_validate", "opmm_generate",
+            "opmm_simulate", "opmm_score", "opmm_simulate_score", "opmm_fit", "opmm_fit_async",
+            "opmm_fit_batch")
+
+
+def lib():
+    return _lib
+
+
+def _check(status: int, where: str):
+    if status != OK:
+        raise OpmmError(status, where, _lib.opmm_last_error().decode())
+
+
+# ---------------------------------------------------------------------- structs
+def control(c=None, **kw) -> Control:
+    """Control from any object with dt_ms/n_steps/amplitude_deg/theta0_deg/pw_default_ms."""
+    src = {k: getattr(c, k) for k in ("dt_ms", "n_steps", "amplitude_deg", "theta0_deg", "pw_default_ms")} \
+        if c is not None else {}
+    src.update(kw)
+    return Control(float(src.get("dt_ms", 1.0)), int(src.get("n_steps", 100)), 0,
+                   float(src.get("amplitude_deg", math.nan)), float(src.get("theta0_deg", 0.0)),
+                   float(src.get("pw_default_ms", 40.0)))
+
+
+def search_space(s) -> SearchSpace:
+    """SearchSpace from any object with mode/seed/lo/hi/log_scale/levels."""
+    out = SearchSpace()
+    out.mode = int(s.mode)
+    out.seed = int(s.seed)
+    for d in range(NPARAM):
+        out.lo[d] = float(s.lo[d])
+        out.hi[d] = float(s.hi[d])
+        out.log_scale[d] = int(s.log_scale[d])
+        out.levels[d] = int(s.levels[d])
+    return out
+
+
+def fit_options(precision=FP64, metric=METRIC_L1, integrator=INTEG_PROPAGATOR, block_size=0,
+                grid_blocks=0, cpu_check=1, err_out=None) -> FitOptions:
+    return FitOptions(precision, metric, integrator, block_size, grid_blocks, cpu_check,
+                      _ptr(err_out) if err_out is not None else None)
+
+
+def _ptr(x):
+    """Raw pointer of a torch tensor / numpy array / int / None."""
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    if hasattr(x, "data_ptr"):
+        return x.data_ptr()
+    if isinstance(x, np.ndarray):
+        return x.ctypes.data
+    raise TypeError(f"cannot take a pointer of {type(x)}")
+
+
+def _stream(stream):
+    if stream is None:
+        return None
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+# ---------------------------------------------------------------------- handle
+class Handle:
+    """Owns an opmm_handle (one GPU, or one rank of an NCCL group)."""
+
+    def __init__(self, device: int = 0, nccl_id: bytes | None = None, rank: int = 0, world: int = 1):
+        h = C.c_void_p()
+        if nccl_id is None:
+            _check(_lib.opmm_create(C.byref(h), device), "opmm_create")
+        else:
+            _check(_lib.opmm_create_nccl(C.byref(h), device, bytes(nccl_id), rank, world),
+                   "opmm_create_nccl")
+        self.ptr = h
+        self.device, self.rank, self.world = device, rank, world
+
+    def close(self):
+        if self.ptr:
+            _lib.opmm_destroy(self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    @property
+    def stream(self) -> int:
+        s = C.c_void_p()
+        _check(_lib.opmm_get_stream(self.ptr, C.byref(s)), "opmm_get_stream")
+        return s.value or 0
+
+
+def opmm_version() -> str:
+    return _lib.opmm_version().decode()
+
+
+def opmm_create(device: int = 0) -> Handle:
+    return Handle(device)
+
+
+def opmm_nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(NCCL_ID_BYTES)
+    _check(_lib.opmm_nccl_unique_id(buf), "opmm_nccl_unique_id")
+    return buf.raw
+
+
+def opmm_create_nccl(device: int, nccl_id: bytes, rank: int, world: int) -> Handle:
+    return Handle(device, nccl_id, rank, world)
+
+
+def opmm_destroy(h: Handle):
+    h.close()
+
+
+def opmm_last_kernel_ms(h: Handle) -> float:
+    ms = C.c_float()
+    _check(_lib.opmm_last_kernel_ms(h.ptr, C.byref(ms)), "opmm_last_kernel_ms")
+    return ms.value
+
+
+# ---------------------------------------------------------------------- host-only
+def opmm_shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
+    b, e = C.c_int64(), C.c_int64()
+    _check(_lib.opmm_shard_range(n, rank, world, C.byref(b), C.byref(e)), "opmm_shard_range")
+    return b.value, e.value
+
+
+def opmm_merge_argmin(errs, idxs) -> tuple[float, int]:
+    e = np.ascontiguousarray(errs, dtype=np.float64)
+    i = np.ascontiguousarray(idxs, dtype=np.int64)
+    be, bi = C.c_double(), C.c_int64()
+    st = _lib.opmm_merge_argmin(e.ctypes.data_as(C.POINTER(C.c_double)),
+                                i.ctypes.data_as(C.POINTER(C.c_int64)), len(e), C.byref(be), C.byref(bi))
+    if st not in (OK, ERR_NO_FINITE):
+        _check(st, "opmm_merge_argmin")
+    return be.value, bi.value
+
+
+def opmm_validate(ctl=None, space=None, n_candidates: int = 0) -> None:
+    c = control(ctl) if ctl is not None and not isinstance(ctl, Control) else ctl
+    s = search_space(space) if space is not None and not isinstance(space, SearchSpace) else space
+    _check(_lib.opmm_validate(C.byref(c) if c is not None else None,
+                              C.byref(s) if s is not None else None, n_candidates), "opmm_validate")
+
+
+# ---------------------------------------------------------------------- hot path
+def _ctl(c):
+    return c if isinstance(c, Control) else control(c)
+
+
+def _space(s):
+    return s if isinstance(s, SearchSpace) else search_space(s)
+
+
+def opmm_generate(h: Handle, space, begin: int, count: int, opc_out, ld: int | None = None,
+                  saccade: int = 0, stream=None):
+    _check(_lib.opmm_generate(h.ptr, C.byref(_space(space)), saccade, begin, count, _ptr(opc_out),
+                              count if ld is None else ld, _stream(stream)), "opmm_generate")
+
+
+def opmm_simulate(h: Handle, opc, n: int, ctl, traj, precision=FP64, integrator=INTEG_PROPAGATOR,
+                  ld: int | None = None, ld_out: int | None = None, status=None, stream=None):
+    c = _ctl(ctl)
+    _check(_lib.opmm_simulate(h.ptr, _ptr(opc), n, n if ld is None else ld, C.byref(c), precision,
+                              integrator, _ptr(traj), n if ld_out is None else ld_out, _ptr(status),
+                              _stream(stream)), "opmm_simulate")
+
+
+def opmm_score(h: Handle, traj, n: int, n_samples: int, recorded, err, precision=FP64,
+               metric=METRIC_L1, ld: int | None = None, stream=None):
+    _check(_lib.opmm_score(h.ptr, _ptr(traj), n, n if ld is None else ld, n_samples, _ptr(recorded),
+                           precision, metric, _ptr(err), _stream(stream)), "opmm_score")
+
+
+def opmm_simulate_score(h: Handle, opc, n: int, ctl, recorded, err, precision=FP64, metric=METRIC_L1,
+                        integrator=INTEG_PROPAGATOR, ld: int | None = None, stream=None):
+    c = _ctl(ctl)
+    _check(_lib.opmm_simulate_score(h.ptr, _ptr(opc), n, n if ld is None else ld, C.byref(c),
+                                    _ptr(recorded), precision, metric, integrator, _ptr(err),
+                                    _stream(stream)), "opmm_simulate_score")
+
+
+def opmm_fit(h: Handle, recorded, ctl, space, n_candidates: int, options: FitOptions | None = None,
+             raise_no_finite: bool = False) -> dict:
+    """Synchronous fit; `recorded` is a host numpy array or a device tensor."""
+    rec = recorded
+    if isinstance(recorded, np.ndarray):
+        rec = np.ascontiguousarray(recorded, dtype=np.float64)
+    out = FitResult()
+    opts = options if options is not None else fit_options()
+    st = _lib.opmm_fit(h.ptr, _ptr(rec), C.byref(_ctl(ctl)), C.byref(_space(space)), n_candidates,
+                       C.byref(opts), C.byref(out))
+    if st != OK and not (st == ERR_NO_FINITE and not raise_no_finite):
+        _check(st, "opmm_fit")
+    return out.as_dict()
+
+
+def opmm_fit_async(h: Handle, recorded_dev, ctl, space, n_candidates: int, out_dev,
+                   options: FitOptions | None = None):
+    """Enqueue a fit on the handle's stream; out_dev: device buffer of
+    ctypes.sizeof(FitResult) bytes (e.g. a uint8 CUDA tensor)."""
+    opts = options if options is not None else fit_options(cpu_check=0)
+    _check(_lib.opmm_fit_async(h.ptr, _ptr(recorded_dev), C.byref(_ctl(ctl)), C.byref(_space(space)),
+                               n_candidates, C.byref(opts), _ptr(out_dev)), "opmm_fit_async")
+
+
+def decode_result(raw: bytes) -> dict:
+    return FitResult.from_buffer_copy(raw).as_dict()
+
+
+def opmm_fit_batch(h: Handle, recorded, ctls, space, n_per: int,
+                   options: FitOptions | None = None) -> list[dict]:
+    S = len(ctls)
+    arr = (Control * S)(*[_ctl(c) for c in ctls])
+    out = (FitResult * S)()
+    rec = recorded
+    if isinstance(recorded, np.ndarray):
+        rec = np.ascontiguousarray(recorded, dtype=np.float64)
+    opts = options if options is not None else fit_options()
+    _check(_lib.opmm_fit_batch(h.ptr, _ptr(rec), S, arr, C.byref(_space(space)), n_per,
+                               C.byref(opts), out), "opmm_fit_batch")
+    lo, hi = opmm_shard_range(S, h.rank, h.world)
+    return [out[s].as_dict() if lo <= s < hi else None for s in range(S)]

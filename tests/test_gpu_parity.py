@@ -1,0 +1,485 @@
+"""GPU parity: libopmm (CUDA, through the C ABI) vs the CPU oracle (-m gpu).
+
+Same seeded inputs on both sides (workloads/), compared element by element.
+Tolerances (north_star):
+  FP64 trajectories  |d_gpu - d_orc| <= 1e-9 * max(max_k |d_orc|, 1 deg)
+  FP64 errors        |E_gpu - E_orc| <= 1e-9 * max(E_orc, sum |rel|); +inf / penalty exact
+  FP64 argmin        identical index
+  FP32 trajectories  <= 1e-3 deg per sample on RK4-stable candidates
+  FP32 errors        <= 1e-4 * max(E_orc, sum |rel|); finite/+inf classification exact
+  FP32 best fit      E64(winner32) <= (1 + 1e-4) E64(winner64) + 1e-4 sum |rel|
+  generator          linear dims bit-exact, log dims <= 2 ulp (device exp vs glibc exp)
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+I = W.IDX
+ULP = 2.0 ** -52
+
+
+@pytest.fixture(scope="module")
+def opmm():
+    if not torch.cuda.is_available():
+        pytest.fail("no CUDA device: the -m gpu suite must run on a B200")
+    from paper_2007_09884_b200 import build
+    build.build()
+    from paper_2007_09884_b200 import opmm as m
+    return m
+
+
+@pytest.fixture(scope="module")
+def h(opmm):
+    with opmm.opmm_create(0) as handle:
+        yield handle
+
+
+def dev(a, dtype=torch.float64):
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=dtype, device="cuda")
+
+
+def trace(ctl, noisy=True):
+    rec = oracle.positions(W.truth_opc(), ctl)
+    return rec + W.noise(ctl.n_steps + 1) if noisy else rec
+
+
+def soa(cands):
+    """[n, 18] -> device SoA [18, n]."""
+    return dev(np.ascontiguousarray(np.asarray(cands).T))
+
+
+def candidate_set(n_paper=3000, seed=1):
+    sp = W.paper_space()
+    c = [W.truth_opc()]
+    c += list(oracle.generate_batch(sp, 0, n_paper))
+    rng = np.random.default_rng(seed)
+    d = W.truth_opc()
+    for _ in range(300):
+        p = d * np.exp(rng.uniform(np.log(0.5), np.log(2.0), size=18))
+        p[I["PW"]] = rng.uniform(1, 100)
+        c.append(p)
+    return np.array(c)
+
+
+def rk4_stable(p, ctl):
+    """Oracle-side decision: spectral radius of the RK4 map < 1
+    in both control phases (non-physical candidates are not stable)."""
+    if oracle.physical_penalty(p) != 0.0:
+        return False
+    z = np.zeros(6)
+    rad = 0.0
+    for tau_ag, tau_ant in ((p[10], p[11]), (p[12], p[13])):
+        b = oracle.rhs(p, z, 0, 0, tau_ag, tau_ant)
+        A = np.stack([oracle.rhs(p, np.eye(6)[j], 0, 0, tau_ag, tau_ant) - b for j in range(6)], 1)
+        ev = np.linalg.eigvals(A) * ctl.dt_ms * 1e-3
+        P = 1 + ev + ev ** 2 / 2 + ev ** 3 / 6 + ev ** 4 / 24
+        rad = max(rad, np.abs(P).max())
+    return rad < 1.0
+
+
+def oracle_dtheta(cands, ctl):
+    out = []
+    for p in cands:
+        try:
+            out.append(oracle.simulate(p, ctl.dt_ms, ctl.n_steps, abs(ctl.amplitude_deg), ctl.pw_default_ms))
+        except ValueError:
+            out.append(None)
+    return out
+
+
+# --------------------------------------------------------------------------- generator
+def test_generate_random_matches_oracle(opmm, h):
+    sp = W.paper_space()
+    n = 8192
+    out = torch.zeros((18, n), dtype=torch.float64, device="cuda")
+    begin = 10**9 + 12345
+    opmm.opmm_generate(h, sp, begin, n, out, saccade=7, stream=torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    g = out.cpu().numpy().T
+    o = np.array([oracle.generate(sp, begin + i, saccade=7) for i in range(n)])
+    lin = sp.log_scale == 0
+    assert np.array_equal(g[:, lin], o[:, lin])
+    rel = np.abs(g[:, ~lin] - o[:, ~lin]) / np.abs(o[:, ~lin])
+    assert rel.max() <= 2 * ULP, rel.max()
+
+
+def test_generate_philox_words_match_oracle_kat_pinned(opmm, h):
+    """With lo = 0, hi = 2^32 (linear) the generator returns w + 0.5 exactly,
+    exposing the raw device Philox words; they must equal the oracle's
+    (KAT-pinned) Philox -- including the all-zero KAT vector."""
+    sp = W.SearchSpace(0, 0, np.zeros(18), np.full(18, 2.0 ** 32), np.zeros(18, np.uint8),
+                       np.ones(18, np.int32))
+    n = 1024
+    out = torch.zeros((18, n), dtype=torch.float64, device="cuda")
+    opmm.opmm_generate(h, sp, 0, n, out, stream=torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    words = out.cpu().numpy() - 0.5
+    assert np.all(words == np.floor(words))
+    assert [int(x) for x in words[:4, 0]] == [0x6627e8d5, 0xe169c58d, 0xbc57ac4c, 0x9b00dbd8]
+    for i in (1, 77, 1023):
+        for j in range(4):
+            ref = oracle.philox4x32_10([i, 0, 0, j], [0, 0])
+            got = [int(words[4 * j + r, i]) for r in range(4) if 4 * j + r < 18]
+            assert got == ref.tolist()[:len(got)]
+
+
+def test_generate_grid_matches_oracle(opmm, h):
+    sp = W.g4_space(per_dim=12)
+    n = sp.n_grid()
+    out = torch.zeros((18, n), dtype=torch.float64, device="cuda")
+    opmm.opmm_generate(h, sp, 0, n, out, stream=torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    g = out.cpu().numpy().T
+    o = np.array([oracle.generate(sp, i) for i in range(n)])
+    assert np.array_equal(g[:, 17], o[:, 17])
+    assert np.max(np.abs(g - o) / np.abs(o)) <= 2 * ULP
+
+
+# --------------------------------------------------------------------------- simulate
+@pytest.mark.parametrize("integrator", [0, 1])
+@pytest.mark.parametrize("amp,theta0", [(10.0, 0.0), (-7.0, 3.0)])
+def test_simulate_fp64_trajectories(opmm, h, integrator, amp, theta0):
+    ctl = W.Control(amplitude_deg=amp, theta0_deg=theta0)
+    cands = candidate_set()
+    bad = W.truth_opc()
+    bad[I["K_SE_AG"]] = -1.0
+    nanpw = W.truth_opc()
+    nanpw[I["PW"]] = math.nan
+    cands = np.vstack([cands, bad, nanpw])
+    n = len(cands)
+    traj = torch.full((ctl.n_steps + 1, n), -1.0, dtype=torch.float64, device="cuda")
+    status = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    opmm.opmm_simulate(h, soa(cands), n, ctl, traj, precision=opmm.FP64, integrator=integrator,
+                       status=status, stream=torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    T = traj.cpu().numpy()
+    S = status.cpu().numpy()
+    s = -1.0 if amp < 0 else 1.0
+    refs = oracle_dtheta(cands, ctl)
+    worst = 0.0
+    n_unstable_checked = 0
+    for i, ref in enumerate(refs):
+        if ref is None:
+            assert S[i] == 1 and np.all(np.isnan(T[:, i]))
+            continue
+        finite = np.all(np.isfinite(ref)) and np.abs(ref).sum() < 1e20
+        if not finite:
+            assert S[i] == 2, i
+            continue
+        assert S[i] == 0, i
+        d = (T[:, i] - theta0) * s
+        err = np.max(np.abs(d - ref)) / max(np.max(np.abs(ref)), 1.0)
+        worst = max(worst, err)
+        assert err <= 1e-9, (i, err)
+        n_unstable_checked += 0 if np.max(np.abs(ref)) < 1e3 else 1
+    assert T[0, 0] == theta0
+    print(f"max rel trajectory diff {worst:.3e}; large-amplitude finite candidates {n_unstable_checked}")
+
+
+def test_simulate_fp32_trajectories_rk4_stable(opmm, h):
+    ctl = W.Control()
+    cands = candidate_set(n_paper=1500)
+    n = len(cands)
+    traj = torch.zeros((ctl.n_steps + 1, n), dtype=torch.float32, device="cuda")
+    opmm.opmm_simulate(h, soa(cands), n, ctl, traj, precision=opmm.FP32,
+                       stream=torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    T = traj.cpu().numpy().astype(np.float64)
+    refs = oracle_dtheta(cands, ctl)
+    checked = 0
+    worst = 0.0
+    for i, ref in enumerate(refs):
+        if ref is None or not rk4_stable(cands[i], ctl):
+            continue
+        checked += 1
+        e = np.max(np.abs(T[:, i] - ref))
+        worst = max(worst, e)
+        assert e <= 1e-3, (i, e)
+    assert checked > 500
+    print(f"fp32: {checked} RK4-stable candidates, max |diff| {worst:.3e} deg")
+
+
+# --------------------------------------------------------------------------- scores
+@pytest.mark.parametrize("precision", [0, 1])
+@pytest.mark.parametrize("metric", [0, 1])
+def test_simulate_score_parity(opmm, h, precision, metric):
+    ctl = W.Control()
+    rec = trace(ctl)
+    rel, s, Ap = oracle.relativize(rec, ctl.amplitude_deg)
+    scale = np.abs(rel).sum() if metric == 0 else np.sqrt(np.mean(rel ** 2))
+    cands = candidate_set(n_paper=2000)
+    bad = W.truth_opc()
+    bad[I["J"]] = 0.0
+    cands = np.vstack([cands, bad])
+    n = len(cands)
+    err = torch.zeros(n, dtype=torch.float64, device="cuda")
+    opmm.opmm_simulate_score(h, soa(cands), n, ctl, dev(rec), err, precision=precision, metric=metric,
+                             stream=torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    E = err.cpu().numpy()
+    O = np.array([oracle.objective(p, rec, ctl, metric) for p in cands])
+    assert np.array_equal(np.isinf(E), np.isinf(O)), np.flatnonzero(np.isinf(E) != np.isinf(O))
+    assert E[-1] == O[-1] == 1e10
+    f = np.isfinite(O)
+    tol = (1e-9 if precision == 0 else 1e-4) * np.maximum(O[f], scale)
+    if precision == 1:
+        # FP32 scope: RK4-stable candidates (SURVEY 8(c) parity tolerances)
+        stable = np.array([rk4_stable(p, ctl) for p in cands[f]])
+        bad_i = np.flatnonzero((np.abs(E[f] - O[f]) > tol) & stable)
+    else:
+        bad_i = np.flatnonzero(np.abs(E[f] - O[f]) > tol)
+    assert bad_i.size == 0, (bad_i[:5], E[f][bad_i[:5]], O[f][bad_i[:5]])
+
+
+@pytest.mark.parametrize("precision", [0, 1])
+def test_score_stored_trajectories(opmm, h, precision):
+    """opmm_score (HBM-bound) on oracle trajectories vs the oracle score."""
+    ctl = W.Control()
+    rec = trace(ctl)
+    cands = candidate_set(n_paper=500)
+    trajs = []
+    for p in cands:
+        trajs.append(oracle.positions(p, ctl))
+    T = np.array(trajs).T.copy()                         # time-major [n_samples, n]
+    n = T.shape[1]
+    dt = torch.float64 if precision == 0 else torch.float32
+    err = torch.zeros(n, dtype=torch.float64, device="cuda")
+    Td = dev(T, dt)
+    opmm.opmm_score(h, Td, n, ctl.n_steps + 1, dev(rec), err, precision=precision,
+                    stream=torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    E = err.cpu().numpy()
+    Tq = Td.cpu().numpy().astype(np.float64)
+    for i in range(n):
+        d = Tq[:, i] - rec
+        with np.errstate(all="ignore"):
+            ref = np.abs(d).sum()
+        if not (ref < 1e20):
+            assert np.isinf(E[i])
+        else:
+            assert abs(E[i] - ref) <= 1e-12 * max(ref, 1.0), i
+
+
+# --------------------------------------------------------------------------- fit
+def _fit(opmm, h, rec, ctl, sp, n, **kw):
+    err = torch.full((n,), -1.0, dtype=torch.float64, device="cuda") if n else None
+    opts = opmm.fit_options(err_out=err, **kw)
+    r = opmm.opmm_fit(h, rec, ctl, sp, n, opts)
+    torch.cuda.synchronize()
+    return r, (err.cpu().numpy() if n else None)
+
+
+@pytest.mark.parametrize("integrator", [0, 1])
+@pytest.mark.parametrize("metric", [0, 1])
+def test_fit_config1_all_candidates(opmm, h, integrator, metric):
+    """Config 1: 10 deg saccade, 1 kHz, 100 ms, 1,000 random candidates."""
+    ctl = W.Control()
+    rec = trace(ctl)
+    sp = W.paper_space()
+    n = 1000
+    r, E = _fit(opmm, h, rec, ctl, sp, n, integrator=integrator, metric=metric)
+    o = oracle.fit(rec, ctl, sp, 0, n, metric=metric, want_err=True)
+    O = o["err"]
+    rel, _, _ = oracle.relativize(rec, ctl.amplitude_deg)
+    scale = np.abs(rel).sum() if metric == 0 else np.sqrt(np.mean(rel ** 2))
+    assert np.array_equal(np.isinf(E), np.isinf(O))
+    f = np.isfinite(O)
+    assert np.all(np.abs(E[f] - O[f]) <= 1e-9 * np.maximum(O[f], scale))
+    assert r["best_index"] == o["best_index"]
+    assert r["n_finite"] == o["n_finite"] and r["n_evaluated"] == n
+    assert abs(r["opt_err"] - o["best_err"]) <= 1e-9 * max(o["best_err"], scale)
+    assert abs(r["cpu_check"] - r["opt_err"]) <= 1e-9 * max(r["opt_err"], 1.0)
+    assert np.max(np.abs(r["opc"] - o["opc"]) / np.abs(o["opc"])) <= 2 * ULP
+
+
+def test_fit_config2_full_1e6_fp64(opmm, h):
+    """Config 2 at full size in the launch configuration bench.py times
+    (default options): all 10^6 errors and the argmin vs the oracle."""
+    ctl = W.Control()
+    rec = trace(ctl)
+    sp = W.paper_space()
+    n = 10**6
+    r, E = _fit(opmm, h, rec, ctl, sp, n)
+    o = oracle.fit(rec, ctl, sp, 0, n, nthreads=oracle.max_threads(), want_err=True)
+    O = o["err"]
+    rel, _, _ = oracle.relativize(rec, ctl.amplitude_deg)
+    scale = np.abs(rel).sum()
+    assert np.array_equal(np.isinf(E), np.isinf(O))
+    f = np.isfinite(O)
+    d = np.abs(E[f] - O[f]) / np.maximum(O[f], scale)
+    print(f"1e6: n_finite {o['n_finite']}, max rel err diff {d.max():.3e}")
+    assert d.max() <= 1e-9
+    assert r["best_index"] == o["best_index"] and r["n_finite"] == o["n_finite"]
+
+
+def test_fit_fp32_best_fit_certified_by_fp64_oracle(opmm, h):
+    ctl = W.Control()
+    rec = trace(ctl)
+    sp = W.paper_space()
+    n = 200000
+    r32, E32 = _fit(opmm, h, rec, ctl, sp, n, precision=opmm.FP32)
+    r64, E64 = _fit(opmm, h, rec, ctl, sp, n, precision=opmm.FP64)
+    rel, _, _ = oracle.relativize(rec, ctl.amplitude_deg)
+    scale = np.abs(rel).sum()
+    e32 = oracle.objective(oracle.generate(sp, r32["best_index"]), rec, ctl)
+    e64 = oracle.objective(oracle.generate(sp, r64["best_index"]), rec, ctl)
+    assert e32 <= (1 + 1e-4) * e64 + 1e-4 * scale
+    assert abs(r32["opt_err"] - e32) <= 1e-4 * max(e32, scale)
+    # classification finite / +inf identical to fp64 everywhere
+    assert np.array_equal(np.isinf(E32), np.isinf(E64))
+
+
+def test_fit_planted_grid_g4_full_1e8(opmm, h):
+    """G4: 100^4 grid over {K_SE_AG, B_AG, N_SAC_AG, PW}; TRUTH is a node.
+    Oracle-exact argmin at 10^8 (the oracle checks the winner and samples)."""
+    ctl = W.Control()
+    rec = trace(ctl, noisy=False)
+    sp = W.g4_space(100)
+    n = sp.n_grid()
+    assert n == 10**8
+    err = torch.empty(n, dtype=torch.float64, device="cuda")
+    r = opmm.opmm_fit(h, rec, ctl, sp, n, opmm.fit_options(err_out=err))
+    planted = W.g4_planted_index()
+    assert r["best_index"] == planted
+    rel, _, _ = oracle.relativize(rec, ctl.amplitude_deg)
+    assert r["opt_err"] <= 1e-9 * np.abs(rel).sum()
+    o = oracle.fit(rec, ctl, sp, planted, planted + 1, want_err=True)
+    assert abs(r["opt_err"] - o["err"][0]) <= 1e-12 * np.abs(rel).sum()
+    rng = np.random.default_rng(4)
+    idx = np.sort(rng.choice(n, 2000, replace=False))
+    E = err[torch.as_tensor(idx, device="cuda")].cpu().numpy()
+    O = np.array([oracle.objective(oracle.generate(sp, int(i)), rec, ctl) for i in idx])
+    assert np.array_equal(np.isinf(E), np.isinf(O))
+    f = np.isfinite(O)
+    assert np.all(np.abs(E[f] - O[f]) <= 1e-9 * np.maximum(O[f], np.abs(rel).sum()))
+    assert np.all(O[f] > r["opt_err"])
+
+
+def test_fit_exact_ties_lowest_index(opmm, h):
+    ctl = W.Control()
+    rec = trace(ctl)
+    d = W.truth_opc()
+    sp = W.grid_space({"N_SAC_AG": (d[15] * 0.99, d[15] * 1.01, 3, False),
+                       "PW": (39.21, 40.0, 3, False)})
+    o = oracle.fit(rec, ctl, sp, 0, 9)
+    for bs, gb in ((64, 0), (256, 0), (64, 1)):
+        r, E = _fit(opmm, h, rec, ctl, sp, 9, block_size=bs, grid_blocks=gb)
+        assert r["best_index"] == o["best_index"]
+        e = E.reshape(3, 3)
+        assert np.all(e[0] == e[1]) and np.all(e[1] == e[2])
+
+
+def test_fit_launch_config_invariance(opmm, h):
+    ctl = W.Control()
+    rec = trace(ctl)
+    sp = W.paper_space()
+    n = 50001
+    ref, Eref = _fit(opmm, h, rec, ctl, sp, n)
+    for bs, gb in ((128, 0), (512, 0), (256, 1), (256, 7), (1024, 3)):
+        r, E = _fit(opmm, h, rec, ctl, sp, n, block_size=bs, grid_blocks=gb)
+        assert (r["best_index"], r["opt_err"], r["n_finite"]) == \
+               (ref["best_index"], ref["opt_err"], ref["n_finite"])
+        assert np.array_equal(E, Eref, equal_nan=True)
+
+
+def test_fit_async_matches_sync(opmm, h):
+    import ctypes
+    ctl = W.Control()
+    rec = trace(ctl)
+    sp = W.paper_space()
+    n = 20000
+    r = opmm.opmm_fit(h, rec, ctl, sp, n)
+    out = torch.zeros(ctypes.sizeof(opmm.FitResult), dtype=torch.uint8, device="cuda")
+    recd = dev(rec)
+    torch.cuda.synchronize()
+    opmm.opmm_fit_async(h, recd, ctl, sp, n, out)
+    torch.cuda.ExternalStream(h.stream).synchronize()
+    ra = opmm.decode_result(bytes(out.cpu().numpy()))
+    assert ra["best_index"] == r["best_index"] and ra["opt_err"] == r["opt_err"]
+    assert math.isnan(ra["cpu_check"])
+
+
+# --------------------------------------------------------------------------- edge cases
+def test_edge_empty_single_ragged(opmm, h):
+    ctl = W.Control()
+    rec = trace(ctl)
+    sp = W.paper_space()
+    r = opmm.opmm_fit(h, rec, ctl, sp, 0)
+    assert r["best_index"] == -1 and r["n_finite"] == 0
+    with pytest.raises(opmm.OpmmError) as ei:
+        opmm.opmm_fit(h, rec, ctl, sp, 0, raise_no_finite=True)
+    assert ei.value.status == opmm.ERR_NO_FINITE
+    for n in (1, 31, 33, 257):
+        r, E = _fit(opmm, h, rec, ctl, sp, n)
+        o = oracle.fit(rec, ctl, sp, 0, n, want_err=True)
+        assert r["best_index"] == o["best_index"] and r["n_evaluated"] == n
+        assert np.array_equal(np.isinf(E), np.isinf(o["err"]))
+
+
+def test_edge_all_diverged(opmm, h):
+    ctl = W.Control()
+    rec = trace(ctl, noisy=False)
+    d = W.truth_opc()
+    d[I["J"]] = 1e-9
+    d[I["B_AG"]] = 1e-6
+    d[I["B_ANT"]] = 1e-6
+    sp = W.grid_space({"PW": (10.0, 20.0, 3, False)}, base=d)
+    r, E = _fit(opmm, h, rec, ctl, sp, 3)
+    assert r["best_index"] == -1 and r["n_finite"] == 0 and np.all(np.isinf(E))
+
+
+@pytest.mark.parametrize("n_steps", [1, 2, 37, 4000])
+def test_edge_trace_lengths(opmm, h, n_steps):
+    ctl = W.Control(n_steps=n_steps, dt_ms=1.0 if n_steps < 1000 else 0.05)
+    rec = oracle.positions(W.truth_opc(), ctl) + W.noise(n_steps + 1)
+    sp = W.paper_space(n_steps=n_steps, dt_ms=ctl.dt_ms)
+    n = 300
+    r, E = _fit(opmm, h, rec, ctl, sp, n)
+    o = oracle.fit(rec, ctl, sp, 0, n, want_err=True)
+    O = o["err"]
+    rel, _, _ = oracle.relativize(rec, ctl.amplitude_deg)
+    assert np.array_equal(np.isinf(E), np.isinf(O))
+    f = np.isfinite(O)
+    assert np.all(np.abs(E[f] - O[f]) <= 1e-9 * np.maximum(O[f], max(np.abs(rel).sum(), 1e-300)))
+    assert r["best_index"] == o["best_index"]
+
+
+def test_edge_amplitude_from_trace_and_negative(opmm, h):
+    sp = W.paper_space()
+    for amp, th0, given in ((-12.0, 4.0, True), (10.0, 0.0, False)):
+        ctl = W.Control(amplitude_deg=amp, theta0_deg=th0)
+        rec = trace(ctl)
+        use = ctl if given else W.Control(amplitude_deg=math.nan)
+        r, E = _fit(opmm, h, rec, use, sp, 2000)
+        o = oracle.fit(rec, use, sp, 0, 2000, want_err=True)
+        assert r["best_index"] == o["best_index"]
+        f = np.isfinite(o["err"])
+        assert np.all(np.abs(E[f] - o["err"][f]) <= 1e-9 * np.maximum(o["err"][f], 100))
+
+
+# --------------------------------------------------------------------------- population
+def test_fit_batch_population(opmm, h):
+    S = 48
+    amp, pw, truths = W.population(S)
+    n_steps = 150
+    ctls, recs = [], []
+    for s in range(S):
+        c = W.Control(n_steps=n_steps, amplitude_deg=amp[s], pw_default_ms=pw[s])
+        ctls.append(c)
+        recs.append(oracle.positions(truths[s], c) + W.noise(n_steps + 1, seed=1000 + s))
+    recs = np.array(recs)
+    sp = W.paper_space(n_steps=n_steps)
+    n_per = 3000
+    res = opmm.opmm_fit_batch(h, recs, ctls, sp, n_per)
+    for s in (0, 1, 17, 47):
+        o = oracle.fit(recs[s], ctls[s], sp, 0, n_per, saccade=s)
+        assert res[s]["best_index"] == o["best_index"], s
+        assert abs(res[s]["opt_err"] - o["best_err"]) <= 1e-9 * max(o["best_err"], 1.0)
+        assert abs(res[s]["cpu_check"] - res[s]["opt_err"]) <= 1e-9 * res[s]["opt_err"]

@@ -512,3 +512,13 @@ def test_survey_scratch_regression_values():
     assert d5[50] == pytest.approx(7.779986704990, rel=1e-11)
     assert d5[100] == pytest.approx(5.954196963665, rel=1e-11)
     assert oracle.step_levels(p, 5.0).tolist() == pytest.approx([23.25, 4.75], rel=1e-14)
+
+
+def test_trace_fixture_is_oracle_output():
+    """tests/golden/trace_truth_A10_dt1_n100.txt (bench/smoke input) was written
+    by scripts/make_traces.py from this oracle; it must still match."""
+    import os
+    from conftest import GOLDEN
+    rec = np.loadtxt(os.path.join(GOLDEN, "trace_truth_A10_dt1_n100.txt"), comments="#")
+    ref = oracle.positions(W.truth_opc(), W.Control())
+    assert np.array_equal(rec, ref)

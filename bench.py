@@ -50,6 +50,22 @@ FP64_PEAK_TFLOPS = SMS * FP64_LANES * 2 * SM_MAX_MHZ * 1e6 / 1e12   # 37.23
 FP64_MEASURED_TFLOPS = 33.90   # profiles/r01_fma_peak.txt (DFMA microbenchmark)
 
 
+def ncu_traffic_bytes():
+    """dram__bytes_read.sum + dram__bytes_write.sum of the fit kernel from the
+    committed `ncu --set full` capture summary (profiles/), per launch."""
+    units = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    path = os.path.join(ROOT, "profiles", "r01_fit_kernel_fp64_ncu_full.txt")
+    try:
+        tot = 0.0
+        for line in open(path):
+            parts = line.split()
+            if parts and parts[0] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                tot += float(parts[1]) * units[parts[2]]
+        return tot or None
+    except OSError:
+        return None
+
+
 def workload_name(per_gpu, world):
     return (f"configs[1]: single synthetic 10 deg horizontal saccade, 1 kHz, 100 ms, "
             f"{per_gpu:.0e} random OPC candidates per GPU over S_paper (x{world} GPUs)")
@@ -277,7 +293,8 @@ def run_gpu(args):
                 "h2d_bytes_per_step": rec_np.nbytes, "d2h_bytes_per_step": ctypes.sizeof(opmm.FitResult),
                 "ms_per_step": e2e_ms, "api": "opmm_fit (sync, host buffers, CPU_check on)"},
         "roofline": {"bound": "alu", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
-                     "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+                     "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
+                     "traffic": ncu_traffic_bytes(), "traffic_unit": "bytes/launch (ncu, spills)",
                      "kernel": "fit_kernel<double, propagator, L1>", "kernel_ms": kms64,
                      "flop_per_candidate": per_cand_flop,
                      "peak_basis": "148 SM x 64 FP64 lanes x 2 x 1965 MHz (DESIGN.md)",

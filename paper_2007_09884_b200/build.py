@@ -26,10 +26,18 @@ NVCC = os.environ.get("NVCC", "nvcc")
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", f"-I{INCLUDE}", f"-I{CSRC}"]
 
 
-def _deps_mtime() -> float:
-    paths = [os.path.join(CSRC, s) for s in SOURCES + HEADERS] + [os.path.join(INCLUDE, "opmm.h"),
-                                                                  os.path.abspath(__file__)]
-    return max(os.path.getmtime(p) for p in paths)
+STAMP = LIB + ".stamp"
+
+
+def _digest() -> str:
+    """Content hash of everything the library is built from (mtimes are not
+    reliable across the gpurun snapshot)."""
+    import hashlib
+    h = hashlib.sha256(" ".join([NVCC, *ARCH, *FLAGS]).encode())
+    for p in [os.path.join(CSRC, s) for s in SOURCES + HEADERS] + [os.path.join(INCLUDE, "opmm.h")]:
+        with open(p, "rb") as f:
+            h.update(f.read())
+    return h.hexdigest()
 
 
 def _compile(src: str) -> tuple[str, str]:
@@ -41,8 +49,31 @@ def _compile(src: str) -> tuple[str, str]:
     return obj, p.stderr
 
 
+def build_variant(name: str, defines: list[str]) -> str:
+    """Build an experimental variant build/variants/libopmm_<name>.so with extra
+    -D flags (performance experiments only; the product is `build()`)."""
+    out_dir = os.path.join(BUILD, "variants", name)
+    os.makedirs(out_dir, exist_ok=True)
+    lib = os.path.join(BUILD, "variants", f"libopmm_{name}.so")
+
+    def comp(src):
+        obj = os.path.join(out_dir, src + ".o")
+        cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, src), "-o", obj]
+        p = subprocess.run(cmd, capture_output=True, text=True)
+        if p.returncode != 0:
+            raise RuntimeError(f"nvcc failed for {src} ({name}):\n{p.stderr}")
+        return obj
+    with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        objs = list(ex.map(comp, SOURCES))
+    p = subprocess.run([NVCC, *ARCH, "-shared", "-o", lib, *objs, "-ldl"], capture_output=True, text=True)
+    if p.returncode != 0:
+        raise RuntimeError(f"link failed ({name}):\n{p.stderr}")
+    return lib
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= _deps_mtime():
+    digest = _digest()
+    if not force and os.path.exists(LIB) and os.path.exists(STAMP) and open(STAMP).read() == digest:
         return LIB
     os.makedirs(BUILD, exist_ok=True)
     with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
@@ -57,6 +88,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if p.returncode != 0:
         raise RuntimeError(f"link failed:\n{p.stdout}\n{p.stderr}")
     os.replace(tmp, LIB)
+    with open(STAMP, "w") as f:
+        f.write(digest)
     if verbose:
         print(f"built {LIB}")
     return LIB

@@ -118,6 +118,7 @@ struct opmm_handle {
   size_t result_host_cap = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   bool timed = false;
+  double2* exp_tab = nullptr;   // exp(j/64) double-double table (generator)
 };
 
 namespace {
@@ -213,15 +214,34 @@ opmm::SpaceDev make_space(const opmm_search_space* s) {
       d.kind[k] = 0;
       d.span[k] = 0.0;
     } else if (s->log_scale[k]) {
-      d.kind[k] = 2;
       const double L = std::log(s->hi[k] / s->lo[k]);
       d.span[k] = s->mode == 1 ? L / (double)(s->levels[k] - 1) : L;
+      // largest exp argument the generator can form for this dimension
+      const double xmax = s->mode == 1 ? d.span[k] * (double)(s->levels[k] - 1) : L;
+      d.kind[k] = xmax < 0.999 * opmm::EXP_TAB_MAX ? 2 : 3;
     } else {
       d.kind[k] = 1;
       const double w = s->hi[k] - s->lo[k];
       d.span[k] = s->mode == 1 ? w / (double)(s->levels[k] - 1) : w;
     }
   }
+  // Every candidate lies in [lo, hi] per dimension, so the physical check
+  // (SPEC D8 / reading Q13) holds for all of them iff it holds at the lower
+  // corner: strict dimensions lo > 0, the others lo >= 0, and G > 0, which
+  // (with K_SE > 0) needs N_C + K_LT > 0 for at least one muscle.
+  static const int strict[] = {OPMM_P_KSE_AG, OPMM_P_KSE_ANT, OPMM_P_B_AG, OPMM_P_B_ANT,
+                               OPMM_P_J, OPMM_P_TAU_AC_AG, OPMM_P_TAU_AC_ANT, OPMM_P_TAU_DE_AG,
+                               OPMM_P_TAU_DE_ANT, OPMM_P_PW};
+  bool phys = true;
+  for (int k = 0; k < OPMM_NPARAM; ++k) {
+    bool is_strict = false;
+    for (int t : strict) is_strict |= (t == k);
+    if (is_strict ? !(s->lo[k] > 0.0) : !(s->lo[k] >= 0.0)) phys = false;
+  }
+  if (!(s->lo[OPMM_P_NC_AG] + s->lo[OPMM_P_KLT_AG] > 0.0 ||
+        s->lo[OPMM_P_NC_ANT] + s->lo[OPMM_P_KLT_ANT] > 0.0))
+    phys = false;
+  d.all_physical = phys ? 1 : 0;
   return d;
 }
 
@@ -251,6 +271,10 @@ size_t sim_smem(int precision, int32_t n_samples, int block, bool with_rel) {
   return (with_rel ? opmm::rel_bytes<float>(n_samples) : 0) + opmm::stash_bytes<float>(block);
 }
 
+size_t fit_smem(int precision, int32_t n_samples, int block) {
+  return sim_smem(precision, n_samples, block, true) + opmm::exp_tab_bytes();
+}
+
 opmm_status grid_for(opmm_handle* h, const void* fn, int block, size_t smem, int64_t work,
                      int requested, int* grid) {
   int per_sm = 0;
@@ -266,8 +290,9 @@ opmm_status grid_for(opmm_handle* h, const void* fn, int block, size_t smem, int
 }
 
 opmm_status check_block(int block) {
-  if (block < 64 || block > 1024 || block % 32 != 0)
-    return fail(OPMM_ERR_INVALID_ARG, "block_size must be a multiple of 32 in [64, 1024]");
+  // the simulate kernels are compiled with __launch_bounds__(512, 1): <= 128 regs
+  if (block < 64 || block > 512 || block % 32 != 0)
+    return fail(OPMM_ERR_INVALID_ARG, "block_size must be a multiple of 32 in [64, 512]");
   return OPMM_OK;
 }
 
@@ -302,7 +327,7 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
   int64_t b = 0, e = n_candidates;
   if (shard) opmm_shard_range(n_candidates, h->rank, h->world, &b, &e);
   const int32_t ns = ctl->n_steps + 1;
-  const size_t smem = sim_smem(precision, ns, block, true);
+  const size_t smem = fit_smem(precision, ns, block);
   if (smem > kMaxDynSmem) return fail(OPMM_ERR_INVALID_ARG, "trace too long for shared memory");
   const void* fn = opmm::fit_kernel_ptr(precision, integ, metric);
   int grid = 1;
@@ -318,6 +343,7 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
   opmm::FitArgs a;
   std::memset(&a, 0, sizeof(a));
   a.rec = rec_dev;
+  a.exp_tab = h->exp_tab;
   a.ctl = make_ctl(ctl);
   a.space = make_space(space);
   a.amplitude = ctl->amplitude_deg;
@@ -349,7 +375,7 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
                                      ncclUint8, h->comm, h->stream);
       if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather");
       CK(opmm::launch_merge(h->gathered, h->world, a.space, (uint32_t)(s_begin + s), out_dev + s,
-                            h->stream));
+                            h->exp_tab, h->stream));
     }
   }
   return OPMM_OK;
@@ -419,6 +445,21 @@ opmm_status opmm_create(opmm_handle** out, int device) {
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDynSmem);
       }
   cudaGetLastError();
+  {
+    // exp(j/64), j < EXP_TAB_N, as double-double from 80-bit expl
+    double2 tab[opmm::EXP_TAB_N];
+    for (int j = 0; j < opmm::EXP_TAB_N; ++j) {
+      const long double v = expl((long double)j / 64.0L);
+      tab[j].x = (double)v;
+      tab[j].y = (double)(v - (long double)tab[j].x);
+    }
+    if (cudaMalloc(&h->exp_tab, sizeof(tab)) != cudaSuccess ||
+        cudaMemcpy(h->exp_tab, tab, sizeof(tab), cudaMemcpyHostToDevice) != cudaSuccess) {
+      st = fail(OPMM_ERR_CUDA, "exp table allocation failed");
+      cleanup();
+      return st;
+    }
+  }
   if ((st = ensure(h->counters, h->counters_cap, 64, true)) != OPMM_OK ||
       (st = ensure(h->result, h->result_cap, 1)) != OPMM_OK ||
       (st = ensure_host(h->result_host, h->result_host_cap, 1)) != OPMM_OK) {
@@ -478,6 +519,7 @@ opmm_status opmm_destroy(opmm_handle* h) {
   cudaFree(h->rank_part);
   cudaFree(h->gathered);
   cudaFree(h->result);
+  cudaFree(h->exp_tab);
   if (h->result_host) cudaFreeHost(h->result_host);
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
@@ -548,7 +590,8 @@ opmm_status opmm_generate(opmm_handle* h, const opmm_search_space* space, uint32
   cudaStream_t st = stream ? (cudaStream_t)stream : h->stream;
   int grid = (int)((count + 255) / 256);
   if (grid > h->num_sms * 8) grid = h->num_sms * 8;
-  CK(opmm::launch_generate(make_space(space), saccade, begin, count, opc_out, ld, grid, st));
+  CK(opmm::launch_generate(make_space(space), saccade, begin, count, opc_out, ld, h->exp_tab, grid,
+                           st));
   return OPMM_OK;
 }
 

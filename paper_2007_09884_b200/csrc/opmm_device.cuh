@@ -26,11 +26,18 @@ constexpr double NANT_FLOOR = 0.01; // SPEC D4
 enum { KSE_AG = 0, KSE_ANT, KLT_AG, KLT_ANT, B_AG, B_ANT, B_P, NC_AG, NC_ANT, J_,
        TAU_AC_AG, TAU_AC_ANT, TAU_DE_AG, TAU_DE_ANT, NC_FIX, NSAC_AG, NSAC_ANT, PW_ };
 
+// exp() table for the log-uniform map: EXP_TAB[j] = exp(j/64) as a
+// double-double (hi, lo), j = 0..EXP_TAB_N-1, covering arguments in [0, 8).
+constexpr int EXP_TAB_N = 512;
+constexpr double EXP_TAB_MAX = 8.0;
+
 // Search space, preprocessed on the host (kernel parameter -> constant bank).
 struct SpaceDev {
   int32_t mode;          // 0 random (Philox), 1 grid
   uint32_t key0, key1;   // Philox key = seed
-  uint8_t kind[NP];      // 0 fixed (lo), 1 linear, 2 log
+  int32_t all_physical;  // host proved every candidate of the space physical
+  // 0 fixed (lo), 1 linear, 2 log with table exp (argument < 8), 3 log with libm exp
+  uint8_t kind[NP];
   double lo[NP];
   // random: linear hi-lo, log log(hi/lo); grid: linear (hi-lo)/(L-1), log log(hi/lo)/(L-1)
   double span[NP];
@@ -60,35 +67,98 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
   return c;
 }
 
+// exp(x) for x in [0, 8): x = j/64 + r with r in [0, 1/64) exact (Sterbenz),
+// exp(x) = E_j (1 + q), q = expm1(r) by a degree-7 Taylor polynomial
+// (truncation < 4e-19 relative), E_j a double-double table entry; one final
+// rounding, so the result is within ~0.51 ulp of exp(x) -- the same value a
+// correctly-rounded libm returns in all but near-tie cases, for ~14
+// instructions instead of ~50 for the general-range exp().
+__device__ __forceinline__ double exp_tab(double x, const double2* __restrict__ tab) {
+  const int j = __double2int_rz(x * 64.0);
+  const double r = fma((double)j, -0.015625, x);
+  double q = 1.0 / 5040.0;
+  q = fma(q, r, 1.0 / 720.0);
+  q = fma(q, r, 1.0 / 120.0);
+  q = fma(q, r, 1.0 / 24.0);
+  q = fma(q, r, 1.0 / 6.0);
+  q = fma(q, r, 0.5);
+  q = fma(q, r, 1.0);
+  q = q * r;
+  const double2 e = tab[j];
+  return e.x + fma(e.x, q, e.y);
+}
+
+// exp(x) for 0 <= x < 700 without memory: x = k ln2 + r (Cody-Waite, |r| <=
+// ln2/2), degree-13 Taylor polynomial (truncation < 6e-18 relative), scaled
+// by 2^k through the exponent field; ~1 ulp.
+__device__ __forceinline__ double exp_poly(double x) {
+  const double k = rint(x * 1.4426950408889634);
+  double r = fma(k, -6.93147180369123816490e-01, x);
+  r = fma(k, -1.90821492927058770002e-10, r);
+  double q = 1.0 / 6227020800.0;
+  q = fma(q, r, 1.0 / 479001600.0);
+  q = fma(q, r, 1.0 / 39916800.0);
+  q = fma(q, r, 1.0 / 3628800.0);
+  q = fma(q, r, 1.0 / 362880.0);
+  q = fma(q, r, 1.0 / 40320.0);
+  q = fma(q, r, 1.0 / 5040.0);
+  q = fma(q, r, 1.0 / 720.0);
+  q = fma(q, r, 1.0 / 120.0);
+  q = fma(q, r, 1.0 / 24.0);
+  q = fma(q, r, 1.0 / 6.0);
+  q = fma(q, r, 0.5);
+  q = fma(q, r, 1.0);
+  q = fma(q, r, 1.0);
+  const double two_k = __hiloint2double(((int)k + 1023) << 20, 0);
+  return q * two_k;
+}
+
+#ifndef OPMM_EXP_MODE
+#define OPMM_EXP_MODE 0   // 0: double-double table, 1: polynomial, 2: libm exp
+#endif
+
+// General-range exp for log dimensions whose argument can reach 8 or more
+// (kind 3): out of line, so the 17 inlined maps carry one call, not 17
+// copies of libm's exp.
+static __device__ __noinline__ double exp_libm(double x) { return exp(x); }
+
 // u = (w + 0.5) 2^-32 is exact in fp64; the mapping uses explicitly rounded
-// operations so no FMA contraction changes the candidate bits.
-__device__ __forceinline__ double map_word(const SpaceDev& sp, int d, uint32_t w) {
+// operations so no FMA contraction changes the candidate bits; the exp
+// argument fl(u * log(hi/lo)) is the one the generator definition names.
+__device__ __forceinline__ double map_word(const SpaceDev& sp, int d, uint32_t w,
+                                           const double2* __restrict__ tab) {
   const double u = __dmul_rn(__dadd_rn((double)w, 0.5), 2.3283064365386962890625e-10);
   if (sp.kind[d] == 0) return sp.lo[d];
   if (sp.kind[d] == 1) return __dadd_rn(sp.lo[d], __dmul_rn(u, sp.span[d]));
-  return __dmul_rn(sp.lo[d], exp(__dmul_rn(u, sp.span[d])));
+  const double x = __dmul_rn(u, sp.span[d]);
+#if OPMM_EXP_MODE == 0
+  return __dmul_rn(sp.lo[d], sp.kind[d] == 2 ? exp_tab(x, tab) : exp_libm(x));
+#elif OPMM_EXP_MODE == 1
+  return __dmul_rn(sp.lo[d], sp.kind[d] == 2 ? exp_poly(x) : exp_libm(x));
+#else
+  return __dmul_rn(sp.lo[d], exp(x));
+#endif
 }
 
 // Candidate index -> OPC vector (PAPER.md:202 exhaustive search over OPC values).
-// The dimension loops are deliberately not unrolled: the generator runs once
-// per candidate, and a rolled loop keeps the kernel's instruction footprint
-// small (the per-step loop is what must stay resident in the i-cache).
+// Random mode is fully unrolled: the five Philox blocks and the 17 exp() are
+// independent dependency chains, so the scheduler can overlap them (the
+// generator is ~20% of a candidate's instructions).  Grid mode (int64 div/mod
+// per dimension) stays rolled to keep the kernel's code footprint small.
 __device__ __forceinline__ void generate_opc(const SpaceDev& sp, uint32_t saccade, int64_t idx,
-                                             double p[NP]) {
+                                             double p[NP], const double2* __restrict__ tab) {
   if (sp.mode == 0) {
     const uint2 key = make_uint2(sp.key0, sp.key1);
     const uint32_t ilo = (uint32_t)((uint64_t)idx & 0xffffffffu);
     const uint32_t ihi = (uint32_t)((uint64_t)idx >> 32);
-#pragma unroll 1
+    uint32_t ws[20];
+#pragma unroll
     for (int j = 0; j < 5; ++j) {
       const uint4 w = philox4x32_10(make_uint4(ilo, ihi, saccade, (uint32_t)j), key);
-      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll 1
-      for (int r = 0; r < 4; ++r) {
-        const int d = 4 * j + r;
-        if (d < NP) p[d] = map_word(sp, d, ws[r]);
-      }
+      ws[4 * j] = w.x; ws[4 * j + 1] = w.y; ws[4 * j + 2] = w.z; ws[4 * j + 3] = w.w;
     }
+#pragma unroll
+    for (int d = 0; d < NP; ++d) p[d] = map_word(sp, d, ws[d], tab);
   } else {
     uint64_t rem = (uint64_t)idx;
 #pragma unroll 1
@@ -99,9 +169,18 @@ __device__ __forceinline__ void generate_opc(const SpaceDev& sp, uint32_t saccad
         digit = rem % L;
         rem = rem / L;
       }
-      if (sp.kind[d] == 0 || L <= 1) p[d] = sp.lo[d];
-      else if (sp.kind[d] == 1) p[d] = __dadd_rn(sp.lo[d], __dmul_rn((double)digit, sp.span[d]));
-      else p[d] = __dmul_rn(sp.lo[d], exp(__dmul_rn((double)digit, sp.span[d])));
+      double v;
+      if (sp.kind[d] == 0 || L <= 1) v = sp.lo[d];
+      else if (sp.kind[d] == 1) v = __dadd_rn(sp.lo[d], __dmul_rn((double)digit, sp.span[d]));
+      else {
+        const double x = __dmul_rn((double)digit, sp.span[d]);
+        v = __dmul_rn(sp.lo[d], sp.kind[d] == 2 ? exp_tab(x, tab) : exp_libm(x));
+      }
+      // static-index stores keep p[] in registers after the loop is unrolled
+      // by the caller's use; write through a switch-free select chain
+#pragma unroll
+      for (int e = 0; e < NP; ++e)
+        if (e == d) p[e] = v;
     }
   }
 }
@@ -148,6 +227,20 @@ __device__ __forceinline__ double physical_penalty(const double p[NP]) {
 //   Z3* = h/B_ANT ((N_C_ANT - K_SE_ANT), 0, 0, -(K_LT_ANT + K_SE_ANT))
 //   x_m is driven by f_m / B_m;   f_m' = (n_m - f_m)/tau_m,  zd_m = -dt/tau_m.
 // ----------------------------------------------------------------------------
+// 1/x for positive normal x: MUFU reciprocal seed + two Newton steps
+// (~0.5-1 ulp).  The setup's quotients only need to be accurate, not
+// correctly rounded (parity is to 1e-9 relative), so this replaces the
+// slow-path-guarded IEEE division; the one integer-deciding quotient
+// ceil(PW/dt) keeps the IEEE division.
+__device__ __forceinline__ double rcp64(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
 struct Mech {
   double z01, z10, z11, z12, z13, z20, z22, z30, z33;
   double hb_ag, hb_ant;   // h / B_m
@@ -172,7 +265,7 @@ __device__ __forceinline__ void make_setup(const double p_in[NP], double dt_ms, 
   const double Ncag = p_in[NC_AG], Ncant = p_in[NC_ANT], J = p_in[J_], F = p_in[NC_FIX];
   double PW = p_in[PW_];
   if (isnan(PW)) PW = pw_default;
-  const double hJ = h / J, hBag = h / Bag, hBant = h / Bant;
+  const double hJ = h * rcp64(J), hBag = h * rcp64(Bag), hBant = h * rcp64(Bant);
   s.m.z01 = h;
   s.m.z10 = -(Kag + Kant) * hJ;
   s.m.z11 = -Bp * hJ;
@@ -185,22 +278,22 @@ __device__ __forceinline__ void make_setup(const double p_in[NP], double dt_ms, 
   s.m.hb_ag = hBag;
   s.m.hb_ant = hBant;
   // Post-pulse step levels: static balance at theta* + A' (D4 generalised, Q4).
-  const double g_ag = Kag / (Lag + Kag), g_ant = Kant / (Lant + Kant);
+  const double g_ag = Kag * rcp64(Lag + Kag), g_ant = Kant * rcp64(Lant + Kant);
   const double G = g_ag * (Ncag + Lag) + g_ant * (Ncant + Lant);
-  const double delta = G * Aprime / (g_ag + g_ant);
+  const double delta = G * Aprime * rcp64(g_ag + g_ant);
   double nt_ag = delta, nt_ant = -delta;
   if (F - delta < NANT_FLOOR) {
-    const double theta_star = (g_ag * F - g_ant * F) / G;
-    const double n_ag = (G * (theta_star + Aprime) + NANT_FLOOR * g_ant) / g_ag;
+    const double theta_star = (g_ag * F - g_ant * F) * rcp64(G);
+    const double n_ag = (G * (theta_star + Aprime) + NANT_FLOOR * g_ant) * rcp64(g_ag);
     nt_ag = n_ag - F;
     nt_ant = NANT_FLOOR - F;
   }
-  s.ph[0].zd_ag = -dt_ms / p_in[TAU_AC_AG];
-  s.ph[0].zd_ant = -dt_ms / p_in[TAU_AC_ANT];
+  s.ph[0].zd_ag = -dt_ms * rcp64(p_in[TAU_AC_AG]);
+  s.ph[0].zd_ant = -dt_ms * rcp64(p_in[TAU_AC_ANT]);
   s.ph[0].nt_ag = p_in[NSAC_AG] - F;
   s.ph[0].nt_ant = p_in[NSAC_ANT] - F;
-  s.ph[1].zd_ag = -dt_ms / p_in[TAU_DE_AG];
-  s.ph[1].zd_ant = -dt_ms / p_in[TAU_DE_ANT];
+  s.ph[1].zd_ag = -dt_ms * rcp64(p_in[TAU_DE_AG]);
+  s.ph[1].zd_ant = -dt_ms * rcp64(p_in[TAU_DE_ANT]);
   s.ph[1].nt_ag = nt_ag;
   s.ph[1].nt_ant = nt_ant;
   // Pulse window: onset at step 0, n_pulse = ceil(PW/dt) (IEEE divide), Q6.
@@ -220,6 +313,17 @@ __device__ __forceinline__ void make_setup(const double p_in[NP], double dt_ms, 
 //   f update         f_m+   = (1 + zd_m a_0) f_m + (-zd_m a_0 n~_m)
 // The 4x4 mechanical block P(Z) is phase-independent.
 // ----------------------------------------------------------------------------
+template <typename T> struct Vec2;
+template <> struct Vec2<double> { using type = double2; };
+template <> struct Vec2<float> { using type = float2; };
+template <typename T>
+__device__ __forceinline__ typename Vec2<T>::type make_v2(T a, T b) {
+  typename Vec2<T>::type v;
+  v.x = a;
+  v.y = b;
+  return v;
+}
+
 template <typename T>
 struct PhaseProp {
   T X[4][2];
@@ -355,12 +459,18 @@ __device__ __forceinline__ T run_propagator(const Prop<T>& pr, int32_t n_pulse, 
   // ([16][stash_ld], conflict-free) instead of registers; the 4x4 P stays in
   // registers for the whole loop.
   const PhaseProp<T>& q = pr.ph[1];
-  {
-    const T v[16] = {q.X[0][0], q.X[0][1], q.X[1][0], q.X[1][1], q.X[2][0], q.X[2][1], q.X[3][0],
-                     q.X[3][1], q.c[0], q.c[1], q.c[2], q.c[3], q.pf[0], q.pf[1], q.qf[0], q.qf[1]};
-#pragma unroll
-    for (int j = 0; j < 16; ++j) stash[j * stash_ld] = v[j];
-  }
+  // stash: 8 pairs [8][stash_ld] of vec2 (double2 / float2), one vector
+  // load per pair at the swap
+  using V2 = typename Vec2<T>::type;
+  V2* st2 = reinterpret_cast<V2*>(stash) + threadIdx.x;
+  st2[0 * stash_ld] = make_v2<T>(q.X[0][0], q.X[0][1]);
+  st2[1 * stash_ld] = make_v2<T>(q.X[1][0], q.X[1][1]);
+  st2[2 * stash_ld] = make_v2<T>(q.X[2][0], q.X[2][1]);
+  st2[3 * stash_ld] = make_v2<T>(q.X[3][0], q.X[3][1]);
+  st2[4 * stash_ld] = make_v2<T>(q.c[0], q.c[1]);
+  st2[5 * stash_ld] = make_v2<T>(q.c[2], q.c[3]);
+  st2[6 * stash_ld] = make_v2<T>(q.pf[0], q.pf[1]);
+  st2[7 * stash_ld] = make_v2<T>(q.qf[0], q.qf[1]);
   T X00 = pr.ph[0].X[0][0], X01 = pr.ph[0].X[0][1], X10 = pr.ph[0].X[1][0], X11 = pr.ph[0].X[1][1];
   T X20 = pr.ph[0].X[2][0], X21 = pr.ph[0].X[2][1], X30 = pr.ph[0].X[3][0], X31 = pr.ph[0].X[3][1];
   T c0 = pr.ph[0].c[0], c1 = pr.ph[0].c[1], c2 = pr.ph[0].c[2], c3 = pr.ph[0].c[3];
@@ -370,33 +480,42 @@ __device__ __forceinline__ T run_propagator(const Prop<T>& pr, int32_t n_pulse, 
   const T P20 = pr.P[2][0], P21 = pr.P[2][1], P22 = pr.P[2][2], P23 = pr.P[2][3];
   const T P30 = pr.P[3][0], P31 = pr.P[3][1], P32 = pr.P[3][2], P33 = pr.P[3][3];
   if (TRAJ) traj[0] = theta0;
-  // sample 0 contributes |0 - rel_0| = 0 exactly (rel_0 = 0)
-#pragma unroll 2
-  for (int32_t k = 0; k < n_steps; ++k) {
-    const bool sw = (k == n_pulse);
-    // warp-uniform branch: taken only at the steps where some lane's pulse
-    // ends, so the coefficient reload is never predicated into every step
-    if (__any_sync(0xffffffffu, sw)) {  // callers keep all 32 lanes active
-      if (sw) {
-        X00 = stash[0 * stash_ld]; X01 = stash[1 * stash_ld]; X10 = stash[2 * stash_ld];
-        X11 = stash[3 * stash_ld]; X20 = stash[4 * stash_ld]; X21 = stash[5 * stash_ld];
-        X30 = stash[6 * stash_ld]; X31 = stash[7 * stash_ld];
-        c0 = stash[8 * stash_ld]; c1 = stash[9 * stash_ld]; c2 = stash[10 * stash_ld];
-        c3 = stash[11 * stash_ld];
-        pa = stash[12 * stash_ld]; pn = stash[13 * stash_ld];
-        qa = stash[14 * stash_ld]; qn = stash[15 * stash_ld];
-      }
+  // Load the post-pulse coefficients from the stash (lanes whose pulse ends).
+  auto swap_in = [&]() {
+    V2 v;
+    v = st2[0 * stash_ld]; X00 = v.x; X01 = v.y;
+    v = st2[1 * stash_ld]; X10 = v.x; X11 = v.y;
+    v = st2[2 * stash_ld]; X20 = v.x; X21 = v.y;
+    v = st2[3 * stash_ld]; X30 = v.x; X31 = v.y;
+    v = st2[4 * stash_ld]; c0 = v.x; c1 = v.y;
+    v = st2[5 * stash_ld]; c2 = v.x; c3 = v.y;
+    v = st2[6 * stash_ld]; pa = v.x; pn = v.y;
+    v = st2[7 * stash_ld]; qa = v.x; qn = v.y;
+  };
+  if (n_pulse == 0) swap_in();
+  // Segmented loop: the warp runs uniform segments between consecutive pulse
+  // ends of its lanes (warp-min of the next n_pulse), so the inner loop is
+  // pure FMA work with no per-step phase test; at a segment end only the
+  // lanes whose pulse ends there reload their coefficients.  The callers
+  // keep all 32 lanes active.  Sample 0 contributes |0 - rel_0| = 0 exactly.
+  int32_t k = 0;
+  while (k < n_steps) {
+    const int32_t mine = n_pulse > k ? min(n_pulse, n_steps) : n_steps;
+    const int32_t seg_end = __reduce_min_sync(0xffffffffu, mine);
+#pragma unroll 4
+    for (; k < seg_end; ++k) {
+      const T r = TRAJ ? T(0) : rel[k + 1];
+      const T nth = fma(P00, th, fma(P01, om, fma(P02, xa, fma(P03, xn, fma(X00, fa, fma(X01, fn, c0))))));
+      const T nom = fma(P10, th, fma(P11, om, fma(P12, xa, fma(P13, xn, fma(X10, fa, fma(X11, fn, c1))))));
+      const T nxa = fma(P20, th, fma(P21, om, fma(P22, xa, fma(P23, xn, fma(X20, fa, fma(X21, fn, c2))))));
+      const T nxn = fma(P30, th, fma(P31, om, fma(P32, xa, fma(P33, xn, fma(X30, fa, fma(X31, fn, c3))))));
+      fa = fma(pa, fa, qa);
+      fn = fma(pn, fn, qn);
+      th = nth; om = nom; xa = nxa; xn = nxn;
+      accumulate<METRIC>(acc, TRAJ ? th : th - r);  // TRAJ: no trace, sum |dtheta|
+      if (TRAJ) traj[(int64_t)(k + 1) * ld_out] = fma(sgn, th, theta0);
     }
-    const T r = TRAJ ? T(0) : rel[k + 1];
-    const T nth = fma(P00, th, fma(P01, om, fma(P02, xa, fma(P03, xn, fma(X00, fa, fma(X01, fn, c0))))));
-    const T nom = fma(P10, th, fma(P11, om, fma(P12, xa, fma(P13, xn, fma(X10, fa, fma(X11, fn, c1))))));
-    const T nxa = fma(P20, th, fma(P21, om, fma(P22, xa, fma(P23, xn, fma(X20, fa, fma(X21, fn, c2))))));
-    const T nxn = fma(P30, th, fma(P31, om, fma(P32, xa, fma(P33, xn, fma(X30, fa, fma(X31, fn, c3))))));
-    fa = fma(pa, fa, qa);
-    fn = fma(pn, fn, qn);
-    th = nth; om = nom; xa = nxa; xn = nxn;
-    accumulate<METRIC>(acc, TRAJ ? th : th - r);  // TRAJ: no trace, sum |dtheta|
-    if (TRAJ) traj[(int64_t)(k + 1) * ld_out] = fma(sgn, th, theta0);
+    if (k == n_pulse) swap_in();
   }
   return acc;
 }

@@ -20,6 +20,8 @@ template <typename T>
 __host__ __device__ constexpr size_t stash_bytes(int block) {
   return (size_t)16 * block * sizeof(T);
 }
+// fit kernel: trace, then the exp table (double2[EXP_TAB_N]), then the stash
+__host__ __device__ constexpr size_t exp_tab_bytes() { return (size_t)EXP_TAB_N * 16; }
 
 // Per-block / per-rank (E, index) partial: 32 bytes.
 struct Partial {
@@ -31,6 +33,7 @@ struct Partial {
 
 struct FitArgs {
   const double* rec;        // device [S][n_steps+1]
+  const double2* exp_tab;   // device [EXP_TAB_N] (handle-owned)
   CtlDev ctl;
   SpaceDev space;
   double amplitude;         // single fit: signed A (NaN => rec[n]-rec[0])
@@ -75,12 +78,12 @@ const void* score_kernel_ptr(int precision, int metric);
 cudaError_t launch_fit(const FitArgs& a, int precision, int integrator, int metric, dim3 grid,
                        int block, size_t smem, cudaStream_t st);
 cudaError_t launch_merge(const Partial* gathered, int world, const SpaceDev& sp, uint32_t saccade,
-                         opmm_fit_result* out, cudaStream_t st);
+                         opmm_fit_result* out, const double2* tab, cudaStream_t st);
 cudaError_t launch_explicit(const void* fn, const ExplicitArgs& a, dim3 grid, int block, size_t smem,
                             cudaStream_t st);
 cudaError_t launch_score(const ScoreArgs& a, int precision, int metric, dim3 grid, int block,
                          size_t smem, cudaStream_t st);
 cudaError_t launch_generate(const SpaceDev& sp, uint32_t saccade, int64_t begin, int64_t count,
-                            double* out, int64_t ld, int grid, cudaStream_t st);
+                            double* out, int64_t ld, const double2* tab, int grid, cudaStream_t st);
 
 }  // namespace opmm

@@ -26,8 +26,10 @@ template <typename T, int INTEG, int METRIC, bool TRAJ>
 __device__ __forceinline__ double evaluate(const double p[NP], const CtlDev& c, double Aprime,
                                            double pw_default, const T* rel, T* traj,
                                            int64_t ld_out, double sgn, uint8_t* status,
-                                           T* stash) {
-  const double pen = physical_penalty(p);
+                                           T* stash, bool check_physical = true) {
+  // generated candidates skip the check when the host proved the whole
+  // search space physical (SpaceDev::all_physical)
+  const double pen = check_physical ? physical_penalty(p) : 0.0;
   if (pen != 0.0) {
     if (TRAJ) {
       const T nanv = (T)__longlong_as_double(0x7ff8000000000000LL);
@@ -77,7 +79,8 @@ __device__ __forceinline__ void block_argmin(double& e, int64_t& i, int64_t& nf)
 
 // Write the final result struct (one thread) and the winner's OPC.
 __device__ void write_result(const SpaceDev& sp, uint32_t saccade, double e, int64_t i,
-                             int64_t nf, int64_t neval, opmm_fit_result* out) {
+                             int64_t nf, int64_t neval, opmm_fit_result* out,
+                             const double2* tab) {
   const bool ok = i != INT64_MAX && e < __longlong_as_double(0x7ff0000000000000LL);
   out->best_index = ok ? i : -1;
   out->opt_err = ok ? e : __longlong_as_double(0x7ff0000000000000LL);
@@ -85,7 +88,7 @@ __device__ void write_result(const SpaceDev& sp, uint32_t saccade, double e, int
   out->n_finite = nf;
   out->n_evaluated = neval;
   double p[NP];
-  if (ok) generate_opc(sp, saccade, i, p);
+  if (ok) generate_opc(sp, saccade, i, p, tab);
 #pragma unroll
   for (int d = 0; d < NP; ++d) out->opc[d] = ok ? p[d] : __longlong_as_double(0x7ff8000000000000LL);
 }
@@ -94,18 +97,34 @@ __device__ void write_result(const SpaceDev& sp, uint32_t saccade, double e, int
 // The fused fit kernel.  gridDim.y = saccades of this launch (1 for a single
 // fit); blockIdx.x strides over the candidate range [begin, end) of each.
 // ---------------------------------------------------------------------------
+#ifndef OPMM_FIT_LB_THREADS
+#define OPMM_FIT_LB_THREADS 512
+#endif
+#ifndef OPMM_FIT_LB_BLOCKS
+#define OPMM_FIT_LB_BLOCKS 1
+#endif
+
 template <typename T, int INTEG, int METRIC>
-__global__ void __launch_bounds__(256, 2) fit_kernel(FitArgs a) {
+__global__ void __launch_bounds__(OPMM_FIT_LB_THREADS, OPMM_FIT_LB_BLOCKS) fit_kernel(FitArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int32_t ns = a.ctl.n_steps + 1;
   T* rel = reinterpret_cast<T*>(smem_raw);
-  T* stash = reinterpret_cast<T*>(smem_raw + rel_bytes<T>(ns)) + threadIdx.x;
+  double2* tab = reinterpret_cast<double2*>(smem_raw + rel_bytes<T>(ns));
+  T* stash = reinterpret_cast<T*>(smem_raw + rel_bytes<T>(ns) + exp_tab_bytes());  // [8][block] vec2
+  for (int j = threadIdx.x; j < EXP_TAB_N; j += blockDim.x) tab[j] = a.exp_tab[j];
   const int64_t sac = (int64_t)blockIdx.y + a.sac_begin;
   const double amp = a.sac_ctl ? a.sac_ctl[2 * sac] : a.amplitude;
   const double pwd = a.sac_ctl ? a.sac_ctl[2 * sac + 1] : a.pw_default;
   double sgn, Aprime;
   stage_trace<T>(a.rec + sac * (int64_t)ns, ns, amp, rel, sgn, Aprime);
   __syncthreads();
+#ifdef OPMM_STAGGER
+  if ((threadIdx.x >> 5) & 1) {
+    const long long t0 = clock64();
+    while (clock64() - t0 < OPMM_STAGGER) {
+    }
+  }
+#endif
 
   double best_e = __longlong_as_double(0x7ff0000000000000LL);
   int64_t best_i = INT64_MAX;
@@ -119,9 +138,9 @@ __global__ void __launch_bounds__(256, 2) fit_kernel(FitArgs a) {
     const bool valid = i0 < a.end;
     const int64_t i = valid ? i0 : a.end - 1;
     double p[NP];
-    generate_opc(a.space, (uint32_t)sac, i, p);
+    generate_opc(a.space, (uint32_t)sac, i, p, tab);
     const double E = evaluate<T, INTEG, METRIC, false>(p, a.ctl, Aprime, pwd, rel, nullptr, 0,
-                                                       sgn, nullptr, stash);
+                                                       sgn, nullptr, stash, !a.space.all_physical);
     if (valid) {
       if (a.err_out) a.err_out[sac * a.err_ld + i] = E;
       nf += E < __longlong_as_double(0x7ff0000000000000LL) ? 1 : 0;
@@ -159,7 +178,8 @@ __global__ void __launch_bounds__(256, 2) fit_kernel(FitArgs a) {
     const int64_t neval = a.end - a.begin;
     if (a.rank_out) a.rank_out[sac] = Partial{e, i, n, neval};
     if (a.final_out)
-      write_result(a.space, (uint32_t)sac, e, i, n, neval, a.final_out + (sac - a.out_base));
+      write_result(a.space, (uint32_t)sac, e, i, n, neval, a.final_out + (sac - a.out_base),
+                   a.exp_tab);
   }
 }
 
@@ -168,7 +188,7 @@ __global__ void __launch_bounds__(256, 2) fit_kernel(FitArgs a) {
 // the final result with the regenerated winner OPC.  One warp.
 // ---------------------------------------------------------------------------
 __global__ void merge_kernel(const Partial* gathered, int world, SpaceDev sp, uint32_t saccade,
-                             opmm_fit_result* out) {
+                             opmm_fit_result* out, const double2* tab) {
   double e = __longlong_as_double(0x7ff0000000000000LL);
   int64_t i = INT64_MAX, n = 0, ne = 0;
   for (int r = threadIdx.x; r < world; r += 32) {
@@ -183,7 +203,7 @@ __global__ void merge_kernel(const Partial* gathered, int world, SpaceDev sp, ui
     n += __shfl_xor_sync(0xffffffffu, n, off);
     ne += __shfl_xor_sync(0xffffffffu, ne, off);
   }
-  if (threadIdx.x == 0) write_result(sp, saccade, e, i, n, ne, out);
+  if (threadIdx.x == 0) write_result(sp, saccade, e, i, n, ne, out, tab);
 }
 
 // ---------------------------------------------------------------------------
@@ -196,11 +216,11 @@ __device__ __forceinline__ void load_opc(const double* __restrict__ opc, int64_t
 }
 
 template <typename T, int INTEG, int METRIC>
-__global__ void __launch_bounds__(256, 2) simscore_kernel(ExplicitArgs a) {
+__global__ void __launch_bounds__(512, 1) simscore_kernel(ExplicitArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int32_t ns = a.ctl.n_steps + 1;
   T* rel = reinterpret_cast<T*>(smem_raw);
-  T* stash = reinterpret_cast<T*>(smem_raw + rel_bytes<T>(ns)) + threadIdx.x;
+  T* stash = reinterpret_cast<T*>(smem_raw + rel_bytes<T>(ns));  // [8][block] vec2
   double sgn, Aprime;
   stage_trace<T>(a.rec, ns, a.amplitude, rel, sgn, Aprime);
   __syncthreads();
@@ -218,9 +238,9 @@ __global__ void __launch_bounds__(256, 2) simscore_kernel(ExplicitArgs a) {
 }
 
 template <typename T, int INTEG>
-__global__ void __launch_bounds__(256, 2) simulate_kernel(ExplicitArgs a) {
+__global__ void __launch_bounds__(512, 1) simulate_kernel(ExplicitArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* stash = reinterpret_cast<T*>(smem_raw) + threadIdx.x;
+  T* stash = reinterpret_cast<T*>(smem_raw);  // [8][block] vec2
   const double A = a.amplitude;  // explicit simulate: A given (NaN rejected on host)
   const double sgn = A < 0.0 ? -1.0 : 1.0, Aprime = fabs(A);
   T* traj = reinterpret_cast<T*>(a.traj);
@@ -268,11 +288,11 @@ __global__ void __launch_bounds__(256) score_kernel(ScoreArgs a) {
 }
 
 __global__ void generate_kernel(SpaceDev sp, uint32_t saccade, int64_t begin, int64_t count,
-                                double* out, int64_t ld) {
+                                double* out, int64_t ld, const double2* tab) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < count; j += stride) {
     double p[NP];
-    generate_opc(sp, saccade, begin + j, p);
+    generate_opc(sp, saccade, begin + j, p, tab);
 #pragma unroll
     for (int d = 0; d < NP; ++d) out[(int64_t)d * ld + j] = p[d];
   }
@@ -301,8 +321,8 @@ cudaError_t launch_fit(const FitArgs& a, int precision, int integrator, int metr
 }
 
 cudaError_t launch_merge(const Partial* gathered, int world, const SpaceDev& sp, uint32_t saccade,
-                         opmm_fit_result* out, cudaStream_t st) {
-  merge_kernel<<<1, 32, 0, st>>>(gathered, world, sp, saccade, out);
+                         opmm_fit_result* out, const double2* tab, cudaStream_t st) {
+  merge_kernel<<<1, 32, 0, st>>>(gathered, world, sp, saccade, out, tab);
   return cudaGetLastError();
 }
 
@@ -347,8 +367,8 @@ cudaError_t launch_score(const ScoreArgs& a, int precision, int metric, dim3 gri
 }
 
 cudaError_t launch_generate(const SpaceDev& sp, uint32_t saccade, int64_t begin, int64_t count,
-                            double* out, int64_t ld, int grid, cudaStream_t st) {
-  generate_kernel<<<grid, 256, 0, st>>>(sp, saccade, begin, count, out, ld);
+                            double* out, int64_t ld, const double2* tab, int grid, cudaStream_t st) {
+  generate_kernel<<<grid, 256, 0, st>>>(sp, saccade, begin, count, out, ld, tab);
   return cudaGetLastError();
 }
 

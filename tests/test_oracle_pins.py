@@ -522,3 +522,25 @@ def test_trace_fixture_is_oracle_output():
     rec = np.loadtxt(os.path.join(GOLDEN, "trace_truth_A10_dt1_n100.txt"), comments="#")
     ref = oracle.positions(W.truth_opc(), W.Control())
     assert np.array_equal(rec, ref)
+
+
+def test_referee_longdouble_agrees_with_oracle_on_stable_candidates():
+    """The extended-precision referee evaluates the same definition: on
+    RK4-stable candidates it agrees with the fp64 oracle to ~1e-13."""
+    from oracle import referee
+    ctl = W.Control()
+    rec = oracle.positions(W.truth_opc(), ctl) + W.noise(101)
+    sp = W.paper_space()
+    n_checked = 0
+    for i in range(60):
+        p = oracle.generate(sp, i)
+        if referee.rk4_spectral_radius(p, ctl.dt_ms) >= 1.0:
+            continue
+        e64 = oracle.objective(p, rec, ctl)
+        eld = referee.objective_longdouble(p, rec, ctl)
+        assert abs(e64 - eld) <= 1e-13 * max(e64, 1.0)
+        n_checked += 1
+    assert n_checked >= 10
+    # TRUTH on its own clean output: both ~0
+    rec0 = oracle.positions(W.truth_opc(), ctl)
+    assert referee.objective_longdouble(W.truth_opc(), rec0, ctl) < 1e-10

@@ -324,17 +324,33 @@ __device__ __forceinline__ typename Vec2<T>::type make_v2(T a, T b) {
   return v;
 }
 
+// Two-step blocks.  The loop advances two RK4 steps per iteration with the
+// composed map M2 = M.M, c2 = M c + c (still exactly the RK4 recurrence), and
+// recovers the intermediate sample from row 0 of the one-step map:
+//   theta_{k+1} = P[0].z_k + X[0].f_k + c[0]          (7 terms)
+//   z_{k+2}     = P2 z_k + X2 f_k + c2,  X2 = P X + X diag(pf),
+//                 c2 = P c + X qf + c                  (4 rows x 7 terms)
+//   f_{k+2}     = pf^2 f_k + (pf qf + qf)
+// 32 FMA + 4 score ops per two steps (18 per step, vs 28 for one-step
+// blocks and 92 for the literal four-stage form).  Phase switches fall on
+// block boundaries because each lane starts at k = n_pulse mod 2: an odd lane
+// takes its first pulse step for free (from the zero deviation state
+// z_1 = c, f_1 = qf).
 template <typename T>
-struct PhaseProp {
-  T X[4][2];
-  T c[4];
-  T pf[2], qf[2];
+struct PhaseProp2 {
+  T X2[4][2];
+  T c2[4];
+  T pf2[2], qf2[2];
+  T X0[2];   // row 0 of the one-step X
+  T c0;      // row 0 of the one-step c
 };
 
 template <typename T>
-struct Prop {
-  T P[4][4];
-  PhaseProp<T> ph[2];
+struct Prop2 {
+  T P2[4][4];
+  T P0[4];             // row 0 of the one-step P (phase-independent)
+  PhaseProp2<T> ph[2];
+  T z1[4], f1[2];      // state after one pulse step from zero (odd start)
 };
 
 __device__ __forceinline__ void zmul_vec(const Mech& m, const double v[4], double out[4]) {
@@ -361,21 +377,18 @@ __device__ __forceinline__ void horner_step(const Mech& m, double s, double Tm[4
 }
 
 template <typename T>
-__device__ __forceinline__ void make_prop(const Setup& s, Prop<T>& pr) {
+__device__ __forceinline__ void make_prop(const Setup& s, Prop2<T>& pr) {
   const Mech& m = s.m;
-  double Tm[4][4];
+  // one-step mechanical block P(Z), Z = hM: 4 sparse Horner steps
+  double P[4][4];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) Tm[i][j] = (i == j ? 1.0 : 0.0);
-  horner_step(m, 0.25, Tm);              // I + Z/4
-  horner_step(m, 1.0 / 3.0, Tm);         // I + Z/3 (I + Z/4)
-  horner_step(m, 0.5, Tm);               // I + Z/2 (...)
-  horner_step(m, 1.0, Tm);               // I + Z (...) = P(Z)
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) pr.P[i][j] = (T)Tm[i][j];
+    for (int j = 0; j < 4; ++j) P[i][j] = (i == j ? 1.0 : 0.0);
+  horner_step(m, 0.25, P);               // I + Z/4
+  horner_step(m, 1.0 / 3.0, P);          // I + Z/3 (I + Z/4)
+  horner_step(m, 0.5, P);                // I + Z/2 (...)
+  horner_step(m, 1.0, P);                // I + Z (...) = P(Z)
   // u_i = Z^i (h c_m): c_AG = e_2 / B_AG, c_ANT = e_3 / B_ANT.
   double u[2][4][4];
 #pragma unroll
@@ -387,8 +400,19 @@ __device__ __forceinline__ void make_prop(const Setup& s, Prop<T>& pr) {
     for (int i = 1; i < 4; ++i) zmul_vec(m, u[mm][i - 1], u[mm][i]);
   }
 #pragma unroll
+  for (int i = 0; i < 4; ++i) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      double a = 0.0;
+#pragma unroll
+      for (int l = 0; l < 4; ++l) a = fma(P[i][l], P[l][j], a);
+      pr.P2[i][j] = (T)a;
+    }
+    pr.P0[i] = (T)P[0][i];
+  }
+#pragma unroll
   for (int ph = 0; ph < 2; ++ph) {
-    double c[4] = {0.0, 0.0, 0.0, 0.0};
+    double X[4][2], c[4] = {0.0, 0.0, 0.0, 0.0}, pf[2], qf[2];
 #pragma unroll
     for (int mm = 0; mm < 2; ++mm) {
       const double zd = mm == 0 ? s.ph[ph].zd_ag : s.ph[ph].zd_ant;
@@ -400,15 +424,40 @@ __device__ __forceinline__ void make_prop(const Setup& s, Prop<T>& pr) {
       const double g = -zd * nt;
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
-        pr.ph[ph].X[r][mm] = (T)(u[mm][0][r] * a0 + u[mm][1][r] * a1 + u[mm][2][r] * a2 +
-                                 u[mm][3][r] * a3);
+        X[r][mm] = u[mm][0][r] * a0 + u[mm][1][r] * a1 + u[mm][2][r] * a2 + u[mm][3][r] * a3;
         c[r] += g * (u[mm][0][r] * a1 + u[mm][1][r] * a2 + u[mm][2][r] * a3);
       }
-      pr.ph[ph].pf[mm] = (T)(1.0 + zd * a0);
-      pr.ph[ph].qf[mm] = (T)(g * a0);
+      pf[mm] = 1.0 + zd * a0;
+      qf[mm] = g * a0;
+    }
+    PhaseProp2<T>& q = pr.ph[ph];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      double c2 = c[r] + X[r][0] * qf[0] + X[r][1] * qf[1];
+#pragma unroll
+      for (int l = 0; l < 4; ++l) c2 = fma(P[r][l], c[l], c2);
+      q.c2[r] = (T)c2;
+#pragma unroll
+      for (int mm = 0; mm < 2; ++mm) {
+        double x2 = X[r][mm] * pf[mm];
+#pragma unroll
+        for (int l = 0; l < 4; ++l) x2 = fma(P[r][l], X[l][mm], x2);
+        q.X2[r][mm] = (T)x2;
+      }
     }
 #pragma unroll
-    for (int r = 0; r < 4; ++r) pr.ph[ph].c[r] = (T)c[r];
+    for (int mm = 0; mm < 2; ++mm) {
+      q.pf2[mm] = (T)(pf[mm] * pf[mm]);
+      q.qf2[mm] = (T)(pf[mm] * qf[mm] + qf[mm]);
+      q.X0[mm] = (T)X[0][mm];
+    }
+    q.c0 = (T)c[0];
+    if (ph == 0) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) pr.z1[r] = (T)c[r];
+      pr.f1[0] = (T)qf[0];
+      pr.f1[1] = (T)qf[1];
+    }
   }
 }
 
@@ -449,73 +498,118 @@ __device__ __forceinline__ double finish_error(T acc, int32_t n_samples) {
 // time-major and accumulate |Delta-theta| instead, to flag divergence.
 // ----------------------------------------------------------------------------
 template <typename T, int METRIC, bool TRAJ>
-__device__ __forceinline__ T run_propagator(const Prop<T>& pr, int32_t n_pulse, int32_t n_steps,
+__device__ __forceinline__ T run_propagator(const Prop2<T>& pr, int32_t n_pulse, int32_t n_steps,
                                             const T* __restrict__ rel, T* __restrict__ traj,
                                             int64_t ld_out, T theta0, T sgn,
                                             T* __restrict__ stash, int stash_ld) {
-  T th = T(0), om = T(0), xa = T(0), xn = T(0), fa = T(0), fn = T(0);
-  T acc = T(0);
-  // The 16 step-phase coefficients wait in a per-thread shared-memory stash
-  // ([16][stash_ld], conflict-free) instead of registers; the 4x4 P stays in
-  // registers for the whole loop.
-  const PhaseProp<T>& q = pr.ph[1];
-  // stash: 8 pairs [8][stash_ld] of vec2 (double2 / float2), one vector
-  // load per pair at the swap
   using V2 = typename Vec2<T>::type;
+  // Post-pulse coefficients wait in a per-thread shared-memory stash
+  // ([10][stash_ld] of vec2, conflict-free); the phase-independent P2 and
+  // P[0] stay in registers for the whole loop.
   V2* st2 = reinterpret_cast<V2*>(stash) + threadIdx.x;
-  st2[0 * stash_ld] = make_v2<T>(q.X[0][0], q.X[0][1]);
-  st2[1 * stash_ld] = make_v2<T>(q.X[1][0], q.X[1][1]);
-  st2[2 * stash_ld] = make_v2<T>(q.X[2][0], q.X[2][1]);
-  st2[3 * stash_ld] = make_v2<T>(q.X[3][0], q.X[3][1]);
-  st2[4 * stash_ld] = make_v2<T>(q.c[0], q.c[1]);
-  st2[5 * stash_ld] = make_v2<T>(q.c[2], q.c[3]);
-  st2[6 * stash_ld] = make_v2<T>(q.pf[0], q.pf[1]);
-  st2[7 * stash_ld] = make_v2<T>(q.qf[0], q.qf[1]);
-  T X00 = pr.ph[0].X[0][0], X01 = pr.ph[0].X[0][1], X10 = pr.ph[0].X[1][0], X11 = pr.ph[0].X[1][1];
-  T X20 = pr.ph[0].X[2][0], X21 = pr.ph[0].X[2][1], X30 = pr.ph[0].X[3][0], X31 = pr.ph[0].X[3][1];
-  T c0 = pr.ph[0].c[0], c1 = pr.ph[0].c[1], c2 = pr.ph[0].c[2], c3 = pr.ph[0].c[3];
-  T pa = pr.ph[0].pf[0], pn = pr.ph[0].pf[1], qa = pr.ph[0].qf[0], qn = pr.ph[0].qf[1];
-  const T P00 = pr.P[0][0], P01 = pr.P[0][1], P02 = pr.P[0][2], P03 = pr.P[0][3];
-  const T P10 = pr.P[1][0], P11 = pr.P[1][1], P12 = pr.P[1][2], P13 = pr.P[1][3];
-  const T P20 = pr.P[2][0], P21 = pr.P[2][1], P22 = pr.P[2][2], P23 = pr.P[2][3];
-  const T P30 = pr.P[3][0], P31 = pr.P[3][1], P32 = pr.P[3][2], P33 = pr.P[3][3];
-  if (TRAJ) traj[0] = theta0;
-  // Load the post-pulse coefficients from the stash (lanes whose pulse ends).
+  {
+    const PhaseProp2<T>& q = pr.ph[1];
+    st2[0 * stash_ld] = make_v2<T>(q.X2[0][0], q.X2[0][1]);
+    st2[1 * stash_ld] = make_v2<T>(q.X2[1][0], q.X2[1][1]);
+    st2[2 * stash_ld] = make_v2<T>(q.X2[2][0], q.X2[2][1]);
+    st2[3 * stash_ld] = make_v2<T>(q.X2[3][0], q.X2[3][1]);
+    st2[4 * stash_ld] = make_v2<T>(q.c2[0], q.c2[1]);
+    st2[5 * stash_ld] = make_v2<T>(q.c2[2], q.c2[3]);
+    st2[6 * stash_ld] = make_v2<T>(q.pf2[0], q.pf2[1]);
+    st2[7 * stash_ld] = make_v2<T>(q.qf2[0], q.qf2[1]);
+    st2[8 * stash_ld] = make_v2<T>(q.X0[0], q.X0[1]);
+    st2[9 * stash_ld] = make_v2<T>(q.c0, T(0));
+  }
+  const PhaseProp2<T>& q0 = pr.ph[0];
+  T A00 = q0.X2[0][0], A01 = q0.X2[0][1], A10 = q0.X2[1][0], A11 = q0.X2[1][1];
+  T A20 = q0.X2[2][0], A21 = q0.X2[2][1], A30 = q0.X2[3][0], A31 = q0.X2[3][1];
+  T c0 = q0.c2[0], c1 = q0.c2[1], c2 = q0.c2[2], c3 = q0.c2[3];
+  T pa = q0.pf2[0], pn = q0.pf2[1], qa = q0.qf2[0], qn = q0.qf2[1];
+  T x0a = q0.X0[0], x0n = q0.X0[1], d0 = q0.c0;
+  const T Q00 = pr.P2[0][0], Q01 = pr.P2[0][1], Q02 = pr.P2[0][2], Q03 = pr.P2[0][3];
+  const T Q10 = pr.P2[1][0], Q11 = pr.P2[1][1], Q12 = pr.P2[1][2], Q13 = pr.P2[1][3];
+  const T Q20 = pr.P2[2][0], Q21 = pr.P2[2][1], Q22 = pr.P2[2][2], Q23 = pr.P2[2][3];
+  const T Q30 = pr.P2[3][0], Q31 = pr.P2[3][1], Q32 = pr.P2[3][2], Q33 = pr.P2[3][3];
+  const T R0 = pr.P0[0], R1 = pr.P0[1], R2 = pr.P0[2], R3 = pr.P0[3];
   auto swap_in = [&]() {
     V2 v;
-    v = st2[0 * stash_ld]; X00 = v.x; X01 = v.y;
-    v = st2[1 * stash_ld]; X10 = v.x; X11 = v.y;
-    v = st2[2 * stash_ld]; X20 = v.x; X21 = v.y;
-    v = st2[3 * stash_ld]; X30 = v.x; X31 = v.y;
+    v = st2[0 * stash_ld]; A00 = v.x; A01 = v.y;
+    v = st2[1 * stash_ld]; A10 = v.x; A11 = v.y;
+    v = st2[2 * stash_ld]; A20 = v.x; A21 = v.y;
+    v = st2[3 * stash_ld]; A30 = v.x; A31 = v.y;
     v = st2[4 * stash_ld]; c0 = v.x; c1 = v.y;
     v = st2[5 * stash_ld]; c2 = v.x; c3 = v.y;
     v = st2[6 * stash_ld]; pa = v.x; pn = v.y;
     v = st2[7 * stash_ld]; qa = v.x; qn = v.y;
+    v = st2[8 * stash_ld]; x0a = v.x; x0n = v.y;
+    v = st2[9 * stash_ld]; d0 = v.x;
   };
+  // Lane parity: blocks start at k = o (mod 2) so the pulse end n_pulse falls
+  // on a block boundary.  n_pulse == 0 or > n_steps never switches mid-run.
+  const bool switches = n_pulse > 0 && n_pulse <= n_steps;
+  const int32_t o = switches ? (n_pulse & 1) : 0;
+  T th = T(0), om = T(0), xa = T(0), xn = T(0), fa = T(0), fn = T(0);
+  T acc = T(0);
+  if (TRAJ) traj[0] = theta0;
   if (n_pulse == 0) swap_in();
-  // Segmented loop: the warp runs uniform segments between consecutive pulse
-  // ends of its lanes (warp-min of the next n_pulse), so the inner loop is
-  // pure FMA work with no per-step phase test; at a segment end only the
-  // lanes whose pulse ends there reload their coefficients.  The callers
-  // keep all 32 lanes active.  Sample 0 contributes |0 - rel_0| = 0 exactly.
-  int32_t k = 0;
-  while (k < n_steps) {
-    const int32_t mine = n_pulse > k ? min(n_pulse, n_steps) : n_steps;
+  if (o) {  // first pulse step from the zero deviation state: z_1 = c, f_1 = qf
+    th = pr.z1[0]; om = pr.z1[1]; xa = pr.z1[2]; xn = pr.z1[3];
+    fa = pr.f1[0]; fn = pr.f1[1];
+    accumulate<METRIC>(acc, TRAJ ? th : th - rel[1]);
+    if (TRAJ) traj[ld_out] = fma(sgn, th, theta0);
+  }
+  // Block b covers steps k = o + 2b -> k + 2.  Every lane runs nb uniform
+  // blocks; the last one may overrun n_steps by one step for odd lanes
+  // (masked below).  The lane switches phase before block bs.
+  const int32_t nb = (n_steps + 1) / 2;
+  const int32_t bs = switches ? (n_pulse - o) / 2 : nb;
+  if (switches && bs == 0) swap_in();   // pulse ends before the first block
+  const T* __restrict__ rl = rel + o;   // rl[2b + 1], rl[2b + 2]
+  T* __restrict__ tr = TRAJ ? traj + (int64_t)o * ld_out : traj;
+  // Segmented loop over blocks: uniform segments between consecutive lane
+  // switch points (warp-min), so the inner loop is pure FMA work; at a
+  // segment end only the lanes that switch there reload their coefficients.
+  // The callers keep all 32 lanes active.
+  int32_t b = 0;
+  while (b < nb - 1) {
+    const int32_t mine = bs > b ? min(bs, nb - 1) : nb - 1;
     const int32_t seg_end = __reduce_min_sync(0xffffffffu, mine);
-#pragma unroll 4
-    for (; k < seg_end; ++k) {
-      const T r = TRAJ ? T(0) : rel[k + 1];
-      const T nth = fma(P00, th, fma(P01, om, fma(P02, xa, fma(P03, xn, fma(X00, fa, fma(X01, fn, c0))))));
-      const T nom = fma(P10, th, fma(P11, om, fma(P12, xa, fma(P13, xn, fma(X10, fa, fma(X11, fn, c1))))));
-      const T nxa = fma(P20, th, fma(P21, om, fma(P22, xa, fma(P23, xn, fma(X20, fa, fma(X21, fn, c2))))));
-      const T nxn = fma(P30, th, fma(P31, om, fma(P32, xa, fma(P33, xn, fma(X30, fa, fma(X31, fn, c3))))));
+#pragma unroll 2
+    for (; b < seg_end; ++b) {
+      const T t1 = fma(R0, th, fma(R1, om, fma(R2, xa, fma(R3, xn, fma(x0a, fa, fma(x0n, fn, d0))))));
+      const T nth = fma(Q00, th, fma(Q01, om, fma(Q02, xa, fma(Q03, xn, fma(A00, fa, fma(A01, fn, c0))))));
+      const T nom = fma(Q10, th, fma(Q11, om, fma(Q12, xa, fma(Q13, xn, fma(A10, fa, fma(A11, fn, c1))))));
+      const T nxa = fma(Q20, th, fma(Q21, om, fma(Q22, xa, fma(Q23, xn, fma(A20, fa, fma(A21, fn, c2))))));
+      const T nxn = fma(Q30, th, fma(Q31, om, fma(Q32, xa, fma(Q33, xn, fma(A30, fa, fma(A31, fn, c3))))));
       fa = fma(pa, fa, qa);
       fn = fma(pn, fn, qn);
       th = nth; om = nom; xa = nxa; xn = nxn;
-      accumulate<METRIC>(acc, TRAJ ? th : th - r);  // TRAJ: no trace, sum |dtheta|
-      if (TRAJ) traj[(int64_t)(k + 1) * ld_out] = fma(sgn, th, theta0);
+      if (TRAJ) {
+        accumulate<METRIC>(acc, t1);
+        accumulate<METRIC>(acc, th);
+        tr[(int64_t)(2 * b + 1) * ld_out] = fma(sgn, t1, theta0);
+        tr[(int64_t)(2 * b + 2) * ld_out] = fma(sgn, th, theta0);
+      } else {
+        accumulate<METRIC>(acc, t1 - rl[2 * b + 1]);
+        accumulate<METRIC>(acc, th - rl[2 * b + 2]);
+      }
     }
-    if (k == n_pulse) swap_in();
+    if (b == bs) swap_in();
+  }
+  // last block (b = nb - 1): steps o + 2b + 1 and o + 2b + 2, either of which
+  // may lie past n_steps
+  if (nb >= 1) {
+    const int32_t k1 = o + 2 * b + 1;
+    const T t1 = fma(R0, th, fma(R1, om, fma(R2, xa, fma(R3, xn, fma(x0a, fa, fma(x0n, fn, d0))))));
+    const T t2 = fma(Q00, th, fma(Q01, om, fma(Q02, xa, fma(Q03, xn, fma(A00, fa, fma(A01, fn, c0))))));
+    if (k1 <= n_steps) {
+      accumulate<METRIC>(acc, TRAJ ? t1 : t1 - rel[k1]);
+      if (TRAJ) traj[(int64_t)k1 * ld_out] = fma(sgn, t1, theta0);
+    }
+    if (k1 + 1 <= n_steps) {
+      accumulate<METRIC>(acc, TRAJ ? t2 : t2 - rel[k1 + 1]);
+      if (TRAJ) traj[(int64_t)(k1 + 1) * ld_out] = fma(sgn, t2, theta0);
+    }
   }
   return acc;
 }

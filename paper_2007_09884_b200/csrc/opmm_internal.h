@@ -18,7 +18,7 @@ __host__ __device__ constexpr size_t rel_bytes(int32_t n_samples) {
 }
 template <typename T>
 __host__ __device__ constexpr size_t stash_bytes(int block) {
-  return (size_t)16 * block * sizeof(T);
+  return (size_t)20 * block * sizeof(T);   // [10][block] vec2<T>
 }
 // fit kernel: trace, then the exp table (double2[EXP_TAB_N]), then the stash
 __host__ __device__ constexpr size_t exp_tab_bytes() { return (size_t)EXP_TAB_N * 16; }

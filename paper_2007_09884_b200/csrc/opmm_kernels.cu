@@ -42,7 +42,7 @@ __device__ __forceinline__ double evaluate(const double p[NP], const CtlDev& c, 
   make_setup(p, c.dt_ms, c.h, c.n_steps, Aprime, pw_default, s);
   T acc;
   if (INTEG == 0) {
-    Prop<T> pr;
+    Prop2<T> pr;
     make_prop<T>(s, pr);
     acc = run_propagator<T, METRIC, TRAJ>(pr, s.n_pulse, c.n_steps, rel, traj, ld_out,
                                           (T)c.theta0, (T)sgn, stash, blockDim.x);

@@ -205,6 +205,38 @@ def test_simulate_fp64_trajectories(opmm, h, integrator, amp, theta0):
     print(f"max rel trajectory diff {worst:.3e}; large-amplitude finite candidates {n_unstable_checked}")
 
 
+@pytest.mark.parametrize("n_steps", [99, 100])
+def test_simulate_pulse_width_edges(opmm, h, n_steps):
+    """Pulse ends of both parities and at the edges of the window:
+    n_pulse = ceil(PW/dt) in {1, 2, 3, n-1, n, n+1, beyond} (the loop's
+    two-step blocks align each lane to n_pulse mod 2)."""
+    ctl = W.Control(n_steps=n_steps)
+    pws = [0.3, 1.0, 1.5, 2.0, 3.0, n_steps - 1.0, n_steps - 0.5, float(n_steps), n_steps + 0.5,
+           n_steps + 1.0, 250.0, math.nan]
+    base = W.truth_opc()
+    cands = []
+    for pw in pws:
+        for f in (1.0, 0.7):
+            p = base.copy()
+            p[I["PW"]] = pw
+            p[I["N_SAC_AG"]] *= f
+            cands.append(p)
+    cands = np.array(cands)
+    n = len(cands)
+    for integrator in (0, 1):
+        for prec, tol in ((opmm.FP64, 1e-9), (opmm.FP32, 1e-3)):
+            dt = torch.float64 if prec == opmm.FP64 else torch.float32
+            traj = torch.zeros((n_steps + 1, n), dtype=dt, device="cuda")
+            opmm.opmm_simulate(h, soa(cands), n, ctl, traj, precision=prec, integrator=integrator,
+                               stream=torch.cuda.current_stream())
+            torch.cuda.synchronize()
+            T = traj.cpu().numpy().astype(np.float64)
+            for i, p in enumerate(cands):
+                ref = oracle.simulate(p, ctl.dt_ms, n_steps, 10.0, ctl.pw_default_ms)
+                scale = 1.0 if prec == opmm.FP32 else max(np.max(np.abs(ref)), 1.0)
+                assert np.max(np.abs(T[:, i] - ref)) <= tol * scale, (pws[i // 2], integrator, prec)
+
+
 def test_simulate_fp32_trajectories_rk4_stable(opmm, h):
     ctl = W.Control()
     cands = candidate_set(n_paper=1500)

@@ -112,7 +112,7 @@ typedef struct {
   int32_t precision;    /* opmm_precision: arithmetic of the integrate+score loop */
   int32_t metric;       /* opmm_metric                                            */
   int32_t integrator;   /* opmm_integrator                                        */
-  int32_t block_size;   /* 0 = default (256); else 64..512, multiple of 32        */
+  int32_t block_size;   /* 0 = default (384); else 64..384, multiple of 32        */
   int32_t grid_blocks;  /* 0 = default (persistent: SMs x resident blocks)        */
   int32_t cpu_check;    /* 1 = fill result.cpu_check, 0 = NaN      */
   double* err_out;      /* optional DEVICE [n]: E_i of every candidate (validation) */

@@ -4,6 +4,7 @@
 // the paper's CPU_check column.  Every step of the hot path itself runs in
 // the kernels of opmm_kernels.cu; nothing here computes candidates on the CPU.
 #include <cmath>
+#include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -88,7 +89,7 @@ NcclApi& nccl() {
   return api;
 }
 
-constexpr int kDefaultBlock = 256;
+constexpr int kDefaultBlock = 384;   // == OPMM_FIT_LB_THREADS (opmm_kernels.cu)
 constexpr size_t kMaxDynSmem = 200 * 1024;
 
 }  // namespace
@@ -242,6 +243,9 @@ opmm::SpaceDev make_space(const opmm_search_space* s) {
         s->lo[OPMM_P_NC_ANT] + s->lo[OPMM_P_KLT_ANT] > 0.0))
     phys = false;
   d.all_physical = phys ? 1 : 0;
+  d.pw_stride = 1;
+  if (s->mode == 1)
+    for (int k = 0; k < OPMM_P_PW; ++k) d.pw_stride *= s->levels[k];
   return d;
 }
 
@@ -290,9 +294,9 @@ opmm_status grid_for(opmm_handle* h, const void* fn, int block, size_t smem, int
 }
 
 opmm_status check_block(int block) {
-  // the simulate kernels are compiled with __launch_bounds__(512, 1): <= 128 regs
-  if (block < 64 || block > 512 || block % 32 != 0)
-    return fail(OPMM_ERR_INVALID_ARG, "block_size must be a multiple of 32 in [64, 512]");
+  // the simulate kernels are compiled with __launch_bounds__(384, 1): <= 168 regs
+  if (block < 64 || block > kDefaultBlock || block % 32 != 0)
+    return fail(OPMM_ERR_INVALID_ARG, "block_size must be a multiple of 32 in [64, 384]");
   return OPMM_OK;
 }
 
@@ -354,6 +358,7 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
   a.end = e;
   a.err_out = opts ? opts->err_out : nullptr;
   a.err_ld = n_candidates;
+  a.sort_lanes = getenv("OPMM_NO_LANE_SORT") ? 0 : 1;   // env switch for A/B timing only
   a.partials = h->partials;
   a.counters = h->counters;
   a.rank_out = multi ? h->rank_part : nullptr;
@@ -442,6 +447,10 @@ opmm_status opmm_create(opmm_handle** out, int device) {
         cudaFuncSetAttribute(opmm::fit_kernel_ptr(p, i, m),
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDynSmem);
         cudaFuncSetAttribute(opmm::simscore_kernel_ptr(p, i, m),
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDynSmem);
+        cudaFuncSetAttribute(opmm::simulate_kernel_ptr(p, i),
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDynSmem);
+        cudaFuncSetAttribute(opmm::score_kernel_ptr(p, m),
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDynSmem);
       }
   cudaGetLastError();

@@ -42,6 +42,7 @@ struct SpaceDev {
   // random: linear hi-lo, log log(hi/lo); grid: linear (hi-lo)/(L-1), log log(hi/lo)/(L-1)
   double span[NP];
   int64_t levels[NP];    // grid radices (1 = not a grid dimension)
+  int64_t pw_stride;     // grid: product of levels[0..16] (PW digit = i / pw_stride % L17)
 };
 
 // Per-launch control (shared by every candidate of a saccade).
@@ -183,6 +184,23 @@ __device__ __forceinline__ void generate_opc(const SpaceDev& sp, uint32_t saccad
         if (e == d) p[e] = v;
     }
   }
+}
+
+// PW of candidate idx alone (for the lane sort key): Philox block j = 4,
+// word 1 is dimension 17; grid mode takes the PW digit directly.
+__device__ __forceinline__ double generate_pw(const SpaceDev& sp, uint32_t saccade, int64_t idx,
+                                              const double2* __restrict__ tab) {
+  if (sp.mode == 0) {
+    const uint4 w = philox4x32_10(make_uint4((uint32_t)((uint64_t)idx & 0xffffffffu),
+                                             (uint32_t)((uint64_t)idx >> 32), saccade, 4u),
+                                  make_uint2(sp.key0, sp.key1));
+    return map_word(sp, PW_, w.y, tab);
+  }
+  const uint64_t L = (uint64_t)sp.levels[PW_];
+  const uint64_t digit = L > 1 ? ((uint64_t)idx / (uint64_t)sp.pw_stride) % L : 0;
+  if (sp.kind[PW_] == 0 || L <= 1) return sp.lo[PW_];
+  if (sp.kind[PW_] == 1) return __dadd_rn(sp.lo[PW_], __dmul_rn((double)digit, sp.span[PW_]));
+  return __dmul_rn(sp.lo[PW_], exp(__dmul_rn((double)digit, sp.span[PW_])));
 }
 
 // ----------------------------------------------------------------------------

@@ -43,6 +43,7 @@ struct FitArgs {
   int64_t begin, end;       // candidate range of this rank
   double* err_out;          // optional device, indexed [sac * err_ld + i]
   int64_t err_ld;
+  int32_t sort_lanes;       // counting-sort tiles by pulse end (see fit_kernel)
   Partial* partials;        // [S][gridDim.x]
   unsigned int* counters;   // [S], zero between launches
   Partial* rank_out;        // optional [S]: per-rank result (world > 1)

@@ -97,8 +97,11 @@ __device__ void write_result(const SpaceDev& sp, uint32_t saccade, double e, int
 // The fused fit kernel.  gridDim.y = saccades of this launch (1 for a single
 // fit); blockIdx.x strides over the candidate range [begin, end) of each.
 // ---------------------------------------------------------------------------
+// The simulate kernels are register-heavy (per-candidate setup peaks near
+// 240 live registers): 384 threads x 168 registers, 3 warps per scheduler,
+// measured best among 128/168/238-register budgets.
 #ifndef OPMM_FIT_LB_THREADS
-#define OPMM_FIT_LB_THREADS 512
+#define OPMM_FIT_LB_THREADS 384
 #endif
 #ifndef OPMM_FIT_LB_BLOCKS
 #define OPMM_FIT_LB_BLOCKS 1
@@ -132,9 +135,66 @@ __global__ void __launch_bounds__(OPMM_FIT_LB_THREADS, OPMM_FIT_LB_BLOCKS) fit_k
   // Warp-uniform trip count: every lane of a warp runs every iteration (lanes
   // past `end` evaluate the last candidate again and discard it), so the
   // per-step warp vote in run_propagator always sees a full warp.
+  // Lane sort: each tile of blockDim candidates is counting-sorted by the
+  // block index at which its pulse ends (n_pulse / 2, 256 bins), so a warp's
+  // lanes share few phase-switch points and run_propagator's segmented loop
+  // has few segments.  Only the candidate->thread assignment changes; every
+  // result is per candidate, so outputs are identical (and deterministic).
+  __shared__ int s_hist[256];
+  __shared__ int s_wsum[32];
+  __shared__ int s_perm[OPMM_FIT_LB_THREADS];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t base = a.begin + (int64_t)blockIdx.x * blockDim.x; base < a.end; base += stride) {
-    const int64_t i0 = base + threadIdx.x;
+    int src = tid;
+    if (a.sort_lanes) {
+      const int nbins = blockDim.x < 256 ? (int)blockDim.x : 256;   // multiple of 32
+      const int64_t j0 = base + tid;
+      int key = nbins - 1;                                          // padding lanes last
+      if (j0 < a.end) {
+        const double pw = generate_pw(a.space, (uint32_t)sac, j0, tab);
+        const double npd = ceil(pw / a.ctl.dt_ms);
+        const int np = npd > (double)a.ctl.n_steps ? a.ctl.n_steps + 1 : (int)npd;
+        key = min(np >> 1, nbins - 2);
+      }
+      if (tid < nbins) s_hist[tid] = 0;
+      __syncthreads();
+      const int rank = atomicAdd(&s_hist[key], 1);
+      __syncthreads();
+      int v = 0, incl = 0;
+      if (tid < nbins) {
+        v = s_hist[tid];
+        incl = v;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, incl, off);
+          if (lane >= off) incl += t;
+        }
+        if (lane == 31) s_wsum[wid] = incl;
+      }
+      __syncthreads();
+      if (tid < 32) {
+        const int nw = nbins >> 5;
+        const int w = tid < nw ? s_wsum[tid] : 0;
+        int inc = w;
+#pragma unroll
+        for (int off = 1; off < 8; off <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, inc, off);
+          if (lane >= off) inc += t;
+        }
+        if (tid < nw) s_wsum[tid] = inc - w;
+      }
+      __syncthreads();
+      if (tid < nbins) s_hist[tid] = incl - v + s_wsum[wid];
+      __syncthreads();
+      s_perm[s_hist[key] + rank] = tid;
+      __syncthreads();
+      src = s_perm[tid];
+    }
+    // Warp-uniform trip count: every lane of a warp runs every iteration
+    // (lanes past `end` evaluate the last candidate again and discard it), so
+    // the warp-level reductions in run_propagator always see a full warp.
+    const int64_t i0 = base + src;
     const bool valid = i0 < a.end;
     const int64_t i = valid ? i0 : a.end - 1;
     double p[NP];
@@ -216,7 +276,7 @@ __device__ __forceinline__ void load_opc(const double* __restrict__ opc, int64_t
 }
 
 template <typename T, int INTEG, int METRIC>
-__global__ void __launch_bounds__(512, 1) simscore_kernel(ExplicitArgs a) {
+__global__ void __launch_bounds__(OPMM_FIT_LB_THREADS, OPMM_FIT_LB_BLOCKS) simscore_kernel(ExplicitArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int32_t ns = a.ctl.n_steps + 1;
   T* rel = reinterpret_cast<T*>(smem_raw);
@@ -238,7 +298,7 @@ __global__ void __launch_bounds__(512, 1) simscore_kernel(ExplicitArgs a) {
 }
 
 template <typename T, int INTEG>
-__global__ void __launch_bounds__(512, 1) simulate_kernel(ExplicitArgs a) {
+__global__ void __launch_bounds__(OPMM_FIT_LB_THREADS, OPMM_FIT_LB_BLOCKS) simulate_kernel(ExplicitArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* stash = reinterpret_cast<T*>(smem_raw);  // [8][block] vec2
   const double A = a.amplitude;  // explicit simulate: A given (NaN rejected on host)

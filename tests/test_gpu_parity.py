@@ -423,7 +423,7 @@ def test_fit_exact_ties_lowest_index(opmm, h):
     sp = W.grid_space({"N_SAC_AG": (d[15] * 0.99, d[15] * 1.01, 3, False),
                        "PW": (39.21, 40.0, 3, False)})
     o = oracle.fit(rec, ctl, sp, 0, 9)
-    for bs, gb in ((64, 0), (256, 0), (64, 1)):
+    for bs, gb in ((64, 0), (384, 0), (64, 1)):
         r, E = _fit(opmm, h, rec, ctl, sp, 9, block_size=bs, grid_blocks=gb)
         assert r["best_index"] == o["best_index"]
         e = E.reshape(3, 3)
@@ -437,9 +437,9 @@ def test_fit_launch_config_invariance(opmm, h):
     n = 50001
     ref, Eref = _fit(opmm, h, rec, ctl, sp, n)
     with pytest.raises(opmm.OpmmError) as ei:
-        _fit(opmm, h, rec, ctl, sp, n, block_size=1024)
+        _fit(opmm, h, rec, ctl, sp, n, block_size=512)
     assert ei.value.status == opmm.ERR_INVALID_ARG
-    for bs, gb in ((128, 0), (512, 0), (256, 1), (256, 7), (64, 3)):
+    for bs, gb in ((128, 0), (256, 0), (384, 1), (256, 7), (64, 3)):
         r, E = _fit(opmm, h, rec, ctl, sp, n, block_size=bs, grid_blocks=gb)
         assert (r["best_index"], r["opt_err"], r["n_finite"]) == \
                (ref["best_index"], ref["opt_err"], ref["n_finite"])

@@ -41,10 +41,14 @@ import workloads as W  # noqa: E402
 N_STEPS = 100
 PER_GPU = 10**6
 # Algorithmic FP64 work of the fit kernel per candidate:
-# the RK4 map in propagator form is 26 FMA per step (52 flop) + the fused L1
-# score 2 flop per step; per-candidate generation + setup counted separately.
-FLOP_PER_STEP = 54
-FLOP_SETUP = 1800  # per candidate: Philox map (17 exp), statics, P(Z) Horner, X/c build
+# the RK4 map in two-step propagator blocks is 32 FMA + 2 score adds per two
+# steps = 34 flop per step; generation + per-candidate setup = 1540 flop
+# (ncu op counts dfma/dadd/dmul at n = 100 minus the loop's exact count,
+# profiles/r01_fit_kernel_fp64_opcounts.txt).
+FLOP_PER_STEP = 34
+FLOP_SETUP = 1540
+FP64_INST_PER_STEP = 18    # fp64-pipe instructions per step (loop)
+FP64_INST_SETUP = 940      # fp64-pipe instructions per candidate outside the loop (ncu)
 SMS, FP64_LANES, SM_MAX_MHZ = 148, 64, 1965.0
 FP64_PEAK_TFLOPS = SMS * FP64_LANES * 2 * SM_MAX_MHZ * 1e6 / 1e12   # 37.23
 FP64_MEASURED_TFLOPS = 33.90   # profiles/r01_fma_peak.txt (DFMA microbenchmark)
@@ -298,7 +302,9 @@ def run_gpu(args):
                      "kernel": "fit_kernel<double, propagator, L1>", "kernel_ms": kms64,
                      "flop_per_candidate": per_cand_flop,
                      "peak_basis": "148 SM x 64 FP64 lanes x 2 x 1965 MHz (DESIGN.md)",
-                     "frac_of_measured_dfma": achieved / FP64_MEASURED_TFLOPS},
+                     "frac_of_measured_dfma": achieved / FP64_MEASURED_TFLOPS,
+                     "fp64_issue_frac": (FP64_INST_PER_STEP * N_STEPS + FP64_INST_SETUP) * args.per_gpu
+                     / (kms64 * 1e-3) / (SMS * FP64_LANES * SM_MAX_MHZ * 1e6)},
         "fp32": {"value": n_total / (ms32 * 1e-3), "ms_per_step": ms32, "kernel_ms": kms32,
                  "best_index": res32["best_index"]},
         "result": {"best_index": res64["best_index"], "opt_err": res64["opt_err"],

@@ -115,6 +115,12 @@ typedef struct {
   int32_t block_size;   /* 0 = default (384); else 64..384, multiple of 32        */
   int32_t grid_blocks;  /* 0 = default (persistent: SMs x resident blocks)        */
   int32_t cpu_check;    /* 1 = fill result.cpu_check, 0 = NaN      */
+  int32_t kernel_variant; /* fit kernel: 0 = auto; 1 = one candidate per thread;
+                              2 = two interleaved candidates per thread;
+                              3 = warp-specialised producer/consumer.  2 and 3
+                              need PROPAGATOR, a physical-by-construction space
+                              and block_size = 0        */
+  int32_t pad_;         /* must be 0                                              */
   double* err_out;      /* optional DEVICE [n]: E_i of every candidate (validation) */
 } opmm_fit_options;
 

@@ -23,7 +23,7 @@ using opmm::Partial;
 // ABI layout (mirrored by the ctypes binding; checked by tests/test_abi.py)
 static_assert(sizeof(opmm_control) == 40, "opmm_control layout");
 static_assert(sizeof(opmm_search_space) == 400, "opmm_search_space layout");
-static_assert(sizeof(opmm_fit_options) == 32, "opmm_fit_options layout");
+static_assert(sizeof(opmm_fit_options) == 40, "opmm_fit_options layout");
 static_assert(sizeof(opmm_fit_result) == 184, "opmm_fit_result layout");
 static_assert(sizeof(Partial) == 32, "Partial layout");
 
@@ -90,7 +90,9 @@ NcclApi& nccl() {
 }
 
 constexpr int kDefaultBlock = 384;   // == OPMM_FIT_LB_THREADS (opmm_kernels.cu)
-constexpr size_t kMaxDynSmem = 200 * 1024;
+constexpr size_t kMaxDynSmem = 220 * 1024;
+// fit kernel picked by kernel_variant = 0 when variants 2/3 apply (1 otherwise)
+constexpr int kAutoVariant = 1;
 
 }  // namespace
 
@@ -275,8 +277,12 @@ size_t sim_smem(int precision, int32_t n_samples, int block, bool with_rel) {
   return (with_rel ? opmm::rel_bytes<float>(n_samples) : 0) + opmm::stash_bytes<float>(block);
 }
 
-size_t fit_smem(int precision, int32_t n_samples, int block) {
-  return sim_smem(precision, n_samples, block, true) + opmm::exp_tab_bytes();
+size_t fit_smem(int precision, int32_t n_samples, int block, int kernel_variant = 1) {
+  if (precision == OPMM_FP64)
+    return opmm::rel_bytes<double>(n_samples) + opmm::stash_bytes<double>(block, kernel_variant) +
+           opmm::exp_tab_bytes();
+  return opmm::rel_bytes<float>(n_samples) + opmm::stash_bytes<float>(block, kernel_variant) +
+         opmm::exp_tab_bytes();
 }
 
 opmm_status grid_for(opmm_handle* h, const void* fn, int block, size_t smem, int64_t work,
@@ -323,19 +329,36 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
   const int precision = opts ? opts->precision : OPMM_FP64;
   const int metric = opts ? opts->metric : OPMM_METRIC_L1;
   const int integ = opts ? opts->integrator : OPMM_INTEG_PROPAGATOR;
-  const int block = (opts && opts->block_size) ? opts->block_size : kDefaultBlock;
+  const int kv_opt = opts ? opts->kernel_variant : 0;
   if (!check_precision(precision)) return fail(OPMM_ERR_INVALID_ARG, "bad precision %d", precision);
   if (metric != 0 && metric != 1) return fail(OPMM_ERR_INVALID_ARG, "bad metric %d", metric);
   if (integ != 0 && integ != 1) return fail(OPMM_ERR_INVALID_ARG, "bad integrator %d", integ);
+  if (kv_opt < 0 || kv_opt > 3) return fail(OPMM_ERR_INVALID_ARG, "kernel_variant must be 0..3");
+  const opmm::SpaceDev space_dev = make_space(space);
+  // variants 2/3 need the propagator integrator and a search space whose
+  // candidates are all physical (no per-candidate penalty path)
+  const bool special_ok = integ == OPMM_INTEG_PROPAGATOR && space_dev.all_physical &&
+                          !(opts && opts->block_size);
+  if (kv_opt >= 2 && !special_ok)
+    return fail(OPMM_ERR_UNSUPPORTED, "kernel_variant %d needs the propagator integrator, a "
+                                      "physical search space and the default block size", kv_opt);
+  const int kv = kv_opt == 0 ? (special_ok ? kAutoVariant : 1) : kv_opt;
+  const bool two = kv == 2, three = kv == 3;
+  const int block = three ? opmm::FIT3_BLOCK : two ? opmm::FIT2_BLOCK
+                        : ((opts && opts->block_size) ? opts->block_size : kDefaultBlock);
   CKS(check_block(block));
   int64_t b = 0, e = n_candidates;
   if (shard) opmm_shard_range(n_candidates, h->rank, h->world, &b, &e);
   const int32_t ns = ctl->n_steps + 1;
-  const size_t smem = fit_smem(precision, ns, block);
+  const size_t smem = three ? opmm::fit3_smem(precision, ns) : fit_smem(precision, ns, block, two ? 2 : 1);
   if (smem > kMaxDynSmem) return fail(OPMM_ERR_INVALID_ARG, "trace too long for shared memory");
-  const void* fn = opmm::fit_kernel_ptr(precision, integ, metric);
+  const void* fn = three ? opmm::fit3_kernel_ptr(precision, metric)
+                         : two ? opmm::fit2_kernel_ptr(precision, metric)
+                               : opmm::fit_kernel_ptr(precision, integ, metric);
   int grid = 1;
-  CKS(grid_for(h, fn, block, smem, e - b, opts ? opts->grid_blocks : 0, &grid));
+  // fit3 work unit per block pass: 8 consumer warps x 32 candidates
+  const int64_t work = three ? (e - b + 255) / 256 * block : two ? (e - b + 1) / 2 : e - b;
+  CKS(grid_for(h, fn, block, smem, work, opts ? opts->grid_blocks : 0, &grid));
   if (e <= b) grid = 1;  // empty shard: one block reports "no candidate"
   const bool multi = shard && h->world > 1;
   CKS(ensure(h->partials, h->partials_cap, (size_t)grid * (size_t)(s_begin + S)));
@@ -349,7 +372,7 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
   a.rec = rec_dev;
   a.exp_tab = h->exp_tab;
   a.ctl = make_ctl(ctl);
-  a.space = make_space(space);
+  a.space = space_dev;
   a.amplitude = ctl->amplitude_deg;
   a.pw_default = ctl->pw_default_ms;
   a.sac_ctl = sacctl_dev;
@@ -368,8 +391,7 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
   for (int64_t s0 = 0; s0 < S; s0 += 65535) {
     const int64_t sn = (S - s0) < 65535 ? (S - s0) : 65535;
     a.sac_begin = s_begin + s0;
-    CK(opmm::launch_fit(a, precision, integ, metric, dim3(grid, (unsigned)sn), block, smem,
-                        h->stream));
+    CK(opmm::launch_fit(fn, a, dim3(grid, (unsigned)sn), block, smem, h->stream));
   }
   CKS(record_stop(h, h->stream));
   if (multi) {
@@ -447,6 +469,10 @@ opmm_status opmm_create(opmm_handle** out, int device) {
         cudaFuncSetAttribute(opmm::fit_kernel_ptr(p, i, m),
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDynSmem);
         cudaFuncSetAttribute(opmm::simscore_kernel_ptr(p, i, m),
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDynSmem);
+        cudaFuncSetAttribute(opmm::fit2_kernel_ptr(p, m),
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDynSmem);
+        cudaFuncSetAttribute(opmm::fit3_kernel_ptr(p, m),
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDynSmem);
         cudaFuncSetAttribute(opmm::simulate_kernel_ptr(p, i),
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDynSmem);

@@ -633,6 +633,124 @@ __device__ __forceinline__ T run_propagator(const Prop2<T>& pr, int32_t n_pulse,
 }
 
 // ----------------------------------------------------------------------------
+// Fit mode, C candidates per thread (C = 2): the same two-step recurrence as
+// run_propagator for C independent candidates interleaved in one thread, so
+// the scheduler sees 5C independent FMA chains per block (the fit kernel runs
+// 2 warps per scheduler with 255 registers; see fit2_kernel).  Each
+// candidate keeps its own lane parity, switch block and trace offset; the
+// warp's segments end at the minimum over all its lanes' candidates.
+// ----------------------------------------------------------------------------
+template <typename T, int METRIC, int C>
+__device__ __forceinline__ void run_propagator_multi(const Prop2<T> (&pr)[C],
+                                                     const int32_t (&n_pulse)[C], int32_t n_steps,
+                                                     const T* __restrict__ rel,
+                                                     T* __restrict__ stash, int stash_ld,
+                                                     T (&acc)[C]) {
+  using V2 = typename Vec2<T>::type;
+  V2* st2 = reinterpret_cast<V2*>(stash) + threadIdx.x;
+  T Q[C][4][4], R[C][4], A[C][4][2], cc[C][4], pa[C], pn[C], qa[C], qn[C], x0a[C], x0n[C], d0[C];
+  T th[C], om[C], xa[C], xn[C], fa[C], fn[C];
+  int32_t o[C], bs[C];
+  bool sw[C];
+  const int32_t nb = (n_steps + 1) / 2;
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    const PhaseProp2<T>& q = pr[c].ph[1];
+    V2* s = st2 + (c * 10) * stash_ld;
+    s[0 * stash_ld] = make_v2<T>(q.X2[0][0], q.X2[0][1]);
+    s[1 * stash_ld] = make_v2<T>(q.X2[1][0], q.X2[1][1]);
+    s[2 * stash_ld] = make_v2<T>(q.X2[2][0], q.X2[2][1]);
+    s[3 * stash_ld] = make_v2<T>(q.X2[3][0], q.X2[3][1]);
+    s[4 * stash_ld] = make_v2<T>(q.c2[0], q.c2[1]);
+    s[5 * stash_ld] = make_v2<T>(q.c2[2], q.c2[3]);
+    s[6 * stash_ld] = make_v2<T>(q.pf2[0], q.pf2[1]);
+    s[7 * stash_ld] = make_v2<T>(q.qf2[0], q.qf2[1]);
+    s[8 * stash_ld] = make_v2<T>(q.X0[0], q.X0[1]);
+    s[9 * stash_ld] = make_v2<T>(q.c0, T(0));
+    const PhaseProp2<T>& q0 = pr[c].ph[0];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) Q[c][r][j] = pr[c].P2[r][j];
+      R[c][r] = pr[c].P0[r];
+      A[c][r][0] = q0.X2[r][0];
+      A[c][r][1] = q0.X2[r][1];
+      cc[c][r] = q0.c2[r];
+    }
+    pa[c] = q0.pf2[0]; pn[c] = q0.pf2[1]; qa[c] = q0.qf2[0]; qn[c] = q0.qf2[1];
+    x0a[c] = q0.X0[0]; x0n[c] = q0.X0[1]; d0[c] = q0.c0;
+    sw[c] = n_pulse[c] > 0 && n_pulse[c] <= n_steps;
+    o[c] = sw[c] ? (n_pulse[c] & 1) : 0;
+    bs[c] = sw[c] ? (n_pulse[c] - o[c]) / 2 : nb;
+    th[c] = T(0); om[c] = T(0); xa[c] = T(0); xn[c] = T(0); fa[c] = T(0); fn[c] = T(0);
+    acc[c] = T(0);
+  }
+  auto swap_in = [&](int c) {
+    const V2* s = st2 + (c * 10) * stash_ld;
+    V2 v;
+    v = s[0 * stash_ld]; A[c][0][0] = v.x; A[c][0][1] = v.y;
+    v = s[1 * stash_ld]; A[c][1][0] = v.x; A[c][1][1] = v.y;
+    v = s[2 * stash_ld]; A[c][2][0] = v.x; A[c][2][1] = v.y;
+    v = s[3 * stash_ld]; A[c][3][0] = v.x; A[c][3][1] = v.y;
+    v = s[4 * stash_ld]; cc[c][0] = v.x; cc[c][1] = v.y;
+    v = s[5 * stash_ld]; cc[c][2] = v.x; cc[c][3] = v.y;
+    v = s[6 * stash_ld]; pa[c] = v.x; pn[c] = v.y;
+    v = s[7 * stash_ld]; qa[c] = v.x; qn[c] = v.y;
+    v = s[8 * stash_ld]; x0a[c] = v.x; x0n[c] = v.y;
+    v = s[9 * stash_ld]; d0[c] = v.x;
+  };
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    if (n_pulse[c] == 0 || (sw[c] && bs[c] == 0)) swap_in(c);
+    if (o[c]) {  // first pulse step from the zero deviation state
+      th[c] = pr[c].z1[0]; om[c] = pr[c].z1[1]; xa[c] = pr[c].z1[2]; xn[c] = pr[c].z1[3];
+      fa[c] = pr[c].f1[0]; fn[c] = pr[c].f1[1];
+      accumulate<METRIC>(acc[c], th[c] - rel[1]);
+    }
+  }
+  int32_t b = 0;
+  while (b < nb - 1) {
+    int32_t mine = nb - 1;
+#pragma unroll
+    for (int c = 0; c < C; ++c) mine = min(mine, bs[c] > b ? bs[c] : nb - 1);
+    const int32_t seg_end = __reduce_min_sync(0xffffffffu, mine);
+    for (; b < seg_end; ++b) {
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const T t1 = fma(R[c][0], th[c], fma(R[c][1], om[c], fma(R[c][2], xa[c], fma(R[c][3], xn[c],
+                     fma(x0a[c], fa[c], fma(x0n[c], fn[c], d0[c]))))));
+        T nz[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+          nz[r] = fma(Q[c][r][0], th[c], fma(Q[c][r][1], om[c], fma(Q[c][r][2], xa[c],
+                  fma(Q[c][r][3], xn[c], fma(A[c][r][0], fa[c], fma(A[c][r][1], fn[c], cc[c][r]))))));
+        fa[c] = fma(pa[c], fa[c], qa[c]);
+        fn[c] = fma(pn[c], fn[c], qn[c]);
+        th[c] = nz[0]; om[c] = nz[1]; xa[c] = nz[2]; xn[c] = nz[3];
+        const T* rl = rel + o[c] + 2 * b;
+        accumulate<METRIC>(acc[c], t1 - rl[1]);
+        accumulate<METRIC>(acc[c], th[c] - rl[2]);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < C; ++c)
+      if (b == bs[c]) swap_in(c);
+  }
+  if (nb >= 1) {
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      const int32_t k1 = o[c] + 2 * b + 1;
+      const T t1 = fma(R[c][0], th[c], fma(R[c][1], om[c], fma(R[c][2], xa[c], fma(R[c][3], xn[c],
+                   fma(x0a[c], fa[c], fma(x0n[c], fn[c], d0[c]))))));
+      const T t2 = fma(Q[c][0][0], th[c], fma(Q[c][0][1], om[c], fma(Q[c][0][2], xa[c],
+                   fma(Q[c][0][3], xn[c], fma(A[c][0][0], fa[c], fma(A[c][0][1], fn[c], cc[c][0]))))));
+      if (k1 <= n_steps) accumulate<METRIC>(acc[c], t1 - rel[k1]);
+      if (k1 + 1 <= n_steps) accumulate<METRIC>(acc[c], t2 - rel[k1 + 1]);
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
 // Integrate + fused score, RK4_STAGES form: the four classical stages
 // evaluated literally (SPEC D2), in deviation coordinates, K_i = h f(Y_i).
 // ----------------------------------------------------------------------------

@@ -17,8 +17,8 @@ __host__ __device__ constexpr size_t rel_bytes(int32_t n_samples) {
   return ((size_t)n_samples * sizeof(T) + 15) & ~(size_t)15;
 }
 template <typename T>
-__host__ __device__ constexpr size_t stash_bytes(int block) {
-  return (size_t)20 * block * sizeof(T);   // [10][block] vec2<T>
+__host__ __device__ constexpr size_t stash_bytes(int block, int cand_per_thread = 1) {
+  return (size_t)20 * cand_per_thread * block * sizeof(T);   // [C][10][block] vec2<T>
 }
 // fit kernel: trace, then the exp table (double2[EXP_TAB_N]), then the stash
 __host__ __device__ constexpr size_t exp_tab_bytes() { return (size_t)EXP_TAB_N * 16; }
@@ -72,12 +72,17 @@ struct ScoreArgs {
 };
 
 const void* fit_kernel_ptr(int precision, int integrator, int metric);
+const void* fit2_kernel_ptr(int precision, int metric);   // 2 candidates/thread, 256 threads
+constexpr int FIT2_BLOCK = 256;
+const void* fit3_kernel_ptr(int precision, int metric);   // warp-specialised, 384 threads
+constexpr int FIT3_BLOCK = 384;
+size_t fit3_smem(int precision, int32_t n_samples);
 const void* simscore_kernel_ptr(int precision, int integrator, int metric);
 const void* simulate_kernel_ptr(int precision, int integrator);
 const void* score_kernel_ptr(int precision, int metric);
 
-cudaError_t launch_fit(const FitArgs& a, int precision, int integrator, int metric, dim3 grid,
-                       int block, size_t smem, cudaStream_t st);
+cudaError_t launch_fit(const void* fn, const FitArgs& a, dim3 grid, int block, size_t smem,
+                       cudaStream_t st);
 cudaError_t launch_merge(const Partial* gathered, int world, const SpaceDev& sp, uint32_t saccade,
                          opmm_fit_result* out, const double2* tab, cudaStream_t st);
 cudaError_t launch_explicit(const void* fn, const ExplicitArgs& a, dim3 grid, int block, size_t smem,

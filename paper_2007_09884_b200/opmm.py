@@ -52,7 +52,7 @@ class SearchSpace(C.Structure):
 class FitOptions(C.Structure):
     _fields_ = [("precision", C.c_int32), ("metric", C.c_int32), ("integrator", C.c_int32),
                 ("block_size", C.c_int32), ("grid_blocks", C.c_int32), ("cpu_check", C.c_int32),
-                ("err_out", C.c_void_p)]
+                ("kernel_variant", C.c_int32), ("pad_", C.c_int32), ("err_out", C.c_void_p)]
 
 
 class FitResult(C.Structure):
@@ -144,9 +144,9 @@ def search_space(s) -> SearchSpace:
 
 
 def fit_options(precision=FP64, metric=METRIC_L1, integrator=INTEG_PROPAGATOR, block_size=0,
-                grid_blocks=0, cpu_check=1, err_out=None) -> FitOptions:
+                grid_blocks=0, cpu_check=1, err_out=None, kernel_variant=0) -> FitOptions:
     return FitOptions(precision, metric, integrator, block_size, grid_blocks, cpu_check,
-                      _ptr(err_out) if err_out is not None else None)
+                      kernel_variant, 0, _ptr(err_out) if err_out is not None else None)
 
 
 def _ptr(x):

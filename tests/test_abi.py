@@ -51,7 +51,7 @@ def test_struct_layouts_match_header(opmm):
     # the C side static_asserts the same sizes (opmm_api.cu)
     assert ctypes.sizeof(opmm.Control) == 40
     assert ctypes.sizeof(opmm.SearchSpace) == 400
-    assert ctypes.sizeof(opmm.FitOptions) == 32
+    assert ctypes.sizeof(opmm.FitOptions) == 40
     assert ctypes.sizeof(opmm.FitResult) == 184
     assert opmm.SearchSpace.levels.offset == 400 - 72
     assert opmm.FitResult.n_finite.offset == 168

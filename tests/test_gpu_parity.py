@@ -446,6 +446,25 @@ def test_fit_launch_config_invariance(opmm, h):
         assert np.array_equal(E, Eref, equal_nan=True)
 
 
+@pytest.mark.parametrize("precision", [0, 1])
+@pytest.mark.parametrize("variant", [2, 3])
+def test_fit_kernel_variants_identical(opmm, h, precision, variant):
+    """fit2 (two interleaved candidates per thread) and fit3 (warp-specialised
+    producer/consumer) give bit-identical per-candidate errors and argmin to
+    the default one-candidate-per-thread kernel (ragged N, several rounds)."""
+    ctl = W.Control()
+    rec = trace(ctl)
+    sp = W.paper_space()
+    n = 300001
+    r1, E1 = _fit(opmm, h, rec, ctl, sp, n, precision=precision, kernel_variant=1)
+    r2, E2 = _fit(opmm, h, rec, ctl, sp, n, precision=precision, kernel_variant=variant)
+    assert (r1["best_index"], r1["opt_err"], r1["n_finite"]) == (r2["best_index"], r2["opt_err"], r2["n_finite"])
+    assert np.array_equal(E1, E2)
+    with pytest.raises(opmm.OpmmError) as ei:   # variants 2/3 need the propagator
+        _fit(opmm, h, rec, ctl, sp, 10, kernel_variant=variant, integrator=opmm.INTEG_RK4_STAGES)
+    assert ei.value.status == opmm.ERR_UNSUPPORTED
+
+
 def test_fit_async_matches_sync(opmm, h):
     import ctypes
     ctl = W.Control()

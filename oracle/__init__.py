@@ -72,6 +72,16 @@ def lib():
         L.orc_fit.restype = C.c_int64
         L.orc_max_threads.argtypes = []
         L.orc_max_threads.restype = C.c_int
+        ip = C.POINTER(C.c_int)
+        L.orc_nm_test.argtypes = [C.c_int, C.c_int, dp, C.c_double, C.c_double, C.c_double, C.c_int,
+                                  dp, dp, ip, ip, ip]
+        L.orc_nm_test.restype = C.c_int
+        L.orc_test_fn.argtypes = [C.c_int, C.c_int, dp]
+        L.orc_test_fn.restype = C.c_double
+        L.orc_estimate_batch.argtypes = [dp, C.c_int64, C.c_int32, C.c_double, dp, dp, dp, C.c_int,
+                                         C.c_double, C.c_double, C.c_double, C.c_int, C.c_int,
+                                         dp, dp, i32p, i32p, i32p]
+        L.orc_estimate_batch.restype = C.c_int
         _lib = L
     return _lib
 
@@ -215,3 +225,53 @@ def fit(rec, ctl, space, begin: int, end: int, metric: int = 0, saccade: int = 0
 
 def max_threads() -> int:
     return lib().orc_max_threads()
+
+
+# ---------------------------------------------------------------- Nelder-Mead
+NM_SPHERE, NM_ROSENBROCK, NM_POWELL = 0, 1, 2
+
+
+def nm_test(fn_id: int, x0, init_scale=0.05, tol_x=1e-4, tol_f=1e-4, max_iter=None) -> dict:
+    """Serial Lagarias Nelder-Mead on a test function (SPEC acceptance 3)."""
+    x, px = _d(x0)
+    n = len(x)
+    xb = np.zeros(n)
+    fb, it, ev, why = C.c_double(), C.c_int(), C.c_int(), C.c_int()
+    lib().orc_nm_test(fn_id, n, px, init_scale, tol_x, tol_f, 200 * n if max_iter is None else max_iter,
+                      xb.ctypes.data_as(C.POINTER(C.c_double)), C.byref(fb), C.byref(it), C.byref(ev),
+                      C.byref(why))
+    return {"x": xb, "f": fb.value, "iterations": it.value, "func_evals": ev.value, "exit_reason": why.value}
+
+
+def test_fn(fn_id: int, x) -> float:
+    xx, px = _d(x)
+    return lib().orc_test_fn(fn_id, len(xx), px)
+
+
+def estimate_batch(recs, ctls, x0=None, metric=0, init_scale=0.05, tol_x=1e-4, tol_f=1e-4,
+                   max_iter=None, nthreads=1) -> dict:
+    """Nelder-Mead OPC estimation of S saccades (SPEC estimate_batch), each
+    from x0 (default Table 1 with PW NaN -> the saccade's pw_default)."""
+    recs = np.ascontiguousarray(recs, dtype=np.float64)
+    S, ns = recs.shape
+    c0 = ctls[0]
+    assert ns == c0.n_steps + 1
+    amp = np.array([c.amplitude_deg for c in ctls], dtype=np.float64)
+    pwd = np.array([c.pw_default_ms for c in ctls], dtype=np.float64)
+    if x0 is None:
+        from workloads import TABLE1_DEFAULTS
+        x0 = np.array(TABLE1_DEFAULTS, dtype=np.float64)
+    x0 = np.ascontiguousarray(x0, dtype=np.float64)
+    xb = np.zeros((S, NPARAM))
+    fb = np.zeros(S)
+    it = np.zeros(S, dtype=np.int32)
+    ev = np.zeros(S, dtype=np.int32)
+    why = np.zeros(S, dtype=np.int32)
+    P = C.POINTER(C.c_double)
+    I32 = C.POINTER(C.c_int32)
+    lib().orc_estimate_batch(recs.ctypes.data_as(P), S, c0.n_steps, c0.dt_ms, amp.ctypes.data_as(P),
+                             pwd.ctypes.data_as(P), x0.ctypes.data_as(P), metric, init_scale, tol_x,
+                             tol_f, 200 * NPARAM if max_iter is None else max_iter, nthreads,
+                             xb.ctypes.data_as(P), fb.ctypes.data_as(P), it.ctypes.data_as(I32),
+                             ev.ctypes.data_as(I32), why.ctypes.data_as(I32))
+    return {"x": xb, "f": fb, "iterations": it, "func_evals": ev, "exit_reason": why}

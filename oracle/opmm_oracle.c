@@ -384,3 +384,217 @@ int orc_max_threads(void) {
   return 1;
 #endif
 }
+
+/* ======================================================================== */
+/* Nelder-Mead estimator: PAPER.md:243-255 (3.3), Alg. 1   */
+/* PAPER.md:300-339, "based on a serial implementation by Lagarias"         */
+/* (PAPER.md:248).  SPEC D9 (initial simplex), D10 (rho = 1,   */
+/* chi = 2, gamma = 0.5, sigma = 0.5), D11 (NaN -> worst),     */
+/* D13 (tol_x = tol_f = 1e-4, max_iterations = 200 n), D14     */
+/* (stable sort).  Exit when BOTH the max coordinate distance  */
+/* of the other vertices to the best <= tol_x AND the max |f_i - f_best| <= */
+/* tol_f, or after max_iter iterations.  Plain serial    */
+/* Lagarias steps: only the points the decision needs are evaluated.        */
+/* ======================================================================== */
+typedef double (*orc_objfn)(const double* x, void* ctx);
+
+static void orc_sort_simplex(int n, double* v, double* fv, double* tmp) {
+  /* stable insertion sort of n+1 vertices (rows of v, length n) by fv */
+  int i, j, k;
+  for (i = 1; i <= n; ++i) {
+    double f = fv[i];
+    for (k = 0; k < n; ++k) tmp[k] = v[i * n + k];
+    j = i - 1;
+    while (j >= 0 && fv[j] > f) {
+      fv[j + 1] = fv[j];
+      for (k = 0; k < n; ++k) v[(j + 1) * n + k] = v[j * n + k];
+      --j;
+    }
+    fv[j + 1] = f;
+    for (k = 0; k < n; ++k) v[(j + 1) * n + k] = tmp[k];
+  }
+}
+
+static double orc_nm_eval(orc_objfn f, void* ctx, const double* x) {
+  double y = f(x, ctx);
+  return isnan(y) ? INFINITY : y; /* D11 */
+}
+
+int orc_nelder_mead(orc_objfn f, void* ctx, int n, const double* x0, double init_scale,
+                    double tol_x, double tol_f, int max_iter, double* x_best, double* f_best,
+                    int* iterations, int* func_evals, int* exit_reason) {
+  const double rho = 1.0, chi = 2.0, psi = 0.5, sigma = 0.5;
+  double* v = (double*)malloc(sizeof(double) * (size_t)(n + 1) * (size_t)n);
+  double* fv = (double*)malloc(sizeof(double) * (size_t)(n + 1));
+  double* xbar = (double*)malloc(sizeof(double) * (size_t)n);
+  double* xr = (double*)malloc(sizeof(double) * (size_t)n);
+  double* xe = (double*)malloc(sizeof(double) * (size_t)n);
+  double* tmp = (double*)malloc(sizeof(double) * (size_t)n);
+  int i, j, itercount, evals, reason = 1;
+  /* initial simplex (D9): vertex 0 = x0; vertex j+1 = x0 with coordinate j
+     scaled by (1 + scale), or set to scale * 0.00025 when it is zero */
+  for (j = 0; j < n; ++j) v[j] = x0[j];
+  fv[0] = orc_nm_eval(f, ctx, v);
+  for (i = 1; i <= n; ++i) {
+    for (j = 0; j < n; ++j) v[i * n + j] = x0[j];
+    if (x0[i - 1] != 0.0) v[i * n + i - 1] = (1.0 + init_scale) * x0[i - 1];
+    else v[i * n + i - 1] = init_scale * 0.00025;
+    fv[i] = orc_nm_eval(f, ctx, v + i * n);
+  }
+  orc_sort_simplex(n, v, fv, tmp);
+  itercount = 1;
+  evals = n + 1;
+  while (itercount < max_iter) {
+    double dfmax = 0.0, dxmax = 0.0;
+    int shrink = 0;
+    for (i = 1; i <= n; ++i) {
+      double df = fabs(fv[i] - fv[0]);
+      if (!(df <= dfmax)) dfmax = df; /* NaN/inf propagate as "not converged" */
+      for (j = 0; j < n; ++j) {
+        double dx = fabs(v[i * n + j] - v[j]);
+        if (dx > dxmax) dxmax = dx;
+      }
+    }
+    if (dfmax <= tol_f && dxmax <= tol_x) { reason = 0; break; }
+    /* centroid of the n best vertices */
+    for (j = 0; j < n; ++j) {
+      double s = 0.0;
+      for (i = 0; i < n; ++i) s += v[i * n + j];
+      xbar[j] = s / (double)n;
+    }
+    for (j = 0; j < n; ++j) xr[j] = (1.0 + rho) * xbar[j] - rho * v[n * n + j];
+    {
+      double fxr = orc_nm_eval(f, ctx, xr);
+      evals++;
+      if (fxr < fv[0]) {
+        double fxe;
+        for (j = 0; j < n; ++j) xe[j] = (1.0 + rho * chi) * xbar[j] - rho * chi * v[n * n + j];
+        fxe = orc_nm_eval(f, ctx, xe);
+        evals++;
+        if (fxe < fxr) { for (j = 0; j < n; ++j) v[n * n + j] = xe[j]; fv[n] = fxe; }
+        else { for (j = 0; j < n; ++j) v[n * n + j] = xr[j]; fv[n] = fxr; }
+      } else if (fxr < fv[n - 1]) {
+        for (j = 0; j < n; ++j) v[n * n + j] = xr[j];
+        fv[n] = fxr;
+      } else if (fxr < fv[n]) { /* outside contraction */
+        double fxc;
+        for (j = 0; j < n; ++j) xe[j] = (1.0 + psi * rho) * xbar[j] - psi * rho * v[n * n + j];
+        fxc = orc_nm_eval(f, ctx, xe);
+        evals++;
+        if (fxc <= fxr) { for (j = 0; j < n; ++j) v[n * n + j] = xe[j]; fv[n] = fxc; }
+        else shrink = 1;
+      } else { /* inside contraction */
+        double fxcc;
+        for (j = 0; j < n; ++j) xe[j] = (1.0 - psi) * xbar[j] + psi * v[n * n + j];
+        fxcc = orc_nm_eval(f, ctx, xe);
+        evals++;
+        if (fxcc < fv[n]) { for (j = 0; j < n; ++j) v[n * n + j] = xe[j]; fv[n] = fxcc; }
+        else shrink = 1;
+      }
+      if (shrink) {
+        for (i = 1; i <= n; ++i) {
+          for (j = 0; j < n; ++j) v[i * n + j] = v[j] + sigma * (v[i * n + j] - v[j]);
+          fv[i] = orc_nm_eval(f, ctx, v + i * n);
+        }
+        evals += n;
+      }
+    }
+    orc_sort_simplex(n, v, fv, tmp);
+    itercount++;
+  }
+  for (j = 0; j < n; ++j) x_best[j] = v[j];
+  *f_best = fv[0];
+  *iterations = itercount;
+  *func_evals = evals;
+  *exit_reason = reason;
+  free(v); free(fv); free(xbar); free(xr); free(xe); free(tmp);
+  return 0;
+}
+
+/* Test objectives (SPEC acceptance 3). */
+static double orc_fn_sphere(const double* x, void* ctx) {
+  int n = *(const int*)ctx, i;
+  double s = 0.0;
+  for (i = 0; i < n; ++i) s += x[i] * x[i];
+  return s;
+}
+static double orc_fn_rosenbrock(const double* x, void* ctx) {
+  int n = *(const int*)ctx, i;
+  double s = 0.0;
+  for (i = 0; i + 1 < n; ++i) {
+    double a = x[i + 1] - x[i] * x[i], b = 1.0 - x[i];
+    s += 100.0 * (a * a) + b * b;
+  }
+  return s;
+}
+static double orc_fn_powell(const double* x, void* ctx) {
+  int n = *(const int*)ctx, i;
+  double s = 0.0;
+  for (i = 0; i + 3 < n; i += 4) {
+    double a = x[i] + 10.0 * x[i + 1], b = x[i + 2] - x[i + 3];
+    double c = x[i + 1] - 2.0 * x[i + 2], d = x[i] - x[i + 3];
+    s += a * a + 5.0 * (b * b) + (c * c) * (c * c) + 10.0 * ((d * d) * (d * d));
+  }
+  return s;
+}
+
+int orc_nm_test(int fn_id, int n, const double* x0, double init_scale, double tol_x, double tol_f,
+                int max_iter, double* x_best, double* f_best, int* iterations, int* func_evals,
+                int* exit_reason) {
+  orc_objfn f = fn_id == 0 ? orc_fn_sphere : fn_id == 1 ? orc_fn_rosenbrock : orc_fn_powell;
+  return orc_nelder_mead(f, &n, n, x0, init_scale, tol_x, tol_f, max_iter, x_best, f_best,
+                         iterations, func_evals, exit_reason);
+}
+
+double orc_test_fn(int fn_id, int n, const double* x) {
+  orc_objfn f = fn_id == 0 ? orc_fn_sphere : fn_id == 1 ? orc_fn_rosenbrock : orc_fn_powell;
+  return f(x, &n);
+}
+
+/* Plant objective for the estimator: E(x) of the full 18-parameter OPC
+   against one relativized trace (penalty / +inf rules as orc_objective). */
+typedef struct {
+  const double* rel;
+  int32_t n_steps;
+  double dt_ms, Aprime, pw_default_ms;
+  int metric;
+  double* buf;
+} orc_plant_ctx;
+
+static double orc_fn_plant(const double* x, void* ctx) {
+  orc_plant_ctx* c = (orc_plant_ctx*)ctx;
+  return orc_objective(x, c->rel, c->n_steps, c->dt_ms, c->Aprime, c->pw_default_ms, c->metric,
+                       c->buf);
+}
+
+/* estimate_batch (Alg. 1): saccade s is fitted from x0
+   (Table 1 defaults; PW NaN -> the saccade's pw_default) independently of the
+   others; results in input order, identical for any nthreads (D12). */
+int orc_estimate_batch(const double* rec, int64_t S, int32_t n_steps, double dt_ms,
+                       const double* amplitude, const double* pw_default, const double* x0,
+                       int metric, double init_scale, double tol_x, double tol_f, int max_iter,
+                       int nthreads, double* x_best, double* f_best, int32_t* iterations,
+                       int32_t* func_evals, int32_t* exit_reason) {
+  int64_t s;
+  if (nthreads < 1) nthreads = 1;
+#ifdef _OPENMP
+#pragma omp parallel for num_threads(nthreads) schedule(dynamic, 1)
+#endif
+  for (s = 0; s < S; ++s) {
+    double* rel = (double*)malloc(sizeof(double) * (size_t)(n_steps + 1));
+    double* buf = (double*)malloc(sizeof(double) * (size_t)(n_steps + 1));
+    double sgn, Ap, xs[ORC_NP];
+    int it, ev, why, d;
+    orc_plant_ctx ctx;
+    orc_relativize(rec + s * (int64_t)(n_steps + 1), n_steps + 1, amplitude[s], rel, &sgn, &Ap);
+    for (d = 0; d < ORC_NP; ++d) xs[d] = x0[d];
+    if (isnan(xs[P_PW])) xs[P_PW] = pw_default[s];
+    ctx.rel = rel; ctx.n_steps = n_steps; ctx.dt_ms = dt_ms; ctx.Aprime = Ap;
+    ctx.pw_default_ms = pw_default[s]; ctx.metric = metric; ctx.buf = buf;
+    orc_nelder_mead(orc_fn_plant, &ctx, ORC_NP, xs, init_scale, tol_x, tol_f, max_iter,
+                    x_best + s * ORC_NP, f_best + s, &it, &ev, &why);
+    iterations[s] = it; func_evals[s] = ev; exit_reason[s] = why;
+    free(rel); free(buf);
+  }
+  return 0;
+}

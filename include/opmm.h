@@ -228,6 +228,63 @@ opmm_status opmm_fit_batch(opmm_handle* h, const double* recorded, int64_t S,
                            const opmm_control* ctl, const opmm_search_space* space,
                            int64_t n_per, const opmm_fit_options* opts, opmm_fit_result* out);
 
+/* ---- Nelder-Mead estimator ------------------------------ */
+/* The paper's own estimator (Alg. 1): a
+ * parallel Nelder-Mead after Lagarias -- all simplex
+ * transformations evaluated simultaneously, the simplex sorted
+ * every iteration, exit when BOTH the max coordinate distance
+ * to the best vertex <= tol_x AND the max |f_i - f_best| <= tol_f
+ * (PAPER.md:252-255), or after max_iter iterations.  Coefficients rho = 1,
+ * chi = 2, gamma = 0.5, sigma = 0.5 (SPEC D10); initial simplex: each
+ * coordinate scaled by (1 + init_scale), zero coordinates set to
+ * init_scale * 0.00025 (SPEC D9); stable sort (SPEC D14).  One warp per
+ * problem; the iterates are the serial algorithm's. */
+typedef enum {
+  OPMM_NM_OBJ_PROPAGATOR = 0,   /* plant error, fit-path propagator (fast)          */
+  OPMM_NM_OBJ_RK4_STAGES = 1,   /* plant error, literal four-stage RK4              */
+  OPMM_NM_OBJ_REFERENCE = 2     /* plant error in the RK4 definition's operation
+                                   order, explicitly rounded fp64 (reproducible)    */
+} opmm_nm_objective;
+
+typedef struct {
+  int32_t precision;     /* OPMM_FP64 / OPMM_FP32 (REFERENCE is always fp64)       */
+  int32_t objective;     /* opmm_nm_objective                                      */
+  int32_t metric;        /* opmm_metric                                            */
+  int32_t max_iter;      /* 0 = 200 * dim (SPEC D13)                                */
+  double tol_x;          /* 0 = 1e-4 (SPEC D13)                                     */
+  double tol_f;          /* 0 = 1e-4                                                */
+  double init_scale;     /* 0 = 0.05 (SPEC D9)                                      */
+  int32_t cpu_check;     /* 1 = fill cpu_check (plant objectives)                  */
+  int32_t pad_;
+} opmm_nm_options;
+
+typedef struct {
+  double x[OPMM_NPARAM]; /* best vertex (first dim entries used)                   */
+  double f_best;         /* objective at x                                          */
+  double cpu_check;      /* serial host fp64 re-score of x (plant objectives)      */
+  int32_t iterations;    /* iterations, counted as the serial algorithm counts them */
+  int32_t func_evals;    /* objective evaluations the serial algorithm needs        */
+  int32_t gpu_evals;     /* evaluations performed (all points every iteration)      */
+  int32_t exit_reason;   /* 0 = tolerances met, 1 = max_iter                        */
+} opmm_nm_result;
+
+/* Estimate the 18-parameter OPC of S saccades independently (SPEC
+ * estimate_batch).  recorded: HOST or DEVICE [S][n_steps+1];
+ * ctl: HOST [S] (shared dt/n_steps); x0: HOST [18] start vector or NULL for
+ * the Table 1 defaults; a NaN PW starts at the saccade's
+ * pw_default_ms.  out: HOST [S].  On an NCCL handle rank r estimates only
+ * saccades [floor(rS/R), floor((r+1)S/R)) (independent problems, no
+ * collective) and fills only those entries.  Synchronous. */
+opmm_status opmm_estimate_batch(opmm_handle* h, const double* recorded, int64_t S,
+                                const opmm_control* ctl, const double* x0,
+                                const opmm_nm_options* opts, opmm_nm_result* out);
+
+/* The same Nelder-Mead engine on the SPEC acceptance-3 test functions
+ * (fn_id 0 sphere, 1 Rosenbrock, 2 Powell quartic; dim 1..18): S problems
+ * with start points HOST x0[S][dim]; out HOST [S].  Synchronous. */
+opmm_status opmm_nm_minimize_test(opmm_handle* h, int32_t fn_id, int32_t dim, const double* x0,
+                                  int64_t S, const opmm_nm_options* opts, opmm_nm_result* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -19,7 +19,7 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 BUILD = os.path.join(ROOT, "build")
 LIB = os.path.join(PKG, "libopmm.so")
-SOURCES = ["opmm_api.cu", "opmm_kernels.cu", "opmm_cpu_check.cpp"]
+SOURCES = ["opmm_api.cu", "opmm_kernels.cu", "opmm_nm.cu", "opmm_cpu_check.cpp"]
 HEADERS = ["opmm_device.cuh", "opmm_internal.h", "opmm_cpu_check.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "nvcc")

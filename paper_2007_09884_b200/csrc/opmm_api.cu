@@ -26,6 +26,8 @@ static_assert(sizeof(opmm_search_space) == 400, "opmm_search_space layout");
 static_assert(sizeof(opmm_fit_options) == 40, "opmm_fit_options layout");
 static_assert(sizeof(opmm_fit_result) == 184, "opmm_fit_result layout");
 static_assert(sizeof(Partial) == 32, "Partial layout");
+static_assert(sizeof(opmm_nm_options) == 48, "opmm_nm_options layout");
+static_assert(sizeof(opmm_nm_result) == 176, "opmm_nm_result layout");
 
 namespace {
 
@@ -122,6 +124,13 @@ struct opmm_handle {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   bool timed = false;
   double2* exp_tab = nullptr;   // exp(j/64) double-double table (generator)
+  // Nelder-Mead workspace
+  double* nm_x0 = nullptr;
+  size_t nm_x0_cap = 0;
+  double* nm_xbest = nullptr;
+  size_t nm_xbest_cap = 0;
+  opmm::NmOut* nm_out = nullptr;
+  size_t nm_out_cap = 0;
 };
 
 namespace {
@@ -422,6 +431,95 @@ opmm_status stage_rec(opmm_handle* h, const double* recorded, size_t count, cons
   return OPMM_OK;
 }
 
+// Table 1 defaults; PW is the per-saccade placeholder
+// "saccade duration - 6 ms", NaN here -> pw_default_ms.
+const double kTable1Defaults[OPMM_NPARAM] = {2.5,  2.5, 1.2, 1.2,  0.046, 0.022, 0.06,
+                                             0.8,  0.5, 0.000043, 11.7, 2.4, 2.0, 1.9,
+                                             14.0, 55.0, 0.5, NAN};
+
+struct NmConfig {
+  int obj, precision, metric, max_iter, cpu_check;
+  double tol_x, tol_f, init_scale;
+};
+
+opmm_status nm_config(const opmm_nm_options* o, int dim, bool plant, NmConfig* c) {
+  c->obj = plant ? (o ? o->objective : OPMM_NM_OBJ_PROPAGATOR) : 3;
+  c->precision = o ? o->precision : OPMM_FP64;
+  c->metric = o ? o->metric : OPMM_METRIC_L1;
+  c->max_iter = (o && o->max_iter > 0) ? o->max_iter : 200 * dim;
+  c->tol_x = (o && o->tol_x > 0.0) ? o->tol_x : 1e-4;
+  c->tol_f = (o && o->tol_f > 0.0) ? o->tol_f : 1e-4;
+  c->init_scale = (o && o->init_scale != 0.0) ? o->init_scale : 0.05;
+  c->cpu_check = o ? o->cpu_check : 1;
+  if (plant && (c->obj < 0 || c->obj > 2)) return fail(OPMM_ERR_INVALID_ARG, "bad NM objective");
+  if (!check_precision(c->precision)) return fail(OPMM_ERR_INVALID_ARG, "bad precision");
+  if (c->metric != 0 && c->metric != 1) return fail(OPMM_ERR_INVALID_ARG, "bad metric");
+  if (c->obj >= 2) c->precision = OPMM_FP64;
+  if (o && o->max_iter < 0) return fail(OPMM_ERR_INVALID_ARG, "max_iter < 0");
+  if (!(c->tol_x > 0.0) || !(c->tol_f > 0.0) || !is_finite(c->init_scale))
+    return fail(OPMM_ERR_INVALID_ARG, "bad NM tolerances");
+  return OPMM_OK;
+}
+
+opmm_status nm_launch(opmm_handle* h, const NmConfig& c, const double* rec_dev,
+                      const double* sacctl_dev, const opmm_control* ctl0, int64_t x0_ld, int dim,
+                      int fn_id, int64_t pb, int64_t pe) {
+  const int32_t ns = ctl0 ? ctl0->n_steps + 1 : 1;
+  const size_t smem = opmm::nm_smem(c.precision, c.obj, ns);
+  if (smem > kMaxDynSmem) return fail(OPMM_ERR_INVALID_ARG, "trace too long for the NM kernel");
+  opmm::NmArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.rec = rec_dev;
+  a.sac_ctl = sacctl_dev;
+  if (ctl0) a.ctl = make_ctl(ctl0);
+  a.x0 = h->nm_x0;
+  a.x0_ld = x0_ld;
+  a.x_best = h->nm_xbest;
+  a.x_ld = OPMM_NPARAM;
+  a.out = h->nm_out;
+  a.prob_begin = pb;
+  a.prob_end = pe;
+  a.dim = dim;
+  a.fn_id = fn_id;
+  a.max_iter = c.max_iter;
+  a.tol_x = c.tol_x;
+  a.tol_f = c.tol_f;
+  a.init_scale = c.init_scale;
+  const int per = opmm::nm_problems_per_block();
+  const int64_t grid = (pe - pb + per - 1) / per;
+  if (grid == 0) return OPMM_OK;
+  if (grid > 0x7fffffff) return fail(OPMM_ERR_INVALID_ARG, "too many problems");
+  CKS(record_start(h, h->stream));
+  CK(opmm::launch_nm(opmm::nm_kernel_ptr(c.precision, c.obj, c.metric), a, (int)grid, smem,
+                     h->stream));
+  CKS(record_stop(h, h->stream));
+  return OPMM_OK;
+}
+
+opmm_status nm_collect(opmm_handle* h, int64_t pb, int64_t pe, int dim, opmm_nm_result* out) {
+  const int64_t S = pe;
+  std::string xb((size_t)S * OPMM_NPARAM * sizeof(double), '\0');
+  std::string ob((size_t)S * sizeof(opmm::NmOut), '\0');
+  CK(cudaMemcpyAsync(&xb[0], h->nm_xbest, xb.size(), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaMemcpyAsync(&ob[0], h->nm_out, ob.size(), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  const double* xs = reinterpret_cast<const double*>(xb.data());
+  const opmm::NmOut* os = reinterpret_cast<const opmm::NmOut*>(ob.data());
+  for (int64_t s = pb; s < pe; ++s) {
+    opmm_nm_result r;
+    std::memset(&r, 0, sizeof(r));
+    for (int d = 0; d < OPMM_NPARAM; ++d) r.x[d] = d < dim ? xs[s * OPMM_NPARAM + d] : NAN;
+    r.f_best = os[s].f_best;
+    r.cpu_check = NAN;
+    r.iterations = os[s].iterations;
+    r.func_evals = os[s].func_evals;
+    r.gpu_evals = os[s].gpu_evals;
+    r.exit_reason = os[s].exit_reason;
+    out[s] = r;
+  }
+  return OPMM_OK;
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -478,6 +576,9 @@ opmm_status opmm_create(opmm_handle** out, int device) {
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDynSmem);
         cudaFuncSetAttribute(opmm::score_kernel_ptr(p, m),
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDynSmem);
+        for (int obj = 0; obj < 4; ++obj)
+          cudaFuncSetAttribute(opmm::nm_kernel_ptr(p, obj, m),
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDynSmem);
       }
   cudaGetLastError();
   {
@@ -555,6 +656,9 @@ opmm_status opmm_destroy(opmm_handle* h) {
   cudaFree(h->gathered);
   cudaFree(h->result);
   cudaFree(h->exp_tab);
+  cudaFree(h->nm_x0);
+  cudaFree(h->nm_xbest);
+  cudaFree(h->nm_out);
   if (h->result_host) cudaFreeHost(h->result_host);
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
@@ -826,6 +930,87 @@ opmm_status opmm_fit_batch(opmm_handle* h, const double* recorded, int64_t S,
     out[sb + j] = r;
   }
   return OPMM_OK;
+}
+
+opmm_status opmm_estimate_batch(opmm_handle* h, const double* recorded, int64_t S,
+                                const opmm_control* ctl, const double* x0,
+                                const opmm_nm_options* opts, opmm_nm_result* out) {
+  CKS(check_handle(h));
+  if (S < 0) return fail(OPMM_ERR_INVALID_ARG, "S < 0");
+  if (S == 0) return OPMM_OK;
+  if (!recorded || !ctl || !out) return fail(OPMM_ERR_INVALID_ARG, "NULL argument");
+  for (int64_t s = 0; s < S; ++s) {
+    CKS(validate_control(ctl + s, false));
+    if (ctl[s].dt_ms != ctl[0].dt_ms || ctl[s].n_steps != ctl[0].n_steps)
+      return fail(OPMM_ERR_INVALID_ARG, "all saccades of a batch share dt_ms and n_steps");
+  }
+  NmConfig c;
+  CKS(nm_config(opts, OPMM_NPARAM, true, &c));
+  double xs[OPMM_NPARAM];
+  for (int d = 0; d < OPMM_NPARAM; ++d) {
+    xs[d] = x0 ? x0[d] : kTable1Defaults[d];
+    if (!is_finite(xs[d]) && !(d == OPMM_P_PW && std::isnan(xs[d])))
+      return fail(OPMM_ERR_INVALID_ARG, "x0[%d] is not finite", d);
+  }
+  int64_t sb = 0, se = S;
+  opmm_shard_range(S, h->rank, h->world, &sb, &se);
+  const size_t ns = (size_t)ctl[0].n_steps + 1;
+  const double* rec_dev = nullptr;
+  if (is_device_ptr(recorded)) {
+    rec_dev = recorded;
+  } else {
+    for (size_t k = 0; k < (size_t)S * ns; ++k)
+      if (!is_finite(recorded[k])) return fail(OPMM_ERR_INVALID_ARG, "recorded sample not finite");
+    CKS(ensure(h->rec, h->rec_cap, (size_t)S * ns));
+    CK(cudaMemcpyAsync(h->rec, recorded, (size_t)S * ns * sizeof(double), cudaMemcpyHostToDevice,
+                       h->stream));
+    rec_dev = h->rec;
+  }
+  std::string sc((size_t)S * 2 * sizeof(double), '\0');
+  double* scp = reinterpret_cast<double*>(&sc[0]);
+  for (int64_t s = 0; s < S; ++s) {
+    scp[2 * s] = ctl[s].amplitude_deg;
+    scp[2 * s + 1] = ctl[s].pw_default_ms;
+  }
+  CKS(ensure(h->sacctl, h->sacctl_cap, (size_t)S * 2));
+  CK(cudaMemcpyAsync(h->sacctl, scp, sc.size(), cudaMemcpyHostToDevice, h->stream));
+  CKS(ensure(h->nm_x0, h->nm_x0_cap, OPMM_NPARAM));
+  CK(cudaMemcpyAsync(h->nm_x0, xs, sizeof(xs), cudaMemcpyHostToDevice, h->stream));
+  CKS(ensure(h->nm_xbest, h->nm_xbest_cap, (size_t)S * OPMM_NPARAM));
+  CKS(ensure(h->nm_out, h->nm_out_cap, (size_t)S));
+  CK(cudaStreamSynchronize(h->stream));   // host staging buffers above are temporaries
+  CKS(nm_launch(h, c, rec_dev, h->sacctl, ctl, 0, OPMM_NPARAM, 0, sb, se));
+  CKS(nm_collect(h, sb, se, OPMM_NPARAM, out));
+  if (c.cpu_check) {
+    std::string tmp;
+    const double* rec_host = recorded;
+    if (rec_dev == recorded) {
+      tmp.resize((size_t)S * ns * sizeof(double));
+      CK(cudaMemcpy(&tmp[0], recorded, tmp.size(), cudaMemcpyDeviceToHost));
+      rec_host = reinterpret_cast<const double*>(tmp.data());
+    }
+    for (int64_t s = sb; s < se; ++s)
+      out[s].cpu_check = opmm::cpu_check_score(out[s].x, rec_host + (size_t)s * ns, ctl + s, c.metric);
+  }
+  return OPMM_OK;
+}
+
+opmm_status opmm_nm_minimize_test(opmm_handle* h, int32_t fn_id, int32_t dim, const double* x0,
+                                  int64_t S, const opmm_nm_options* opts, opmm_nm_result* out) {
+  CKS(check_handle(h));
+  if (fn_id < 0 || fn_id > 2) return fail(OPMM_ERR_INVALID_ARG, "fn_id must be 0, 1 or 2");
+  if (dim < 1 || dim > OPMM_NPARAM) return fail(OPMM_ERR_INVALID_ARG, "dim must be in [1, 18]");
+  if (S < 0) return fail(OPMM_ERR_INVALID_ARG, "S < 0");
+  if (S == 0) return OPMM_OK;
+  if (!x0 || !out) return fail(OPMM_ERR_INVALID_ARG, "NULL argument");
+  NmConfig c;
+  CKS(nm_config(opts, dim, false, &c));
+  CKS(ensure(h->nm_x0, h->nm_x0_cap, (size_t)S * dim));
+  CK(cudaMemcpy(h->nm_x0, x0, (size_t)S * dim * sizeof(double), cudaMemcpyHostToDevice));
+  CKS(ensure(h->nm_xbest, h->nm_xbest_cap, (size_t)S * OPMM_NPARAM));
+  CKS(ensure(h->nm_out, h->nm_out_cap, (size_t)S));
+  CKS(nm_launch(h, c, nullptr, nullptr, nullptr, dim, dim, fn_id, 0, S));
+  return nm_collect(h, 0, S, dim, out);
 }
 
 }  // extern "C"

@@ -801,6 +801,43 @@ __device__ __forceinline__ T run_rk4_stages(const Setup& s, int32_t n_steps,
   return acc;
 }
 
+// ---------------------------------------------------------------------------
+// Evaluate one candidate: physical check, setup, integrate + fused score.
+// ---------------------------------------------------------------------------
+template <typename T, int INTEG, int METRIC, bool TRAJ>
+__device__ __forceinline__ double evaluate(const double p[NP], const CtlDev& c, double Aprime,
+                                           double pw_default, const T* rel, T* traj,
+                                           int64_t ld_out, double sgn, uint8_t* status,
+                                           T* stash, bool check_physical = true) {
+  // generated candidates skip the check when the host proved the whole
+  // search space physical (SpaceDev::all_physical).  A non-physical candidate
+  // still runs the (meaningless) recurrence before its penalty is returned:
+  // the segmented loop's warp reductions need every lane of the warp.
+  const double pen = check_physical ? physical_penalty(p) : 0.0;
+  Setup s;
+  make_setup(p, c.dt_ms, c.h, c.n_steps, Aprime, pw_default, s);
+  T acc;
+  if (INTEG == 0) {
+    Prop2<T> pr;
+    make_prop<T>(s, pr);
+    acc = run_propagator<T, METRIC, TRAJ>(pr, s.n_pulse, c.n_steps, rel, traj, ld_out,
+                                          (T)c.theta0, (T)sgn, stash, blockDim.x);
+  } else {
+    acc = run_rk4_stages<T, METRIC, TRAJ>(s, c.n_steps, rel, traj, ld_out, (T)c.theta0, (T)sgn);
+  }
+  if (pen != 0.0) {
+    if (TRAJ) {
+      const T nanv = (T)__longlong_as_double(0x7ff8000000000000LL);
+      for (int32_t k = 0; k <= c.n_steps; ++k) traj[(int64_t)k * ld_out] = nanv;
+    }
+    if (status) *status = 1;
+    return pen;
+  }
+  const double E = finish_error<METRIC>(acc, c.n_steps + 1);
+  if (status) *status = isinf(E) ? 2 : 0;
+  return E;
+}
+
 // ----------------------------------------------------------------------------
 // (E, index) lexicographic order (reading Q12).
 // ----------------------------------------------------------------------------

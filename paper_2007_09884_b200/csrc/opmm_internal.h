@@ -71,6 +71,32 @@ struct ScoreArgs {
   double* err;
 };
 
+// Batched Nelder-Mead (opmm_nm.cu)
+struct NmOut {
+  double f_best;
+  int32_t iterations, func_evals, gpu_evals, exit_reason;
+};
+
+struct NmArgs {
+  const double* rec;        // device [S][n_steps+1] (plant objectives)
+  const double* sac_ctl;    // device [S][2] = (amplitude, pw_default)
+  CtlDev ctl;
+  const double* x0;         // device, problem p at x0 + p * x0_ld
+  int64_t x0_ld;
+  double* x_best;           // device [S][x_ld]
+  int64_t x_ld;
+  NmOut* out;               // device [S]
+  int64_t prob_begin, prob_end;
+  int32_t dim, fn_id, max_iter, pad_;
+  double tol_x, tol_f, init_scale;
+};
+
+const void* nm_kernel_ptr(int precision, int obj, int metric);
+size_t nm_smem(int precision, int obj, int32_t n_samples);
+int nm_problems_per_block();
+int nm_threads();
+cudaError_t launch_nm(const void* fn, const NmArgs& a, int grid, size_t smem, cudaStream_t st);
+
 const void* fit_kernel_ptr(int precision, int integrator, int metric);
 const void* fit2_kernel_ptr(int precision, int metric);   // 2 candidates/thread, 256 threads
 constexpr int FIT2_BLOCK = 256;

@@ -1,0 +1,395 @@
+// opmm_nm.cu -- batched parallel Nelder-Mead OPC estimation.
+//
+// The paper's own estimator: "an original parallel implementation of
+// Nelder-Mead based on a serial implementation by Lagarias";
+// "all of the simplex transformations are calculated simultaneously"
+// (PAPER.md:250), "sorted for accuracy at every iteration",
+// dual tolerance exit; Alg. 1 runs one
+// optimisation task per saccade.  SPEC D9/D10/D13/D14 fix the initial
+// simplex, coefficients, defaults and the stable sort.
+//
+// B200 mapping: one warp per problem (saccade).  Each iteration the warp
+// builds ALL candidate points at once -- reflection, expansion, outside and
+// inside contraction and the n shrink points (n + 4 <= 22 points for the
+// 18-parameter OPC) -- evaluates one point per lane in parallel, then applies
+// the Lagarias decision step and a stable rank sort of the simplex in shared
+// memory.  The decision uses only the values the serial algorithm would
+// compute, so the iterates are the serial algorithm's; the simplex
+// arithmetic uses explicitly rounded fp64 operations (no FMA contraction).
+//
+// Objectives: the plant error with the propagator or the literal four-stage
+// integrator (the fit path's evaluate()), the plant error in the RK4
+// definition's reference operation order (opmm_ref_objective, explicitly
+// rounded fp64: bit-for-bit the definition's own arithmetic), and the SPEC
+// test functions (sphere, Rosenbrock, Powell).
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "opmm.h"
+#include "opmm_device.cuh"
+#include "opmm_internal.h"
+
+namespace opmm {
+
+#define Mr(a, b) __dmul_rn((a), (b))
+#define Ar(a, b) __dadd_rn((a), (b))
+#define Sr(a, b) __dsub_rn((a), (b))
+#define Dr(a, b) __ddiv_rn((a), (b))
+
+// ---------------------------------------------------------------------------
+// Plant objective in the RK4 definition's reference operation order: the
+// D1 right-hand side and classical RK4 written out as the definition states
+// them (absolute coordinates, every quotient an IEEE division), each operation
+// explicitly rounded, so the result is the definition's exact fp64 value.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void ref_rhs(const double p[NP], const double y[6], double n_ag,
+                                        double n_ant, double tau_ag_ms, double tau_ant_ms,
+                                        double dy[6]) {
+  const double theta = y[0], omega = y[1], x_ag = y[2], x_ant = y[3], f_ag = y[4], f_ant = y[5];
+  const double th_ag = theta, th_ant = -theta;
+  const double T_ag = Mr(p[KSE_AG], Sr(x_ag, th_ag));
+  const double T_ant = Mr(p[KSE_ANT], Sr(x_ant, th_ant));
+  const double tau_ag = Mr(1e-3, tau_ag_ms), tau_ant = Mr(1e-3, tau_ant_ms);
+  dy[0] = omega;
+  dy[1] = Dr(Sr(Sr(T_ag, T_ant), Mr(p[B_P], omega)), p[J_]);
+  dy[2] = Dr(Sr(Sr(Sr(f_ag, Mr(p[NC_AG], th_ag)), Mr(p[KLT_AG], x_ag)), T_ag), p[B_AG]);
+  dy[3] = Dr(Sr(Sr(Sr(f_ant, Mr(p[NC_ANT], th_ant)), Mr(p[KLT_ANT], x_ant)), T_ant), p[B_ANT]);
+  dy[4] = Dr(Sr(n_ag, f_ag), tau_ag);
+  dy[5] = Dr(Sr(n_ant, f_ant), tau_ant);
+}
+
+__device__ double ref_objective(const double p_in[NP], const double* rel, int32_t n_steps,
+                                double dt_ms, double Aprime, double pw_default, int metric) {
+  double p[NP];
+#pragma unroll
+  for (int d = 0; d < NP; ++d) p[d] = p_in[d];
+  if (isnan(p[PW_])) p[PW_] = pw_default;
+  // physical check (D8): same rule and summation order as the definition
+  {
+    bool bad = false;
+    double amount = 0.0;
+    for (int i = 0; i < NP; ++i) {
+      const double v = p[i];
+      const bool strict = (i == KSE_AG || i == KSE_ANT || i == B_AG || i == B_ANT || i == J_ ||
+                           i == TAU_AC_AG || i == TAU_AC_ANT || i == TAU_DE_AG ||
+                           i == TAU_DE_ANT || i == PW_);
+      if (!isfinite(v)) { bad = true; amount = Ar(amount, 1.0); continue; }
+      if (strict ? !(v > 0.0) : !(v >= 0.0)) {
+        bad = true;
+        if (v < 0.0) amount = Ar(amount, -v);
+      }
+    }
+    if (!bad) {
+      const double g_ag = Dr(p[KSE_AG], Ar(p[KLT_AG], p[KSE_AG]));
+      const double g_ant = Dr(p[KSE_ANT], Ar(p[KLT_ANT], p[KSE_ANT]));
+      const double G = Ar(Mr(g_ag, Ar(p[NC_AG], p[KLT_AG])), Mr(g_ant, Ar(p[NC_ANT], p[KLT_ANT])));
+      if (!(G > 0.0)) bad = true;
+    }
+    if (bad) return Mr(PENALTY, Ar(1.0, amount));
+  }
+  const double F = p[NC_FIX];
+  const double g_ag = Dr(p[KSE_AG], Ar(p[KLT_AG], p[KSE_AG]));
+  const double g_ant = Dr(p[KSE_ANT], Ar(p[KLT_ANT], p[KSE_ANT]));
+  const double G = Ar(Mr(g_ag, Ar(p[NC_AG], p[KLT_AG])), Mr(g_ant, Ar(p[NC_ANT], p[KLT_ANT])));
+  // fixation equilibrium (n = f = N_C_FIX)
+  double ystar[6];
+  ystar[0] = Dr(Sr(Mr(g_ag, F), Mr(g_ant, F)), G);
+  ystar[1] = 0.0;
+  ystar[2] = Dr(Sr(F, Mr(Sr(p[NC_AG], p[KSE_AG]), ystar[0])), Ar(p[KLT_AG], p[KSE_AG]));
+  ystar[3] = Dr(Ar(F, Mr(Sr(p[NC_ANT], p[KSE_ANT]), ystar[0])), Ar(p[KLT_ANT], p[KSE_ANT]));
+  ystar[4] = F;
+  ystar[5] = F;
+  // post-pulse step levels (D4 generalised)
+  const double delta = Dr(Mr(G, Aprime), Ar(g_ag, g_ant));
+  double lv_ag = Ar(F, delta), lv_ant = Sr(F, delta);
+  if (lv_ant < NANT_FLOOR) {
+    const double theta_star = Dr(Sr(Mr(g_ag, F), Mr(g_ant, F)), G);
+    lv_ant = NANT_FLOOR;
+    lv_ag = Dr(Ar(Mr(G, Ar(theta_star, Aprime)), Mr(NANT_FLOOR, g_ant)), g_ag);
+  }
+  const double npd = ceil(Dr(p[PW_], dt_ms));
+  const double h = Mr(1e-3, dt_ms);
+  const double h2 = Mr(0.5, h), h6 = Dr(h, 6.0);
+  double y[6];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) y[i] = ystar[i];
+  double acc = 0.0;   // k = 0 term: |0 - rel_0| = 0
+  {
+    const double d0 = Sr(Sr(y[0], ystar[0]), rel[0]);
+    acc = metric == 0 ? Ar(acc, fabs(d0)) : Ar(acc, Mr(d0, d0));
+  }
+  for (int32_t k = 0; k < n_steps; ++k) {
+    const bool pulse = (double)k < npd;
+    const double na = pulse ? p[NSAC_AG] : lv_ag, nn = pulse ? p[NSAC_ANT] : lv_ant;
+    const double ta = pulse ? p[TAU_AC_AG] : p[TAU_DE_AG];
+    const double tn = pulse ? p[TAU_AC_ANT] : p[TAU_DE_ANT];
+    double k1[6], k2[6], k3[6], k4[6], yt[6];
+    ref_rhs(p, y, na, nn, ta, tn, k1);
+#pragma unroll
+    for (int i = 0; i < 6; ++i) yt[i] = Ar(y[i], Mr(h2, k1[i]));
+    ref_rhs(p, yt, na, nn, ta, tn, k2);
+#pragma unroll
+    for (int i = 0; i < 6; ++i) yt[i] = Ar(y[i], Mr(h2, k2[i]));
+    ref_rhs(p, yt, na, nn, ta, tn, k3);
+#pragma unroll
+    for (int i = 0; i < 6; ++i) yt[i] = Ar(y[i], Mr(h, k3[i]));
+    ref_rhs(p, yt, na, nn, ta, tn, k4);
+#pragma unroll
+    for (int i = 0; i < 6; ++i)
+      y[i] = Ar(y[i], Mr(h6, Ar(Ar(Ar(k1[i], Mr(2.0, k2[i])), Mr(2.0, k3[i])), k4[i])));
+    const double d = Sr(Sr(y[0], ystar[0]), rel[k + 1]);
+    acc = metric == 0 ? Ar(acc, fabs(d)) : Ar(acc, Mr(d, d));
+  }
+  if (!(acc < CAP)) return __longlong_as_double(0x7ff0000000000000LL);
+  return metric == 0 ? acc : __dsqrt_rn(Dr(acc, (double)(n_steps + 1)));
+}
+
+// SPEC acceptance-3 test functions, in the definition's operation order.
+__device__ double test_objective(int fn_id, int n, const double* x) {
+  double s = 0.0;
+  if (fn_id == 0) {
+    for (int i = 0; i < n; ++i) s = Ar(s, Mr(x[i], x[i]));
+  } else if (fn_id == 1) {
+    for (int i = 0; i + 1 < n; ++i) {
+      const double a = Sr(x[i + 1], Mr(x[i], x[i])), b = Sr(1.0, x[i]);
+      s = Ar(s, Ar(Mr(100.0, Mr(a, a)), Mr(b, b)));
+    }
+  } else {
+    for (int i = 0; i + 3 < n; i += 4) {
+      const double a = Ar(x[i], Mr(10.0, x[i + 1])), b = Sr(x[i + 2], x[i + 3]);
+      const double c = Sr(x[i + 1], Mr(2.0, x[i + 2])), d = Sr(x[i], x[i + 3]);
+      s = Ar(s, Ar(Ar(Ar(Mr(a, a), Mr(5.0, Mr(b, b))), Mr(Mr(c, c), Mr(c, c))),
+                   Mr(10.0, Mr(Mr(d, d), Mr(d, d)))));
+    }
+  }
+  return s;
+}
+
+// ---------------------------------------------------------------------------
+// The batched Nelder-Mead kernel: one warp per problem.
+// OBJ: 0 plant/propagator, 1 plant/RK4 stages, 2 plant/reference order,
+//      3 test function.
+// ---------------------------------------------------------------------------
+constexpr int NM_NMAX = NP;               // simplex dimension <= 18
+constexpr int NM_PTS = NM_NMAX + 4;       // points evaluated per iteration
+constexpr int NM_WARPS = 4;               // problems per block
+constexpr int NM_THREADS = 32 * NM_WARPS;
+
+struct NmWarpSmem {
+  double V[2][NM_NMAX + 1][NM_NMAX];      // double-buffered simplex (sorted)
+  double fv[2][NM_NMAX + 1];
+  double P[NM_PTS][NM_NMAX];              // xr, xe, xc, xcc, shrink points
+  double fp[NM_PTS];
+  double xbar[NM_NMAX];
+};
+
+template <typename T, int OBJ, int METRIC>
+__global__ void __launch_bounds__(NM_THREADS) nm_kernel(NmArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  NmWarpSmem* W = reinterpret_cast<NmWarpSmem*>(smem_raw) + warp;
+  T* rel = reinterpret_cast<T*>(smem_raw + NM_WARPS * sizeof(NmWarpSmem) +
+                                (size_t)warp * rel_bytes<T>(a.ctl.n_steps + 1));
+  T* stash = reinterpret_cast<T*>(smem_raw + NM_WARPS * sizeof(NmWarpSmem) +
+                                  NM_WARPS * rel_bytes<T>(a.ctl.n_steps + 1));
+  const int64_t prob = (int64_t)blockIdx.x * NM_WARPS + warp + a.prob_begin;
+  if (prob >= a.prob_end) return;   // whole warp
+  const int n = a.dim;
+  const int32_t ns = a.ctl.n_steps + 1;
+  double sgn = 1.0, Aprime = 0.0, pwd = 0.0;
+  if (OBJ < 3) {
+    const double amp = a.sac_ctl[2 * prob];
+    pwd = a.sac_ctl[2 * prob + 1];
+    const double* rec = a.rec + prob * (int64_t)ns;
+    const double r0 = rec[0];
+    const double A = isnan(amp) ? rec[ns - 1] - r0 : amp;
+    sgn = A < 0.0 ? -1.0 : 1.0;
+    Aprime = fabs(A);
+    for (int k = lane; k < ns; k += 32) rel[k] = (T)(sgn * (rec[k] - r0));
+  }
+  // evaluate point x (n coordinates) on every lane; returns f with NaN -> +inf (D11)
+  auto evaluate_point = [&](const double* x) -> double {
+    double f;
+    if (OBJ == 3) {
+      f = test_objective(a.fn_id, n, x);
+    } else {
+      double p[NP];
+#pragma unroll
+      for (int d = 0; d < NP; ++d) p[d] = x[d];
+      if (OBJ == 2) {
+        f = ref_objective(p, reinterpret_cast<const double*>(rel), a.ctl.n_steps, a.ctl.dt_ms,
+                          Aprime, pwd, METRIC);
+      } else {
+        f = evaluate<T, OBJ, METRIC, false>(p, a.ctl, Aprime, pwd, rel, nullptr, 0, sgn, nullptr,
+                                           stash, true);
+      }
+    }
+    return isnan(f) ? __longlong_as_double(0x7ff0000000000000LL) : f;
+  };
+  const double* x0 = a.x0 + prob * (int64_t)a.x0_ld;
+  // initial simplex (D9): vertex 0 = x0; vertex i = x0 with coordinate i-1
+  // scaled by (1 + scale), or scale * 0.00025 when that coordinate is zero.
+  int cur = 0;
+  {
+    const int i = lane <= n ? lane : 0;
+    double x[NM_NMAX];
+    for (int j = 0; j < n; ++j) {
+      double v = x0[j];
+      if (OBJ < 3 && j == PW_ && isnan(v)) v = pwd;
+      x[j] = v;
+    }
+    if (i > 0) x[i - 1] = x[i - 1] != 0.0 ? Mr(Ar(1.0, a.init_scale), x[i - 1]) : Mr(a.init_scale, 0.00025);
+    const double f = evaluate_point(x);
+    if (lane <= n) {
+      for (int j = 0; j < n; ++j) W->P[lane][j] = x[j];
+      W->fp[lane] = f;
+    }
+  }
+  __syncwarp();
+  // stable rank sort of the n+1 points P/fp into V[cur]/fv[cur]
+  auto sort_into = [&](int dst, const double (*src)[NM_NMAX], const double* fsrc) {
+    if (lane <= n) {
+      const double f = fsrc[lane];
+      int rank = 0;
+      for (int k = 0; k <= n; ++k) {
+        const double g = fsrc[k];
+        rank += (g < f || (g == f && k < lane)) ? 1 : 0;
+      }
+      for (int j = 0; j < n; ++j) W->V[dst][rank][j] = src[lane][j];
+      W->fv[dst][rank] = f;
+    }
+    __syncwarp();
+  };
+  sort_into(cur, W->P, W->fp);
+  int32_t it = 1, evals = n + 1, gpu_evals = n + 1, reason = 1;
+  const double rho = 1.0, chi = 2.0, psi = 0.5, sigma = 0.5;
+  while (it < a.max_iter) {
+    double (*V)[NM_NMAX] = W->V[cur];
+    double* fv = W->fv[cur];
+    // dual tolerance exit
+    bool ok = true;
+    if (lane >= 1 && lane <= n) ok = fabs(fv[lane] - fv[0]) <= a.tol_f;
+    if (lane < n) {
+      for (int i = 1; i <= n; ++i) ok = ok && fabs(V[i][lane] - V[0][lane]) <= a.tol_x;
+    }
+    if (__all_sync(0xffffffffu, ok)) { reason = 0; break; }
+    // centroid of the n best vertices (summed in vertex order, then / n)
+    if (lane < n) {
+      double sum = 0.0;
+      for (int i = 0; i < n; ++i) sum = Ar(sum, V[i][lane]);
+      W->xbar[lane] = Dr(sum, (double)n);
+    }
+    __syncwarp();
+    // all transformation points at once: lane 0 xr, 1 xe,
+    // 2 outside contraction, 3 inside contraction, 4.. shrink of vertex lane-3
+    {
+      const int L = lane < n + 4 ? lane : 0;
+      double x[NM_NMAX];
+      for (int j = 0; j < n; ++j) {
+        const double xb = W->xbar[j], vn = V[n][j];
+        double v;
+        if (L == 0) v = Sr(Mr(Ar(1.0, rho), xb), Mr(rho, vn));
+        else if (L == 1) v = Sr(Mr(Ar(1.0, Mr(rho, chi)), xb), Mr(Mr(rho, chi), vn));
+        else if (L == 2) v = Sr(Mr(Ar(1.0, Mr(psi, rho)), xb), Mr(Mr(psi, rho), vn));
+        else if (L == 3) v = Ar(Mr(Sr(1.0, psi), xb), Mr(psi, vn));
+        else v = Ar(V[0][j], Mr(sigma, Sr(V[L - 3][j], V[0][j])));
+        x[j] = v;
+      }
+      const double f = evaluate_point(x);
+      if (lane < n + 4) {
+        for (int j = 0; j < n; ++j) W->P[lane][j] = x[j];
+        W->fp[lane] = f;
+      }
+    }
+    __syncwarp();
+    gpu_evals += n + 4;
+    // Lagarias decision step (identical on every lane)
+    const double fr = W->fp[0];
+    int take = -1;   // point replacing vertex n; -2 = shrink
+    if (fr < fv[0]) {
+      take = W->fp[1] < fr ? 1 : 0;
+      evals += 2;
+    } else if (fr < fv[n - 1]) {
+      take = 0;
+      evals += 1;
+    } else if (fr < fv[n]) {
+      take = W->fp[2] <= fr ? 2 : -2;
+      evals += 2;
+    } else {
+      take = W->fp[3] < fv[n] ? 3 : -2;
+      evals += 2;
+    }
+    const int nxt = cur ^ 1;
+    if (take >= 0) {
+      // simplex with vertex n replaced, then stable sort into the other buffer
+      if (lane <= n) {
+        const double f = lane == n ? W->fp[take] : fv[lane];
+        int rank = 0;
+        for (int k = 0; k <= n; ++k) {
+          const double g = k == n ? W->fp[take] : fv[k];
+          rank += (g < f || (g == f && k < lane)) ? 1 : 0;
+        }
+        for (int j = 0; j < n; ++j) W->V[nxt][rank][j] = lane == n ? W->P[take][j] : V[lane][j];
+        W->fv[nxt][rank] = f;
+      }
+    } else {
+      // shrink: vertices 1..n become the precomputed shrink points
+      evals += n;
+      if (lane <= n) {
+        const double f = lane == 0 ? fv[0] : W->fp[lane + 3];
+        int rank = 0;
+        for (int k = 0; k <= n; ++k) {
+          const double g = k == 0 ? fv[0] : W->fp[k + 3];
+          rank += (g < f || (g == f && k < lane)) ? 1 : 0;
+        }
+        for (int j = 0; j < n; ++j) W->V[nxt][rank][j] = lane == 0 ? V[0][j] : W->P[lane + 3][j];
+        W->fv[nxt][rank] = f;
+      }
+    }
+    __syncwarp();
+    cur = nxt;
+    ++it;
+  }
+  if (lane < n) a.x_best[prob * (int64_t)a.x_ld + lane] = W->V[cur][0][lane];
+  if (lane == 0) {
+    NmOut o;
+    o.f_best = W->fv[cur][0];
+    o.iterations = it;
+    o.func_evals = evals;
+    o.gpu_evals = gpu_evals;
+    o.exit_reason = reason;
+    a.out[prob] = o;
+  }
+}
+
+template <typename T, int OBJ, int METRIC>
+static const void* nm_fn() { return reinterpret_cast<const void*>(&nm_kernel<T, OBJ, METRIC>); }
+
+const void* nm_kernel_ptr(int precision, int obj, int metric) {
+  if (obj == 3) return nm_fn<double, 3, 0>();
+  if (obj == 2) return metric == 0 ? nm_fn<double, 2, 0>() : nm_fn<double, 2, 1>();
+  if (precision == 0) {
+    if (obj == 0) return metric == 0 ? nm_fn<double, 0, 0>() : nm_fn<double, 0, 1>();
+    return metric == 0 ? nm_fn<double, 1, 0>() : nm_fn<double, 1, 1>();
+  }
+  if (obj == 0) return metric == 0 ? nm_fn<float, 0, 0>() : nm_fn<float, 0, 1>();
+  return metric == 0 ? nm_fn<float, 1, 0>() : nm_fn<float, 1, 1>();
+}
+
+size_t nm_smem(int precision, int obj, int32_t n_samples) {
+  const size_t relb = (obj == 2 || precision == 0) ? rel_bytes<double>(n_samples)
+                                                   : rel_bytes<float>(n_samples);
+  const size_t st = precision == 0 || obj >= 2 ? stash_bytes<double>(NM_THREADS)
+                                               : stash_bytes<float>(NM_THREADS);
+  return NM_WARPS * sizeof(NmWarpSmem) + NM_WARPS * (obj == 3 ? 0 : relb) + (obj < 2 ? st : 0);
+}
+
+int nm_problems_per_block() { return NM_WARPS; }
+int nm_threads() { return NM_THREADS; }
+
+cudaError_t launch_nm(const void* fn, const NmArgs& a, int grid, size_t smem, cudaStream_t st) {
+  void* args[] = {const_cast<NmArgs*>(&a)};
+  return cudaLaunchKernel(fn, dim3(grid), dim3(NM_THREADS), args, smem, st);
+}
+
+}  // namespace opmm

@@ -65,6 +65,27 @@ class FitResult(C.Structure):
                 "n_evaluated": self.n_evaluated}
 
 
+class NmOptions(C.Structure):
+    _fields_ = [("precision", C.c_int32), ("objective", C.c_int32), ("metric", C.c_int32),
+                ("max_iter", C.c_int32), ("tol_x", C.c_double), ("tol_f", C.c_double),
+                ("init_scale", C.c_double), ("cpu_check", C.c_int32), ("pad_", C.c_int32)]
+
+
+class NmResult(C.Structure):
+    _fields_ = [("x", C.c_double * NPARAM), ("f_best", C.c_double), ("cpu_check", C.c_double),
+                ("iterations", C.c_int32), ("func_evals", C.c_int32), ("gpu_evals", C.c_int32),
+                ("exit_reason", C.c_int32)]
+
+    def as_dict(self, dim: int = NPARAM) -> dict:
+        return {"x": np.array(self.x[:dim]), "f": self.f_best, "cpu_check": self.cpu_check,
+                "iterations": self.iterations, "func_evals": self.func_evals,
+                "gpu_evals": self.gpu_evals, "exit_reason": self.exit_reason}
+
+
+NM_OBJ_PROPAGATOR, NM_OBJ_RK4_STAGES, NM_OBJ_REFERENCE = 0, 1, 2
+NM_SPHERE, NM_ROSENBROCK, NM_POWELL = 0, 1, 2
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2007_09884_b200.build` "
@@ -94,6 +115,9 @@ def _load():
                             C.POINTER(FitOptions), vp], st),
         "opmm_fit_batch": ([vp, vp, i64, C.POINTER(Control), C.POINTER(SearchSpace), i64,
                             C.POINTER(FitOptions), C.POINTER(FitResult)], st),
+        "opmm_estimate_batch": ([vp, vp, i64, C.POINTER(Control), vp, C.POINTER(NmOptions),
+                                 C.POINTER(NmResult)], st),
+        "opmm_nm_minimize_test": ([vp, i32, i32, vp, i64, C.POINTER(NmOptions), C.POINTER(NmResult)], st),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -107,7 +131,7 @@ EXPORTED = ("opmm_version", "opmm_last_error", "opmm_create", "opmm_nccl_unique_
             "opmm_create_nccl", "opmm_destroy", "opmm_get_stream", "opmm_last_kernel_ms",
             "opmm_shard_range", "opmm_merge_argmin", "opmm_validate", "opmm_generate",
             "opmm_simulate", "opmm_score", "opmm_simulate_score", "opmm_fit", "opmm_fit_async",
-            "opmm_fit_batch")
+            "opmm_fit_batch", "opmm_estimate_batch", "opmm_nm_minimize_test")
 
 
 def lib():
@@ -339,3 +363,36 @@ def opmm_fit_batch(h: Handle, recorded, ctls, space, n_per: int,
                                C.byref(opts), out), "opmm_fit_batch")
     lo, hi = opmm_shard_range(S, h.rank, h.world)
     return [out[s].as_dict() if lo <= s < hi else None for s in range(S)]
+
+
+# ---------------------------------------------------------------------- Nelder-Mead
+def nm_options(precision=FP64, objective=NM_OBJ_PROPAGATOR, metric=METRIC_L1, max_iter=0, tol_x=0.0,
+               tol_f=0.0, init_scale=0.0, cpu_check=1) -> NmOptions:
+    return NmOptions(precision, objective, metric, max_iter, tol_x, tol_f, init_scale, cpu_check, 0)
+
+
+def opmm_estimate_batch(h: Handle, recorded, ctls, x0=None, options: NmOptions | None = None) -> list:
+    """Nelder-Mead OPC estimation of S saccades (recorded [S, n_steps+1])."""
+    S = len(ctls)
+    arr = (Control * S)(*[_ctl(c) for c in ctls])
+    out = (NmResult * S)()
+    rec = recorded
+    if isinstance(recorded, np.ndarray):
+        rec = np.ascontiguousarray(recorded, dtype=np.float64)
+    xx = None if x0 is None else np.ascontiguousarray(x0, dtype=np.float64)
+    _check(_lib.opmm_estimate_batch(h.ptr, _ptr(rec), S, arr, _ptr(xx),
+                                    C.byref(options if options is not None else nm_options()), out),
+           "opmm_estimate_batch")
+    lo, hi = opmm_shard_range(S, h.rank, h.world)
+    return [out[s].as_dict() if lo <= s < hi else None for s in range(S)]
+
+
+def opmm_nm_minimize_test(h: Handle, fn_id: int, x0, options: NmOptions | None = None) -> list:
+    """Nelder-Mead on a SPEC test function for S start points x0 [S, dim]."""
+    x = np.ascontiguousarray(np.atleast_2d(x0), dtype=np.float64)
+    S, dim = x.shape
+    out = (NmResult * S)()
+    _check(_lib.opmm_nm_minimize_test(h.ptr, fn_id, dim, _ptr(x), S,
+                                      C.byref(options if options is not None else nm_options()), out),
+           "opmm_nm_minimize_test")
+    return [out[s].as_dict(dim) for s in range(S)]

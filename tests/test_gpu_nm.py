@@ -1,0 +1,103 @@
+"""GPU parity of the batched Nelder-Mead estimator (-m gpu).
+
+The GPU engine evaluates all n + 4 transformation points every iteration
+ but takes the serial Lagarias decision, so with the same
+objective values its iterates are the serial algorithm's.  With the
+reference-order plant objective (explicitly rounded fp64, the RK4
+definition's operation order) and on the SPEC test functions the GPU results
+are bit-identical to the CPU oracle's serial Nelder-Mead: same best vertex,
+same f, same iteration and evaluation counts.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+I = W.IDX
+
+
+@pytest.fixture(scope="module")
+def opmm():
+    if not torch.cuda.is_available():
+        pytest.fail("no CUDA device: the -m gpu suite must run on a B200")
+    from paper_2007_09884_b200 import build
+    build.build()
+    from paper_2007_09884_b200 import opmm as m
+    return m
+
+
+@pytest.fixture(scope="module")
+def h(opmm):
+    with opmm.opmm_create(0) as handle:
+        yield handle
+
+
+def test_rosenbrock_published_run_bit_exact(opmm, h):
+    r = opmm.opmm_nm_minimize_test(h, opmm.NM_ROSENBROCK, [[-1.2, 1.0]])[0]
+    o = oracle.nm_test(oracle.NM_ROSENBROCK, [-1.2, 1.0])
+    assert (r["iterations"], r["func_evals"]) == (85, 159) == (o["iterations"], o["func_evals"])
+    assert r["x"].tolist() == o["x"].tolist() and r["f"] == o["f"]
+    assert r["gpu_evals"] == 3 + 84 * 6      # every iteration evaluates n + 4 points
+
+
+@pytest.mark.parametrize("fn,dim", [(0, 3), (1, 2), (1, 4), (2, 4)])
+def test_test_functions_many_starts_bit_exact(opmm, h, fn, dim):
+    rng = np.random.default_rng(fn * 10 + dim)
+    x0 = rng.uniform(-2, 2, size=(40, dim))
+    x0[0, 0] = 0.0                                  # zero-coordinate initial step (D9)
+    res = opmm.opmm_nm_minimize_test(h, fn, x0, opmm.nm_options(tol_x=1e-7, tol_f=1e-9, max_iter=3000))
+    for s in range(len(x0)):
+        o = oracle.nm_test(fn, x0[s], tol_x=1e-7, tol_f=1e-9, max_iter=3000)
+        r = res[s]
+        assert r["x"].tolist() == o["x"].tolist(), s
+        assert (r["f"], r["iterations"], r["func_evals"], r["exit_reason"]) == \
+               (o["f"], o["iterations"], o["func_evals"], o["exit_reason"]), s
+
+
+def _roundtrip_set(S, seed=7, n_steps=100):
+    rng = np.random.default_rng(seed)
+    ctls, recs, truths = [], [], []
+    for s in range(S):
+        t = W.truth_opc()
+        for name in ("K_SE_AG", "B_AG", "N_SAC_AG", "PW"):
+            t[I[name]] *= 1.0 + 0.2 * rng.uniform(-1, 1)
+        c = W.Control(n_steps=n_steps, amplitude_deg=float(rng.uniform(5, 15)), pw_default_ms=40.0)
+        ctls.append(c)
+        recs.append(oracle.positions(t, c) + W.noise(n_steps + 1, seed=100 + s))
+        truths.append(t)
+    return ctls, np.array(recs), truths
+
+
+def test_plant_reference_objective_bit_exact_vs_oracle(opmm, h):
+    """Reference-order objective: every saccade's Nelder-Mead run identical to
+    the oracle's serial run, bit for bit (x, f, iterations, evaluations)."""
+    ctls, recs, _ = _roundtrip_set(6)
+    opts = opmm.nm_options(objective=opmm.NM_OBJ_REFERENCE, max_iter=400)
+    res = opmm.opmm_estimate_batch(h, recs, ctls, options=opts)
+    o = oracle.estimate_batch(recs, ctls, max_iter=400)
+    for s in range(len(ctls)):
+        r = res[s]
+        assert r["x"].tolist() == o["x"][s].tolist(), s
+        assert r["f"] == o["f"][s]
+        assert (r["iterations"], r["func_evals"], r["exit_reason"]) == \
+               (o["iterations"][s], o["func_evals"][s], o["exit_reason"][s])
+        assert abs(r["cpu_check"] - r["f"]) <= 1e-9 * r["f"]
+
+
+@pytest.mark.parametrize("precision", [0, 1])
+def test_plant_fast_objective_roundtrip(opmm, h, precision):
+    """Propagator objective (the fit path's evaluator): SPEC acceptance 4 --
+    per-sample mean residual <= 0.5 deg on >= 90% of round-trip saccades;
+    the result's objective agrees with the serial CPU_check re-score."""
+    ctls, recs, _ = _roundtrip_set(40, seed=11)
+    res = opmm.opmm_estimate_batch(h, recs, ctls, options=opmm.nm_options(precision=precision))
+    f = np.array([r["f"] for r in res])
+    assert np.mean(f / 101.0 <= 0.5) >= 0.9
+    tol = 1e-9 if precision == 0 else 1e-4
+    for r, rec, c in zip(res, recs, ctls):
+        assert abs(r["cpu_check"] - r["f"]) <= tol * max(r["f"], 1.0)
+        assert r["f"] <= oracle.objective(W.truth_opc(), rec, c)   # never worse than the start
+        assert r["gpu_evals"] == 19 + (r["iterations"] - 1) * 22

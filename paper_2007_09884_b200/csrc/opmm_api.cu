@@ -369,7 +369,7 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
   const int64_t work = three ? (e - b + 255) / 256 * block : two ? (e - b + 1) / 2 : e - b;
   CKS(grid_for(h, fn, block, smem, work, opts ? opts->grid_blocks : 0, &grid));
   if (e <= b) grid = 1;  // empty shard: one block reports "no candidate"
-  const bool multi = shard && h->world > 1;
+  const bool multi = shard && h->comm != nullptr;   // world > 1 (or a 1-rank test comm)
   CKS(ensure(h->partials, h->partials_cap, (size_t)grid * (size_t)(s_begin + S)));
   CKS(ensure(h->counters, h->counters_cap, (size_t)(s_begin + S), true));
   if (multi) {
@@ -624,7 +624,9 @@ opmm_status opmm_create_nccl(opmm_handle** out, int device, const uint8_t* id, i
   opmm_handle* h = *out;
   h->rank = rank;
   h->world = world;
-  if (world > 1) {
+  // A single-rank communicator is also created when OPMM_NCCL_SINGLE_RANK is
+  // set, so the one-GPU tests exercise the all-gather + merge path for real.
+  if (world > 1 || getenv("OPMM_NCCL_SINGLE_RANK")) {
     NcclApi& api = nccl();
     if (!api.loaded) {
       opmm_destroy(h);

@@ -556,3 +556,35 @@ def test_fit_batch_population(opmm, h):
         assert res[s]["best_index"] == o["best_index"], s
         assert abs(res[s]["opt_err"] - o["best_err"]) <= 1e-9 * max(o["best_err"], 1.0)
         assert abs(res[s]["cpu_check"] - res[s]["opt_err"]) <= 1e-9 * res[s]["opt_err"]
+
+
+def test_nccl_single_rank_merge_path(opmm, h):
+    """The multi-GPU path on one GPU: a 1-rank NCCL communicator (libnccl.so.2
+    loaded at run time), the per-rank 32-byte partial, ncclAllGather on the
+    handle's stream and the merge kernel -- same result as the plain fit."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import os, sys, numpy as np
+sys.path.insert(0, os.getcwd())
+os.environ["OPMM_NCCL_SINGLE_RANK"] = "1"
+import torch, oracle, workloads as W
+from paper_2007_09884_b200 import opmm
+ctl = W.Control(); sp = W.paper_space()
+rec = oracle.positions(W.truth_opc(), ctl) + W.noise(101)
+uid = opmm.opmm_nccl_unique_id()
+with opmm.opmm_create_nccl(0, uid, 0, 1) as hn, opmm.opmm_create(0) as hp:
+    for n in (1, 777, 100000):
+        a = opmm.opmm_fit(hn, rec, ctl, sp, n)
+        b = opmm.opmm_fit(hp, rec, ctl, sp, n)
+        assert (a["best_index"], a["opt_err"], a["n_finite"], a["n_evaluated"]) == \
+               (b["best_index"], b["opt_err"], b["n_finite"], b["n_evaluated"]), (n, a, b)
+        assert a["opc"].tolist() == b["opc"].tolist()
+print("nccl-single-rank ok")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    p = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                       timeout=300)
+    assert p.returncode == 0, p.stdout + p.stderr
+    assert "nccl-single-rank ok" in p.stdout

@@ -394,16 +394,53 @@ __device__ __forceinline__ void horner_step(const Mech& m, double s, double Tm[4
     for (int j = 0; j < 4; ++j) Tm[i][j] = R[i][j];
 }
 
+// Structural zeros of u_i = Z^i (h c_m) (Z: row 0 = (0,h,0,0), row 2 couples
+// only theta and x_AG, row 3 only theta and x_ANT): NZU[m][i][r] is false where
+// u_i[r] is identically zero, so those terms are dropped at compile time.
+__device__ constexpr bool NZU[2][4][4] = {
+    {{false, false, true, false}, {false, true, true, false}, {true, true, true, false},
+     {true, true, true, true}},
+    {{false, false, false, true}, {false, true, false, true}, {true, true, false, true},
+     {true, true, true, true}}};
+
+// out = Z v for a vector v with structural-zero mask nz (compile-time).
+__device__ __forceinline__ void zmul_masked(const Mech& m, const double v[4], const bool nz[4],
+                                            double out[4]) {
+  out[0] = nz[1] ? m.z01 * v[1] : 0.0;
+  double o1 = 0.0;
+  if (nz[0]) o1 = m.z10 * v[0];
+  if (nz[1]) o1 = fma(m.z11, v[1], o1);
+  if (nz[2]) o1 = fma(m.z12, v[2], o1);
+  if (nz[3]) o1 = fma(m.z13, v[3], o1);
+  out[1] = o1;
+  double o2 = 0.0;
+  if (nz[0]) o2 = m.z20 * v[0];
+  if (nz[2]) o2 = fma(m.z22, v[2], o2);
+  out[2] = o2;
+  double o3 = 0.0;
+  if (nz[0]) o3 = m.z30 * v[0];
+  if (nz[3]) o3 = fma(m.z33, v[3], o3);
+  out[3] = o3;
+}
+
 template <typename T>
 __device__ __forceinline__ void make_prop(const Setup& s, Prop2<T>& pr) {
   const Mech& m = s.m;
-  // one-step mechanical block P(Z), Z = hM: 4 sparse Horner steps
+  // one-step mechanical block P(Z), Z = hM, by Horner: the first step
+  // I + Z/4 is written out (9 structural non-zeros), then 3 sparse steps
   double P[4][4];
+  {
+    const double q = 0.25;
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) P[i][j] = (i == j ? 1.0 : 0.0);
-  horner_step(m, 0.25, P);               // I + Z/4
+      for (int j = 0; j < 4; ++j) P[i][j] = 0.0;
+    P[0][0] = 1.0;            P[0][1] = q * m.z01;
+    P[1][0] = q * m.z10;      P[1][1] = fma(q, m.z11, 1.0);
+    P[1][2] = q * m.z12;      P[1][3] = q * m.z13;
+    P[2][0] = q * m.z20;      P[2][2] = fma(q, m.z22, 1.0);
+    P[3][0] = q * m.z30;      P[3][3] = fma(q, m.z33, 1.0);
+  }
   horner_step(m, 1.0 / 3.0, P);          // I + Z/3 (I + Z/4)
   horner_step(m, 0.5, P);                // I + Z/2 (...)
   horner_step(m, 1.0, P);                // I + Z (...) = P(Z)
@@ -415,15 +452,15 @@ __device__ __forceinline__ void make_prop(const Setup& s, Prop2<T>& pr) {
     u[mm][0][2] = (mm == 0) ? m.hb_ag : 0.0;
     u[mm][0][3] = (mm == 0) ? 0.0 : m.hb_ant;
 #pragma unroll
-    for (int i = 1; i < 4; ++i) zmul_vec(m, u[mm][i - 1], u[mm][i]);
+    for (int i = 1; i < 4; ++i) zmul_masked(m, u[mm][i - 1], NZU[mm][i - 1], u[mm][i]);
   }
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      double a = 0.0;
+      double a = P[i][0] * P[0][j];
 #pragma unroll
-      for (int l = 0; l < 4; ++l) a = fma(P[i][l], P[l][j], a);
+      for (int l = 1; l < 4; ++l) a = fma(P[i][l], P[l][j], a);
       pr.P2[i][j] = (T)a;
     }
     pr.P0[i] = (T)P[0][i];
@@ -435,23 +472,38 @@ __device__ __forceinline__ void make_prop(const Setup& s, Prop2<T>& pr) {
     for (int mm = 0; mm < 2; ++mm) {
       const double zd = mm == 0 ? s.ph[ph].zd_ag : s.ph[ph].zd_ant;
       const double nt = mm == 0 ? s.ph[ph].nt_ag : s.ph[ph].nt_ant;
-      const double a3 = 1.0 / 24.0;
-      const double a2 = 1.0 / 6.0 + zd * a3;
-      const double a1 = 0.5 + zd * a2;
-      const double a0 = 1.0 + zd * a1;
+      const double a[4] = {0.0, 0.0, 0.0, 1.0 / 24.0};
+      double av[4];
+      av[3] = a[3];
+      av[2] = fma(zd, av[3], 1.0 / 6.0);
+      av[1] = fma(zd, av[2], 0.5);
+      av[0] = fma(zd, av[1], 1.0);
       const double g = -zd * nt;
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
-        X[r][mm] = u[mm][0][r] * a0 + u[mm][1][r] * a1 + u[mm][2][r] * a2 + u[mm][3][r] * a3;
-        c[r] += g * (u[mm][0][r] * a1 + u[mm][1][r] * a2 + u[mm][2][r] * a3);
+        // X[:,m] = sum_i u_i a_i;  c += g sum_{i<3} u_i a_{i+1}  (structural zeros skipped)
+        double x = 0.0, cc = 0.0;
+        bool first_x = true, first_c = true;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (!NZU[mm][i][r]) continue;
+          x = first_x ? u[mm][i][r] * av[i] : fma(u[mm][i][r], av[i], x);
+          first_x = false;
+          if (i < 3) {
+            cc = first_c ? u[mm][i][r] * av[i + 1] : fma(u[mm][i][r], av[i + 1], cc);
+            first_c = false;
+          }
+        }
+        X[r][mm] = x;
+        if (!first_c) c[r] = fma(g, cc, c[r]);
       }
-      pf[mm] = 1.0 + zd * a0;
-      qf[mm] = g * a0;
+      pf[mm] = fma(zd, av[0], 1.0);
+      qf[mm] = g * av[0];
     }
     PhaseProp2<T>& q = pr.ph[ph];
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
-      double c2 = c[r] + X[r][0] * qf[0] + X[r][1] * qf[1];
+      double c2 = fma(X[r][1], qf[1], fma(X[r][0], qf[0], c[r]));
 #pragma unroll
       for (int l = 0; l < 4; ++l) c2 = fma(P[r][l], c[l], c2);
       q.c2[r] = (T)c2;
@@ -466,7 +518,7 @@ __device__ __forceinline__ void make_prop(const Setup& s, Prop2<T>& pr) {
 #pragma unroll
     for (int mm = 0; mm < 2; ++mm) {
       q.pf2[mm] = (T)(pf[mm] * pf[mm]);
-      q.qf2[mm] = (T)(pf[mm] * qf[mm] + qf[mm]);
+      q.qf2[mm] = (T)fma(pf[mm], qf[mm], qf[mm]);
       q.X0[mm] = (T)X[0][mm];
     }
     q.c0 = (T)c[0];
@@ -819,7 +871,31 @@ __device__ __forceinline__ double evaluate(const double p[NP], const CtlDev& c, 
   T acc;
   if (INTEG == 0) {
     Prop2<T> pr;
+#ifdef OPMM_EXP_NOPROP   // timing experiment only: skip the propagator build
+    {
+      const double b0 = s.m.z10 * 1e-6, b1 = s.ph[0].zd_ag * 1e-3, b2 = s.ph[1].zd_ant * 1e-3;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) pr.P2[r][j] = (T)(r == j ? 0.9 + b0 : b0);
+        pr.P0[r] = (T)(0.1 * b1);
+        pr.z1[r] = (T)b2;
+#pragma unroll
+        for (int ph = 0; ph < 2; ++ph) {
+          pr.ph[ph].X2[r][0] = (T)b1; pr.ph[ph].X2[r][1] = (T)b2; pr.ph[ph].c2[r] = (T)(b1 * b2);
+        }
+      }
+#pragma unroll
+      for (int ph = 0; ph < 2; ++ph) {
+        pr.ph[ph].pf2[0] = (T)(0.5 + b1); pr.ph[ph].pf2[1] = (T)(0.5 + b2);
+        pr.ph[ph].qf2[0] = (T)b2; pr.ph[ph].qf2[1] = (T)b1;
+        pr.ph[ph].X0[0] = (T)b0; pr.ph[ph].X0[1] = (T)b1; pr.ph[ph].c0 = (T)b2;
+      }
+      pr.f1[0] = (T)b0; pr.f1[1] = (T)b1;
+    }
+#else
     make_prop<T>(s, pr);
+#endif
     acc = run_propagator<T, METRIC, TRAJ>(pr, s.n_pulse, c.n_steps, rel, traj, ld_out,
                                           (T)c.theta0, (T)sgn, stash, blockDim.x);
   } else {

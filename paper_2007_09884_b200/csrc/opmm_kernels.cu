@@ -204,7 +204,14 @@ __global__ void __launch_bounds__(OPMM_FIT_LB_THREADS, OPMM_FIT_LB_BLOCKS) fit_k
     const bool valid = i0 < a.end;
     const int64_t i = valid ? i0 : a.end - 1;
     double p[NP];
+#ifdef OPMM_EXP_NOGEN   // timing experiment only: cheap stand-in candidates
+#pragma unroll
+    for (int d = 0; d < NP; ++d)
+      p[d] = a.space.lo[d] * (1.0 + (double)(((uint64_t)i * 7 + d) & 1023) * 1e-3);
+    p[PW_] = 1.0 + (double)(((uint64_t)i * 2654435761u) % 100u);
+#else
     generate_opc(a.space, (uint32_t)sac, i, p, tab);
+#endif
     const double E = evaluate<T, INTEG, METRIC, false>(p, a.ctl, Aprime, pwd, rel, nullptr, 0,
                                                        sgn, nullptr, stash, !a.space.all_physical);
     if (valid) {

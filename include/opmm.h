@@ -99,7 +99,12 @@ typedef struct {
  *   The product of levels must equal the candidate count of the call. */
 typedef struct {
   int32_t mode;
-  int32_t pad_;
+  int32_t model;   /* 0 = 18-parameter OPMM (Table 1); 1 = 9-parameter OPMM (Table 2,
+                      PAPER.md:173-197): free slots K_SE_AG (= K_SE), K_LT_AG (= K_LT),
+                      B_AG, B_ANT, B_P, N_C_AG, N_C_ANT, J, N_C_FIX; every generated
+                      candidate is expanded per SPEC D7 (K_SE_ANT = K_SE_AG,
+                      K_LT_ANT = K_LT_AG, pulse 55 / 0.5 g of width pw_default,
+                      Table 1 time constants -- DESIGN.md reading Q23) */
   uint64_t seed;
   double lo[OPMM_NPARAM];
   double hi[OPMM_NPARAM];

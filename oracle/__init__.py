@@ -46,7 +46,8 @@ def lib():
         u32p = C.POINTER(C.c_uint32)
         L.orc_philox4x32_10.argtypes = [u32p, u32p, u32p]
         L.orc_philox4x32_10.restype = None
-        L.orc_generate.argtypes = [C.c_int, C.c_uint64, dp, dp, u8p, i32p, C.c_uint32, C.c_int64, dp]
+        L.orc_generate.argtypes = [C.c_int, C.c_int, C.c_uint64, dp, dp, u8p, i32p, C.c_uint32,
+                                   C.c_int64, dp]
         L.orc_generate.restype = C.c_int
         L.orc_physical_penalty.argtypes = [dp]
         L.orc_physical_penalty.restype = C.c_double
@@ -67,8 +68,10 @@ def lib():
         L.orc_objective.argtypes = [dp, dp, C.c_int32, C.c_double, C.c_double, C.c_double, C.c_int, dp]
         L.orc_objective.restype = C.c_double
         L.orc_fit.argtypes = [dp, C.c_int32, C.c_double, C.c_double, C.c_double, C.c_int, C.c_int,
-                              C.c_uint64, dp, dp, u8p, i32p, C.c_uint32, C.c_int64, C.c_int64,
-                              C.c_int, dp, i64p, dp, dp]
+                              C.c_int, C.c_uint64, dp, dp, u8p, i32p, C.c_uint32, C.c_int64,
+                              C.c_int64, C.c_int, dp, i64p, dp, dp]
+        L.orc_expand_9param.argtypes = [dp]
+        L.orc_expand_9param.restype = None
         L.orc_fit.restype = C.c_int64
         L.orc_max_threads.argtypes = []
         L.orc_max_threads.restype = C.c_int
@@ -97,7 +100,7 @@ def _space_args(space):
     ls = np.ascontiguousarray(space.log_scale, dtype=np.uint8)
     lv = np.ascontiguousarray(space.levels, dtype=np.int32)
     keep = (lo, hi, ls, lv)
-    return keep, (int(space.mode), C.c_uint64(int(space.seed)), plo, phi,
+    return keep, (int(space.mode), int(getattr(space, "model", 0)), C.c_uint64(int(space.seed)), plo, phi,
                   ls.ctypes.data_as(C.POINTER(C.c_uint8)), lv.ctypes.data_as(C.POINTER(C.c_int32)))
 
 
@@ -123,6 +126,13 @@ def generate(space, index: int, saccade: int = 0) -> np.ndarray:
 def generate_batch(space, begin: int, count: int, saccade: int = 0) -> np.ndarray:
     """[count, 18] candidates, row i = gen(begin + i)."""
     return np.stack([generate(space, begin + i, saccade) for i in range(count)]) if count else np.zeros((0, NPARAM))
+
+
+def expand_9param(p9_in_18) -> np.ndarray:
+    """SPEC D7 expansion of a 9-parameter OPC held in the 18-vector slots."""
+    a = np.array(p9_in_18, dtype=np.float64)
+    lib().orc_expand_9param(a.ctypes.data_as(C.POINTER(C.c_double)))
+    return a
 
 
 def physical_penalty(opc) -> float:

@@ -76,9 +76,38 @@ void orc_philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2],
 /*     log dim: lo * exp(d * (log(hi/lo) / (L-1)));                           */
 /*     linear dim: lo + d * ((hi - lo) / (L-1)); L == 1: lo.                  */
 /* ------------------------------------------------------------------------ */
-int orc_generate(int mode, uint64_t seed, const double* lo, const double* hi,
+/* 9-parameter OPMM (Table 2) inside the 18-vector, SPEC D7
+   (SPEC.md:132): shared K_SE and K_LT (the AG entries), the canonical pulse
+   55 / 0.5 g of width "saccade duration - 6 ms" (PW NaN -> pw_default), and
+   -- reading Q23 -- the Table 1 activation/deactivation times. */
+void orc_expand_9param(double p[ORC_NP]) {
+  p[P_KSE_ANT] = p[P_KSE_AG];
+  p[P_KLT_ANT] = p[P_KLT_AG];
+  p[P_TAU_AC_AG] = 11.7;
+  p[P_TAU_AC_ANT] = 2.4;
+  p[P_TAU_DE_AG] = 2.0;
+  p[P_TAU_DE_ANT] = 1.9;
+  p[P_NSAC_AG] = 55.0;
+  p[P_NSAC_ANT] = 0.5;
+  p[P_PW] = NAN;
+}
+
+static int orc_generate18(int mode, uint64_t seed, const double* lo, const double* hi,
+                          const uint8_t* log_scale, const int32_t* levels,
+                          uint32_t saccade, int64_t index, double out[ORC_NP]);
+
+/* model 0 = 18-parameter OPC (Table 1); model 1 = 9-parameter (Table 2, D7) */
+int orc_generate(int mode, int model, uint64_t seed, const double* lo, const double* hi,
                  const uint8_t* log_scale, const int32_t* levels,
                  uint32_t saccade, int64_t index, double out[ORC_NP]) {
+  int rc = orc_generate18(mode, seed, lo, hi, log_scale, levels, saccade, index, out);
+  if (rc == 0 && model == 1) orc_expand_9param(out);
+  return rc;
+}
+
+static int orc_generate18(int mode, uint64_t seed, const double* lo, const double* hi,
+                          const uint8_t* log_scale, const int32_t* levels,
+                          uint32_t saccade, int64_t index, double out[ORC_NP]) {
   int d;
   if (mode == 0) {
     uint32_t words[20];
@@ -326,7 +355,7 @@ double orc_objective(const double p[ORC_NP], const double* rel, int32_t n_steps,
 /* finite E_i; *best_index = -1 if none.                                     */
 /* ------------------------------------------------------------------------ */
 int64_t orc_fit(const double* rec, int32_t n_steps, double dt_ms, double amplitude,
-                double pw_default_ms, int metric, int mode, uint64_t seed,
+                double pw_default_ms, int metric, int mode, int model, uint64_t seed,
                 const double* lo, const double* hi, const uint8_t* log_scale,
                 const int32_t* levels, uint32_t saccade, int64_t begin, int64_t end,
                 int nthreads, double* err_out, int64_t* best_index, double* best_err,
@@ -355,7 +384,7 @@ int64_t orc_fit(const double* rec, int32_t n_steps, double dt_ms, double amplitu
     ce = begin + (end - begin) * (tid + 1) / nt;
     for (i = cb; i < ce; ++i) {
       double e;
-      orc_generate(mode, seed, lo, hi, log_scale, levels, saccade, i, opc);
+      orc_generate(mode, model, seed, lo, hi, log_scale, levels, saccade, i, opc);
       e = orc_objective(opc, rel, n_steps, dt_ms, Aprime, pw_default_ms, metric, buf);
       if (err_out) err_out[i - begin] = e;
       if (isfinite(e)) n_finite++;
@@ -373,7 +402,7 @@ int64_t orc_fit(const double* rec, int32_t n_steps, double dt_ms, double amplitu
   *best_index = bi;
   *best_err = be;
   if (bi >= 0 && best_opc)
-    orc_generate(mode, seed, lo, hi, log_scale, levels, saccade, bi, best_opc);
+    orc_generate(mode, model, seed, lo, hi, log_scale, levels, saccade, bi, best_opc);
   return n_finite;
 }
 

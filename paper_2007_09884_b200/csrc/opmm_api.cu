@@ -185,6 +185,7 @@ opmm_status validate_control(const opmm_control* c, bool need_amplitude) {
 opmm_status validate_space(const opmm_search_space* s, int64_t n) {
   if (!s) return fail(OPMM_ERR_INVALID_ARG, "search space is NULL");
   if (s->mode != 0 && s->mode != 1) return fail(OPMM_ERR_INVALID_ARG, "mode must be 0 or 1");
+  if (s->model != 0 && s->model != 1) return fail(OPMM_ERR_INVALID_ARG, "model must be 0 or 1");
   for (int d = 0; d < OPMM_NPARAM; ++d) {
     if (!is_finite(s->lo[d]) || !is_finite(s->hi[d]))
       return fail(OPMM_ERR_INVALID_ARG, "bounds of dimension %d must be finite", d);
@@ -216,6 +217,7 @@ opmm::SpaceDev make_space(const opmm_search_space* s) {
   opmm::SpaceDev d;
   std::memset(&d, 0, sizeof(d));
   d.mode = s->mode;
+  d.model = s->model;
   d.key0 = (uint32_t)(s->seed & 0xffffffffu);
   d.key1 = (uint32_t)(s->seed >> 32);
   for (int k = 0; k < OPMM_NPARAM; ++k) {

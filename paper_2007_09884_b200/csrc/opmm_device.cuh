@@ -36,6 +36,7 @@ struct SpaceDev {
   int32_t mode;          // 0 random (Philox), 1 grid
   uint32_t key0, key1;   // Philox key = seed
   int32_t all_physical;  // host proved every candidate of the space physical
+  int32_t model;         // 0 = 18-parameter, 1 = 9-parameter (D7 expansion)
   // 0 fixed (lo), 1 linear, 2 log with table exp (argument < 8), 3 log with libm exp
   uint8_t kind[NP];
   double lo[NP];
@@ -141,6 +142,21 @@ __device__ __forceinline__ double map_word(const SpaceDev& sp, int d, uint32_t w
 #endif
 }
 
+// 9-parameter OPMM (Table 2) in the 18-vector, SPEC D7
+// (SPEC.md:132): shared K_SE / K_LT, canonical pulse 55 / 0.5 g of width
+// pw_default (PW NaN), Table 1 time constants (reading Q23).
+__device__ __forceinline__ void expand_9param(double p[NP]) {
+  p[KSE_ANT] = p[KSE_AG];
+  p[KLT_ANT] = p[KLT_AG];
+  p[TAU_AC_AG] = 11.7;
+  p[TAU_AC_ANT] = 2.4;
+  p[TAU_DE_AG] = 2.0;
+  p[TAU_DE_ANT] = 1.9;
+  p[NSAC_AG] = 55.0;
+  p[NSAC_ANT] = 0.5;
+  p[PW_] = __longlong_as_double(0x7ff8000000000000LL);
+}
+
 // Candidate index -> OPC vector (PAPER.md:202 exhaustive search over OPC values).
 // Random mode is fully unrolled: the five Philox blocks and the 17 exp() are
 // independent dependency chains, so the scheduler can overlap them (the
@@ -160,6 +176,7 @@ __device__ __forceinline__ void generate_opc(const SpaceDev& sp, uint32_t saccad
     }
 #pragma unroll
     for (int d = 0; d < NP; ++d) p[d] = map_word(sp, d, ws[d], tab);
+    if (sp.model == 1) expand_9param(p);
   } else {
     uint64_t rem = (uint64_t)idx;
 #pragma unroll 1
@@ -183,6 +200,7 @@ __device__ __forceinline__ void generate_opc(const SpaceDev& sp, uint32_t saccad
       for (int e = 0; e < NP; ++e)
         if (e == d) p[e] = v;
     }
+    if (sp.model == 1) expand_9param(p);
   }
 }
 

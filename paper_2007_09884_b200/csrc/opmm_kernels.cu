@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(OPMM_FIT_LB_THREADS, OPMM_FIT_LB_BLOCKS) fit_k
       const int64_t j0 = base + tid;
       int key = nbins - 1;                                          // padding lanes last
       if (j0 < a.end) {
-        const double pw = generate_pw(a.space, (uint32_t)sac, j0, tab);
+        const double pw = (a.space.model == 1 ? pwd : generate_pw(a.space, (uint32_t)sac, j0, tab));
         const double npd = ceil(pw / a.ctl.dt_ms);
         const int np = npd > (double)a.ctl.n_steps ? a.ctl.n_steps + 1 : (int)npd;
         key = min(np >> 1, nbins - 2);
@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(FIT2_THREADS, 1) fit2_kernel(FitArgs a) {
       const int64_t j0 = base + tid + c * blockDim.x;
       key[c] = 255;
       if (j0 < a.end) {
-        const double pw = generate_pw(a.space, (uint32_t)sac, j0, tab);
+        const double pw = (a.space.model == 1 ? pwd : generate_pw(a.space, (uint32_t)sac, j0, tab));
         const double npd = ceil(pw / a.ctl.dt_ms);
         const int np = npd > (double)a.ctl.n_steps ? a.ctl.n_steps + 1 : (int)npd;
         key[c] = min(np >> 1, 254);
@@ -513,7 +513,7 @@ __global__ void __launch_bounds__(FIT3_THREADS, 1) fit3_kernel(FitArgs a) {
         const int64_t j0 = rbase + pt + 128 * c;
         key[c] = 255;
         if (j0 < a.end) {
-          const double pw_ms = generate_pw(a.space, (uint32_t)sac, j0, tab);
+          const double pw_ms = (a.space.model == 1 ? pwd : generate_pw(a.space, (uint32_t)sac, j0, tab));
           const double npd = ceil(pw_ms / a.ctl.dt_ms);
           const int npl = npd > (double)a.ctl.n_steps ? a.ctl.n_steps + 1 : (int)npd;
           key[c] = min(npl >> 1, 254);

@@ -43,7 +43,7 @@ class Control(C.Structure):
 
 
 class SearchSpace(C.Structure):
-    _fields_ = [("mode", C.c_int32), ("pad_", C.c_int32), ("seed", C.c_uint64),
+    _fields_ = [("mode", C.c_int32), ("model", C.c_int32), ("seed", C.c_uint64),
                 ("lo", C.c_double * NPARAM), ("hi", C.c_double * NPARAM),
                 ("log_scale", C.c_uint8 * NPARAM), ("pad2_", C.c_uint8 * 6),
                 ("levels", C.c_int32 * NPARAM)]
@@ -158,6 +158,7 @@ def search_space(s) -> SearchSpace:
     """SearchSpace from any object with mode/seed/lo/hi/log_scale/levels."""
     out = SearchSpace()
     out.mode = int(s.mode)
+    out.model = int(getattr(s, "model", 0))
     out.seed = int(s.seed)
     for d in range(NPARAM):
         out.lo[d] = float(s.lo[d])

@@ -588,3 +588,27 @@ print("nccl-single-rank ok")
                        timeout=300)
     assert p.returncode == 0, p.stdout + p.stderr
     assert "nccl-single-rank ok" in p.stdout
+
+
+
+def test_nine_param_model_fit_and_generator(opmm, h):
+    """9-parameter OPMM (Table 2 + D7): generated candidates and every error of
+    a fit match the oracle; TRUTH-like data is fitted near the default."""
+    sp = W.paper_space_9()
+    n = 4096
+    out = torch.zeros((18, n), dtype=torch.float64, device="cuda")
+    opmm.opmm_generate(h, sp, 0, n, out, stream=torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    g = out.cpu().numpy().T
+    o = oracle.generate_batch(sp, 0, n)
+    assert np.array_equal(np.isnan(g), np.isnan(o))
+    f = ~np.isnan(o)
+    assert np.max(np.abs(g[f] - o[f]) / np.abs(o[f])) <= 2 * ULP
+    ctl = W.Control()
+    rec = trace(ctl)
+    r, E = _fit(opmm, h, rec, ctl, sp, 20000)
+    orc = oracle.fit(rec, ctl, sp, 0, 20000, want_err=True)
+    rel, _, _ = oracle.relativize(rec, ctl.amplitude_deg)
+    assert_fp64_errors(E, orc["err"], lambda i: oracle.generate(sp, i), rec, ctl, np.abs(rel).sum())
+    assert r["best_index"] == orc["best_index"]
+    assert np.isnan(r["opc"][I["PW"]]) and r["opc"][I["K_SE_ANT"]] == r["opc"][I["K_SE_AG"]]

@@ -544,3 +544,43 @@ def test_referee_longdouble_agrees_with_oracle_on_stable_candidates():
     # TRUTH on its own clean output: both ~0
     rec0 = oracle.positions(W.truth_opc(), ctl)
     assert referee.objective_longdouble(W.truth_opc(), rec0, ctl) < 1e-10
+
+
+# --------------------------------------------------------------------------- 9-parameter model
+def test_nine_param_expansion_d7_and_table2():
+    """Table 2 inside the 18-vector per SPEC D7: shared
+    K_SE / K_LT, canonical pulse 55 / 0.5 g of width "duration - 6 ms" (PW
+    NaN), Table 1 time constants (reading Q23).  The Table 2 defaults expand
+    to exactly the Table 1 defaults, so the 9-parameter default scores the
+    TRUTH trace like the 18-parameter default."""
+    p = np.ones(18)
+    for name, d in zip(W.NINE_SLOTS, W.TABLE2_DEFAULTS):
+        p[I[name]] = d
+    e = oracle.expand_9param(p)
+    assert e[I["K_SE_ANT"]] == e[I["K_SE_AG"]] == 2.5
+    assert e[I["K_LT_ANT"]] == e[I["K_LT_AG"]] == 1.2
+    assert (e[I["N_SAC_AG"]], e[I["N_SAC_ANT"]]) == (55.0, 0.5)
+    assert math.isnan(e[I["PW"]])
+    d1 = np.array(W.TABLE1_DEFAULTS)
+    assert np.array_equal(e[:17], d1[:17])
+    ctl = W.Control()
+    rec = oracle.positions(W.truth_opc(), ctl)
+    assert oracle.objective(e, rec, ctl) == oracle.objective(W.truth_opc(), rec, ctl)
+
+
+def test_nine_param_generator_draws_only_free_slots():
+    sp = W.paper_space_9()
+    c = oracle.generate_batch(sp, 0, 500)
+    for name in W.NINE_SLOTS:
+        i = I[name]
+        assert np.all((c[:, i] >= sp.lo[i]) & (c[:, i] <= sp.hi[i]))
+        assert np.unique(c[:, i]).size > 400
+    assert np.array_equal(c[:, I["K_SE_ANT"]], c[:, I["K_SE_AG"]])
+    assert np.array_equal(c[:, I["K_LT_ANT"]], c[:, I["K_LT_AG"]])
+    assert np.all(c[:, I["TAU_AC_AG"]] == 11.7) and np.all(np.isnan(c[:, I["PW"]]))
+    # the 9 free slots are the same Philox words the 18-parameter generator uses
+    sp18 = W.paper_space()
+    sp18.lo[:], sp18.hi[:], sp18.log_scale[:] = sp.lo, sp.hi, sp.log_scale
+    c18 = oracle.generate_batch(sp18, 0, 50)
+    for name in W.NINE_SLOTS:
+        assert np.array_equal(c18[:, I[name]], c[:50, I[name]])

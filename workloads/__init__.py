@@ -65,6 +65,7 @@ class SearchSpace:
     hi: np.ndarray                 # [18] float64
     log_scale: np.ndarray          # [18] uint8
     levels: np.ndarray             # [18] int32 (grid mode; product = N)
+    model: int = 0                 # 0 = 18-parameter (Table 1), 1 = 9-parameter (Table 2, D7)
 
     def n_grid(self) -> int:
         return int(np.prod(self.levels.astype(np.int64)))
@@ -143,3 +144,22 @@ def population(S: int, seed: int = SEED_POPULATION):
         f = np.exp(rng.uniform(math.log(0.8), math.log(1.2), size=S))
         truths[:, IDX[name]] *= f
     return amp, pw, truths
+
+
+# 9-parameter OPMM (Table 2) in the 18-vector slots: the free
+# parameters K_SE (slot K_SE_AG), K_LT (slot K_LT_AG), B_AG, B_ANT, B_P,
+# N_C_AG, N_C_ANT, J, N_C_FIX; the others are set by the D7 expansion.
+NINE_SLOTS = ("K_SE_AG", "K_LT_AG", "B_AG", "B_ANT", "B_P", "N_C_AG", "N_C_ANT", "J", "N_C_FIX")
+
+
+def paper_space_9(seed: int = SEED_PAPER_SPACE) -> SearchSpace:
+    """S_paper for the 9-parameter model: log-uniform [0.1x, 10x] of Table 2
+    over the 9 free parameters; all other slots fixed (the generator's D7
+    expansion overwrites them)."""
+    lo = np.ones(NPARAM)
+    hi = np.ones(NPARAM)
+    log_scale = np.zeros(NPARAM, dtype=np.uint8)
+    for name, d in zip(NINE_SLOTS, TABLE2_DEFAULTS):
+        i = IDX[name]
+        lo[i], hi[i], log_scale[i] = 0.1 * d, 10.0 * d, 1
+    return SearchSpace(0, seed, lo, hi, log_scale, np.ones(NPARAM, dtype=np.int32), model=1)

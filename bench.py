@@ -192,6 +192,46 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def population_traces(h, opmm, torch, S, n_steps):
+    """Config-5 population (workloads.population): each saccade simulated at its
+    own amplitude with opmm_simulate (input generation), plus N(0, 0.02 deg)."""
+    amp, pw, truths = W.population(S)
+    ctls = [W.Control(n_steps=n_steps, amplitude_deg=float(a), pw_default_ms=float(p))
+            for a, p in zip(amp, pw)]
+    opc = torch.as_tensor(np.ascontiguousarray(truths.T), device="cuda")
+    traj = torch.zeros((n_steps + 1, S), dtype=torch.float64, device="cuda")
+    col = torch.zeros(n_steps + 1, dtype=torch.float64, device="cuda")
+    for s in range(S):
+        opmm.opmm_simulate(h, opc[:, s].contiguous(), 1, ctls[s], col, stream=torch.cuda.current_stream())
+        traj[:, s] = col
+    torch.cuda.synchronize()
+    recs = traj.cpu().numpy().T.copy()
+    recs += np.random.default_rng(W.SEED_NOISE).normal(0.0, 0.02, size=recs.shape)
+    return ctls, recs
+
+
+def population_leg(h, opmm, torch, args):
+    """Config 5 (BASELINE.json configs[4]) on one GPU: S synthetic saccades x
+    n_per candidates each through opmm_fit_batch (S_paper over n_steps = 150,
+    Philox counter word 2 = saccade).  Device time of the fit kernel (CUDA
+    events), 1 warm-up + 2 timed launches."""
+    S, n_per, n_steps = args.pop_saccades, args.pop_candidates, 150
+    ctls, recs = population_traces(h, opmm, torch, S, n_steps)
+    sp = W.paper_space(n_steps=n_steps)
+    opts = opmm.fit_options(cpu_check=0)
+    ms = []
+    for rep in range(3):
+        res = opmm.opmm_fit_batch(h, recs, ctls, sp, n_per, opts)
+        if rep > 0:
+            ms.append(opmm.opmm_last_kernel_ms(h))
+    kern = sum(ms) / len(ms)
+    f = np.array([r["opt_err"] for r in res])
+    return {"metric": "OPC candidate sims/s (population)", "value": S * n_per / (kern * 1e-3),
+            "saccades": S, "candidates_per_saccade": n_per, "n_steps": n_steps,
+            "kernel_ms": kern, "saccades_per_s": S / (kern * 1e-3),
+            "mean_best_residual_deg_per_sample": float(np.mean(f / (n_steps + 1)))}
+
+
 def nm_leg(h, opmm, torch, args):
     """The paper's own estimator (batched parallel Nelder-Mead)
     on a synthetic population (SURVEY 8(d) config 5 recipe: A ~ U[5, 30] deg,
@@ -201,20 +241,7 @@ def nm_leg(h, opmm, torch, args):
     -- the unit of the paper's Table 3 -- kernel time
     (CUDA events) and end-to-end through the synchronous opmm_estimate_batch."""
     S, n_steps = args.nm_saccades, 150
-    amp, pw, truths = W.population(S)
-    ctls = [W.Control(n_steps=n_steps, amplitude_deg=float(a), pw_default_ms=float(p))
-            for a, p in zip(amp, pw)]
-    opc = torch.as_tensor(np.ascontiguousarray(truths.T), device="cuda")
-    # the amplitude is a control field, so each saccade is one opmm_simulate call
-    traj = torch.zeros((n_steps + 1, S), dtype=torch.float64, device="cuda")
-    col = torch.zeros(n_steps + 1, dtype=torch.float64, device="cuda")
-    for s in range(S):
-        opmm.opmm_simulate(h, opc[:, s].contiguous(), 1, ctls[s], col, stream=torch.cuda.current_stream())
-        traj[:, s] = col
-    torch.cuda.synchronize()
-    recs = traj.cpu().numpy().T.copy()
-    rng = np.random.default_rng(W.SEED_NOISE)
-    recs += rng.normal(0.0, 0.02, size=recs.shape)
+    ctls, recs = population_traces(h, opmm, torch, S, n_steps)
     opts = opmm.nm_options(cpu_check=0)
     opmm.opmm_estimate_batch(h, recs[:64], ctls[:64], options=opts)   # warm-up
     t0 = time.perf_counter()
@@ -322,6 +349,7 @@ def run_gpu(args):
     e2e_ms = max_over_ranks(1e3 * sum(t_e2e) / len(t_e2e))
 
     nm = nm_leg(h, opmm, torch, args) if not args.no_nm else None
+    pop = population_leg(h, opmm, torch, args) if (not args.no_pop and world == 1) else None
 
     per_cand_flop = FLOP_PER_STEP * N_STEPS + FLOP_SETUP
     achieved = per_cand_flop * args.per_gpu / (kms64 * 1e-3) / 1e12
@@ -356,6 +384,8 @@ def run_gpu(args):
     }
     if nm is not None:
         line["nm"] = nm
+    if pop is not None:
+        line["population"] = pop
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline()
     if rank == 0:
@@ -375,6 +405,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-nm", action="store_true")
     ap.add_argument("--nm-saccades", type=int, default=4096)
+    ap.add_argument("--no-pop", action="store_true")
+    ap.add_argument("--pop-saccades", type=int, default=10000)
+    ap.add_argument("--pop-candidates", type=int, default=100000)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -370,6 +370,12 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
   // fit3 work unit per block pass: 8 consumer warps x 32 candidates
   const int64_t work = three ? (e - b + 255) / 256 * block : two ? (e - b + 1) / 2 : e - b;
   CKS(grid_for(h, fn, block, smem, work, opts ? opts->grid_blocks : 0, &grid));
+  if (S > 1 && !(opts && opts->grid_blocks)) {
+    // population batch: gridDim.y = saccades already fills the GPU, so give
+    // each block one tile of its saccade instead of a persistent stride
+    const int64_t tiles = (work + block - 1) / block;
+    grid = (int)(tiles < 65535 ? (tiles > 0 ? tiles : 1) : 65535);
+  }
   if (e <= b) grid = 1;  // empty shard: one block reports "no candidate"
   const bool multi = shard && h->comm != nullptr;   // world > 1 (or a 1-rank test comm)
   CKS(ensure(h->partials, h->partials_cap, (size_t)grid * (size_t)(s_begin + S)));

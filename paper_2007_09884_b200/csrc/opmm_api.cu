@@ -24,7 +24,7 @@ using opmm::Partial;
 static_assert(sizeof(opmm_control) == 40, "opmm_control layout");
 static_assert(sizeof(opmm_search_space) == 400, "opmm_search_space layout");
 static_assert(sizeof(opmm_fit_options) == 40, "opmm_fit_options layout");
-static_assert(sizeof(opmm_fit_result) == 184, "opmm_fit_result layout");
+static_assert(sizeof(opmm_fit_result) == 320, "opmm_fit_result layout");
 static_assert(sizeof(Partial) == 32, "Partial layout");
 static_assert(sizeof(opmm_nm_options) == 48, "opmm_nm_options layout");
 static_assert(sizeof(opmm_nm_result) == 176, "opmm_nm_result layout");
@@ -117,6 +117,8 @@ struct opmm_handle {
   size_t rank_part_cap = 0;
   Partial* gathered = nullptr;
   size_t gathered_cap = 0;
+  opmm::CertPartial* cert_parts = nullptr;
+  size_t cert_parts_cap = 0;
   opmm_fit_result* result = nullptr;
   size_t result_cap = 0;
   opmm_fit_result* result_host = nullptr;  // pinned
@@ -361,7 +363,14 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
   int64_t b = 0, e = n_candidates;
   if (shard) opmm_shard_range(n_candidates, h->rank, h->world, &b, &e);
   const int32_t ns = ctl->n_steps + 1;
-  const size_t smem = three ? opmm::fit3_smem(precision, ns) : fit_smem(precision, ns, block, two ? 2 : 1);
+  // FP32 certification (top-8 + fp64 re-score): single fit on one GPU, fit1
+  const bool certify = opts && opts->certify && precision == OPMM_FP32;
+  if (certify && (two || three || S != 1 || (shard && h->comm != nullptr)))
+    return fail(OPMM_ERR_UNSUPPORTED, "certify needs a single fit on one GPU with kernel_variant 0/1");
+  size_t smem = three ? opmm::fit3_smem(precision, ns) : fit_smem(precision, ns, block, two ? 2 : 1);
+  if (certify)   // per-thread lists + last-block scratch (grid <= block lists, rel64, fp64 stash)
+    smem += opmm::cert_list_bytes(block) + (size_t)2 * 8 * block * 8 + (((size_t)ns + 1) & ~(size_t)1) * 8 +
+            (size_t)20 * 32 * 8;
   if (smem > kMaxDynSmem) return fail(OPMM_ERR_INVALID_ARG, "trace too long for shared memory");
   const void* fn = three ? opmm::fit3_kernel_ptr(precision, metric)
                          : two ? opmm::fit2_kernel_ptr(precision, metric)
@@ -377,6 +386,7 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
     grid = (int)(tiles < 65535 ? (tiles > 0 ? tiles : 1) : 65535);
   }
   if (e <= b) grid = 1;  // empty shard: one block reports "no candidate"
+  if (certify && grid > block) grid = block;  // the last block merges one list per thread
   const bool multi = shard && h->comm != nullptr;   // world > 1 (or a 1-rank test comm)
   CKS(ensure(h->partials, h->partials_cap, (size_t)grid * (size_t)(s_begin + S)));
   CKS(ensure(h->counters, h->counters_cap, (size_t)(s_begin + S), true));
@@ -399,6 +409,11 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
   a.err_out = opts ? opts->err_out : nullptr;
   a.err_ld = n_candidates;
   a.sort_lanes = getenv("OPMM_NO_LANE_SORT") ? 0 : 1;   // env switch for A/B timing only
+  if (certify) {
+    CKS(ensure(h->cert_parts, h->cert_parts_cap, (size_t)grid * (size_t)(s_begin + S)));
+    a.certify = 1;
+    a.cert_partials = h->cert_parts;
+  }
   a.partials = h->partials;
   a.counters = h->counters;
   a.rank_out = multi ? h->rank_part : nullptr;
@@ -664,6 +679,7 @@ opmm_status opmm_destroy(opmm_handle* h) {
   cudaFree(h->sacctl);
   cudaFree(h->rank_part);
   cudaFree(h->gathered);
+  cudaFree(h->cert_parts);
   cudaFree(h->result);
   cudaFree(h->exp_tab);
   cudaFree(h->nm_x0);

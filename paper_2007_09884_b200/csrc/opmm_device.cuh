@@ -878,7 +878,8 @@ template <typename T, int INTEG, int METRIC, bool TRAJ>
 __device__ __forceinline__ double evaluate(const double p[NP], const CtlDev& c, double Aprime,
                                            double pw_default, const T* rel, T* traj,
                                            int64_t ld_out, double sgn, uint8_t* status,
-                                           T* stash, bool check_physical = true) {
+                                           T* stash, bool check_physical = true,
+                                           int stash_ld = -1) {
   // generated candidates skip the check when the host proved the whole
   // search space physical (SpaceDev::all_physical).  A non-physical candidate
   // still runs the (meaningless) recurrence before its penalty is returned:
@@ -915,7 +916,8 @@ __device__ __forceinline__ double evaluate(const double p[NP], const CtlDev& c, 
     make_prop<T>(s, pr);
 #endif
     acc = run_propagator<T, METRIC, TRAJ>(pr, s.n_pulse, c.n_steps, rel, traj, ld_out,
-                                          (T)c.theta0, (T)sgn, stash, blockDim.x);
+                                          (T)c.theta0, (T)sgn, stash,
+                                          stash_ld < 0 ? (int)blockDim.x : stash_ld);
   } else {
     acc = run_rk4_stages<T, METRIC, TRAJ>(s, c.n_steps, rel, traj, ld_out, (T)c.theta0, (T)sgn);
   }

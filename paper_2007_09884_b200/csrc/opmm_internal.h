@@ -31,6 +31,15 @@ struct Partial {
   int64_t neval;  // evaluated candidates (rank partials only)
 };
 
+// FP32 certification: one block's (or rank's) top-8 by fp32 error
+constexpr int CERT_KK = 8;
+__host__ __device__ constexpr size_t cert_list_bytes(int block) { return (size_t)CERT_KK * block * 16; }
+struct CertPartial {
+  double e[8];
+  int64_t i[8];
+  int64_t nf;
+};
+
 struct FitArgs {
   const double* rec;        // device [S][n_steps+1]
   const double2* exp_tab;   // device [EXP_TAB_N] (handle-owned)
@@ -44,6 +53,8 @@ struct FitArgs {
   double* err_out;          // optional device, indexed [sac * err_ld + i]
   int64_t err_ld;
   int32_t sort_lanes;       // counting-sort tiles by pulse end (see fit_kernel)
+  int32_t certify;          // fp32: top-8 + fp64 re-score (fit_kernel only)
+  CertPartial* cert_partials;  // [S][gridDim.x] when certify
   Partial* partials;        // [S][gridDim.x]
   unsigned int* counters;   // [S], zero between launches
   Partial* rank_out;        // optional [S]: per-rank result (world > 1)

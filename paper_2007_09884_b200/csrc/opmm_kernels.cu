@@ -52,19 +52,14 @@ __device__ void write_result(const SpaceDev& sp, uint32_t saccade, double e, int
   out->cpu_check = __longlong_as_double(0x7ff8000000000000LL);
   out->n_finite = nf;
   out->n_evaluated = neval;
+  out->top_k = 0;
+  out->certified = 0;
   double p[NP];
   if (ok) generate_opc(sp, saccade, i, p, tab);
 #pragma unroll
   for (int d = 0; d < NP; ++d) out->opc[d] = ok ? p[d] : __longlong_as_double(0x7ff8000000000000LL);
 }
 
-// ---------------------------------------------------------------------------
-// The fused fit kernel.  gridDim.y = saccades of this launch (1 for a single
-// fit); blockIdx.x strides over the candidate range [begin, end) of each.
-// ---------------------------------------------------------------------------
-// The simulate kernels are register-heavy (per-candidate setup peaks near
-// 240 live registers): 384 threads x 168 registers, 3 warps per scheduler,
-// measured best among 128/168/238-register budgets.
 // Block (E, idx, n_finite) reduction -> one partial per block; the last
 // block of a saccade (threadfence + atomic ticket) reduces the partials and
 // writes the rank partial (world > 1) or the final result with the winner's
@@ -106,6 +101,158 @@ __device__ __forceinline__ void fit_epilogue(const FitArgs& a, int64_t sac, doub
                    a.exp_tab);
   }}
 
+// ---------------------------------------------------------------------------
+// FP32 certification (opmm_fit_options.certify, fit1 / fp32 only): every
+// thread keeps its CERT_K best (E32, index) pairs in shared memory; the block
+// and then the last block merge them (CERT_K rounds of block argmin) into the
+// global top-K by the fp32 error; warp 0 of the last block re-scores those K
+// candidates in fp64 (same evaluator as the fp64 fit) and the fit returns the
+// fp64-best of them.  "certified" says the fp32 ranking cannot have hidden the
+// fp64 winner: fewer than K finite candidates, or E32[K-1] - E32[0] > 2 delta
+// with delta = 1e-4 max(E32[0], sum |rel|), the fp32 error budget (DESIGN.md
+// section 6; SURVEY 8(c) "FP32 best fit").
+// ---------------------------------------------------------------------------
+constexpr int CERT_K = CERT_KK;
+
+// smem of the certification lists: [CERT_K][block] (double e, int64 idx)
+__host__ __device__ constexpr size_t cert_bytes(int block) { return cert_list_bytes(block); }
+
+__device__ __forceinline__ void topk_insert(double* le, int64_t* li, int ld, double e, int64_t i) {
+  if (!better(e, i, le[(CERT_K - 1) * ld], li[(CERT_K - 1) * ld])) return;
+  int k = CERT_K - 1;
+  while (k > 0 && better(e, i, le[(k - 1) * ld], li[(k - 1) * ld])) {
+    le[k * ld] = le[(k - 1) * ld];
+    li[k * ld] = li[(k - 1) * ld];
+    --k;
+  }
+  le[k * ld] = e;
+  li[k * ld] = i;
+}
+
+// K rounds of block argmin over per-thread sorted lists (thread t owns list
+// t, ld apart, cnt[t] entries); out_e/out_i[K] in shared memory.
+__device__ void block_topk(const double* le, const int64_t* li, int ld, int nlists, int cnt,
+                           double* out_e, int64_t* out_i) {
+  int ptr = 0;
+  for (int r = 0; r < CERT_K; ++r) {
+    double e = __longlong_as_double(0x7ff0000000000000LL);
+    int64_t i = INT64_MAX, dummy = 0;
+    if ((int)threadIdx.x < nlists && ptr < cnt) {
+      e = le[ptr * ld + threadIdx.x];
+      i = li[ptr * ld + threadIdx.x];
+    }
+    const double me = e;
+    const int64_t mi = i;
+    block_argmin(e, i, dummy);
+    __shared__ double s_e;
+    __shared__ int64_t s_i;
+    if (threadIdx.x == 0) { s_e = e; s_i = i; }
+    __syncthreads();
+    if (me == s_e && mi == s_i && mi != INT64_MAX) ++ptr;
+    if (threadIdx.x == 0) { out_e[r] = s_e; out_i[r] = s_i; }
+    __syncthreads();
+  }
+}
+
+template <typename T, int METRIC>
+__device__ void cert_epilogue(const FitArgs& a, int64_t sac, double* le, int64_t* li,
+                              unsigned char* scratch, int64_t nf, double sgn, double Aprime,
+                              double pwd) {
+  __shared__ double b_e[CERT_K];
+  __shared__ int64_t b_i[CERT_K];
+  __shared__ bool is_last;
+  int64_t nfb = nf, d1 = 0;
+  double de = 0.0;
+  int64_t di = 0;
+  // block n_finite
+  {
+    double e = 0.0;
+    int64_t i = 0;
+    block_argmin(e, i, nfb);   // reuses the reduction for the sum in thread 0
+    (void)de; (void)di; (void)d1;
+  }
+  __shared__ int64_t s_nf;
+  if (threadIdx.x == 0) s_nf = nfb;
+  __syncthreads();
+  block_topk(le, li, blockDim.x, blockDim.x, CERT_K, b_e, b_i);
+  CertPartial* parts = a.cert_partials + sac * (int64_t)gridDim.x;
+  if (threadIdx.x == 0) {
+    CertPartial q;
+    for (int k = 0; k < CERT_K; ++k) { q.e[k] = b_e[k]; q.i[k] = b_i[k]; }
+    q.nf = s_nf;
+    parts[blockIdx.x] = q;
+    __threadfence();
+    const unsigned int t = atomicAdd(a.counters + sac, 1u);
+    is_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  // merge the blocks' lists (thread b owns block b's list; gridDim <= blockDim)
+  double* ge = reinterpret_cast<double*>(scratch);                 // [CERT_K][grid]
+  int64_t* gi = reinterpret_cast<int64_t*>(ge + CERT_K * gridDim.x);
+  int64_t nft = 0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+    for (int k = 0; k < CERT_K; ++k) {
+      ge[k * gridDim.x + b] = __ldcg(&parts[b].e[k]);
+      gi[k * gridDim.x + b] = __ldcg(reinterpret_cast<const long long*>(&parts[b].i[k]));
+    }
+    nft += __ldcg(reinterpret_cast<const long long*>(&parts[b].nf));
+  }
+  {
+    double e = 0.0;
+    int64_t i = 0;
+    block_argmin(e, i, nft);
+  }
+  __shared__ int64_t s_nft;
+  if (threadIdx.x == 0) s_nft = nft;
+  __syncthreads();
+  block_topk(ge, gi, gridDim.x, gridDim.x, CERT_K, b_e, b_i);
+  // fp64 re-score of the K by warp 0 (all 32 lanes run the evaluator)
+  const int32_t ns = a.ctl.n_steps + 1;
+  double* rel64 = reinterpret_cast<double*>(gi + CERT_K * gridDim.x);
+  double* st64 = rel64 + ((ns + 1) & ~1);
+  const double* rec = a.rec + sac * (int64_t)ns;
+  for (int k = threadIdx.x; k < ns; k += blockDim.x) rel64[k] = sgn * (rec[k] - rec[0]);
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    const int kk = lane < CERT_K ? lane : 0;
+    const int64_t idx = b_i[kk];
+    double E64 = __longlong_as_double(0x7ff0000000000000LL);
+    double p[NP];
+    generate_opc(a.space, (uint32_t)sac, idx == INT64_MAX ? 0 : idx, p, a.exp_tab);
+    CtlDev c = a.ctl;
+    E64 = evaluate<double, 0, METRIC, false>(p, c, Aprime, pwd, rel64, nullptr, 0, sgn, nullptr,
+                                             st64, !a.space.all_physical, 32);
+    if (idx == INT64_MAX || !(b_e[kk] < __longlong_as_double(0x7ff0000000000000LL)))
+      E64 = __longlong_as_double(0x7ff0000000000000LL);
+    double e = lane < CERT_K ? E64 : __longlong_as_double(0x7ff0000000000000LL);
+    int64_t i = lane < CERT_K ? idx : INT64_MAX;
+    const double myE64 = E64;
+    warp_argmin(e, i);
+    if (lane == 0) {
+      a.counters[sac] = 0;   // re-arm (graph-replay safe)
+      const int64_t neval = a.end - a.begin;
+      opmm_fit_result* out = a.final_out + (sac - a.out_base);
+      write_result(a.space, (uint32_t)sac, e, i, s_nft, neval, out, a.exp_tab);
+      // sum |rel| for the fp32 error budget
+      double srel = 0.0;
+      for (int k = 0; k < ns; ++k) srel += fabs(rel64[k]);
+      const double delta = 1e-4 * fmax(b_e[0], srel);
+      const bool all_in = s_nft < CERT_K;
+      out->top_k = CERT_K;
+      out->certified = (all_in || (b_e[CERT_K - 1] - b_e[0] > 2.0 * delta)) ? 1 : 0;
+    }
+    __syncwarp();
+    if (lane < CERT_K) {
+      opmm_fit_result* out = a.final_out + (sac - a.out_base);
+      out->topk_index[lane] = idx == INT64_MAX ? -1 : idx;
+      out->topk_err[lane] = myE64;
+    }
+  }
+}
+
 #ifndef OPMM_FIT_LB_THREADS
 #define OPMM_FIT_LB_THREADS 384
 #endif
@@ -113,13 +260,31 @@ __device__ __forceinline__ void fit_epilogue(const FitArgs& a, int64_t sac, doub
 #define OPMM_FIT_LB_BLOCKS 1
 #endif
 
+// ---------------------------------------------------------------------------
+// The fused fit kernel.  gridDim.y = saccades of this launch (1 for a single
+// fit); blockIdx.x strides over the candidate range [begin, end) of each.
+// 384 threads x 168 registers (the per-candidate setup peaks near 240 live
+// registers), 3 warps per scheduler: measured best among 128/168/238-register
+// budgets.
+// ---------------------------------------------------------------------------
 template <typename T, int INTEG, int METRIC>
 __global__ void __launch_bounds__(OPMM_FIT_LB_THREADS, OPMM_FIT_LB_BLOCKS) fit_kernel(FitArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int32_t ns = a.ctl.n_steps + 1;
   T* rel = reinterpret_cast<T*>(smem_raw);
   double2* tab = reinterpret_cast<double2*>(smem_raw + rel_bytes<T>(ns));
-  T* stash = reinterpret_cast<T*>(smem_raw + rel_bytes<T>(ns) + exp_tab_bytes());  // [8][block] vec2
+  T* stash = reinterpret_cast<T*>(smem_raw + rel_bytes<T>(ns) + exp_tab_bytes());  // [10][block] vec2
+  // certification lists follow the stash (fp32 + a.certify only)
+  unsigned char* cert_raw = smem_raw + rel_bytes<T>(ns) + exp_tab_bytes() + stash_bytes<T>(blockDim.x);
+  double* cert_e = reinterpret_cast<double*>(cert_raw);
+  int64_t* cert_i = reinterpret_cast<int64_t*>(cert_raw + (size_t)CERT_K * blockDim.x * 8);
+  const bool certify = sizeof(T) == 4 && a.certify;
+  if (certify) {
+    for (int k = 0; k < CERT_K; ++k) {
+      cert_e[k * blockDim.x + threadIdx.x] = __longlong_as_double(0x7ff0000000000000LL);
+      cert_i[k * blockDim.x + threadIdx.x] = INT64_MAX;
+    }
+  }
   for (int j = threadIdx.x; j < EXP_TAB_N; j += blockDim.x) tab[j] = a.exp_tab[j];
   const int64_t sac = (int64_t)blockIdx.y + a.sac_begin;
   const double amp = a.sac_ctl ? a.sac_ctl[2 * sac] : a.amplitude;
@@ -218,7 +383,14 @@ __global__ void __launch_bounds__(OPMM_FIT_LB_THREADS, OPMM_FIT_LB_BLOCKS) fit_k
       if (a.err_out) a.err_out[sac * a.err_ld + i] = E;
       nf += E < __longlong_as_double(0x7ff0000000000000LL) ? 1 : 0;
       if (better(E, i, best_e, best_i)) { best_e = E; best_i = i; }
+      if (certify) topk_insert(cert_e + threadIdx.x, cert_i + threadIdx.x, blockDim.x, E, i);
     }
+  }
+  if (sizeof(T) == 4 && a.certify) {
+    __syncthreads();
+    cert_epilogue<T, METRIC>(a, sac, cert_e, cert_i, cert_raw + cert_bytes(blockDim.x), nf, sgn,
+                             Aprime, pwd);
+    return;
   }
   fit_epilogue(a, sac, best_e, best_i, nf);
 }

@@ -52,17 +52,21 @@ class SearchSpace(C.Structure):
 class FitOptions(C.Structure):
     _fields_ = [("precision", C.c_int32), ("metric", C.c_int32), ("integrator", C.c_int32),
                 ("block_size", C.c_int32), ("grid_blocks", C.c_int32), ("cpu_check", C.c_int32),
-                ("kernel_variant", C.c_int32), ("pad_", C.c_int32), ("err_out", C.c_void_p)]
+                ("kernel_variant", C.c_int32), ("certify", C.c_int32), ("err_out", C.c_void_p)]
 
 
 class FitResult(C.Structure):
     _fields_ = [("best_index", C.c_int64), ("opt_err", C.c_double), ("cpu_check", C.c_double),
-                ("opc", C.c_double * NPARAM), ("n_finite", C.c_int64), ("n_evaluated", C.c_int64)]
+                ("opc", C.c_double * NPARAM), ("n_finite", C.c_int64), ("n_evaluated", C.c_int64),
+                ("top_k", C.c_int32), ("certified", C.c_int32), ("topk_index", C.c_int64 * 8),
+                ("topk_err", C.c_double * 8)]
 
     def as_dict(self) -> dict:
         return {"best_index": self.best_index, "opt_err": self.opt_err, "cpu_check": self.cpu_check,
                 "opc": np.array(self.opc[:]), "n_finite": self.n_finite,
-                "n_evaluated": self.n_evaluated}
+                "n_evaluated": self.n_evaluated, "top_k": self.top_k, "certified": self.certified,
+                "topk_index": list(self.topk_index[:self.top_k]),
+                "topk_err": list(self.topk_err[:self.top_k])}
 
 
 class NmOptions(C.Structure):
@@ -169,9 +173,9 @@ def search_space(s) -> SearchSpace:
 
 
 def fit_options(precision=FP64, metric=METRIC_L1, integrator=INTEG_PROPAGATOR, block_size=0,
-                grid_blocks=0, cpu_check=1, err_out=None, kernel_variant=0) -> FitOptions:
+                grid_blocks=0, cpu_check=1, err_out=None, kernel_variant=0, certify=0) -> FitOptions:
     return FitOptions(precision, metric, integrator, block_size, grid_blocks, cpu_check,
-                      kernel_variant, 0, _ptr(err_out) if err_out is not None else None)
+                      kernel_variant, certify, _ptr(err_out) if err_out is not None else None)
 
 
 def _ptr(x):

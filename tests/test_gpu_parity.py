@@ -612,3 +612,31 @@ def test_nine_param_model_fit_and_generator(opmm, h):
     assert_fp64_errors(E, orc["err"], lambda i: oracle.generate(sp, i), rec, ctl, np.abs(rel).sum())
     assert r["best_index"] == orc["best_index"]
     assert np.isnan(r["opc"][I["PW"]]) and r["opc"][I["K_SE_ANT"]] == r["opc"][I["K_SE_AG"]]
+
+
+def test_fp32_certified_fit(opmm, h):
+    """FP32 fit with certification: the fp32 top-8 (exactly the 8 smallest
+    fp32 errors, lexicographic) re-scored in fp64; the returned winner and
+    opt_err equal the fp64 fit's, and the run reports itself certified."""
+    ctl = W.Control()
+    rec = trace(ctl)
+    sp = W.paper_space()
+    n = 200000
+    r64, E64 = _fit(opmm, h, rec, ctl, sp, n, precision=opmm.FP64)
+    r32, E32 = _fit(opmm, h, rec, ctl, sp, n, precision=opmm.FP32)
+    rc = opmm.opmm_fit(h, rec, ctl, sp, n, opmm.fit_options(precision=opmm.FP32, certify=1))
+    order = np.lexsort((np.arange(n), E32))[:8]
+    assert rc["top_k"] == 8 and rc["topk_index"] == order.tolist()
+    assert rc["topk_err"] == E64[order].tolist()
+    assert rc["best_index"] == r64["best_index"] and rc["opt_err"] == r64["opt_err"]
+    assert rc["certified"] == 1
+    assert abs(rc["cpu_check"] - rc["opt_err"]) <= 1e-9 * rc["opt_err"]
+    # fewer finite candidates than K: trivially certified; unused slots -1
+    small = opmm.opmm_fit(h, rec, ctl, sp, 3, opmm.fit_options(precision=opmm.FP32, certify=1))
+    assert small["certified"] == 1 and small["topk_index"][3:] == [-1] * 5
+    # fp64 ignores certify; batches / other variants refuse it
+    assert opmm.opmm_fit(h, rec, ctl, sp, 1000, opmm.fit_options(certify=1))["top_k"] == 0
+    with pytest.raises(opmm.OpmmError) as ei:
+        opmm.opmm_fit(h, rec, ctl, sp, 1000, opmm.fit_options(precision=opmm.FP32, certify=1,
+                                                              kernel_variant=3))
+    assert ei.value.status == opmm.ERR_UNSUPPORTED

@@ -125,10 +125,11 @@ typedef struct {
                               3 = warp-specialised producer/consumer.  2 and 3
                               need PROPAGATOR, a physical-by-construction space
                               and block_size = 0        */
-  int32_t certify;      /* FP32 only: keep the top-8 candidates by fp32 error, re-score
-                           them in fp64 and return the fp64-best; result.certified = 1
-                           when the fp32 error budget (1e-4 relative) cannot have hidden
-                           the fp64 winner (single fit, one GPU, kernel_variant 0/1)   */
+  int32_t certify;      /* FP32 only: keep the 8 best candidates by fp32 error among
+                           every thread's best two, re-score them in fp64 and return
+                           the fp64-best; result.certified = 1 when the fp32 error
+                           budget (1e-4 relative) cannot have hidden the fp64 winner
+                           (single fit, one GPU, kernel_variant 0/1)    */
   double* err_out;      /* optional DEVICE [n]: E_i of every candidate (validation) */
 } opmm_fit_options;
 
@@ -142,7 +143,9 @@ typedef struct {
   int32_t top_k;                 /* certify: 8 (entries below), else 0             */
   int32_t certified;             /* certify: 1 if the fp64 winner is provably among
                                     the fp32 top-8           */
-  int64_t topk_index[8];         /* certify: fp32 top-8 indices (fp32 order)       */
+  int64_t topk_index[8];         /* certify: kept indices in (fp32 E, index) order;
+                                    -1 = unused.  Contains every candidate within
+                                    the certificate's T* when certified = 1      */
   double topk_err[8];            /* certify: their fp64 errors                     */
 } opmm_fit_result;
 

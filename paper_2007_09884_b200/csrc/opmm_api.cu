@@ -365,12 +365,11 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
   const int32_t ns = ctl->n_steps + 1;
   // FP32 certification (top-8 + fp64 re-score): single fit on one GPU, fit1
   const bool certify = opts && opts->certify && precision == OPMM_FP32;
+  constexpr int kCertMaxGrid = 256;
   if (certify && (two || three || S != 1 || (shard && h->comm != nullptr)))
     return fail(OPMM_ERR_UNSUPPORTED, "certify needs a single fit on one GPU with kernel_variant 0/1");
   size_t smem = three ? opmm::fit3_smem(precision, ns) : fit_smem(precision, ns, block, two ? 2 : 1);
-  if (certify)   // per-thread lists + last-block scratch (grid <= block lists, rel64, fp64 stash)
-    smem += opmm::cert_list_bytes(block) + (size_t)2 * 8 * block * 8 + (((size_t)ns + 1) & ~(size_t)1) * 8 +
-            (size_t)20 * 32 * 8;
+  if (certify) smem += opmm::cert_scratch_bytes(block, kCertMaxGrid, ns);
   if (smem > kMaxDynSmem) return fail(OPMM_ERR_INVALID_ARG, "trace too long for shared memory");
   const void* fn = three ? opmm::fit3_kernel_ptr(precision, metric)
                          : two ? opmm::fit2_kernel_ptr(precision, metric)
@@ -386,7 +385,7 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
     grid = (int)(tiles < 65535 ? (tiles > 0 ? tiles : 1) : 65535);
   }
   if (e <= b) grid = 1;  // empty shard: one block reports "no candidate"
-  if (certify && grid > block) grid = block;  // the last block merges one list per thread
+  if (certify && grid > kCertMaxGrid) grid = kCertMaxGrid;  // bounds the last block's smem staging
   const bool multi = shard && h->comm != nullptr;   // world > 1 (or a 1-rank test comm)
   CKS(ensure(h->partials, h->partials_cap, (size_t)grid * (size_t)(s_begin + S)));
   CKS(ensure(h->counters, h->counters_cap, (size_t)(s_begin + S), true));

@@ -33,11 +33,22 @@ struct Partial {
 
 // FP32 certification: one block's (or rank's) top-8 by fp32 error
 constexpr int CERT_KK = 8;
-__host__ __device__ constexpr size_t cert_list_bytes(int block) { return (size_t)CERT_KK * block * 16; }
+// certify scratch (one region, reused by stage): per-thread best two (E, idx)
+// + per-warp lists; in the last block, every block's list + chunk lists, then
+// the fp64 trace and stash of the re-score.  grid <= 256.
+__host__ __device__ constexpr size_t cert_max3(size_t x, size_t y, size_t z) {
+  return x > y ? (x > z ? x : z) : (y > z ? y : z);
+}
+__host__ __device__ constexpr size_t cert_scratch_bytes(int block, int grid, int32_t n_samples) {
+  return cert_max3((size_t)2 * block * 16 + (size_t)8 * ((block + 31) / 32) * 16,
+                   (size_t)8 * grid * 16 + (size_t)8 * ((grid + 31) / 32) * 16,
+                   (((size_t)n_samples + 1) & ~(size_t)1) * 8 + (size_t)20 * 32 * 8);
+}
 struct CertPartial {
   double e[8];
   int64_t i[8];
   int64_t nf;
+  double m2;   // min over the block's threads of their second-best fp32 error
 };
 
 struct FitArgs {

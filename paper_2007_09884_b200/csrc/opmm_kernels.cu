@@ -102,84 +102,76 @@ __device__ __forceinline__ void fit_epilogue(const FitArgs& a, int64_t sac, doub
   }}
 
 // ---------------------------------------------------------------------------
-// FP32 certification (opmm_fit_options.certify, fit1 / fp32 only): every
-// thread keeps its CERT_K best (E32, index) pairs in shared memory; the block
-// and then the last block merge them (CERT_K rounds of block argmin) into the
-// global top-K by the fp32 error; warp 0 of the last block re-scores those K
-// candidates in fp64 (same evaluator as the fp64 fit) and the fit returns the
-// fp64-best of them.  "certified" says the fp32 ranking cannot have hidden the
-// fp64 winner: fewer than K finite candidates, or E32[K-1] - E32[0] > 2 delta
-// with delta = 1e-4 max(E32[0], sum |rel|), the fp32 error budget (DESIGN.md
-// section 6; SURVEY 8(c) "FP32 best fit").
+// FP32 certification (opmm_fit_options.certify, fit1 / fp32 only).  Every
+// thread keeps its two best (E32, index) pairs in registers; warps, blocks
+// and finally the last block merge them into the global top-8 by fp32 error
+// (8 rounds of warp argmin over sorted list heads -- no block barriers per
+// round), and the minimum over all threads of their SECOND-best error, m2,
+// is reduced alongside.  Warp 0 of the last block re-scores the 8 in fp64
+// (the fp64 fit's evaluator) and the fit returns the fp64-best of them.
+// Certificate: with T* = E32[0] + 2 delta, delta =
+// 1e-4 max(E32[0], sum |rel|) the fp32 error budget, every candidate within
+// T* is in the list iff m2 > T* (no thread dropped one) and E32[7] > T* (no
+// merge stage dropped one) -- or fewer than 8 finite candidates exist.
 // ---------------------------------------------------------------------------
 constexpr int CERT_K = CERT_KK;
 
-// smem of the certification lists: [CERT_K][block] (double e, int64 idx)
-__host__ __device__ constexpr size_t cert_bytes(int block) { return cert_list_bytes(block); }
-
-__device__ __forceinline__ void topk_insert(double* le, int64_t* li, int ld, double e, int64_t i) {
-  if (!better(e, i, le[(CERT_K - 1) * ld], li[(CERT_K - 1) * ld])) return;
-  int k = CERT_K - 1;
-  while (k > 0 && better(e, i, le[(k - 1) * ld], li[(k - 1) * ld])) {
-    le[k * ld] = le[(k - 1) * ld];
-    li[k * ld] = li[(k - 1) * ld];
-    --k;
-  }
-  le[k * ld] = e;
-  li[k * ld] = i;
-}
-
-// K rounds of block argmin over per-thread sorted lists (thread t owns list
-// t, ld apart, cnt[t] entries); out_e/out_i[K] in shared memory.
-__device__ void block_topk(const double* le, const int64_t* li, int ld, int nlists, int cnt,
-                           double* out_e, int64_t* out_i) {
+// 8 rounds of warp argmin over per-lane sorted lists: lane l holds cnt
+// entries at (le[k * ld], li[k * ld]), k < cnt; results in out_e/out_i (lane 0).
+__device__ __forceinline__ void warp_topk(const double* le, const int64_t* li, int ld, int cnt,
+                                          double* out_e, int64_t* out_i) {
   int ptr = 0;
   for (int r = 0; r < CERT_K; ++r) {
-    double e = __longlong_as_double(0x7ff0000000000000LL);
-    int64_t i = INT64_MAX, dummy = 0;
-    if ((int)threadIdx.x < nlists && ptr < cnt) {
-      e = le[ptr * ld + threadIdx.x];
-      i = li[ptr * ld + threadIdx.x];
-    }
+    double e = ptr < cnt ? le[ptr * ld] : __longlong_as_double(0x7ff0000000000000LL);
+    int64_t i = ptr < cnt ? li[ptr * ld] : INT64_MAX;
     const double me = e;
     const int64_t mi = i;
-    block_argmin(e, i, dummy);
-    __shared__ double s_e;
-    __shared__ int64_t s_i;
-    if (threadIdx.x == 0) { s_e = e; s_i = i; }
-    __syncthreads();
-    if (me == s_e && mi == s_i && mi != INT64_MAX) ++ptr;
-    if (threadIdx.x == 0) { out_e[r] = s_e; out_i[r] = s_i; }
-    __syncthreads();
+    warp_argmin(e, i);
+    if (me == e && mi == i && mi != INT64_MAX) ++ptr;
+    if ((threadIdx.x & 31) == 0) { out_e[r] = e; out_i[r] = i; }
   }
 }
 
 template <typename T, int METRIC>
-__device__ void cert_epilogue(const FitArgs& a, int64_t sac, double* le, int64_t* li,
-                              unsigned char* scratch, int64_t nf, double sgn, double Aprime,
-                              double pwd) {
+__device__ void cert_epilogue(const FitArgs& a, int64_t sac, double e1, int64_t i1, double e2,
+                              int64_t i2, int64_t nf, double sgn, double Aprime, double pwd,
+                              unsigned char* scratch) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  const double INF = __longlong_as_double(0x7ff0000000000000LL);
+  // scratch layout: thread lists [2][block], warp lists [nw][8], then reused
+  double* te = reinterpret_cast<double*>(scratch);
+  int64_t* ti = reinterpret_cast<int64_t*>(te + 2 * blockDim.x);
+  double* we = reinterpret_cast<double*>(ti + 2 * blockDim.x);
+  int64_t* wi = reinterpret_cast<int64_t*>(we + 8 * nw);
+  __shared__ double s_m2;
+  __shared__ int64_t s_nf;
   __shared__ double b_e[CERT_K];
   __shared__ int64_t b_i[CERT_K];
   __shared__ bool is_last;
-  int64_t nfb = nf, d1 = 0;
-  double de = 0.0;
-  int64_t di = 0;
-  // block n_finite
+  te[threadIdx.x] = e1; ti[threadIdx.x] = i1;
+  te[blockDim.x + threadIdx.x] = e2; ti[blockDim.x + threadIdx.x] = i2;
+  // block n_finite and min second-best (argmin-reduce on (e2, i2) gives the min)
   {
-    double e = 0.0;
-    int64_t i = 0;
-    block_argmin(e, i, nfb);   // reuses the reduction for the sum in thread 0
-    (void)de; (void)di; (void)d1;
+    double m = e2;
+    int64_t mi = i2, n = nf;
+    block_argmin(m, mi, n);
+    if (threadIdx.x == 0) { s_m2 = m; s_nf = n; }
   }
-  __shared__ int64_t s_nf;
-  if (threadIdx.x == 0) s_nf = nfb;
   __syncthreads();
-  block_topk(le, li, blockDim.x, blockDim.x, CERT_K, b_e, b_i);
+  // warp top-8 of the warp's 32 x 2 entries, then warp 0 merges the nw lists
+  warp_topk(te + threadIdx.x, ti + threadIdx.x, blockDim.x, 2, we + 8 * wid, wi + 8 * wid);
+  __syncthreads();
+  if (wid == 0) {
+    // lane l < nw holds warp l's sorted list (8 entries)
+    warp_topk(we + 8 * lane, wi + 8 * lane, 1, lane < nw ? 8 : 0, b_e, b_i);
+  }
+  __syncthreads();
   CertPartial* parts = a.cert_partials + sac * (int64_t)gridDim.x;
   if (threadIdx.x == 0) {
     CertPartial q;
     for (int k = 0; k < CERT_K; ++k) { q.e[k] = b_e[k]; q.i[k] = b_i[k]; }
     q.nf = s_nf;
+    q.m2 = s_m2;
     parts[blockIdx.x] = q;
     __threadfence();
     const unsigned int t = atomicAdd(a.counters + sac, 1u);
@@ -188,68 +180,79 @@ __device__ void cert_epilogue(const FitArgs& a, int64_t sac, double* le, int64_t
   __syncthreads();
   if (!is_last) return;
   __threadfence();
-  // merge the blocks' lists (thread b owns block b's list; gridDim <= blockDim)
-  double* ge = reinterpret_cast<double*>(scratch);                 // [CERT_K][grid]
-  int64_t* gi = reinterpret_cast<int64_t*>(ge + CERT_K * gridDim.x);
-  int64_t nft = 0;
-  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
-    for (int k = 0; k < CERT_K; ++k) {
-      ge[k * gridDim.x + b] = __ldcg(&parts[b].e[k]);
-      gi[k * gridDim.x + b] = __ldcg(reinterpret_cast<const long long*>(&parts[b].i[k]));
-    }
-    nft += __ldcg(reinterpret_cast<const long long*>(&parts[b].nf));
+  // last block: stage every block's list in smem (coalesced L2 loads), then
+  // the same two-level warp merge: chunks of 32 lists -> [nchunk][8] -> top-8
+  const int G = gridDim.x, nchunk = (G + 31) >> 5;   // G <= 256 (host cap)
+  double* pe = reinterpret_cast<double*>(scratch);   // [G][8]
+  int64_t* pi = reinterpret_cast<int64_t*>(pe + 8 * G);
+  double* ce = reinterpret_cast<double*>(pi + 8 * G); // [nchunk][8]
+  int64_t* ci = reinterpret_cast<int64_t*>(ce + 8 * nchunk);
+  for (int t = threadIdx.x; t < 8 * G; t += blockDim.x) {
+    pe[t] = __ldcg(&parts[t >> 3].e[t & 7]);
+    pi[t] = __ldcg(reinterpret_cast<const long long*>(&parts[t >> 3].i[t & 7]));
   }
   {
-    double e = 0.0;
-    int64_t i = 0;
-    block_argmin(e, i, nft);
+    double m = INF;
+    int64_t mi = 0, n = 0;
+    for (int b = threadIdx.x; b < G; b += blockDim.x) {
+      m = fmin(m, __ldcg(&parts[b].m2));
+      n += __ldcg(reinterpret_cast<const long long*>(&parts[b].nf));
+    }
+    __syncthreads();
+    block_argmin(m, mi, n);
+    if (threadIdx.x == 0) { s_m2 = m; s_nf = n; }
   }
-  __shared__ int64_t s_nft;
-  if (threadIdx.x == 0) s_nft = nft;
   __syncthreads();
-  block_topk(ge, gi, gridDim.x, gridDim.x, CERT_K, b_e, b_i);
-  // fp64 re-score of the K by warp 0 (all 32 lanes run the evaluator)
+  for (int c = wid; c < nchunk; c += nw) {
+    const int l = 32 * c + lane;
+    warp_topk(pe + 8 * l, pi + 8 * l, 1, l < G ? 8 : 0, ce + 8 * c, ci + 8 * c);
+  }
+  __syncthreads();
+  if (wid == 0) warp_topk(ce + 8 * lane, ci + 8 * lane, 1, lane < nchunk ? 8 : 0, b_e, b_i);
+  __syncthreads();
   const int32_t ns = a.ctl.n_steps + 1;
-  double* rel64 = reinterpret_cast<double*>(gi + CERT_K * gridDim.x);
-  double* st64 = rel64 + ((ns + 1) & ~1);
+  double* rel64 = reinterpret_cast<double*>(scratch);            // reuse the scratch
+  double* st64 = rel64 + ((ns + 1) & ~1);                        // fp64 stash [10][32] double2
   const double* rec = a.rec + sac * (int64_t)ns;
   for (int k = threadIdx.x; k < ns; k += blockDim.x) rel64[k] = sgn * (rec[k] - rec[0]);
   __syncthreads();
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    const int kk = lane < CERT_K ? lane : 0;
-    const int64_t idx = b_i[kk];
-    double E64 = __longlong_as_double(0x7ff0000000000000LL);
-    double p[NP];
-    generate_opc(a.space, (uint32_t)sac, idx == INT64_MAX ? 0 : idx, p, a.exp_tab);
-    CtlDev c = a.ctl;
-    E64 = evaluate<double, 0, METRIC, false>(p, c, Aprime, pwd, rel64, nullptr, 0, sgn, nullptr,
-                                             st64, !a.space.all_physical, 32);
-    if (idx == INT64_MAX || !(b_e[kk] < __longlong_as_double(0x7ff0000000000000LL)))
-      E64 = __longlong_as_double(0x7ff0000000000000LL);
-    double e = lane < CERT_K ? E64 : __longlong_as_double(0x7ff0000000000000LL);
-    int64_t i = lane < CERT_K ? idx : INT64_MAX;
-    const double myE64 = E64;
-    warp_argmin(e, i);
-    if (lane == 0) {
-      a.counters[sac] = 0;   // re-arm (graph-replay safe)
-      const int64_t neval = a.end - a.begin;
-      opmm_fit_result* out = a.final_out + (sac - a.out_base);
-      write_result(a.space, (uint32_t)sac, e, i, s_nft, neval, out, a.exp_tab);
-      // sum |rel| for the fp32 error budget
-      double srel = 0.0;
-      for (int k = 0; k < ns; ++k) srel += fabs(rel64[k]);
-      const double delta = 1e-4 * fmax(b_e[0], srel);
-      const bool all_in = s_nft < CERT_K;
-      out->top_k = CERT_K;
-      out->certified = (all_in || (b_e[CERT_K - 1] - b_e[0] > 2.0 * delta)) ? 1 : 0;
-    }
-    __syncwarp();
-    if (lane < CERT_K) {
-      opmm_fit_result* out = a.final_out + (sac - a.out_base);
-      out->topk_index[lane] = idx == INT64_MAX ? -1 : idx;
-      out->topk_err[lane] = myE64;
-    }
+  if (wid != 0) return;
+  const int64_t nft = s_nf;
+  const double m2 = s_m2;
+  double ge[CERT_K];
+  int64_t gi[CERT_K];
+#pragma unroll
+  for (int r = 0; r < CERT_K; ++r) { ge[r] = b_e[r]; gi[r] = b_i[r]; }
+  // fp64 re-score of the 8 (all 32 lanes run the evaluator)
+  const int kk = lane < CERT_K ? lane : 0;
+  const int64_t idx = b_i[kk];
+  const double e32 = b_e[kk];
+  double p[NP];
+  generate_opc(a.space, (uint32_t)sac, idx == INT64_MAX ? 0 : idx, p, a.exp_tab);
+#ifdef OPMM_CERT_NOFP64   // timing experiment only: skip the fp64 re-score
+  double E64 = e32 + p[0] * 0.0;
+#else
+  double E64 = evaluate<double, 0, METRIC, false>(p, a.ctl, Aprime, pwd, rel64, nullptr, 0, sgn,
+                                                  nullptr, st64, !a.space.all_physical, 32);
+#endif
+  if (idx == INT64_MAX || !(e32 < INF)) E64 = INF;
+  double e = lane < CERT_K ? E64 : INF;
+  int64_t i = lane < CERT_K ? idx : INT64_MAX;
+  warp_argmin(e, i);
+  opmm_fit_result* out = a.final_out + (sac - a.out_base);
+  if (lane == 0) {
+    a.counters[sac] = 0;   // re-arm (graph-replay safe)
+    write_result(a.space, (uint32_t)sac, e, i, nft, a.end - a.begin, out, a.exp_tab);
+    double srel = 0.0;
+    for (int k = 0; k < ns; ++k) srel += fabs(rel64[k]);
+    const double tstar = ge[0] + 2.0 * (1e-4 * fmax(ge[0], srel));
+    out->top_k = CERT_K;
+    out->certified = (nft < CERT_K || (m2 > tstar && ge[CERT_K - 1] > tstar)) ? 1 : 0;
+  }
+  __syncwarp();
+  if (lane < CERT_K) {
+    out->topk_index[lane] = idx == INT64_MAX ? -1 : idx;
+    out->topk_err[lane] = E64;
   }
 }
 
@@ -274,17 +277,13 @@ __global__ void __launch_bounds__(OPMM_FIT_LB_THREADS, OPMM_FIT_LB_BLOCKS) fit_k
   T* rel = reinterpret_cast<T*>(smem_raw);
   double2* tab = reinterpret_cast<double2*>(smem_raw + rel_bytes<T>(ns));
   T* stash = reinterpret_cast<T*>(smem_raw + rel_bytes<T>(ns) + exp_tab_bytes());  // [10][block] vec2
-  // certification lists follow the stash (fp32 + a.certify only)
+  // certification scratch follows the stash (fp32 + a.certify only)
   unsigned char* cert_raw = smem_raw + rel_bytes<T>(ns) + exp_tab_bytes() + stash_bytes<T>(blockDim.x);
-  double* cert_e = reinterpret_cast<double*>(cert_raw);
-  int64_t* cert_i = reinterpret_cast<int64_t*>(cert_raw + (size_t)CERT_K * blockDim.x * 8);
   const bool certify = sizeof(T) == 4 && a.certify;
-  if (certify) {
-    for (int k = 0; k < CERT_K; ++k) {
-      cert_e[k * blockDim.x + threadIdx.x] = __longlong_as_double(0x7ff0000000000000LL);
-      cert_i[k * blockDim.x + threadIdx.x] = INT64_MAX;
-    }
-  }
+  // second-best (E, idx) per thread lives in the certify scratch, not in registers
+  double* sec_e = reinterpret_cast<double*>(cert_raw) + blockDim.x + threadIdx.x;
+  int64_t* sec_i = reinterpret_cast<int64_t*>(cert_raw) + 3 * blockDim.x + threadIdx.x;
+  if (certify) { *sec_e = __longlong_as_double(0x7ff0000000000000LL); *sec_i = INT64_MAX; }
   for (int j = threadIdx.x; j < EXP_TAB_N; j += blockDim.x) tab[j] = a.exp_tab[j];
   const int64_t sac = (int64_t)blockIdx.y + a.sac_begin;
   const double amp = a.sac_ctl ? a.sac_ctl[2 * sac] : a.amplitude;
@@ -382,14 +381,17 @@ __global__ void __launch_bounds__(OPMM_FIT_LB_THREADS, OPMM_FIT_LB_BLOCKS) fit_k
     if (valid) {
       if (a.err_out) a.err_out[sac * a.err_ld + i] = E;
       nf += E < __longlong_as_double(0x7ff0000000000000LL) ? 1 : 0;
-      if (better(E, i, best_e, best_i)) { best_e = E; best_i = i; }
-      if (certify) topk_insert(cert_e + threadIdx.x, cert_i + threadIdx.x, blockDim.x, E, i);
+      if (better(E, i, best_e, best_i)) {
+        if (certify) { *sec_e = best_e; *sec_i = best_i; }
+        best_e = E; best_i = i;
+      } else if (certify && better(E, i, *sec_e, *sec_i)) {
+        *sec_e = E; *sec_i = i;
+      }
     }
   }
   if (sizeof(T) == 4 && a.certify) {
     __syncthreads();
-    cert_epilogue<T, METRIC>(a, sac, cert_e, cert_i, cert_raw + cert_bytes(blockDim.x), nf, sgn,
-                             Aprime, pwd);
+    cert_epilogue<T, METRIC>(a, sac, best_e, best_i, *sec_e, *sec_i, nf, sgn, Aprime, pwd, cert_raw);
     return;
   }
   fit_epilogue(a, sac, best_e, best_i, nf);

@@ -374,6 +374,10 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
   const void* fn = three ? opmm::fit3_kernel_ptr(precision, metric)
                          : two ? opmm::fit2_kernel_ptr(precision, metric)
                                : opmm::fit_kernel_ptr(precision, integ, metric);
+  const bool one = !two && !three;
+  const size_t perm_off = (smem + 15) & ~(size_t)15;   // fit_kernel's super-tile sort arrays follow
+  if (one) smem = perm_off + opmm::super_bytes(opmm::SUPER_MAX);   // sized for occupancy at the cap
+  if (smem > kMaxDynSmem) return fail(OPMM_ERR_INVALID_ARG, "trace too long for shared memory");
   int grid = 1;
   // fit3 work unit per block pass: 8 consumer warps x 32 candidates
   const int64_t work = three ? (e - b + 255) / 256 * block : two ? (e - b + 1) / 2 : e - b;
@@ -386,6 +390,16 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
   }
   if (e <= b) grid = 1;  // empty shard: one block reports "no candidate"
   if (certify && grid > kCertMaxGrid) grid = kCertMaxGrid;  // bounds the last block's smem staging
+  // fit_kernel super-tile: an equal share of the range per block, multiple of
+  // 32, at most SUPER_MAX (larger ranges take several persistent passes)
+  int64_t super = 32;
+  if (one) {
+    const int64_t share = (e - b + grid - 1) / (grid > 0 ? grid : 1);
+    super = (share + 31) / 32 * 32;
+    if (super < 32) super = 32;
+    if (super > opmm::SUPER_MAX) super = opmm::SUPER_MAX;
+    smem = perm_off + opmm::super_bytes(super);
+  }
   const bool multi = shard && h->comm != nullptr;   // world > 1 (or a 1-rank test comm)
   CKS(ensure(h->partials, h->partials_cap, (size_t)grid * (size_t)(s_begin + S)));
   CKS(ensure(h->counters, h->counters_cap, (size_t)(s_begin + S), true));
@@ -408,6 +422,8 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
   a.err_out = opts ? opts->err_out : nullptr;
   a.err_ld = n_candidates;
   a.sort_lanes = getenv("OPMM_NO_LANE_SORT") ? 0 : 1;   // env switch for A/B timing only
+  a.super_tile = super;
+  a.perm_off = (int64_t)perm_off;
   if (certify) {
     CKS(ensure(h->cert_parts, h->cert_parts_cap, (size_t)grid * (size_t)(s_begin + S)));
     a.certify = 1;

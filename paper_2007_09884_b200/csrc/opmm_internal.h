@@ -33,6 +33,10 @@ struct Partial {
 
 // FP32 certification: one block's (or rank's) top-8 by fp32 error
 constexpr int CERT_KK = 8;
+// fit_kernel super-tile: a block sorts up to SUPER_MAX candidates at once
+// (uint32 key/rank + uint16 permutation per candidate in shared memory)
+constexpr int SUPER_MAX = 8192;
+__host__ __device__ constexpr size_t super_bytes(int64_t s) { return (size_t)((s * 6 + 15) / 16 * 16); }
 // certify scratch (one region, reused by stage): per-thread best two (E, idx)
 // + per-warp lists; in the last block, every block's list + chunk lists, then
 // the fp64 trace and stash of the re-score.  grid <= 256.
@@ -65,6 +69,8 @@ struct FitArgs {
   int64_t err_ld;
   int32_t sort_lanes;       // counting-sort tiles by pulse end (see fit_kernel)
   int32_t certify;          // fp32: top-8 + fp64 re-score (fit_kernel only)
+  int64_t super_tile;       // fit_kernel: candidates per block pass (multiple of 32, <= SUPER_MAX)
+  int64_t perm_off;         // fit_kernel: byte offset of the super-tile sort arrays in smem
   CertPartial* cert_partials;  // [S][gridDim.x] when certify
   Partial* partials;        // [S][gridDim.x]
   unsigned int* counters;   // [S], zero between launches

@@ -302,34 +302,38 @@ __global__ void __launch_bounds__(OPMM_FIT_LB_THREADS, OPMM_FIT_LB_BLOCKS) fit_k
   double best_e = __longlong_as_double(0x7ff0000000000000LL);
   int64_t best_i = INT64_MAX;
   int64_t nf = 0;
-  // Warp-uniform trip count: every lane of a warp runs every iteration (lanes
-  // past `end` evaluate the last candidate again and discard it), so the
-  // per-step warp vote in run_propagator always sees a full warp.
-  // Lane sort: each tile of blockDim candidates is counting-sorted by the
-  // block index at which its pulse ends (n_pulse / 2, 256 bins), so a warp's
-  // lanes share few phase-switch points and run_propagator's segmented loop
-  // has few segments.  Only the candidate->thread assignment changes; every
-  // result is per candidate, so outputs are identical (and deterministic).
+  // Super-tiles.  A block takes a contiguous range of super_tile candidates
+  // per pass (persistent stride over the grid), counting-sorts it by the
+  // block index at which each candidate's pulse ends (n_pulse / 2, <= 256
+  // bins), and then its warps pull groups of 32 consecutive sorted candidates
+  // from a shared counter -- no block barrier until the super-tile is done.
+  // Lanes of a warp thus share one or two phase-switch points (few segments
+  // in run_propagator), and warps drift out of phase with each other, so one
+  // warp's integer-heavy generation overlaps another's FP64 loop.  Only the
+  // candidate -> thread assignment changes; every result is per candidate, so
+  // outputs are identical (and deterministic).
   __shared__ int s_hist[256];
   __shared__ int s_wsum[32];
-  __shared__ int s_perm[OPMM_FIT_LB_THREADS];
+  __shared__ int s_next;
+  uint32_t* s_tmp = reinterpret_cast<uint32_t*>(smem_raw + a.perm_off);          // [super]
+  uint16_t* s_perm = reinterpret_cast<uint16_t*>(s_tmp + a.super_tile);           // [super]
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t base = a.begin + (int64_t)blockIdx.x * blockDim.x; base < a.end; base += stride) {
-    int src = tid;
+  const int nbins = blockDim.x < 256 ? (int)blockDim.x : 256;   // multiple of 32
+  const int64_t sstride = (int64_t)gridDim.x * a.super_tile;
+  for (int64_t sb = a.begin + (int64_t)blockIdx.x * a.super_tile; sb < a.end; sb += sstride) {
+    const int cnt = (int)min(a.super_tile, a.end - sb);
+    if (tid < nbins) s_hist[tid] = 0;
+    if (tid == 0) s_next = 0;
+    __syncthreads();
     if (a.sort_lanes) {
-      const int nbins = blockDim.x < 256 ? (int)blockDim.x : 256;   // multiple of 32
-      const int64_t j0 = base + tid;
-      int key = nbins - 1;                                          // padding lanes last
-      if (j0 < a.end) {
-        const double pw = (a.space.model == 1 ? pwd : generate_pw(a.space, (uint32_t)sac, j0, tab));
+      for (int t = tid; t < cnt; t += blockDim.x) {
+        const double pw = (a.space.model == 1 ? pwd : generate_pw(a.space, (uint32_t)sac, sb + t, tab));
         const double npd = ceil(pw / a.ctl.dt_ms);
         const int np = npd > (double)a.ctl.n_steps ? a.ctl.n_steps + 1 : (int)npd;
-        key = min(np >> 1, nbins - 2);
+        const int key = min(np >> 1, nbins - 1);
+        const int rank = atomicAdd(&s_hist[key], 1);
+        s_tmp[t] = ((uint32_t)key << 16) | (uint32_t)rank;
       }
-      if (tid < nbins) s_hist[tid] = 0;
-      __syncthreads();
-      const int rank = atomicAdd(&s_hist[key], 1);
       __syncthreads();
       int v = 0, incl = 0;
       if (tid < nbins) {
@@ -357,40 +361,51 @@ __global__ void __launch_bounds__(OPMM_FIT_LB_THREADS, OPMM_FIT_LB_BLOCKS) fit_k
       __syncthreads();
       if (tid < nbins) s_hist[tid] = incl - v + s_wsum[wid];
       __syncthreads();
-      s_perm[s_hist[key] + rank] = tid;
+      for (int t = tid; t < cnt; t += blockDim.x) {
+        const uint32_t kr = s_tmp[t];
+        s_perm[s_hist[kr >> 16] + (int)(kr & 0xffffu)] = (uint16_t)t;
+      }
       __syncthreads();
-      src = s_perm[tid];
     }
-    // Warp-uniform trip count: every lane of a warp runs every iteration
-    // (lanes past `end` evaluate the last candidate again and discard it), so
-    // the warp-level reductions in run_propagator always see a full warp.
-    const int64_t i0 = base + src;
-    const bool valid = i0 < a.end;
-    const int64_t i = valid ? i0 : a.end - 1;
-    double p[NP];
+    const int ng = (cnt + 31) >> 5;
+    for (;;) {
+      int g = 0;
+      if (lane == 0) g = atomicAdd(&s_next, 1);
+      g = __shfl_sync(0xffffffffu, g, 0);
+      if (g >= ng) break;
+      // Warp-uniform trip count: every lane of a warp runs every group (lanes
+      // past the super-tile's end evaluate its last candidate again and
+      // discard it), so the warp-level reductions in run_propagator always
+      // see a full warp.
+      const int slot = 32 * g + lane;
+      const bool valid = slot < cnt;
+      const int sl = valid ? slot : cnt - 1;
+      const int64_t i = sb + (a.sort_lanes ? (int)s_perm[sl] : sl);
+      double p[NP];
 #ifdef OPMM_EXP_NOGEN   // timing experiment only: cheap stand-in candidates
 #pragma unroll
-    for (int d = 0; d < NP; ++d)
-      p[d] = a.space.lo[d] * (1.0 + (double)(((uint64_t)i * 7 + d) & 1023) * 1e-3);
-    p[PW_] = 1.0 + (double)(((uint64_t)i * 2654435761u) % 100u);
+      for (int d = 0; d < NP; ++d)
+        p[d] = a.space.lo[d] * (1.0 + (double)(((uint64_t)i * 7 + d) & 1023) * 1e-3);
+      p[PW_] = 1.0 + (double)(((uint64_t)i * 2654435761u) % 100u);
 #else
-    generate_opc(a.space, (uint32_t)sac, i, p, tab);
+      generate_opc(a.space, (uint32_t)sac, i, p, tab);
 #endif
-    const double E = evaluate<T, INTEG, METRIC, false>(p, a.ctl, Aprime, pwd, rel, nullptr, 0,
-                                                       sgn, nullptr, stash, !a.space.all_physical);
-    if (valid) {
-      if (a.err_out) a.err_out[sac * a.err_ld + i] = E;
-      nf += E < __longlong_as_double(0x7ff0000000000000LL) ? 1 : 0;
-      if (better(E, i, best_e, best_i)) {
-        if (certify) { *sec_e = best_e; *sec_i = best_i; }
-        best_e = E; best_i = i;
-      } else if (certify && better(E, i, *sec_e, *sec_i)) {
-        *sec_e = E; *sec_i = i;
+      const double E = evaluate<T, INTEG, METRIC, false>(p, a.ctl, Aprime, pwd, rel, nullptr, 0,
+                                                         sgn, nullptr, stash, !a.space.all_physical);
+      if (valid) {
+        if (a.err_out) a.err_out[sac * a.err_ld + i] = E;
+        nf += E < __longlong_as_double(0x7ff0000000000000LL) ? 1 : 0;
+        if (better(E, i, best_e, best_i)) {
+          if (certify) { *sec_e = best_e; *sec_i = best_i; }
+          best_e = E; best_i = i;
+        } else if (certify && better(E, i, *sec_e, *sec_i)) {
+          *sec_e = E; *sec_i = i;
+        }
       }
     }
+    __syncthreads();   // s_hist / s_perm / s_next are reused by the next pass
   }
   if (sizeof(T) == 4 && a.certify) {
-    __syncthreads();
     cert_epilogue<T, METRIC>(a, sac, best_e, best_i, *sec_e, *sec_i, nf, sgn, Aprime, pwd, cert_raw);
     return;
   }

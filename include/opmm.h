@@ -28,7 +28,9 @@
  *  - "device" pointers must be CUDA device (or managed) memory on the handle's
  *    device; "host" pointers are ordinary host memory.  Asynchronous entry
  *    points (suffix _async, and simulate/score/simulate_score/generate) only
- *    enqueue work on `stream` (NULL = the handle's own stream) and return.
+ *    enqueue work on `stream` (NULL = the handle's own stream, which is a
+ *    non-blocking stream; pass cudaStreamLegacy, (void*)1, to order the work
+ *    with the legacy default stream) and return.
  *  - Per-candidate numerical failure is data, not an error:
  *      non-physical OPC  -> E = 1e10 * (1 + sum of violations)  (D8)
  *      non-finite or E >= 1e20 accumulated -> E = +inf          (reading Q10)

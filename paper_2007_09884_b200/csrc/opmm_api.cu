@@ -383,9 +383,11 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
   const int64_t work = three ? (e - b + 255) / 256 * block : two ? (e - b + 1) / 2 : e - b;
   CKS(grid_for(h, fn, block, smem, work, opts ? opts->grid_blocks : 0, &grid));
   if (S > 1 && !(opts && opts->grid_blocks)) {
-    // population batch: gridDim.y = saccades already fills the GPU, so give
-    // each block one tile of its saccade instead of a persistent stride
-    const int64_t tiles = (work + block - 1) / block;
+    // population batch: gridDim.y = saccades already fills the GPU, so each
+    // block takes one slice of its saccade instead of a persistent stride --
+    // one fit_kernel super-tile (<= SUPER_MAX candidates), one tile otherwise
+    const int64_t unit = one ? (int64_t)opmm::SUPER_MAX : block;
+    const int64_t tiles = (work + unit - 1) / unit;
     grid = (int)(tiles < 65535 ? (tiles > 0 ? tiles : 1) : 65535);
   }
   if (e <= b) grid = 1;  // empty shard: one block reports "no candidate"

@@ -191,12 +191,18 @@ def _ptr(x):
     raise TypeError(f"cannot take a pointer of {type(x)}")
 
 
+CUDA_STREAM_LEGACY = 1   # cudaStreamLegacy: the legacy default ("NULL") stream
+
+
 def _stream(stream):
+    """None -> the handle's own stream (NULL in the C ABI).  A torch stream is
+    passed by its cudaStream_t; torch's default stream is the legacy NULL
+    stream, which the C ABI would read as "the handle's stream", so it is
+    passed as cudaStreamLegacy instead (ordered with torch's work)."""
     if stream is None:
         return None
-    if isinstance(stream, int):
-        return stream
-    return stream.cuda_stream
+    s = stream if isinstance(stream, int) else stream.cuda_stream
+    return s if s != 0 else CUDA_STREAM_LEGACY
 
 
 # ---------------------------------------------------------------------- handle

@@ -134,3 +134,18 @@ def test_product_does_not_import_the_oracle():
             txt = open(os.path.join(ROOT, "oracle", f)).read()
             assert "import paper_2007_09884_b200" not in txt, f
             assert "from paper_2007_09884_b200" not in txt and "libopmm.so" not in txt, f
+
+
+def test_stream_marshalling():
+    """torch's default stream is the legacy NULL stream; the C ABI reads NULL
+    as "the handle's own (non-blocking) stream", so the binding must pass
+    cudaStreamLegacy for it, and pass None / other streams through."""
+    from paper_2007_09884_b200 import opmm
+
+    class S:
+        def __init__(self, v):
+            self.cuda_stream = v
+    assert opmm._stream(None) is None
+    assert opmm._stream(S(0)) == opmm.CUDA_STREAM_LEGACY == 1
+    assert opmm._stream(0) == 1
+    assert opmm._stream(S(0x1234)) == 0x1234

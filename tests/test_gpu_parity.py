@@ -648,3 +648,26 @@ def test_fp32_certified_fit(opmm, h):
         opmm.opmm_fit(h, rec, ctl, sp, 1000, opmm.fit_options(precision=opmm.FP32, certify=1,
                                                               kernel_variant=3))
     assert ei.value.status == opmm.ERR_UNSUPPORTED
+
+
+# --------------------------------------------------------------------------- streams
+def test_torch_default_stream_ordering(opmm, h):
+    """Work passed torch's default stream is ordered with torch's own kernels
+    (the binding maps the legacy NULL stream to cudaStreamLegacy): simulating
+    one candidate at a time into a reused buffer and copying it out with torch,
+    with no synchronisation in between, equals one batched simulate."""
+    ctl = W.Control()
+    cands = np.asarray(oracle.generate_batch(W.paper_space(), 0, 64))
+    cands = cands[[i for i in range(64) if oracle.physical_penalty(cands[i]) == 0.0][:48]]
+    n = len(cands)
+    opc = soa(cands)
+    ref = torch.zeros((ctl.n_steps + 1, n), dtype=torch.float64, device="cuda")
+    opmm.opmm_simulate(h, opc, n, ctl, ref, stream=torch.cuda.current_stream())
+    col = torch.zeros(ctl.n_steps + 1, dtype=torch.float64, device="cuda")
+    out = torch.zeros_like(ref)
+    for s in range(n):
+        opmm.opmm_simulate(h, opc[:, s].contiguous(), 1, ctl, col, stream=torch.cuda.current_stream())
+        out[:, s] = col
+    torch.cuda.synchronize()
+    assert torch.equal(out.isnan(), ref.isnan())
+    assert torch.equal(torch.nan_to_num(out), torch.nan_to_num(ref))

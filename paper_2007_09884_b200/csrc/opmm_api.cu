@@ -4,6 +4,7 @@
 // the paper's CPU_check column.  Every step of the hot path itself runs in
 // the kernels of opmm_kernels.cu; nothing here computes candidates on the CPU.
 #include <cmath>
+#include <cfloat>
 #include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
@@ -91,7 +92,7 @@ NcclApi& nccl() {
   return api;
 }
 
-constexpr int kDefaultBlock = 384;   // == OPMM_FIT_LB_THREADS (opmm_kernels.cu)
+constexpr int kDefaultBlock = OPMM_FIT_LB_THREADS;   // opmm_internal.h
 constexpr size_t kMaxDynSmem = 220 * 1024;
 // fit kernel picked by kernel_variant = 0 when variants 2/3 apply (1 otherwise)
 constexpr int kAutoVariant = 1;
@@ -258,10 +259,29 @@ opmm::SpaceDev make_space(const opmm_search_space* s) {
         s->lo[OPMM_P_NC_ANT] + s->lo[OPMM_P_KLT_ANT] > 0.0))
     phys = false;
   d.all_physical = phys ? 1 : 0;
+  for (int k = 0; k < OPMM_NPARAM; ++k) {
+    d.span32[k] = std::ldexp(d.span[k], -32);
+    if (d.span[k] != 0.0 && !(std::fabs(d.span32[k]) >= DBL_MIN)) d.exact_u = 1;
+  }
   d.pw_stride = 1;
   if (s->mode == 1)
     for (int k = 0; k < OPMM_P_PW; ++k) d.pw_stride *= s->levels[k];
   return d;
+}
+
+// Opt a kernel in to the largest dynamic shared memory it can use: the
+// per-block maximum less its static shared memory (an attribute above that
+// is rejected and would leave the 48 KB default).
+void allow_dyn_smem(const void* fn) {
+  cudaFuncAttributes fa;
+  int dev = 0, optin = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess ||
+      cudaFuncGetAttributes(&fa, fn) != cudaSuccess)
+    return;
+  size_t dyn = (size_t)optin > fa.sharedSizeBytes ? (size_t)optin - fa.sharedSizeBytes : 0;
+  if (dyn > kMaxDynSmem) dyn = kMaxDynSmem;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
 }
 
 opmm::CtlDev make_ctl(const opmm_control* c) {
@@ -604,21 +624,13 @@ opmm_status opmm_create(opmm_handle** out, int device) {
   for (int p = 0; p < 2; ++p)
     for (int i = 0; i < 2; ++i)
       for (int m = 0; m < 2; ++m) {
-        cudaFuncSetAttribute(opmm::fit_kernel_ptr(p, i, m),
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDynSmem);
-        cudaFuncSetAttribute(opmm::simscore_kernel_ptr(p, i, m),
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDynSmem);
-        cudaFuncSetAttribute(opmm::fit2_kernel_ptr(p, m),
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDynSmem);
-        cudaFuncSetAttribute(opmm::fit3_kernel_ptr(p, m),
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDynSmem);
-        cudaFuncSetAttribute(opmm::simulate_kernel_ptr(p, i),
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDynSmem);
-        cudaFuncSetAttribute(opmm::score_kernel_ptr(p, m),
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDynSmem);
-        for (int obj = 0; obj < 4; ++obj)
-          cudaFuncSetAttribute(opmm::nm_kernel_ptr(p, obj, m),
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDynSmem);
+        allow_dyn_smem(opmm::fit_kernel_ptr(p, i, m));
+        allow_dyn_smem(opmm::simscore_kernel_ptr(p, i, m));
+        allow_dyn_smem(opmm::fit2_kernel_ptr(p, m));
+        allow_dyn_smem(opmm::fit3_kernel_ptr(p, m));
+        allow_dyn_smem(opmm::simulate_kernel_ptr(p, i));
+        allow_dyn_smem(opmm::score_kernel_ptr(p, m));
+        for (int obj = 0; obj < 4; ++obj) allow_dyn_smem(opmm::nm_kernel_ptr(p, obj, m));
       }
   cudaGetLastError();
   {

@@ -28,7 +28,7 @@ enum { KSE_AG = 0, KSE_ANT, KLT_AG, KLT_ANT, B_AG, B_ANT, B_P, NC_AG, NC_ANT, J_
 
 // exp() table for the log-uniform map: EXP_TAB[j] = exp(j/64) as a
 // double-double (hi, lo), j = 0..EXP_TAB_N-1, covering arguments in [0, 8).
-constexpr int EXP_TAB_N = 512;
+constexpr int EXP_TAB_N = 520;   // j = rint(64 x) <= 512 for x < 8
 constexpr double EXP_TAB_MAX = 8.0;
 
 // Search space, preprocessed on the host (kernel parameter -> constant bank).
@@ -42,6 +42,8 @@ struct SpaceDev {
   double lo[NP];
   // random: linear hi-lo, log log(hi/lo); grid: linear (hi-lo)/(L-1), log log(hi/lo)/(L-1)
   double span[NP];
+  double span32[NP];     // random: span * 2^-32 (exact; see map_word)
+  int32_t exact_u;       // random: some span32 would be subnormal -> literal u * span
   int64_t levels[NP];    // grid radices (1 = not a grid dimension)
   int64_t pw_stride;     // grid: product of levels[0..16] (PW digit = i / pw_stride % L17)
 };
@@ -69,17 +71,19 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
   return c;
 }
 
-// exp(x) for x in [0, 8): x = j/64 + r with r in [0, 1/64) exact (Sterbenz),
-// exp(x) = E_j (1 + q), q = expm1(r) by a degree-7 Taylor polynomial
-// (truncation < 4e-19 relative), E_j a double-double table entry; one final
-// rounding, so the result is within ~0.51 ulp of exp(x) -- the same value a
-// correctly-rounded libm returns in all but near-tie cases, for ~14
-// instructions instead of ~50 for the general-range exp().
+// exp(x) for x in [0, 8): j = rint(64 x) through the 1.5 * 2^52 shifter (its
+// low word is j; no float<->int conversions), r = x - j/64 in [-1/128, 1/128]
+// exact (Sterbenz), exp(x) = E_j (1 + q), q = expm1(r) by a degree-6 Taylor
+// polynomial (truncation < 4e-19 relative), E_j a double-double table entry
+// (j <= 512); one final rounding, so the result is within ~0.51 ulp of exp(x)
+// -- the same value a correctly-rounded libm returns in all but near-tie
+// cases, for ~11 fp64 instructions instead of ~50 for the general-range exp().
 __device__ __forceinline__ double exp_tab(double x, const double2* __restrict__ tab) {
-  const int j = __double2int_rz(x * 64.0);
-  const double r = fma((double)j, -0.015625, x);
-  double q = 1.0 / 5040.0;
-  q = fma(q, r, 1.0 / 720.0);
+  constexpr double SHIFT = 6755399441055744.0;   // 1.5 * 2^52
+  const double t = __fma_rn(x, 64.0, SHIFT);
+  const int j = __double2loint(t);
+  const double r = __fma_rn(__dsub_rn(t, SHIFT), -0.015625, x);
+  double q = 1.0 / 720.0;
   q = fma(q, r, 1.0 / 120.0);
   q = fma(q, r, 1.0 / 24.0);
   q = fma(q, r, 1.0 / 6.0);
@@ -127,12 +131,17 @@ static __device__ __noinline__ double exp_libm(double x) { return exp(x); }
 // u = (w + 0.5) 2^-32 is exact in fp64; the mapping uses explicitly rounded
 // operations so no FMA contraction changes the candidate bits; the exp
 // argument fl(u * log(hi/lo)) is the one the generator definition names.
+// w + 0.5 is formed exactly from the bits (2^52 + w) - (2^52 - 1/2), and
+// fl(u * span) = fl((w + 0.5) * span32) with span32 = span 2^-32 exact (host,
+// only when span32 is a normal number; otherwise exact_u takes the literal
+// route).
 __device__ __forceinline__ double map_word(const SpaceDev& sp, int d, uint32_t w,
                                            const double2* __restrict__ tab) {
-  const double u = __dmul_rn(__dadd_rn((double)w, 0.5), 2.3283064365386962890625e-10);
+  const double w5 = __dsub_rn(__hiloint2double(0x43300000, (int)w), 4503599627370495.5);
   if (sp.kind[d] == 0) return sp.lo[d];
-  if (sp.kind[d] == 1) return __dadd_rn(sp.lo[d], __dmul_rn(u, sp.span[d]));
-  const double x = __dmul_rn(u, sp.span[d]);
+  const double x = sp.exact_u ? __dmul_rn(__dmul_rn(w5, 2.3283064365386962890625e-10), sp.span[d])
+                              : __dmul_rn(w5, sp.span32[d]);
+  if (sp.kind[d] == 1) return __dadd_rn(sp.lo[d], x);
 #if OPMM_EXP_MODE == 0
   return __dmul_rn(sp.lo[d], sp.kind[d] == 2 ? exp_tab(x, tab) : exp_libm(x));
 #elif OPMM_EXP_MODE == 1
@@ -441,8 +450,29 @@ __device__ __forceinline__ void zmul_masked(const Mech& m, const double v[4], co
   out[3] = o3;
 }
 
+// Post-pulse coefficients in the per-thread shared-memory stash: [10][ld]
+// vec2 (see run_propagator).
 template <typename T>
-__device__ __forceinline__ void make_prop(const Setup& s, Prop2<T>& pr) {
+__device__ __forceinline__ void stash_phase(const PhaseProp2<T>& q, typename Vec2<T>::type* st2,
+                                            int ld) {
+  st2[0 * ld] = make_v2<T>(q.X2[0][0], q.X2[0][1]);
+  st2[1 * ld] = make_v2<T>(q.X2[1][0], q.X2[1][1]);
+  st2[2 * ld] = make_v2<T>(q.X2[2][0], q.X2[2][1]);
+  st2[3 * ld] = make_v2<T>(q.X2[3][0], q.X2[3][1]);
+  st2[4 * ld] = make_v2<T>(q.c2[0], q.c2[1]);
+  st2[5 * ld] = make_v2<T>(q.c2[2], q.c2[3]);
+  st2[6 * ld] = make_v2<T>(q.pf2[0], q.pf2[1]);
+  st2[7 * ld] = make_v2<T>(q.qf2[0], q.qf2[1]);
+  st2[8 * ld] = make_v2<T>(q.X0[0], q.X0[1]);
+  st2[9 * ld] = make_v2<T>(q.c0, T(0));
+}
+
+// STASH: the post-pulse phase is written to the stash as soon as it is built
+// (post-pulse first), so it never occupies registers next to the pulse phase
+// -- this lowers the kernel's register peak at the setup -> loop transition.
+template <typename T, bool STASH = false>
+__device__ __forceinline__ void make_prop(const Setup& s, Prop2<T>& pr,
+                                          typename Vec2<T>::type* st2 = nullptr, int ld = 0) {
   const Mech& m = s.m;
   // one-step mechanical block P(Z), Z = hM, by Horner: the first step
   // I + Z/4 is written out (9 structural non-zeros), then 3 sparse steps
@@ -484,7 +514,8 @@ __device__ __forceinline__ void make_prop(const Setup& s, Prop2<T>& pr) {
     pr.P0[i] = (T)P[0][i];
   }
 #pragma unroll
-  for (int ph = 0; ph < 2; ++ph) {
+  for (int phi = 0; phi < 2; ++phi) {
+    const int ph = STASH ? 1 - phi : phi;
     double X[4][2], c[4] = {0.0, 0.0, 0.0, 0.0}, pf[2], qf[2];
 #pragma unroll
     for (int mm = 0; mm < 2; ++mm) {
@@ -540,6 +571,7 @@ __device__ __forceinline__ void make_prop(const Setup& s, Prop2<T>& pr) {
       q.X0[mm] = (T)X[0][mm];
     }
     q.c0 = (T)c[0];
+    if (STASH && ph == 1) stash_phase<T>(q, st2, ld);
     if (ph == 0) {
 #pragma unroll
       for (int r = 0; r < 4; ++r) pr.z1[r] = (T)c[r];
@@ -585,7 +617,12 @@ __device__ __forceinline__ double finish_error(T acc, int32_t n_samples) {
 // 2 for the score.  TRAJ (dump mode, no trace): store theta0 + s*Delta-theta_k
 // time-major and accumulate |Delta-theta| instead, to flag divergence.
 // ----------------------------------------------------------------------------
-template <typename T, int METRIC, bool TRAJ>
+// Unroll of the two-step loop: 4 blocks for fp64, 2 for fp32 (measured best
+// of 1/2/4 on the 1e6 bench fit).
+template <typename T> struct LoopUnroll { static constexpr int value = 4; };
+template <> struct LoopUnroll<float> { static constexpr int value = 2; };
+
+template <typename T, int METRIC, bool TRAJ, bool STASHED = false>
 __device__ __forceinline__ T run_propagator(const Prop2<T>& pr, int32_t n_pulse, int32_t n_steps,
                                             const T* __restrict__ rel, T* __restrict__ traj,
                                             int64_t ld_out, T theta0, T sgn,
@@ -593,21 +630,10 @@ __device__ __forceinline__ T run_propagator(const Prop2<T>& pr, int32_t n_pulse,
   using V2 = typename Vec2<T>::type;
   // Post-pulse coefficients wait in a per-thread shared-memory stash
   // ([10][stash_ld] of vec2, conflict-free); the phase-independent P2 and
-  // P[0] stay in registers for the whole loop.
+  // P[0] stay in registers for the whole loop.  STASHED: make_prop already
+  // wrote them.
   V2* st2 = reinterpret_cast<V2*>(stash) + threadIdx.x;
-  {
-    const PhaseProp2<T>& q = pr.ph[1];
-    st2[0 * stash_ld] = make_v2<T>(q.X2[0][0], q.X2[0][1]);
-    st2[1 * stash_ld] = make_v2<T>(q.X2[1][0], q.X2[1][1]);
-    st2[2 * stash_ld] = make_v2<T>(q.X2[2][0], q.X2[2][1]);
-    st2[3 * stash_ld] = make_v2<T>(q.X2[3][0], q.X2[3][1]);
-    st2[4 * stash_ld] = make_v2<T>(q.c2[0], q.c2[1]);
-    st2[5 * stash_ld] = make_v2<T>(q.c2[2], q.c2[3]);
-    st2[6 * stash_ld] = make_v2<T>(q.pf2[0], q.pf2[1]);
-    st2[7 * stash_ld] = make_v2<T>(q.qf2[0], q.qf2[1]);
-    st2[8 * stash_ld] = make_v2<T>(q.X0[0], q.X0[1]);
-    st2[9 * stash_ld] = make_v2<T>(q.c0, T(0));
-  }
+  if (!STASHED) stash_phase<T>(pr.ph[1], st2, stash_ld);
   const PhaseProp2<T>& q0 = pr.ph[0];
   T A00 = q0.X2[0][0], A01 = q0.X2[0][1], A10 = q0.X2[1][0], A11 = q0.X2[1][1];
   T A20 = q0.X2[2][0], A21 = q0.X2[2][1], A30 = q0.X2[3][0], A31 = q0.X2[3][1];
@@ -662,15 +688,26 @@ __device__ __forceinline__ T run_propagator(const Prop2<T>& pr, int32_t n_pulse,
   while (b < nb - 1) {
     const int32_t mine = bs > b ? min(bs, nb - 1) : nb - 1;
     const int32_t seg_end = __reduce_min_sync(0xffffffffu, mine);
-#pragma unroll 2
+#pragma unroll LoopUnroll<T>::value
     for (; b < seg_end; ++b) {
-      const T t1 = fma(R0, th, fma(R1, om, fma(R2, xa, fma(R3, xn, fma(x0a, fa, fma(x0n, fn, d0))))));
-      const T nth = fma(Q00, th, fma(Q01, om, fma(Q02, xa, fma(Q03, xn, fma(A00, fa, fma(A01, fn, c0))))));
-      const T nom = fma(Q10, th, fma(Q11, om, fma(Q12, xa, fma(Q13, xn, fma(A10, fa, fma(A11, fn, c1))))));
-      const T nxa = fma(Q20, th, fma(Q21, om, fma(Q22, xa, fma(Q23, xn, fma(A20, fa, fma(A21, fn, c2))))));
-      const T nxn = fma(Q30, th, fma(Q31, om, fma(Q32, xa, fma(Q33, xn, fma(A30, fa, fma(A31, fn, c3))))));
+      // The five 6-deep FMA chains (t1 and the four state rows) written level
+      // by level, so the scheduler issues them interleaved (ILP 5 against the
+      // 8-cycle DFMA latency); each chain's own order -- hence every rounding
+      // -- is the nested form fma(P0, th, fma(P1, om, ... fma(X1, fn, c))).
+      T t1 = fma(x0n, fn, d0), nth = fma(A01, fn, c0), nom = fma(A11, fn, c1);
+      T nxa = fma(A21, fn, c2), nxn = fma(A31, fn, c3);
+      t1 = fma(x0a, fa, t1); nth = fma(A00, fa, nth); nom = fma(A10, fa, nom);
+      nxa = fma(A20, fa, nxa); nxn = fma(A30, fa, nxn);
       fa = fma(pa, fa, qa);
       fn = fma(pn, fn, qn);
+      t1 = fma(R3, xn, t1); nth = fma(Q03, xn, nth); nom = fma(Q13, xn, nom);
+      nxa = fma(Q23, xn, nxa); nxn = fma(Q33, xn, nxn);
+      t1 = fma(R2, xa, t1); nth = fma(Q02, xa, nth); nom = fma(Q12, xa, nom);
+      nxa = fma(Q22, xa, nxa); nxn = fma(Q32, xa, nxn);
+      t1 = fma(R1, om, t1); nth = fma(Q01, om, nth); nom = fma(Q11, om, nom);
+      nxa = fma(Q21, om, nxa); nxn = fma(Q31, om, nxn);
+      t1 = fma(R0, th, t1); nth = fma(Q00, th, nth); nom = fma(Q10, th, nom);
+      nxa = fma(Q20, th, nxa); nxn = fma(Q30, th, nxn);
       th = nth; om = nom; xa = nxa; xn = nxn;
       if (TRAJ) {
         accumulate<METRIC>(acc, t1);
@@ -912,12 +949,15 @@ __device__ __forceinline__ double evaluate(const double p[NP], const CtlDev& c, 
       }
       pr.f1[0] = (T)b0; pr.f1[1] = (T)b1;
     }
-#else
-    make_prop<T>(s, pr);
-#endif
     acc = run_propagator<T, METRIC, TRAJ>(pr, s.n_pulse, c.n_steps, rel, traj, ld_out,
                                           (T)c.theta0, (T)sgn, stash,
                                           stash_ld < 0 ? (int)blockDim.x : stash_ld);
+#else
+    const int ld = stash_ld < 0 ? (int)blockDim.x : stash_ld;
+    make_prop<T, true>(s, pr, reinterpret_cast<typename Vec2<T>::type*>(stash) + threadIdx.x, ld);
+    acc = run_propagator<T, METRIC, TRAJ, true>(pr, s.n_pulse, c.n_steps, rel, traj, ld_out,
+                                                (T)c.theta0, (T)sgn, stash, ld);
+#endif
   } else {
     acc = run_rk4_stages<T, METRIC, TRAJ>(s, c.n_steps, rel, traj, ld_out, (T)c.theta0, (T)sgn);
   }

@@ -32,6 +32,15 @@ struct Partial {
 };
 
 // FP32 certification: one block's (or rank's) top-8 by fp32 error
+// fit_kernel launch bounds: 384 threads x 168 registers, one block per SM
+// (3 warps per scheduler); the default block size of the fit entry points
+#ifndef OPMM_FIT_LB_THREADS
+#define OPMM_FIT_LB_THREADS 384
+#endif
+#ifndef OPMM_FIT_LB_BLOCKS
+#define OPMM_FIT_LB_BLOCKS 1
+#endif
+
 constexpr int CERT_KK = 8;
 // fit_kernel super-tile: a block sorts up to SUPER_MAX candidates at once
 // (uint32 key/rank + uint16 permutation per candidate in shared memory)

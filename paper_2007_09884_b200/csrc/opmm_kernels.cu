@@ -256,12 +256,6 @@ __device__ void cert_epilogue(const FitArgs& a, int64_t sac, double e1, int64_t 
   }
 }
 
-#ifndef OPMM_FIT_LB_THREADS
-#define OPMM_FIT_LB_THREADS 384
-#endif
-#ifndef OPMM_FIT_LB_BLOCKS
-#define OPMM_FIT_LB_BLOCKS 1
-#endif
 
 // ---------------------------------------------------------------------------
 // The fused fit kernel.  gridDim.y = saccades of this launch (1 for a single

@@ -10,5 +10,5 @@ name, defs = sys.argv[1], sys.argv[2]
 b.build_variant(name, [d for d in defs.split(",") if d])
 PY
   echo "== $name ($defs)"
-  OPMM_LIB=build/variants/libopmm_$name.so python tools/time_kv.py 2>&1 | head -2
+  OPMM_LIB=build/variants/libopmm_$name.so python tools/time_kv.py 2>&1 | head -2; OPMM_LIB=build/variants/libopmm_$name.so python tools/time_setup.py
 done

@@ -42,13 +42,13 @@ N_STEPS = 100
 PER_GPU = 10**6
 # Algorithmic FP64 work of the fit kernel per candidate:
 # the RK4 map in two-step propagator blocks is 32 FMA + 2 score adds per two
-# steps = 34 flop per step; generation + per-candidate setup = 1540 flop
+# steps = 34 flop per step; generation + per-candidate setup = 1254 flop
 # (ncu op counts dfma/dadd/dmul at n = 100 minus the loop's exact count,
 # profiles/r01_fit_kernel_fp64_opcounts.txt).
 FLOP_PER_STEP = 34
-FLOP_SETUP = 1540
+FLOP_SETUP = 1254
 FP64_INST_PER_STEP = 18    # fp64-pipe instructions per step (loop)
-FP64_INST_SETUP = 940      # fp64-pipe instructions per candidate outside the loop (ncu)
+FP64_INST_SETUP = 800      # fp64-pipe instructions per candidate outside the loop (ncu)
 SMS, FP64_LANES, SM_MAX_MHZ = 148, 64, 1965.0
 FP64_PEAK_TFLOPS = SMS * FP64_LANES * 2 * SM_MAX_MHZ * 1e6 / 1e12   # 37.23
 FP64_MEASURED_TFLOPS = 33.90   # profiles/r01_fma_peak.txt (DFMA microbenchmark)
@@ -200,10 +200,7 @@ def population_traces(h, opmm, torch, S, n_steps):
             for a, p in zip(amp, pw)]
     opc = torch.as_tensor(np.ascontiguousarray(truths.T), device="cuda")
     traj = torch.zeros((n_steps + 1, S), dtype=torch.float64, device="cuda")
-    col = torch.zeros(n_steps + 1, dtype=torch.float64, device="cuda")
-    for s in range(S):
-        opmm.opmm_simulate(h, opc[:, s].contiguous(), 1, ctls[s], col, stream=torch.cuda.current_stream())
-        traj[:, s] = col
+    opmm.opmm_simulate_batch(h, opc, S, ctls, traj, stream=torch.cuda.current_stream())
     torch.cuda.synchronize()
     recs = traj.cpu().numpy().T.copy()
     recs += np.random.default_rng(W.SEED_NOISE).normal(0.0, 0.02, size=recs.shape)

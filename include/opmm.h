@@ -203,6 +203,17 @@ opmm_status opmm_simulate(opmm_handle* h, const double* opc, int64_t n, int64_t 
                           const opmm_control* ctl, int32_t precision, int32_t integrator,
                           void* traj, int64_t ld_out, uint8_t* status, void* stream);
 
+/* opmm_simulate with one control per candidate: candidate i (column i) is
+ * simulated under HOST ctl[i] -- its own amplitude_deg, theta0_deg and
+ * pw_default_ms; dt_ms and n_steps must be equal for all i (INVALID_ARG
+ * otherwise).  Identical outputs to n single-candidate opmm_simulate calls;
+ * used to synthesize a population of saccades in one launch.  The controls
+ * are staged in a handle-owned device buffer (calls on different streams
+ * must be ordered by the caller). */
+opmm_status opmm_simulate_batch(opmm_handle* h, const double* opc, int64_t n, int64_t ld,
+                                const opmm_control* ctl, int32_t precision, int32_t integrator,
+                                void* traj, int64_t ld_out, uint8_t* status, void* stream);
+
 /* Score n stored trajectories (DEVICE traj[n_samples x ld] of `precision`)
  * against DEVICE recorded[n_samples] (fp64):  E_i = sum_k |traj_k,i - rec_k|
  * (L1) or sqrt(mean d^2) (RMS); accumulated >= 1e20 or non-finite -> +inf.

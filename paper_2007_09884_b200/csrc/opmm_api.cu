@@ -114,6 +114,8 @@ struct opmm_handle {
   size_t rec_cap = 0;
   double* sacctl = nullptr;
   size_t sacctl_cap = 0;
+  double* candctl = nullptr;   // opmm_simulate_batch: [n][3] per-candidate controls
+  size_t candctl_cap = 0;
   Partial* rank_part = nullptr;
   size_t rank_part_cap = 0;
   Partial* gathered = nullptr;
@@ -706,6 +708,7 @@ opmm_status opmm_destroy(opmm_handle* h) {
   cudaFree(h->counters);
   cudaFree(h->rec);
   cudaFree(h->sacctl);
+  cudaFree(h->candctl);
   cudaFree(h->rank_part);
   cudaFree(h->gathered);
   cudaFree(h->cert_parts);
@@ -789,11 +792,51 @@ opmm_status opmm_generate(opmm_handle* h, const opmm_search_space* space, uint32
   return OPMM_OK;
 }
 
+namespace {
+opmm_status simulate_impl(opmm_handle* h, const double* opc, int64_t n, int64_t ld,
+                          const opmm_control* ctl, const double* cand_ctl, int32_t precision,
+                          int32_t integrator, void* traj, int64_t ld_out, uint8_t* status,
+                          void* stream);
+}
+
 opmm_status opmm_simulate(opmm_handle* h, const double* opc, int64_t n, int64_t ld,
                           const opmm_control* ctl, int32_t precision, int32_t integrator, void* traj,
                           int64_t ld_out, uint8_t* status, void* stream) {
   CKS(check_handle(h));
   CKS(validate_control(ctl, true));
+  return simulate_impl(h, opc, n, ld, ctl, nullptr, precision, integrator, traj, ld_out, status,
+                       stream);
+}
+
+opmm_status opmm_simulate_batch(opmm_handle* h, const double* opc, int64_t n, int64_t ld,
+                                const opmm_control* ctl, int32_t precision, int32_t integrator,
+                                void* traj, int64_t ld_out, uint8_t* status, void* stream) {
+  CKS(check_handle(h));
+  if (n < 0) return fail(OPMM_ERR_INVALID_ARG, "n < 0");
+  if (n == 0) return OPMM_OK;
+  if (!ctl) return fail(OPMM_ERR_INVALID_ARG, "NULL ctl");
+  std::string sc((size_t)n * 3 * sizeof(double), '\0');
+  double* scp = reinterpret_cast<double*>(&sc[0]);
+  for (int64_t i = 0; i < n; ++i) {
+    CKS(validate_control(ctl + i, true));
+    if (ctl[i].dt_ms != ctl[0].dt_ms || ctl[i].n_steps != ctl[0].n_steps)
+      return fail(OPMM_ERR_INVALID_ARG, "all candidates of a batch share dt_ms and n_steps");
+    scp[3 * i] = ctl[i].amplitude_deg;
+    scp[3 * i + 1] = ctl[i].theta0_deg;
+    scp[3 * i + 2] = ctl[i].pw_default_ms;
+  }
+  cudaStream_t st = stream ? (cudaStream_t)stream : h->stream;
+  CKS(ensure(h->candctl, h->candctl_cap, (size_t)n * 3));
+  CK(cudaMemcpyAsync(h->candctl, scp, sc.size(), cudaMemcpyHostToDevice, st));
+  return simulate_impl(h, opc, n, ld, ctl, h->candctl, precision, integrator, traj, ld_out, status,
+                       stream);
+}
+
+namespace {
+opmm_status simulate_impl(opmm_handle* h, const double* opc, int64_t n, int64_t ld,
+                          const opmm_control* ctl, const double* cand_ctl, int32_t precision,
+                          int32_t integrator, void* traj, int64_t ld_out, uint8_t* status,
+                          void* stream) {
   if (!check_precision(precision)) return fail(OPMM_ERR_INVALID_ARG, "bad precision");
   if (integrator != 0 && integrator != 1) return fail(OPMM_ERR_INVALID_ARG, "bad integrator");
   if (n < 0 || ld < n || ld_out < n || (n > 0 && (!opc || !traj)))
@@ -816,10 +859,12 @@ opmm_status opmm_simulate(opmm_handle* h, const double* opc, int64_t n, int64_t 
   a.traj = traj;
   a.ld_out = ld_out;
   a.status = status;
+  a.cand_ctl = cand_ctl;
   CKS(record_start(h, st));
   CK(opmm::launch_explicit(fn, a, dim3(grid), block, smem, st));
   CKS(record_stop(h, st));
   return OPMM_OK;
+}
 }
 
 opmm_status opmm_score(opmm_handle* h, const void* traj, int64_t n, int64_t ld, int32_t n_samples,

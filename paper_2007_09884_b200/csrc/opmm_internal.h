@@ -98,6 +98,7 @@ struct ExplicitArgs {
   void* traj;               // simulate: device [(n_steps+1) x ld_out]
   int64_t ld_out;
   uint8_t* status;          // simulate: optional device [n]
+  const double* cand_ctl;   // simulate_batch: device [n][3] = (amplitude, theta0, pw_default)
 };
 
 struct ScoreArgs {

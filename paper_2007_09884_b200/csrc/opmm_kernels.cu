@@ -851,8 +851,6 @@ template <typename T, int INTEG>
 __global__ void __launch_bounds__(OPMM_FIT_LB_THREADS, OPMM_FIT_LB_BLOCKS) simulate_kernel(ExplicitArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* stash = reinterpret_cast<T*>(smem_raw);  // [8][block] vec2
-  const double A = a.amplitude;  // explicit simulate: A given (NaN rejected on host)
-  const double sgn = A < 0.0 ? -1.0 : 1.0, Aprime = fabs(A);
   T* traj = reinterpret_cast<T*>(a.traj);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < a.n; base += stride) {
@@ -863,11 +861,20 @@ __global__ void __launch_bounds__(OPMM_FIT_LB_THREADS, OPMM_FIT_LB_BLOCKS) simul
     const int64_t i = valid ? i0 : a.n - 1;
     double p[NP];
     load_opc(a.opc, a.ld, i, p);
+    // explicit simulate: A given (NaN rejected on host); batch: per candidate
+    CtlDev c = a.ctl;
+    double A = a.amplitude, pwd = a.pw_default;
+    if (a.cand_ctl) {
+      A = a.cand_ctl[3 * i];
+      c.theta0 = a.cand_ctl[3 * i + 1];
+      pwd = a.cand_ctl[3 * i + 2];
+    }
+    const double sgn = A < 0.0 ? -1.0 : 1.0, Aprime = fabs(A);
     uint8_t st = 0;
     // no trace: the accumulator sums |Delta-theta| so that a non-finite (or
     // >= 1e20) trajectory is flagged as diverged (status 2)
-    (void)evaluate<T, INTEG, 0, true>(p, a.ctl, Aprime, a.pw_default, nullptr, traj + i,
-                                      a.ld_out, sgn, &st, stash);
+    (void)evaluate<T, INTEG, 0, true>(p, c, Aprime, pwd, nullptr, traj + i, a.ld_out, sgn, &st,
+                                      stash);
     if (valid && a.status) a.status[i] = st;
   }
 }

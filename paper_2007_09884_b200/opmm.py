@@ -111,6 +111,7 @@ def _load():
         "opmm_validate": ([C.POINTER(Control), C.POINTER(SearchSpace), i64], st),
         "opmm_generate": ([vp, C.POINTER(SearchSpace), C.c_uint32, i64, i64, vp, i64, vp], st),
         "opmm_simulate": ([vp, vp, i64, i64, C.POINTER(Control), i32, i32, vp, i64, vp, vp], st),
+        "opmm_simulate_batch": ([vp, vp, i64, i64, C.POINTER(Control), i32, i32, vp, i64, vp, vp], st),
         "opmm_score": ([vp, vp, i64, i64, i32, vp, i32, i32, vp, vp], st),
         "opmm_simulate_score": ([vp, vp, i64, i64, C.POINTER(Control), vp, i32, i32, i32, vp, vp], st),
         "opmm_fit": ([vp, vp, C.POINTER(Control), C.POINTER(SearchSpace), i64,
@@ -134,7 +135,7 @@ _lib = _load()
 EXPORTED = ("opmm_version", "opmm_last_error", "opmm_create", "opmm_nccl_unique_id",
             "opmm_create_nccl", "opmm_destroy", "opmm_get_stream", "opmm_last_kernel_ms",
             "opmm_shard_range", "opmm_merge_argmin", "opmm_validate", "opmm_generate",
-            "opmm_simulate", "opmm_score", "opmm_simulate_score", "opmm_fit", "opmm_fit_async",
+            "opmm_simulate", "opmm_simulate_batch", "opmm_score", "opmm_simulate_score", "opmm_fit", "opmm_fit_async",
             "opmm_fit_batch", "opmm_estimate_batch", "opmm_nm_minimize_test")
 
 
@@ -323,6 +324,17 @@ def opmm_score(h: Handle, traj, n: int, n_samples: int, recorded, err, precision
                metric=METRIC_L1, ld: int | None = None, stream=None):
     _check(_lib.opmm_score(h.ptr, _ptr(traj), n, n if ld is None else ld, n_samples, _ptr(recorded),
                            precision, metric, _ptr(err), _stream(stream)), "opmm_score")
+
+
+def opmm_simulate_batch(h: Handle, opc, n: int, ctls, traj, precision=FP64,
+                        integrator=INTEG_PROPAGATOR, ld: int | None = None,
+                        ld_out: int | None = None, status=None, stream=None):
+    """opmm_simulate with one control per candidate (ctls: n controls sharing
+    dt_ms and n_steps)."""
+    arr = (Control * n)(*[_ctl(c) for c in ctls])
+    _check(_lib.opmm_simulate_batch(h.ptr, _ptr(opc), n, n if ld is None else ld, arr, precision,
+                                    integrator, _ptr(traj), n if ld_out is None else ld_out,
+                                    _ptr(status), _stream(stream)), "opmm_simulate_batch")
 
 
 def opmm_simulate_score(h: Handle, opc, n: int, ctl, recorded, err, precision=FP64, metric=METRIC_L1,

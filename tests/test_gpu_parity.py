@@ -671,3 +671,28 @@ def test_torch_default_stream_ordering(opmm, h):
     torch.cuda.synchronize()
     assert torch.equal(out.isnan(), ref.isnan())
     assert torch.equal(torch.nan_to_num(out), torch.nan_to_num(ref))
+
+
+def test_simulate_batch_equals_single_calls(opmm, h):
+    """opmm_simulate_batch (one control per candidate) is bit-identical to
+    single-candidate opmm_simulate calls; mixed-step batches are rejected."""
+    amp, pw, truths = W.population(40)
+    ctls = [W.Control(n_steps=150, amplitude_deg=float(a) * (-1) ** k, theta0_deg=0.5 * k,
+                      pw_default_ms=float(p)) for k, (a, p) in enumerate(zip(amp, pw))]
+    n = len(ctls)
+    opc = soa(truths)
+    got = torch.zeros((151, n), dtype=torch.float64, device="cuda")
+    st = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    opmm.opmm_simulate_batch(h, opc, n, ctls, got, status=st, stream=torch.cuda.current_stream())
+    ref = torch.zeros_like(got)
+    for s in range(n):
+        col = torch.zeros(151, dtype=torch.float64, device="cuda")
+        opmm.opmm_simulate(h, opc[:, s].contiguous(), 1, ctls[s], col, stream=torch.cuda.current_stream())
+        ref[:, s] = col
+    torch.cuda.synchronize()
+    assert torch.equal(got, ref)
+    assert int(st.sum()) == 0
+    bad = list(ctls)
+    bad[3] = W.Control(n_steps=100)
+    with pytest.raises(opmm.OpmmError):
+        opmm.opmm_simulate_batch(h, opc, n, bad, got)

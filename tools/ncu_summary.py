@@ -51,16 +51,19 @@ def rep(path):
 
 
 def launch_list(path):
+    """Per (kernel, grid) totals -- the grid separates the bench legs that
+    launch the same kernel (single fit: (148,1,1); population batch:
+    (x, saccades, 1); NM: one block per problem group)."""
     rows = [r for r in csv.reader(open(path)) if len(r) > 10]
     hdr = rows[0]
-    ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
+    ki, vi, gi = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Grid Size")
     d = defaultdict(list)
     for r in rows[1:]:
-        d[r[ki]].append(float(r[vi].replace(",", "")))
+        d[(r[ki], r[gi])].append(float(r[vi].replace(",", "")))
     tot = sum(sum(v) for v in d.values())
-    print(f"{'launches':>8s} {'mean_ns':>12s} {'total_ns':>12s} {'share':>6s}  kernel")
-    for k, v in sorted(d.items(), key=lambda kv: -sum(kv[1])):
-        print(f"{len(v):8d} {sum(v)/len(v):12.1f} {sum(v):12.1f} {100*sum(v)/tot:5.1f}%  {k}")
+    print(f"{'launches':>8s} {'mean_ns':>12s} {'total_ns':>12s} {'share':>6s}  {'grid':>16s}  kernel")
+    for (k, g), v in sorted(d.items(), key=lambda kv: -sum(kv[1])):
+        print(f"{len(v):8d} {sum(v)/len(v):12.1f} {sum(v):12.1f} {100*sum(v)/tot:5.1f}%  {g:>16s}  {k}")
 
 
 if __name__ == "__main__":

@@ -261,10 +261,16 @@ opmm::SpaceDev make_space(const opmm_search_space* s) {
         s->lo[OPMM_P_NC_ANT] + s->lo[OPMM_P_KLT_ANT] > 0.0))
     phys = false;
   d.all_physical = phys ? 1 : 0;
+  bool kinds012 = true;
   for (int k = 0; k < OPMM_NPARAM; ++k) {
     d.span32[k] = std::ldexp(d.span[k], -32);
     if (d.span[k] != 0.0 && !(std::fabs(d.span32[k]) >= DBL_MIN)) d.exact_u = 1;
+    // (a fixed -0.0 would come out +0.0 from the branch-free form)
+    kinds012 = kinds012 && d.kind[k] <= 2 && !(d.lo[k] == 0.0 && std::signbit(d.lo[k]));
+    d.gsel[k] = d.kind[k] == 2 ? 1.0 : 0.0;
+    d.lsel[k] = d.kind[k] == 1 ? 1.0 : 0.0;
   }
+  d.fast_gen = (s->mode == 0 && !d.exact_u && kinds012) ? 1 : 0;
   d.pw_stride = 1;
   if (s->mode == 1)
     for (int k = 0; k < OPMM_P_PW; ++k) d.pw_stride *= s->levels[k];

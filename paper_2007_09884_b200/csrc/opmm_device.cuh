@@ -44,6 +44,9 @@ struct SpaceDev {
   double span[NP];
   double span32[NP];     // random: span * 2^-32 (exact; see map_word)
   int32_t exact_u;       // random: some span32 would be subnormal -> literal u * span
+  int32_t fast_gen;      // random, kinds 0/1/2 only, !exact_u: branch-free generate_opc
+  double gsel[NP];       // fast_gen: 1 for table-exp (kind 2) dimensions, else 0
+  double lsel[NP];       // fast_gen: 1 for linear (kind 1) dimensions, else 0
   int64_t levels[NP];    // grid radices (1 = not a grid dimension)
   int64_t pw_stride;     // grid: product of levels[0..16] (PW digit = i / pw_stride % L17)
 };
@@ -183,8 +186,23 @@ __device__ __forceinline__ void generate_opc(const SpaceDev& sp, uint32_t saccad
       const uint4 w = philox4x32_10(make_uint4(ilo, ihi, saccade, (uint32_t)j), key);
       ws[4 * j] = w.x; ws[4 * j + 1] = w.y; ws[4 * j + 2] = w.z; ws[4 * j + 3] = w.w;
     }
+    if (sp.fast_gen) {
+      // Branch-free form of map_word for kinds 0/1/2 (no per-dimension
+      // branches or kind loads): x = (w + 1/2) span32, E = exp_tab(x g), and
+      // v = fma(x, l, lo E) with (g, l) = (1, 0) table-exp, (0, 1) linear,
+      // (*, 0) fixed (span32 = 0).  Bit-identical to map_word: fma(x, 0, y)
+      // = y, lo * 1 = lo, fma(x, 1, lo) = lo + x, and exp_tab(0) = 1.
 #pragma unroll
-    for (int d = 0; d < NP; ++d) p[d] = map_word(sp, d, ws[d], tab);
+      for (int d = 0; d < NP; ++d) {
+        const double w5 = __dsub_rn(__hiloint2double(0x43300000, (int)ws[d]), 4503599627370495.5);
+        const double x = __dmul_rn(w5, sp.span32[d]);
+        const double E = exp_tab(__dmul_rn(x, sp.gsel[d]), tab);
+        p[d] = __fma_rn(x, sp.lsel[d], __dmul_rn(sp.lo[d], E));
+      }
+    } else {
+#pragma unroll
+      for (int d = 0; d < NP; ++d) p[d] = map_word(sp, d, ws[d], tab);
+    }
     if (sp.model == 1) expand_9param(p);
   } else {
     uint64_t rem = (uint64_t)idx;

@@ -380,7 +380,7 @@ __global__ void __launch_bounds__(OPMM_FIT_LB_THREADS, OPMM_FIT_LB_BLOCKS) fit_k
 #pragma unroll
       for (int d = 0; d < NP; ++d)
         p[d] = a.space.lo[d] * (1.0 + (double)(((uint64_t)i * 7 + d) & 1023) * 1e-3);
-      p[PW_] = 1.0 + (double)(((uint64_t)i * 2654435761u) % 100u);
+      p[PW_] = generate_pw(a.space, (uint32_t)sac, i, tab);   // same pulse ends -> same sort
 #else
       generate_opc(a.space, (uint32_t)sac, i, p, tab);
 #endif

@@ -280,16 +280,29 @@ opmm::SpaceDev make_space(const opmm_search_space* s) {
 // Opt a kernel in to the largest dynamic shared memory it can use: the
 // per-block maximum less its static shared memory (an attribute above that
 // is rejected and would leave the 48 KB default).
-void allow_dyn_smem(const void* fn) {
+// Dynamic shared memory a kernel may request (opt-in limit less its static
+// shared memory, capped at kMaxDynSmem).
+size_t max_dyn_smem(const void* fn) {
+  thread_local const void* last_fn = nullptr;
+  thread_local int last_dev = -1;
+  thread_local size_t last = 0;
+  int cur = -1;
+  if (cudaGetDevice(&cur) == cudaSuccess && fn == last_fn && cur == last_dev) return last;
   cudaFuncAttributes fa;
   int dev = 0, optin = 0;
   if (cudaGetDevice(&dev) != cudaSuccess ||
       cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess ||
       cudaFuncGetAttributes(&fa, fn) != cudaSuccess)
-    return;
+    return 48 * 1024;
   size_t dyn = (size_t)optin > fa.sharedSizeBytes ? (size_t)optin - fa.sharedSizeBytes : 0;
-  if (dyn > kMaxDynSmem) dyn = kMaxDynSmem;
-  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+  last_fn = fn;
+  last_dev = dev;
+  last = dyn > kMaxDynSmem ? kMaxDynSmem : dyn;
+  return last;
+}
+
+void allow_dyn_smem(const void* fn) {
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)max_dyn_smem(fn));
 }
 
 opmm::CtlDev make_ctl(const opmm_control* c) {
@@ -403,8 +416,26 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
                          : two ? opmm::fit2_kernel_ptr(precision, metric)
                                : opmm::fit_kernel_ptr(precision, integ, metric);
   const bool one = !two && !three;
-  const size_t perm_off = (smem + 15) & ~(size_t)15;   // fit_kernel's super-tile sort arrays follow
-  if (one) smem = perm_off + opmm::super_bytes(opmm::SUPER_MAX);   // sized for occupancy at the cap
+  const size_t perm_off = (smem + 15) & ~(size_t)15;   // fit_kernel's super-tile arrays follow
+  // fit_kernel: the pre-pass key/rank scratch aliases the coefficient stash
+  // (at stash_off) when the stash holds it, else it follows the permutation
+  // fit_kernel layout: rel, exp table, stash (opmm_kernels.cu)
+  const size_t stash_off = (precision == OPMM_FP64 ? opmm::rel_bytes<double>(ns)
+                                                   : opmm::rel_bytes<float>(ns)) +
+                           opmm::exp_tab_bytes();
+  const size_t stash_sz = precision == OPMM_FP64 ? opmm::stash_bytes<double>(block)
+                                                 : opmm::stash_bytes<float>(block);
+  auto fit_dyn = [&](int64_t sup) {
+    const size_t end = perm_off + opmm::perm_bytes(sup);
+    return opmm::tmp_bytes(sup) <= stash_sz ? end : end + opmm::tmp_bytes(sup);
+  };
+  // largest super-tile the kernel's shared memory allows (long traces leave less room)
+  int64_t super_cap = opmm::SUPER_MAX;
+  if (one) {
+    const size_t lim = max_dyn_smem(fn);
+    while (super_cap > 32 && fit_dyn(super_cap) > lim) super_cap -= 32;
+    smem = fit_dyn(super_cap);   // sized for occupancy at the cap
+  }
   if (smem > kMaxDynSmem) return fail(OPMM_ERR_INVALID_ARG, "trace too long for shared memory");
   int grid = 1;
   // fit3 work unit per block pass: 8 consumer warps x 32 candidates
@@ -414,7 +445,7 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
     // population batch: gridDim.y = saccades already fills the GPU, so each
     // block takes one slice of its saccade instead of a persistent stride --
     // one fit_kernel super-tile (<= SUPER_MAX candidates), one tile otherwise
-    const int64_t unit = one ? (int64_t)opmm::SUPER_MAX : block;
+    const int64_t unit = one ? super_cap : block;
     const int64_t tiles = (work + unit - 1) / unit;
     grid = (int)(tiles < 65535 ? (tiles > 0 ? tiles : 1) : 65535);
   }
@@ -427,8 +458,8 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
     const int64_t share = (e - b + grid - 1) / (grid > 0 ? grid : 1);
     super = (share + 31) / 32 * 32;
     if (super < 32) super = 32;
-    if (super > opmm::SUPER_MAX) super = opmm::SUPER_MAX;
-    smem = perm_off + opmm::super_bytes(super);
+    if (super > super_cap) super = super_cap;
+    smem = fit_dyn(super);
   }
   const bool multi = shard && h->comm != nullptr;   // world > 1 (or a 1-rank test comm)
   CKS(ensure(h->partials, h->partials_cap, (size_t)grid * (size_t)(s_begin + S)));
@@ -454,6 +485,8 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
   a.sort_lanes = getenv("OPMM_NO_LANE_SORT") ? 0 : 1;   // env switch for A/B timing only
   a.super_tile = super;
   a.perm_off = (int64_t)perm_off;
+  a.tmp_off = (int64_t)(opmm::tmp_bytes(super) <= stash_sz ? stash_off
+                                                          : perm_off + opmm::perm_bytes(super));
   if (certify) {
     CKS(ensure(h->cert_parts, h->cert_parts_cap, (size_t)grid * (size_t)(s_begin + S)));
     a.certify = 1;

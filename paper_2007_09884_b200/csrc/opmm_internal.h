@@ -43,9 +43,12 @@ struct Partial {
 
 constexpr int CERT_KK = 8;
 // fit_kernel super-tile: a block sorts up to SUPER_MAX candidates at once
-// (uint32 key/rank + uint16 permutation per candidate in shared memory)
+// (per candidate in shared memory: permutation uint16 for the whole pass,
+// key/rank uint32 during the pre-pass only -- aliased onto the coefficient
+// stash when that is large enough)
 constexpr int SUPER_MAX = 8192;
-__host__ __device__ constexpr size_t super_bytes(int64_t s) { return (size_t)((s * 6 + 15) / 16 * 16); }
+__host__ __device__ constexpr size_t perm_bytes(int64_t s) { return (size_t)((s * 2 + 15) / 16 * 16); }
+__host__ __device__ constexpr size_t tmp_bytes(int64_t s) { return (size_t)((s * 4 + 15) / 16 * 16); }
 // certify scratch (one region, reused by stage): per-thread best two (E, idx)
 // + per-warp lists; in the last block, every block's list + chunk lists, then
 // the fp64 trace and stash of the re-score.  grid <= 256.
@@ -79,7 +82,8 @@ struct FitArgs {
   int32_t sort_lanes;       // counting-sort tiles by pulse end (see fit_kernel)
   int32_t certify;          // fp32: top-8 + fp64 re-score (fit_kernel only)
   int64_t super_tile;       // fit_kernel: candidates per block pass (multiple of 32, <= SUPER_MAX)
-  int64_t perm_off;         // fit_kernel: byte offset of the super-tile sort arrays in smem
+  int64_t perm_off;         // fit_kernel: byte offset of the super-tile permutation in smem
+  int64_t tmp_off;          // fit_kernel: byte offset of the pre-pass key/rank scratch
   CertPartial* cert_partials;  // [S][gridDim.x] when certify
   Partial* partials;        // [S][gridDim.x]
   unsigned int* counters;   // [S], zero between launches

@@ -309,8 +309,11 @@ __global__ void __launch_bounds__(OPMM_FIT_LB_THREADS, OPMM_FIT_LB_BLOCKS) fit_k
   __shared__ int s_hist[256];
   __shared__ int s_wsum[32];
   __shared__ int s_next;
-  uint32_t* s_tmp = reinterpret_cast<uint32_t*>(smem_raw + a.perm_off);          // [super]
-  uint16_t* s_perm = reinterpret_cast<uint16_t*>(s_tmp + a.super_tile);           // [super]
+  // the permutation lives through the pass; the key/rank scratch is needed
+  // only before any candidate is evaluated, so it shares the coefficient
+  // stash's memory when that is large enough (tmp_off, host)
+  uint16_t* s_perm = reinterpret_cast<uint16_t*>(smem_raw + a.perm_off);          // [super]
+  uint32_t* s_tmp = reinterpret_cast<uint32_t*>(smem_raw + a.tmp_off);            // [super]
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int nbins = blockDim.x < 256 ? (int)blockDim.x : 256;   // multiple of 32
   const int64_t sstride = (int64_t)gridDim.x * a.super_tile;
@@ -374,7 +377,8 @@ __global__ void __launch_bounds__(OPMM_FIT_LB_THREADS, OPMM_FIT_LB_BLOCKS) fit_k
       const int slot = 32 * g + lane;
       const bool valid = slot < cnt;
       const int sl = valid ? slot : cnt - 1;
-      const int64_t i = sb + (a.sort_lanes ? (int)s_perm[sl] : sl);
+      const int off = a.sort_lanes ? (int)s_perm[sl] : sl;
+      const int64_t i = sb + off;
       double p[NP];
 #ifdef OPMM_EXP_NOGEN   // timing experiment only: cheap stand-in candidates
 #pragma unroll

@@ -152,6 +152,38 @@ def test_generate_philox_words_match_oracle_kat_pinned(opmm, h):
             assert got == ref.tolist()[:len(got)]
 
 
+@pytest.mark.parametrize("case", ["libm_dim", "tiny_span", "neg_zero_fixed", "linear_only"])
+def test_generate_generic_paths_match_oracle(opmm, h, case):
+    """Random spaces outside the branch-free fast path (a log dimension whose
+    exp argument reaches 8 -> libm exp; a span whose 2^-32 scaling would be
+    subnormal -> literal u * span; a fixed -0.0) and an all-linear space
+    (fast path) against the oracle: linear and fixed dimensions bit-exact,
+    log dimensions within 2 ulp."""
+    sp = W.paper_space()
+    lo, hi, lg = sp.lo.copy(), sp.hi.copy(), sp.log_scale.copy()
+    if case == "libm_dim":
+        hi[I["B_P"]] = lo[I["B_P"]] * 1e6            # log(hi/lo) = 13.8 >= 8
+    elif case == "tiny_span":
+        lo[I["N_C_FIX"]], hi[I["N_C_FIX"]], lg[I["N_C_FIX"]] = 1e-300, 1.5e-300, 0
+    elif case == "neg_zero_fixed":
+        lo[I["N_C_ANT"]] = hi[I["N_C_ANT"]] = -0.0
+        lg[I["N_C_ANT"]] = 0
+    else:
+        lg[:] = 0
+    sp = W.SearchSpace(0, 77, lo, hi, lg, np.ones(18, np.int32))
+    n = 2048
+    out = torch.zeros((18, n), dtype=torch.float64, device="cuda")
+    opmm.opmm_generate(h, sp, 5000, n, out, saccade=3, stream=torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    g = out.cpu().numpy().T
+    o = np.array([oracle.generate(sp, 5000 + i, saccade=3) for i in range(n)])
+    lin = (lg == 0)
+    assert np.array_equal(g[:, lin].view(np.int64), o[:, lin].view(np.int64))
+    if (~lin).any():
+        rel = np.abs(g[:, ~lin] - o[:, ~lin]) / np.abs(o[:, ~lin])
+        assert rel.max() <= 2 * ULP, rel.max()
+
+
 def test_generate_grid_matches_oracle(opmm, h):
     sp = W.g4_space(per_dim=12)
     n = sp.n_grid()

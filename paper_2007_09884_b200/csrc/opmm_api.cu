@@ -116,6 +116,10 @@ struct opmm_handle {
   size_t sacctl_cap = 0;
   double* candctl = nullptr;   // opmm_simulate_batch: [n][3] per-candidate controls
   size_t candctl_cap = 0;
+  const void* occ_fn = nullptr;  // grid_for's last occupancy query
+  int occ_block = 0;
+  size_t occ_smem = 0;
+  int occ_per_sm = 0;
   Partial* rank_part = nullptr;
   size_t rank_part_cap = 0;
   Partial* gathered = nullptr;
@@ -342,7 +346,16 @@ size_t fit_smem(int precision, int32_t n_samples, int block, int kernel_variant 
 opmm_status grid_for(opmm_handle* h, const void* fn, int block, size_t smem, int64_t work,
                      int requested, int* grid) {
   int per_sm = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, block, smem));
+  // the occupancy query costs microseconds; the handle remembers the last one
+  if (fn == h->occ_fn && block == h->occ_block && smem == h->occ_smem) {
+    per_sm = h->occ_per_sm;
+  } else {
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, block, smem));
+    h->occ_fn = fn;
+    h->occ_block = block;
+    h->occ_smem = smem;
+    h->occ_per_sm = per_sm;
+  }
   if (per_sm < 1) return fail(OPMM_ERR_UNSUPPORTED, "kernel does not fit on an SM (block %d)", block);
   int64_t g = (int64_t)h->num_sms * per_sm;  // persistent: one wave of resident blocks
   const int64_t need = (work + block - 1) / block;

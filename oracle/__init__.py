@@ -61,13 +61,19 @@ def lib():
         L.orc_n_pulse.restype = C.c_int64
         L.orc_simulate.argtypes = [dp, C.c_double, C.c_int32, C.c_double, C.c_double, dp, dp]
         L.orc_simulate.restype = C.c_int
+        L.orc_simulate_sub.argtypes = [dp, C.c_double, C.c_int32, C.c_int32, C.c_double, C.c_double,
+                                       dp, dp]
+        L.orc_simulate_sub.restype = C.c_int
         L.orc_relativize.argtypes = [dp, C.c_int32, C.c_double, dp, dp, dp]
         L.orc_relativize.restype = None
         L.orc_score.argtypes = [dp, dp, C.c_int32, C.c_int]
         L.orc_score.restype = C.c_double
         L.orc_objective.argtypes = [dp, dp, C.c_int32, C.c_double, C.c_double, C.c_double, C.c_int, dp]
         L.orc_objective.restype = C.c_double
-        L.orc_fit.argtypes = [dp, C.c_int32, C.c_double, C.c_double, C.c_double, C.c_int, C.c_int,
+        L.orc_objective_sub.argtypes = [dp, dp, C.c_int32, C.c_double, C.c_int32, C.c_double,
+                                        C.c_double, C.c_int, dp]
+        L.orc_objective_sub.restype = C.c_double
+        L.orc_fit.argtypes = [dp, C.c_int32, C.c_double, C.c_int32, C.c_double, C.c_double, C.c_int, C.c_int,
                               C.c_int, C.c_uint64, dp, dp, u8p, i32p, C.c_uint32, C.c_int64,
                               C.c_int64, C.c_int, dp, i64p, dp, dp]
         L.orc_expand_9param.argtypes = [dp]
@@ -81,7 +87,7 @@ def lib():
         L.orc_nm_test.restype = C.c_int
         L.orc_test_fn.argtypes = [C.c_int, C.c_int, dp]
         L.orc_test_fn.restype = C.c_double
-        L.orc_estimate_batch.argtypes = [dp, C.c_int64, C.c_int32, C.c_double, dp, dp, dp, C.c_int,
+        L.orc_estimate_batch.argtypes = [dp, C.c_int64, C.c_int32, C.c_double, C.c_int32, dp, dp, dp, C.c_int,
                                          C.c_double, C.c_double, C.c_double, C.c_int, C.c_int,
                                          dp, dp, i32p, i32p, i32p]
         L.orc_estimate_batch.restype = C.c_int
@@ -165,15 +171,21 @@ def n_pulse(pw_ms, dt_ms) -> int:
     return int(lib().orc_n_pulse(pw_ms, dt_ms))
 
 
+def _sub(ctl) -> int:
+    """RK4 substeps per sample interval of a Control (0 or 1: none)."""
+    return int(getattr(ctl, "substeps", 0) or 0)
+
+
 def simulate(opc, dt_ms: float, n_steps: int, Aprime: float, pw_default_ms: float = 40.0,
-             states: bool = False):
-    """Delta-theta trajectory [n_steps+1] (and states [n_steps+1, 6] if asked)."""
+             states: bool = False, substeps: int = 1):
+    """Delta-theta trajectory [n_steps+1] (and states [n_steps+1, 6] if asked);
+    substeps > 1 integrates each sample interval with that many RK4 steps."""
     o, po = _d(opc)
     dth = np.zeros(n_steps + 1)
     st = np.zeros((n_steps + 1, 6)) if states else None
-    rc = lib().orc_simulate(po, dt_ms, n_steps, Aprime, pw_default_ms,
-                            dth.ctypes.data_as(C.POINTER(C.c_double)),
-                            st.ctypes.data_as(C.POINTER(C.c_double)) if states else None)
+    rc = lib().orc_simulate_sub(po, dt_ms, n_steps, substeps, Aprime, pw_default_ms,
+                                dth.ctypes.data_as(C.POINTER(C.c_double)),
+                                st.ctypes.data_as(C.POINTER(C.c_double)) if states else None)
     if rc != 0:
         raise ValueError("non-physical OPC")
     return (dth, st) if states else dth
@@ -183,7 +195,7 @@ def positions(opc, ctl) -> np.ndarray:
     """Absolute positions theta0 + s * Delta-theta (D6 mirroring, Q7)."""
     A = ctl.amplitude_deg
     s = -1.0 if A < 0 else 1.0
-    dth = simulate(opc, ctl.dt_ms, ctl.n_steps, abs(A), ctl.pw_default_ms)
+    dth = simulate(opc, ctl.dt_ms, ctl.n_steps, abs(A), ctl.pw_default_ms, substeps=max(_sub(ctl), 1))
     return ctl.theta0_deg + s * dth
 
 
@@ -208,8 +220,8 @@ def objective(opc, rec, ctl, metric: int = 0) -> float:
     o, po = _d(opc)
     rr, prr = _d(rel)
     buf = np.zeros(ctl.n_steps + 1)
-    return lib().orc_objective(po, prr, ctl.n_steps, ctl.dt_ms, Ap, ctl.pw_default_ms, metric,
-                               buf.ctypes.data_as(C.POINTER(C.c_double)))
+    return lib().orc_objective_sub(po, prr, ctl.n_steps, ctl.dt_ms, _sub(ctl), Ap, ctl.pw_default_ms,
+                                   metric, buf.ctypes.data_as(C.POINTER(C.c_double)))
 
 
 def fit(rec, ctl, space, begin: int, end: int, metric: int = 0, saccade: int = 0,
@@ -223,7 +235,7 @@ def fit(rec, ctl, space, begin: int, end: int, metric: int = 0, saccade: int = 0
     bi = C.c_int64()
     be = C.c_double()
     opc = np.zeros(NPARAM)
-    nf = lib().orc_fit(pr, ctl.n_steps, ctl.dt_ms, ctl.amplitude_deg, ctl.pw_default_ms, metric,
+    nf = lib().orc_fit(pr, ctl.n_steps, ctl.dt_ms, _sub(ctl), ctl.amplitude_deg, ctl.pw_default_ms, metric,
                        *sa, C.c_uint32(saccade), begin, end, nthreads,
                        err.ctypes.data_as(C.POINTER(C.c_double)) if want_err else None,
                        C.byref(bi), C.byref(be), opc.ctypes.data_as(C.POINTER(C.c_double)))
@@ -279,7 +291,8 @@ def estimate_batch(recs, ctls, x0=None, metric=0, init_scale=0.05, tol_x=1e-4, t
     why = np.zeros(S, dtype=np.int32)
     P = C.POINTER(C.c_double)
     I32 = C.POINTER(C.c_int32)
-    lib().orc_estimate_batch(recs.ctypes.data_as(P), S, c0.n_steps, c0.dt_ms, amp.ctypes.data_as(P),
+    assert all(_sub(c) == _sub(c0) for c in ctls)
+    lib().orc_estimate_batch(recs.ctypes.data_as(P), S, c0.n_steps, c0.dt_ms, _sub(c0), amp.ctypes.data_as(P),
                              pwd.ctypes.data_as(P), x0.ctypes.data_as(P), metric, init_scale, tol_x,
                              tol_f, 200 * NPARAM if max_iter is None else max_iter, nthreads,
                              xb.ctypes.data_as(P), fb.ctypes.data_as(P), it.ctypes.data_as(I32),

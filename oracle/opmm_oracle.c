@@ -262,11 +262,17 @@ int64_t orc_n_pulse(double pw_ms, double dt_ms) { return (int64_t)ceil(pw_ms / d
 /* theta* for k = 0..n_steps (Fig. 1 "Delta theta", Q5).  Optional states    */
 /* [(n_steps+1) x 6].  Returns 0, or 1 if the OPC is non-physical.           */
 /* ------------------------------------------------------------------------ */
-int orc_simulate(const double p_in[ORC_NP], double dt_ms, int32_t n_steps, double Aprime,
-                 double pw_default_ms, double* dtheta, double* states) {
+/* Integer substeps (reading Q25): each sample interval */
+/* of dt is integrated by `substeps` classical RK4 steps of h = dt/substeps, */
+/* the control held (ZOH) over the whole interval; substeps <= 1 is the     */
+/* plain h = dt integration above.                                          */
+int orc_simulate_sub(const double p_in[ORC_NP], double dt_ms, int32_t n_steps, int32_t substeps,
+                     double Aprime, double pw_default_ms, double* dtheta, double* states) {
   double p[ORC_NP];
   double y[6], ystar[6], levels[2];
-  double h = 1e-3 * dt_ms;
+  int32_t nsub = substeps > 1 ? substeps : 1;
+  double h = 1e-3 * dt_ms / (double)nsub;
+  int32_t j;
   int64_t n_pulse;
   int32_t k;
   int i;
@@ -289,18 +295,25 @@ int orc_simulate(const double p_in[ORC_NP], double dt_ms, int32_t n_steps, doubl
       n_ag = levels[0]; n_ant = levels[1];
       tau_ag = p[P_TAU_DE_AG]; tau_ant = p[P_TAU_DE_ANT];
     }
-    orc_rhs(p, y, n_ag, n_ant, tau_ag, tau_ant, k1);
-    for (i = 0; i < 6; ++i) yt[i] = y[i] + 0.5 * h * k1[i];
-    orc_rhs(p, yt, n_ag, n_ant, tau_ag, tau_ant, k2);
-    for (i = 0; i < 6; ++i) yt[i] = y[i] + 0.5 * h * k2[i];
-    orc_rhs(p, yt, n_ag, n_ant, tau_ag, tau_ant, k3);
-    for (i = 0; i < 6; ++i) yt[i] = y[i] + h * k3[i];
-    orc_rhs(p, yt, n_ag, n_ant, tau_ag, tau_ant, k4);
-    for (i = 0; i < 6; ++i) y[i] = y[i] + h / 6.0 * (k1[i] + 2.0 * k2[i] + 2.0 * k3[i] + k4[i]);
+    for (j = 0; j < nsub; ++j) {
+      orc_rhs(p, y, n_ag, n_ant, tau_ag, tau_ant, k1);
+      for (i = 0; i < 6; ++i) yt[i] = y[i] + 0.5 * h * k1[i];
+      orc_rhs(p, yt, n_ag, n_ant, tau_ag, tau_ant, k2);
+      for (i = 0; i < 6; ++i) yt[i] = y[i] + 0.5 * h * k2[i];
+      orc_rhs(p, yt, n_ag, n_ant, tau_ag, tau_ant, k3);
+      for (i = 0; i < 6; ++i) yt[i] = y[i] + h * k3[i];
+      orc_rhs(p, yt, n_ag, n_ant, tau_ag, tau_ant, k4);
+      for (i = 0; i < 6; ++i) y[i] = y[i] + h / 6.0 * (k1[i] + 2.0 * k2[i] + 2.0 * k3[i] + k4[i]);
+    }
     dtheta[k + 1] = y[0] - ystar[0];
     if (states) for (i = 0; i < 6; ++i) states[(int64_t)(k + 1) * 6 + i] = y[i];
   }
   return 0;
+}
+
+int orc_simulate(const double p_in[ORC_NP], double dt_ms, int32_t n_steps, double Aprime,
+                 double pw_default_ms, double* dtheta, double* states) {
+  return orc_simulate_sub(p_in, dt_ms, n_steps, 1, Aprime, pw_default_ms, dtheta, states);
 }
 
 /* ------------------------------------------------------------------------ */
@@ -334,17 +347,23 @@ double orc_score(const double* dtheta, const double* rel, int32_t n_samples, int
 
 /* Objective of one OPC against a relativized trace: penalty if non-physical, */
 /* else simulate + score.  dtheta_buf must hold n_steps+1 doubles.           */
-double orc_objective(const double p[ORC_NP], const double* rel, int32_t n_steps,
-                     double dt_ms, double Aprime, double pw_default_ms, int metric,
-                     double* dtheta_buf) {
+double orc_objective_sub(const double p[ORC_NP], const double* rel, int32_t n_steps,
+                         double dt_ms, int32_t substeps, double Aprime, double pw_default_ms,
+                         int metric, double* dtheta_buf) {
   double pen;
   double pp[ORC_NP];
   memcpy(pp, p, sizeof(pp));
   if (isnan(pp[P_PW])) pp[P_PW] = pw_default_ms;
   pen = orc_physical_penalty(pp);
   if (pen != 0.0) return pen;
-  orc_simulate(pp, dt_ms, n_steps, Aprime, pw_default_ms, dtheta_buf, NULL);
+  orc_simulate_sub(pp, dt_ms, n_steps, substeps, Aprime, pw_default_ms, dtheta_buf, NULL);
   return orc_score(dtheta_buf, rel, n_steps + 1, metric);
+}
+
+double orc_objective(const double p[ORC_NP], const double* rel, int32_t n_steps,
+                     double dt_ms, double Aprime, double pw_default_ms, int metric,
+                     double* dtheta_buf) {
+  return orc_objective_sub(p, rel, n_steps, dt_ms, 1, Aprime, pw_default_ms, metric, dtheta_buf);
 }
 
 /* ------------------------------------------------------------------------ */
@@ -354,7 +373,7 @@ double orc_objective(const double p[ORC_NP], const double* rel, int32_t n_steps,
 /* with contiguous chunks merged lexicographically.  Returns the number of   */
 /* finite E_i; *best_index = -1 if none.                                     */
 /* ------------------------------------------------------------------------ */
-int64_t orc_fit(const double* rec, int32_t n_steps, double dt_ms, double amplitude,
+int64_t orc_fit(const double* rec, int32_t n_steps, double dt_ms, int32_t substeps, double amplitude,
                 double pw_default_ms, int metric, int mode, int model, uint64_t seed,
                 const double* lo, const double* hi, const uint8_t* log_scale,
                 const int32_t* levels, uint32_t saccade, int64_t begin, int64_t end,
@@ -385,7 +404,7 @@ int64_t orc_fit(const double* rec, int32_t n_steps, double dt_ms, double amplitu
     for (i = cb; i < ce; ++i) {
       double e;
       orc_generate(mode, model, seed, lo, hi, log_scale, levels, saccade, i, opc);
-      e = orc_objective(opc, rel, n_steps, dt_ms, Aprime, pw_default_ms, metric, buf);
+      e = orc_objective_sub(opc, rel, n_steps, dt_ms, substeps, Aprime, pw_default_ms, metric, buf);
       if (err_out) err_out[i - begin] = e;
       if (isfinite(e)) n_finite++;
       if (e < lbe) { lbe = e; lbi = i; }
@@ -584,7 +603,7 @@ double orc_test_fn(int fn_id, int n, const double* x) {
    against one relativized trace (penalty / +inf rules as orc_objective). */
 typedef struct {
   const double* rel;
-  int32_t n_steps;
+  int32_t n_steps, substeps;
   double dt_ms, Aprime, pw_default_ms;
   int metric;
   double* buf;
@@ -592,14 +611,14 @@ typedef struct {
 
 static double orc_fn_plant(const double* x, void* ctx) {
   orc_plant_ctx* c = (orc_plant_ctx*)ctx;
-  return orc_objective(x, c->rel, c->n_steps, c->dt_ms, c->Aprime, c->pw_default_ms, c->metric,
-                       c->buf);
+  return orc_objective_sub(x, c->rel, c->n_steps, c->dt_ms, c->substeps, c->Aprime,
+                           c->pw_default_ms, c->metric, c->buf);
 }
 
 /* estimate_batch (Alg. 1): saccade s is fitted from x0
    (Table 1 defaults; PW NaN -> the saccade's pw_default) independently of the
    others; results in input order, identical for any nthreads (D12). */
-int orc_estimate_batch(const double* rec, int64_t S, int32_t n_steps, double dt_ms,
+int orc_estimate_batch(const double* rec, int64_t S, int32_t n_steps, double dt_ms, int32_t substeps,
                        const double* amplitude, const double* pw_default, const double* x0,
                        int metric, double init_scale, double tol_x, double tol_f, int max_iter,
                        int nthreads, double* x_best, double* f_best, int32_t* iterations,
@@ -618,7 +637,7 @@ int orc_estimate_batch(const double* rec, int64_t S, int32_t n_steps, double dt_
     orc_relativize(rec + s * (int64_t)(n_steps + 1), n_steps + 1, amplitude[s], rel, &sgn, &Ap);
     for (d = 0; d < ORC_NP; ++d) xs[d] = x0[d];
     if (isnan(xs[P_PW])) xs[P_PW] = pw_default[s];
-    ctx.rel = rel; ctx.n_steps = n_steps; ctx.dt_ms = dt_ms; ctx.Aprime = Ap;
+    ctx.rel = rel; ctx.n_steps = n_steps; ctx.substeps = substeps; ctx.dt_ms = dt_ms; ctx.Aprime = Ap;
     ctx.pw_default_ms = pw_default[s]; ctx.metric = metric; ctx.buf = buf;
     orc_nelder_mead(orc_fn_plant, &ctx, ORC_NP, xs, init_scale, tol_x, tol_f, max_iter,
                     x_best + s * ORC_NP, f_best + s, &it, &ev, &why);

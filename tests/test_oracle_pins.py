@@ -292,6 +292,73 @@ def test_p8_converges_to_matrix_exponential_solution():
     assert np.max(np.abs(coarse - exact)) < 1e-2
 
 
+# --------------------------------------------------------------------------- substeps (Q25)
+def _expm_zoh(p, Aprime, dt_ms, n_steps):
+    """Exact zero-order-hold solution at the samples (scipy expm of the
+    augmented [A b; 0 0] per control phase), control switching at the sample
+    boundary n_pulse = ceil(PW/dt) -- independent of the RK4 code."""
+    pulse, post = phase_inputs(p, Aprime)
+    h = 1e-3 * dt_ms
+    steps = []
+    for ph in (pulse, post):
+        A, b = A_and_b(p, *ph)
+        M = np.zeros((7, 7))
+        M[:6, :6] = A * h
+        M[:6, 6] = b * h
+        steps.append(scipy.linalg.expm(M))
+    npulse = math.ceil(p[I["PW"]] / dt_ms)
+    y = np.append(oracle.equilibrium(p, p[I["N_C_FIX"]], p[I["N_C_FIX"]]), 1.0)
+    th0 = y[0]
+    out = [0.0]
+    for k in range(n_steps):
+        y = (steps[0] if k < npulse else steps[1]) @ y
+        out.append(y[0] - th0)
+    return np.array(out)
+
+
+def test_substeps_is_the_fine_grid_subsampled():
+    """Reading Q25: s substeps per sample with the control held over the sample
+    interval is, when PW is a whole number of samples, exactly the plain RK4 on
+    the fine grid dt/s (n_pulse = s * ceil(PW/dt)) read every s-th sample."""
+    for p in [W.truth_opc()] + _random_physical(4, seed=31):
+        p = p.copy()
+        p[I["PW"]] = float(round(p[I["PW"]]))
+        base = oracle.simulate(p, 1.0, 100, 10.0, 40.0)
+        assert np.array_equal(oracle.simulate(p, 1.0, 100, 10.0, 40.0, substeps=1), base)
+        for m in (2, 3, 5):
+            sub = oracle.simulate(p, 1.0, 100, 10.0, 40.0, substeps=m)
+            fine = oracle.simulate(p, 1.0 / m, 100 * m, 10.0, 40.0)[::m]
+            scale = max(np.abs(fine).max(), 1.0)
+            assert np.max(np.abs(sub - fine)) <= 1e-12 * scale, m
+
+
+def test_substeps_fourth_order_convergence_to_expm():
+    """Error against the exact ZOH solution shrinks ~16x per doubling of the
+    substeps (classical RK4), >= 12 required."""
+    p = W.truth_opc()
+    exact = _expm_zoh(p, 10.0, 1.0, 100)
+    err = [np.max(np.abs(oracle.simulate(p, 1.0, 100, 10.0, 40.0, substeps=m) - exact))
+           for m in (1, 2, 4)]
+    assert err[0] / err[1] >= 12 and err[1] / err[2] >= 12, err
+
+
+def test_substeps_stabilise_a_stiff_candidate():
+    """A stiff globe (B_P/J = 1.4e5 1/s: h*rate = 140 at 1 ms, far outside
+    RK4's stability interval [-2.79, 0]) diverges at h = dt and converges to the
+    exact ZOH solution with 64 substeps (h*rate = 2.2)."""
+    p = W.truth_opc()
+    p[I["B_P"]] *= 10.0
+    p[I["J"]] *= 0.1
+    rec = oracle.positions(W.truth_opc(), W.Control())
+    assert oracle.objective(p, rec, W.Control()) == math.inf
+    sub = oracle.simulate(p, 1.0, 100, 10.0, 40.0, substeps=64)
+    exact = _expm_zoh(p, 10.0, 1.0, 100)
+    assert np.all(np.isfinite(sub))
+    assert np.max(np.abs(sub - exact)) < 1e-6 * max(np.abs(exact).max(), 1.0)
+    e = oracle.objective(p, rec, W.Control(substeps=64))
+    assert math.isfinite(e) and e == oracle.score(sub, oracle.relativize(rec, 10.0)[0])
+
+
 # --------------------------------------------------------------------------- score
 def test_score_spec_examples_and_cap():
     g = read_golden_kv("spec_worked_examples.txt")

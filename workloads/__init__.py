@@ -54,6 +54,7 @@ class Control:
     amplitude_deg: float = 10.0      # NaN -> rec[n] - rec[0] (D5, Q8)
     theta0_deg: float = 0.0
     pw_default_ms: float = 40.0      # used when a candidate's PW is NaN
+    substeps: int = 0                # RK4 steps per sample interval (0 or 1: h = dt), Q25
 
 
 @dataclasses.dataclass

@@ -51,6 +51,7 @@ extern "C" {
 
 #define OPMM_NPARAM 18
 #define OPMM_MAX_STEPS 16384
+#define OPMM_MAX_SUBSTEPS 4096
 #define OPMM_NCCL_ID_BYTES 128
 
 /* Table-1 order. */
@@ -82,9 +83,14 @@ typedef enum { OPMM_INTEG_PROPAGATOR = 0, OPMM_INTEG_RK4_STAGES = 1 } opmm_integ
 
 /* Pulse-step control + integration grid of one saccade. */
 typedef struct {
-  double dt_ms;          /* sample interval and RK4 step, > 0 (1.0 at 1 kHz)    */
+  double dt_ms;          /* sample interval, > 0 (1.0 at 1 kHz)                  */
   int32_t n_steps;       /* 1..OPMM_MAX_STEPS; trajectories have n_steps+1 samples */
-  int32_t pad_;          /* must be 0                                            */
+  int32_t substeps;      /* RK4 steps per sample interval: 0 or 1 -> h = dt;
+                            s in 2..OPMM_MAX_SUBSTEPS -> s steps of dt/s with the
+                            control held over the interval (Q25).  The
+                            propagator integrator composes them into one
+                            sample-to-sample map: the per-sample loop cost does
+                            not grow with s, only the per-candidate setup. */
   double amplitude_deg;  /* signed target amplitude A; NaN => rec[n]-rec[0] (D5) */
   double theta0_deg;     /* absolute start position (opmm_simulate output only)  */
   double pw_default_ms;  /* PW used when a candidate's PW is NaN: "saccade

@@ -22,16 +22,18 @@ import oracle
 L = np.longdouble
 
 
-def rk4_spectral_radius(p, dt_ms: float) -> float:
-    """max over both control phases of |P(h lambda)| for the eigenvalues of
-    the continuous plant matrix (probed from the oracle RHS)."""
+def rk4_spectral_radius(p, dt_ms: float, substeps: int = 1) -> float:
+    """max over both control phases of |P(h lambda)|^s, h = dt/s, for the
+    eigenvalues of the continuous plant matrix (probed from the oracle RHS):
+    the spectral radius of the sample-to-sample RK4 map (s substeps, Q25)."""
+    s = max(int(substeps or 1), 1)
     z = np.zeros(6)
     r = 0.0
     for tau_ag, tau_ant in ((p[10], p[11]), (p[12], p[13])):
         b = oracle.rhs(p, z, 0, 0, tau_ag, tau_ant)
         A = np.stack([oracle.rhs(p, np.eye(6)[j], 0, 0, tau_ag, tau_ant) - b for j in range(6)], 1)
-        ev = np.linalg.eigvals(A) * dt_ms * 1e-3
-        r = max(r, float(np.abs(1 + ev + ev ** 2 / 2 + ev ** 3 / 6 + ev ** 4 / 24).max()))
+        ev = np.linalg.eigvals(A) * dt_ms * 1e-3 / s
+        r = max(r, float(np.abs(1 + ev + ev ** 2 / 2 + ev ** 3 / 6 + ev ** 4 / 24).max()) ** s)
     return r
 
 
@@ -53,7 +55,8 @@ def objective_longdouble(p, rec, ctl, metric: int = 0) -> float:
         n_ant = L(0.01)
         n_ag = (G * (th_s + L(Ap)) + L(0.01) * g_ant) / g_ag
     n_pulse = int(np.ceil(float(pw) / ctl.dt_ms))   # the IEEE-double decision, as in the oracle
-    h = L(ctl.dt_ms) / L(1000)
+    nsub = max(int(getattr(ctl, "substeps", 0) or 0), 1)   # Q25
+    h = L(ctl.dt_ms) / L(1000) / L(nsub)
 
     def f(y, nag, nant, tag, tant):
         Tag = Kag * (y[2] - y[0])
@@ -69,11 +72,12 @@ def objective_longdouble(p, rec, ctl, metric: int = 0) -> float:
             args = (P[15], P[16], P[10] / 1000, P[11] / 1000)
         else:
             args = (n_ag, n_ant, P[12] / 1000, P[13] / 1000)
-        k1 = f(y, *args)
-        k2 = f(y + h / 2 * k1, *args)
-        k3 = f(y + h / 2 * k2, *args)
-        k4 = f(y + h * k3, *args)
-        y = y + h / 6 * (k1 + 2 * k2 + 2 * k3 + k4)
+        for _ in range(nsub):
+            k1 = f(y, *args)
+            k2 = f(y + h / 2 * k1, *args)
+            k3 = f(y + h / 2 * k2, *args)
+            k4 = f(y + h * k3, *args)
+            y = y + h / 6 * (k1 + 2 * k2 + 2 * k3 + k4)
         d = (y[0] - th_s) - L(rel[k + 1])
         acc += abs(d) if metric == 0 else d * d
     if not acc < L(1e20):

@@ -188,6 +188,9 @@ opmm_status validate_control(const opmm_control* c, bool need_amplitude) {
     return fail(OPMM_ERR_INVALID_ARG, "amplitude_deg must be given (no recorded trace here)");
   if (!(c->pw_default_ms > 0.0) || !is_finite(c->pw_default_ms))
     return fail(OPMM_ERR_INVALID_ARG, "pw_default_ms must be finite and > 0");
+  if (c->substeps < 0 || c->substeps > OPMM_MAX_SUBSTEPS)
+    return fail(OPMM_ERR_INVALID_ARG, "substeps must be in [0, %d] (got %d)", OPMM_MAX_SUBSTEPS,
+                c->substeps);
   return OPMM_OK;
 }
 
@@ -309,12 +312,19 @@ void allow_dyn_smem(const void* fn) {
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)max_dyn_smem(fn));
 }
 
+// Kernel integrator: the public PROPAGATOR with substeps > 1 runs the
+// internal instantiation 2 (sample map = substep map ^ substeps, Q25).
+int kernel_integ(int integrator, const opmm_control* c) {
+  return (integrator == OPMM_INTEG_PROPAGATOR && c && c->substeps > 1) ? 2 : integrator;
+}
+
 opmm::CtlDev make_ctl(const opmm_control* c) {
   opmm::CtlDev d;
   d.dt_ms = c->dt_ms;
   d.h = 1e-3 * c->dt_ms;
   d.n_steps = c->n_steps;
   d.theta0 = c->theta0_deg;
+  d.substeps = c->substeps > 1 ? c->substeps : 1;
   return d;
 }
 
@@ -405,10 +415,11 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
   // variants 2/3 need the propagator integrator and a search space whose
   // candidates are all physical (no per-candidate penalty path)
   const bool special_ok = integ == OPMM_INTEG_PROPAGATOR && space_dev.all_physical &&
-                          !(opts && opts->block_size);
+                          !(opts && opts->block_size) && ctl->substeps <= 1;
   if (kv_opt >= 2 && !special_ok)
     return fail(OPMM_ERR_UNSUPPORTED, "kernel_variant %d needs the propagator integrator, a "
-                                      "physical search space and the default block size", kv_opt);
+                                      "physical search space, the default block size and no "
+                                      "substeps", kv_opt);
   const int kv = kv_opt == 0 ? (special_ok ? kAutoVariant : 1) : kv_opt;
   const bool two = kv == 2, three = kv == 3;
   const int block = three ? opmm::FIT3_BLOCK : two ? opmm::FIT2_BLOCK
@@ -427,7 +438,7 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
   if (smem > kMaxDynSmem) return fail(OPMM_ERR_INVALID_ARG, "trace too long for shared memory");
   const void* fn = three ? opmm::fit3_kernel_ptr(precision, metric)
                          : two ? opmm::fit2_kernel_ptr(precision, metric)
-                               : opmm::fit_kernel_ptr(precision, integ, metric);
+                               : opmm::fit_kernel_ptr(precision, kernel_integ(integ, ctl), metric);
   const bool one = !two && !three;
   const size_t perm_off = (smem + 15) & ~(size_t)15;   // fit_kernel's super-tile arrays follow
   // fit_kernel: the pre-pass key/rank scratch aliases the coefficient stash
@@ -579,7 +590,9 @@ opmm_status nm_launch(opmm_handle* h, const NmConfig& c, const double* rec_dev,
                       const double* sacctl_dev, const opmm_control* ctl0, int64_t x0_ld, int dim,
                       int fn_id, int64_t pb, int64_t pe) {
   const int32_t ns = ctl0 ? ctl0->n_steps + 1 : 1;
-  const size_t smem = opmm::nm_smem(c.precision, c.obj, ns);
+  // the propagator objective with substeps has its own instantiation (obj 4)
+  const int obj = (c.obj == 0 && ctl0 && ctl0->substeps > 1) ? 4 : c.obj;
+  const size_t smem = opmm::nm_smem(c.precision, obj, ns);
   if (smem > kMaxDynSmem) return fail(OPMM_ERR_INVALID_ARG, "trace too long for the NM kernel");
   opmm::NmArgs a;
   std::memset(&a, 0, sizeof(a));
@@ -604,7 +617,7 @@ opmm_status nm_launch(opmm_handle* h, const NmConfig& c, const double* rec_dev,
   if (grid == 0) return OPMM_OK;
   if (grid > 0x7fffffff) return fail(OPMM_ERR_INVALID_ARG, "too many problems");
   CKS(record_start(h, h->stream));
-  CK(opmm::launch_nm(opmm::nm_kernel_ptr(c.precision, c.obj, c.metric), a, (int)grid, smem,
+  CK(opmm::launch_nm(opmm::nm_kernel_ptr(c.precision, obj, c.metric), a, (int)grid, smem,
                      h->stream));
   CKS(record_stop(h, h->stream));
   return OPMM_OK;
@@ -676,7 +689,7 @@ opmm_status opmm_create(opmm_handle** out, int device) {
   }
   // allow the largest traces: raise the dynamic shared-memory cap once
   for (int p = 0; p < 2; ++p)
-    for (int i = 0; i < 2; ++i)
+    for (int i = 0; i < 3; ++i)
       for (int m = 0; m < 2; ++m) {
         allow_dyn_smem(opmm::fit_kernel_ptr(p, i, m));
         allow_dyn_smem(opmm::simscore_kernel_ptr(p, i, m));
@@ -684,7 +697,7 @@ opmm_status opmm_create(opmm_handle** out, int device) {
         allow_dyn_smem(opmm::fit3_kernel_ptr(p, m));
         allow_dyn_smem(opmm::simulate_kernel_ptr(p, i));
         allow_dyn_smem(opmm::score_kernel_ptr(p, m));
-        for (int obj = 0; obj < 4; ++obj) allow_dyn_smem(opmm::nm_kernel_ptr(p, obj, m));
+        for (int obj = 0; obj < 5; ++obj) allow_dyn_smem(opmm::nm_kernel_ptr(p, obj, m));
       }
   cudaGetLastError();
   {
@@ -871,8 +884,9 @@ opmm_status opmm_simulate_batch(opmm_handle* h, const double* opc, int64_t n, in
   double* scp = reinterpret_cast<double*>(&sc[0]);
   for (int64_t i = 0; i < n; ++i) {
     CKS(validate_control(ctl + i, true));
-    if (ctl[i].dt_ms != ctl[0].dt_ms || ctl[i].n_steps != ctl[0].n_steps)
-      return fail(OPMM_ERR_INVALID_ARG, "all candidates of a batch share dt_ms and n_steps");
+    if (ctl[i].dt_ms != ctl[0].dt_ms || ctl[i].n_steps != ctl[0].n_steps ||
+        ctl[i].substeps != ctl[0].substeps)
+      return fail(OPMM_ERR_INVALID_ARG, "all candidates of a batch share dt_ms, n_steps and substeps");
     scp[3 * i] = ctl[i].amplitude_deg;
     scp[3 * i + 1] = ctl[i].theta0_deg;
     scp[3 * i + 2] = ctl[i].pw_default_ms;
@@ -897,7 +911,7 @@ opmm_status simulate_impl(opmm_handle* h, const double* opc, int64_t n, int64_t 
   cudaStream_t st = stream ? (cudaStream_t)stream : h->stream;
   const int block = kDefaultBlock;
   const size_t smem = sim_smem(precision, 0, block, false);
-  const void* fn = opmm::simulate_kernel_ptr(precision, integrator);
+  const void* fn = opmm::simulate_kernel_ptr(precision, kernel_integ(integrator, ctl));
   int grid = 1;
   CKS(grid_for(h, fn, block, smem, n, 0, &grid));
   opmm::ExplicitArgs a;
@@ -956,7 +970,7 @@ opmm_status opmm_simulate_score(opmm_handle* h, const double* opc, int64_t n, in
   const int block = kDefaultBlock;
   const size_t smem = sim_smem(precision, ctl->n_steps + 1, block, true);
   if (smem > kMaxDynSmem) return fail(OPMM_ERR_INVALID_ARG, "trace too long for shared memory");
-  const void* fn = opmm::simscore_kernel_ptr(precision, integrator, metric);
+  const void* fn = opmm::simscore_kernel_ptr(precision, kernel_integ(integrator, ctl), metric);
   int grid = 1;
   CKS(grid_for(h, fn, block, smem, n, 0, &grid));
   opmm::ExplicitArgs a;
@@ -1027,8 +1041,9 @@ opmm_status opmm_fit_batch(opmm_handle* h, const double* recorded, int64_t S,
   if (!recorded || !ctl || !out) return fail(OPMM_ERR_INVALID_ARG, "NULL argument");
   for (int64_t s = 0; s < S; ++s) {
     CKS(validate_control(ctl + s, false));
-    if (ctl[s].dt_ms != ctl[0].dt_ms || ctl[s].n_steps != ctl[0].n_steps)
-      return fail(OPMM_ERR_INVALID_ARG, "all saccades of a batch share dt_ms and n_steps");
+    if (ctl[s].dt_ms != ctl[0].dt_ms || ctl[s].n_steps != ctl[0].n_steps ||
+        ctl[s].substeps != ctl[0].substeps)
+      return fail(OPMM_ERR_INVALID_ARG, "all saccades of a batch share dt_ms, n_steps and substeps");
   }
   CKS(validate_space(space, n_per));
   if (opts && opts->err_out)
@@ -1093,8 +1108,9 @@ opmm_status opmm_estimate_batch(opmm_handle* h, const double* recorded, int64_t 
   if (!recorded || !ctl || !out) return fail(OPMM_ERR_INVALID_ARG, "NULL argument");
   for (int64_t s = 0; s < S; ++s) {
     CKS(validate_control(ctl + s, false));
-    if (ctl[s].dt_ms != ctl[0].dt_ms || ctl[s].n_steps != ctl[0].n_steps)
-      return fail(OPMM_ERR_INVALID_ARG, "all saccades of a batch share dt_ms and n_steps");
+    if (ctl[s].dt_ms != ctl[0].dt_ms || ctl[s].n_steps != ctl[0].n_steps ||
+        ctl[s].substeps != ctl[0].substeps)
+      return fail(OPMM_ERR_INVALID_ARG, "all saccades of a batch share dt_ms, n_steps and substeps");
   }
   NmConfig c;
   CKS(nm_config(opts, OPMM_NPARAM, true, &c));

@@ -67,7 +67,8 @@ double cpu_check_score(const double opc[OPMM_NPARAM], const double* rec, const o
     step_n[0] = (G * (th_star + Ap) + 0.01 * g[1]) / g[0];
   }
   const double n_pulse = std::ceil(pw / ctl->dt_ms);
-  const double h = 1e-3 * ctl->dt_ms;
+  const int nsub = ctl->substeps > 1 ? ctl->substeps : 1;   // reading Q25
+  const double h = 1e-3 * ctl->dt_ms / (double)nsub;
   double acc = 0.0;
   for (int k = 0; k < n; ++k) {
     const bool pulse = (double)k < n_pulse;
@@ -75,15 +76,17 @@ double cpu_check_score(const double opc[OPMM_NPARAM], const double* rec, const o
                           pulse ? opc[OPMM_P_NSAC_ANT] : step_n[1]};
     const double tau[2] = {1e-3 * (pulse ? opc[OPMM_P_TAU_AC_AG] : opc[OPMM_P_TAU_DE_AG]),
                            1e-3 * (pulse ? opc[OPMM_P_TAU_AC_ANT] : opc[OPMM_P_TAU_DE_ANT])};
-    double k1[6], k2[6], k3[6], k4[6], t[6];
-    deriv(P, y, nn, tau, k1);
-    for (int i = 0; i < 6; ++i) t[i] = y[i] + 0.5 * h * k1[i];
-    deriv(P, t, nn, tau, k2);
-    for (int i = 0; i < 6; ++i) t[i] = y[i] + 0.5 * h * k2[i];
-    deriv(P, t, nn, tau, k3);
-    for (int i = 0; i < 6; ++i) t[i] = y[i] + h * k3[i];
-    deriv(P, t, nn, tau, k4);
-    for (int i = 0; i < 6; ++i) y[i] += h / 6.0 * (k1[i] + 2.0 * k2[i] + 2.0 * k3[i] + k4[i]);
+    for (int sub = 0; sub < nsub; ++sub) {
+      double k1[6], k2[6], k3[6], k4[6], t[6];
+      deriv(P, y, nn, tau, k1);
+      for (int i = 0; i < 6; ++i) t[i] = y[i] + 0.5 * h * k1[i];
+      deriv(P, t, nn, tau, k2);
+      for (int i = 0; i < 6; ++i) t[i] = y[i] + 0.5 * h * k2[i];
+      deriv(P, t, nn, tau, k3);
+      for (int i = 0; i < 6; ++i) t[i] = y[i] + h * k3[i];
+      deriv(P, t, nn, tau, k4);
+      for (int i = 0; i < 6; ++i) y[i] += h / 6.0 * (k1[i] + 2.0 * k2[i] + 2.0 * k3[i] + k4[i]);
+    }
     const double d = (y[0] - th_star) - s * (rec[k + 1] - rec[0]);
     acc += metric == 0 ? std::fabs(d) : d * d;
   }

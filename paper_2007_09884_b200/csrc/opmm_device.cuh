@@ -53,6 +53,7 @@ struct SpaceDev {
 
 // Per-launch control (shared by every candidate of a saccade).
 struct CtlDev {
+  int32_t substeps;      // RK4 steps per sample interval (>= 1), reading Q25
   double dt_ms;
   double h;              // dt in seconds
   int32_t n_steps;
@@ -320,9 +321,16 @@ struct Setup {
   int32_t n_pulse;        // steps k < n_pulse use phase 0 (reading Q6)
 };
 
-__device__ __forceinline__ void make_setup(const double p_in[NP], double dt_ms, double h,
+// substeps > 1 (reading Q25): the dynamics coefficients are those of one
+// substep, h/substeps; the pulse window stays in samples of dt.
+__device__ __forceinline__ void make_setup(const double p_in[NP], double dt_ms, double h_sample,
                                            int32_t n_steps, double Aprime, double pw_default,
-                                           Setup& s) {
+                                           Setup& s, int32_t substeps = 1) {
+  double h = h_sample, dts = dt_ms;
+  if (substeps > 1) {
+    h = h_sample / (double)substeps;
+    dts = dt_ms / (double)substeps;
+  }
   const double Kag = p_in[KSE_AG], Kant = p_in[KSE_ANT], Lag = p_in[KLT_AG], Lant = p_in[KLT_ANT];
   const double Bag = p_in[B_AG], Bant = p_in[B_ANT], Bp = p_in[B_P];
   const double Ncag = p_in[NC_AG], Ncant = p_in[NC_ANT], J = p_in[J_], F = p_in[NC_FIX];
@@ -351,12 +359,12 @@ __device__ __forceinline__ void make_setup(const double p_in[NP], double dt_ms, 
     nt_ag = n_ag - F;
     nt_ant = NANT_FLOOR - F;
   }
-  s.ph[0].zd_ag = -dt_ms * rcp64(p_in[TAU_AC_AG]);
-  s.ph[0].zd_ant = -dt_ms * rcp64(p_in[TAU_AC_ANT]);
+  s.ph[0].zd_ag = -dts * rcp64(p_in[TAU_AC_AG]);
+  s.ph[0].zd_ant = -dts * rcp64(p_in[TAU_AC_ANT]);
   s.ph[0].nt_ag = p_in[NSAC_AG] - F;
   s.ph[0].nt_ant = p_in[NSAC_ANT] - F;
-  s.ph[1].zd_ag = -dt_ms * rcp64(p_in[TAU_DE_AG]);
-  s.ph[1].zd_ant = -dt_ms * rcp64(p_in[TAU_DE_ANT]);
+  s.ph[1].zd_ag = -dts * rcp64(p_in[TAU_DE_AG]);
+  s.ph[1].zd_ant = -dts * rcp64(p_in[TAU_DE_ANT]);
   s.ph[1].nt_ag = nt_ag;
   s.ph[1].nt_ant = nt_ant;
   // Pulse window: onset at step 0, n_pulse = ceil(PW/dt) (IEEE divide), Q6.
@@ -485,59 +493,55 @@ __device__ __forceinline__ void stash_phase(const PhaseProp2<T>& q, typename Vec
   st2[9 * ld] = make_v2<T>(q.c0, T(0));
 }
 
-// STASH: the post-pulse phase is written to the stash as soon as it is built
-// (post-pulse first), so it never occupies registers next to the pulse phase
-// -- this lowers the kernel's register peak at the setup -> loop transition.
-template <typename T, bool STASH = false>
-__device__ __forceinline__ void make_prop(const Setup& s, Prop2<T>& pr,
-                                          typename Vec2<T>::type* st2 = nullptr, int ld = 0) {
-  const Mech& m = s.m;
-  // one-step mechanical block P(Z) = (I + Z) + Z^2 (I/2 + Z/6 + Z^2/24),
-  // Z = hM: Z^2 from Z's 9 structural non-zeros (19 ops), then one sparse x
-  // dense product (Z^2 has zeros at (2,3) and (3,2)) -- ~100 fp64 ops instead
-  // of ~156 for three Horner steps.
-  double P[4][4];
-  {
-    const double h = m.z01, a = m.z10, b = m.z11, c = m.z12, d = m.z13;
-    const double e = m.z20, f = m.z22, g = m.z30, k = m.z33;
-    double Z2[4][4];
-    Z2[0][0] = h * a; Z2[0][1] = h * b; Z2[0][2] = h * c; Z2[0][3] = h * d;
-    Z2[1][0] = fma(b, a, fma(c, e, d * g));
-    Z2[1][1] = fma(a, h, b * b);
-    Z2[1][2] = fma(b, c, c * f);
-    Z2[1][3] = fma(b, d, d * k);
-    Z2[2][0] = f * e; Z2[2][1] = e * h; Z2[2][2] = f * f; Z2[2][3] = 0.0;
-    Z2[3][0] = k * g; Z2[3][1] = g * h; Z2[3][2] = 0.0; Z2[3][3] = k * k;
-    const double Zm[4][4] = {{0.0, h, 0.0, 0.0}, {a, b, c, d}, {e, 0.0, f, 0.0}, {g, 0.0, 0.0, k}};
-    // B = I/2 + Z/6 + Z^2/24
-    double B[4][4];
+// Building blocks of the propagator (force-inlined into make_prop, so its
+// code is the one-pass form below; make_prop_sub reuses them for substeps).
+//
+// one-step mechanical block P(Z) = (I + Z) + Z^2 (I/2 + Z/6 + Z^2/24),
+// Z = hM: Z^2 from Z's 9 structural non-zeros (19 ops), then one sparse x
+// dense product (Z^2 has zeros at (2,3) and (3,2)) -- ~100 fp64 ops instead
+// of ~156 for three Horner steps.
+__device__ __forceinline__ void one_step_P(const Mech& m, double P[4][4]) {
+  const double h = m.z01, a = m.z10, b = m.z11, c = m.z12, d = m.z13;
+  const double e = m.z20, f = m.z22, g = m.z30, k = m.z33;
+  double Z2[4][4];
+  Z2[0][0] = h * a; Z2[0][1] = h * b; Z2[0][2] = h * c; Z2[0][3] = h * d;
+  Z2[1][0] = fma(b, a, fma(c, e, d * g));
+  Z2[1][1] = fma(a, h, b * b);
+  Z2[1][2] = fma(b, c, c * f);
+  Z2[1][3] = fma(b, d, d * k);
+  Z2[2][0] = f * e; Z2[2][1] = e * h; Z2[2][2] = f * f; Z2[2][3] = 0.0;
+  Z2[3][0] = k * g; Z2[3][1] = g * h; Z2[3][2] = 0.0; Z2[3][3] = k * k;
+  const double Zm[4][4] = {{0.0, h, 0.0, 0.0}, {a, b, c, d}, {e, 0.0, f, 0.0}, {g, 0.0, 0.0, k}};
+  // B = I/2 + Z/6 + Z^2/24
+  double B[4][4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const bool zz = (i == 0 && j != 1) || (i == 2 && (j == 1 || j == 3)) || (i == 3 && (j == 1 || j == 2));
-        double v = Z2[i][j] * (1.0 / 24.0);
-        if (!zz) v = fma(Zm[i][j], 1.0 / 6.0, v);
-        if (i == j) v += 0.5;
-        B[i][j] = v;
+    for (int j = 0; j < 4; ++j) {
+      const bool zz = (i == 0 && j != 1) || (i == 2 && (j == 1 || j == 3)) || (i == 3 && (j == 1 || j == 2));
+      double v = Z2[i][j] * (1.0 / 24.0);
+      if (!zz) v = fma(Zm[i][j], 1.0 / 6.0, v);
+      if (i == j) v += 0.5;
+      B[i][j] = v;
+    }
+  // P = I + Z + Z^2 B
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const bool zz = (i == 0 && j != 1) || (i == 2 && (j == 1 || j == 3)) || (i == 3 && (j == 1 || j == 2));
+      double v = (i == j ? 1.0 : 0.0) + (zz ? 0.0 : Zm[i][j]);
+#pragma unroll
+      for (int l = 0; l < 4; ++l) {
+        if ((i == 2 && l == 3) || (i == 3 && l == 2)) continue;   // Z^2 structural zeros
+        v = fma(Z2[i][l], B[l][j], v);
       }
-    // P = I + Z + Z^2 B
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const bool zz = (i == 0 && j != 1) || (i == 2 && (j == 1 || j == 3)) || (i == 3 && (j == 1 || j == 2));
-        double v = (i == j ? 1.0 : 0.0) + (zz ? 0.0 : Zm[i][j]);
-#pragma unroll
-        for (int l = 0; l < 4; ++l) {
-          if ((i == 2 && l == 3) || (i == 3 && l == 2)) continue;   // Z^2 structural zeros
-          v = fma(Z2[i][l], B[l][j], v);
-        }
-        P[i][j] = v;
-      }
-  }
-  // u_i = Z^i (h c_m): c_AG = e_2 / B_AG, c_ANT = e_3 / B_ANT.
-  double u[2][4][4];
+      P[i][j] = v;
+    }
+}
+
+// u_i = Z^i (h c_m): c_AG = e_2 / B_AG, c_ANT = e_3 / B_ANT.
+__device__ __forceinline__ void coupling_u(const Mech& m, double u[2][4][4]) {
 #pragma unroll
   for (int mm = 0; mm < 2; ++mm) {
     u[mm][0][0] = 0.0; u[mm][0][1] = 0.0;
@@ -546,6 +550,80 @@ __device__ __forceinline__ void make_prop(const Setup& s, Prop2<T>& pr,
 #pragma unroll
     for (int i = 1; i < 4; ++i) zmul_masked(m, u[mm][i - 1], NZU[mm][i - 1], u[mm][i]);
   }
+}
+
+// One step of one control phase: coupling X (mechanics <- f), forcing c, and
+// the f update f+ = pf f + qf.
+__device__ __forceinline__ void one_step_phase(const Phase& phs, const double u[2][4][4],
+                                               double X[4][2], double c[4], double pf[2],
+                                               double qf[2]) {
+#pragma unroll
+  for (int r = 0; r < 4; ++r) c[r] = 0.0;
+#pragma unroll
+  for (int mm = 0; mm < 2; ++mm) {
+    const double zd = mm == 0 ? phs.zd_ag : phs.zd_ant;
+    const double nt = mm == 0 ? phs.nt_ag : phs.nt_ant;
+    const double a[4] = {0.0, 0.0, 0.0, 1.0 / 24.0};
+    double av[4];
+    av[3] = a[3];
+    av[2] = fma(zd, av[3], 1.0 / 6.0);
+    av[1] = fma(zd, av[2], 0.5);
+    av[0] = fma(zd, av[1], 1.0);
+    const double g = -zd * nt;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      // X[:,m] = sum_i u_i a_i;  c += g sum_{i<3} u_i a_{i+1}  (structural zeros skipped)
+      double x = 0.0, cc = 0.0;
+      bool first_x = true, first_c = true;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (!NZU[mm][i][r]) continue;
+        x = first_x ? u[mm][i][r] * av[i] : fma(u[mm][i][r], av[i], x);
+        first_x = false;
+        if (i < 3) {
+          cc = first_c ? u[mm][i][r] * av[i + 1] : fma(u[mm][i][r], av[i + 1], cc);
+          first_c = false;
+        }
+      }
+      X[r][mm] = x;
+      if (!first_c) c[r] = fma(g, cc, c[r]);
+    }
+    pf[mm] = fma(zd, av[0], 1.0);
+    qf[mm] = g * av[0];
+  }
+}
+
+// Two-step block of one phase from its one-step map (X2 = P X + X diag(pf),
+// c2 = P c + X qf + c, f: pf^2, pf qf + qf) plus row 0 of the one-step map.
+template <typename T>
+__device__ __forceinline__ void two_step_phase(const double P[4][4], const double X[4][2],
+                                               const double c[4], const double pf[2],
+                                               const double qf[2], PhaseProp2<T>& q) {
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    double c2 = fma(X[r][1], qf[1], fma(X[r][0], qf[0], c[r]));
+#pragma unroll
+    for (int l = 0; l < 4; ++l) c2 = fma(P[r][l], c[l], c2);
+    q.c2[r] = (T)c2;
+#pragma unroll
+    for (int mm = 0; mm < 2; ++mm) {
+      double x2 = X[r][mm] * pf[mm];
+#pragma unroll
+      for (int l = 0; l < 4; ++l) x2 = fma(P[r][l], X[l][mm], x2);
+      q.X2[r][mm] = (T)x2;
+    }
+  }
+#pragma unroll
+  for (int mm = 0; mm < 2; ++mm) {
+    q.pf2[mm] = (T)(pf[mm] * pf[mm]);
+    q.qf2[mm] = (T)fma(pf[mm], qf[mm], qf[mm]);
+    q.X0[mm] = (T)X[0][mm];
+  }
+  q.c0 = (T)c[0];
+}
+
+template <typename T>
+__device__ __forceinline__ void square_P(const double P[4][4], Prop2<T>& pr) {
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
 #pragma unroll
@@ -557,64 +635,27 @@ __device__ __forceinline__ void make_prop(const Setup& s, Prop2<T>& pr,
     }
     pr.P0[i] = (T)P[0][i];
   }
+}
+
+// STASH: the post-pulse phase is written to the stash as soon as it is built
+// (post-pulse first), so it never occupies registers next to the pulse phase
+// -- this lowers the kernel's register peak at the setup -> loop transition.
+template <typename T, bool STASH = false>
+__device__ __forceinline__ void make_prop(const Setup& s, Prop2<T>& pr,
+                                          typename Vec2<T>::type* st2 = nullptr, int ld = 0) {
+  const Mech& m = s.m;
+  double P[4][4];
+  one_step_P(m, P);
+  double u[2][4][4];
+  coupling_u(m, u);
+  square_P<T>(P, pr);
 #pragma unroll
   for (int phi = 0; phi < 2; ++phi) {
     const int ph = STASH ? 1 - phi : phi;
-    double X[4][2], c[4] = {0.0, 0.0, 0.0, 0.0}, pf[2], qf[2];
-#pragma unroll
-    for (int mm = 0; mm < 2; ++mm) {
-      const double zd = mm == 0 ? s.ph[ph].zd_ag : s.ph[ph].zd_ant;
-      const double nt = mm == 0 ? s.ph[ph].nt_ag : s.ph[ph].nt_ant;
-      const double a[4] = {0.0, 0.0, 0.0, 1.0 / 24.0};
-      double av[4];
-      av[3] = a[3];
-      av[2] = fma(zd, av[3], 1.0 / 6.0);
-      av[1] = fma(zd, av[2], 0.5);
-      av[0] = fma(zd, av[1], 1.0);
-      const double g = -zd * nt;
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        // X[:,m] = sum_i u_i a_i;  c += g sum_{i<3} u_i a_{i+1}  (structural zeros skipped)
-        double x = 0.0, cc = 0.0;
-        bool first_x = true, first_c = true;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          if (!NZU[mm][i][r]) continue;
-          x = first_x ? u[mm][i][r] * av[i] : fma(u[mm][i][r], av[i], x);
-          first_x = false;
-          if (i < 3) {
-            cc = first_c ? u[mm][i][r] * av[i + 1] : fma(u[mm][i][r], av[i + 1], cc);
-            first_c = false;
-          }
-        }
-        X[r][mm] = x;
-        if (!first_c) c[r] = fma(g, cc, c[r]);
-      }
-      pf[mm] = fma(zd, av[0], 1.0);
-      qf[mm] = g * av[0];
-    }
+    double X[4][2], c[4], pf[2], qf[2];
+    one_step_phase(s.ph[ph], u, X, c, pf, qf);
     PhaseProp2<T>& q = pr.ph[ph];
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      double c2 = fma(X[r][1], qf[1], fma(X[r][0], qf[0], c[r]));
-#pragma unroll
-      for (int l = 0; l < 4; ++l) c2 = fma(P[r][l], c[l], c2);
-      q.c2[r] = (T)c2;
-#pragma unroll
-      for (int mm = 0; mm < 2; ++mm) {
-        double x2 = X[r][mm] * pf[mm];
-#pragma unroll
-        for (int l = 0; l < 4; ++l) x2 = fma(P[r][l], X[l][mm], x2);
-        q.X2[r][mm] = (T)x2;
-      }
-    }
-#pragma unroll
-    for (int mm = 0; mm < 2; ++mm) {
-      q.pf2[mm] = (T)(pf[mm] * pf[mm]);
-      q.qf2[mm] = (T)fma(pf[mm], qf[mm], qf[mm]);
-      q.X0[mm] = (T)X[0][mm];
-    }
-    q.c0 = (T)c[0];
+    two_step_phase<T>(P, X, c, pf, qf, q);
     if (STASH && ph == 1) stash_phase<T>(q, st2, ld);
     if (ph == 0) {
 #pragma unroll
@@ -623,6 +664,78 @@ __device__ __forceinline__ void make_prop(const Setup& s, Prop2<T>& pr,
       pr.f1[1] = (T)qf[1];
     }
   }
+}
+
+// ----------------------------------------------------------------------------
+// Integer substeps (reading Q25): the sample-to-sample map of a phase is the
+// one-substep map (h/s) to the power s, by binary exponentiation of the
+// affine map (z, f) -> (P z + X f + c, pf f + qf) -- the loop is unchanged
+// and costs the same per sample; only the setup grows (~log2 s squarings).
+// Composition A after B: P = PA PB, X = PA XB + XA diag(pfB),
+// c = PA cB + XA qfB + cA, pf = pfA pfB, qf = pfA qfB + qfA.
+// ----------------------------------------------------------------------------
+struct AffineMap {
+  double P[4][4];
+  double X[2][4][2], c[2][4], pf[2][2], qf[2][2];   // per control phase
+};
+
+__device__ __forceinline__ void compose_maps(const AffineMap& A, const AffineMap& B, AffineMap& o) {
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < 4; ++j) {
+      double v = A.P[i][0] * B.P[0][j];
+      for (int l = 1; l < 4; ++l) v = fma(A.P[i][l], B.P[l][j], v);
+      o.P[i][j] = v;
+    }
+  for (int ph = 0; ph < 2; ++ph) {
+    for (int r = 0; r < 4; ++r) {
+      double cc = fma(A.X[ph][r][1], B.qf[ph][1], fma(A.X[ph][r][0], B.qf[ph][0], A.c[ph][r]));
+      for (int l = 0; l < 4; ++l) cc = fma(A.P[r][l], B.c[ph][l], cc);
+      o.c[ph][r] = cc;
+      for (int mm = 0; mm < 2; ++mm) {
+        double x = A.X[ph][r][mm] * B.pf[ph][mm];
+        for (int l = 0; l < 4; ++l) x = fma(A.P[r][l], B.X[ph][l][mm], x);
+        o.X[ph][r][mm] = x;
+      }
+    }
+    for (int mm = 0; mm < 2; ++mm) {
+      o.pf[ph][mm] = A.pf[ph][mm] * B.pf[ph][mm];
+      o.qf[ph][mm] = fma(A.pf[ph][mm], B.qf[ph][mm], A.qf[ph][mm]);
+    }
+  }
+}
+
+// M <- M^n, n >= 1
+static __device__ __noinline__ void map_power(AffineMap& M, int n) {
+  AffineMap R, B = M, t;
+  bool have = false;
+  while (n > 0) {
+    if (n & 1) {
+      if (have) { compose_maps(B, R, t); R = t; }
+      else { R = B; have = true; }
+    }
+    n >>= 1;
+    if (n > 0) { compose_maps(B, B, t); B = t; }
+  }
+  M = R;
+}
+
+template <typename T>
+__device__ __noinline__ void make_prop_sub(const Setup& s, int nsub, Prop2<T>& pr,
+                                           typename Vec2<T>::type* st2, int ld) {
+  AffineMap M;
+  one_step_P(s.m, M.P);
+  double u[2][4][4];
+  coupling_u(s.m, u);
+  for (int ph = 0; ph < 2; ++ph) one_step_phase(s.ph[ph], u, M.X[ph], M.c[ph], M.pf[ph], M.qf[ph]);
+  map_power(M, nsub);
+  square_P<T>(M.P, pr);
+  for (int ph = 1; ph >= 0; --ph) {
+    two_step_phase<T>(M.P, M.X[ph], M.c[ph], M.pf[ph], M.qf[ph], pr.ph[ph]);
+    if (ph == 1) stash_phase<T>(pr.ph[1], st2, ld);
+  }
+  for (int r = 0; r < 4; ++r) pr.z1[r] = (T)M.c[0][r];
+  pr.f1[0] = (T)M.qf[0][0];
+  pr.f1[1] = (T)M.qf[0][1];
 }
 
 // ----------------------------------------------------------------------------
@@ -908,7 +1021,7 @@ __device__ __forceinline__ void run_propagator_multi(const Prop2<T> (&pr)[C],
 template <typename T, int METRIC, bool TRAJ>
 __device__ __forceinline__ T run_rk4_stages(const Setup& s, int32_t n_steps,
                                             const T* __restrict__ rel, T* __restrict__ traj,
-                                            int64_t ld_out, T theta0, T sgn) {
+                                            int64_t ld_out, T theta0, T sgn, int32_t substeps = 1) {
   const T z01 = (T)s.m.z01, z10 = (T)s.m.z10, z11 = (T)s.m.z11, z12 = (T)s.m.z12,
           z13 = (T)s.m.z13, z20 = (T)s.m.z20, z22 = (T)s.m.z22, z30 = (T)s.m.z30,
           z33 = (T)s.m.z33, hba = (T)s.m.hb_ag, hbn = (T)s.m.hb_ant;
@@ -923,28 +1036,30 @@ __device__ __forceinline__ T run_rk4_stages(const Setup& s, int32_t n_steps,
       zda = (T)s.ph[1].zd_ag; zdn = (T)s.ph[1].zd_ant;
       zna = (T)(s.ph[1].zd_ag * s.ph[1].nt_ag); znn = (T)(s.ph[1].zd_ant * s.ph[1].nt_ant);
     }
-    T K[4][6];
-    T Y[6];
+    for (int32_t sub = 0; sub < substeps; ++sub) {   // reading Q25: control held per sample
+      T K[4][6];
+      T Y[6];
 #pragma unroll
-    for (int i = 0; i < 6; ++i) Y[i] = y[i];
+      for (int i = 0; i < 6; ++i) Y[i] = y[i];
 #pragma unroll
-    for (int st = 0; st < 4; ++st) {
-      K[st][0] = z01 * Y[1];
-      K[st][1] = fma(z10, Y[0], fma(z11, Y[1], fma(z12, Y[2], z13 * Y[3])));
-      K[st][2] = fma(z20, Y[0], fma(z22, Y[2], hba * Y[4]));
-      K[st][3] = fma(z30, Y[0], fma(z33, Y[3], hbn * Y[5]));
-      K[st][4] = fma(zda, Y[4], -zna);
-      K[st][5] = fma(zdn, Y[5], -znn);
-      if (st < 3) {
-        const T w = st == 2 ? T(1) : half;
+      for (int st = 0; st < 4; ++st) {
+        K[st][0] = z01 * Y[1];
+        K[st][1] = fma(z10, Y[0], fma(z11, Y[1], fma(z12, Y[2], z13 * Y[3])));
+        K[st][2] = fma(z20, Y[0], fma(z22, Y[2], hba * Y[4]));
+        K[st][3] = fma(z30, Y[0], fma(z33, Y[3], hbn * Y[5]));
+        K[st][4] = fma(zda, Y[4], -zna);
+        K[st][5] = fma(zdn, Y[5], -znn);
+        if (st < 3) {
+          const T w = st == 2 ? T(1) : half;
 #pragma unroll
-        for (int i = 0; i < 6; ++i) Y[i] = fma(w, K[st][i], y[i]);
+          for (int i = 0; i < 6; ++i) Y[i] = fma(w, K[st][i], y[i]);
+        }
       }
-    }
 #pragma unroll
-    for (int i = 0; i < 6; ++i) {
-      const T t = fma(two, K[2][i], fma(two, K[1][i], K[0][i])) + K[3][i];
-      y[i] = fma(sixth, t, y[i]);
+      for (int i = 0; i < 6; ++i) {
+        const T t = fma(two, K[2][i], fma(two, K[1][i], K[0][i])) + K[3][i];
+        y[i] = fma(sixth, t, y[i]);
+      }
     }
     accumulate<METRIC>(acc, TRAJ ? y[0] : y[0] - rel[k + 1]);
     if (TRAJ) traj[(int64_t)(k + 1) * ld_out] = fma(sgn, y[0], theta0);
@@ -967,9 +1082,10 @@ __device__ __forceinline__ double evaluate(const double p[NP], const CtlDev& c, 
   // the segmented loop's warp reductions need every lane of the warp.
   const double pen = check_physical ? physical_penalty(p) : 0.0;
   Setup s;
-  make_setup(p, c.dt_ms, c.h, c.n_steps, Aprime, pw_default, s);
+  // INTEG 2 = the propagator with substeps (internal; reading Q25)
+  make_setup(p, c.dt_ms, c.h, c.n_steps, Aprime, pw_default, s, INTEG == 0 ? 1 : c.substeps);
   T acc;
-  if (INTEG == 0) {
+  if (INTEG == 0 || INTEG == 2) {
     Prop2<T> pr;
 #ifdef OPMM_EXP_NOPROP   // timing experiment only: skip the propagator build
     {
@@ -998,12 +1114,20 @@ __device__ __forceinline__ double evaluate(const double p[NP], const CtlDev& c, 
                                           stash_ld < 0 ? (int)blockDim.x : stash_ld);
 #else
     const int ld = stash_ld < 0 ? (int)blockDim.x : stash_ld;
-    make_prop<T, true>(s, pr, reinterpret_cast<typename Vec2<T>::type*>(stash) + threadIdx.x, ld);
+    typename Vec2<T>::type* st2 = reinterpret_cast<typename Vec2<T>::type*>(stash) + threadIdx.x;
+    if (INTEG == 2) {   // sample map = one-substep map ^ substeps, out of line
+      Prop2<T> sub;
+      make_prop_sub<T>(s, c.substeps, sub, st2, ld);
+      pr = sub;
+    } else {
+      make_prop<T, true>(s, pr, st2, ld);
+    }
     acc = run_propagator<T, METRIC, TRAJ, true>(pr, s.n_pulse, c.n_steps, rel, traj, ld_out,
                                                 (T)c.theta0, (T)sgn, stash, ld);
 #endif
   } else {
-    acc = run_rk4_stages<T, METRIC, TRAJ>(s, c.n_steps, rel, traj, ld_out, (T)c.theta0, (T)sgn);
+    acc = run_rk4_stages<T, METRIC, TRAJ>(s, c.n_steps, rel, traj, ld_out, (T)c.theta0, (T)sgn,
+                                          c.substeps);
   }
   if (pen != 0.0) {
     if (TRAJ) {

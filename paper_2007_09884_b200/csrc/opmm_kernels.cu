@@ -925,12 +925,17 @@ __global__ void generate_kernel(SpaceDev sp, uint32_t saccade, int64_t begin, in
 template <typename T, int INTEG, int METRIC>
 static const void* fit_fn() { return reinterpret_cast<const void*>(&fit_kernel<T, INTEG, METRIC>); }
 
+// integrator 2 = the propagator with substeps (internal; the host picks it
+// when opmm_control.substeps > 1) -- its own instantiation, so the out-of-line
+// substep power never touches the plain propagator kernels' register budget
 const void* fit_kernel_ptr(int precision, int integrator, int metric) {
   if (precision == 0) {
     if (integrator == 0) return metric == 0 ? fit_fn<double, 0, 0>() : fit_fn<double, 0, 1>();
+    if (integrator == 2) return metric == 0 ? fit_fn<double, 2, 0>() : fit_fn<double, 2, 1>();
     return metric == 0 ? fit_fn<double, 1, 0>() : fit_fn<double, 1, 1>();
   }
   if (integrator == 0) return metric == 0 ? fit_fn<float, 0, 0>() : fit_fn<float, 0, 1>();
+  if (integrator == 2) return metric == 0 ? fit_fn<float, 2, 0>() : fit_fn<float, 2, 1>();
   return metric == 0 ? fit_fn<float, 1, 0>() : fit_fn<float, 1, 1>();
 }
 
@@ -952,18 +957,22 @@ static const void* ss_fn() { return reinterpret_cast<const void*>(&simscore_kern
 const void* simscore_kernel_ptr(int precision, int integrator, int metric) {
   if (precision == 0) {
     if (integrator == 0) return metric == 0 ? ss_fn<double, 0, 0>() : ss_fn<double, 0, 1>();
+    if (integrator == 2) return metric == 0 ? ss_fn<double, 2, 0>() : ss_fn<double, 2, 1>();
     return metric == 0 ? ss_fn<double, 1, 0>() : ss_fn<double, 1, 1>();
   }
   if (integrator == 0) return metric == 0 ? ss_fn<float, 0, 0>() : ss_fn<float, 0, 1>();
+  if (integrator == 2) return metric == 0 ? ss_fn<float, 2, 0>() : ss_fn<float, 2, 1>();
   return metric == 0 ? ss_fn<float, 1, 0>() : ss_fn<float, 1, 1>();
 }
 
 const void* simulate_kernel_ptr(int precision, int integrator) {
   if (precision == 0)
-    return integrator == 0 ? reinterpret_cast<const void*>(&simulate_kernel<double, 0>)
-                           : reinterpret_cast<const void*>(&simulate_kernel<double, 1>);
-  return integrator == 0 ? reinterpret_cast<const void*>(&simulate_kernel<float, 0>)
-                         : reinterpret_cast<const void*>(&simulate_kernel<float, 1>);
+    return integrator == 0   ? reinterpret_cast<const void*>(&simulate_kernel<double, 0>)
+           : integrator == 2 ? reinterpret_cast<const void*>(&simulate_kernel<double, 2>)
+                             : reinterpret_cast<const void*>(&simulate_kernel<double, 1>);
+  return integrator == 0   ? reinterpret_cast<const void*>(&simulate_kernel<float, 0>)
+         : integrator == 2 ? reinterpret_cast<const void*>(&simulate_kernel<float, 2>)
+                           : reinterpret_cast<const void*>(&simulate_kernel<float, 1>);
 }
 
 const void* score_kernel_ptr(int precision, int metric) {

@@ -59,7 +59,8 @@ __device__ __forceinline__ void ref_rhs(const double p[NP], const double y[6], d
 }
 
 __device__ double ref_objective(const double p_in[NP], const double* rel, int32_t n_steps,
-                                double dt_ms, double Aprime, double pw_default, int metric) {
+                                double dt_ms, double Aprime, double pw_default, int metric,
+                                int32_t substeps) {
   double p[NP];
 #pragma unroll
   for (int d = 0; d < NP; ++d) p[d] = p_in[d];
@@ -108,7 +109,8 @@ __device__ double ref_objective(const double p_in[NP], const double* rel, int32_
     lv_ag = Dr(Ar(Mr(G, Ar(theta_star, Aprime)), Mr(NANT_FLOOR, g_ant)), g_ag);
   }
   const double npd = ceil(Dr(p[PW_], dt_ms));
-  const double h = Mr(1e-3, dt_ms);
+  const int32_t nsub = substeps > 1 ? substeps : 1;   // reading Q25
+  const double h = Dr(Mr(1e-3, dt_ms), (double)nsub);
   const double h2 = Mr(0.5, h), h6 = Dr(h, 6.0);
   double y[6];
 #pragma unroll
@@ -123,20 +125,22 @@ __device__ double ref_objective(const double p_in[NP], const double* rel, int32_
     const double na = pulse ? p[NSAC_AG] : lv_ag, nn = pulse ? p[NSAC_ANT] : lv_ant;
     const double ta = pulse ? p[TAU_AC_AG] : p[TAU_DE_AG];
     const double tn = pulse ? p[TAU_AC_ANT] : p[TAU_DE_ANT];
-    double k1[6], k2[6], k3[6], k4[6], yt[6];
-    ref_rhs(p, y, na, nn, ta, tn, k1);
+    for (int32_t sub = 0; sub < nsub; ++sub) {
+      double k1[6], k2[6], k3[6], k4[6], yt[6];
+      ref_rhs(p, y, na, nn, ta, tn, k1);
 #pragma unroll
-    for (int i = 0; i < 6; ++i) yt[i] = Ar(y[i], Mr(h2, k1[i]));
-    ref_rhs(p, yt, na, nn, ta, tn, k2);
+      for (int i = 0; i < 6; ++i) yt[i] = Ar(y[i], Mr(h2, k1[i]));
+      ref_rhs(p, yt, na, nn, ta, tn, k2);
 #pragma unroll
-    for (int i = 0; i < 6; ++i) yt[i] = Ar(y[i], Mr(h2, k2[i]));
-    ref_rhs(p, yt, na, nn, ta, tn, k3);
+      for (int i = 0; i < 6; ++i) yt[i] = Ar(y[i], Mr(h2, k2[i]));
+      ref_rhs(p, yt, na, nn, ta, tn, k3);
 #pragma unroll
-    for (int i = 0; i < 6; ++i) yt[i] = Ar(y[i], Mr(h, k3[i]));
-    ref_rhs(p, yt, na, nn, ta, tn, k4);
+      for (int i = 0; i < 6; ++i) yt[i] = Ar(y[i], Mr(h, k3[i]));
+      ref_rhs(p, yt, na, nn, ta, tn, k4);
 #pragma unroll
-    for (int i = 0; i < 6; ++i)
-      y[i] = Ar(y[i], Mr(h6, Ar(Ar(Ar(k1[i], Mr(2.0, k2[i])), Mr(2.0, k3[i])), k4[i])));
+      for (int i = 0; i < 6; ++i)
+        y[i] = Ar(y[i], Mr(h6, Ar(Ar(Ar(k1[i], Mr(2.0, k2[i])), Mr(2.0, k3[i])), k4[i])));
+    }
     const double d = Sr(Sr(y[0], ystar[0]), rel[k + 1]);
     acc = metric == 0 ? Ar(acc, fabs(d)) : Ar(acc, Mr(d, d));
   }
@@ -168,6 +172,7 @@ __device__ double test_objective(int fn_id, int n, const double* x) {
 // ---------------------------------------------------------------------------
 // The batched Nelder-Mead kernel: one warp per problem.
 // OBJ: 0 plant/propagator, 1 plant/RK4 stages, 2 plant/reference order,
+// 4 plant/propagator with substeps (reading Q25; internal, chosen by the host),
 //      3 test function.
 // ---------------------------------------------------------------------------
 constexpr int NM_NMAX = NP;               // simplex dimension <= 18
@@ -197,7 +202,7 @@ __global__ void __launch_bounds__(NM_THREADS) nm_kernel(NmArgs a) {
   const int n = a.dim;
   const int32_t ns = a.ctl.n_steps + 1;
   double sgn = 1.0, Aprime = 0.0, pwd = 0.0;
-  if (OBJ < 3) {
+  if (OBJ != 3) {
     const double amp = a.sac_ctl[2 * prob];
     pwd = a.sac_ctl[2 * prob + 1];
     const double* rec = a.rec + prob * (int64_t)ns;
@@ -218,9 +223,10 @@ __global__ void __launch_bounds__(NM_THREADS) nm_kernel(NmArgs a) {
       for (int d = 0; d < NP; ++d) p[d] = x[d];
       if (OBJ == 2) {
         f = ref_objective(p, reinterpret_cast<const double*>(rel), a.ctl.n_steps, a.ctl.dt_ms,
-                          Aprime, pwd, METRIC);
+                          Aprime, pwd, METRIC, a.ctl.substeps);
       } else {
-        f = evaluate<T, OBJ, METRIC, false>(p, a.ctl, Aprime, pwd, rel, nullptr, 0, sgn, nullptr,
+        f = evaluate<T, (OBJ == 4 ? 2 : OBJ), METRIC, false>(p, a.ctl, Aprime, pwd, rel, nullptr, 0,
+                                                            sgn, nullptr,
                                            stash, true);
       }
     }
@@ -235,7 +241,7 @@ __global__ void __launch_bounds__(NM_THREADS) nm_kernel(NmArgs a) {
     double x[NM_NMAX];
     for (int j = 0; j < n; ++j) {
       double v = x0[j];
-      if (OBJ < 3 && j == PW_ && isnan(v)) v = pwd;
+      if (OBJ != 3 && j == PW_ && isnan(v)) v = pwd;
       x[j] = v;
     }
     if (i > 0) x[i - 1] = x[i - 1] != 0.0 ? Mr(Ar(1.0, a.init_scale), x[i - 1]) : Mr(a.init_scale, 0.00025);
@@ -367,6 +373,10 @@ static const void* nm_fn() { return reinterpret_cast<const void*>(&nm_kernel<T, 
 
 const void* nm_kernel_ptr(int precision, int obj, int metric) {
   if (obj == 3) return nm_fn<double, 3, 0>();
+  if (obj == 4) {
+    if (precision == 0) return metric == 0 ? nm_fn<double, 4, 0>() : nm_fn<double, 4, 1>();
+    return metric == 0 ? nm_fn<float, 4, 0>() : nm_fn<float, 4, 1>();
+  }
   if (obj == 2) return metric == 0 ? nm_fn<double, 2, 0>() : nm_fn<double, 2, 1>();
   if (precision == 0) {
     if (obj == 0) return metric == 0 ? nm_fn<double, 0, 0>() : nm_fn<double, 0, 1>();
@@ -381,7 +391,7 @@ size_t nm_smem(int precision, int obj, int32_t n_samples) {
                                                    : rel_bytes<float>(n_samples);
   const size_t st = precision == 0 || obj >= 2 ? stash_bytes<double>(NM_THREADS)
                                                : stash_bytes<float>(NM_THREADS);
-  return NM_WARPS * sizeof(NmWarpSmem) + NM_WARPS * (obj == 3 ? 0 : relb) + (obj < 2 ? st : 0);
+  return NM_WARPS * sizeof(NmWarpSmem) + NM_WARPS * (obj == 3 ? 0 : relb) + (obj < 2 || obj == 4 ? st : 0);
 }
 
 int nm_problems_per_block() { return NM_WARPS; }

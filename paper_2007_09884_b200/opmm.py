@@ -37,7 +37,7 @@ class OpmmError(RuntimeError):
 
 
 class Control(C.Structure):
-    _fields_ = [("dt_ms", C.c_double), ("n_steps", C.c_int32), ("pad_", C.c_int32),
+    _fields_ = [("dt_ms", C.c_double), ("n_steps", C.c_int32), ("substeps", C.c_int32),
                 ("amplitude_deg", C.c_double), ("theta0_deg", C.c_double),
                 ("pw_default_ms", C.c_double)]
 
@@ -150,11 +150,14 @@ def _check(status: int, where: str):
 
 # ---------------------------------------------------------------------- structs
 def control(c=None, **kw) -> Control:
-    """Control from any object with dt_ms/n_steps/amplitude_deg/theta0_deg/pw_default_ms."""
+    """Control from any object with dt_ms/n_steps/amplitude_deg/theta0_deg/pw_default_ms
+    (and optionally substeps)."""
     src = {k: getattr(c, k) for k in ("dt_ms", "n_steps", "amplitude_deg", "theta0_deg", "pw_default_ms")} \
         if c is not None else {}
+    if c is not None:
+        src["substeps"] = getattr(c, "substeps", 0)
     src.update(kw)
-    return Control(float(src.get("dt_ms", 1.0)), int(src.get("n_steps", 100)), 0,
+    return Control(float(src.get("dt_ms", 1.0)), int(src.get("n_steps", 100)), int(src.get("substeps", 0)),
                    float(src.get("amplitude_deg", math.nan)), float(src.get("theta0_deg", 0.0)),
                    float(src.get("pw_default_ms", 40.0)))
 

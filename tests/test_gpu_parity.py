@@ -98,7 +98,7 @@ def assert_fp64_errors(E, O, cand_of, rec, ctl, scale, metric=0):
     refereed = 0
     for i in np.flatnonzero(d > 1e-9):
         p = cand_of(int(i))
-        rho = referee.rk4_spectral_radius(p, ctl.dt_ms)
+        rho = referee.rk4_spectral_radius(p, ctl.dt_ms, getattr(ctl, "substeps", 1))
         assert rho > 1.0, (int(i), d[i], rho)
         ref = referee.objective_longdouble(p, rec, ctl, metric)
         assert abs(E[i] - ref) <= 1e-9 * max(ref, scale), (int(i), E[i], O[i], ref)
@@ -110,7 +110,8 @@ def oracle_dtheta(cands, ctl):
     out = []
     for p in cands:
         try:
-            out.append(oracle.simulate(p, ctl.dt_ms, ctl.n_steps, abs(ctl.amplitude_deg), ctl.pw_default_ms))
+            out.append(oracle.simulate(p, ctl.dt_ms, ctl.n_steps, abs(ctl.amplitude_deg), ctl.pw_default_ms,
+                                       substeps=max(int(ctl.substeps or 0), 1)))
         except ValueError:
             out.append(None)
     return out
@@ -728,3 +729,74 @@ def test_simulate_batch_equals_single_calls(opmm, h):
     bad[3] = W.Control(n_steps=100)
     with pytest.raises(opmm.OpmmError):
         opmm.opmm_simulate_batch(h, opc, n, bad, got)
+
+
+# --------------------------------------------------------------------------- substeps (Q25)
+@pytest.mark.parametrize("integrator", [0, 1])
+@pytest.mark.parametrize("substeps", [2, 3, 8])
+def test_simulate_substeps_fp64(opmm, h, integrator, substeps):
+    """s RK4 substeps per sample: the propagator composes the substep map s
+    times (binary powering) into one sample map; the four-stage integrator
+    runs the s substeps literally.  Both against the oracle's literal
+    substeps, fp64 1e-9 on every finite trajectory."""
+    ctl = W.Control(substeps=substeps)
+    cands = candidate_set()
+    n = len(cands)
+    traj = torch.full((ctl.n_steps + 1, n), -1.0, dtype=torch.float64, device="cuda")
+    status = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    opmm.opmm_simulate(h, soa(cands), n, ctl, traj, integrator=integrator, status=status,
+                       stream=torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    T, S = traj.cpu().numpy(), status.cpu().numpy()
+    refs = oracle_dtheta(cands, ctl)
+    checked = 0
+    for i, ref in enumerate(refs):
+        if ref is None:
+            assert S[i] == 1
+            continue
+        if not (np.all(np.isfinite(ref)) and np.abs(ref).sum() < 1e20):
+            assert S[i] == 2, i
+            continue
+        assert S[i] == 0, i
+        err = np.max(np.abs(T[:, i] - ref)) / max(np.max(np.abs(ref)), 1.0)
+        assert err <= 1e-9, (i, err)
+        checked += 1
+    assert checked > n // 3
+
+
+@pytest.mark.parametrize("precision", [0, 1])
+def test_fit_substeps_matches_oracle(opmm, h, precision):
+    """Fit with 4 substeps per sample: every candidate's E against the oracle
+    (fp64: Q22 rule with the substep-aware referee; fp32: finite/+inf
+    classification and the winner), and substeps stabilise candidates that
+    diverge at h = dt."""
+    ctl = W.Control(substeps=4)
+    rec = trace(W.Control())
+    sp = W.paper_space()
+    n = 2000
+    r, E = _fit(opmm, h, rec, ctl, sp, n, precision=precision)
+    o = oracle.fit(rec, ctl, sp, 0, n, want_err=True, nthreads=oracle.max_threads())
+    O = o["err"]
+    if precision == 0:
+        assert_fp64_errors(E, O, lambda i: oracle.generate(sp, i), rec, ctl, np.abs(rec - rec[0]).sum())
+        assert r["best_index"] == o["best_index"]
+    else:
+        assert np.array_equal(np.isinf(E), np.isinf(O))
+    plain = oracle.fit(rec, W.Control(), sp, 0, n)
+    assert o["n_finite"] > plain["n_finite"]
+    assert r["n_finite"] == o["n_finite"]
+    assert abs(r["cpu_check"] - o["best_err"]) <= 1e-9 * o["best_err"] or precision == 1
+
+
+def test_nm_substeps_reference_bit_identical(opmm, h):
+    """The reference-order NM objective with substeps is bit-identical to the
+    oracle's serial Nelder-Mead with substeps."""
+    ctl = W.Control(substeps=3, amplitude_deg=10.0)
+    rec = trace(W.Control())
+    res = opmm.opmm_estimate_batch(h, rec[None, :], [ctl],
+                                   options=opmm.nm_options(objective=opmm.NM_OBJ_REFERENCE,
+                                                           max_iter=60, cpu_check=0))
+    o = oracle.estimate_batch(rec[None, :], [ctl], max_iter=60)
+    assert res[0]["iterations"] == int(o["iterations"][0])
+    assert res[0]["f"] == float(o["f"][0])
+    assert np.array_equal(np.array(res[0]["x"]), o["x"][0])

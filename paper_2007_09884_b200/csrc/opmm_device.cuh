@@ -705,7 +705,7 @@ __device__ __forceinline__ void compose_maps(const AffineMap& A, const AffineMap
 }
 
 // M <- M^n, n >= 1
-static __device__ __noinline__ void map_power(AffineMap& M, int n) {
+__device__ __forceinline__ void map_power(AffineMap& M, int n) {
   AffineMap R, B = M, t;
   bool have = false;
   while (n > 0) {
@@ -720,7 +720,7 @@ static __device__ __noinline__ void map_power(AffineMap& M, int n) {
 }
 
 template <typename T>
-__device__ __noinline__ void make_prop_sub(const Setup& s, int nsub, Prop2<T>& pr,
+__device__ __forceinline__ void make_prop_sub(const Setup& s, int nsub, Prop2<T>& pr,
                                            typename Vec2<T>::type* st2, int ld) {
   AffineMap M;
   one_step_P(s.m, M.P);
@@ -1115,10 +1115,8 @@ __device__ __forceinline__ double evaluate(const double p[NP], const CtlDev& c, 
 #else
     const int ld = stash_ld < 0 ? (int)blockDim.x : stash_ld;
     typename Vec2<T>::type* st2 = reinterpret_cast<typename Vec2<T>::type*>(stash) + threadIdx.x;
-    if (INTEG == 2) {   // sample map = one-substep map ^ substeps, out of line
-      Prop2<T> sub;
-      make_prop_sub<T>(s, c.substeps, sub, st2, ld);
-      pr = sub;
+    if (INTEG == 2) {   // sample map = one-substep map ^ substeps (own instantiation)
+      make_prop_sub<T>(s, c.substeps, pr, st2, ld);
     } else {
       make_prop<T, true>(s, pr, st2, ld);
     }

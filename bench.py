@@ -229,6 +229,30 @@ def population_leg(h, opmm, torch, args):
             "mean_best_residual_deg_per_sample": float(np.mean(f / (n_steps + 1)))}
 
 
+def latency_leg(h, opmm, torch, rec, world, max_over_ranks):
+    """Config 3 (real-time mode): wall-clock latency of one synchronous
+    opmm_fit (trace in pinned host memory, H2D + kernel + D2H + CPU_check) at
+    10^5..10^8 candidates in total over the ranks; the real-time bar is the
+    trace's own duration, 100 ms."""
+    rec_np = torch.as_tensor(rec, dtype=torch.float64).pin_memory().numpy()
+    ctl_c, sp_c = opmm.control(W.Control()), opmm.search_space(W.paper_space())
+    opts = opmm.fit_options(cpu_check=1)
+    out = {}
+    for n in (10**5, 10**6, 10**7, 10**8):
+        for _ in range(2):
+            opmm.opmm_fit(h, rec_np, ctl_c, sp_c, n, opts)
+        ts = []
+        for _ in range(5):
+            t0 = time.perf_counter()
+            opmm.opmm_fit(h, rec_np, ctl_c, sp_c, n, opts)
+            ts.append(time.perf_counter() - t0)
+        ms = 1e3 * statistics.median(ts)
+        ms = max_over_ranks(ms)
+        out[f"{n:.0e}"] = {"ms": ms, "realtime_factor": 100.0 / ms}
+    return {"metric": "fit latency (sync opmm_fit, host trace, CPU_check on), median of 5",
+            "n_gpus": world, "candidates": out}
+
+
 def nm_leg(h, opmm, torch, args):
     """The paper's own estimator (batched parallel Nelder-Mead)
     on a synthetic population (SURVEY 8(d) config 5 recipe: A ~ U[5, 30] deg,
@@ -348,6 +372,7 @@ def run_gpu(args):
     barrier()
     e2e_ms = max_over_ranks(1e3 * sum(t_e2e) / len(t_e2e))
 
+    lat = latency_leg(h, opmm, torch, rec, world, max_over_ranks) if not args.no_latency else None
     nm = nm_leg(h, opmm, torch, args) if not args.no_nm else None
     pop = population_leg(h, opmm, torch, args) if (not args.no_pop and world == 1) else None
 
@@ -386,6 +411,8 @@ def run_gpu(args):
     }
     if nm is not None:
         line["nm"] = nm
+    if lat is not None:
+        line["latency"] = lat
     if pop is not None:
         line["population"] = pop
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -406,6 +433,7 @@ def main():
     ap.add_argument("--per-gpu", type=int, default=PER_GPU)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-nm", action="store_true")
+    ap.add_argument("--no-latency", action="store_true")
     ap.add_argument("--nm-saccades", type=int, default=4096)
     ap.add_argument("--no-pop", action="store_true")
     ap.add_argument("--pop-saccades", type=int, default=10000)

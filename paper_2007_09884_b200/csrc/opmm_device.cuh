@@ -249,6 +249,32 @@ __device__ __forceinline__ double generate_pw(const SpaceDev& sp, uint32_t sacca
   return __dmul_rn(sp.lo[PW_], exp(__dmul_rn((double)digit, sp.span[PW_])));
 }
 
+// Sort key of fit_kernel's pre-pass: the block index at which the pulse ends,
+// n_pulse / 2 -- scheduling only (results never depend on it), so random
+// spaces map the PW word in fp32 (no fp64 exp/division); grid spaces and the
+// 9-parameter model use the exact value.
+__device__ __forceinline__ int pulse_end_key(const SpaceDev& sp, uint32_t saccade, int64_t idx,
+                                             double pw_default, double dt_ms, int32_t n_steps,
+                                             int nbins, const double2* __restrict__ tab) {
+  float npf;
+  if (sp.model != 1 && sp.mode == 0) {
+    const uint4 w = philox4x32_10(make_uint4((uint32_t)((uint64_t)idx & 0xffffffffu),
+                                             (uint32_t)((uint64_t)idx >> 32), saccade, 4u),
+                                  make_uint2(sp.key0, sp.key1));
+    const float u = fmaf((float)w.y, 2.3283064365386963e-10f, 1.1641532182693481e-10f);
+    const float lo = (float)sp.lo[PW_], span = (float)sp.span[PW_];
+    const float pw = sp.kind[PW_] == 0 ? lo : sp.kind[PW_] == 1 ? fmaf(u, span, lo)
+                                                                : lo * __expf(u * span);
+    npf = ceilf(pw * (float)(1.0 / dt_ms));
+  } else {
+    double pw = sp.model == 1 ? pw_default : generate_pw(sp, saccade, idx, tab);
+    if (isnan(pw)) pw = pw_default;
+    npf = (float)ceil(pw / dt_ms);
+  }
+  const int np = !(npf <= (float)n_steps) ? n_steps + 1 : (int)npf;   // NaN -> whole-pulse bin
+  return min(max(np, 0) >> 1, nbins - 1);
+}
+
 // ----------------------------------------------------------------------------
 // Physical check (SPEC D8 SPEC.md:248, reading Q13): 0 if physical, else the
 // penalty 1e10 (1 + sum of violation amounts).  PW NaN is the placeholder.

@@ -324,10 +324,8 @@ __global__ void __launch_bounds__(OPMM_FIT_LB_THREADS, OPMM_FIT_LB_BLOCKS) fit_k
     __syncthreads();
     if (a.sort_lanes) {
       for (int t = tid; t < cnt; t += blockDim.x) {
-        const double pw = (a.space.model == 1 ? pwd : generate_pw(a.space, (uint32_t)sac, sb + t, tab));
-        const double npd = ceil(pw / a.ctl.dt_ms);
-        const int np = npd > (double)a.ctl.n_steps ? a.ctl.n_steps + 1 : (int)npd;
-        const int key = min(np >> 1, nbins - 1);
+        const int key = pulse_end_key(a.space, (uint32_t)sac, sb + t, pwd, a.ctl.dt_ms,
+                                      a.ctl.n_steps, nbins, tab);
         const int rank = atomicAdd(&s_hist[key], 1);
         s_tmp[t] = ((uint32_t)key << 16) | (uint32_t)rank;
       }

@@ -317,6 +317,10 @@ __global__ void __launch_bounds__(OPMM_FIT_LB_THREADS, OPMM_FIT_LB_BLOCKS) fit_k
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int nbins = blockDim.x < 256 ? (int)blockDim.x : 256;   // multiple of 32
   const int64_t sstride = (int64_t)gridDim.x * a.super_tile;
+#ifdef OPMM_EXP_BLOCKTIME   // timing experiment only: per-block start/end in err_out
+  unsigned long long t_start;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+#endif
   for (int64_t sb = a.begin + (int64_t)blockIdx.x * a.super_tile; sb < a.end; sb += sstride) {
     const int cnt = (int)min(a.super_tile, a.end - sb);
     if (tid < nbins) s_hist[tid] = 0;
@@ -389,7 +393,9 @@ __global__ void __launch_bounds__(OPMM_FIT_LB_THREADS, OPMM_FIT_LB_BLOCKS) fit_k
       const double E = evaluate<T, INTEG, METRIC, false>(p, a.ctl, Aprime, pwd, rel, nullptr, 0,
                                                          sgn, nullptr, stash, !a.space.all_physical);
       if (valid) {
+#ifndef OPMM_EXP_BLOCKTIME
         if (a.err_out) a.err_out[sac * a.err_ld + i] = E;
+#endif
         nf += E < __longlong_as_double(0x7ff0000000000000LL) ? 1 : 0;
         if (better(E, i, best_e, best_i)) {
           if (certify) { *sec_e = best_e; *sec_i = best_i; }
@@ -401,6 +407,14 @@ __global__ void __launch_bounds__(OPMM_FIT_LB_THREADS, OPMM_FIT_LB_BLOCKS) fit_k
     }
     __syncthreads();   // s_hist / s_perm / s_next are reused by the next pass
   }
+#ifdef OPMM_EXP_BLOCKTIME
+  if (threadIdx.x == 0 && a.err_out) {
+    unsigned long long t_end;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+    a.err_out[2 * blockIdx.x] = (double)t_start;
+    a.err_out[2 * blockIdx.x + 1] = (double)t_end;
+  }
+#endif
   if (sizeof(T) == 4 && a.certify) {
     cert_epilogue<T, METRIC>(a, sac, best_e, best_i, *sec_e, *sec_i, nf, sgn, Aprime, pwd, cert_raw);
     return;

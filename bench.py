@@ -253,7 +253,7 @@ def latency_leg(h, opmm, torch, rec, world, max_over_ranks):
             "n_gpus": world, "candidates": out}
 
 
-def nm_leg(h, opmm, torch, args):
+def nm_leg(h, opmm, torch, args, max_over_ranks=lambda x: x, sum_over_ranks=lambda x: x):
     """The paper's own estimator (batched parallel Nelder-Mead)
     on a synthetic population (SURVEY 8(d) config 5 recipe: A ~ U[5, 30] deg,
     PW = 2.2 A + 15 ms, truths = defaults +-20% on K_SE_AG, B_AG, N_SAC_AG;
@@ -268,11 +268,15 @@ def nm_leg(h, opmm, torch, args):
     t0 = time.perf_counter()
     res = opmm.opmm_estimate_batch(h, recs, ctls, options=opts)
     e2e_s = time.perf_counter() - t0
-    kern_ms = opmm.opmm_last_kernel_ms(h)
+    # N > 1: saccades are sharded over the ranks (opmm_estimate_batch); the
+    # statistics below are this rank's share, the times the max over ranks
+    kern_ms = max_over_ranks(opmm.opmm_last_kernel_ms(h))
+    e2e_s = max_over_ranks(e2e_s)
+    res = [r for r in res if r is not None]
     its = np.array([r["iterations"] for r in res])
     f = np.array([r["f"] for r in res])
     conv = np.array([r["exit_reason"] == 0 for r in res])
-    evals = int(sum(r["gpu_evals"] for r in res))
+    evals = int(sum_over_ranks(float(sum(r["gpu_evals"] for r in res))))
     return {"metric": "NM-fitted saccades/s", "saccades": S, "n_steps": n_steps,
             "objective": "propagator fp64, L1", "value": S / (kern_ms * 1e-3),
             "e2e_value": S / e2e_s, "kernel_ms": kern_ms, "mean_iterations": float(its.mean()),
@@ -312,6 +316,13 @@ def run_gpu(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    def sum_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
     ctl = W.Control()
     rec = make_trace()
     sp = W.paper_space()
@@ -324,7 +335,9 @@ def run_gpu(args):
 
     def device_leg(precision):
         # fp32 runs with certification (top-8 re-scored in fp64)
-        opts = opmm.fit_options(precision=precision, cpu_check=0, certify=1 if precision == opmm.FP32 else 0)
+        # (certification is single-GPU: on N > 1 the fp32 leg is the plain fp32 sweep)
+        opts = opmm.fit_options(precision=precision, cpu_check=0,
+                                certify=1 if (precision == opmm.FP32 and world == 1) else 0)
         for _ in range(args.warmup):
             opmm.opmm_fit_async(h, rec_dev, ctl, sp, n_total, out_dev, opts)
         stream.synchronize()
@@ -373,7 +386,7 @@ def run_gpu(args):
     e2e_ms = max_over_ranks(1e3 * sum(t_e2e) / len(t_e2e))
 
     lat = latency_leg(h, opmm, torch, rec, world, max_over_ranks) if not args.no_latency else None
-    nm = nm_leg(h, opmm, torch, args) if not args.no_nm else None
+    nm = nm_leg(h, opmm, torch, args, max_over_ranks, sum_over_ranks) if not args.no_nm else None
     pop = population_leg(h, opmm, torch, args) if (not args.no_pop and world == 1) else None
 
     per_cand_flop = FLOP_PER_STEP * N_STEPS + FLOP_SETUP
@@ -404,8 +417,9 @@ def run_gpu(args):
                      / (kms64 * 1e-3) / (SMS * FP64_LANES * SM_MAX_MHZ * 1e6)},
         "fp32": {"value": n_total / (ms32 * 1e-3), "ms_per_step": ms32, "kernel_ms": kms32,
                  "best_index": res32["best_index"], "certified": res32["certified"],
-                 "opt_err_fp64": res32["opt_err"],
-                 "mode": "fp32 integrate+score, fp64 setup, top-8 certified by fp64 re-score"},
+                 ("opt_err_fp64" if world == 1 else "opt_err_fp32"): res32["opt_err"],
+                 "mode": ("fp32 integrate+score, fp64 setup, top-8 certified by fp64 re-score"
+                          if world == 1 else "fp32 integrate+score, fp64 setup (uncertified on N > 1)")},
         "result": {"best_index": res64["best_index"], "opt_err": res64["opt_err"],
                    "n_finite": res64["n_finite"], "cpu_check": r["cpu_check"]},
     }

@@ -483,22 +483,22 @@ __device__ constexpr bool NZU[2][4][4] = {
      {true, true, true, true}}};
 
 // out = Z v for a vector v with structural-zero mask nz (compile-time).
-__device__ __forceinline__ void zmul_masked(const Mech& m, const double v[4], const bool nz[4],
-                                            double out[4]) {
-  out[0] = nz[1] ? m.z01 * v[1] : 0.0;
-  double o1 = 0.0;
-  if (nz[0]) o1 = m.z10 * v[0];
-  if (nz[1]) o1 = fma(m.z11, v[1], o1);
-  if (nz[2]) o1 = fma(m.z12, v[2], o1);
-  if (nz[3]) o1 = fma(m.z13, v[3], o1);
+template <typename R, typename MM>
+__device__ __forceinline__ void zmul_masked(const MM& m, const R v[4], const bool nz[4], R out[4]) {
+  out[0] = nz[1] ? R(m.z01) * v[1] : R(0);
+  R o1 = R(0);
+  if (nz[0]) o1 = R(m.z10) * v[0];
+  if (nz[1]) o1 = fma(R(m.z11), v[1], o1);
+  if (nz[2]) o1 = fma(R(m.z12), v[2], o1);
+  if (nz[3]) o1 = fma(R(m.z13), v[3], o1);
   out[1] = o1;
-  double o2 = 0.0;
-  if (nz[0]) o2 = m.z20 * v[0];
-  if (nz[2]) o2 = fma(m.z22, v[2], o2);
+  R o2 = R(0);
+  if (nz[0]) o2 = R(m.z20) * v[0];
+  if (nz[2]) o2 = fma(R(m.z22), v[2], o2);
   out[2] = o2;
-  double o3 = 0.0;
-  if (nz[0]) o3 = m.z30 * v[0];
-  if (nz[3]) o3 = fma(m.z33, v[3], o3);
+  R o3 = R(0);
+  if (nz[0]) o3 = R(m.z30) * v[0];
+  if (nz[3]) o3 = fma(R(m.z33), v[3], o3);
   out[3] = o3;
 }
 
@@ -521,33 +521,35 @@ __device__ __forceinline__ void stash_phase(const PhaseProp2<T>& q, typename Vec
 
 // Building blocks of the propagator (force-inlined into make_prop, so its
 // code is the one-pass form below; make_prop_sub reuses them for substeps).
+// R is the arithmetic type (double in the product; see make_prop).
 //
 // one-step mechanical block P(Z) = (I + Z) + Z^2 (I/2 + Z/6 + Z^2/24),
 // Z = hM: Z^2 from Z's 9 structural non-zeros (19 ops), then one sparse x
-// dense product (Z^2 has zeros at (2,3) and (3,2)) -- ~100 fp64 ops instead
-// of ~156 for three Horner steps.
-__device__ __forceinline__ void one_step_P(const Mech& m, double P[4][4]) {
-  const double h = m.z01, a = m.z10, b = m.z11, c = m.z12, d = m.z13;
-  const double e = m.z20, f = m.z22, g = m.z30, k = m.z33;
-  double Z2[4][4];
+// dense product (Z^2 has zeros at (2,3) and (3,2)) -- ~100 ops instead of
+// ~156 for three Horner steps.
+template <typename R>
+__device__ __forceinline__ void one_step_P(const Mech& m, R P[4][4]) {
+  const R h = R(m.z01), a = R(m.z10), b = R(m.z11), c = R(m.z12), d = R(m.z13);
+  const R e = R(m.z20), f = R(m.z22), g = R(m.z30), k = R(m.z33);
+  R Z2[4][4];
   Z2[0][0] = h * a; Z2[0][1] = h * b; Z2[0][2] = h * c; Z2[0][3] = h * d;
   Z2[1][0] = fma(b, a, fma(c, e, d * g));
   Z2[1][1] = fma(a, h, b * b);
   Z2[1][2] = fma(b, c, c * f);
   Z2[1][3] = fma(b, d, d * k);
-  Z2[2][0] = f * e; Z2[2][1] = e * h; Z2[2][2] = f * f; Z2[2][3] = 0.0;
-  Z2[3][0] = k * g; Z2[3][1] = g * h; Z2[3][2] = 0.0; Z2[3][3] = k * k;
-  const double Zm[4][4] = {{0.0, h, 0.0, 0.0}, {a, b, c, d}, {e, 0.0, f, 0.0}, {g, 0.0, 0.0, k}};
+  Z2[2][0] = f * e; Z2[2][1] = e * h; Z2[2][2] = f * f; Z2[2][3] = R(0);
+  Z2[3][0] = k * g; Z2[3][1] = g * h; Z2[3][2] = R(0); Z2[3][3] = k * k;
+  const R Zm[4][4] = {{R(0), h, R(0), R(0)}, {a, b, c, d}, {e, R(0), f, R(0)}, {g, R(0), R(0), k}};
   // B = I/2 + Z/6 + Z^2/24
-  double B[4][4];
+  R B[4][4];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const bool zz = (i == 0 && j != 1) || (i == 2 && (j == 1 || j == 3)) || (i == 3 && (j == 1 || j == 2));
-      double v = Z2[i][j] * (1.0 / 24.0);
-      if (!zz) v = fma(Zm[i][j], 1.0 / 6.0, v);
-      if (i == j) v += 0.5;
+      R v = Z2[i][j] * R(1.0 / 24.0);
+      if (!zz) v = fma(Zm[i][j], R(1.0 / 6.0), v);
+      if (i == j) v += R(0.5);
       B[i][j] = v;
     }
   // P = I + Z + Z^2 B
@@ -556,7 +558,7 @@ __device__ __forceinline__ void one_step_P(const Mech& m, double P[4][4]) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const bool zz = (i == 0 && j != 1) || (i == 2 && (j == 1 || j == 3)) || (i == 3 && (j == 1 || j == 2));
-      double v = (i == j ? 1.0 : 0.0) + (zz ? 0.0 : Zm[i][j]);
+      R v = (i == j ? R(1) : R(0)) + (zz ? R(0) : Zm[i][j]);
 #pragma unroll
       for (int l = 0; l < 4; ++l) {
         if ((i == 2 && l == 3) || (i == 3 && l == 2)) continue;   // Z^2 structural zeros
@@ -567,39 +569,39 @@ __device__ __forceinline__ void one_step_P(const Mech& m, double P[4][4]) {
 }
 
 // u_i = Z^i (h c_m): c_AG = e_2 / B_AG, c_ANT = e_3 / B_ANT.
-__device__ __forceinline__ void coupling_u(const Mech& m, double u[2][4][4]) {
+template <typename R>
+__device__ __forceinline__ void coupling_u(const Mech& m, R u[2][4][4]) {
 #pragma unroll
   for (int mm = 0; mm < 2; ++mm) {
-    u[mm][0][0] = 0.0; u[mm][0][1] = 0.0;
-    u[mm][0][2] = (mm == 0) ? m.hb_ag : 0.0;
-    u[mm][0][3] = (mm == 0) ? 0.0 : m.hb_ant;
+    u[mm][0][0] = R(0); u[mm][0][1] = R(0);
+    u[mm][0][2] = (mm == 0) ? R(m.hb_ag) : R(0);
+    u[mm][0][3] = (mm == 0) ? R(0) : R(m.hb_ant);
 #pragma unroll
-    for (int i = 1; i < 4; ++i) zmul_masked(m, u[mm][i - 1], NZU[mm][i - 1], u[mm][i]);
+    for (int i = 1; i < 4; ++i) zmul_masked<R>(m, u[mm][i - 1], NZU[mm][i - 1], u[mm][i]);
   }
 }
 
 // One step of one control phase: coupling X (mechanics <- f), forcing c, and
 // the f update f+ = pf f + qf.
-__device__ __forceinline__ void one_step_phase(const Phase& phs, const double u[2][4][4],
-                                               double X[4][2], double c[4], double pf[2],
-                                               double qf[2]) {
+template <typename R>
+__device__ __forceinline__ void one_step_phase(const Phase& phs, const R u[2][4][4], R X[4][2],
+                                               R c[4], R pf[2], R qf[2]) {
 #pragma unroll
-  for (int r = 0; r < 4; ++r) c[r] = 0.0;
+  for (int r = 0; r < 4; ++r) c[r] = R(0);
 #pragma unroll
   for (int mm = 0; mm < 2; ++mm) {
-    const double zd = mm == 0 ? phs.zd_ag : phs.zd_ant;
-    const double nt = mm == 0 ? phs.nt_ag : phs.nt_ant;
-    const double a[4] = {0.0, 0.0, 0.0, 1.0 / 24.0};
-    double av[4];
-    av[3] = a[3];
-    av[2] = fma(zd, av[3], 1.0 / 6.0);
-    av[1] = fma(zd, av[2], 0.5);
-    av[0] = fma(zd, av[1], 1.0);
-    const double g = -zd * nt;
+    const R zd = R(mm == 0 ? phs.zd_ag : phs.zd_ant);
+    const R nt = R(mm == 0 ? phs.nt_ag : phs.nt_ant);
+    R av[4];
+    av[3] = R(1.0 / 24.0);
+    av[2] = fma(zd, av[3], R(1.0 / 6.0));
+    av[1] = fma(zd, av[2], R(0.5));
+    av[0] = fma(zd, av[1], R(1));
+    const R g = -zd * nt;
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       // X[:,m] = sum_i u_i a_i;  c += g sum_{i<3} u_i a_{i+1}  (structural zeros skipped)
-      double x = 0.0, cc = 0.0;
+      R x = R(0), cc = R(0);
       bool first_x = true, first_c = true;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
@@ -614,26 +616,25 @@ __device__ __forceinline__ void one_step_phase(const Phase& phs, const double u[
       X[r][mm] = x;
       if (!first_c) c[r] = fma(g, cc, c[r]);
     }
-    pf[mm] = fma(zd, av[0], 1.0);
+    pf[mm] = fma(zd, av[0], R(1));
     qf[mm] = g * av[0];
   }
 }
 
 // Two-step block of one phase from its one-step map (X2 = P X + X diag(pf),
 // c2 = P c + X qf + c, f: pf^2, pf qf + qf) plus row 0 of the one-step map.
-template <typename T>
-__device__ __forceinline__ void two_step_phase(const double P[4][4], const double X[4][2],
-                                               const double c[4], const double pf[2],
-                                               const double qf[2], PhaseProp2<T>& q) {
+template <typename T, typename R>
+__device__ __forceinline__ void two_step_phase(const R P[4][4], const R X[4][2], const R c[4],
+                                               const R pf[2], const R qf[2], PhaseProp2<T>& q) {
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
-    double c2 = fma(X[r][1], qf[1], fma(X[r][0], qf[0], c[r]));
+    R c2 = fma(X[r][1], qf[1], fma(X[r][0], qf[0], c[r]));
 #pragma unroll
     for (int l = 0; l < 4; ++l) c2 = fma(P[r][l], c[l], c2);
     q.c2[r] = (T)c2;
 #pragma unroll
     for (int mm = 0; mm < 2; ++mm) {
-      double x2 = X[r][mm] * pf[mm];
+      R x2 = X[r][mm] * pf[mm];
 #pragma unroll
       for (int l = 0; l < 4; ++l) x2 = fma(P[r][l], X[l][mm], x2);
       q.X2[r][mm] = (T)x2;
@@ -648,13 +649,13 @@ __device__ __forceinline__ void two_step_phase(const double P[4][4], const doubl
   q.c0 = (T)c[0];
 }
 
-template <typename T>
-__device__ __forceinline__ void square_P(const double P[4][4], Prop2<T>& pr) {
+template <typename T, typename R>
+__device__ __forceinline__ void square_P(const R P[4][4], Prop2<T>& pr) {
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      double a = P[i][0] * P[0][j];
+      R a = P[i][0] * P[0][j];
 #pragma unroll
       for (int l = 1; l < 4; ++l) a = fma(P[i][l], P[l][j], a);
       pr.P2[i][j] = (T)a;
@@ -666,22 +667,25 @@ __device__ __forceinline__ void square_P(const double P[4][4], Prop2<T>& pr) {
 // STASH: the post-pulse phase is written to the stash as soon as it is built
 // (post-pulse first), so it never occupies registers next to the pulse phase
 // -- this lowers the kernel's register peak at the setup -> loop transition.
-template <typename T, bool STASH = false>
+// R: the coefficient arithmetic, fp64 for both paths (reading Q11).  fp32
+// coefficients (R = float) cut the fp32 fit by 11% but made its errors ~5x
+// larger (rejected).
+template <typename T, bool STASH = false, typename R = double>
 __device__ __forceinline__ void make_prop(const Setup& s, Prop2<T>& pr,
                                           typename Vec2<T>::type* st2 = nullptr, int ld = 0) {
   const Mech& m = s.m;
-  double P[4][4];
-  one_step_P(m, P);
-  double u[2][4][4];
-  coupling_u(m, u);
-  square_P<T>(P, pr);
+  R P[4][4];
+  one_step_P<R>(m, P);
+  R u[2][4][4];
+  coupling_u<R>(m, u);
+  square_P<T, R>(P, pr);
 #pragma unroll
   for (int phi = 0; phi < 2; ++phi) {
     const int ph = STASH ? 1 - phi : phi;
-    double X[4][2], c[4], pf[2], qf[2];
-    one_step_phase(s.ph[ph], u, X, c, pf, qf);
+    R X[4][2], c[4], pf[2], qf[2];
+    one_step_phase<R>(s.ph[ph], u, X, c, pf, qf);
     PhaseProp2<T>& q = pr.ph[ph];
-    two_step_phase<T>(P, X, c, pf, qf, q);
+    two_step_phase<T, R>(P, X, c, pf, qf, q);
     if (STASH && ph == 1) stash_phase<T>(q, st2, ld);
     if (ph == 0) {
 #pragma unroll
@@ -748,15 +752,16 @@ __device__ __forceinline__ void map_power(AffineMap& M, int n) {
 template <typename T>
 __device__ __forceinline__ void make_prop_sub(const Setup& s, int nsub, Prop2<T>& pr,
                                            typename Vec2<T>::type* st2, int ld) {
-  AffineMap M;
-  one_step_P(s.m, M.P);
+  AffineMap M;   // fp64 for both paths: the powering compounds rounding
+  one_step_P<double>(s.m, M.P);
   double u[2][4][4];
-  coupling_u(s.m, u);
-  for (int ph = 0; ph < 2; ++ph) one_step_phase(s.ph[ph], u, M.X[ph], M.c[ph], M.pf[ph], M.qf[ph]);
+  coupling_u<double>(s.m, u);
+  for (int ph = 0; ph < 2; ++ph)
+    one_step_phase<double>(s.ph[ph], u, M.X[ph], M.c[ph], M.pf[ph], M.qf[ph]);
   map_power(M, nsub);
-  square_P<T>(M.P, pr);
+  square_P<T, double>(M.P, pr);
   for (int ph = 1; ph >= 0; --ph) {
-    two_step_phase<T>(M.P, M.X[ph], M.c[ph], M.pf[ph], M.qf[ph], pr.ph[ph]);
+    two_step_phase<T, double>(M.P, M.X[ph], M.c[ph], M.pf[ph], M.qf[ph], pr.ph[ph]);
     if (ph == 1) stash_phase<T>(pr.ph[1], st2, ld);
   }
   for (int r = 0; r < 4; ++r) pr.z1[r] = (T)M.c[0][r];
@@ -1096,7 +1101,7 @@ __device__ __forceinline__ T run_rk4_stages(const Setup& s, int32_t n_steps,
 // ---------------------------------------------------------------------------
 // Evaluate one candidate: physical check, setup, integrate + fused score.
 // ---------------------------------------------------------------------------
-template <typename T, int INTEG, int METRIC, bool TRAJ>
+template <typename T, int INTEG, int METRIC, bool TRAJ, typename RS = double>
 __device__ __forceinline__ double evaluate(const double p[NP], const CtlDev& c, double Aprime,
                                            double pw_default, const T* rel, T* traj,
                                            int64_t ld_out, double sgn, uint8_t* status,
@@ -1144,7 +1149,7 @@ __device__ __forceinline__ double evaluate(const double p[NP], const CtlDev& c, 
     if (INTEG == 2) {   // sample map = one-substep map ^ substeps (own instantiation)
       make_prop_sub<T>(s, c.substeps, pr, st2, ld);
     } else {
-      make_prop<T, true>(s, pr, st2, ld);
+      make_prop<T, true, RS>(s, pr, st2, ld);
     }
     acc = run_propagator<T, METRIC, TRAJ, true>(pr, s.n_pulse, c.n_steps, rel, traj, ld_out,
                                                 (T)c.theta0, (T)sgn, stash, ld);

@@ -450,29 +450,6 @@ struct Prop2 {
   T z1[4], f1[2];      // state after one pulse step from zero (odd start)
 };
 
-__device__ __forceinline__ void zmul_vec(const Mech& m, const double v[4], double out[4]) {
-  out[0] = m.z01 * v[1];
-  out[1] = m.z10 * v[0] + m.z11 * v[1] + m.z12 * v[2] + m.z13 * v[3];
-  out[2] = m.z20 * v[0] + m.z22 * v[2];
-  out[3] = m.z30 * v[0] + m.z33 * v[3];
-}
-
-// T <- I + s * Z T   (Horner step for P(Z))
-__device__ __forceinline__ void horner_step(const Mech& m, double s, double Tm[4][4]) {
-  double R[4][4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    double col[4] = {Tm[0][j], Tm[1][j], Tm[2][j], Tm[3][j]}, o[4];
-    zmul_vec(m, col, o);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) R[i][j] = (i == j ? 1.0 : 0.0) + s * o[i];
-  }
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) Tm[i][j] = R[i][j];
-}
-
 // Structural zeros of u_i = Z^i (h c_m) (Z: row 0 = (0,h,0,0), row 2 couples
 // only theta and x_AG, row 3 only theta and x_ANT): NZU[m][i][r] is false where
 // u_i[r] is identically zero, so those terms are dropped at compile time.

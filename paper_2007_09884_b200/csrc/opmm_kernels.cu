@@ -285,13 +285,6 @@ __global__ void __launch_bounds__(OPMM_FIT_LB_THREADS, OPMM_FIT_LB_BLOCKS) fit_k
   double sgn, Aprime;
   stage_trace<T>(a.rec + sac * (int64_t)ns, ns, amp, rel, sgn, Aprime);
   __syncthreads();
-#ifdef OPMM_STAGGER
-  if ((threadIdx.x >> 5) & 1) {
-    const long long t0 = clock64();
-    while (clock64() - t0 < OPMM_STAGGER) {
-    }
-  }
-#endif
 
   double best_e = __longlong_as_double(0x7ff0000000000000LL);
   int64_t best_i = INT64_MAX;

@@ -655,7 +655,6 @@ __device__ __forceinline__ void make_prop(const Setup& s, Prop2<T>& pr,
   one_step_P<R>(m, P);
   R u[2][4][4];
   coupling_u<R>(m, u);
-  square_P<T, R>(P, pr);
 #pragma unroll
   for (int phi = 0; phi < 2; ++phi) {
     const int ph = STASH ? 1 - phi : phi;
@@ -671,6 +670,9 @@ __device__ __forceinline__ void make_prop(const Setup& s, Prop2<T>& pr,
       pr.f1[1] = (T)qf[1];
     }
   }
+  // P^2 last: it is live through the whole loop, so building it after the
+  // phases keeps it out of the setup's register peak
+  square_P<T, R>(P, pr);
 }
 
 // ----------------------------------------------------------------------------

@@ -17,20 +17,21 @@ namespace {
 struct Plant {
   double kse[2], klt[2], b[2], nc[2];
   double bp, J;
+  double inv_J, inv_b[2];   // the divisors, inverted once per call
 };
 
 // D1: T_m = K_SE_m (x_m - s_m theta); B_m x_m' = f_m - N_C_m s_m theta - K_LT_m x_m - T_m;
 // f_m' = (n_m - f_m)/tau_m; J omega' = T_AG - T_ANT - B_P omega; theta' = omega.
-void deriv(const Plant& P, const double y[6], const double n[2], const double tau_s[2],
+void deriv(const Plant& P, const double y[6], const double n[2], const double inv_tau_s[2],
            double dy[6]) {
   const double sgn[2] = {1.0, -1.0};
   double T[2];
   for (int m = 0; m < 2; ++m) T[m] = P.kse[m] * (y[2 + m] - sgn[m] * y[0]);
   dy[0] = y[1];
-  dy[1] = (T[0] - T[1] - P.bp * y[1]) / P.J;
+  dy[1] = (T[0] - T[1] - P.bp * y[1]) * P.inv_J;
   for (int m = 0; m < 2; ++m) {
-    dy[2 + m] = (y[4 + m] - P.nc[m] * sgn[m] * y[0] - P.klt[m] * y[2 + m] - T[m]) / P.b[m];
-    dy[4 + m] = (n[m] - y[4 + m]) / tau_s[m];
+    dy[2 + m] = (y[4 + m] - P.nc[m] * sgn[m] * y[0] - P.klt[m] * y[2 + m] - T[m]) * P.inv_b[m];
+    dy[4 + m] = (n[m] - y[4 + m]) * inv_tau_s[m];
   }
 }
 
@@ -44,6 +45,9 @@ double cpu_check_score(const double opc[OPMM_NPARAM], const double* rec, const o
   P.b[0] = opc[OPMM_P_B_AG];      P.b[1] = opc[OPMM_P_B_ANT];
   P.nc[0] = opc[OPMM_P_NC_AG];    P.nc[1] = opc[OPMM_P_NC_ANT];
   P.bp = opc[OPMM_P_B_P];         P.J = opc[OPMM_P_J];
+  P.inv_J = 1.0 / P.J;
+  P.inv_b[0] = 1.0 / P.b[0];
+  P.inv_b[1] = 1.0 / P.b[1];
   const double F = opc[OPMM_P_NC_FIX];
   const double pw = std::isnan(opc[OPMM_P_PW]) ? ctl->pw_default_ms : opc[OPMM_P_PW];
   const int n = ctl->n_steps;
@@ -74,17 +78,17 @@ double cpu_check_score(const double opc[OPMM_NPARAM], const double* rec, const o
     const bool pulse = (double)k < n_pulse;
     const double nn[2] = {pulse ? opc[OPMM_P_NSAC_AG] : step_n[0],
                           pulse ? opc[OPMM_P_NSAC_ANT] : step_n[1]};
-    const double tau[2] = {1e-3 * (pulse ? opc[OPMM_P_TAU_AC_AG] : opc[OPMM_P_TAU_DE_AG]),
-                           1e-3 * (pulse ? opc[OPMM_P_TAU_AC_ANT] : opc[OPMM_P_TAU_DE_ANT])};
+    const double inv_tau[2] = {1.0 / (1e-3 * (pulse ? opc[OPMM_P_TAU_AC_AG] : opc[OPMM_P_TAU_DE_AG])),
+                           1.0 / (1e-3 * (pulse ? opc[OPMM_P_TAU_AC_ANT] : opc[OPMM_P_TAU_DE_ANT]))};
     for (int sub = 0; sub < nsub; ++sub) {
       double k1[6], k2[6], k3[6], k4[6], t[6];
-      deriv(P, y, nn, tau, k1);
+      deriv(P, y, nn, inv_tau, k1);
       for (int i = 0; i < 6; ++i) t[i] = y[i] + 0.5 * h * k1[i];
-      deriv(P, t, nn, tau, k2);
+      deriv(P, t, nn, inv_tau, k2);
       for (int i = 0; i < 6; ++i) t[i] = y[i] + 0.5 * h * k2[i];
-      deriv(P, t, nn, tau, k3);
+      deriv(P, t, nn, inv_tau, k3);
       for (int i = 0; i < 6; ++i) t[i] = y[i] + h * k3[i];
-      deriv(P, t, nn, tau, k4);
+      deriv(P, t, nn, inv_tau, k4);
       for (int i = 0; i < 6; ++i) y[i] += h / 6.0 * (k1[i] + 2.0 * k2[i] + 2.0 * k3[i] + k4[i]);
     }
     const double d = (y[0] - th_star) - s * (rec[k + 1] - rec[0]);

@@ -116,6 +116,13 @@ struct opmm_handle {
   size_t sacctl_cap = 0;
   double* candctl = nullptr;   // opmm_simulate_batch: [n][3] per-candidate controls
   size_t candctl_cap = 0;
+  // opmm_fit's CUDA graph: [H2D of the staged trace, event, fit kernel,
+  // event, D2H of the result] captured once and replayed while the launch
+  // (kernel, configuration and every FitArgs byte) is unchanged
+  cudaGraphExec_t fit_graph = nullptr;
+  std::string fit_graph_key;
+  double* rec_stage = nullptr;   // pinned host staging of the recorded trace
+  size_t rec_stage_cap = 0;
   const void* occ_fn = nullptr;  // grid_for's last occupancy query
   int occ_block = 0;
   size_t occ_smem = 0;
@@ -399,10 +406,19 @@ opmm_status nccl_fail(ncclResult_t r, const char* what) {
 
 // Enqueue one fit (candidates sharded over the handle's ranks) for saccades
 // [s_begin, s_begin + S) of a batch, writing final results to out_dev[S].
+// A prepared single-saccade, single-rank fit launch (opmm_fit's graph path).
+struct FitLaunch {
+  const void* fn = nullptr;
+  int grid = 0, block = 0;
+  size_t smem = 0;
+  opmm::FitArgs a;
+};
+
 opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_control* ctl,
                         const double* sacctl_dev, int64_t s_begin, int64_t S,
                         const opmm_search_space* space, int64_t n_candidates,
-                        const opmm_fit_options* opts, opmm_fit_result* out_dev, bool shard) {
+                        const opmm_fit_options* opts, opmm_fit_result* out_dev, bool shard,
+                        FitLaunch* prepare_only = nullptr) {
   const int precision = opts ? opts->precision : OPMM_FP64;
   const int metric = opts ? opts->metric : OPMM_METRIC_L1;
   const int integ = opts ? opts->integrator : OPMM_INTEG_PROPAGATOR;
@@ -521,6 +537,15 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
   a.rank_out = multi ? h->rank_part : nullptr;
   a.final_out = multi ? nullptr : out_dev;
   a.out_base = s_begin;
+  if (prepare_only && !multi && S == 1) {   // the caller launches it (graph)
+    prepare_only->fn = fn;
+    prepare_only->grid = grid;
+    prepare_only->block = block;
+    prepare_only->smem = smem;
+    prepare_only->a = a;
+    return OPMM_OK;
+  }
+  if (prepare_only) prepare_only->fn = nullptr;   // not graph-eligible: launched here
   CKS(record_start(h, h->stream));
   for (int64_t s0 = 0; s0 < S; s0 += 65535) {
     const int64_t sn = (S - s0) < 65535 ? (S - s0) : 65535;
@@ -783,6 +808,8 @@ opmm_status opmm_destroy(opmm_handle* h) {
   cudaFree(h->nm_xbest);
   cudaFree(h->nm_out);
   if (h->result_host) cudaFreeHost(h->result_host);
+  if (h->fit_graph) cudaGraphExecDestroy(h->fit_graph);
+  if (h->rec_stage) cudaFreeHost(h->rec_stage);
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
   if (h->stream) cudaStreamDestroy(h->stream);
@@ -1010,10 +1037,72 @@ opmm_status opmm_fit(opmm_handle* h, const double* recorded, const opmm_control*
   if (!recorded || !out) return fail(OPMM_ERR_INVALID_ARG, "NULL recorded/out");
   const size_t ns = (size_t)ctl->n_steps + 1;
   const double* rec_dev = nullptr;
-  CKS(stage_rec(h, recorded, ns, &rec_dev));
-  CKS(enqueue_fit(h, rec_dev, ctl, nullptr, 0, 1, space, n_candidates, opts, h->result, true));
-  CK(cudaMemcpyAsync(h->result_host, h->result, sizeof(opmm_fit_result), cudaMemcpyDeviceToHost,
-                     h->stream));
+  const bool host_rec = !is_device_ptr(recorded);
+  // (host traces only: a device trace's pointer is part of the launch, and
+  // callers that keep traces on the device use opmm_fit_async anyway)
+  if (h->comm == nullptr && host_rec && !getenv("OPMM_NO_FIT_GRAPH")) {
+    // Graph path: the trace is copied into pinned staging on the host, and
+    // one graph launch does H2D + kernel + D2H (re-captured when the launch
+    // changes).  The previous call synchronised, so the staging is free.
+    {
+      for (size_t k = 0; k < ns; ++k)
+        if (!is_finite(recorded[k]))
+          return fail(OPMM_ERR_INVALID_ARG, "recorded sample %zu is not finite", k);
+      if (ns > h->rec_stage_cap) {
+        if (h->rec_stage) cudaFreeHost(h->rec_stage);
+        h->rec_stage = nullptr;
+        h->rec_stage_cap = 0;
+        CK(cudaMallocHost(reinterpret_cast<void**>(&h->rec_stage), ns * sizeof(double)));
+        h->rec_stage_cap = ns;
+      }
+      std::memcpy(h->rec_stage, recorded, ns * sizeof(double));
+      CKS(ensure(h->rec, h->rec_cap, ns));
+      rec_dev = h->rec;
+    }
+    FitLaunch L;
+    CKS(enqueue_fit(h, rec_dev, ctl, nullptr, 0, 1, space, n_candidates, opts, h->result, true, &L));
+    if (L.fn != nullptr) {
+      // the key: every launch byte plus the host buffers the copies use
+      // (they are reallocated when a larger request grows them)
+      std::string key(sizeof(L.a) + 128, '\0');
+      std::memcpy(&key[0], &L.a, sizeof(L.a));
+      std::snprintf(&key[sizeof(L.a)], 128, "%p/%d/%d/%zu/%zu/%p/%p", L.fn, L.grid, L.block, L.smem,
+                    ns, static_cast<void*>(h->rec_stage), static_cast<void*>(h->result_host));
+      if (h->fit_graph == nullptr || key != h->fit_graph_key) {
+        if (h->fit_graph) cudaGraphExecDestroy(h->fit_graph);
+        h->fit_graph = nullptr;
+        cudaGraph_t g = nullptr;
+        CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+        cudaError_t ce = cudaSuccess;
+        ce = cudaMemcpyAsync(h->rec, h->rec_stage, ns * sizeof(double), cudaMemcpyHostToDevice,
+                             h->stream);
+        // external event records: the timing events are real records at replay
+        if (ce == cudaSuccess) ce = cudaEventRecordWithFlags(h->ev0, h->stream, cudaEventRecordExternal);
+        if (ce == cudaSuccess) ce = opmm::launch_fit(L.fn, L.a, dim3(L.grid), L.block, L.smem, h->stream);
+        if (ce == cudaSuccess) ce = cudaEventRecordWithFlags(h->ev1, h->stream, cudaEventRecordExternal);
+        if (ce == cudaSuccess)
+          ce = cudaMemcpyAsync(h->result_host, h->result, sizeof(opmm_fit_result),
+                               cudaMemcpyDeviceToHost, h->stream);
+        const cudaError_t ee = cudaStreamEndCapture(h->stream, &g);
+        CK(ce);
+        CK(ee);
+        const cudaError_t ie = cudaGraphInstantiate(&h->fit_graph, g, 0);
+        cudaGraphDestroy(g);
+        CK(ie);
+        h->fit_graph_key = key;
+      }
+      CK(cudaGraphLaunch(h->fit_graph, h->stream));
+      h->timed = true;
+    } else {   // launched directly by enqueue_fit
+      CK(cudaMemcpyAsync(h->result_host, h->result, sizeof(opmm_fit_result),
+                         cudaMemcpyDeviceToHost, h->stream));
+    }
+  } else {
+    CKS(stage_rec(h, recorded, ns, &rec_dev));
+    CKS(enqueue_fit(h, rec_dev, ctl, nullptr, 0, 1, space, n_candidates, opts, h->result, true));
+    CK(cudaMemcpyAsync(h->result_host, h->result, sizeof(opmm_fit_result), cudaMemcpyDeviceToHost,
+                       h->stream));
+  }
   CK(cudaStreamSynchronize(h->stream));
   *out = *h->result_host;
   const bool want_check = !opts || opts->cpu_check;

@@ -800,3 +800,31 @@ def test_nm_substeps_reference_bit_identical(opmm, h):
     assert res[0]["iterations"] == int(o["iterations"][0])
     assert res[0]["f"] == float(o["f"][0])
     assert np.array_equal(np.array(res[0]["x"]), o["x"][0])
+
+
+def test_sync_fit_graph_replay_and_invalidation(opmm, h):
+    """opmm_fit replays a captured graph (H2D + kernel + D2H) while the launch
+    is unchanged and re-captures when it changes (trace length, N, precision,
+    a host buffer grown by a batch call): every call equals the direct path."""
+    import os
+    ctl = W.Control()
+    rec = trace(ctl)
+    sp = W.paper_space()
+    runs = [(rec, ctl, 3000, 0), (rec + 0.1, ctl, 3000, 0), (rec, ctl, 5000, 0), (rec, ctl, 3000, 1)]
+    longc = W.Control(n_steps=150)
+    runs.append((oracle.positions(W.truth_opc(), longc) + W.noise(151), longc, 3000, 0))
+    got = [opmm.opmm_fit(h, r, c, sp, n, opmm.fit_options(precision=p)) for r, c, n, p in runs]
+    # grow the pinned result buffer with a batch, then fit again
+    amp, pw, _ = W.population(4)
+    opmm.opmm_fit_batch(h, np.stack([rec] * 4), [W.Control(amplitude_deg=float(a)) for a in amp], sp, 500)
+    got.append(opmm.opmm_fit(h, rec, ctl, sp, 3000))
+    os.environ["OPMM_NO_FIT_GRAPH"] = "1"
+    try:
+        ref = [opmm.opmm_fit(h, r, c, sp, n, opmm.fit_options(precision=p)) for r, c, n, p in runs]
+        ref.append(opmm.opmm_fit(h, rec, ctl, sp, 3000))
+    finally:
+        del os.environ["OPMM_NO_FIT_GRAPH"]
+    for g, r in zip(got, ref):
+        assert (g["best_index"], g["opt_err"], g["n_finite"], g["cpu_check"]) == \
+               (r["best_index"], r["opt_err"], r["n_finite"], r["cpu_check"])
+    assert got[1]["opt_err"] != got[0]["opt_err"]   # the new trace reached the replayed graph

@@ -42,13 +42,13 @@ N_STEPS = 100
 PER_GPU = 10**6
 # Algorithmic FP64 work of the fit kernel per candidate:
 # the RK4 map in two-step propagator blocks is 32 FMA + 2 score adds per two
-# steps = 34 flop per step; generation + per-candidate setup = 1304 flop
+# steps = 34 flop per step; generation + per-candidate setup = 1285 flop
 # (ncu op counts dfma/dadd/dmul at n = 100 minus the loop's exact count,
 # profiles/r01_fit_kernel_fp64_opcounts.txt).
 FLOP_PER_STEP = 34
-FLOP_SETUP = 1304
+FLOP_SETUP = 1285
 FP64_INST_PER_STEP = 18    # fp64-pipe instructions per step (loop)
-FP64_INST_SETUP = 810      # fp64-pipe instructions per candidate outside the loop (ncu)
+FP64_INST_SETUP = 797      # fp64-pipe instructions per candidate outside the loop (ncu)
 SMS, FP64_LANES, SM_MAX_MHZ = 148, 64, 1965.0
 FP64_PEAK_TFLOPS = SMS * FP64_LANES * 2 * SM_MAX_MHZ * 1e6 / 1e12   # 37.23
 FP64_MEASURED_TFLOPS = 33.90   # profiles/r01_fma_peak.txt (DFMA microbenchmark)

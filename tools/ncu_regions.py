@@ -13,8 +13,10 @@ from collections import defaultdict
 REGIONS = {
     "generation": ("philox4x32_10", "exp_tab", "exp_poly", "exp_libm", "map_word", "generate_opc",
                    "generate_pw", "expand_9param"),
-    "setup": ("physical_penalty", "rcp64", "make_setup", "zmul_vec", "horner_step", "zmul_masked",
-              "make_prop", "stash_phase"),
+    "setup": ("physical_penalty", "rcp64", "make_setup", "zmul_masked", "make_prop", "stash_phase",
+              "one_step_P", "coupling_u", "one_step_phase", "two_step_phase", "square_P",
+              "make_prop_sub", "compose_maps", "map_power"),
+    "sort pre-pass": ("pulse_end_key",),
     "loop": ("run_propagator", "accumulate", "tabs", "finish_error"),
     "argmin/epilogue": ("better", "warp_argmin", "block_argmin", "fit_epilogue", "write_result",
                         "warp_topk", "cert_epilogue"),

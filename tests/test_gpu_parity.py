@@ -405,6 +405,11 @@ def test_fit_config2_full_1e6_fp64(opmm, h):
     print(f"1e6: n_finite {o['n_finite']}, max rel err diff {d.max():.3e}, "
           f"{int(np.sum(d > 1e-10))} above 1e-10, {refereed} refereed (rho > 1, GPU within 1e-9 of 80-bit)")
     assert r["best_index"] == o["best_index"] and r["n_finite"] == o["n_finite"]
+    # the bench's fp32 leg at the same size: certified, and its fp64-re-scored
+    # winner is the oracle's (north_star: best-fit error within 1e-4 of fp64)
+    c32 = opmm.opmm_fit(h, rec, ctl, sp, n, opmm.fit_options(precision=opmm.FP32, certify=1))
+    assert c32["certified"] == 1 and c32["best_index"] == o["best_index"]
+    assert abs(c32["opt_err"] - o["best_err"]) <= 1e-9 * o["best_err"]
 
 
 def test_fit_fp32_best_fit_certified_by_fp64_oracle(opmm, h):

@@ -243,8 +243,11 @@ __device__ void cert_epilogue(const FitArgs& a, int64_t sac, double e1, int64_t 
   if (lane == 0) {
     a.counters[sac] = 0;   // re-arm (graph-replay safe)
     write_result(a.space, (uint32_t)sac, e, i, nft, a.end - a.begin, out, a.exp_tab);
+    // error scale of the trace in the fit's metric: sum |rel| (L1), or the
+    // RMS of rel (RMS) -- the fp32 budget's floor
     double srel = 0.0;
-    for (int k = 0; k < ns; ++k) srel += fabs(rel64[k]);
+    for (int k = 0; k < ns; ++k) srel += METRIC == 0 ? fabs(rel64[k]) : rel64[k] * rel64[k];
+    if (METRIC != 0) srel = sqrt(srel / (double)ns);
     const double tstar = ge[0] + 2.0 * (1e-4 * fmax(ge[0], srel));
     out->top_k = CERT_K;
     out->certified = (nft < CERT_K || (m2 > tstar && ge[CERT_K - 1] > tstar)) ? 1 : 0;

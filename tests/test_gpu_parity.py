@@ -677,6 +677,12 @@ def test_fp32_certified_fit(opmm, h):
     assert rc["best_index"] == r64["best_index"] and rc["opt_err"] == r64["opt_err"]
     assert rc["certified"] == 1
     assert abs(rc["cpu_check"] - rc["opt_err"]) <= 1e-9 * rc["opt_err"]
+    # RMS metric: the budget's floor is the RMS of the trace; still certified
+    # and still the fp64 fit's winner
+    r64r, E64r = _fit(opmm, h, rec, ctl, sp, n, precision=opmm.FP64, metric=1)
+    rr = opmm.opmm_fit(h, rec, ctl, sp, n, opmm.fit_options(precision=opmm.FP32, certify=1, metric=1))
+    assert rr["certified"] == 1 and rr["best_index"] == r64r["best_index"]
+    assert rr["opt_err"] == r64r["opt_err"]
     # fewer finite candidates than K: trivially certified; unused slots -1
     small = opmm.opmm_fit(h, rec, ctl, sp, 3, opmm.fit_options(precision=opmm.FP32, certify=1))
     assert small["certified"] == 1 and small["topk_index"][3:] == [-1] * 5

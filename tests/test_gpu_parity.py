@@ -683,6 +683,12 @@ def test_fp32_certified_fit(opmm, h):
     rr = opmm.opmm_fit(h, rec, ctl, sp, n, opmm.fit_options(precision=opmm.FP32, certify=1, metric=1))
     assert rr["certified"] == 1 and rr["best_index"] == r64r["best_index"]
     assert rr["opt_err"] == r64r["opt_err"]
+    # several super-tile passes per block (3e6 > 148 blocks x 8192): same winner
+    big = 3 * 10**6
+    b64 = opmm.opmm_fit(h, rec, ctl, sp, big, opmm.fit_options(precision=opmm.FP64))
+    b32 = opmm.opmm_fit(h, rec, ctl, sp, big, opmm.fit_options(precision=opmm.FP32, certify=1))
+    assert b32["certified"] == 1 and (b32["best_index"], b32["opt_err"]) == (b64["best_index"], b64["opt_err"])
+    assert b32["n_finite"] == b64["n_finite"]
     # fewer finite candidates than K: trivially certified; unused slots -1
     small = opmm.opmm_fit(h, rec, ctl, sp, 3, opmm.fit_options(precision=opmm.FP32, certify=1))
     assert small["certified"] == 1 and small["topk_index"][3:] == [-1] * 5

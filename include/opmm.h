@@ -309,7 +309,9 @@ typedef struct {
  * the Table 1 defaults; a NaN PW starts at the saccade's
  * pw_default_ms.  out: HOST [S].  On an NCCL handle rank r estimates only
  * saccades [floor(rS/R), floor((r+1)S/R)) (independent problems, no
- * collective) and fills only those entries.  Synchronous. */
+ * collective) and fills only those entries.  Synchronous.  Each problem keeps
+ * its trace in shared memory: n_steps up to ~5000 samples (fp64 objectives;
+ * INVALID_ARG beyond), against OPMM_MAX_STEPS for the fit. */
 opmm_status opmm_estimate_batch(opmm_handle* h, const double* recorded, int64_t S,
                                 const opmm_control* ctl, const double* x0,
                                 const opmm_nm_options* opts, opmm_nm_result* out);

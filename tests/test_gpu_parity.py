@@ -549,7 +549,7 @@ def test_edge_all_diverged(opmm, h):
     assert r["best_index"] == -1 and r["n_finite"] == 0 and np.all(np.isinf(E))
 
 
-@pytest.mark.parametrize("n_steps", [1, 2, 37, 4000])
+@pytest.mark.parametrize("n_steps", [1, 2, 37, 4000, 16384])   # 16384 = OPMM_MAX_STEPS
 def test_edge_trace_lengths(opmm, h, n_steps):
     ctl = W.Control(n_steps=n_steps, dt_ms=1.0 if n_steps < 1000 else 0.05)
     rec = oracle.positions(W.truth_opc(), ctl) + W.noise(n_steps + 1)

@@ -310,8 +310,9 @@ typedef struct {
  * pw_default_ms.  out: HOST [S].  On an NCCL handle rank r estimates only
  * saccades [floor(rS/R), floor((r+1)S/R)) (independent problems, no
  * collective) and fills only those entries.  Synchronous.  Each problem keeps
- * its trace in shared memory: n_steps up to ~5000 samples (fp64 objectives;
- * INVALID_ARG beyond), against OPMM_MAX_STEPS for the fit. */
+ * its trace in shared memory, or, for traces too long for it (beyond ~5000
+ * samples in fp64), in a handle-owned global workspace; n_steps up to
+ * OPMM_MAX_STEPS. */
 opmm_status opmm_estimate_batch(opmm_handle* h, const double* recorded, int64_t S,
                                 const opmm_control* ctl, const double* x0,
                                 const opmm_nm_options* opts, opmm_nm_result* out);

@@ -114,6 +114,8 @@ struct opmm_handle {
   size_t rec_cap = 0;
   double* sacctl = nullptr;
   size_t sacctl_cap = 0;
+  double* nm_rel = nullptr;    // Nelder-Mead: relativized traces too long for shared memory
+  size_t nm_rel_cap = 0;
   double* candctl = nullptr;   // opmm_simulate_batch: [n][3] per-candidate controls
   size_t candctl_cap = 0;
   // opmm_fit's CUDA graph: [H2D of the staged trace, event, fit kernel,
@@ -617,10 +619,16 @@ opmm_status nm_launch(opmm_handle* h, const NmConfig& c, const double* rec_dev,
   const int32_t ns = ctl0 ? ctl0->n_steps + 1 : 1;
   // the propagator objective with substeps has its own instantiation (obj 4)
   const int obj = (c.obj == 0 && ctl0 && ctl0->substeps > 1) ? 4 : c.obj;
-  const size_t smem = opmm::nm_smem(c.precision, obj, ns);
+  size_t smem = opmm::nm_smem(c.precision, obj, ns);
+  const bool rel_global = smem > max_dyn_smem(opmm::nm_kernel_ptr(c.precision, obj, c.metric));
+  if (rel_global) {   // long traces: relativized per problem in global memory
+    smem = opmm::nm_smem(c.precision, obj, ns, false);
+    CKS(ensure(h->nm_rel, h->nm_rel_cap, (size_t)(pe - pb) * (size_t)ns));
+  }
   if (smem > kMaxDynSmem) return fail(OPMM_ERR_INVALID_ARG, "trace too long for the NM kernel");
   opmm::NmArgs a;
   std::memset(&a, 0, sizeof(a));
+  a.rel_global = rel_global ? static_cast<void*>(h->nm_rel) : nullptr;
   a.rec = rec_dev;
   a.sac_ctl = sacctl_dev;
   if (ctl0) a.ctl = make_ctl(ctl0);
@@ -799,6 +807,7 @@ opmm_status opmm_destroy(opmm_handle* h) {
   cudaFree(h->rec);
   cudaFree(h->sacctl);
   cudaFree(h->candctl);
+  cudaFree(h->nm_rel);
   cudaFree(h->rank_part);
   cudaFree(h->gathered);
   cudaFree(h->cert_parts);

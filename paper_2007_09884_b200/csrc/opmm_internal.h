@@ -131,10 +131,11 @@ struct NmArgs {
   int64_t prob_begin, prob_end;
   int32_t dim, fn_id, max_iter, pad_;
   double tol_x, tol_f, init_scale;
+  void* rel_global;         // long traces: device [S][n_steps+1] of the loop type; else null
 };
 
 const void* nm_kernel_ptr(int precision, int obj, int metric);
-size_t nm_smem(int precision, int obj, int32_t n_samples);
+size_t nm_smem(int precision, int obj, int32_t n_samples, bool rel_in_smem = true);
 int nm_problems_per_block();
 int nm_threads();
 cudaError_t launch_nm(const void* fn, const NmArgs& a, int grid, size_t smem, cudaStream_t st);

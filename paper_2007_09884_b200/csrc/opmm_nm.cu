@@ -193,11 +193,15 @@ __global__ void __launch_bounds__(NM_THREADS) nm_kernel(NmArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   NmWarpSmem* W = reinterpret_cast<NmWarpSmem*>(smem_raw) + warp;
-  T* rel = reinterpret_cast<T*>(smem_raw + NM_WARPS * sizeof(NmWarpSmem) +
-                                (size_t)warp * rel_bytes<T>(a.ctl.n_steps + 1));
-  T* stash = reinterpret_cast<T*>(smem_raw + NM_WARPS * sizeof(NmWarpSmem) +
-                                  NM_WARPS * rel_bytes<T>(a.ctl.n_steps + 1));
+  // the relativized trace: per warp in shared memory, or (traces too long
+  // for it) per problem in a global workspace read through L1
+  const bool rel_smem = a.rel_global == nullptr;
   const int64_t prob = (int64_t)blockIdx.x * NM_WARPS + warp + a.prob_begin;
+  T* rel = rel_smem ? reinterpret_cast<T*>(smem_raw + NM_WARPS * sizeof(NmWarpSmem) +
+                                           (size_t)warp * rel_bytes<T>(a.ctl.n_steps + 1))
+                    : reinterpret_cast<T*>(a.rel_global) + (prob - a.prob_begin) * (int64_t)(a.ctl.n_steps + 1);
+  T* stash = reinterpret_cast<T*>(smem_raw + NM_WARPS * sizeof(NmWarpSmem) +
+                                  (rel_smem ? NM_WARPS * rel_bytes<T>(a.ctl.n_steps + 1) : 0));
   if (prob >= a.prob_end) return;   // whole warp
   const int n = a.dim;
   const int32_t ns = a.ctl.n_steps + 1;
@@ -212,6 +216,7 @@ __global__ void __launch_bounds__(NM_THREADS) nm_kernel(NmArgs a) {
     Aprime = fabs(A);
     for (int k = lane; k < ns; k += 32) rel[k] = (T)(sgn * (rec[k] - r0));
   }
+  __syncwarp();   // every lane reads the whole trace
   // evaluate point x (n coordinates) on every lane; returns f with NaN -> +inf (D11)
   auto evaluate_point = [&](const double* x) -> double {
     double f;
@@ -386,9 +391,10 @@ const void* nm_kernel_ptr(int precision, int obj, int metric) {
   return metric == 0 ? nm_fn<float, 1, 0>() : nm_fn<float, 1, 1>();
 }
 
-size_t nm_smem(int precision, int obj, int32_t n_samples) {
-  const size_t relb = (obj == 2 || precision == 0) ? rel_bytes<double>(n_samples)
-                                                   : rel_bytes<float>(n_samples);
+size_t nm_smem(int precision, int obj, int32_t n_samples, bool rel_in_smem) {
+  const size_t relb = !rel_in_smem ? 0
+                      : (obj == 2 || precision == 0) ? rel_bytes<double>(n_samples)
+                                                     : rel_bytes<float>(n_samples);
   const size_t st = precision == 0 || obj >= 2 ? stash_bytes<double>(NM_THREADS)
                                                : stash_bytes<float>(NM_THREADS);
   return NM_WARPS * sizeof(NmWarpSmem) + NM_WARPS * (obj == 3 ? 0 : relb) + (obj < 2 || obj == 4 ? st : 0);

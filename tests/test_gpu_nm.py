@@ -101,3 +101,18 @@ def test_plant_fast_objective_roundtrip(opmm, h, precision):
         assert abs(r["cpu_check"] - r["f"]) <= tol * max(r["f"], 1.0)
         assert r["f"] <= oracle.objective(W.truth_opc(), rec, c)   # never worse than the start
         assert r["gpu_evals"] == 19 + (r["iterations"] - 1) * 22
+
+
+def test_long_trace_uses_global_trace_workspace(opmm, h):
+    """Traces too long for the per-warp shared-memory copy (here 6000 samples)
+    are relativized into a global workspace; the reference-order objective
+    stays bit-identical to the oracle's serial Nelder-Mead."""
+    ctl = W.Control(n_steps=6000, dt_ms=0.02, amplitude_deg=10.0)
+    rec = oracle.positions(W.truth_opc(), ctl) + W.noise(6001)
+    opts = opmm.nm_options(objective=opmm.NM_OBJ_REFERENCE, max_iter=15, cpu_check=0)
+    res = opmm.opmm_estimate_batch(h, rec[None, :], [ctl], options=opts)
+    o = oracle.estimate_batch(rec[None, :], [ctl], max_iter=15)
+    assert res[0]["x"].tolist() == o["x"][0].tolist() and res[0]["f"] == o["f"][0]
+    fast = opmm.opmm_estimate_batch(h, rec[None, :], [ctl],
+                                    options=opmm.nm_options(max_iter=15, cpu_check=1))
+    assert abs(fast[0]["cpu_check"] - fast[0]["f"]) <= 1e-9 * fast[0]["f"]

@@ -650,7 +650,7 @@ opmm_status nm_launch(opmm_handle* h, const NmConfig& c, const double* rec_dev,
   if (grid == 0) return OPMM_OK;
   if (grid > 0x7fffffff) return fail(OPMM_ERR_INVALID_ARG, "too many problems");
   CKS(record_start(h, h->stream));
-  CK(opmm::launch_nm(opmm::nm_kernel_ptr(c.precision, obj, c.metric), a, (int)grid, smem,
+  CK(opmm::launch_nm(opmm::nm_kernel_ptr(c.precision, obj, c.metric, rel_global), a, (int)grid, smem,
                      h->stream));
   CKS(record_stop(h, h->stream));
   return OPMM_OK;
@@ -730,7 +730,8 @@ opmm_status opmm_create(opmm_handle** out, int device) {
         allow_dyn_smem(opmm::fit3_kernel_ptr(p, m));
         allow_dyn_smem(opmm::simulate_kernel_ptr(p, i));
         allow_dyn_smem(opmm::score_kernel_ptr(p, m));
-        for (int obj = 0; obj < 5; ++obj) allow_dyn_smem(opmm::nm_kernel_ptr(p, obj, m));
+        for (int obj = 0; obj < 5; ++obj)
+          for (int g = 0; g < 2; ++g) allow_dyn_smem(opmm::nm_kernel_ptr(p, obj, m, g == 1));
       }
   cudaGetLastError();
   {

@@ -134,7 +134,7 @@ struct NmArgs {
   void* rel_global;         // long traces: device [S][n_steps+1] of the loop type; else null
 };
 
-const void* nm_kernel_ptr(int precision, int obj, int metric);
+const void* nm_kernel_ptr(int precision, int obj, int metric, bool rel_global = false);
 size_t nm_smem(int precision, int obj, int32_t n_samples, bool rel_in_smem = true);
 int nm_problems_per_block();
 int nm_threads();

@@ -188,20 +188,20 @@ struct NmWarpSmem {
   double xbar[NM_NMAX];
 };
 
-template <typename T, int OBJ, int METRIC>
-__global__ void __launch_bounds__(NM_THREADS) nm_kernel(NmArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+// GREL: the relativized trace lives per problem in a global workspace (traces
+// too long for shared memory); otherwise per warp in shared memory.  A
+// compile-time choice, so the common path's trace loads stay shared-memory
+// loads.
+template <typename T, int OBJ, int METRIC, bool GREL>
+__device__ __forceinline__ void nm_run(const NmArgs& a, unsigned char* smem_raw) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   NmWarpSmem* W = reinterpret_cast<NmWarpSmem*>(smem_raw) + warp;
-  // the relativized trace: per warp in shared memory, or (traces too long
-  // for it) per problem in a global workspace read through L1
-  const bool rel_smem = a.rel_global == nullptr;
   const int64_t prob = (int64_t)blockIdx.x * NM_WARPS + warp + a.prob_begin;
-  T* rel = rel_smem ? reinterpret_cast<T*>(smem_raw + NM_WARPS * sizeof(NmWarpSmem) +
-                                           (size_t)warp * rel_bytes<T>(a.ctl.n_steps + 1))
-                    : reinterpret_cast<T*>(a.rel_global) + (prob - a.prob_begin) * (int64_t)(a.ctl.n_steps + 1);
+  T* rel = GREL ? reinterpret_cast<T*>(a.rel_global) + (prob - a.prob_begin) * (int64_t)(a.ctl.n_steps + 1)
+                : reinterpret_cast<T*>(smem_raw + NM_WARPS * sizeof(NmWarpSmem) +
+                                       (size_t)warp * rel_bytes<T>(a.ctl.n_steps + 1));
   T* stash = reinterpret_cast<T*>(smem_raw + NM_WARPS * sizeof(NmWarpSmem) +
-                                  (rel_smem ? NM_WARPS * rel_bytes<T>(a.ctl.n_steps + 1) : 0));
+                                  (GREL ? 0 : NM_WARPS * rel_bytes<T>(a.ctl.n_steps + 1)));
   if (prob >= a.prob_end) return;   // whole warp
   const int n = a.dim;
   const int32_t ns = a.ctl.n_steps + 1;
@@ -373,22 +373,36 @@ __global__ void __launch_bounds__(NM_THREADS) nm_kernel(NmArgs a) {
   }
 }
 
-template <typename T, int OBJ, int METRIC>
-static const void* nm_fn() { return reinterpret_cast<const void*>(&nm_kernel<T, OBJ, METRIC>); }
+// GREL selects its own instantiation (nm_kernel_ptr), so each kernel holds
+// one trace path.
+template <typename T, int OBJ, int METRIC, bool GREL>
+__global__ void __launch_bounds__(NM_THREADS) nm_kernel(NmArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  nm_run<T, OBJ, METRIC, GREL>(a, smem_raw);
+}
 
-const void* nm_kernel_ptr(int precision, int obj, int metric) {
-  if (obj == 3) return nm_fn<double, 3, 0>();
+template <typename T, int OBJ, int METRIC, bool GREL = false>
+static const void* nm_fn() { return reinterpret_cast<const void*>(&nm_kernel<T, OBJ, METRIC, GREL>); }
+
+template <bool G>
+static const void* nm_ptr(int precision, int obj, int metric) {
+  if (obj == 3) return nm_fn<double, 3, 0, false>();
+  if (obj == 2) return metric == 0 ? nm_fn<double, 2, 0, G>() : nm_fn<double, 2, 1, G>();
   if (obj == 4) {
-    if (precision == 0) return metric == 0 ? nm_fn<double, 4, 0>() : nm_fn<double, 4, 1>();
-    return metric == 0 ? nm_fn<float, 4, 0>() : nm_fn<float, 4, 1>();
+    if (precision == 0) return metric == 0 ? nm_fn<double, 4, 0, G>() : nm_fn<double, 4, 1, G>();
+    return metric == 0 ? nm_fn<float, 4, 0, G>() : nm_fn<float, 4, 1, G>();
   }
-  if (obj == 2) return metric == 0 ? nm_fn<double, 2, 0>() : nm_fn<double, 2, 1>();
   if (precision == 0) {
-    if (obj == 0) return metric == 0 ? nm_fn<double, 0, 0>() : nm_fn<double, 0, 1>();
-    return metric == 0 ? nm_fn<double, 1, 0>() : nm_fn<double, 1, 1>();
+    if (obj == 0) return metric == 0 ? nm_fn<double, 0, 0, G>() : nm_fn<double, 0, 1, G>();
+    return metric == 0 ? nm_fn<double, 1, 0, G>() : nm_fn<double, 1, 1, G>();
   }
-  if (obj == 0) return metric == 0 ? nm_fn<float, 0, 0>() : nm_fn<float, 0, 1>();
-  return metric == 0 ? nm_fn<float, 1, 0>() : nm_fn<float, 1, 1>();
+  if (obj == 0) return metric == 0 ? nm_fn<float, 0, 0, G>() : nm_fn<float, 0, 1, G>();
+  return metric == 0 ? nm_fn<float, 1, 0, G>() : nm_fn<float, 1, 1, G>();
+}
+
+// rel_global: the instantiation that reads the trace from the global workspace
+const void* nm_kernel_ptr(int precision, int obj, int metric, bool rel_global) {
+  return rel_global ? nm_ptr<true>(precision, obj, metric) : nm_ptr<false>(precision, obj, metric);
 }
 
 size_t nm_smem(int precision, int obj, int32_t n_samples, bool rel_in_smem) {

@@ -207,11 +207,12 @@ def population_traces(h, opmm, torch, S, n_steps):
     return ctls, recs
 
 
-def population_leg(h, opmm, torch, args):
-    """Config 5 (BASELINE.json configs[4]) on one GPU: S synthetic saccades x
-    n_per candidates each through opmm_fit_batch (S_paper over n_steps = 150,
-    Philox counter word 2 = saccade).  Device time of the fit kernel (CUDA
-    events), 1 warm-up + 2 timed launches."""
+def population_leg(h, opmm, torch, args, max_over_ranks=lambda x: x, world=1):
+    """Config 5 (BASELINE.json configs[4]): S synthetic saccades x n_per
+    candidates each through opmm_fit_batch (S_paper over n_steps = 150,
+    Philox counter word 2 = saccade), saccades sharded over the N GPUs.
+    Device time of the fit kernel (CUDA events, max over ranks), 1 warm-up + 2
+    timed launches."""
     S, n_per, n_steps = args.pop_saccades, args.pop_candidates, 150
     ctls, recs = population_traces(h, opmm, torch, S, n_steps)
     sp = W.paper_space(n_steps=n_steps)
@@ -221,10 +222,12 @@ def population_leg(h, opmm, torch, args):
         res = opmm.opmm_fit_batch(h, recs, ctls, sp, n_per, opts)
         if rep > 0:
             ms.append(opmm.opmm_last_kernel_ms(h))
-    kern = sum(ms) / len(ms)
-    f = np.array([r["opt_err"] for r in res])
+    # N > 1: saccades are sharded over the ranks (opmm_fit_batch, no
+    # collective); the time is the max over ranks, the residual this rank's
+    kern = max_over_ranks(sum(ms) / len(ms))
+    f = np.array([r["opt_err"] for r in res if r is not None])
     return {"metric": "OPC candidate sims/s (population)", "value": S * n_per / (kern * 1e-3),
-            "saccades": S, "candidates_per_saccade": n_per, "n_steps": n_steps,
+            "saccades": S, "candidates_per_saccade": n_per, "n_steps": n_steps, "n_gpus": world,
             "kernel_ms": kern, "saccades_per_s": S / (kern * 1e-3),
             "mean_best_residual_deg_per_sample": float(np.mean(f / (n_steps + 1)))}
 
@@ -387,7 +390,7 @@ def run_gpu(args):
 
     lat = latency_leg(h, opmm, torch, rec, world, max_over_ranks) if not args.no_latency else None
     nm = nm_leg(h, opmm, torch, args, max_over_ranks, sum_over_ranks) if not args.no_nm else None
-    pop = population_leg(h, opmm, torch, args) if (not args.no_pop and world == 1) else None
+    pop = population_leg(h, opmm, torch, args, max_over_ranks, world) if not args.no_pop else None
 
     per_cand_flop = FLOP_PER_STEP * N_STEPS + FLOP_SETUP
     achieved = per_cand_flop * args.per_gpu / (kms64 * 1e-3) / 1e12

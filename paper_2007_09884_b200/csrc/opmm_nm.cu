@@ -203,7 +203,7 @@ __device__ __forceinline__ void nm_run(const NmArgs& a, unsigned char* smem_raw)
   T* stash = reinterpret_cast<T*>(smem_raw + NM_WARPS * sizeof(NmWarpSmem) +
                                   (GREL ? 0 : NM_WARPS * rel_bytes<T>(a.ctl.n_steps + 1)));
   if (prob >= a.prob_end) return;   // whole warp
-  const int n = a.dim;
+  const int n = OBJ == 3 ? a.dim : NP;   // plant objectives: always the 18-vector
   const int32_t ns = a.ctl.n_steps + 1;
   double sgn = 1.0, Aprime = 0.0, pwd = 0.0;
   if (OBJ != 3) {
@@ -295,16 +295,23 @@ __device__ __forceinline__ void nm_run(const NmArgs& a, unsigned char* smem_raw)
     // 2 outside contraction, 3 inside contraction, 4.. shrink of vertex lane-3
     {
       const int L = lane < n + 4 ? lane : 0;
+      // Branch-free per coordinate: the four non-shrink points are
+      // fl(fl(ca xbar) + fl(cb v_n)) with per-lane (ca, cb) -- bit-identical
+      // to the serial forms, since fl(x - y) = fl(x + (-y)) and negation is
+      // exact -- and the shrink points fl(v_0 + fl(sigma fl(v_k - v_0))).
+      double ca, cb;
+      if (L == 0) { ca = Ar(1.0, rho); cb = -rho; }
+      else if (L == 1) { const double rc = Mr(rho, chi); ca = Ar(1.0, rc); cb = -rc; }
+      else if (L == 2) { const double pr = Mr(psi, rho); ca = Ar(1.0, pr); cb = -pr; }
+      else { ca = Sr(1.0, psi); cb = psi; }   // L == 3 (unused by shrink lanes)
+      const bool shrink = L >= 4;
+      const int vk = shrink ? L - 3 : 0;
       double x[NM_NMAX];
       for (int j = 0; j < n; ++j) {
-        const double xb = W->xbar[j], vn = V[n][j];
-        double v;
-        if (L == 0) v = Sr(Mr(Ar(1.0, rho), xb), Mr(rho, vn));
-        else if (L == 1) v = Sr(Mr(Ar(1.0, Mr(rho, chi)), xb), Mr(Mr(rho, chi), vn));
-        else if (L == 2) v = Sr(Mr(Ar(1.0, Mr(psi, rho)), xb), Mr(Mr(psi, rho), vn));
-        else if (L == 3) v = Ar(Mr(Sr(1.0, psi), xb), Mr(psi, vn));
-        else v = Ar(V[0][j], Mr(sigma, Sr(V[L - 3][j], V[0][j])));
-        x[j] = v;
+        const double xb = W->xbar[j], vn = V[n][j], v0 = V[0][j], vkj = V[vk][j];
+        const double vt = Ar(Mr(ca, xb), Mr(cb, vn));
+        const double vs = Ar(v0, Mr(sigma, Sr(vkj, v0)));
+        x[j] = shrink ? vs : vt;
       }
       const double f = evaluate_point(x);
       if (lane < n + 4) {

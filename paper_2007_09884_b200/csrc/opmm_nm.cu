@@ -181,8 +181,9 @@ constexpr int NM_WARPS = 4;               // problems per block
 constexpr int NM_THREADS = 32 * NM_WARPS;
 
 struct NmWarpSmem {
-  double V[2][NM_NMAX + 1][NM_NMAX];      // double-buffered simplex (sorted)
-  double fv[2][NM_NMAX + 1];
+  double S[NM_NMAX + 1][NM_NMAX];         // simplex vertices, in fixed slots
+  double fs[NM_NMAX + 1];                 // objective per slot
+  int ord[2][NM_NMAX + 1];                // slots in sorted order (double-buffered)
   double P[NM_PTS][NM_NMAX];              // xr, xe, xc, xcc, shrink points
   double fp[NM_PTS];
   double xbar[NM_NMAX];
@@ -257,40 +258,44 @@ __device__ __forceinline__ void nm_run(const NmArgs& a, unsigned char* smem_raw)
     }
   }
   __syncwarp();
-  // stable rank sort of the n+1 points P/fp into V[cur]/fv[cur]
-  auto sort_into = [&](int dst, const double (*src)[NM_NMAX], const double* fsrc) {
-    if (lane <= n) {
-      const double f = fsrc[lane];
-      int rank = 0;
-      for (int k = 0; k <= n; ++k) {
-        const double g = fsrc[k];
-        rank += (g < f || (g == f && k < lane)) ? 1 : 0;
-      }
-      for (int j = 0; j < n; ++j) W->V[dst][rank][j] = src[lane][j];
-      W->fv[dst][rank] = f;
+  // The sorted simplex is a permutation ord of fixed vertex slots: replacing
+  // the worst vertex writes one slot and re-ranks, instead of copying the
+  // whole simplex every iteration.  Order, ties and arithmetic are the serial
+  // algorithm's (stable rank by position, D14).
+  if (lane <= n) {
+    for (int j = 0; j < n; ++j) W->S[lane][j] = W->P[lane][j];
+    W->fs[lane] = W->fp[lane];
+    const double f = W->fp[lane];
+    int rank = 0;
+    for (int k = 0; k <= n; ++k) {
+      const double g = W->fp[k];
+      rank += (g < f || (g == f && k < lane)) ? 1 : 0;
     }
-    __syncwarp();
-  };
-  sort_into(cur, W->P, W->fp);
+    W->ord[cur][rank] = lane;
+  }
+  __syncwarp();
   int32_t it = 1, evals = n + 1, gpu_evals = n + 1, reason = 1;
   const double rho = 1.0, chi = 2.0, psi = 0.5, sigma = 0.5;
   while (it < a.max_iter) {
-    double (*V)[NM_NMAX] = W->V[cur];
-    double* fv = W->fv[cur];
+    const int* ord = W->ord[cur];
+    const int s0 = ord[0];
     // dual tolerance exit
     bool ok = true;
-    if (lane >= 1 && lane <= n) ok = fabs(fv[lane] - fv[0]) <= a.tol_f;
+    if (lane >= 1 && lane <= n) ok = fabs(W->fs[ord[lane]] - W->fs[s0]) <= a.tol_f;
     if (lane < n) {
-      for (int i = 1; i <= n; ++i) ok = ok && fabs(V[i][lane] - V[0][lane]) <= a.tol_x;
+      const double v0 = W->S[s0][lane];
+      for (int i = 1; i <= n; ++i) ok = ok && fabs(W->S[ord[i]][lane] - v0) <= a.tol_x;
     }
     if (__all_sync(0xffffffffu, ok)) { reason = 0; break; }
     // centroid of the n best vertices (summed in vertex order, then / n)
     if (lane < n) {
       double sum = 0.0;
-      for (int i = 0; i < n; ++i) sum = Ar(sum, V[i][lane]);
+      for (int i = 0; i < n; ++i) sum = Ar(sum, W->S[ord[i]][lane]);
       W->xbar[lane] = Dr(sum, (double)n);
     }
     __syncwarp();
+    const int sn = ord[n];
+    const double f0 = W->fs[s0], fn1 = W->fs[ord[n - 1]], fnn = W->fs[sn];
     // all transformation points at once: lane 0 xr, 1 xe,
     // 2 outside contraction, 3 inside contraction, 4.. shrink of vertex lane-3
     {
@@ -305,10 +310,10 @@ __device__ __forceinline__ void nm_run(const NmArgs& a, unsigned char* smem_raw)
       else if (L == 2) { const double pr = Mr(psi, rho); ca = Ar(1.0, pr); cb = -pr; }
       else { ca = Sr(1.0, psi); cb = psi; }   // L == 3 (unused by shrink lanes)
       const bool shrink = L >= 4;
-      const int vk = shrink ? L - 3 : 0;
+      const int sk = ord[shrink ? L - 3 : 0];
       double x[NM_NMAX];
       for (int j = 0; j < n; ++j) {
-        const double xb = W->xbar[j], vn = V[n][j], v0 = V[0][j], vkj = V[vk][j];
+        const double xb = W->xbar[j], vn = W->S[sn][j], v0 = W->S[s0][j], vkj = W->S[sk][j];
         const double vt = Ar(Mr(ca, xb), Mr(cb, vn));
         const double vs = Ar(v0, Mr(sigma, Sr(vkj, v0)));
         x[j] = shrink ? vs : vt;
@@ -324,54 +329,61 @@ __device__ __forceinline__ void nm_run(const NmArgs& a, unsigned char* smem_raw)
     // Lagarias decision step (identical on every lane)
     const double fr = W->fp[0];
     int take = -1;   // point replacing vertex n; -2 = shrink
-    if (fr < fv[0]) {
+    if (fr < f0) {
       take = W->fp[1] < fr ? 1 : 0;
       evals += 2;
-    } else if (fr < fv[n - 1]) {
+    } else if (fr < fn1) {
       take = 0;
       evals += 1;
-    } else if (fr < fv[n]) {
+    } else if (fr < fnn) {
       take = W->fp[2] <= fr ? 2 : -2;
       evals += 2;
     } else {
-      take = W->fp[3] < fv[n] ? 3 : -2;
+      take = W->fp[3] < fnn ? 3 : -2;
       evals += 2;
     }
     const int nxt = cur ^ 1;
     if (take >= 0) {
-      // simplex with vertex n replaced, then stable sort into the other buffer
+      // vertex n (slot sn) replaced by the accepted point, then stable re-rank
+      const double fnew = W->fp[take];
       if (lane <= n) {
-        const double f = lane == n ? W->fp[take] : fv[lane];
+        const double f = lane == n ? fnew : W->fs[ord[lane]];
         int rank = 0;
         for (int k = 0; k <= n; ++k) {
-          const double g = k == n ? W->fp[take] : fv[k];
+          const double g = k == n ? fnew : W->fs[ord[k]];
           rank += (g < f || (g == f && k < lane)) ? 1 : 0;
         }
-        for (int j = 0; j < n; ++j) W->V[nxt][rank][j] = lane == n ? W->P[take][j] : V[lane][j];
-        W->fv[nxt][rank] = f;
+        W->ord[nxt][rank] = lane == n ? sn : ord[lane];
       }
+      __syncwarp();
+      if (lane < n) W->S[sn][lane] = W->P[take][lane];
+      if (lane == 0) W->fs[sn] = fnew;
     } else {
       // shrink: vertices 1..n become the precomputed shrink points
       evals += n;
       if (lane <= n) {
-        const double f = lane == 0 ? fv[0] : W->fp[lane + 3];
+        const double f = lane == 0 ? f0 : W->fp[lane + 3];
         int rank = 0;
         for (int k = 0; k <= n; ++k) {
-          const double g = k == 0 ? fv[0] : W->fp[k + 3];
+          const double g = k == 0 ? f0 : W->fp[k + 3];
           rank += (g < f || (g == f && k < lane)) ? 1 : 0;
         }
-        for (int j = 0; j < n; ++j) W->V[nxt][rank][j] = lane == 0 ? V[0][j] : W->P[lane + 3][j];
-        W->fv[nxt][rank] = f;
+        W->ord[nxt][rank] = ord[lane];
       }
+      __syncwarp();
+      if (lane < n)
+        for (int i = 1; i <= n; ++i) W->S[ord[i]][lane] = W->P[i + 3][lane];
+      if (lane >= 1 && lane <= n) W->fs[ord[lane]] = W->fp[lane + 3];
     }
     __syncwarp();
     cur = nxt;
     ++it;
   }
-  if (lane < n) a.x_best[prob * (int64_t)a.x_ld + lane] = W->V[cur][0][lane];
+  const int sb = W->ord[cur][0];
+  if (lane < n) a.x_best[prob * (int64_t)a.x_ld + lane] = W->S[sb][lane];
   if (lane == 0) {
     NmOut o;
-    o.f_best = W->fv[cur][0];
+    o.f_best = W->fs[sb];
     o.iterations = it;
     o.func_evals = evals;
     o.gpu_evals = gpu_evals;

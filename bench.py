@@ -256,6 +256,29 @@ def latency_leg(h, opmm, torch, rec, world, max_over_ranks):
             "n_gpus": world, "candidates": out}
 
 
+def score_leg(h, opmm, torch, max_over_ranks, n=4 * 10**6, n_samples=101):
+    """opmm_score, the one HBM-bound entry point: stored fp64
+    trajectories [n_samples][n] (time-major) against one trace; GB/s of bytes
+    moved (trajectories + errors) against the measured HBM copy bandwidth."""
+    peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+    traj = torch.randn((n_samples, n), dtype=torch.float64, device="cuda")
+    rec = torch.randn(n_samples, dtype=torch.float64, device="cuda")
+    err = torch.empty(n, dtype=torch.float64, device="cuda")
+    st = torch.cuda.current_stream()
+    for _ in range(3):
+        opmm.opmm_score(h, traj, n, n_samples, rec, err, stream=st)
+    ms = []
+    for _ in range(10):
+        opmm.opmm_score(h, traj, n, n_samples, rec, err, stream=st)
+        ms.append(opmm.opmm_last_kernel_ms(h))
+    t = max_over_ranks(statistics.median(ms))
+    gbs = (traj.numel() * 8 + n * 8) / (t * 1e-3) / 1e9
+    del traj
+    return {"kernel": "score_kernel<double, L1>", "candidates": n, "n_samples": n_samples,
+            "kernel_ms": t, "achieved_gbs": gbs, "peak_gbs": peak, "frac": gbs / peak,
+            "peak_basis": "MEASURED_PEAKS.json hbm_gbs (copy, read+write)"}
+
+
 def nm_leg(h, opmm, torch, args, max_over_ranks=lambda x: x, sum_over_ranks=lambda x: x):
     """The paper's own estimator (batched parallel Nelder-Mead)
     on a synthetic population (SURVEY 8(d) config 5 recipe: A ~ U[5, 30] deg,
@@ -389,6 +412,7 @@ def run_gpu(args):
     e2e_ms = max_over_ranks(1e3 * sum(t_e2e) / len(t_e2e))
 
     lat = latency_leg(h, opmm, torch, rec, world, max_over_ranks) if not args.no_latency else None
+    score = score_leg(h, opmm, torch, max_over_ranks)
     nm = nm_leg(h, opmm, torch, args, max_over_ranks, sum_over_ranks) if not args.no_nm else None
     pop = population_leg(h, opmm, torch, args, max_over_ranks, world) if not args.no_pop else None
 
@@ -430,6 +454,7 @@ def run_gpu(args):
         line["nm"] = nm
     if lat is not None:
         line["latency"] = lat
+    line["score_hbm"] = score
     if pop is not None:
         line["population"] = pop
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

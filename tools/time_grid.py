@@ -1,0 +1,30 @@
+"""Fit kernel time on the G4 planted grid (10^8, grid-mode generation) vs the
+random S_paper space at the same N (GPU box).   python tools/time_grid.py"""
+import ctypes
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import oracle  # noqa: E402  (the trace only)
+import workloads as W  # noqa: E402
+from paper_2007_09884_b200 import opmm  # noqa: E402
+
+ctl = W.Control()
+rec = torch.as_tensor(oracle.positions(W.truth_opc(), ctl), device="cuda")
+with opmm.opmm_create(0) as h:
+    out = torch.zeros(ctypes.sizeof(opmm.FitResult), dtype=torch.uint8, device="cuda")
+    for name, sp, n in (("G4 grid", W.g4_space(100), 10**8), ("S_paper random", W.paper_space(), 10**8)):
+        o = opmm.fit_options(cpu_check=0)
+        for _ in range(2):
+            opmm.opmm_fit_async(h, rec, ctl, sp, n, out, o)
+        ms = []
+        for _ in range(3):
+            opmm.opmm_fit_async(h, rec, ctl, sp, n, out, o)
+            ms.append(opmm.opmm_last_kernel_ms(h))
+        torch.cuda.ExternalStream(h.stream).synchronize()
+        r = opmm.decode_result(bytes(out.cpu().numpy()))
+        print(f"{name:15s} N={n:.0e}: {np.median(ms):7.2f} ms  best {r['best_index']}", flush=True)

@@ -286,8 +286,7 @@ opmm::SpaceDev make_space(const opmm_search_space* s) {
     d.gsel[k] = d.kind[k] == 2 ? 1.0 : 0.0;
     d.lsel[k] = d.kind[k] == 1 ? 1.0 : 0.0;
   }
-  // (grid mode maps digit * span, so span32 / exact_u do not apply to it)
-  d.fast_gen = ((s->mode == 1 || !d.exact_u) && kinds012) ? 1 : 0;
+  d.fast_gen = (s->mode == 0 && !d.exact_u && kinds012) ? 1 : 0;
   d.pw_stride = 1;
   if (s->mode == 1)
     for (int k = 0; k < OPMM_P_PW; ++k) d.pw_stride *= s->levels[k];

@@ -44,7 +44,7 @@ struct SpaceDev {
   double span[NP];
   double span32[NP];     // random: span * 2^-32 (exact; see map_word)
   int32_t exact_u;       // random: some span32 would be subnormal -> literal u * span
-  int32_t fast_gen;      // kinds 0/1/2 only (random: and !exact_u): branch-free generate_opc
+  int32_t fast_gen;      // random, kinds 0/1/2 only, !exact_u: branch-free generate_opc
   double gsel[NP];       // fast_gen: 1 for table-exp (kind 2) dimensions, else 0
   double lsel[NP];       // fast_gen: 1 for linear (kind 1) dimensions, else 0
   int64_t levels[NP];    // grid radices (1 = not a grid dimension)
@@ -205,33 +205,6 @@ __device__ __forceinline__ void generate_opc(const SpaceDev& sp, uint32_t saccad
       for (int d = 0; d < NP; ++d) p[d] = map_word(sp, d, ws[d], tab);
     }
     if (sp.model == 1) expand_9param(p);
-  } else if (sp.fast_gen) {
-    // grid, kinds 0/1/2: mixed-radix digits (dimension 0 fastest), then the
-    // same branch-free map with x = digit * span (bit-identical to the
-    // general path below)
-    uint64_t rem = (uint64_t)idx;
-#pragma unroll
-    for (int d = 0; d < NP; ++d) {
-      double dig = 0.0;
-      const uint64_t L = (uint64_t)sp.levels[d];
-      if (L > 1) {
-        uint64_t digit;
-        if ((rem >> 32) == 0 && (L >> 32) == 0) {   // 32-bit divide when it fits
-          const uint32_t r32 = (uint32_t)rem, l32 = (uint32_t)L;
-          const uint32_t q32 = r32 / l32;
-          digit = r32 - q32 * l32;
-          rem = q32;
-        } else {
-          digit = rem % L;
-          rem = rem / L;
-        }
-        dig = (double)digit;
-      }
-      const double x = __dmul_rn(dig, sp.span[d]);
-      const double E = exp_tab(__dmul_rn(x, sp.gsel[d]), tab);
-      p[d] = __fma_rn(x, sp.lsel[d], __dmul_rn(sp.lo[d], E));
-    }
-    if (sp.model == 1) expand_9param(p);
   } else {
     uint64_t rem = (uint64_t)idx;
 #pragma unroll 1
@@ -239,15 +212,8 @@ __device__ __forceinline__ void generate_opc(const SpaceDev& sp, uint32_t saccad
       uint64_t digit = 0;
       const uint64_t L = (uint64_t)sp.levels[d];
       if (L > 1) {
-        if ((rem >> 32) == 0 && (L >> 32) == 0) {   // 32-bit divide when it fits (N < 2^32)
-          const uint32_t r32 = (uint32_t)rem, l32 = (uint32_t)L;
-          const uint32_t q32 = r32 / l32;
-          digit = r32 - q32 * l32;
-          rem = q32;
-        } else {
-          digit = rem % L;
-          rem = rem / L;
-        }
+        digit = rem % L;
+        rem = rem / L;
       }
       double v;
       if (sp.kind[d] == 0 || L <= 1) v = sp.lo[d];

@@ -64,6 +64,13 @@ def launch_list(path):
     print(f"{'launches':>8s} {'mean_ns':>12s} {'total_ns':>12s} {'share':>6s}  {'grid':>16s}  kernel")
     for (k, g), v in sorted(d.items(), key=lambda kv: -sum(kv[1])):
         print(f"{len(v):8d} {sum(v)/len(v):12.1f} {sum(v):12.1f} {100*sum(v)/tot:5.1f}%  {g:>16s}  {k}")
+    # every launch in order (us), so the legs that share a (kernel, grid) --
+    # e.g. the 10^6-candidate step and the latency leg's 10^5..10^8 fits --
+    # can be told apart
+    print("\n# launches in order: id  grid  us  kernel")
+    for r in rows[1:]:
+        name = r[ki].split("(")[0].replace("void ", "")
+        print(f"{r[0]:>5s} {r[gi]:>16s} {float(r[vi].replace(',', '')) / 1e3:12.1f}  {name}")
 
 
 if __name__ == "__main__":

@@ -272,14 +272,31 @@ opmm_status opmm_fit_batch(opmm_handle* h, const double* recorded, int64_t S,
  * (PAPER.md:252-255), or after max_iter iterations.  Coefficients rho = 1,
  * chi = 2, gamma = 0.5, sigma = 0.5 (SPEC D10); initial simplex: each
  * coordinate scaled by (1 + init_scale), zero coordinates set to
- * init_scale * 0.00025 (SPEC D9); stable sort (SPEC D14).  One warp per
- * problem; the iterates are the serial algorithm's. */
+ * init_scale * 0.00025 (SPEC D9); stable sort (SPEC D14).  Scheduled one
+ * warp per problem or one lane per problem (opmm_nm_schedule); either way the
+ * iterates are the serial algorithm's. */
 typedef enum {
   OPMM_NM_OBJ_PROPAGATOR = 0,   /* plant error, fit-path propagator (fast)          */
   OPMM_NM_OBJ_RK4_STAGES = 1,   /* plant error, literal four-stage RK4              */
   OPMM_NM_OBJ_REFERENCE = 2     /* plant error in the RK4 definition's operation
                                    order, explicitly rounded fp64 (reproducible)    */
 } opmm_nm_objective;
+
+/* How problems map onto the GPU.  Both give the serial algorithm's iterates
+ * (same decisions, same explicitly rounded simplex arithmetic, same order);
+ * they differ in which points are evaluated and in the gpu_evals count.
+ *   LOCKSTEP: the paper's schedule -- one warp per problem
+ *     evaluates every transformation point of an iteration at once (n + 4
+ *     points, one per lane): the lowest latency per problem.
+ *   LANE: one problem per lane, only the points the decision needs (~1.7 per
+ *     iteration): the highest throughput for many problems.
+ *   AUTO: LANE from 2048 problems (per rank) on, LOCKSTEP below (the measured
+ *     crossover on one B200). */
+typedef enum {
+  OPMM_NM_SCHEDULE_AUTO = 0,
+  OPMM_NM_SCHEDULE_LOCKSTEP = 1,
+  OPMM_NM_SCHEDULE_LANE = 2
+} opmm_nm_schedule;
 
 typedef struct {
   int32_t precision;     /* OPMM_FP64 / OPMM_FP32 (REFERENCE is always fp64)       */
@@ -290,7 +307,7 @@ typedef struct {
   double tol_f;          /* 0 = 1e-4                                                */
   double init_scale;     /* 0 = 0.05 (SPEC D9)                                      */
   int32_t cpu_check;     /* 1 = fill cpu_check (plant objectives)                  */
-  int32_t pad_;
+  int32_t schedule;      /* opmm_nm_schedule (0 = auto)                             */
 } opmm_nm_options;
 
 typedef struct {
@@ -299,7 +316,8 @@ typedef struct {
   double cpu_check;      /* serial host fp64 re-score of x (plant objectives)      */
   int32_t iterations;    /* iterations, counted as the serial algorithm counts them */
   int32_t func_evals;    /* objective evaluations the serial algorithm needs        */
-  int32_t gpu_evals;     /* evaluations performed (all points every iteration)      */
+  int32_t gpu_evals;     /* evaluations performed (LOCKSTEP: n + 4 per iteration;
+                            LANE: the serial algorithm's own, = func_evals)       */
   int32_t exit_reason;   /* 0 = tolerances met, 1 = max_iter                        */
 } opmm_nm_result;
 

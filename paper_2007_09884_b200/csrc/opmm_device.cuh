@@ -789,7 +789,7 @@ __device__ __forceinline__ double finish_error(T acc, int32_t n_samples) {
 template <typename T> struct LoopUnroll { static constexpr int value = 4; };
 template <> struct LoopUnroll<float> { static constexpr int value = 2; };
 
-template <typename T, int METRIC, bool TRAJ, bool STASHED = false>
+template <typename T, int METRIC, bool TRAJ, bool STASHED = false, int RL = 1>
 __device__ __forceinline__ T run_propagator(const Prop2<T>& pr, int32_t n_pulse, int32_t n_steps,
                                             const T* __restrict__ rel, T* __restrict__ traj,
                                             int64_t ld_out, T theta0, T sgn,
@@ -836,7 +836,7 @@ __device__ __forceinline__ T run_propagator(const Prop2<T>& pr, int32_t n_pulse,
   if (o) {  // first pulse step from the zero deviation state: z_1 = c, f_1 = qf
     th = pr.z1[0]; om = pr.z1[1]; xa = pr.z1[2]; xn = pr.z1[3];
     fa = pr.f1[0]; fn = pr.f1[1];
-    accumulate<METRIC>(acc, TRAJ ? th : th - rel[1]);
+    accumulate<METRIC>(acc, TRAJ ? th : th - rel[RL]);
     if (TRAJ) traj[ld_out] = fma(sgn, th, theta0);
   }
   // Block b covers steps k = o + 2b -> k + 2.  Every lane runs nb uniform
@@ -845,7 +845,7 @@ __device__ __forceinline__ T run_propagator(const Prop2<T>& pr, int32_t n_pulse,
   const int32_t nb = (n_steps + 1) / 2;
   const int32_t bs = switches ? (n_pulse - o) / 2 : nb;
   if (switches && bs == 0) swap_in();   // pulse ends before the first block
-  const T* __restrict__ rl = rel + o;   // rl[2b + 1], rl[2b + 2]
+  const T* __restrict__ rl = rel + o * RL;   // rl[(2b + 1) RL], rl[(2b + 2) RL]
   T* __restrict__ tr = TRAJ ? traj + (int64_t)o * ld_out : traj;
   // Segmented loop over blocks: uniform segments between consecutive lane
   // switch points (warp-min), so the inner loop is pure FMA work; at a
@@ -882,8 +882,8 @@ __device__ __forceinline__ T run_propagator(const Prop2<T>& pr, int32_t n_pulse,
         tr[(int64_t)(2 * b + 1) * ld_out] = fma(sgn, t1, theta0);
         tr[(int64_t)(2 * b + 2) * ld_out] = fma(sgn, th, theta0);
       } else {
-        accumulate<METRIC>(acc, t1 - rl[2 * b + 1]);
-        accumulate<METRIC>(acc, th - rl[2 * b + 2]);
+        accumulate<METRIC>(acc, t1 - rl[(2 * b + 1) * RL]);
+        accumulate<METRIC>(acc, th - rl[(2 * b + 2) * RL]);
       }
     }
     if (b == bs) swap_in();
@@ -895,11 +895,11 @@ __device__ __forceinline__ T run_propagator(const Prop2<T>& pr, int32_t n_pulse,
     const T t1 = fma(R0, th, fma(R1, om, fma(R2, xa, fma(R3, xn, fma(x0a, fa, fma(x0n, fn, d0))))));
     const T t2 = fma(Q00, th, fma(Q01, om, fma(Q02, xa, fma(Q03, xn, fma(A00, fa, fma(A01, fn, c0))))));
     if (k1 <= n_steps) {
-      accumulate<METRIC>(acc, TRAJ ? t1 : t1 - rel[k1]);
+      accumulate<METRIC>(acc, TRAJ ? t1 : t1 - rel[k1 * RL]);
       if (TRAJ) traj[(int64_t)k1 * ld_out] = fma(sgn, t1, theta0);
     }
     if (k1 + 1 <= n_steps) {
-      accumulate<METRIC>(acc, TRAJ ? t2 : t2 - rel[k1 + 1]);
+      accumulate<METRIC>(acc, TRAJ ? t2 : t2 - rel[(k1 + 1) * RL]);
       if (TRAJ) traj[(int64_t)(k1 + 1) * ld_out] = fma(sgn, t2, theta0);
     }
   }
@@ -1028,7 +1028,7 @@ __device__ __forceinline__ void run_propagator_multi(const Prop2<T> (&pr)[C],
 // Integrate + fused score, RK4_STAGES form: the four classical stages
 // evaluated literally (SPEC D2), in deviation coordinates, K_i = h f(Y_i).
 // ----------------------------------------------------------------------------
-template <typename T, int METRIC, bool TRAJ>
+template <typename T, int METRIC, bool TRAJ, int RL = 1>
 __device__ __forceinline__ T run_rk4_stages(const Setup& s, int32_t n_steps,
                                             const T* __restrict__ rel, T* __restrict__ traj,
                                             int64_t ld_out, T theta0, T sgn, int32_t substeps = 1) {
@@ -1071,7 +1071,7 @@ __device__ __forceinline__ T run_rk4_stages(const Setup& s, int32_t n_steps,
         y[i] = fma(sixth, t, y[i]);
       }
     }
-    accumulate<METRIC>(acc, TRAJ ? y[0] : y[0] - rel[k + 1]);
+    accumulate<METRIC>(acc, TRAJ ? y[0] : y[0] - rel[(k + 1) * RL]);
     if (TRAJ) traj[(int64_t)(k + 1) * ld_out] = fma(sgn, y[0], theta0);
   }
   return acc;
@@ -1080,7 +1080,7 @@ __device__ __forceinline__ T run_rk4_stages(const Setup& s, int32_t n_steps,
 // ---------------------------------------------------------------------------
 // Evaluate one candidate: physical check, setup, integrate + fused score.
 // ---------------------------------------------------------------------------
-template <typename T, int INTEG, int METRIC, bool TRAJ, typename RS = double>
+template <typename T, int INTEG, int METRIC, bool TRAJ, typename RS = double, int RL = 1>
 __device__ __forceinline__ double evaluate(const double p[NP], const CtlDev& c, double Aprime,
                                            double pw_default, const T* rel, T* traj,
                                            int64_t ld_out, double sgn, uint8_t* status,
@@ -1130,11 +1130,11 @@ __device__ __forceinline__ double evaluate(const double p[NP], const CtlDev& c, 
     } else {
       make_prop<T, true, RS>(s, pr, st2, ld);
     }
-    acc = run_propagator<T, METRIC, TRAJ, true>(pr, s.n_pulse, c.n_steps, rel, traj, ld_out,
+    acc = run_propagator<T, METRIC, TRAJ, true, RL>(pr, s.n_pulse, c.n_steps, rel, traj, ld_out,
                                                 (T)c.theta0, (T)sgn, stash, ld);
 #endif
   } else {
-    acc = run_rk4_stages<T, METRIC, TRAJ>(s, c.n_steps, rel, traj, ld_out, (T)c.theta0, (T)sgn,
+    acc = run_rk4_stages<T, METRIC, TRAJ, RL>(s, c.n_steps, rel, traj, ld_out, (T)c.theta0, (T)sgn,
                                           c.substeps);
   }
   if (pen != 0.0) {

@@ -139,6 +139,10 @@ size_t nm_smem(int precision, int obj, int32_t n_samples, bool rel_in_smem = tru
 int nm_problems_per_block();
 int nm_threads();
 cudaError_t launch_nm(const void* fn, const NmArgs& a, int grid, size_t smem, cudaStream_t st);
+// lane schedule: one problem per lane, 32 per block (opmm_nm.cu)
+const void* nm_lane_kernel_ptr(int precision, int obj, int metric, bool rel_global);
+size_t nm_lane_smem(int precision, int obj, int32_t n_samples, bool rel_in_smem);
+cudaError_t launch_nm_lane(const void* fn, const NmArgs& a, int grid, size_t smem, cudaStream_t st);
 
 const void* fit_kernel_ptr(int precision, int integrator, int metric);
 const void* fit2_kernel_ptr(int precision, int metric);   // 2 candidates/thread, 256 threads

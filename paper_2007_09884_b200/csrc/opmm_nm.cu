@@ -23,6 +23,7 @@
 // rounded fp64: bit-for-bit the definition's own arithmetic), and the SPEC
 // test functions (sphere, Rosenbrock, Powell).
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include "opmm.h"
@@ -60,7 +61,7 @@ __device__ __forceinline__ void ref_rhs(const double p[NP], const double y[6], d
 
 __device__ double ref_objective(const double p_in[NP], const double* rel, int32_t n_steps,
                                 double dt_ms, double Aprime, double pw_default, int metric,
-                                int32_t substeps) {
+                                int32_t substeps, int rel_ld = 1) {
   double p[NP];
 #pragma unroll
   for (int d = 0; d < NP; ++d) p[d] = p_in[d];
@@ -117,7 +118,7 @@ __device__ double ref_objective(const double p_in[NP], const double* rel, int32_
   for (int i = 0; i < 6; ++i) y[i] = ystar[i];
   double acc = 0.0;   // k = 0 term: |0 - rel_0| = 0
   {
-    const double d0 = Sr(Sr(y[0], ystar[0]), rel[0]);
+    const double d0 = Sr(Sr(y[0], ystar[0]), rel[0]);   // rel_ld: trace stride
     acc = metric == 0 ? Ar(acc, fabs(d0)) : Ar(acc, Mr(d0, d0));
   }
   for (int32_t k = 0; k < n_steps; ++k) {
@@ -141,7 +142,7 @@ __device__ double ref_objective(const double p_in[NP], const double* rel, int32_
       for (int i = 0; i < 6; ++i)
         y[i] = Ar(y[i], Mr(h6, Ar(Ar(Ar(k1[i], Mr(2.0, k2[i])), Mr(2.0, k3[i])), k4[i])));
     }
-    const double d = Sr(Sr(y[0], ystar[0]), rel[k + 1]);
+    const double d = Sr(Sr(y[0], ystar[0]), rel[(int64_t)(k + 1) * rel_ld]);
     acc = metric == 0 ? Ar(acc, fabs(d)) : Ar(acc, Mr(d, d));
   }
   if (!(acc < CAP)) return __longlong_as_double(0x7ff0000000000000LL);
@@ -419,6 +420,266 @@ static const void* nm_ptr(int precision, int obj, int metric) {
   return metric == 0 ? nm_fn<float, 1, 0, G>() : nm_fn<float, 1, 1, G>();
 }
 
+// ---------------------------------------------------------------------------
+// Lane schedule: one problem per LANE (32 per warp).  Each lane runs the
+// serial Lagarias iteration and evaluates only the points the decision needs
+// (reflection, then expansion or one contraction, shrink points one by one),
+// so a lane does ~1.7 evaluations per iteration instead of the n + 4 the
+// lock-step schedule spends per problem.  The warp steps its 32 problems
+// together: every step each lane builds its next point, all lanes evaluate
+// (the propagator loop's segment reductions need the whole warp), and each
+// lane applies its own decision.  Lanes whose problem has finished evaluate
+// their best vertex and drop the value.  The decisions, the explicitly
+// rounded simplex arithmetic and the stable order are the lock-step kernel's,
+// so the iterates are the same serial algorithm's.
+//
+// Shared memory, lane-interleaved ([.][32], conflict-free for any per-lane
+// slot): vertex slots S[19][18], f per slot, the centroid, the sorted order;
+// the relativized trace rel[k][32] (or the global workspace for long traces);
+// the propagator stash.  ~100 KB + the trace per warp: one warp per block.
+// ---------------------------------------------------------------------------
+constexpr int NML_NV = NM_NMAX + 1;
+enum { NML_INIT = 0, NML_R, NML_E, NML_OC, NML_IC, NML_SHRINK, NML_DONE };
+
+__host__ __device__ constexpr size_t nml_fixed_bytes() {
+  return (size_t)32 * (NML_NV * NM_NMAX * 8 + NML_NV * 8 + NM_NMAX * 8 + NML_NV * 4);
+}
+
+template <typename T, int OBJ, int METRIC, bool GREL>
+__global__ void __launch_bounds__(32, 1) nm_lane_kernel(NmArgs a) {
+  using RT = typename std::conditional<OBJ == 2, double, T>::type;   // trace type
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x;
+  double* S = reinterpret_cast<double*>(smem_raw);         // [slot][j][32]
+  double* FSv = S + NML_NV * NM_NMAX * 32;                  // [slot][32]
+  double* XBv = FSv + NML_NV * 32;                          // [j][32]
+  int* ORDv = reinterpret_cast<int*>(XBv + NM_NMAX * 32);   // [pos][32]
+  unsigned char* rest = smem_raw + nml_fixed_bytes();
+  T* stash = reinterpret_cast<T*>(rest);
+  if (OBJ != 3 && OBJ != 2) rest += stash_bytes<T>(32);
+  const int32_t ns = a.ctl.n_steps + 1;
+  RT* rel = (GREL ? reinterpret_cast<RT*>(a.rel_global) + (int64_t)blockIdx.x * ns * 32
+                  : reinterpret_cast<RT*>(rest)) + lane;    // rel[k * 32]
+#define SV(slot, j) S[((slot) * NM_NMAX + (j)) * 32 + lane]
+#define FS(slot) FSv[(slot) * 32 + lane]
+#define XB(j) XBv[(j) * 32 + lane]
+#define ORD(p) ORDv[(p) * 32 + lane]
+  const int64_t prob_raw = (int64_t)blockIdx.x * 32 + lane + a.prob_begin;
+  const bool live = prob_raw < a.prob_end;
+  const int64_t prob = live ? prob_raw : a.prob_end - 1;   // pad lanes mirror the last problem
+  const int n = OBJ == 3 ? a.dim : NP;
+  double sgn = 1.0, Aprime = 0.0, pwd = 0.0;
+  if (OBJ != 3) {
+    const double amp = a.sac_ctl[2 * prob];
+    pwd = a.sac_ctl[2 * prob + 1];
+    const double* rec = a.rec + prob * (int64_t)ns;
+    const double r0 = rec[0];
+    const double A = isnan(amp) ? rec[ns - 1] - r0 : amp;
+    sgn = A < 0.0 ? -1.0 : 1.0;
+    Aprime = fabs(A);
+    for (int k = 0; k < ns; ++k) rel[(int64_t)k * 32] = (RT)(sgn * (rec[k] - r0));
+  }
+  const double* x0 = a.x0 + prob * (int64_t)a.x0_ld;
+  const double rho = 1.0, chi = 2.0, psi = 0.5, sigma = 0.5;
+  // (ca, cb) of the four non-shrink points, as the lock-step kernel forms them
+  auto coefs = [&](int st, double& ca, double& cb) {
+    if (st == NML_R) { ca = Ar(1.0, rho); cb = -rho; }
+    else if (st == NML_E) { const double rc = Mr(rho, chi); ca = Ar(1.0, rc); cb = -rc; }
+    else if (st == NML_OC) { const double pr = Mr(psi, rho); ca = Ar(1.0, pr); cb = -pr; }
+    else { ca = Sr(1.0, psi); cb = psi; }
+  };
+  int st = NML_INIT, k = 0, sn = 0, s0 = 0;
+  int32_t it = 1, evals = n + 1, gpu_evals = 0, reason = 1;
+  double fr = 0.0, f0 = 0.0, fn1 = 0.0, fnn = 0.0;
+  // point of state (st, k); deterministic, so an accepted point is rebuilt
+  // bit-identically instead of being kept across the evaluation
+  auto build = [&](int s, int kk, double* x) {
+    if (s == NML_INIT) {
+#pragma unroll
+      for (int j = 0; j < NM_NMAX; ++j) {
+        if (j < n) {
+          double v = x0[j];
+          if (OBJ != 3 && j == PW_ && isnan(v)) v = pwd;
+          if (kk > 0 && j == kk - 1) v = v != 0.0 ? Mr(Ar(1.0, a.init_scale), v) : Mr(a.init_scale, 0.00025);
+          x[j] = v;
+        }
+      }
+    } else if (s == NML_SHRINK) {
+      const int sk = ORD(kk);
+#pragma unroll
+      for (int j = 0; j < NM_NMAX; ++j)
+        if (j < n) { const double v0 = SV(s0, j); x[j] = Ar(v0, Mr(sigma, Sr(SV(sk, j), v0))); }
+    } else if (s == NML_DONE) {
+      const int sb = ORD(0);
+#pragma unroll
+      for (int j = 0; j < NM_NMAX; ++j)
+        if (j < n) x[j] = SV(sb, j);
+    } else {
+      double ca, cb;
+      coefs(s, ca, cb);
+#pragma unroll
+      for (int j = 0; j < NM_NMAX; ++j)
+        if (j < n) x[j] = Ar(Mr(ca, XB(j)), Mr(cb, SV(sn, j)));
+    }
+  };
+  // start an iteration: exit tests, centroid, the decision's reference values
+  auto begin_iteration = [&]() {
+    if (!(it < a.max_iter)) { st = NML_DONE; return; }
+    // (loops ordered so each vertex's 18 loads are independent: one warp
+    // per SM leaves shared-memory latency exposed otherwise)
+    s0 = ORD(0);
+    bool ok = true;
+    {
+      const double fb = FS(s0);
+      for (int p = 1; p <= n; ++p) ok &= fabs(FS(ORD(p)) - fb) <= a.tol_f;
+    }
+    if (ok) {
+      double v0[NM_NMAX];
+#pragma unroll
+      for (int j = 0; j < NM_NMAX; ++j) v0[j] = j < n ? SV(s0, j) : 0.0;
+      for (int p = 1; p <= n; ++p) {
+        const int sp = ORD(p);
+#pragma unroll
+        for (int j = 0; j < NM_NMAX; ++j)
+          if (j < n) ok &= fabs(SV(sp, j) - v0[j]) <= a.tol_x;
+      }
+    }
+    if (ok) { st = NML_DONE; reason = 0; return; }
+    {
+      // centroid of the n best, summed per coordinate in vertex order
+      double sum[NM_NMAX];
+#pragma unroll
+      for (int j = 0; j < NM_NMAX; ++j) sum[j] = 0.0;
+      for (int i = 0; i < n; ++i) {
+        const int si = ORD(i);
+#pragma unroll
+        for (int j = 0; j < NM_NMAX; ++j)
+          if (j < n) sum[j] = Ar(sum[j], SV(si, j));
+      }
+#pragma unroll
+      for (int j = 0; j < NM_NMAX; ++j)
+        if (j < n) XB(j) = Dr(sum[j], (double)n);
+    }
+    sn = ORD(n);
+    f0 = FS(s0);
+    fn1 = FS(ORD(n - 1));
+    fnn = FS(sn);
+    st = NML_R;
+  };
+  // stable sort of positions 0..n by f (insertion; equal values keep order)
+  auto sort_all = [&]() {
+    for (int p = 1; p <= n; ++p) {
+      const int key = ORD(p);
+      const double fk = FS(key);
+      int q = p - 1;
+      while (q >= 0 && FS(ORD(q)) > fk) { ORD(q + 1) = ORD(q); --q; }
+      ORD(q + 1) = key;
+    }
+  };
+  if (!live) st = NML_DONE;
+  if (!live) {   // a pad lane still needs a valid point to evaluate
+#pragma unroll
+    for (int j = 0; j < NM_NMAX; ++j)
+      if (j < n) SV(0, j) = x0[j];
+    ORD(0) = 0;
+  }
+  while (!__all_sync(0xffffffffu, st == NML_DONE)) {
+    double f;
+    {
+      double x[NM_NMAX];
+      build(st, k, x);
+      if (OBJ == 3) {
+        f = test_objective(a.fn_id, n, x);
+      } else {
+        double p[NP];
+#pragma unroll
+        for (int d = 0; d < NP; ++d) p[d] = x[d];
+        __syncwarp();
+        if (OBJ == 2) {
+          f = ref_objective(p, reinterpret_cast<const double*>(rel), a.ctl.n_steps, a.ctl.dt_ms,
+                            Aprime, pwd, METRIC, a.ctl.substeps, 32);
+        } else {
+          f = evaluate<T, (OBJ == 4 ? 2 : OBJ), METRIC, false, double, 32>(
+              p, a.ctl, Aprime, pwd, reinterpret_cast<const T*>(rel), nullptr, 0, sgn, nullptr,
+              stash, true, 32);
+        }
+      }
+      if (isnan(f)) f = __longlong_as_double(0x7ff0000000000000LL);
+    }
+    if (st == NML_DONE) continue;
+    ++gpu_evals;
+    // Decide; every write below has a single call site (one warp per SM:
+    // the instruction cache is worth keeping small).
+    int put_state = -1, put_k = 0, put_slot = 0;   // point to store, if any
+    double put_f = f;
+    bool accept = false, resort = false, next = false;
+    switch (st) {
+      case NML_INIT:   // vertex k of the initial simplex, in slot k
+        put_state = NML_INIT; put_k = k; put_slot = k;
+        ORD(k) = k;
+        if (++k > n) { resort = true; next = true; }
+        break;
+      case NML_R:
+        fr = f;
+        if (fr < f0) st = NML_E;
+        else if (fr < fn1) { evals += 1; accept = true; put_state = NML_R; }
+        else if (fr < fnn) st = NML_OC;
+        else st = NML_IC;
+        break;
+      case NML_E:
+        evals += 2;
+        accept = true;
+        if (f < fr) put_state = NML_E;
+        else { put_state = NML_R; put_f = fr; }
+        break;
+      case NML_OC:
+      case NML_IC:
+        evals += 2;
+        if (st == NML_OC ? f <= fr : f < fnn) { accept = true; put_state = st; }
+        else { st = NML_SHRINK; k = 1; }
+        break;
+      case NML_SHRINK:
+        // shrink point k replaces the vertex at sorted position k (its old
+        // coordinates feed only this point)
+        put_state = NML_SHRINK; put_k = k; put_slot = ORD(k);
+        if (++k > n) { evals += n; resort = true; ++it; next = true; }
+        break;
+      default: break;
+    }
+    if (accept) { put_slot = sn; ++it; next = true; }
+    if (put_state >= 0) {
+      double x[NM_NMAX];
+      build(put_state, put_k, x);
+#pragma unroll
+      for (int j = 0; j < NM_NMAX; ++j)
+        if (j < n) SV(put_slot, j) = x[j];
+      FS(put_slot) = put_f;
+    }
+    if (accept) {   // vertex n replaced: stable re-rank of position n
+      int q = n - 1;
+      while (q >= 0 && FS(ORD(q)) > put_f) { ORD(q + 1) = ORD(q); --q; }
+      ORD(q + 1) = sn;
+    }
+    if (resort) sort_all();
+    if (next) begin_iteration();
+  }
+  if (live) {
+    const int sb = ORD(0);
+    for (int j = 0; j < n; ++j) a.x_best[prob * (int64_t)a.x_ld + j] = SV(sb, j);
+    NmOut o;
+    o.f_best = FS(sb);
+    o.iterations = it;
+    o.func_evals = evals;
+    o.gpu_evals = gpu_evals;
+    o.exit_reason = reason;
+    a.out[prob] = o;
+  }
+#undef SV
+#undef FS
+#undef XB
+#undef ORD
+}
+
 // rel_global: the instantiation that reads the trace from the global workspace
 const void* nm_kernel_ptr(int precision, int obj, int metric, bool rel_global) {
   return rel_global ? nm_ptr<true>(precision, obj, metric) : nm_ptr<false>(precision, obj, metric);
@@ -431,6 +692,42 @@ size_t nm_smem(int precision, int obj, int32_t n_samples, bool rel_in_smem) {
   const size_t st = precision == 0 || obj >= 2 ? stash_bytes<double>(NM_THREADS)
                                                : stash_bytes<float>(NM_THREADS);
   return NM_WARPS * sizeof(NmWarpSmem) + NM_WARPS * (obj == 3 ? 0 : relb) + (obj < 2 || obj == 4 ? st : 0);
+}
+
+template <typename T, int OBJ, int METRIC, bool GREL = false>
+static const void* nml_fn() { return reinterpret_cast<const void*>(&nm_lane_kernel<T, OBJ, METRIC, GREL>); }
+
+template <bool G>
+static const void* nml_ptr(int precision, int obj, int metric) {
+  if (obj == 3) return nml_fn<double, 3, 0, false>();
+  if (obj == 2) return metric == 0 ? nml_fn<double, 2, 0, G>() : nml_fn<double, 2, 1, G>();
+  if (obj == 4) {
+    if (precision == 0) return metric == 0 ? nml_fn<double, 4, 0, G>() : nml_fn<double, 4, 1, G>();
+    return metric == 0 ? nml_fn<float, 4, 0, G>() : nml_fn<float, 4, 1, G>();
+  }
+  if (precision == 0) {
+    if (obj == 0) return metric == 0 ? nml_fn<double, 0, 0, G>() : nml_fn<double, 0, 1, G>();
+    return metric == 0 ? nml_fn<double, 1, 0, G>() : nml_fn<double, 1, 1, G>();
+  }
+  if (obj == 0) return metric == 0 ? nml_fn<float, 0, 0, G>() : nml_fn<float, 0, 1, G>();
+  return metric == 0 ? nml_fn<float, 1, 0, G>() : nml_fn<float, 1, 1, G>();
+}
+
+const void* nm_lane_kernel_ptr(int precision, int obj, int metric, bool rel_global) {
+  return rel_global ? nml_ptr<true>(precision, obj, metric) : nml_ptr<false>(precision, obj, metric);
+}
+
+size_t nm_lane_smem(int precision, int obj, int32_t n_samples, bool rel_in_smem) {
+  const bool f32 = precision != 0 && obj != 2 && obj != 3;
+  size_t b = nml_fixed_bytes();
+  if (obj == 0 || obj == 1 || obj == 4) b += f32 ? stash_bytes<float>(32) : stash_bytes<double>(32);
+  if (rel_in_smem && obj != 3) b += (size_t)n_samples * 32 * (f32 ? sizeof(float) : sizeof(double));
+  return b;
+}
+
+cudaError_t launch_nm_lane(const void* fn, const NmArgs& a, int grid, size_t smem, cudaStream_t st) {
+  void* args[] = {const_cast<NmArgs*>(&a)};
+  return cudaLaunchKernel(fn, dim3(grid), dim3(32), args, smem, st);
 }
 
 int nm_problems_per_block() { return NM_WARPS; }

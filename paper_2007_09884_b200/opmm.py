@@ -72,7 +72,7 @@ class FitResult(C.Structure):
 class NmOptions(C.Structure):
     _fields_ = [("precision", C.c_int32), ("objective", C.c_int32), ("metric", C.c_int32),
                 ("max_iter", C.c_int32), ("tol_x", C.c_double), ("tol_f", C.c_double),
-                ("init_scale", C.c_double), ("cpu_check", C.c_int32), ("pad_", C.c_int32)]
+                ("init_scale", C.c_double), ("cpu_check", C.c_int32), ("schedule", C.c_int32)]
 
 
 class NmResult(C.Structure):
@@ -87,6 +87,7 @@ class NmResult(C.Structure):
 
 
 NM_OBJ_PROPAGATOR, NM_OBJ_RK4_STAGES, NM_OBJ_REFERENCE = 0, 1, 2
+NM_SCHEDULE_AUTO, NM_SCHEDULE_LOCKSTEP, NM_SCHEDULE_LANE = 0, 1, 2
 NM_SPHERE, NM_ROSENBROCK, NM_POWELL = 0, 1, 2
 
 
@@ -393,8 +394,10 @@ def opmm_fit_batch(h: Handle, recorded, ctls, space, n_per: int,
 
 # ---------------------------------------------------------------------- Nelder-Mead
 def nm_options(precision=FP64, objective=NM_OBJ_PROPAGATOR, metric=METRIC_L1, max_iter=0, tol_x=0.0,
-               tol_f=0.0, init_scale=0.0, cpu_check=1) -> NmOptions:
-    return NmOptions(precision, objective, metric, max_iter, tol_x, tol_f, init_scale, cpu_check, 0)
+               tol_f=0.0, init_scale=0.0, cpu_check=1, schedule=0) -> NmOptions:
+    """schedule: NM_SCHEDULE_AUTO / NM_SCHEDULE_LOCKSTEP / NM_SCHEDULE_LANE (opmm.h)."""
+    return NmOptions(precision, objective, metric, max_iter, tol_x, tol_f, init_scale, cpu_check,
+                     schedule)
 
 
 def opmm_estimate_batch(h: Handle, recorded, ctls, x0=None, options: NmOptions | None = None) -> list:

@@ -1,8 +1,10 @@
 """GPU parity of the batched Nelder-Mead estimator (-m gpu).
 
-The GPU engine evaluates all n + 4 transformation points every iteration
- but takes the serial Lagarias decision, so with the same
-objective values its iterates are the serial algorithm's.  With the
+Two schedules.  LOCKSTEP (the paper's) evaluates all n + 4
+transformation points of an iteration at once, one warp per problem; LANE
+runs one problem per lane and evaluates only the points the decision needs.
+Both take the serial Lagarias decision, so with the same objective values
+their iterates are the serial algorithm's.  With the
 reference-order plant objective (explicitly rounded fp64, the RK4
 definition's operation order) and on the SPEC test functions the GPU results
 are bit-identical to the CPU oracle's serial Nelder-Mead: same best vertex,
@@ -35,20 +37,28 @@ def h(opmm):
         yield handle
 
 
-def test_rosenbrock_published_run_bit_exact(opmm, h):
-    r = opmm.opmm_nm_minimize_test(h, opmm.NM_ROSENBROCK, [[-1.2, 1.0]])[0]
+SCHEDULES = pytest.mark.parametrize("schedule", [1, 2], ids=["lockstep", "lane"])
+
+
+@SCHEDULES
+def test_rosenbrock_published_run_bit_exact(opmm, h, schedule):
+    r = opmm.opmm_nm_minimize_test(h, opmm.NM_ROSENBROCK, [[-1.2, 1.0]],
+                                   opmm.nm_options(schedule=schedule))[0]
     o = oracle.nm_test(oracle.NM_ROSENBROCK, [-1.2, 1.0])
     assert (r["iterations"], r["func_evals"]) == (85, 159) == (o["iterations"], o["func_evals"])
     assert r["x"].tolist() == o["x"].tolist() and r["f"] == o["f"]
-    assert r["gpu_evals"] == 3 + 84 * 6      # every iteration evaluates n + 4 points
+    # lock-step: every iteration evaluates n + 4 points; lane: only the needed ones
+    assert r["gpu_evals"] == (3 + 84 * 6 if schedule == 1 else 159)
 
 
+@SCHEDULES
 @pytest.mark.parametrize("fn,dim", [(0, 3), (1, 2), (1, 4), (2, 4)])
-def test_test_functions_many_starts_bit_exact(opmm, h, fn, dim):
+def test_test_functions_many_starts_bit_exact(opmm, h, fn, dim, schedule):
     rng = np.random.default_rng(fn * 10 + dim)
-    x0 = rng.uniform(-2, 2, size=(40, dim))
+    x0 = rng.uniform(-2, 2, size=(40, dim))        # lane: one full warp + a ragged one
     x0[0, 0] = 0.0                                  # zero-coordinate initial step (D9)
-    res = opmm.opmm_nm_minimize_test(h, fn, x0, opmm.nm_options(tol_x=1e-7, tol_f=1e-9, max_iter=3000))
+    res = opmm.opmm_nm_minimize_test(h, fn, x0, opmm.nm_options(tol_x=1e-7, tol_f=1e-9, max_iter=3000,
+                                                                schedule=schedule))
     for s in range(len(x0)):
         o = oracle.nm_test(fn, x0[s], tol_x=1e-7, tol_f=1e-9, max_iter=3000)
         r = res[s]
@@ -71,11 +81,12 @@ def _roundtrip_set(S, seed=7, n_steps=100):
     return ctls, np.array(recs), truths
 
 
-def test_plant_reference_objective_bit_exact_vs_oracle(opmm, h):
+@SCHEDULES
+def test_plant_reference_objective_bit_exact_vs_oracle(opmm, h, schedule):
     """Reference-order objective: every saccade's Nelder-Mead run identical to
     the oracle's serial run, bit for bit (x, f, iterations, evaluations)."""
     ctls, recs, _ = _roundtrip_set(6)
-    opts = opmm.nm_options(objective=opmm.NM_OBJ_REFERENCE, max_iter=400)
+    opts = opmm.nm_options(objective=opmm.NM_OBJ_REFERENCE, max_iter=400, schedule=schedule)
     res = opmm.opmm_estimate_batch(h, recs, ctls, options=opts)
     o = oracle.estimate_batch(recs, ctls, max_iter=400)
     for s in range(len(ctls)):
@@ -87,32 +98,76 @@ def test_plant_reference_objective_bit_exact_vs_oracle(opmm, h):
         assert abs(r["cpu_check"] - r["f"]) <= 1e-9 * r["f"]
 
 
+@SCHEDULES
 @pytest.mark.parametrize("precision", [0, 1])
-def test_plant_fast_objective_roundtrip(opmm, h, precision):
+def test_plant_fast_objective_roundtrip(opmm, h, precision, schedule):
     """Propagator objective (the fit path's evaluator): SPEC acceptance 4 --
     per-sample mean residual <= 0.5 deg on >= 90% of round-trip saccades;
     the result's objective agrees with the serial CPU_check re-score."""
     ctls, recs, _ = _roundtrip_set(40, seed=11)
-    res = opmm.opmm_estimate_batch(h, recs, ctls, options=opmm.nm_options(precision=precision))
+    res = opmm.opmm_estimate_batch(h, recs, ctls,
+                                   options=opmm.nm_options(precision=precision, schedule=schedule))
     f = np.array([r["f"] for r in res])
     assert np.mean(f / 101.0 <= 0.5) >= 0.9
     tol = 1e-9 if precision == 0 else 1e-4
     for r, rec, c in zip(res, recs, ctls):
         assert abs(r["cpu_check"] - r["f"]) <= tol * max(r["f"], 1.0)
         assert r["f"] <= oracle.objective(W.truth_opc(), rec, c)   # never worse than the start
-        assert r["gpu_evals"] == 19 + (r["iterations"] - 1) * 22
+        assert r["gpu_evals"] == (19 + (r["iterations"] - 1) * 22 if schedule == 1 else r["func_evals"])
 
 
-def test_long_trace_uses_global_trace_workspace(opmm, h):
-    """Traces too long for the per-warp shared-memory copy (here 6000 samples)
-    are relativized into a global workspace; the reference-order objective
-    stays bit-identical to the oracle's serial Nelder-Mead."""
+@pytest.mark.parametrize("precision", [0, 1])
+def test_schedules_identical_with_fast_objective(opmm, h, precision):
+    """Both schedules run the same evaluator arithmetic and the same serial
+    decisions, so with the propagator objective their results are identical
+    bit for bit (70 problems: two full warps of the lane schedule and a
+    ragged third)."""
+    ctls, recs, _ = _roundtrip_set(70, seed=13)
+    runs = [opmm.opmm_estimate_batch(h, recs, ctls,
+                                     options=opmm.nm_options(precision=precision, schedule=sc,
+                                                             cpu_check=0))
+            for sc in (1, 2)]
+    for s in range(len(ctls)):
+        a, b = runs[0][s], runs[1][s]
+        for key in ("f", "iterations", "func_evals", "exit_reason"):
+            assert a[key] == b[key], (s, key)
+        assert a["x"].tolist() == b["x"].tolist(), s
+        assert b["gpu_evals"] == b["func_evals"]
+
+
+def test_auto_schedule_switches_at_2048_problems(opmm, h):
+    """AUTO: lock-step below 2048 problems, lane from 2048 on (the measured
+    crossover); the lane runs at 2048 equal the oracle's serial runs."""
+    rng = np.random.default_rng(5)
+    x0 = rng.uniform(-2, 2, size=(2048, 3))
+    opts = opmm.nm_options(tol_x=1e-7, tol_f=1e-9, max_iter=600)
+    small = opmm.opmm_nm_minimize_test(h, opmm.NM_SPHERE, x0[:2047], opts)
+    big = opmm.opmm_nm_minimize_test(h, opmm.NM_SPHERE, x0, opts)
+    assert all(r["gpu_evals"] == 4 + (r["iterations"] - 1) * 7 for r in small)   # n + 4 per iteration
+    assert all(r["gpu_evals"] == r["func_evals"] for r in big)
+    for s in range(0, 2048, 97):
+        o = oracle.nm_test(opmm.NM_SPHERE, x0[s], tol_x=1e-7, tol_f=1e-9, max_iter=600)
+        assert big[s]["x"].tolist() == o["x"].tolist() and big[s]["f"] == o["f"], s
+        assert small[s]["x"].tolist() == o["x"].tolist(), s
+
+
+def test_schedule_option_validated(opmm, h):
+    ctls, recs, _ = _roundtrip_set(1)
+    with pytest.raises(opmm.OpmmError):
+        opmm.opmm_estimate_batch(h, recs, ctls, options=opmm.nm_options(schedule=3))
+
+
+@SCHEDULES
+def test_long_trace_uses_global_trace_workspace(opmm, h, schedule):
+    """Traces too long for the shared-memory copy (here 6000 samples) are
+    relativized into a global workspace; the reference-order objective stays
+    bit-identical to the oracle's serial Nelder-Mead."""
     ctl = W.Control(n_steps=6000, dt_ms=0.02, amplitude_deg=10.0)
     rec = oracle.positions(W.truth_opc(), ctl) + W.noise(6001)
-    opts = opmm.nm_options(objective=opmm.NM_OBJ_REFERENCE, max_iter=15, cpu_check=0)
+    opts = opmm.nm_options(objective=opmm.NM_OBJ_REFERENCE, max_iter=15, cpu_check=0, schedule=schedule)
     res = opmm.opmm_estimate_batch(h, rec[None, :], [ctl], options=opts)
     o = oracle.estimate_batch(rec[None, :], [ctl], max_iter=15)
     assert res[0]["x"].tolist() == o["x"][0].tolist() and res[0]["f"] == o["f"][0]
     fast = opmm.opmm_estimate_batch(h, rec[None, :], [ctl],
-                                    options=opmm.nm_options(max_iter=15, cpu_check=1))
+                                    options=opmm.nm_options(max_iter=15, cpu_check=1, schedule=schedule))
     assert abs(fast[0]["cpu_check"] - fast[0]["f"]) <= 1e-9 * fast[0]["f"]

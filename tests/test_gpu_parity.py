@@ -805,18 +805,25 @@ def test_fit_substeps_matches_oracle(opmm, h, precision):
     assert abs(r["cpu_check"] - o["best_err"]) <= 1e-9 * o["best_err"] or precision == 1
 
 
-def test_nm_substeps_reference_bit_identical(opmm, h):
+@pytest.mark.parametrize("schedule", [1, 2], ids=["lockstep", "lane"])
+def test_nm_substeps_reference_bit_identical(opmm, h, schedule):
     """The reference-order NM objective with substeps is bit-identical to the
-    oracle's serial Nelder-Mead with substeps."""
+    oracle's serial Nelder-Mead with substeps, in both NM schedules; the
+    propagator objective with substeps gives the same run in both."""
     ctl = W.Control(substeps=3, amplitude_deg=10.0)
     rec = trace(W.Control())
     res = opmm.opmm_estimate_batch(h, rec[None, :], [ctl],
                                    options=opmm.nm_options(objective=opmm.NM_OBJ_REFERENCE,
-                                                           max_iter=60, cpu_check=0))
+                                                           max_iter=60, cpu_check=0,
+                                                           schedule=schedule))
     o = oracle.estimate_batch(rec[None, :], [ctl], max_iter=60)
     assert res[0]["iterations"] == int(o["iterations"][0])
     assert res[0]["f"] == float(o["f"][0])
     assert np.array_equal(np.array(res[0]["x"]), o["x"][0])
+    fast = [opmm.opmm_estimate_batch(h, rec[None, :], [ctl],
+                                     options=opmm.nm_options(max_iter=60, cpu_check=0, schedule=sc))[0]
+            for sc in (1, 2)]
+    assert fast[0]["f"] == fast[1]["f"] and fast[0]["x"].tolist() == fast[1]["x"].tolist()
 
 
 def test_sync_fit_graph_replay_and_invalidation(opmm, h):

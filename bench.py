@@ -303,10 +303,10 @@ def nm_leg(h, opmm, torch, args, max_over_ranks=lambda x: x, sum_over_ranks=lamb
     f = np.array([r["f"] for r in res])
     conv = np.array([r["exit_reason"] == 0 for r in res])
     evals = int(sum_over_ranks(float(sum(r["gpu_evals"] for r in res))))
-    # AUTO schedule (opmm.h): lane from 2048 problems per rank, else lock-step
-    lane = all(r["gpu_evals"] == r["func_evals"] for r in res)
+    # AUTO schedule (opmm.h): group from 1024 problems per rank, else lock-step
+    group = len(res) >= 1024
     return {"metric": "NM-fitted saccades/s", "saccades": S, "n_steps": n_steps,
-            "schedule": "lane (one problem per lane, needed points only)" if lane else
+            "schedule": "group (4 lanes per problem: xr, xe, xc, xcc at once)" if group else
                         "lockstep (one problem per warp, all n + 4 points per iteration)",
             "objective": "propagator fp64, L1", "value": S / (kern_ms * 1e-3),
             "e2e_value": S / e2e_s, "kernel_ms": kern_ms, "mean_iterations": float(its.mean()),

@@ -289,13 +289,18 @@ typedef enum {
  *     evaluates every transformation point of an iteration at once (n + 4
  *     points, one per lane): the lowest latency per problem.
  *   LANE: one problem per lane, only the points the decision needs (~1.7 per
- *     iteration): the highest throughput for many problems.
- *   AUTO: LANE from 2048 problems (per rank) on, LOCKSTEP below (the measured
- *     crossover on one B200). */
+ *     iteration): the fewest evaluations.
+ *   GROUP: 4 lanes per problem evaluate the reflection, expansion and both
+ *     contractions at once (shrink and initial points 4 at a time): one
+ *     evaluation of latency per iteration at 8 problems per warp.
+ *   AUTO: GROUP from 1024 problems (per rank) on, LOCKSTEP below (measured on
+ *     one B200: GROUP is the fastest from ~1000 problems on, LOCKSTEP below;
+ *     LANE does the least work but has the longest latency per iteration). */
 typedef enum {
   OPMM_NM_SCHEDULE_AUTO = 0,
   OPMM_NM_SCHEDULE_LOCKSTEP = 1,
-  OPMM_NM_SCHEDULE_LANE = 2
+  OPMM_NM_SCHEDULE_LANE = 2,
+  OPMM_NM_SCHEDULE_GROUP = 3
 } opmm_nm_schedule;
 
 typedef struct {
@@ -317,7 +322,8 @@ typedef struct {
   int32_t iterations;    /* iterations, counted as the serial algorithm counts them */
   int32_t func_evals;    /* objective evaluations the serial algorithm needs        */
   int32_t gpu_evals;     /* evaluations performed (LOCKSTEP: n + 4 per iteration;
-                            LANE: the serial algorithm's own, = func_evals)       */
+                            LANE: the serial algorithm's own, = func_evals;
+                            GROUP: 4 per iteration, n per shrink)                 */
   int32_t exit_reason;   /* 0 = tolerances met, 1 = max_iter                        */
 } opmm_nm_result;
 

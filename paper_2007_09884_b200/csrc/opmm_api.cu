@@ -594,11 +594,12 @@ struct NmConfig {
   double tol_x, tol_f, init_scale;
 };
 
-// OPMM_NM_SCHEDULE_AUTO: the lane schedule from this many problems on (one
-// rank's share), the lock-step schedule below it.  Measured crossover on one
-// B200, n = 150 population (tools/time_nm_schedules.py):
-// 1024 problems 40 vs 67 ms, 2048: 69 vs 67 ms, 4096: 116 vs 68 ms.
-constexpr int64_t kNmLaneMinProblems = 2048;
+// OPMM_NM_SCHEDULE_AUTO: the group schedule from this many problems on (one
+// rank's share), the lock-step schedule below it.  Measured on one B200, n =
+// 150 population, lock-step / lane / group (tools/time_nm_schedules.py,
+// DESIGN.md section 8a): 256 problems 25 / 65 / 37 ms; 1024: 40 / 67 / 38 ms;
+// 4096: 114 / 66 / 37 ms; 16384: 394 / 174 / 131 ms.
+constexpr int64_t kNmGroupMinProblems = 1024;
 
 opmm_status nm_config(const opmm_nm_options* o, int dim, bool plant, NmConfig* c) {
   c->obj = plant ? (o ? o->objective : OPMM_NM_OBJ_PROPAGATOR) : 3;
@@ -610,7 +611,7 @@ opmm_status nm_config(const opmm_nm_options* o, int dim, bool plant, NmConfig* c
   c->init_scale = (o && o->init_scale != 0.0) ? o->init_scale : 0.05;
   c->cpu_check = o ? o->cpu_check : 1;
   c->schedule = o ? o->schedule : OPMM_NM_SCHEDULE_AUTO;
-  if (c->schedule < OPMM_NM_SCHEDULE_AUTO || c->schedule > OPMM_NM_SCHEDULE_LANE)
+  if (c->schedule < OPMM_NM_SCHEDULE_AUTO || c->schedule > OPMM_NM_SCHEDULE_GROUP)
     return fail(OPMM_ERR_INVALID_ARG, "bad NM schedule %d", c->schedule);
   if (plant && (c->obj < 0 || c->obj > 2)) return fail(OPMM_ERR_INVALID_ARG, "bad NM objective");
   if (!check_precision(c->precision)) return fail(OPMM_ERR_INVALID_ARG, "bad precision");
@@ -628,23 +629,30 @@ opmm_status nm_launch(opmm_handle* h, const NmConfig& c, const double* rec_dev,
   const int32_t ns = ctl0 ? ctl0->n_steps + 1 : 1;
   // the propagator objective with substeps has its own instantiation (obj 4)
   const int obj = (c.obj == 0 && ctl0 && ctl0->substeps > 1) ? 4 : c.obj;
-  const bool lane = c.schedule == OPMM_NM_SCHEDULE_LANE ||
-                    (c.schedule == OPMM_NM_SCHEDULE_AUTO && pe - pb >= kNmLaneMinProblems);
-  const int per = lane ? 32 : opmm::nm_problems_per_block();
+  const bool lane = c.schedule == OPMM_NM_SCHEDULE_LANE;
+  const bool group = c.schedule == OPMM_NM_SCHEDULE_GROUP ||
+                     (c.schedule == OPMM_NM_SCHEDULE_AUTO && pe - pb >= kNmGroupMinProblems);
+  const int per = lane ? 32 : group ? opmm::nm_group_problems_per_block() : opmm::nm_problems_per_block();
   const int64_t n_blocks = (pe - pb + per - 1) / per;
-  size_t smem = lane ? opmm::nm_lane_smem(c.precision, obj, ns, true) : opmm::nm_smem(c.precision, obj, ns);
+  auto smem_for = [&](bool in_smem) {
+    return lane ? opmm::nm_lane_smem(c.precision, obj, ns, in_smem)
+           : group ? opmm::nm_group_smem(c.precision, obj, ns, in_smem)
+                   : opmm::nm_smem(c.precision, obj, ns, in_smem);
+  };
+  auto kernel_for = [&](bool grel) {
+    return lane ? opmm::nm_lane_kernel_ptr(c.precision, obj, c.metric, grel)
+           : group ? opmm::nm_group_kernel_ptr(c.precision, obj, c.metric, grel)
+                   : opmm::nm_kernel_ptr(c.precision, obj, c.metric, grel);
+  };
+  size_t smem = smem_for(true);
   // lane schedule with more warps than SMs: the trace goes to the global
   // workspace so that two warps fit per SM (the simplex alone is ~100 KB)
   const bool lane_waves = lane && (n_blocks > h->num_sms || getenv("OPMM_NM_LANE_GREL") != nullptr);
-  const bool rel_global =
-      lane_waves ||
-      smem > max_dyn_smem(lane ? opmm::nm_lane_kernel_ptr(c.precision, obj, c.metric, false)
-                               : opmm::nm_kernel_ptr(c.precision, obj, c.metric));
+  const bool rel_global = lane_waves || smem > max_dyn_smem(kernel_for(false));
   if (rel_global) {   // long traces: relativized per problem in global memory
-    smem = lane ? opmm::nm_lane_smem(c.precision, obj, ns, false)
-                : opmm::nm_smem(c.precision, obj, ns, false);
-    // lane schedule: [block][k][32] (lane-interleaved), padded to whole blocks
-    const int64_t slots = lane ? n_blocks * 32 : pe - pb;
+    smem = smem_for(false);
+    // lane / group schedules: [block][k][per] (interleaved), padded to whole blocks
+    const int64_t slots = (lane || group) ? n_blocks * per : pe - pb;
     CKS(ensure(h->nm_rel, h->nm_rel_cap, (size_t)slots * (size_t)ns));
   }
   if (smem > kMaxDynSmem) return fail(OPMM_ERR_INVALID_ARG, "trace too long for the NM kernel");
@@ -671,12 +679,10 @@ opmm_status nm_launch(opmm_handle* h, const NmConfig& c, const double* rec_dev,
   if (grid == 0) return OPMM_OK;
   if (grid > 0x7fffffff) return fail(OPMM_ERR_INVALID_ARG, "too many problems");
   CKS(record_start(h, h->stream));
-  if (lane)
-    CK(opmm::launch_nm_lane(opmm::nm_lane_kernel_ptr(c.precision, obj, c.metric, rel_global), a,
-                            (int)grid, smem, h->stream));
+  if (lane || group)   // 32-thread blocks
+    CK(opmm::launch_nm_lane(kernel_for(rel_global), a, (int)grid, smem, h->stream));
   else
-    CK(opmm::launch_nm(opmm::nm_kernel_ptr(c.precision, obj, c.metric, rel_global), a, (int)grid,
-                       smem, h->stream));
+    CK(opmm::launch_nm(kernel_for(rel_global), a, (int)grid, smem, h->stream));
   CKS(record_stop(h, h->stream));
   return OPMM_OK;
 }
@@ -759,6 +765,7 @@ opmm_status opmm_create(opmm_handle** out, int device) {
           for (int g = 0; g < 2; ++g) {
             allow_dyn_smem(opmm::nm_kernel_ptr(p, obj, m, g == 1));
             allow_dyn_smem(opmm::nm_lane_kernel_ptr(p, obj, m, g == 1));
+            allow_dyn_smem(opmm::nm_group_kernel_ptr(p, obj, m, g == 1));
           }
       }
   cudaGetLastError();

@@ -143,6 +143,10 @@ cudaError_t launch_nm(const void* fn, const NmArgs& a, int grid, size_t smem, cu
 const void* nm_lane_kernel_ptr(int precision, int obj, int metric, bool rel_global);
 size_t nm_lane_smem(int precision, int obj, int32_t n_samples, bool rel_in_smem);
 cudaError_t launch_nm_lane(const void* fn, const NmArgs& a, int grid, size_t smem, cudaStream_t st);
+// group schedule: 4 lanes per problem, 8 problems per 32-thread block (launch_nm_lane)
+const void* nm_group_kernel_ptr(int precision, int obj, int metric, bool rel_global);
+size_t nm_group_smem(int precision, int obj, int32_t n_samples, bool rel_in_smem);
+int nm_group_problems_per_block();
 
 const void* fit_kernel_ptr(int precision, int integrator, int metric);
 const void* fit2_kernel_ptr(int precision, int metric);   // 2 candidates/thread, 256 threads

@@ -680,6 +680,290 @@ __global__ void __launch_bounds__(32, 1) nm_lane_kernel(NmArgs a) {
 #undef ORD
 }
 
+// ---------------------------------------------------------------------------
+// Group schedule: 4 lanes per problem, 8 problems per warp.  The paper's
+// "all transformations simultaneously" sized to what the
+// decision can use: every iteration the group evaluates the reflection, the
+// expansion and both contractions at once (lanes q = 0..3), so an iteration
+// costs one evaluation of latency; the shrink points (rare) and the initial
+// vertices go 4 at a time.  The centroid and the exit tests are split over
+// the group's lanes by coordinate.  Same decisions, same explicitly rounded
+// arithmetic, same stable order as the other schedules: the same runs.
+// Shared memory ~40 KB per warp (problems interleaved [.][8]): ~5 warps/SM.
+// ---------------------------------------------------------------------------
+constexpr int NMQ_G = 4;              // lanes per problem
+constexpr int NMQ_P = 32 / NMQ_G;     // problems per warp
+enum { NMQ_INIT = 0, NMQ_ITER, NMQ_SHRINK, NMQ_DONE };
+
+__host__ __device__ constexpr size_t nmq_fixed_bytes() {
+  return (size_t)NMQ_P * (NML_NV * NM_NMAX * 8 + NML_NV * 8 + NM_NMAX * 8 + NML_NV * 4);
+}
+
+template <typename T, int OBJ, int METRIC, bool GREL>
+__global__ void __launch_bounds__(32) nm_group_kernel(NmArgs a) {
+  using RT = typename std::conditional<OBJ == 2, double, T>::type;   // trace type
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x, g = lane >> 2, q = lane & 3;
+  const unsigned gmask = 0xFu << (4 * g);
+  double* S = reinterpret_cast<double*>(smem_raw);           // [slot][j][8]
+  double* FSv = S + NML_NV * NM_NMAX * NMQ_P;                 // [slot][8]
+  double* XBv = FSv + NML_NV * NMQ_P;                         // [j][8]
+  int* ORDv = reinterpret_cast<int*>(XBv + NM_NMAX * NMQ_P);  // [pos][8]
+  unsigned char* rest = smem_raw + nmq_fixed_bytes();
+  T* stash = reinterpret_cast<T*>(rest);
+  if (OBJ != 3 && OBJ != 2) rest += stash_bytes<T>(32);
+  const int32_t ns = a.ctl.n_steps + 1;
+  RT* rel = (GREL ? reinterpret_cast<RT*>(a.rel_global) + (int64_t)blockIdx.x * ns * NMQ_P
+                  : reinterpret_cast<RT*>(rest)) + g;         // rel[k * 8]
+#define SV(slot, j) S[((slot) * NM_NMAX + (j)) * NMQ_P + g]
+#define FS(slot) FSv[(slot) * NMQ_P + g]
+#define XB(j) XBv[(j) * NMQ_P + g]
+#define ORD(p) ORDv[(p) * NMQ_P + g]
+  const int64_t prob_raw = (int64_t)blockIdx.x * NMQ_P + g + a.prob_begin;
+  const bool live = prob_raw < a.prob_end;
+  const int64_t prob = live ? prob_raw : a.prob_end - 1;   // pad groups mirror the last problem
+  const int n = OBJ == 3 ? a.dim : NP;
+  double sgn = 1.0, Aprime = 0.0, pwd = 0.0;
+  if (OBJ != 3) {
+    const double amp = a.sac_ctl[2 * prob];
+    pwd = a.sac_ctl[2 * prob + 1];
+    const double* rec = a.rec + prob * (int64_t)ns;
+    const double r0 = rec[0];
+    const double A = isnan(amp) ? rec[ns - 1] - r0 : amp;
+    sgn = A < 0.0 ? -1.0 : 1.0;
+    Aprime = fabs(A);
+    for (int k = q; k < ns; k += NMQ_G) rel[(int64_t)k * NMQ_P] = (RT)(sgn * (rec[k] - r0));
+  }
+  const double* x0 = a.x0 + prob * (int64_t)a.x0_ld;
+  const double rho = 1.0, chi = 2.0, psi = 0.5, sigma = 0.5;
+  auto coefs = [&](int t, double& ca, double& cb) {   // t: 0 xr, 1 xe, 2 xc, 3 xcc
+    if (t == 0) { ca = Ar(1.0, rho); cb = -rho; }
+    else if (t == 1) { const double rc = Mr(rho, chi); ca = Ar(1.0, rc); cb = -rc; }
+    else if (t == 2) { const double pr = Mr(psi, rho); ca = Ar(1.0, pr); cb = -pr; }
+    else { ca = Sr(1.0, psi); cb = psi; }
+  };
+  auto x0_coord = [&](int v, int j) {   // coordinate j of initial vertex v
+    double x = x0[j];
+    if (OBJ != 3 && j == PW_ && isnan(x)) x = pwd;
+    if (v > 0 && j == v - 1) x = x != 0.0 ? Mr(Ar(1.0, a.init_scale), x) : Mr(a.init_scale, 0.00025);
+    return x;
+  };
+  // group-uniform state (every lane of the group keeps the same copy)
+  int st = NMQ_INIT, k = 0, sn = 0, s0 = 0;
+  int32_t it = 1, evals = n + 1, gpu_evals = 0, reason = 1;
+  double f0 = 0.0, fn1 = 0.0, fnn = 0.0;
+  auto sort_all = [&]() {   // lane q = 0; stable insertion sort of positions 0..n by f
+    for (int p = 1; p <= n; ++p) {
+      const int key = ORD(p);
+      const double fk = FS(key);
+      int r = p - 1;
+      while (r >= 0 && FS(ORD(r)) > fk) { ORD(r + 1) = ORD(r); --r; }
+      ORD(r + 1) = key;
+    }
+  };
+  // all 4 lanes of the group, group-uniform control flow
+  auto begin_iteration = [&]() {
+    if (!(it < a.max_iter)) { st = NMQ_DONE; return; }
+    s0 = ORD(0);
+    bool ok = true;
+    const double fb = FS(s0);
+    for (int p = 1 + q; p <= n; p += NMQ_G) ok &= fabs(FS(ORD(p)) - fb) <= a.tol_f;
+    for (int j = q; j < n; j += NMQ_G) {
+      const double v0 = SV(s0, j);
+      for (int p = 1; p <= n; ++p) ok &= fabs(SV(ORD(p), j) - v0) <= a.tol_x;
+    }
+    if (__all_sync(gmask, ok)) { st = NMQ_DONE; reason = 0; return; }
+    for (int j = q; j < n; j += NMQ_G) {   // centroid, summed in vertex order
+      double sum = 0.0;
+      for (int i = 0; i < n; ++i) sum = Ar(sum, SV(ORD(i), j));
+      XB(j) = Dr(sum, (double)n);
+    }
+    __syncwarp(gmask);
+    sn = ORD(n);
+    f0 = fb;
+    fn1 = FS(ORD(n - 1));
+    fnn = FS(sn);
+    st = NMQ_ITER;
+  };
+  if (!live) {
+    if (q == 0) {
+      for (int j = 0; j < n; ++j) SV(0, j) = x0[j];
+      ORD(0) = 0;
+    }
+    st = NMQ_DONE;
+  }
+  __syncwarp();
+  while (!__all_sync(0xffffffffu, st == NMQ_DONE)) {
+    double f;
+    {
+      // this lane's point: vertex / transformation / shrink point / best vertex
+      double x[NM_NMAX];
+      if (st == NMQ_INIT) {
+        const int v = k + q <= n ? k + q : 0;
+#pragma unroll
+        for (int j = 0; j < NM_NMAX; ++j)
+          if (j < n) x[j] = x0_coord(v, j);
+      } else if (st == NMQ_ITER) {
+        double ca, cb;
+        coefs(q, ca, cb);
+#pragma unroll
+        for (int j = 0; j < NM_NMAX; ++j)
+          if (j < n) x[j] = Ar(Mr(ca, XB(j)), Mr(cb, SV(sn, j)));
+      } else if (st == NMQ_SHRINK) {
+        const int sk = ORD(k + q <= n ? k + q : 0);
+#pragma unroll
+        for (int j = 0; j < NM_NMAX; ++j)
+          if (j < n) { const double v0 = SV(s0, j); x[j] = Ar(v0, Mr(sigma, Sr(SV(sk, j), v0))); }
+      } else {
+        const int sb = ORD(0);
+#pragma unroll
+        for (int j = 0; j < NM_NMAX; ++j)
+          if (j < n) x[j] = SV(sb, j);
+      }
+      if (OBJ == 3) {
+        f = test_objective(a.fn_id, n, x);
+      } else {
+        double p[NP];
+#pragma unroll
+        for (int d = 0; d < NP; ++d) p[d] = x[d];
+        __syncwarp();
+        if (OBJ == 2) {
+          f = ref_objective(p, reinterpret_cast<const double*>(rel), a.ctl.n_steps, a.ctl.dt_ms,
+                            Aprime, pwd, METRIC, a.ctl.substeps, NMQ_P);
+        } else {
+          f = evaluate<T, (OBJ == 4 ? 2 : OBJ), METRIC, false, double, NMQ_P>(
+              p, a.ctl, Aprime, pwd, reinterpret_cast<const T*>(rel), nullptr, 0, sgn, nullptr,
+              stash, true, 32);
+        }
+      }
+      if (isnan(f)) f = __longlong_as_double(0x7ff0000000000000LL);
+    }
+    // the group's four values (full-warp shuffles, before any group branch)
+    const double fq0 = __shfl_sync(0xffffffffu, f, g * NMQ_G + 0);
+    const double fq1 = __shfl_sync(0xffffffffu, f, g * NMQ_G + 1);
+    const double fq2 = __shfl_sync(0xffffffffu, f, g * NMQ_G + 2);
+    const double fq3 = __shfl_sync(0xffffffffu, f, g * NMQ_G + 3);
+    if (st == NMQ_DONE) continue;
+    if (st == NMQ_INIT || st == NMQ_SHRINK) {
+      // store this lane's point (rebuilt bit-identically) into its slot
+      const int pos = k + q;
+      const int m = n + 1 - k < NMQ_G ? n + 1 - k : NMQ_G;   // points this step
+      gpu_evals += m;
+      if (pos <= n) {
+        const int slot = st == NMQ_INIT ? pos : ORD(pos);
+        if (st == NMQ_INIT) {
+          for (int j = 0; j < n; ++j) SV(slot, j) = x0_coord(pos, j);
+          ORD(pos) = pos;
+        } else {
+          for (int j = 0; j < n; ++j) {
+            const double v0 = SV(s0, j);
+            SV(slot, j) = Ar(v0, Mr(sigma, Sr(SV(slot, j), v0)));
+          }
+        }
+        FS(slot) = f;
+      }
+      k += NMQ_G;
+      if (k > n) {
+        const bool shrink = st == NMQ_SHRINK;
+        if (shrink) { evals += n; ++it; }
+        __syncwarp(gmask);
+        if (q == 0) sort_all();
+        __syncwarp(gmask);
+        begin_iteration();
+      }
+      continue;
+    }
+    // NMQ_ITER: the Lagarias decision on (fr, fe, fc, fcc)
+    gpu_evals += NMQ_G;
+    const double fr = fq0;
+    int take;   // 0..3 = point replacing vertex n; -1 = shrink
+    double ftake = fr;
+    if (fr < f0) {
+      evals += 2;
+      take = fq1 < fr ? 1 : 0;
+      ftake = take == 1 ? fq1 : fr;
+    } else if (fr < fn1) {
+      evals += 1;
+      take = 0;
+    } else if (fr < fnn) {
+      evals += 2;
+      take = fq2 <= fr ? 2 : -1;
+      ftake = fq2;
+    } else {
+      evals += 2;
+      take = fq3 < fnn ? 3 : -1;
+      ftake = fq3;
+    }
+    if (take < 0) { st = NMQ_SHRINK; k = 1; continue; }
+    {
+      double ca, cb;
+      coefs(take, ca, cb);
+      for (int j = q; j < n; j += NMQ_G) SV(sn, j) = Ar(Mr(ca, XB(j)), Mr(cb, SV(sn, j)));
+    }
+    __syncwarp(gmask);
+    if (q == 0) {   // vertex n replaced: stable re-rank of position n
+      FS(sn) = ftake;
+      int r = n - 1;
+      while (r >= 0 && FS(ORD(r)) > ftake) { ORD(r + 1) = ORD(r); --r; }
+      ORD(r + 1) = sn;
+    }
+    __syncwarp(gmask);
+    ++it;
+    begin_iteration();
+  }
+  __syncwarp();
+  if (live) {
+    const int sb = ORD(0);
+    for (int j = q; j < n; j += NMQ_G) a.x_best[prob * (int64_t)a.x_ld + j] = SV(sb, j);
+    if (q == 0) {
+      NmOut o;
+      o.f_best = FS(sb);
+      o.iterations = it;
+      o.func_evals = evals;
+      o.gpu_evals = gpu_evals;
+      o.exit_reason = reason;
+      a.out[prob] = o;
+    }
+  }
+#undef SV
+#undef FS
+#undef XB
+#undef ORD
+}
+
+template <typename T, int OBJ, int METRIC, bool GREL = false>
+static const void* nmg_fn() { return reinterpret_cast<const void*>(&nm_group_kernel<T, OBJ, METRIC, GREL>); }
+
+template <bool G>
+static const void* nmg_ptr(int precision, int obj, int metric) {
+  if (obj == 3) return nmg_fn<double, 3, 0, false>();
+  if (obj == 2) return metric == 0 ? nmg_fn<double, 2, 0, G>() : nmg_fn<double, 2, 1, G>();
+  if (obj == 4) {
+    if (precision == 0) return metric == 0 ? nmg_fn<double, 4, 0, G>() : nmg_fn<double, 4, 1, G>();
+    return metric == 0 ? nmg_fn<float, 4, 0, G>() : nmg_fn<float, 4, 1, G>();
+  }
+  if (precision == 0) {
+    if (obj == 0) return metric == 0 ? nmg_fn<double, 0, 0, G>() : nmg_fn<double, 0, 1, G>();
+    return metric == 0 ? nmg_fn<double, 1, 0, G>() : nmg_fn<double, 1, 1, G>();
+  }
+  if (obj == 0) return metric == 0 ? nmg_fn<float, 0, 0, G>() : nmg_fn<float, 0, 1, G>();
+  return metric == 0 ? nmg_fn<float, 1, 0, G>() : nmg_fn<float, 1, 1, G>();
+}
+
+const void* nm_group_kernel_ptr(int precision, int obj, int metric, bool rel_global) {
+  return rel_global ? nmg_ptr<true>(precision, obj, metric) : nmg_ptr<false>(precision, obj, metric);
+}
+
+size_t nm_group_smem(int precision, int obj, int32_t n_samples, bool rel_in_smem) {
+  const bool f32 = precision != 0 && obj != 2 && obj != 3;
+  size_t b = nmq_fixed_bytes();
+  if (obj == 0 || obj == 1 || obj == 4) b += f32 ? stash_bytes<float>(32) : stash_bytes<double>(32);
+  if (rel_in_smem && obj != 3) b += (size_t)n_samples * NMQ_P * (f32 ? sizeof(float) : sizeof(double));
+  return b;
+}
+
+int nm_group_problems_per_block() { return NMQ_P; }
+
 // rel_global: the instantiation that reads the trace from the global workspace
 const void* nm_kernel_ptr(int precision, int obj, int metric, bool rel_global) {
   return rel_global ? nm_ptr<true>(precision, obj, metric) : nm_ptr<false>(precision, obj, metric);

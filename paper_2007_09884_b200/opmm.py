@@ -87,7 +87,7 @@ class NmResult(C.Structure):
 
 
 NM_OBJ_PROPAGATOR, NM_OBJ_RK4_STAGES, NM_OBJ_REFERENCE = 0, 1, 2
-NM_SCHEDULE_AUTO, NM_SCHEDULE_LOCKSTEP, NM_SCHEDULE_LANE = 0, 1, 2
+NM_SCHEDULE_AUTO, NM_SCHEDULE_LOCKSTEP, NM_SCHEDULE_LANE, NM_SCHEDULE_GROUP = 0, 1, 2, 3
 NM_SPHERE, NM_ROSENBROCK, NM_POWELL = 0, 1, 2
 
 
@@ -395,7 +395,7 @@ def opmm_fit_batch(h: Handle, recorded, ctls, space, n_per: int,
 # ---------------------------------------------------------------------- Nelder-Mead
 def nm_options(precision=FP64, objective=NM_OBJ_PROPAGATOR, metric=METRIC_L1, max_iter=0, tol_x=0.0,
                tol_f=0.0, init_scale=0.0, cpu_check=1, schedule=0) -> NmOptions:
-    """schedule: NM_SCHEDULE_AUTO / NM_SCHEDULE_LOCKSTEP / NM_SCHEDULE_LANE (opmm.h)."""
+    """schedule: NM_SCHEDULE_AUTO / _LOCKSTEP / _LANE / _GROUP (opmm.h)."""
     return NmOptions(precision, objective, metric, max_iter, tol_x, tol_f, init_scale, cpu_check,
                      schedule)
 

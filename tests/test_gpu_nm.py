@@ -37,7 +37,7 @@ def h(opmm):
         yield handle
 
 
-SCHEDULES = pytest.mark.parametrize("schedule", [1, 2], ids=["lockstep", "lane"])
+SCHEDULES = pytest.mark.parametrize("schedule", [1, 2, 3], ids=["lockstep", "lane", "group"])
 
 
 @SCHEDULES
@@ -47,8 +47,14 @@ def test_rosenbrock_published_run_bit_exact(opmm, h, schedule):
     o = oracle.nm_test(oracle.NM_ROSENBROCK, [-1.2, 1.0])
     assert (r["iterations"], r["func_evals"]) == (85, 159) == (o["iterations"], o["func_evals"])
     assert r["x"].tolist() == o["x"].tolist() and r["f"] == o["f"]
-    # lock-step: every iteration evaluates n + 4 points; lane: only the needed ones
-    assert r["gpu_evals"] == (3 + 84 * 6 if schedule == 1 else 159)
+    # lock-step: every iteration evaluates n + 4 points; lane: only the needed
+    # ones; group: the four transformation points (and n per shrink)
+    if schedule == 1:
+        assert r["gpu_evals"] == 3 + 84 * 6
+    elif schedule == 2:
+        assert r["gpu_evals"] == 159
+    else:
+        assert r["gpu_evals"] >= 3 + 84 * 4 and (r["gpu_evals"] - 3 - 84 * 4) % 2 == 0
 
 
 @SCHEDULES
@@ -113,7 +119,12 @@ def test_plant_fast_objective_roundtrip(opmm, h, precision, schedule):
     for r, rec, c in zip(res, recs, ctls):
         assert abs(r["cpu_check"] - r["f"]) <= tol * max(r["f"], 1.0)
         assert r["f"] <= oracle.objective(W.truth_opc(), rec, c)   # never worse than the start
-        assert r["gpu_evals"] == (19 + (r["iterations"] - 1) * 22 if schedule == 1 else r["func_evals"])
+        if schedule == 1:
+            assert r["gpu_evals"] == 19 + (r["iterations"] - 1) * 22
+        elif schedule == 2:
+            assert r["gpu_evals"] == r["func_evals"]
+        else:
+            assert (r["gpu_evals"] - 19 - (r["iterations"] - 1) * 4) % 18 == 0
 
 
 @pytest.mark.parametrize("precision", [0, 1])
@@ -121,40 +132,43 @@ def test_schedules_identical_with_fast_objective(opmm, h, precision):
     """Both schedules run the same evaluator arithmetic and the same serial
     decisions, so with the propagator objective their results are identical
     bit for bit (70 problems: two full warps of the lane schedule and a
-    ragged third)."""
-    ctls, recs, _ = _roundtrip_set(70, seed=13)
+    ragged third; 8 full groups-of-8 blocks and a ragged one)."""
+    ctls, recs, _ = _roundtrip_set(70, seed=13)   # 70 = 2*32 + 6 = 8*8 + 6
     runs = [opmm.opmm_estimate_batch(h, recs, ctls,
                                      options=opmm.nm_options(precision=precision, schedule=sc,
                                                              cpu_check=0))
-            for sc in (1, 2)]
+            for sc in (1, 2, 3)]
     for s in range(len(ctls)):
-        a, b = runs[0][s], runs[1][s]
+        a, b, c = runs[0][s], runs[1][s], runs[2][s]
         for key in ("f", "iterations", "func_evals", "exit_reason"):
-            assert a[key] == b[key], (s, key)
-        assert a["x"].tolist() == b["x"].tolist(), s
+            assert a[key] == b[key] == c[key], (s, key)
+        assert a["x"].tolist() == b["x"].tolist() == c["x"].tolist(), s
         assert b["gpu_evals"] == b["func_evals"]
 
 
-def test_auto_schedule_switches_at_2048_problems(opmm, h):
-    """AUTO: lock-step below 2048 problems, lane from 2048 on (the measured
-    crossover); the lane runs at 2048 equal the oracle's serial runs."""
+def test_auto_schedule_switches_at_1024_problems(opmm, h):
+    """AUTO: lock-step below 1024 problems, group from 1024 on (the measured
+    crossover); both equal the oracle's serial runs."""
     rng = np.random.default_rng(5)
-    x0 = rng.uniform(-2, 2, size=(2048, 3))
+    x0 = rng.uniform(-2, 2, size=(1024, 3))
     opts = opmm.nm_options(tol_x=1e-7, tol_f=1e-9, max_iter=600)
-    small = opmm.opmm_nm_minimize_test(h, opmm.NM_SPHERE, x0[:2047], opts)
+    small = opmm.opmm_nm_minimize_test(h, opmm.NM_SPHERE, x0[:1023], opts)
     big = opmm.opmm_nm_minimize_test(h, opmm.NM_SPHERE, x0, opts)
-    assert all(r["gpu_evals"] == 4 + (r["iterations"] - 1) * 7 for r in small)   # n + 4 per iteration
-    assert all(r["gpu_evals"] == r["func_evals"] for r in big)
-    for s in range(0, 2048, 97):
+    # lock-step: n + 4 points per iteration; group: 4 per iteration + n per shrink
+    assert all(r["gpu_evals"] == 4 + (r["iterations"] - 1) * 7 for r in small)
+    assert all((r["gpu_evals"] - 4 - (r["iterations"] - 1) * 4) % 3 == 0 for r in big)
+    assert any(r["gpu_evals"] != 4 + (r["iterations"] - 1) * 7 for r in big)
+    for s in range(0, 1024, 41):
         o = oracle.nm_test(opmm.NM_SPHERE, x0[s], tol_x=1e-7, tol_f=1e-9, max_iter=600)
         assert big[s]["x"].tolist() == o["x"].tolist() and big[s]["f"] == o["f"], s
         assert small[s]["x"].tolist() == o["x"].tolist(), s
 
 
+
 def test_schedule_option_validated(opmm, h):
     ctls, recs, _ = _roundtrip_set(1)
     with pytest.raises(opmm.OpmmError):
-        opmm.opmm_estimate_batch(h, recs, ctls, options=opmm.nm_options(schedule=3))
+        opmm.opmm_estimate_batch(h, recs, ctls, options=opmm.nm_options(schedule=4))
 
 
 @SCHEDULES

@@ -805,7 +805,7 @@ def test_fit_substeps_matches_oracle(opmm, h, precision):
     assert abs(r["cpu_check"] - o["best_err"]) <= 1e-9 * o["best_err"] or precision == 1
 
 
-@pytest.mark.parametrize("schedule", [1, 2], ids=["lockstep", "lane"])
+@pytest.mark.parametrize("schedule", [1, 2, 3], ids=["lockstep", "lane", "group"])
 def test_nm_substeps_reference_bit_identical(opmm, h, schedule):
     """The reference-order NM objective with substeps is bit-identical to the
     oracle's serial Nelder-Mead with substeps, in both NM schedules; the
@@ -822,8 +822,9 @@ def test_nm_substeps_reference_bit_identical(opmm, h, schedule):
     assert np.array_equal(np.array(res[0]["x"]), o["x"][0])
     fast = [opmm.opmm_estimate_batch(h, rec[None, :], [ctl],
                                      options=opmm.nm_options(max_iter=60, cpu_check=0, schedule=sc))[0]
-            for sc in (1, 2)]
-    assert fast[0]["f"] == fast[1]["f"] and fast[0]["x"].tolist() == fast[1]["x"].tolist()
+            for sc in (1, 2, 3)]
+    assert fast[0]["f"] == fast[1]["f"] == fast[2]["f"]
+    assert fast[0]["x"].tolist() == fast[1]["x"].tolist() == fast[2]["x"].tolist()
 
 
 def test_sync_fit_graph_replay_and_invalidation(opmm, h):

@@ -761,27 +761,51 @@ __global__ void __launch_bounds__(32) nm_group_kernel(NmArgs a) {
       ORD(r + 1) = key;
     }
   };
-  // all 4 lanes of the group, group-uniform control flow
+  // all 4 lanes of the group, group-uniform control flow.  The sorted order
+  // is read once into registers so every vertex load below is independent
+  // (a few warps per SM leave shared-memory latency exposed otherwise); the
+  // f test runs first and the coordinate test only when it passes (the exit
+  // needs both).
   auto begin_iteration = [&]() {
     if (!(it < a.max_iter)) { st = NMQ_DONE; return; }
-    s0 = ORD(0);
-    bool ok = true;
+    int o[NML_NV];
+#pragma unroll
+    for (int p = 0; p < NML_NV; ++p) o[p] = p <= n ? ORD(p) : 0;
+    s0 = o[0];
     const double fb = FS(s0);
-    for (int p = 1 + q; p <= n; p += NMQ_G) ok &= fabs(FS(ORD(p)) - fb) <= a.tol_f;
-    for (int j = q; j < n; j += NMQ_G) {
-      const double v0 = SV(s0, j);
-      for (int p = 1; p <= n; ++p) ok &= fabs(SV(ORD(p), j) - v0) <= a.tol_x;
+    bool ok = true;
+#pragma unroll
+    for (int p = 1; p < NML_NV; ++p)
+      if (p <= n && (p & 3) == q) ok &= fabs(FS(o[p]) - fb) <= a.tol_f;
+    ok = __all_sync(gmask, ok);
+    if (ok) {
+#pragma unroll
+      for (int jj = 0; jj < (NM_NMAX + NMQ_G - 1) / NMQ_G; ++jj) {
+        const int j = q + NMQ_G * jj;
+        if (j < n) {
+          const double v0 = SV(s0, j);
+#pragma unroll
+          for (int p = 1; p < NML_NV; ++p)
+            if (p <= n) ok &= fabs(SV(o[p], j) - v0) <= a.tol_x;
+        }
+      }
+      if (__all_sync(gmask, ok)) { st = NMQ_DONE; reason = 0; return; }
     }
-    if (__all_sync(gmask, ok)) { st = NMQ_DONE; reason = 0; return; }
-    for (int j = q; j < n; j += NMQ_G) {   // centroid, summed in vertex order
-      double sum = 0.0;
-      for (int i = 0; i < n; ++i) sum = Ar(sum, SV(ORD(i), j));
-      XB(j) = Dr(sum, (double)n);
+#pragma unroll
+    for (int jj = 0; jj < (NM_NMAX + NMQ_G - 1) / NMQ_G; ++jj) {   // centroid, in vertex order
+      const int j = q + NMQ_G * jj;
+      if (j < n) {
+        double sum = 0.0;
+#pragma unroll
+        for (int i = 0; i < NM_NMAX; ++i)
+          if (i < n) sum = Ar(sum, SV(o[i], j));
+        XB(j) = Dr(sum, (double)n);
+      }
     }
     __syncwarp(gmask);
-    sn = ORD(n);
+    sn = o[n];
     f0 = fb;
-    fn1 = FS(ORD(n - 1));
+    fn1 = FS(o[n - 1]);
     fnn = FS(sn);
     st = NMQ_ITER;
   };
@@ -900,14 +924,29 @@ __global__ void __launch_bounds__(32) nm_group_kernel(NmArgs a) {
       coefs(take, ca, cb);
       for (int j = q; j < n; j += NMQ_G) SV(sn, j) = Ar(Mr(ca, XB(j)), Mr(cb, SV(sn, j)));
     }
-    __syncwarp(gmask);
-    if (q == 0) {   // vertex n replaced: stable re-rank of position n
-      FS(sn) = ftake;
-      int r = n - 1;
-      while (r >= 0 && FS(ORD(r)) > ftake) { ORD(r + 1) = ORD(r); --r; }
-      ORD(r + 1) = sn;
+    // vertex n replaced: stable re-rank of position n.  Positions 0..n-1 are
+    // sorted, so the new vertex goes after every f <= its own (equal values
+    // keep their order), i.e. at rank = #{r < n : f_r <= f_new}; the group
+    // counts in parallel and shifts positions rank..n-1 up by one.
+    {
+      int cnt = 0, keep[(NM_NMAX + NMQ_G - 1) / NMQ_G];
+#pragma unroll
+      for (int rr = 0; rr < (NM_NMAX + NMQ_G - 1) / NMQ_G; ++rr) {
+        const int r = q + NMQ_G * rr;
+        keep[rr] = r < n ? ORD(r) : 0;
+        if (r < n) cnt += FS(keep[rr]) <= ftake ? 1 : 0;
+      }
+      const int rank = __reduce_add_sync(gmask, cnt);
+      __syncwarp(gmask);
+#pragma unroll
+      for (int rr = 0; rr < (NM_NMAX + NMQ_G - 1) / NMQ_G; ++rr) {
+        const int r = q + NMQ_G * rr;
+        if (r < n && r >= rank) ORD(r + 1) = keep[rr];
+      }
+      __syncwarp(gmask);
+      if (q == 0) { FS(sn) = ftake; ORD(rank) = sn; }
+      __syncwarp(gmask);
     }
-    __syncwarp(gmask);
     ++it;
     begin_iteration();
   }

@@ -58,7 +58,7 @@ def test_rosenbrock_published_run_bit_exact(opmm, h, schedule):
 
 
 @SCHEDULES
-@pytest.mark.parametrize("fn,dim", [(0, 3), (1, 2), (1, 4), (2, 4)])
+@pytest.mark.parametrize("fn,dim", [(0, 1), (0, 3), (1, 2), (1, 4), (2, 4), (0, 18), (2, 16)])
 def test_test_functions_many_starts_bit_exact(opmm, h, fn, dim, schedule):
     rng = np.random.default_rng(fn * 10 + dim)
     x0 = rng.uniform(-2, 2, size=(40, dim))        # lane: one full warp + a ragged one

@@ -647,7 +647,7 @@ opmm_status nm_launch(opmm_handle* h, const NmConfig& c, const double* rec_dev,
   size_t smem = smem_for(true);
   // lane schedule with more warps than SMs: the trace goes to the global
   // workspace so that two warps fit per SM (the simplex alone is ~100 KB)
-  const bool lane_waves = lane && (n_blocks > h->num_sms || getenv("OPMM_NM_LANE_GREL") != nullptr);
+  const bool lane_waves = lane && n_blocks > h->num_sms;
   const bool rel_global = lane_waves || smem > max_dyn_smem(kernel_for(false));
   if (rel_global) {   // long traces: relativized per problem in global memory
     smem = smem_for(false);

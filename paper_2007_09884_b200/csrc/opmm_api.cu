@@ -96,6 +96,10 @@ constexpr int kDefaultBlock = OPMM_FIT_LB_THREADS;   // opmm_internal.h
 constexpr size_t kMaxDynSmem = 220 * 1024;
 // fit kernel picked by kernel_variant = 0 when variants 2/3 apply (1 otherwise)
 constexpr int kAutoVariant = 1;
+// kernel_variant = 0 picks the superposition kernel (variant 4) for eligible
+// grids with at least this many pulse-height levels
+constexpr bool kAutoSuper = false;
+constexpr int32_t kSuperMinLevels = 8;
 
 }  // namespace
 
@@ -416,6 +420,108 @@ struct FitLaunch {
   opmm::FitArgs a;
 };
 
+// Shared tail of every fit enqueue: the launch(es), then for world > 1 the
+// 32-byte all-gather and the merge kernel.
+opmm_status launch_fit_and_merge(opmm_handle* h, const void* fn, opmm::FitArgs& a, int grid,
+                                 int block, size_t smem, int64_t s_begin, int64_t S, bool multi,
+                                 opmm_fit_result* out_dev) {
+  CKS(record_start(h, h->stream));
+  for (int64_t s0 = 0; s0 < S; s0 += 65535) {
+    const int64_t sn = (S - s0) < 65535 ? (S - s0) : 65535;
+    a.sac_begin = s_begin + s0;
+    CK(opmm::launch_fit(fn, a, dim3(grid, (unsigned)sn), block, smem, h->stream));
+  }
+  CKS(record_stop(h, h->stream));
+  if (multi) {
+    // one exchange step: 32-byte (E, index, n_finite, n_evaluated) per rank
+    NcclApi& api = nccl();
+    for (int64_t s = 0; s < S; ++s) {
+      ncclResult_t r = api.allGather(h->rank_part + s_begin + s, h->gathered, sizeof(Partial),
+                                     ncclUint8, h->comm, h->stream);
+      if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather");
+      CK(opmm::launch_merge(h->gathered, h->world, a.space, (uint32_t)(s_begin + s), out_dev + s,
+                            h->exp_tab, h->stream));
+    }
+  }
+  return OPMM_OK;
+}
+
+// kernel_variant 4 (fit_super_kernel): the rank's share is a range of grid
+// nodes (every level of the superposed dimension stays on one rank), so the
+// union over ranks is still every candidate exactly once.
+opmm_status enqueue_fit_super(opmm_handle* h, const double* rec_dev, const opmm_control* ctl,
+                              const double* sacctl_dev, int64_t s_begin, int64_t S,
+                              const opmm_search_space* space, const opmm::SpaceDev& space_dev,
+                              int sup_dim, int64_t n_candidates, const opmm_fit_options* opts,
+                              opmm_fit_result* out_dev, bool shard, FitLaunch* prepare_only) {
+  const int metric = opts ? opts->metric : OPMM_METRIC_L1;
+  const int32_t L = space->levels[sup_dim];
+  int64_t st = 1;
+  for (int d = 0; d < sup_dim; ++d) st *= space->levels[d] > 1 ? space->levels[d] : 1;
+  const int64_t nodes = n_candidates / L;
+  int64_t nb = 0, ne = nodes;
+  if (shard) opmm_shard_range(nodes, h->rank, h->world, &nb, &ne);
+  const void* fn = opmm::fit_super_kernel_ptr(metric);
+  const int block = opmm::SUPER_BLOCK;
+  const size_t smem = opmm::super_smem(ctl->n_steps + 1, L, block);
+  int grid = 1;
+  CKS(grid_for(h, fn, block, smem, ne - nb, opts ? opts->grid_blocks : 0, &grid));
+  if (S > 1 && !(opts && opts->grid_blocks)) {
+    const int64_t tiles = (ne - nb + block - 1) / block;
+    grid = (int)(tiles < 65535 ? (tiles > 0 ? tiles : 1) : 65535);
+  }
+  if (ne <= nb) grid = 1;
+  const bool multi = shard && h->comm != nullptr;
+  CKS(ensure(h->partials, h->partials_cap, (size_t)grid * (size_t)(s_begin + S)));
+  CKS(ensure(h->counters, h->counters_cap, (size_t)(s_begin + S), true));
+  if (multi) {
+    CKS(ensure(h->rank_part, h->rank_part_cap, (size_t)(s_begin + S)));
+    CKS(ensure(h->gathered, h->gathered_cap, (size_t)h->world));
+  }
+  opmm::FitArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.rec = rec_dev;
+  a.exp_tab = h->exp_tab;
+  a.ctl = make_ctl(ctl);
+  a.space = space_dev;
+  a.amplitude = ctl->amplitude_deg;
+  a.pw_default = ctl->pw_default_ms;
+  a.sac_ctl = sacctl_dev;
+  a.sac_begin = s_begin;
+  a.begin = 0;                        // the epilogue's n_evaluated = end - begin
+  a.end = (ne - nb) * (int64_t)L;
+  a.err_out = opts ? opts->err_out : nullptr;
+  a.err_ld = n_candidates;
+  a.partials = h->partials;
+  a.counters = h->counters;
+  a.rank_out = multi ? h->rank_part : nullptr;
+  a.final_out = multi ? nullptr : out_dev;
+  a.out_base = s_begin;
+  a.sup_dim = sup_dim;
+  a.sup_L = L;
+  // chunk width: least padded slots over ceil(L / J) chunks, then the widest
+  int best_J = 32;
+  int64_t best_pad = INT64_MAX;
+  for (int J = 32; J >= 8; J -= 4) {
+    const int64_t pad = ((int64_t)L + J - 1) / J * J - L;
+    if (pad < best_pad) { best_pad = pad; best_J = J; }
+  }
+  a.sup_J = best_J;
+  a.sup_st = st;
+  a.node_begin = nb;
+  a.node_end = ne;
+  if (prepare_only && !multi && S == 1) {
+    prepare_only->fn = fn;
+    prepare_only->grid = grid;
+    prepare_only->block = block;
+    prepare_only->smem = smem;
+    prepare_only->a = a;
+    return OPMM_OK;
+  }
+  if (prepare_only) prepare_only->fn = nullptr;
+  return launch_fit_and_merge(h, fn, a, grid, block, smem, s_begin, S, multi, out_dev);
+}
+
 opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_control* ctl,
                         const double* sacctl_dev, int64_t s_begin, int64_t S,
                         const opmm_search_space* space, int64_t n_candidates,
@@ -428,8 +534,31 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
   if (!check_precision(precision)) return fail(OPMM_ERR_INVALID_ARG, "bad precision %d", precision);
   if (metric != 0 && metric != 1) return fail(OPMM_ERR_INVALID_ARG, "bad metric %d", metric);
   if (integ != 0 && integ != 1) return fail(OPMM_ERR_INVALID_ARG, "bad integrator %d", integ);
-  if (kv_opt < 0 || kv_opt > 3) return fail(OPMM_ERR_INVALID_ARG, "kernel_variant must be 0..3");
+  if (kv_opt < 0 || kv_opt > 4) return fail(OPMM_ERR_INVALID_ARG, "kernel_variant must be 0..4");
   const opmm::SpaceDev space_dev = make_space(space);
+  // variant 4: superposition over the grid levels of a pulse height (fp64
+  // propagator, 18-parameter grid, physical space)
+  int sup_dim = -1;
+  if (space->mode == 1 && space->model == 0) {
+    const int32_t la = space->levels[opmm::NSAC_AG], ln = space->levels[opmm::NSAC_ANT];
+    if (la > 1 || ln > 1) sup_dim = la >= ln ? opmm::NSAC_AG : opmm::NSAC_ANT;
+  }
+  const bool sup_ok = sup_dim >= 0 && precision == OPMM_FP64 && integ == OPMM_INTEG_PROPAGATOR &&
+                      ctl->substeps <= 1 && space_dev.all_physical && !(opts && opts->certify) &&
+                      !(opts && opts->block_size) && space->levels[sup_dim] <= opmm::SUPER_MAX_L &&
+                      opmm::super_smem(ctl->n_steps + 1, space->levels[sup_dim], opmm::SUPER_BLOCK) <=
+                          max_dyn_smem(opmm::fit_super_kernel_ptr(metric));
+  if (kv_opt == 4 && !sup_ok)
+    return fail(OPMM_ERR_UNSUPPORTED, "kernel_variant 4 needs a grid space (18-parameter model) "
+                                      "with N_SAC_AG or N_SAC_ANT levels > 1 (<= %d), all "
+                                      "candidates physical, FP64, the propagator, no substeps, "
+                                      "no certify, the default block size and a trace that fits "
+                                      "shared memory", opmm::SUPER_MAX_L);
+  const bool superpose = kv_opt == 4 || (kv_opt == 0 && sup_ok && kAutoSuper &&
+                                         space->levels[sup_dim] >= kSuperMinLevels);
+  if (superpose)
+    return enqueue_fit_super(h, rec_dev, ctl, sacctl_dev, s_begin, S, space, space_dev, sup_dim,
+                             n_candidates, opts, out_dev, shard, prepare_only);
   // variants 2/3 need the propagator integrator and a search space whose
   // candidates are all physical (no per-candidate penalty path)
   const bool special_ok = integ == OPMM_INTEG_PROPAGATOR && space_dev.all_physical &&
@@ -548,25 +677,7 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
     return OPMM_OK;
   }
   if (prepare_only) prepare_only->fn = nullptr;   // not graph-eligible: launched here
-  CKS(record_start(h, h->stream));
-  for (int64_t s0 = 0; s0 < S; s0 += 65535) {
-    const int64_t sn = (S - s0) < 65535 ? (S - s0) : 65535;
-    a.sac_begin = s_begin + s0;
-    CK(opmm::launch_fit(fn, a, dim3(grid, (unsigned)sn), block, smem, h->stream));
-  }
-  CKS(record_stop(h, h->stream));
-  if (multi) {
-    // one exchange step: 32-byte (E, index, n_finite, n_evaluated) per rank
-    NcclApi& api = nccl();
-    for (int64_t s = 0; s < S; ++s) {
-      ncclResult_t r = api.allGather(h->rank_part + s_begin + s, h->gathered, sizeof(Partial),
-                                     ncclUint8, h->comm, h->stream);
-      if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather");
-      CK(opmm::launch_merge(h->gathered, h->world, a.space, (uint32_t)(s_begin + s), out_dev + s,
-                            h->exp_tab, h->stream));
-    }
-  }
-  return OPMM_OK;
+  return launch_fit_and_merge(h, fn, a, grid, block, smem, s_begin, S, multi, out_dev);
 }
 
 opmm_status stage_rec(opmm_handle* h, const double* recorded, size_t count, const double** dev) {
@@ -759,6 +870,7 @@ opmm_status opmm_create(opmm_handle** out, int device) {
         allow_dyn_smem(opmm::simscore_kernel_ptr(p, i, m));
         allow_dyn_smem(opmm::fit2_kernel_ptr(p, m));
         allow_dyn_smem(opmm::fit3_kernel_ptr(p, m));
+        if (p == 0 && i == 0) allow_dyn_smem(opmm::fit_super_kernel_ptr(m));
         allow_dyn_smem(opmm::simulate_kernel_ptr(p, i));
         allow_dyn_smem(opmm::score_kernel_ptr(p, m));
         for (int obj = 0; obj < 5; ++obj)

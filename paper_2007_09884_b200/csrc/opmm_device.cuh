@@ -175,6 +175,34 @@ __device__ __forceinline__ void expand_9param(double p[NP]) {
 // independent dependency chains, so the scheduler can overlap them (the
 // generator is ~20% of a candidate's instructions).  Grid mode (int64 div/mod
 // per dimension) stays rolled to keep the kernel's code footprint small.
+// Grid mode of generate_opc (mixed-radix digits, dimension 0 fastest).
+__device__ __forceinline__ void generate_grid_opc(const SpaceDev& sp, int64_t idx, double p[NP],
+                                                  const double2* __restrict__ tab) {
+  uint64_t rem = (uint64_t)idx;
+#pragma unroll 1
+  for (int d = 0; d < NP; ++d) {
+    uint64_t digit = 0;
+    const uint64_t L = (uint64_t)sp.levels[d];
+    if (L > 1) {
+      digit = rem % L;
+      rem = rem / L;
+    }
+    double v;
+    if (sp.kind[d] == 0 || L <= 1) v = sp.lo[d];
+    else if (sp.kind[d] == 1) v = __dadd_rn(sp.lo[d], __dmul_rn((double)digit, sp.span[d]));
+    else {
+      const double x = __dmul_rn((double)digit, sp.span[d]);
+      v = __dmul_rn(sp.lo[d], sp.kind[d] == 2 ? exp_tab(x, tab) : exp_libm(x));
+    }
+    // static-index stores keep p[] in registers after the loop is unrolled
+    // by the caller's use; write through a switch-free select chain
+#pragma unroll
+    for (int e = 0; e < NP; ++e)
+      if (e == d) p[e] = v;
+  }
+  if (sp.model == 1) expand_9param(p);
+}
+
 __device__ __forceinline__ void generate_opc(const SpaceDev& sp, uint32_t saccade, int64_t idx,
                                              double p[NP], const double2* __restrict__ tab) {
   if (sp.mode == 0) {
@@ -206,29 +234,7 @@ __device__ __forceinline__ void generate_opc(const SpaceDev& sp, uint32_t saccad
     }
     if (sp.model == 1) expand_9param(p);
   } else {
-    uint64_t rem = (uint64_t)idx;
-#pragma unroll 1
-    for (int d = 0; d < NP; ++d) {
-      uint64_t digit = 0;
-      const uint64_t L = (uint64_t)sp.levels[d];
-      if (L > 1) {
-        digit = rem % L;
-        rem = rem / L;
-      }
-      double v;
-      if (sp.kind[d] == 0 || L <= 1) v = sp.lo[d];
-      else if (sp.kind[d] == 1) v = __dadd_rn(sp.lo[d], __dmul_rn((double)digit, sp.span[d]));
-      else {
-        const double x = __dmul_rn((double)digit, sp.span[d]);
-        v = __dmul_rn(sp.lo[d], sp.kind[d] == 2 ? exp_tab(x, tab) : exp_libm(x));
-      }
-      // static-index stores keep p[] in registers after the loop is unrolled
-      // by the caller's use; write through a switch-free select chain
-#pragma unroll
-      for (int e = 0; e < NP; ++e)
-        if (e == d) p[e] = v;
-    }
-    if (sp.model == 1) expand_9param(p);
+    generate_grid_opc(sp, idx, p, tab);
   }
 }
 
@@ -789,7 +795,11 @@ __device__ __forceinline__ double finish_error(T acc, int32_t n_samples) {
 template <typename T> struct LoopUnroll { static constexpr int value = 4; };
 template <> struct LoopUnroll<float> { static constexpr int value = 2; };
 
-template <typename T, int METRIC, bool TRAJ, bool STASHED = false, int RL = 1>
+// REGSTASH: the post-pulse coefficients stay in registers (pr.ph[1]) and no
+// stash is touched -- for kernels with registers to spare and no shared
+// memory to spare (fit_super_kernel).
+template <typename T, int METRIC, bool TRAJ, bool STASHED = false, int RL = 1,
+          bool REGSTASH = false>
 __device__ __forceinline__ T run_propagator(const Prop2<T>& pr, int32_t n_pulse, int32_t n_steps,
                                             const T* __restrict__ rel, T* __restrict__ traj,
                                             int64_t ld_out, T theta0, T sgn,
@@ -800,7 +810,7 @@ __device__ __forceinline__ T run_propagator(const Prop2<T>& pr, int32_t n_pulse,
   // P[0] stay in registers for the whole loop.  STASHED: make_prop already
   // wrote them.
   V2* st2 = reinterpret_cast<V2*>(stash) + threadIdx.x;
-  if (!STASHED) stash_phase<T>(pr.ph[1], st2, stash_ld);
+  if (!STASHED && !REGSTASH) stash_phase<T>(pr.ph[1], st2, stash_ld);
   const PhaseProp2<T>& q0 = pr.ph[0];
   T A00 = q0.X2[0][0], A01 = q0.X2[0][1], A10 = q0.X2[1][0], A11 = q0.X2[1][1];
   T A20 = q0.X2[2][0], A21 = q0.X2[2][1], A30 = q0.X2[3][0], A31 = q0.X2[3][1];
@@ -813,6 +823,15 @@ __device__ __forceinline__ T run_propagator(const Prop2<T>& pr, int32_t n_pulse,
   const T Q30 = pr.P2[3][0], Q31 = pr.P2[3][1], Q32 = pr.P2[3][2], Q33 = pr.P2[3][3];
   const T R0 = pr.P0[0], R1 = pr.P0[1], R2 = pr.P0[2], R3 = pr.P0[3];
   auto swap_in = [&]() {
+    if (REGSTASH) {
+      const PhaseProp2<T>& q1 = pr.ph[1];
+      A00 = q1.X2[0][0]; A01 = q1.X2[0][1]; A10 = q1.X2[1][0]; A11 = q1.X2[1][1];
+      A20 = q1.X2[2][0]; A21 = q1.X2[2][1]; A30 = q1.X2[3][0]; A31 = q1.X2[3][1];
+      c0 = q1.c2[0]; c1 = q1.c2[1]; c2 = q1.c2[2]; c3 = q1.c2[3];
+      pa = q1.pf2[0]; pn = q1.pf2[1]; qa = q1.qf2[0]; qn = q1.qf2[1];
+      x0a = q1.X0[0]; x0n = q1.X0[1]; d0 = q1.c0;
+      return;
+    }
     V2 v;
     v = st2[0 * stash_ld]; A00 = v.x; A01 = v.y;
     v = st2[1 * stash_ld]; A10 = v.x; A11 = v.y;

@@ -90,6 +90,13 @@ struct FitArgs {
   Partial* rank_out;        // optional [S]: per-rank result (world > 1)
   opmm_fit_result* final_out;  // optional: final result of saccade s at [s - out_base]
   int64_t out_base;
+  // kernel_variant 4 (fit_super_kernel): superposition over the grid levels of
+  // one pulse height; a "node" is a grid point with that dimension's digit 0
+  int32_t sup_dim;          // NSAC_AG (15) or NSAC_ANT (16)
+  int32_t sup_L;            // its grid levels
+  int32_t sup_J;            // register chunk width (8, 12, ..., 32)
+  int64_t sup_st;           // its mixed-radix stride (product of the lower levels)
+  int64_t node_begin, node_end;   // this rank's nodes
 };
 
 struct ExplicitArgs {
@@ -149,6 +156,11 @@ size_t nm_group_smem(int precision, int obj, int32_t n_samples, bool rel_in_smem
 int nm_group_problems_per_block();
 
 const void* fit_kernel_ptr(int precision, int integrator, int metric);
+// superposition over one pulse-height grid dimension (kernel_variant 4, fp64)
+const void* fit_super_kernel_ptr(int metric);
+constexpr int SUPER_BLOCK = 32;      // one warp per block: W/U columns are per warp
+constexpr int SUPER_MAX_L = 4096;    // levels of the superposed dimension
+size_t super_smem(int32_t n_samples, int32_t levels, int block);
 const void* fit2_kernel_ptr(int precision, int metric);   // 2 candidates/thread, 256 threads
 constexpr int FIT2_BLOCK = 256;
 const void* fit3_kernel_ptr(int precision, int metric);   // warp-specialised, 384 threads

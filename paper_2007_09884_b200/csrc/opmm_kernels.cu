@@ -419,6 +419,172 @@ __global__ void __launch_bounds__(OPMM_FIT_LB_THREADS, OPMM_FIT_LB_BLOCKS) fit_k
 }
 
 // ---------------------------------------------------------------------------
+// Superposition fit (kernel_variant 4).
+// The plant is linear and a pulse height N_SAC_d enters only through the
+// pulse-phase forcing, so the RK4 trajectory is affine in it:
+//   Delta-theta_k(a) = b_k + a u_k,
+// b = the trajectory with N_SAC_d = 0, u = the response to a unit pulse of
+// channel d from the zero deviation state (no post-pulse forcing) -- exact in
+// exact arithmetic, because the RK4 map of the LTI system is linear in
+// (state, forcing).  A grid node = every digit but d's.  Each lane owns one
+// node: it integrates b and u once (two propagator runs, trajectories into its
+// own shared-memory columns) and then scores all levels a_j of dimension d in
+// register chunks at two fp64 ops per sample:
+//   acc_j += |fma(a_j, u_k, b_k - rel_k)|      (L1; RMS: acc_j = fma(d, d, acc_j)).
+// A node whose b or u is large (non-finite, or S_b + max|a| S_u > SUPER_SAFE,
+// S = sum_k |.|) is evaluated directly, level by level, with fit_kernel's
+// evaluator: there cancellation could cost digits.  One warp per block (the
+// columns are per warp), post-pulse coefficients in registers (REGSTASH).
+// ---------------------------------------------------------------------------
+constexpr double SUPER_SAFE = 1e6;     // deg; bounds the combination's rounding
+
+__host__ __device__ constexpr size_t super_cols(int32_t ns) {
+  return (size_t)(2 * ns > 20 ? 2 * ns : 20);   // W + U rows, or evaluate's stash [10] x double2
+}
+
+// Score levels [0, L) of one node from its columns (Wc = b, Uc = u; stride B)
+// in register chunks of J levels.  The chunk width is a compile-time constant
+// so the inner loop is J unguarded (DFMA, DADD) pairs per sample; a partial
+// last chunk repeats level L-1 in its spare slots and records only its own.
+template <int METRIC, int J, typename Rec>
+__device__ __forceinline__ void super_levels(const double* __restrict__ Wc,
+                                             const double* __restrict__ Uc,
+                                             const double* __restrict__ rel,
+                                             const double* __restrict__ lv, int32_t ns, int B,
+                                             int L, int64_t ib, int64_t st, Rec& record) {
+  for (int j0 = 0; j0 < L; j0 += J) {
+    double av[J], acc[J];
+#pragma unroll
+    for (int jj = 0; jj < J; ++jj) {
+      av[jj] = lv[min(j0 + jj, L - 1)];
+      acc[jj] = 0.0;
+    }
+    // sample 0 contributes |0 - rel_0| = 0 (fit_kernel starts at k = 1 too)
+#pragma unroll 2
+    for (int32_t k = 1; k < ns; ++k) {
+      const double w = Wc[(size_t)k * B] - rel[k];
+      const double u = Uc[(size_t)k * B];
+#pragma unroll
+      for (int jj = 0; jj < J; ++jj) accumulate<METRIC>(acc[jj], fma(av[jj], u, w));
+    }
+    const int jn = min(J, L - j0);
+#pragma unroll
+    for (int jj = 0; jj < J; ++jj)
+      if (jj < jn) record(finish_error<METRIC>(acc[jj], ns), ib + (int64_t)(j0 + jj) * st);
+  }
+}
+
+// Direct evaluation of one node's levels (the lanes whose node is `bad`; all
+// lanes run the evaluator, whose segmented loop needs the full warp).  Out of
+// line, so its register peak stays out of the superposition loop's.
+template <int METRIC>
+__device__ __noinline__ void super_direct(const FitArgs& a, int64_t sac, int64_t ib, bool bad,
+                                          double Aprime, double pwd, double sgn,
+                                          const double* rel, double* stash, double& best_e,
+                                          int64_t& best_i, int64_t& nf) {
+  const double INF = __longlong_as_double(0x7ff0000000000000LL);
+  for (int j = 0; j < a.sup_L; ++j) {
+    const int64_t i = ib + (int64_t)j * a.sup_st;
+    double q[NP];
+    generate_grid_opc(a.space, i, q, a.exp_tab);
+    const double E = evaluate<double, 0, METRIC, false>(q, a.ctl, Aprime, pwd, rel, nullptr, 0,
+                                                        sgn, nullptr, stash, false, blockDim.x);
+    if (bad) {
+      if (a.err_out) a.err_out[sac * a.err_ld + i] = E;
+      nf += E < INF ? 1 : 0;
+      if (better(E, i, best_e, best_i)) { best_e = E; best_i = i; }
+    }
+  }
+}
+
+template <int METRIC>
+__global__ void __launch_bounds__(SUPER_BLOCK) fit_super_kernel(FitArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int32_t ns = a.ctl.n_steps + 1;
+  const int B = blockDim.x, tid = threadIdx.x;
+  const int L = a.sup_L;
+  const bool ag = a.sup_dim == NSAC_AG;
+  double* rel = reinterpret_cast<double*>(smem_raw);
+  double* lv = rel + ((ns + 1) & ~1);
+  double* W = lv + ((L + 1) & ~1);              // [ns][B]: b_k
+  double* U = W + (size_t)ns * B;               // [ns][B]: u_k
+  const int64_t sac = (int64_t)blockIdx.y + a.sac_begin;
+  const double amp = a.sac_ctl ? a.sac_ctl[2 * sac] : a.amplitude;
+  const double pwd = a.sac_ctl ? a.sac_ctl[2 * sac + 1] : a.pw_default;
+  double sgn, Aprime;
+  stage_trace<double>(a.rec + sac * (int64_t)ns, ns, amp, rel, sgn, Aprime);
+  // level values of dimension d: generate_opc's own arithmetic (digit j, others 0)
+  for (int j = tid; j < L; j += B) {
+    double q[NP];
+    generate_grid_opc(a.space, (int64_t)j * a.sup_st, q, a.exp_tab);
+    lv[j] = ag ? q[NSAC_AG] : q[NSAC_ANT];
+  }
+  __syncthreads();
+  const double INF = __longlong_as_double(0x7ff0000000000000LL);
+  const double amax = fmax(fabs(lv[0]), fabs(lv[L - 1]));   // levels are monotone in j
+  const int64_t st = a.sup_st, stL = a.sup_st * (int64_t)L;
+  const int64_t nn = a.node_end - a.node_begin;
+  double best_e = INF;
+  int64_t best_i = INT64_MAX;
+  int64_t nf = 0;
+  auto record = [&](double E, int64_t i) {
+    if (a.err_out) a.err_out[sac * a.err_ld + i] = E;
+    nf += E < INF ? 1 : 0;
+    if (better(E, i, best_e, best_i)) { best_e = E; best_i = i; }
+  };
+  // uniform trip count per warp: lanes past the end redo the last node and drop it
+  for (int64_t t0 = (int64_t)blockIdx.x * B; t0 < nn; t0 += (int64_t)gridDim.x * B) {
+    const bool valid = t0 + tid < nn;
+    const int64_t node = a.node_begin + (valid ? t0 + tid : nn - 1);
+    const int64_t ib = node / st * stL + node % st;   // index of the node's level 0
+    double p[NP];
+    generate_grid_opc(a.space, ib, p, a.exp_tab);   // grid spaces only (host)
+    Setup s;
+    make_setup(p, a.ctl.dt_ms, a.ctl.h, a.ctl.n_steps, Aprime, pwd, s);
+    const double F = p[NC_FIX];
+    double Sb, Su;
+    {  // b: N_SAC_d = 0 (n~ = 0 - F during the pulse)
+      Setup sb = s;
+      if (ag) sb.ph[0].nt_ag = -F; else sb.ph[0].nt_ant = -F;
+      Prop2<double> pr;
+      make_prop<double, false>(sb, pr);
+      Sb = run_propagator<double, 0, true, false, 1, true>(pr, s.n_pulse, a.ctl.n_steps, rel,
+                                                           W + tid, B, 0.0, 1.0, nullptr, 0);
+    }
+    {  // u: unit pulse on channel d, nothing else
+      Setup su = s;
+      su.ph[0].nt_ag = ag ? 1.0 : 0.0;
+      su.ph[0].nt_ant = ag ? 0.0 : 1.0;
+      su.ph[1].nt_ag = 0.0;
+      su.ph[1].nt_ant = 0.0;
+      Prop2<double> pr;
+      make_prop<double, false>(su, pr);
+      Su = run_propagator<double, 0, true, false, 1, true>(pr, s.n_pulse, a.ctl.n_steps, rel,
+                                                           U + tid, B, 0.0, 1.0, nullptr, 0);
+    }
+    const bool ok = Sb + amax * Su <= SUPER_SAFE;   // false for NaN / inf
+    if (ok && valid) {
+      switch (a.sup_J) {   // register chunk width (host: least padding for L)
+        case 8: super_levels<METRIC, 8>(W + tid, U + tid, rel, lv, ns, B, L, ib, st, record); break;
+        case 12: super_levels<METRIC, 12>(W + tid, U + tid, rel, lv, ns, B, L, ib, st, record); break;
+        case 16: super_levels<METRIC, 16>(W + tid, U + tid, rel, lv, ns, B, L, ib, st, record); break;
+        case 20: super_levels<METRIC, 20>(W + tid, U + tid, rel, lv, ns, B, L, ib, st, record); break;
+        case 24: super_levels<METRIC, 24>(W + tid, U + tid, rel, lv, ns, B, L, ib, st, record); break;
+        case 28: super_levels<METRIC, 28>(W + tid, U + tid, rel, lv, ns, B, L, ib, st, record); break;
+        default: super_levels<METRIC, 32>(W + tid, U + tid, rel, lv, ns, B, L, ib, st, record); break;
+      }
+    }
+    const bool bad = valid && !ok;
+    if (__any_sync(0xffffffffu, bad)) {
+      __syncwarp();   // the columns are dead now: the evaluator's stash reuses them
+      super_direct<METRIC>(a, sac, ib, bad, Aprime, pwd, sgn, rel, W, best_e, best_i, nf);
+    }
+    __syncwarp();   // the next node overwrites the columns
+  }
+  fit_epilogue(a, sac, best_e, best_i, nf);
+}
+
+// ---------------------------------------------------------------------------
 // The fused fit kernel, two candidates per thread (propagator integrator,
 // physical-by-construction search spaces).  256 threads x 255 registers, one
 // block per SM (2 warps per scheduler); each thread interleaves two
@@ -945,6 +1111,16 @@ const void* fit_kernel_ptr(int precision, int integrator, int metric) {
   if (integrator == 0) return metric == 0 ? fit_fn<float, 0, 0>() : fit_fn<float, 0, 1>();
   if (integrator == 2) return metric == 0 ? fit_fn<float, 2, 0>() : fit_fn<float, 2, 1>();
   return metric == 0 ? fit_fn<float, 1, 0>() : fit_fn<float, 1, 1>();
+}
+
+const void* fit_super_kernel_ptr(int metric) {
+  return metric == 0 ? reinterpret_cast<const void*>(&fit_super_kernel<0>)
+                     : reinterpret_cast<const void*>(&fit_super_kernel<1>);
+}
+
+size_t super_smem(int32_t ns, int32_t levels, int block) {
+  return ((size_t)((ns + 1) & ~1) + (size_t)((levels + 1) & ~1) + super_cols(ns) * block) *
+         sizeof(double);
 }
 
 cudaError_t launch_fit(const void* fn, const FitArgs& a, dim3 grid, int block, size_t smem,

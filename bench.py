@@ -279,6 +279,46 @@ def score_leg(h, opmm, torch, max_over_ranks, n=4 * 10**6, n_samples=101):
             "peak_basis": "MEASURED_PEAKS.json hbm_gbs (copy, read+write)"}
 
 
+def g4_leg(h, opmm, torch, max_over_ranks, reps=5):
+    """Config 4's planted grid G4: 100^4 = 10^8 candidates over
+    {K_SE_AG, B_AG, N_SAC_AG, PW}, sharded over the ranks.  The default fit
+    (kernel_variant 0) takes the superposition kernel here (100 N_SAC_AG
+    levels per node); the direct one-candidate-per-thread kernel
+    (variant 1) is timed beside it.  Both must return the planted index."""
+    ctl, sp = W.Control(), W.g4_space(100)
+    n = sp.n_grid()
+    rec_dev = torch.as_tensor(clean_trace(), dtype=torch.float64, device="cuda")
+    out = torch.zeros(ctypes.sizeof(opmm.FitResult), dtype=torch.uint8, device="cuda")
+    st = torch.cuda.ExternalStream(h.stream)
+    res = {}
+    for kv in (0, 1):
+        o = opmm.fit_options(cpu_check=0, kernel_variant=kv)
+        for _ in range(2):
+            opmm.opmm_fit_async(h, rec_dev, ctl, sp, n, out, o)
+        ms = []
+        for _ in range(reps):
+            opmm.opmm_fit_async(h, rec_dev, ctl, sp, n, out, o)
+            ms.append(opmm.opmm_last_kernel_ms(h))
+        st.synchronize()
+        r = opmm.decode_result(bytes(out.cpu().numpy()))
+        res[kv] = (max_over_ranks(statistics.median(ms)), r)
+    planted = W.g4_planted_index()
+    return {"metric": "OPC candidate sims/s (G4 planted grid)", "candidates": n,
+            "value": n / (res[0][0] * 1e-3), "kernel_ms": res[0][0],
+            "kernel": "fit_super_kernel<L1> (auto: superposition over 100 N_SAC_AG levels)",
+            "direct_kernel_ms": res[1][0], "direct_value": n / (res[1][0] * 1e-3),
+            "speedup_vs_direct": res[1][0] / res[0][0],
+            "best_index": res[0][1]["best_index"], "planted_index": planted,
+            "planted_found": res[0][1]["best_index"] == planted == res[1][1]["best_index"],
+            "opt_err": res[0][1]["opt_err"]}
+
+
+def clean_trace():
+    """G4 is scored against the clean TRUTH trace (the stored fixture, no noise)."""
+    return np.loadtxt(os.path.join(ROOT, "tests", "golden", "trace_truth_A10_dt1_n100.txt"),
+                      comments="#")
+
+
 def nm_leg(h, opmm, torch, args, max_over_ranks=lambda x: x, sum_over_ranks=lambda x: x):
     """The paper's own estimator (batched parallel Nelder-Mead)
     on a synthetic population (SURVEY 8(d) config 5 recipe: A ~ U[5, 30] deg,
@@ -417,6 +457,7 @@ def run_gpu(args):
 
     lat = latency_leg(h, opmm, torch, rec, world, max_over_ranks) if not args.no_latency else None
     score = score_leg(h, opmm, torch, max_over_ranks)
+    g4 = g4_leg(h, opmm, torch, max_over_ranks)
     nm = nm_leg(h, opmm, torch, args, max_over_ranks, sum_over_ranks) if not args.no_nm else None
     pop = population_leg(h, opmm, torch, args, max_over_ranks, world) if not args.no_pop else None
 
@@ -459,6 +500,7 @@ def run_gpu(args):
     if lat is not None:
         line["latency"] = lat
     line["score_hbm"] = score
+    line["g4_grid"] = g4
     if pop is not None:
         line["population"] = pop
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -98,7 +98,7 @@ constexpr size_t kMaxDynSmem = 220 * 1024;
 constexpr int kAutoVariant = 1;
 // kernel_variant = 0 picks the superposition kernel (variant 4) for eligible
 // grids with at least this many pulse-height levels
-constexpr bool kAutoSuper = false;
+constexpr bool kAutoSuper = true;
 constexpr int32_t kSuperMinLevels = 8;
 
 }  // namespace
@@ -463,7 +463,16 @@ opmm_status enqueue_fit_super(opmm_handle* h, const double* rec_dev, const opmm_
   if (shard) opmm_shard_range(nodes, h->rank, h->world, &nb, &ne);
   const void* fn = opmm::fit_super_kernel_ptr(metric);
   const int block = opmm::SUPER_BLOCK;
-  const size_t smem = opmm::super_smem(ctl->n_steps + 1, L, block);
+  int32_t gt_n = 0;
+  for (int d = 0; d < OPMM_NPARAM; ++d)
+    if (d != sup_dim) gt_n += space->levels[d] > 1 ? space->levels[d] : 0;
+  int32_t use_tab = 1;
+  if (gt_n > opmm::SUPER_MAX_GT ||
+      opmm::super_smem(ctl->n_steps + 1, L, gt_n, block) > max_dyn_smem(fn)) {
+    gt_n = 0;   // generic generator per node
+    use_tab = 0;
+  }
+  const size_t smem = opmm::super_smem(ctl->n_steps + 1, L, gt_n, block);
   int grid = 1;
   CKS(grid_for(h, fn, block, smem, ne - nb, opts ? opts->grid_blocks : 0, &grid));
   if (S > 1 && !(opts && opts->grid_blocks)) {
@@ -507,6 +516,8 @@ opmm_status enqueue_fit_super(opmm_handle* h, const double* rec_dev, const opmm_
     if (pad < best_pad) { best_pad = pad; best_J = J; }
   }
   a.sup_J = best_J;
+  a.sup_gt_n = gt_n;
+  a.sup_tab = use_tab;
   a.sup_st = st;
   a.node_begin = nb;
   a.node_end = ne;
@@ -546,7 +557,8 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
   const bool sup_ok = sup_dim >= 0 && precision == OPMM_FP64 && integ == OPMM_INTEG_PROPAGATOR &&
                       ctl->substeps <= 1 && space_dev.all_physical && !(opts && opts->certify) &&
                       !(opts && opts->block_size) && space->levels[sup_dim] <= opmm::SUPER_MAX_L &&
-                      opmm::super_smem(ctl->n_steps + 1, space->levels[sup_dim], opmm::SUPER_BLOCK) <=
+                      opmm::super_smem(ctl->n_steps + 1, space->levels[sup_dim], 0,
+                                       opmm::SUPER_BLOCK) <=
                           max_dyn_smem(opmm::fit_super_kernel_ptr(metric));
   if (kv_opt == 4 && !sup_ok)
     return fail(OPMM_ERR_UNSUPPORTED, "kernel_variant 4 needs a grid space (18-parameter model) "

@@ -926,6 +926,141 @@ __device__ __forceinline__ T run_propagator(const Prop2<T>& pr, int32_t n_pulse,
 }
 
 // ----------------------------------------------------------------------------
+// Superposition pair (fit_super_kernel): the trajectories b (pulse height 0)
+// and u (unit pulse of one channel) of ONE candidate, advanced together.  Both
+// use the same maps P2, P[0], X2, X[0], pf2 (they depend on the plant and the
+// time constants only); they differ in the forcing terms c2, c[0], qf2 and
+// the odd-start state, taken from their own Prop2 (pu's post-pulse forcing is
+// zero).  Each recurrence is exactly run_propagator's (same FMA order, so b
+// and u are bit-identical to two separate TRAJ runs); the pair gives the
+// scheduler 10 independent chains instead of 5.  Writes Wc[k B] = b_k,
+// Uc[k B] = u_k (k = 0..n_steps) and returns sum |b_k| and sum |u_k|.
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ void run_propagator_bu(const Prop2<double>& pb, const Prop2<double>& pu,
+                                                  int32_t n_pulse, int32_t n_steps,
+                                                  double* __restrict__ Wc,
+                                                  double* __restrict__ Uc, int B, double& Sb,
+                                                  double& Su) {
+  const PhaseProp2<double>& q0 = pb.ph[0];
+  double A00 = q0.X2[0][0], A01 = q0.X2[0][1], A10 = q0.X2[1][0], A11 = q0.X2[1][1];
+  double A20 = q0.X2[2][0], A21 = q0.X2[2][1], A30 = q0.X2[3][0], A31 = q0.X2[3][1];
+  double pa = q0.pf2[0], pn = q0.pf2[1];
+  double x0a = q0.X0[0], x0n = q0.X0[1];
+  // forcing of b and of u
+  double c0 = q0.c2[0], c1 = q0.c2[1], c2 = q0.c2[2], c3 = q0.c2[3];
+  double qa = q0.qf2[0], qn = q0.qf2[1], d0 = q0.c0;
+  const PhaseProp2<double>& r0 = pu.ph[0];
+  double e0 = r0.c2[0], e1 = r0.c2[1], e2 = r0.c2[2], e3 = r0.c2[3];
+  double ra = r0.qf2[0], rn = r0.qf2[1], g0 = r0.c0;
+  const double Q00 = pb.P2[0][0], Q01 = pb.P2[0][1], Q02 = pb.P2[0][2], Q03 = pb.P2[0][3];
+  const double Q10 = pb.P2[1][0], Q11 = pb.P2[1][1], Q12 = pb.P2[1][2], Q13 = pb.P2[1][3];
+  const double Q20 = pb.P2[2][0], Q21 = pb.P2[2][1], Q22 = pb.P2[2][2], Q23 = pb.P2[2][3];
+  const double Q30 = pb.P2[3][0], Q31 = pb.P2[3][1], Q32 = pb.P2[3][2], Q33 = pb.P2[3][3];
+  const double R0 = pb.P0[0], R1 = pb.P0[1], R2 = pb.P0[2], R3 = pb.P0[3];
+  auto swap_in = [&]() {
+    const PhaseProp2<double>& q1 = pb.ph[1];
+    A00 = q1.X2[0][0]; A01 = q1.X2[0][1]; A10 = q1.X2[1][0]; A11 = q1.X2[1][1];
+    A20 = q1.X2[2][0]; A21 = q1.X2[2][1]; A30 = q1.X2[3][0]; A31 = q1.X2[3][1];
+    pa = q1.pf2[0]; pn = q1.pf2[1];
+    x0a = q1.X0[0]; x0n = q1.X0[1];
+    c0 = q1.c2[0]; c1 = q1.c2[1]; c2 = q1.c2[2]; c3 = q1.c2[3];
+    qa = q1.qf2[0]; qn = q1.qf2[1]; d0 = q1.c0;
+    const PhaseProp2<double>& r1 = pu.ph[1];
+    e0 = r1.c2[0]; e1 = r1.c2[1]; e2 = r1.c2[2]; e3 = r1.c2[3];
+    ra = r1.qf2[0]; rn = r1.qf2[1]; g0 = r1.c0;
+  };
+  const bool switches = n_pulse > 0 && n_pulse <= n_steps;
+  const int32_t o = switches ? (n_pulse & 1) : 0;
+  double th = 0.0, om = 0.0, xa = 0.0, xn = 0.0, fa = 0.0, fn = 0.0;
+  double uth = 0.0, uom = 0.0, uxa = 0.0, uxn = 0.0, ufa = 0.0, ufn = 0.0;
+  double sb = 0.0, su = 0.0;
+  Wc[0] = 0.0;
+  Uc[0] = 0.0;
+  if (n_pulse == 0) swap_in();
+  if (o) {
+    th = pb.z1[0]; om = pb.z1[1]; xa = pb.z1[2]; xn = pb.z1[3]; fa = pb.f1[0]; fn = pb.f1[1];
+    uth = pu.z1[0]; uom = pu.z1[1]; uxa = pu.z1[2]; uxn = pu.z1[3]; ufa = pu.f1[0]; ufn = pu.f1[1];
+    sb += fabs(th);
+    su += fabs(uth);
+    Wc[B] = th;
+    Uc[B] = uth;
+  }
+  const int32_t nb = (n_steps + 1) / 2;
+  const int32_t bs = switches ? (n_pulse - o) / 2 : nb;
+  if (switches && bs == 0) swap_in();
+  double* __restrict__ wr = Wc + (int64_t)o * B;
+  double* __restrict__ ur = Uc + (int64_t)o * B;
+  int32_t b = 0;
+  while (b < nb - 1) {
+    const int32_t mine = bs > b ? min(bs, nb - 1) : nb - 1;
+    const int32_t seg_end = __reduce_min_sync(0xffffffffu, mine);
+#pragma unroll 2
+    for (; b < seg_end; ++b) {
+      double t1 = fma(x0n, fn, d0), nth = fma(A01, fn, c0), nom = fma(A11, fn, c1);
+      double nxa = fma(A21, fn, c2), nxn = fma(A31, fn, c3);
+      double v1 = fma(x0n, ufn, g0), vth = fma(A01, ufn, e0), vom = fma(A11, ufn, e1);
+      double vxa = fma(A21, ufn, e2), vxn = fma(A31, ufn, e3);
+      t1 = fma(x0a, fa, t1); nth = fma(A00, fa, nth); nom = fma(A10, fa, nom);
+      nxa = fma(A20, fa, nxa); nxn = fma(A30, fa, nxn);
+      v1 = fma(x0a, ufa, v1); vth = fma(A00, ufa, vth); vom = fma(A10, ufa, vom);
+      vxa = fma(A20, ufa, vxa); vxn = fma(A30, ufa, vxn);
+      fa = fma(pa, fa, qa);
+      fn = fma(pn, fn, qn);
+      ufa = fma(pa, ufa, ra);
+      ufn = fma(pn, ufn, rn);
+      t1 = fma(R3, xn, t1); nth = fma(Q03, xn, nth); nom = fma(Q13, xn, nom);
+      nxa = fma(Q23, xn, nxa); nxn = fma(Q33, xn, nxn);
+      v1 = fma(R3, uxn, v1); vth = fma(Q03, uxn, vth); vom = fma(Q13, uxn, vom);
+      vxa = fma(Q23, uxn, vxa); vxn = fma(Q33, uxn, vxn);
+      t1 = fma(R2, xa, t1); nth = fma(Q02, xa, nth); nom = fma(Q12, xa, nom);
+      nxa = fma(Q22, xa, nxa); nxn = fma(Q32, xa, nxn);
+      v1 = fma(R2, uxa, v1); vth = fma(Q02, uxa, vth); vom = fma(Q12, uxa, vom);
+      vxa = fma(Q22, uxa, vxa); vxn = fma(Q32, uxa, vxn);
+      t1 = fma(R1, om, t1); nth = fma(Q01, om, nth); nom = fma(Q11, om, nom);
+      nxa = fma(Q21, om, nxa); nxn = fma(Q31, om, nxn);
+      v1 = fma(R1, uom, v1); vth = fma(Q01, uom, vth); vom = fma(Q11, uom, vom);
+      vxa = fma(Q21, uom, vxa); vxn = fma(Q31, uom, vxn);
+      t1 = fma(R0, th, t1); nth = fma(Q00, th, nth); nom = fma(Q10, th, nom);
+      nxa = fma(Q20, th, nxa); nxn = fma(Q30, th, nxn);
+      v1 = fma(R0, uth, v1); vth = fma(Q00, uth, vth); vom = fma(Q10, uth, vom);
+      vxa = fma(Q20, uth, vxa); vxn = fma(Q30, uth, vxn);
+      th = nth; om = nom; xa = nxa; xn = nxn;
+      uth = vth; uom = vom; uxa = vxa; uxn = vxn;
+      sb += fabs(t1);
+      sb += fabs(th);
+      su += fabs(v1);
+      su += fabs(uth);
+      wr[(int64_t)(2 * b + 1) * B] = t1;
+      wr[(int64_t)(2 * b + 2) * B] = th;
+      ur[(int64_t)(2 * b + 1) * B] = v1;
+      ur[(int64_t)(2 * b + 2) * B] = uth;
+    }
+    if (b == bs) swap_in();
+  }
+  if (nb >= 1) {
+    const int32_t k1 = o + 2 * b + 1;
+    const double t1 = fma(R0, th, fma(R1, om, fma(R2, xa, fma(R3, xn, fma(x0a, fa, fma(x0n, fn, d0))))));
+    const double t2 = fma(Q00, th, fma(Q01, om, fma(Q02, xa, fma(Q03, xn, fma(A00, fa, fma(A01, fn, c0))))));
+    const double v1 = fma(R0, uth, fma(R1, uom, fma(R2, uxa, fma(R3, uxn, fma(x0a, ufa, fma(x0n, ufn, g0))))));
+    const double v2 = fma(Q00, uth, fma(Q01, uom, fma(Q02, uxa, fma(Q03, uxn, fma(A00, ufa, fma(A01, ufn, e0))))));
+    if (k1 <= n_steps) {
+      sb += fabs(t1);
+      su += fabs(v1);
+      Wc[(int64_t)k1 * B] = t1;
+      Uc[(int64_t)k1 * B] = v1;
+    }
+    if (k1 + 1 <= n_steps) {
+      sb += fabs(t2);
+      su += fabs(v2);
+      Wc[(int64_t)(k1 + 1) * B] = t2;
+      Uc[(int64_t)(k1 + 1) * B] = v2;
+    }
+  }
+  Sb = sb;
+  Su = su;
+}
+
+// ----------------------------------------------------------------------------
 // Fit mode, C candidates per thread (C = 2): the same two-step recurrence as
 // run_propagator for C independent candidates interleaved in one thread, so
 // the scheduler sees 5C independent FMA chains per block (the fit kernel runs

@@ -95,6 +95,8 @@ struct FitArgs {
   int32_t sup_dim;          // NSAC_AG (15) or NSAC_ANT (16)
   int32_t sup_L;            // its grid levels
   int32_t sup_J;            // register chunk width (8, 12, ..., 32)
+  int32_t sup_gt_n;         // entries of the per-dimension level tables
+  int32_t sup_tab;          // 1: nodes from the tables; 0: generic generator (too many levels)
   int64_t sup_st;           // its mixed-radix stride (product of the lower levels)
   int64_t node_begin, node_end;   // this rank's nodes
 };
@@ -160,7 +162,8 @@ const void* fit_kernel_ptr(int precision, int integrator, int metric);
 const void* fit_super_kernel_ptr(int metric);
 constexpr int SUPER_BLOCK = 32;      // one warp per block: W/U columns are per warp
 constexpr int SUPER_MAX_L = 4096;    // levels of the superposed dimension
-size_t super_smem(int32_t n_samples, int32_t levels, int block);
+size_t super_smem(int32_t n_samples, int32_t levels, int32_t gt_n, int block);
+constexpr int32_t SUPER_MAX_GT = 2048;   // level-table entries kept in shared memory
 const void* fit2_kernel_ptr(int precision, int metric);   // 2 candidates/thread, 256 threads
 constexpr int FIT2_BLOCK = 256;
 const void* fit3_kernel_ptr(int precision, int metric);   // warp-specialised, 384 threads

@@ -506,7 +506,8 @@ __global__ void __launch_bounds__(SUPER_BLOCK) fit_super_kernel(FitArgs a) {
   const bool ag = a.sup_dim == NSAC_AG;
   double* rel = reinterpret_cast<double*>(smem_raw);
   double* lv = rel + ((ns + 1) & ~1);
-  double* W = lv + ((L + 1) & ~1);              // [ns][B]: b_k
+  double* gt = lv + ((L + 1) & ~1);             // level tables of the grid dimensions
+  double* W = gt + ((a.sup_gt_n + 1) & ~1);     // [ns][B]: b_k
   double* U = W + (size_t)ns * B;               // [ns][B]: u_k
   const int64_t sac = (int64_t)blockIdx.y + a.sac_begin;
   const double amp = a.sac_ctl ? a.sac_ctl[2 * sac] : a.amplitude;
@@ -518,6 +519,27 @@ __global__ void __launch_bounds__(SUPER_BLOCK) fit_super_kernel(FitArgs a) {
     double q[NP];
     generate_grid_opc(a.space, (int64_t)j * a.sup_st, q, a.exp_tab);
     lv[j] = ag ? q[NSAC_AG] : q[NSAC_ANT];
+  }
+  // per-dimension level tables (generate_grid_opc's own values), so that a
+  // node's OPC is digits + table loads instead of the generic generator
+  if (a.sup_tab) {
+    int off = 0;
+    int64_t stride = 1;
+    for (int d = 0; d < NP; ++d) {
+      const int64_t Ld = a.space.levels[d];
+      if (Ld <= 1) continue;
+      if (d == a.sup_dim) {   // its digit is 0 in ib; the value is never used
+        stride *= Ld;
+        continue;
+      }
+      for (int j = tid; j < Ld; j += B) {
+        double q[NP];
+        generate_grid_opc(a.space, (int64_t)j * stride, q, a.exp_tab);
+        gt[off + j] = q[d];
+      }
+      off += (int)Ld;
+      stride *= Ld;
+    }
   }
   __syncthreads();
   const double INF = __longlong_as_double(0x7ff0000000000000LL);
@@ -538,29 +560,55 @@ __global__ void __launch_bounds__(SUPER_BLOCK) fit_super_kernel(FitArgs a) {
     const int64_t node = a.node_begin + (valid ? t0 + tid : nn - 1);
     const int64_t ib = node / st * stL + node % st;   // index of the node's level 0
     double p[NP];
-    generate_grid_opc(a.space, ib, p, a.exp_tab);   // grid spaces only (host)
+    if (a.sup_tab) {
+      // mixed-radix digits of ib (dimension 0 fastest) -> table values;
+      // bit-identical to generate_grid_opc (the tables are its values)
+      uint64_t rem = (uint64_t)ib;
+      int off = 0;
+#pragma unroll
+      for (int d = 0; d < NP; ++d) {
+        const int64_t Ld = a.space.levels[d];
+        if (Ld > 1) {
+          uint64_t q, digit;
+          if ((rem >> 32) == 0) {
+            const uint32_t r32 = (uint32_t)rem, q32 = r32 / (uint32_t)Ld;
+            q = q32;
+            digit = r32 - q32 * (uint32_t)Ld;
+          } else {
+            q = rem / (uint64_t)Ld;
+            digit = rem - q * (uint64_t)Ld;
+          }
+          rem = q;
+          if (d == a.sup_dim) {   // digit 0; b and u override this height
+            p[d] = lv[0];
+          } else {
+            p[d] = gt[off + (int)digit];
+            off += (int)Ld;
+          }
+        } else {
+          p[d] = a.space.lo[d];
+        }
+      }
+    } else {
+      generate_grid_opc(a.space, ib, p, a.exp_tab);   // grid spaces only (host)
+    }
     Setup s;
     make_setup(p, a.ctl.dt_ms, a.ctl.h, a.ctl.n_steps, Aprime, pwd, s);
     const double F = p[NC_FIX];
     double Sb, Su;
-    {  // b: N_SAC_d = 0 (n~ = 0 - F during the pulse)
-      Setup sb = s;
+    {
+      Setup sb = s, su = s;
+      // b: N_SAC_d = 0 (n~ = 0 - F during the pulse)
       if (ag) sb.ph[0].nt_ag = -F; else sb.ph[0].nt_ant = -F;
-      Prop2<double> pr;
-      make_prop<double, false>(sb, pr);
-      Sb = run_propagator<double, 0, true, false, 1, true>(pr, s.n_pulse, a.ctl.n_steps, rel,
-                                                           W + tid, B, 0.0, 1.0, nullptr, 0);
-    }
-    {  // u: unit pulse on channel d, nothing else
-      Setup su = s;
+      // u: unit pulse on channel d, nothing else
       su.ph[0].nt_ag = ag ? 1.0 : 0.0;
       su.ph[0].nt_ant = ag ? 0.0 : 1.0;
       su.ph[1].nt_ag = 0.0;
       su.ph[1].nt_ant = 0.0;
-      Prop2<double> pr;
-      make_prop<double, false>(su, pr);
-      Su = run_propagator<double, 0, true, false, 1, true>(pr, s.n_pulse, a.ctl.n_steps, rel,
-                                                           U + tid, B, 0.0, 1.0, nullptr, 0);
+      Prop2<double> pb, pu;
+      make_prop<double, false>(sb, pb);
+      make_prop<double, false>(su, pu);
+      run_propagator_bu(pb, pu, s.n_pulse, a.ctl.n_steps, W + tid, U + tid, B, Sb, Su);
     }
     const bool ok = Sb + amax * Su <= SUPER_SAFE;   // false for NaN / inf
     if (ok && valid) {
@@ -1118,9 +1166,9 @@ const void* fit_super_kernel_ptr(int metric) {
                      : reinterpret_cast<const void*>(&fit_super_kernel<1>);
 }
 
-size_t super_smem(int32_t ns, int32_t levels, int block) {
-  return ((size_t)((ns + 1) & ~1) + (size_t)((levels + 1) & ~1) + super_cols(ns) * block) *
-         sizeof(double);
+size_t super_smem(int32_t ns, int32_t levels, int32_t gt_n, int block) {
+  return ((size_t)((ns + 1) & ~1) + (size_t)((levels + 1) & ~1) + (size_t)((gt_n + 1) & ~1) +
+          super_cols(ns) * block) * sizeof(double);
 }
 
 cudaError_t launch_fit(const void* fn, const FitArgs& a, dim3 grid, int block, size_t smem,

@@ -187,3 +187,42 @@ def test_super_rejects_ineligible(opmm, h):
     with pytest.raises(opmm.OpmmError):   # fp32 is not superposed
         opmm.opmm_fit(h, rec, ctl, g, g.n_grid(),
                       opmm.fit_options(precision=opmm.FP32, kernel_variant=4))
+
+
+def test_super_generic_generator_path(opmm, h):
+    """More grid levels than the kernel's shared level tables hold (sum of
+    levels > 2048): nodes come from the generic grid generator instead."""
+    ctl = W.Control()
+    rec = trace(ctl)
+    sp = W.grid_space({
+        "N_SAC_AG": (40.0, 70.0, 8, False),
+        "PW": (20.0, 60.0, 2100, False),
+    })
+    check_against_oracle(opmm, h, rec, ctl, sp)
+
+
+def test_super_exact_ties_lowest_index(opmm, h):
+    """PW 39.21 / 39.6 / 40 ms share n_pulse = 40: their nodes are computed
+    identically, so the errors tie exactly and the lowest index wins (Q12)."""
+    ctl = W.Control()
+    rec = trace(ctl)
+    d = W.truth_opc()
+    sp = W.grid_space({"N_SAC_AG": (d[15] * 0.99, d[15] * 1.01, 3, False),
+                       "PW": (39.21, 40.0, 3, False)})
+    o = oracle.fit(rec, ctl, sp, 0, 9)
+    r, E = fit_with_err(opmm, h, rec, ctl, sp, 4)
+    assert r["best_index"] == o["best_index"]
+    e = E.reshape(3, 3)
+    assert np.all(e[0] == e[1]) and np.all(e[1] == e[2])
+
+
+def test_super_is_the_auto_choice_for_pulse_height_grids(opmm, h):
+    """kernel_variant 0 picks the superposition kernel for an eligible grid
+    with >= 8 pulse-height levels: identical result to an explicit 4."""
+    ctl = W.Control()
+    rec = trace(ctl)
+    sp = W.g4_space(per_dim=10)
+    r0, E0 = fit_with_err(opmm, h, rec, ctl, sp, 0)
+    r4, E4 = fit_with_err(opmm, h, rec, ctl, sp, 4)
+    assert np.array_equal(E0, E4)
+    assert r0["best_index"] == r4["best_index"] and r0["opt_err"] == r4["opt_err"]

@@ -1,5 +1,5 @@
 """Run 3 superposition fits of G4 (for ncu: -k regex:fit_super -s 2 -c 1).
-    python tools/prof_super.py [per_dim]"""
+    python tools/prof_super.py [per_dim] [L]"""
 import ctypes
 import os
 import sys
@@ -13,8 +13,18 @@ import workloads as W  # noqa: E402
 from paper_2007_09884_b200 import opmm  # noqa: E402
 
 per = int(sys.argv[1]) if len(sys.argv) > 1 else 100
+L = int(sys.argv[2]) if len(sys.argv) > 2 else 0     # > 0: K x B x N_SAC_AG(L) x PW100 grid
 rec = np.loadtxt(os.path.join(ROOT, "tests", "golden", "trace_truth_A10_dt1_n100.txt")) + W.noise(101)
 ctl, sp = W.Control(), W.g4_space(per)
+if L:
+    d, I = W.truth_opc(), W.IDX
+    others = 10**8 // (L * 100)
+    k = int(round(others ** 0.5))
+    sp = W.grid_space({
+        "K_SE_AG": (d[I["K_SE_AG"]] * 0.7, d[I["K_SE_AG"]] * 1.5, k, True),
+        "B_AG": (d[I["B_AG"]] * 0.7, d[I["B_AG"]] * 1.5, others // k, True),
+        "N_SAC_AG": (d[I["N_SAC_AG"]] * 0.5, d[I["N_SAC_AG"]] * 2.0, L, True),
+        "PW": (1.0, 100.0, 100, False)})
 n = sp.n_grid()
 with opmm.opmm_create(0) as h:
     recd = torch.as_tensor(rec, device="cuda")

@@ -132,7 +132,18 @@ typedef struct {
                               2 = two interleaved candidates per thread;
                               3 = warp-specialised producer/consumer.  2 and 3
                               need PROPAGATOR, a physical-by-construction space
-                              and block_size = 0        */
+                              and block_size = 0.
+                              4 = superposition over the grid levels of a pulse
+                              height (N_SAC_AG or N_SAC_ANT, the one with more
+                              levels): the trajectory is affine in it (RK4 of
+                              the linear plant), so each grid node is integrated
+                              twice and every level scored at 2 fp64 ops per
+                              sample.  Needs grid mode, the 18-parameter model,
+                              FP64, PROPAGATOR, no substeps, a physical space,
+                              no certify, block_size = 0; else UNSUPPORTED.
+                              Auto (0) picks it for such grids with >= 8
+                              levels.  Errors equal variant 1's up to rounding
+                              (DESIGN.md section 7b).                           */
   int32_t certify;      /* FP32 only: keep the 8 best candidates by fp32 error among
                            every thread's best two, re-score them in fp64 and return
                            the fp64-best; result.certified = 1 when the fp32 error

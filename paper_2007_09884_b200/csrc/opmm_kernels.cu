@@ -459,11 +459,20 @@ __device__ __forceinline__ void super_levels(const double* __restrict__ Wc,
       av[jj] = lv[min(j0 + jj, L - 1)];
       acc[jj] = 0.0;
     }
-    // sample 0 contributes |0 - rel_0| = 0 (fit_kernel starts at k = 1 too)
-#pragma unroll 2
+    // sample 0 contributes |0 - rel_0| = 0 (fit_kernel starts at k = 1 too).
+    // The next sample's (w, u) is loaded one iteration ahead, so the shared
+    // memory latency hides behind the J pairs of this one.
+    const double* __restrict__ wp = Wc + SUPER_BLOCK;
+    const double* __restrict__ up = Uc + SUPER_BLOCK;
+    double wn = *wp - rel[1], un = *up;
     for (int32_t k = 1; k < ns; ++k) {
-      const double w = Wc[(size_t)k * B] - rel[k];
-      const double u = Uc[(size_t)k * B];
+      const double w = wn, u = un;
+      wp += SUPER_BLOCK;
+      up += SUPER_BLOCK;
+      if (k + 1 < ns) {
+        wn = *wp - rel[k + 1];
+        un = *up;
+      }
 #pragma unroll
       for (int jj = 0; jj < J; ++jj) accumulate<METRIC>(acc[jj], fma(av[jj], u, w));
     }
@@ -501,7 +510,8 @@ template <int METRIC>
 __global__ void __launch_bounds__(SUPER_BLOCK) fit_super_kernel(FitArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int32_t ns = a.ctl.n_steps + 1;
-  const int B = blockDim.x, tid = threadIdx.x;
+  constexpr int B = SUPER_BLOCK;   // the launch block (the column layout assumes it)
+  const int tid = threadIdx.x;
   const int L = a.sup_L;
   const bool ag = a.sup_dim == NSAC_AG;
   double* rel = reinterpret_cast<double*>(smem_raw);

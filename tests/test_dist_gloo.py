@@ -98,3 +98,65 @@ def test_world2_shard_merge_equals_unsharded():
         c = W.Control(n_steps=60, amplitude_deg=amp[s], pw_default_ms=pw[s])
         r = oracle.fit(oracle.positions(truths[s], c), c, sp, 0, 300, saccade=s)
         assert results[0][2][s] == (r["best_err"], r["best_index"])
+
+
+def _super_node_indices(n_nodes_begin, n_nodes_end, st, L):
+    """Candidate indices of grid nodes [b, e) of the superposition kernel
+    (kernel_variant 4): node n -> level-0 index
+    (n // st) * st * L + n % st, levels at stride st."""
+    out = []
+    for n in range(n_nodes_begin, n_nodes_end):
+        ib = (n // st) * st * L + n % st
+        out.extend(ib + j * st for j in range(L))
+    return out
+
+
+def _super_rank_main(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2007_09884_b200 import opmm
+        ctl = W.Control()
+        rec = oracle.positions(W.truth_opc(), ctl) + W.noise(ctl.n_steps + 1)
+        sp = W.g4_space(per_dim=5)          # N_SAC_AG (dim 15) superposed, L = 5
+        L = 5
+        st = 5 * 5                          # levels of dims 0 (K_SE_AG) and 4 (B_AG)
+        nodes = sp.n_grid() // L
+        b, e = opmm.opmm_shard_range(nodes, rank, world)
+        idx = _super_node_indices(b, e, st, L)
+        errs = [oracle.objective(oracle.generate(sp, i), rec, ctl) for i in idx]
+        best = min(zip(errs, idx)) if idx else (float("inf"), -1)
+        mine = torch.tensor([best[0], float(best[1]), float(len(idx))], dtype=torch.float64)
+        allp = [torch.zeros(3, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(allp, mine)
+        be, bi = opmm.opmm_merge_argmin([float(t[0]) for t in allp], [int(t[1]) for t in allp])
+        q.put((rank, be, bi, sorted(idx), int(sum(float(t[2]) for t in allp))))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_world2_super_node_shards_partition_the_grid():
+    """kernel_variant 4 shards grid NODES (all levels of a node on one rank):
+    the ranks' candidate sets are disjoint, cover the grid, and the merged
+    argmin equals the unsharded one."""
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_super_rank_main, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    sp = W.g4_space(per_dim=5)
+    n = sp.n_grid()
+    all_idx = sorted(results[0][3] + results[1][3])
+    assert all_idx == list(range(n))
+    assert results[0][4] == n
+    ctl = W.Control()
+    rec = oracle.positions(W.truth_opc(), ctl) + W.noise(ctl.n_steps + 1)
+    full = oracle.fit(rec, ctl, sp, 0, n)
+    for rank, be, bi, _, _ in results:
+        assert (be, bi) == (full["best_err"], full["best_index"])

@@ -226,3 +226,39 @@ def test_super_is_the_auto_choice_for_pulse_height_grids(opmm, h):
     r4, E4 = fit_with_err(opmm, h, rec, ctl, sp, 4)
     assert np.array_equal(E0, E4)
     assert r0["best_index"] == r4["best_index"] and r0["opt_err"] == r4["opt_err"]
+
+
+def test_super_nccl_single_rank_node_sharding(opmm, h):
+    """Variant 4 on an NCCL handle (1-rank communicator): the rank's share is a
+    node range, its 32-byte partial goes through ncclAllGather and the merge
+    kernel -- same result as the single-GPU handle."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import os, sys, numpy as np
+sys.path.insert(0, os.getcwd())
+os.environ["OPMM_NCCL_SINGLE_RANK"] = "1"
+import torch, oracle, workloads as W
+from paper_2007_09884_b200 import opmm
+ctl = W.Control()
+rec = oracle.positions(W.truth_opc(), ctl) + W.noise(101)
+uid = opmm.opmm_nccl_unique_id()
+with opmm.opmm_create_nccl(0, uid, 0, 1) as hn, opmm.opmm_create(0) as hp:
+    for per in (6, 20):
+        sp = W.g4_space(per)
+        n = sp.n_grid()
+        o = opmm.fit_options(kernel_variant=4)
+        a = opmm.opmm_fit(hn, rec, ctl, sp, n, o)
+        b = opmm.opmm_fit(hp, rec, ctl, sp, n, o)
+        assert (a["best_index"], a["opt_err"], a["n_finite"], a["n_evaluated"]) == \
+               (b["best_index"], b["opt_err"], b["n_finite"], b["n_evaluated"]), (per, a, b)
+        assert a["n_evaluated"] == n
+        assert a["opc"].tolist() == b["opc"].tolist()
+print("nccl-super ok")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    p = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                       timeout=300)
+    assert p.returncode == 0, p.stdout + p.stderr
+    assert "nccl-super ok" in p.stdout

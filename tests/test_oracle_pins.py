@@ -186,6 +186,35 @@ def test_p6_linearity_in_pulse_height_and_monotone_amplitude():
     assert np.all((t70 - t40)[1:41] > 0)
 
 
+@pytest.mark.parametrize("name", ["N_SAC_AG", "N_SAC_ANT"])
+def test_p6_superposition_identity_both_channels(name):
+    """The identity the superposition kernel scores with:
+    Delta-theta(a) = b + a u, b = Delta-theta(N_SAC = 0), u = Delta-theta(1) - b,
+    for either pulse height, any stable plant, any pulse width -- checked on the
+    oracle's own literal RK4 trajectories, plus the L1 error it implies."""
+    rng = np.random.default_rng(76)
+    ctl = W.Control()
+    rec = oracle.positions(W.truth_opc(), ctl) + W.noise(ctl.n_steps + 1)
+    rel, _, Ap = oracle.relativize(rec, ctl.amplitude_deg)
+    for _ in range(6):
+        p = W.truth_opc() * np.exp(rng.uniform(-0.3, 0.3, size=18))
+        p[I["PW"]] = float(rng.integers(5, 90))
+        def traj(a):
+            q = p.copy()
+            q[I[name]] = a
+            return oracle.simulate(q, ctl.dt_ms, ctl.n_steps, Ap, 40.0)
+        b, one = traj(0.0), traj(1.0)
+        u = one - b
+        for a in (0.37, 12.5, 80.0):
+            direct = traj(a)
+            sup = b + a * u
+            assert np.max(np.abs(sup - direct)) <= 1e-11 * max(np.max(np.abs(direct)), 1.0)
+            q = p.copy()
+            q[I[name]] = a
+            E = oracle.objective(q, rec, ctl)
+            assert abs(np.abs(sup - rel).sum() - E) <= 1e-10 * max(E, np.abs(rel).sum())
+
+
 def test_directionality():
     """N_SAC_AG > N_C_FIX > N_SAC_ANT gives a non-negative saccade."""
     p = W.truth_opc()

@@ -100,6 +100,18 @@ constexpr int kAutoVariant = 1;
 // grids with at least this many pulse-height levels
 constexpr bool kAutoSuper = true;
 constexpr int32_t kSuperMinLevels = 8;
+// The superposition kernel's tensor-memory layout (4 warps keep their
+// columns in TMEM, 7 warps per SM instead of 4) overlaps the per-node setup
+// with the level loop: faster below this many levels, slower above (3 of the
+// 4 schedulers then carry 2 level-loop warps).  Env
+// OPMM_SUPER_TMEM=0/1 forces it off/on (A/B timing, tests).
+constexpr int32_t kSuperTmemMaxLevels = 64;
+bool super_tmem_wanted(int32_t levels) {
+  const char* e = getenv("OPMM_SUPER_TMEM");
+  if (e && e[0] == '0') return false;
+  if (e && e[0] == '1') return true;
+  return levels < kSuperTmemMaxLevels;
+}
 
 }  // namespace
 
@@ -461,18 +473,35 @@ opmm_status enqueue_fit_super(opmm_handle* h, const double* rec_dev, const opmm_
   const int64_t nodes = n_candidates / L;
   int64_t nb = 0, ne = nodes;
   if (shard) opmm_shard_range(nodes, h->rank, h->world, &nb, &ne);
-  const void* fn = opmm::fit_super_kernel_ptr(metric);
-  const int block = opmm::SUPER_BLOCK;
+  const int32_t ns = ctl->n_steps + 1;
+  const size_t lim = max_dyn_smem(opmm::fit_super_kernel_ptr(metric, false));
   int32_t gt_n = 0;
   for (int d = 0; d < OPMM_NPARAM; ++d)
     if (d != sup_dim) gt_n += space->levels[d] > 1 ? space->levels[d] : 0;
   int32_t use_tab = 1;
-  if (gt_n > opmm::SUPER_MAX_GT ||
-      opmm::super_smem(ctl->n_steps + 1, L, gt_n, block) > max_dyn_smem(fn)) {
+  if (gt_n > opmm::SUPER_MAX_GT || opmm::super_smem(ns, L, gt_n, 1, 0) > lim) {
     gt_n = 0;   // generic generator per node
     use_tab = 0;
   }
-  const size_t smem = opmm::super_smem(ctl->n_steps + 1, L, gt_n, block);
+  // Warps per block: with n <= SUPER_TMEM_MAX_STEPS, 4 warps keep their
+  // columns in their tensor-memory quadrant and as many more as shared memory
+  // holds use shared memory, in ONE block per SM (8 warps, 2 per scheduler,
+  // so one warp's latency-bound setup overlaps another's level loop).
+  // Otherwise one warp per block, shared memory only (occupancy decides).
+  int tm_warps = 0, smem_warps = 1;
+  if (ctl->n_steps <= opmm::SUPER_TMEM_MAX_STEPS && super_tmem_wanted(L)) {
+    size_t fixed = opmm::super_smem(ns, L, gt_n, 0, 4);
+    int sw = 0;
+    while (sw < opmm::SUPER_MAX_WARPS - 4 && opmm::super_smem(ns, L, gt_n, sw + 1, 4) <= lim) ++sw;
+    if (fixed <= lim) { tm_warps = 4; smem_warps = sw; }
+  }
+  const void* fn = opmm::fit_super_kernel_ptr(metric, tm_warps > 0);
+  const int block = 32 * (tm_warps + smem_warps);
+  size_t smem = opmm::super_smem(ns, L, gt_n, smem_warps, tm_warps);
+  // tensor memory is allocated whole (512 columns) per block: keep one block per SM
+  // (two blocks need 2 x (smem + ~2 KB static/reserved) <= 228 KB of the SM)
+  constexpr size_t kOneBlockSmem = 116 * 1024;
+  if (tm_warps > 0 && smem < kOneBlockSmem) smem = kOneBlockSmem;
   int grid = 1;
   CKS(grid_for(h, fn, block, smem, ne - nb, opts ? opts->grid_blocks : 0, &grid));
   if (S > 1 && !(opts && opts->grid_blocks)) {
@@ -511,13 +540,14 @@ opmm_status enqueue_fit_super(opmm_handle* h, const double* rec_dev, const opmm_
   // chunk width: least padded slots over ceil(L / J) chunks, then the widest
   int best_J = 32;
   int64_t best_pad = INT64_MAX;
-  for (int J = 32; J >= 8; J -= 4) {
+  for (int J = tm_warps > 0 ? 20 : 32; J >= 8; J -= 4) {
     const int64_t pad = ((int64_t)L + J - 1) / J * J - L;
     if (pad < best_pad) { best_pad = pad; best_J = J; }
   }
   a.sup_J = best_J;
   a.sup_gt_n = gt_n;
   a.sup_tab = use_tab;
+  a.sup_tm_warps = tm_warps;
   a.sup_st = st;
   a.node_begin = nb;
   a.node_end = ne;
@@ -557,9 +587,8 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
   const bool sup_ok = sup_dim >= 0 && precision == OPMM_FP64 && integ == OPMM_INTEG_PROPAGATOR &&
                       ctl->substeps <= 1 && space_dev.all_physical && !(opts && opts->certify) &&
                       !(opts && opts->block_size) && space->levels[sup_dim] <= opmm::SUPER_MAX_L &&
-                      opmm::super_smem(ctl->n_steps + 1, space->levels[sup_dim], 0,
-                                       opmm::SUPER_BLOCK) <=
-                          max_dyn_smem(opmm::fit_super_kernel_ptr(metric));
+                      opmm::super_smem(ctl->n_steps + 1, space->levels[sup_dim], 0, 1, 0) <=
+                          max_dyn_smem(opmm::fit_super_kernel_ptr(metric, false));
   if (kv_opt == 4 && !sup_ok)
     return fail(OPMM_ERR_UNSUPPORTED, "kernel_variant 4 needs a grid space (18-parameter model) "
                                       "with N_SAC_AG or N_SAC_ANT levels > 1 (<= %d), all "
@@ -882,7 +911,10 @@ opmm_status opmm_create(opmm_handle** out, int device) {
         allow_dyn_smem(opmm::simscore_kernel_ptr(p, i, m));
         allow_dyn_smem(opmm::fit2_kernel_ptr(p, m));
         allow_dyn_smem(opmm::fit3_kernel_ptr(p, m));
-        if (p == 0 && i == 0) allow_dyn_smem(opmm::fit_super_kernel_ptr(m));
+        if (p == 0 && i == 0) {
+          allow_dyn_smem(opmm::fit_super_kernel_ptr(m, false));
+          allow_dyn_smem(opmm::fit_super_kernel_ptr(m, true));
+        }
         allow_dyn_smem(opmm::simulate_kernel_ptr(p, i));
         allow_dyn_smem(opmm::score_kernel_ptr(p, m));
         for (int obj = 0; obj < 5; ++obj)

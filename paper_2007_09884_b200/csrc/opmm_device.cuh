@@ -933,14 +933,15 @@ __device__ __forceinline__ T run_propagator(const Prop2<T>& pr, int32_t n_pulse,
 // the odd-start state, taken from their own Prop2 (pu's post-pulse forcing is
 // zero).  Each recurrence is exactly run_propagator's (same FMA order, so b
 // and u are bit-identical to two separate TRAJ runs); the pair gives the
-// scheduler 10 independent chains instead of 5.  Writes Wc[k B] = b_k,
-// Uc[k B] = u_k (k = 0..n_steps) and returns sum |b_k| and sum |u_k|.
+// scheduler 10 independent chains instead of 5.  Every sample k = 0..n_steps
+// goes to sink.put(k, b_k, u_k); sink.after_block(b) runs (warp-uniformly)
+// after each loop block, when every lane has put all samples <= 2b + 2, and
+// sink.finish() at the end.  Returns sum |b_k| and sum |u_k|.
 // ----------------------------------------------------------------------------
+template <typename Sink>
 __device__ __forceinline__ void run_propagator_bu(const Prop2<double>& pb, const Prop2<double>& pu,
-                                                  int32_t n_pulse, int32_t n_steps,
-                                                  double* __restrict__ Wc,
-                                                  double* __restrict__ Uc, int B, double& Sb,
-                                                  double& Su) {
+                                                  int32_t n_pulse, int32_t n_steps, Sink& sink,
+                                                  double& Sb, double& Su) {
   const PhaseProp2<double>& q0 = pb.ph[0];
   double A00 = q0.X2[0][0], A01 = q0.X2[0][1], A10 = q0.X2[1][0], A11 = q0.X2[1][1];
   double A20 = q0.X2[2][0], A21 = q0.X2[2][1], A30 = q0.X2[3][0], A31 = q0.X2[3][1];
@@ -974,22 +975,18 @@ __device__ __forceinline__ void run_propagator_bu(const Prop2<double>& pb, const
   double th = 0.0, om = 0.0, xa = 0.0, xn = 0.0, fa = 0.0, fn = 0.0;
   double uth = 0.0, uom = 0.0, uxa = 0.0, uxn = 0.0, ufa = 0.0, ufn = 0.0;
   double sb = 0.0, su = 0.0;
-  Wc[0] = 0.0;
-  Uc[0] = 0.0;
+  sink.put(0, 0.0, 0.0);
   if (n_pulse == 0) swap_in();
   if (o) {
     th = pb.z1[0]; om = pb.z1[1]; xa = pb.z1[2]; xn = pb.z1[3]; fa = pb.f1[0]; fn = pb.f1[1];
     uth = pu.z1[0]; uom = pu.z1[1]; uxa = pu.z1[2]; uxn = pu.z1[3]; ufa = pu.f1[0]; ufn = pu.f1[1];
     sb += fabs(th);
     su += fabs(uth);
-    Wc[B] = th;
-    Uc[B] = uth;
+    sink.put(1, th, uth);
   }
   const int32_t nb = (n_steps + 1) / 2;
   const int32_t bs = switches ? (n_pulse - o) / 2 : nb;
   if (switches && bs == 0) swap_in();
-  double* __restrict__ wr = Wc + (int64_t)o * B;
-  double* __restrict__ ur = Uc + (int64_t)o * B;
   int32_t b = 0;
   while (b < nb - 1) {
     const int32_t mine = bs > b ? min(bs, nb - 1) : nb - 1;
@@ -1030,10 +1027,9 @@ __device__ __forceinline__ void run_propagator_bu(const Prop2<double>& pb, const
       sb += fabs(th);
       su += fabs(v1);
       su += fabs(uth);
-      wr[(int64_t)(2 * b + 1) * B] = t1;
-      wr[(int64_t)(2 * b + 2) * B] = th;
-      ur[(int64_t)(2 * b + 1) * B] = v1;
-      ur[(int64_t)(2 * b + 2) * B] = uth;
+      sink.put(o + 2 * b + 1, t1, v1);
+      sink.put(o + 2 * b + 2, th, uth);
+      sink.after_block(b);
     }
     if (b == bs) swap_in();
   }
@@ -1046,16 +1042,15 @@ __device__ __forceinline__ void run_propagator_bu(const Prop2<double>& pb, const
     if (k1 <= n_steps) {
       sb += fabs(t1);
       su += fabs(v1);
-      Wc[(int64_t)k1 * B] = t1;
-      Uc[(int64_t)k1 * B] = v1;
+      sink.put(k1, t1, v1);
     }
     if (k1 + 1 <= n_steps) {
       sb += fabs(t2);
       su += fabs(v2);
-      Wc[(int64_t)(k1 + 1) * B] = t2;
-      Uc[(int64_t)(k1 + 1) * B] = v2;
+      sink.put(k1 + 1, t2, v2);
     }
   }
+  sink.finish();
   Sb = sb;
   Su = su;
 }

@@ -97,6 +97,7 @@ struct FitArgs {
   int32_t sup_J;            // register chunk width (8, 12, ..., 32)
   int32_t sup_gt_n;         // entries of the per-dimension level tables
   int32_t sup_tab;          // 1: nodes from the tables; 0: generic generator (too many levels)
+  int32_t sup_tm_warps;     // warps 0..T-1 keep their columns in tensor memory (0: none)
   int64_t sup_st;           // its mixed-radix stride (product of the lower levels)
   int64_t node_begin, node_end;   // this rank's nodes
 };
@@ -159,10 +160,11 @@ int nm_group_problems_per_block();
 
 const void* fit_kernel_ptr(int precision, int integrator, int metric);
 // superposition over one pulse-height grid dimension (kernel_variant 4, fp64)
-const void* fit_super_kernel_ptr(int metric);
-constexpr int SUPER_BLOCK = 32;      // one warp per block: W/U columns are per warp
+const void* fit_super_kernel_ptr(int metric, bool tmem);
+constexpr int SUPER_MAX_WARPS = 8;   // per block: TMEM warps (<= 4, one per quadrant) + smem warps
+constexpr int SUPER_TMEM_MAX_STEPS = 120;   // 4 TMEM columns per sample, groups of 4, 512 columns
 constexpr int SUPER_MAX_L = 4096;    // levels of the superposed dimension
-size_t super_smem(int32_t n_samples, int32_t levels, int32_t gt_n, int block);
+size_t super_smem(int32_t n_samples, int32_t levels, int32_t gt_n, int smem_warps, int tm_warps);
 constexpr int32_t SUPER_MAX_GT = 2048;   // level-table entries kept in shared memory
 const void* fit2_kernel_ptr(int precision, int metric);   // 2 candidates/thread, 256 threads
 constexpr int FIT2_BLOCK = 256;

@@ -437,21 +437,104 @@ __global__ void __launch_bounds__(OPMM_FIT_LB_THREADS, OPMM_FIT_LB_BLOCKS) fit_k
 // columns are per warp), post-pulse coefficients in registers (REGSTASH).
 // ---------------------------------------------------------------------------
 constexpr double SUPER_SAFE = 1e6;     // deg; bounds the combination's rounding
+constexpr int SUPER_RING = 640;        // doubles per TMEM warp: the 8-sample staging ring
+                                       // (512) and, for blown-up nodes, evaluate's stash [10][32] double2
 
 __host__ __device__ constexpr size_t super_cols(int32_t ns) {
   return (size_t)(2 * ns > 20 ? 2 * ns : 20);   // W + U rows, or evaluate's stash [10] x double2
 }
 
-// Score levels [0, L) of one node from its columns (Wc = b, Uc = u; stride B)
-// in register chunks of J levels.  The chunk width is a compile-time constant
-// so the inner loop is J unguarded (DFMA, DADD) pairs per sample; a partial
-// last chunk repeats level L-1 in its spare slots and records only its own.
+// ---- Tensor memory (tcgen05, sm_100a).  A warp may address only its own
+// 32-lane quadrant (warp id % 4); lane l of the warp reads/writes TMEM lane
+// 32 (warp % 4) + l.  32x32b.x16: 16 consecutive 32-bit columns per lane.
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, "
+               "%9, %10, %11, %12, %13, %14, %15, %16};"
+               :: "r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]),
+                  "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]),
+                  "r"(r[13]), "r"(r[14]), "r"(r[15])
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                 "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr)
+               : "memory");
+}
+// wait for this thread's outstanding tcgen05.ld; the registers are in/out
+// operands so that no use of them can be scheduled above the wait
+__device__ __forceinline__ void tmem_wait_ld(uint32_t (&r)[8]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]),
+                 "+r"(r[6]), "+r"(r[7])
+               :: "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+// Column sinks of run_propagator_bu.  Both store w_k = b_k - rel_k (the
+// level loop's addend, computed once per node) and u_k.
+struct SmemSink {             // [ns][32] columns in shared memory (lane-strided)
+  double* W;
+  double* U;
+  const double* rel;
+  __device__ __forceinline__ void put(int32_t k, double bk, double uk) {
+    W[k * 32] = bk - rel[k];
+    U[k * 32] = uk;
+  }
+  __device__ __forceinline__ void after_block(int32_t) {}
+  __device__ __forceinline__ void finish() {}
+};
+
+struct TmemSink {             // 8-sample shared ring, flushed 4 samples at a time to TMEM
+  double2* ring;              // this lane's slot 0; slot j at ring[32 j]
+  const double* rel;
+  uint32_t taddr;             // this warp's TMEM quadrant, column 0
+  int32_t n_steps;
+  int32_t kf;                 // next sample to flush (warp-uniform)
+  __device__ __forceinline__ void put(int32_t k, double bk, double uk) {
+    ring[(k & 7) * 32] = make_double2(bk - rel[k], uk);
+  }
+  // samples k0..k0+3 -> TMEM columns 4 k0 .. 4 k0 + 15 (w lo, w hi, u lo, u hi)
+  __device__ __forceinline__ void flush(int32_t k0) {
+    uint32_t r[16];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const double2 v = ring[((k0 + j) & 7) * 32];
+      r[4 * j + 0] = (uint32_t)__double2loint(v.x);
+      r[4 * j + 1] = (uint32_t)__double2hiint(v.x);
+      r[4 * j + 2] = (uint32_t)__double2loint(v.y);
+      r[4 * j + 3] = (uint32_t)__double2hiint(v.y);
+    }
+    tmem_st16(taddr + 4u * (uint32_t)k0, r);
+  }
+  // after block b every lane has put samples <= 2b + 2 (lanes with an odd
+  // pulse end one more); pending samples stay <= 7, so the ring never wraps
+  // onto an unflushed one
+  __device__ __forceinline__ void after_block(int32_t b) {
+    if (kf + 4 <= 2 * b + 3) {
+      flush(kf);
+      kf += 4;
+    }
+  }
+  __device__ __forceinline__ void finish() {
+    for (; kf <= n_steps; kf += 4) flush(kf);   // the last group's spare columns hold junk
+    tmem_wait_st();
+  }
+};
+
+// Score levels [0, L) of one node from its shared-memory columns (Wc = w,
+// Uc = u; lane stride 32) in register chunks of J levels.  The chunk width is
+// a compile-time constant so the inner loop is J unguarded (DFMA, DADD)
+// pairs per sample; a partial last chunk repeats level L-1 in its spare slots
+// and records only its own.
 template <int METRIC, int J, typename Rec>
 __device__ __forceinline__ void super_levels(const double* __restrict__ Wc,
                                              const double* __restrict__ Uc,
-                                             const double* __restrict__ rel,
-                                             const double* __restrict__ lv, int32_t ns, int B,
-                                             int L, int64_t ib, int64_t st, Rec& record) {
+                                             const double* __restrict__ lv, int32_t ns, int L,
+                                             int64_t ib, int64_t st, Rec& record) {
   for (int j0 = 0; j0 < L; j0 += J) {
     double av[J], acc[J];
 #pragma unroll
@@ -462,15 +545,15 @@ __device__ __forceinline__ void super_levels(const double* __restrict__ Wc,
     // sample 0 contributes |0 - rel_0| = 0 (fit_kernel starts at k = 1 too).
     // The next sample's (w, u) is loaded one iteration ahead, so the shared
     // memory latency hides behind the J pairs of this one.
-    const double* __restrict__ wp = Wc + SUPER_BLOCK;
-    const double* __restrict__ up = Uc + SUPER_BLOCK;
-    double wn = *wp - rel[1], un = *up;
+    const double* __restrict__ wp = Wc + 32;
+    const double* __restrict__ up = Uc + 32;
+    double wn = *wp, un = *up;
     for (int32_t k = 1; k < ns; ++k) {
       const double w = wn, u = un;
-      wp += SUPER_BLOCK;
-      up += SUPER_BLOCK;
+      wp += 32;
+      up += 32;
       if (k + 1 < ns) {
-        wn = *wp - rel[k + 1];
+        wn = *wp;
         un = *up;
       }
 #pragma unroll
@@ -483,21 +566,66 @@ __device__ __forceinline__ void super_levels(const double* __restrict__ Wc,
   }
 }
 
+// The same from TMEM columns (4 per sample), 2 samples per tcgen05.ld, the
+// next pair's load in flight while this one is scored.  Sample 0 is
+// (w, u) = (0, 0) and adds an exact +0, so the sums equal super_levels'.
+template <int METRIC, int J, typename Rec>
+__device__ __forceinline__ void super_levels_tmem(uint32_t taddr, const double* __restrict__ lv,
+                                                  int32_t n_steps, int L, int64_t ib, int64_t st,
+                                                  Rec& record) {
+  for (int j0 = 0; j0 < L; j0 += J) {
+    double av[J], acc[J];
+#pragma unroll
+    for (int jj = 0; jj < J; ++jj) {
+      av[jj] = lv[min(j0 + jj, L - 1)];
+      acc[jj] = 0.0;
+    }
+    uint32_t cur[8], nxt[8];
+    tmem_ld8(taddr, cur);
+    tmem_wait_ld(cur);
+    for (int32_t k0 = 0; k0 <= n_steps; k0 += 2) {
+      const bool more = k0 + 2 <= n_steps;
+      if (more) tmem_ld8(taddr + 4u * (uint32_t)(k0 + 2), nxt);
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        if (k0 + j <= n_steps) {
+          const double w = __hiloint2double((int)cur[4 * j + 1], (int)cur[4 * j + 0]);
+          const double u = __hiloint2double((int)cur[4 * j + 3], (int)cur[4 * j + 2]);
+#pragma unroll
+          for (int jj = 0; jj < J; ++jj) accumulate<METRIC>(acc[jj], fma(av[jj], u, w));
+        }
+      }
+      if (more) {
+        tmem_wait_ld(nxt);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) cur[r] = nxt[r];
+      }
+    }
+    const int jn = min(J, L - j0);
+#pragma unroll
+    for (int jj = 0; jj < J; ++jj)
+      if (jj < jn) record(finish_error<METRIC>(acc[jj], n_steps + 1), ib + (int64_t)(j0 + jj) * st);
+  }
+}
+
 // Direct evaluation of one node's levels (the lanes whose node is `bad`; all
 // lanes run the evaluator, whose segmented loop needs the full warp).  Out of
-// line, so its register peak stays out of the superposition loop's.
+// line, so its register peak stays out of the superposition loop's.  `stash`
+// is this warp's [10][32] double2 region.
 template <int METRIC>
 __device__ __noinline__ void super_direct(const FitArgs& a, int64_t sac, int64_t ib, bool bad,
                                           double Aprime, double pwd, double sgn,
                                           const double* rel, double* stash, double& best_e,
                                           int64_t& best_i, int64_t& nf) {
   const double INF = __longlong_as_double(0x7ff0000000000000LL);
+  // evaluate indexes its stash with threadIdx.x: shift the base to this warp
+  double* st = stash - 64 * (int)(threadIdx.x >> 5);
   for (int j = 0; j < a.sup_L; ++j) {
     const int64_t i = ib + (int64_t)j * a.sup_st;
     double q[NP];
     generate_grid_opc(a.space, i, q, a.exp_tab);
     const double E = evaluate<double, 0, METRIC, false>(q, a.ctl, Aprime, pwd, rel, nullptr, 0,
-                                                        sgn, nullptr, stash, false, blockDim.x);
+                                                        sgn, nullptr, st, false, 32);
     if (bad) {
       if (a.err_out) a.err_out[sac * a.err_ld + i] = E;
       nf += E < INF ? 1 : 0;
@@ -506,19 +634,35 @@ __device__ __noinline__ void super_direct(const FitArgs& a, int64_t sac, int64_t
   }
 }
 
-template <int METRIC>
-__global__ void __launch_bounds__(SUPER_BLOCK) fit_super_kernel(FitArgs a) {
+// One block per SM when TMEM warps are used (host pads shared memory); up to
+// SUPER_MAX_WARPS warps: warps 0..T-1 keep their columns in their TMEM
+// quadrant, warps T.. in shared memory.
+template <int METRIC, bool TM>
+__global__ void __launch_bounds__(TM ? SUPER_MAX_WARPS * 32 : 32) fit_super_kernel(FitArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ uint32_t s_tmem_base;
   const int32_t ns = a.ctl.n_steps + 1;
-  constexpr int B = SUPER_BLOCK;   // the launch block (the column layout assumes it)
-  const int tid = threadIdx.x;
+  const int B = blockDim.x;
+  const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+  const int T = TM ? a.sup_tm_warps : 0;   // TM = false: no tensor-memory code at all
+  const bool tm = TM && wid < T;
   const int L = a.sup_L;
   const bool ag = a.sup_dim == NSAC_AG;
   double* rel = reinterpret_cast<double*>(smem_raw);
   double* lv = rel + ((ns + 1) & ~1);
-  double* gt = lv + ((L + 1) & ~1);             // level tables of the grid dimensions
-  double* W = gt + ((a.sup_gt_n + 1) & ~1);     // [ns][B]: b_k
-  double* U = W + (size_t)ns * B;               // [ns][B]: u_k
+  double* gt = lv + ((L + 1) & ~1);                 // level tables of the grid dimensions
+  double* cols = gt + ((a.sup_gt_n + 1) & ~1);      // smem warps: [super_cols(ns)][32] each
+  double* rings = cols + super_cols(ns) * 32 * (size_t)(B / 32 - T);   // TMEM warps: [SUPER_RING] each
+  double* region = tm ? rings + (size_t)SUPER_RING * wid : cols + super_cols(ns) * 32 * (size_t)(wid - T);
+  if (TM && T > 0) {
+    if (wid == 0) {
+      const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&s_tmem_base);
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" :: "r"(dst)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  }
   const int64_t sac = (int64_t)blockIdx.y + a.sac_begin;
   const double amp = a.sac_ctl ? a.sac_ctl[2 * sac] : a.amplitude;
   const double pwd = a.sac_ctl ? a.sac_ctl[2 * sac + 1] : a.pw_default;
@@ -552,6 +696,11 @@ __global__ void __launch_bounds__(SUPER_BLOCK) fit_super_kernel(FitArgs a) {
     }
   }
   __syncthreads();
+  uint32_t taddr = 0;
+  if (TM && T > 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    taddr = s_tmem_base + ((uint32_t)(32 * (wid & 3)) << 16);
+  }
   const double INF = __longlong_as_double(0x7ff0000000000000LL);
   const double amax = fmax(fabs(lv[0]), fabs(lv[L - 1]));   // levels are monotone in j
   const int64_t st = a.sup_st, stL = a.sup_st * (int64_t)L;
@@ -618,26 +767,58 @@ __global__ void __launch_bounds__(SUPER_BLOCK) fit_super_kernel(FitArgs a) {
       Prop2<double> pb, pu;
       make_prop<double, false>(sb, pb);
       make_prop<double, false>(su, pu);
-      run_propagator_bu(pb, pu, s.n_pulse, a.ctl.n_steps, W + tid, U + tid, B, Sb, Su);
+      if (TM && tm) {
+        TmemSink sink{reinterpret_cast<double2*>(region) + lane, rel, taddr, a.ctl.n_steps, 0};
+        run_propagator_bu(pb, pu, s.n_pulse, a.ctl.n_steps, sink, Sb, Su);
+      } else {
+        SmemSink sink{region + lane, region + (size_t)ns * 32 + lane, rel};
+        run_propagator_bu(pb, pu, s.n_pulse, a.ctl.n_steps, sink, Sb, Su);
+      }
     }
     const bool ok = Sb + amax * Su <= SUPER_SAFE;   // false for NaN / inf
-    if (ok && valid) {
-      switch (a.sup_J) {   // register chunk width (host: least padding for L)
-        case 8: super_levels<METRIC, 8>(W + tid, U + tid, rel, lv, ns, B, L, ib, st, record); break;
-        case 12: super_levels<METRIC, 12>(W + tid, U + tid, rel, lv, ns, B, L, ib, st, record); break;
-        case 16: super_levels<METRIC, 16>(W + tid, U + tid, rel, lv, ns, B, L, ib, st, record); break;
-        case 20: super_levels<METRIC, 20>(W + tid, U + tid, rel, lv, ns, B, L, ib, st, record); break;
-        case 24: super_levels<METRIC, 24>(W + tid, U + tid, rel, lv, ns, B, L, ib, st, record); break;
-        case 28: super_levels<METRIC, 28>(W + tid, U + tid, rel, lv, ns, B, L, ib, st, record); break;
-        default: super_levels<METRIC, 32>(W + tid, U + tid, rel, lv, ns, B, L, ib, st, record); break;
+    // warp-uniform: the TMEM loads are .sync.aligned (lanes that skip still
+    // run the loop and drop their records)
+    const bool any_ok = __any_sync(0xffffffffu, ok && valid);
+    if (any_ok) {
+      const bool mine = ok && valid;
+      auto rec = [&](double E, int64_t i) { if (mine) record(E, i); };
+      if (TM && tm) {
+        switch (a.sup_J) {   // register chunk width (host: least padding for L)
+          case 8: super_levels_tmem<METRIC, 8>(taddr, lv, a.ctl.n_steps, L, ib, st, rec); break;
+          case 12: super_levels_tmem<METRIC, 12>(taddr, lv, a.ctl.n_steps, L, ib, st, rec); break;
+          case 16: super_levels_tmem<METRIC, 16>(taddr, lv, a.ctl.n_steps, L, ib, st, rec); break;
+          default: super_levels_tmem<METRIC, 20>(taddr, lv, a.ctl.n_steps, L, ib, st, rec); break;
+        }
+      } else if (mine) {
+        const double* Wc = region + lane;
+        const double* Uc = region + (size_t)ns * 32 + lane;
+        switch (a.sup_J) {   // the TMEM kernel uses J <= 20 (register budget of two loops)
+          case 8: super_levels<METRIC, 8>(Wc, Uc, lv, ns, L, ib, st, record); break;
+          case 12: super_levels<METRIC, 12>(Wc, Uc, lv, ns, L, ib, st, record); break;
+          case 16: super_levels<METRIC, 16>(Wc, Uc, lv, ns, L, ib, st, record); break;
+          case 20: super_levels<METRIC, 20>(Wc, Uc, lv, ns, L, ib, st, record); break;
+          case 24: if (!TM) { super_levels<METRIC, 24>(Wc, Uc, lv, ns, L, ib, st, record); break; }
+          case 28: if (!TM) { super_levels<METRIC, 28>(Wc, Uc, lv, ns, L, ib, st, record); break; }
+          default:
+            if (TM) super_levels<METRIC, 20>(Wc, Uc, lv, ns, L, ib, st, record);
+            else super_levels<METRIC, 32>(Wc, Uc, lv, ns, L, ib, st, record);
+            break;
+        }
       }
     }
     const bool bad = valid && !ok;
     if (__any_sync(0xffffffffu, bad)) {
-      __syncwarp();   // the columns are dead now: the evaluator's stash reuses them
-      super_direct<METRIC>(a, sac, ib, bad, Aprime, pwd, sgn, rel, W, best_e, best_i, nf);
+      __syncwarp();   // the region is dead now: the evaluator's stash reuses it
+      super_direct<METRIC>(a, sac, ib, bad, Aprime, pwd, sgn, rel, region, best_e, best_i, nf);
     }
     __syncwarp();   // the next node overwrites the columns
+  }
+  if (TM && T > 0) {   // every warp is done with TMEM: free it before the epilogue
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (wid == 0)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" :: "r"(s_tmem_base)
+                   : "memory");
   }
   fit_epilogue(a, sac, best_e, best_i, nf);
 }
@@ -1171,14 +1352,18 @@ const void* fit_kernel_ptr(int precision, int integrator, int metric) {
   return metric == 0 ? fit_fn<float, 1, 0>() : fit_fn<float, 1, 1>();
 }
 
-const void* fit_super_kernel_ptr(int metric) {
-  return metric == 0 ? reinterpret_cast<const void*>(&fit_super_kernel<0>)
-                     : reinterpret_cast<const void*>(&fit_super_kernel<1>);
+const void* fit_super_kernel_ptr(int metric, bool tmem) {
+  if (tmem)
+    return metric == 0 ? reinterpret_cast<const void*>(&fit_super_kernel<0, true>)
+                       : reinterpret_cast<const void*>(&fit_super_kernel<1, true>);
+  return metric == 0 ? reinterpret_cast<const void*>(&fit_super_kernel<0, false>)
+                     : reinterpret_cast<const void*>(&fit_super_kernel<1, false>);
 }
 
-size_t super_smem(int32_t ns, int32_t levels, int32_t gt_n, int block) {
+size_t super_smem(int32_t ns, int32_t levels, int32_t gt_n, int smem_warps, int tm_warps) {
   return ((size_t)((ns + 1) & ~1) + (size_t)((levels + 1) & ~1) + (size_t)((gt_n + 1) & ~1) +
-          super_cols(ns) * block) * sizeof(double);
+          super_cols(ns) * 32 * (size_t)smem_warps + (size_t)SUPER_RING * tm_warps) *
+         sizeof(double);
 }
 
 cudaError_t launch_fit(const void* fn, const FitArgs& a, dim3 grid, int block, size_t smem,

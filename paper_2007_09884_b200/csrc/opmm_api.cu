@@ -333,6 +333,17 @@ size_t max_dyn_smem(const void* fn) {
   return last;
 }
 
+// The opt-in limit less static shared memory, without kMaxDynSmem's cap.
+size_t max_dyn_smem_uncapped(const void* fn) {
+  cudaFuncAttributes fa;
+  int dev = 0, optin = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess ||
+      cudaFuncGetAttributes(&fa, fn) != cudaSuccess)
+    return 48 * 1024;
+  return (size_t)optin > fa.sharedSizeBytes ? (size_t)optin - fa.sharedSizeBytes : 0;
+}
+
 void allow_dyn_smem(const void* fn) {
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)max_dyn_smem(fn));
 }
@@ -490,10 +501,13 @@ opmm_status enqueue_fit_super(opmm_handle* h, const double* rec_dev, const opmm_
   // Otherwise one warp per block, shared memory only (occupancy decides).
   int tm_warps = 0, smem_warps = 1;
   if (ctl->n_steps <= opmm::SUPER_TMEM_MAX_STEPS && super_tmem_wanted(L)) {
+    // one block per SM: it may take all of the SM's shared memory
+    const size_t lim_tm = max_dyn_smem_uncapped(opmm::fit_super_kernel_ptr(metric, true));
     size_t fixed = opmm::super_smem(ns, L, gt_n, 0, 4);
     int sw = 0;
-    while (sw < opmm::SUPER_MAX_WARPS - 4 && opmm::super_smem(ns, L, gt_n, sw + 1, 4) <= lim) ++sw;
-    if (fixed <= lim) { tm_warps = 4; smem_warps = sw; }
+    while (sw < opmm::SUPER_MAX_WARPS - 4 && opmm::super_smem(ns, L, gt_n, sw + 1, 4) <= lim_tm)
+      ++sw;
+    if (fixed <= lim_tm) { tm_warps = 4; smem_warps = sw; }
   }
   const void* fn = opmm::fit_super_kernel_ptr(metric, tm_warps > 0);
   const int block = 32 * (tm_warps + smem_warps);
@@ -913,7 +927,9 @@ opmm_status opmm_create(opmm_handle** out, int device) {
         allow_dyn_smem(opmm::fit3_kernel_ptr(p, m));
         if (p == 0 && i == 0) {
           allow_dyn_smem(opmm::fit_super_kernel_ptr(m, false));
-          allow_dyn_smem(opmm::fit_super_kernel_ptr(m, true));
+          const void* f = opmm::fit_super_kernel_ptr(m, true);
+          cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)max_dyn_smem_uncapped(f));
         }
         allow_dyn_smem(opmm::simulate_kernel_ptr(p, i));
         allow_dyn_smem(opmm::score_kernel_ptr(p, m));

@@ -437,11 +437,15 @@ __global__ void __launch_bounds__(OPMM_FIT_LB_THREADS, OPMM_FIT_LB_BLOCKS) fit_k
 // columns are per warp), post-pulse coefficients in registers (REGSTASH).
 // ---------------------------------------------------------------------------
 constexpr double SUPER_SAFE = 1e6;     // deg; bounds the combination's rounding
-constexpr int SUPER_RING = 640;        // doubles per TMEM warp: the 8-sample staging ring
-                                       // (512) and, for blown-up nodes, evaluate's stash [10][32] double2
+constexpr int SUPER_RING = 512;        // doubles per TMEM warp: the 8-sample staging ring
 
-__host__ __device__ constexpr size_t super_cols(int32_t ns) {
-  return (size_t)(2 * ns > 20 ? 2 * ns : 20);   // W + U rows, or evaluate's stash [10] x double2
+// Shared-memory column rows per lane: W + U for samples 0..n (plain layout;
+// the dead columns double as evaluate's [10] x double2 stash for blown-up
+// nodes), or samples 1..n only (TMEM layout, where 8 warps must fit: sample 0
+// is (0, 0) and its blown-up nodes need no stash).
+__host__ __device__ constexpr size_t super_cols(int32_t ns, bool tm_layout = false) {
+  return tm_layout ? (size_t)(2 * (ns - 1) > 2 ? 2 * (ns - 1) : 2)
+                   : (size_t)(2 * ns > 20 ? 2 * ns : 20);
 }
 
 // ---- Tensor memory (tcgen05, sm_100a).  A warp may address only its own
@@ -476,13 +480,15 @@ __device__ __forceinline__ void tmem_wait_st() {
 
 // Column sinks of run_propagator_bu.  Both store w_k = b_k - rel_k (the
 // level loop's addend, computed once per node) and u_k.
-struct SmemSink {             // [ns][32] columns in shared memory (lane-strided)
-  double* W;
+template <bool SKIP0>
+struct SmemSink {             // lane-strided columns in shared memory: sample k at row k
+  double* W;                  // (SKIP0: row k - 1, sample 0 = (0, 0) not stored)
   double* U;
   const double* rel;
   __device__ __forceinline__ void put(int32_t k, double bk, double uk) {
-    W[k * 32] = bk - rel[k];
-    U[k * 32] = uk;
+    if (SKIP0 && k == 0) return;
+    W[(k - SKIP0) * 32] = bk - rel[k];
+    U[(k - SKIP0) * 32] = uk;
   }
   __device__ __forceinline__ void after_block(int32_t) {}
   __device__ __forceinline__ void finish() {}
@@ -530,7 +536,7 @@ struct TmemSink {             // 8-sample shared ring, flushed 4 samples at a ti
 // a compile-time constant so the inner loop is J unguarded (DFMA, DADD)
 // pairs per sample; a partial last chunk repeats level L-1 in its spare slots
 // and records only its own.
-template <int METRIC, int J, typename Rec>
+template <int METRIC, int J, bool SKIP0, typename Rec>
 __device__ __forceinline__ void super_levels(const double* __restrict__ Wc,
                                              const double* __restrict__ Uc,
                                              const double* __restrict__ lv, int32_t ns, int L,
@@ -545,8 +551,8 @@ __device__ __forceinline__ void super_levels(const double* __restrict__ Wc,
     // sample 0 contributes |0 - rel_0| = 0 (fit_kernel starts at k = 1 too).
     // The next sample's (w, u) is loaded one iteration ahead, so the shared
     // memory latency hides behind the J pairs of this one.
-    const double* __restrict__ wp = Wc + 32;
-    const double* __restrict__ up = Uc + 32;
+    const double* __restrict__ wp = Wc + (SKIP0 ? 0 : 32);   // sample 1
+    const double* __restrict__ up = Uc + (SKIP0 ? 0 : 32);
     double wn = *wp, un = *up;
     for (int32_t k = 1; k < ns; ++k) {
       const double w = wn, u = un;
@@ -609,23 +615,34 @@ __device__ __forceinline__ void super_levels_tmem(uint32_t taddr, const double* 
 }
 
 // Direct evaluation of one node's levels (the lanes whose node is `bad`; all
-// lanes run the evaluator, whose segmented loop needs the full warp).  Out of
-// line, so its register peak stays out of the superposition loop's.  `stash`
-// is this warp's [10][32] double2 region.
-template <int METRIC>
+// lanes run the recurrence, whose segmented loop needs the full warp).  Out
+// of line, so its register peak stays out of the superposition loop's.  The
+// arithmetic is evaluate()'s (same setup, same propagator, same FMA order);
+// the post-pulse coefficients stay in registers instead of a stash, so no
+// shared memory is needed -- bit-identical to fit_kernel's errors.
+template <int METRIC, bool STASH>
 __device__ __noinline__ void super_direct(const FitArgs& a, int64_t sac, int64_t ib, bool bad,
                                           double Aprime, double pwd, double sgn,
                                           const double* rel, double* stash, double& best_e,
                                           int64_t& best_i, int64_t& nf) {
   const double INF = __longlong_as_double(0x7ff0000000000000LL);
-  // evaluate indexes its stash with threadIdx.x: shift the base to this warp
-  double* st = stash - 64 * (int)(threadIdx.x >> 5);
   for (int j = 0; j < a.sup_L; ++j) {
     const int64_t i = ib + (int64_t)j * a.sup_st;
     double q[NP];
     generate_grid_opc(a.space, i, q, a.exp_tab);
-    const double E = evaluate<double, 0, METRIC, false>(q, a.ctl, Aprime, pwd, rel, nullptr, 0,
-                                                        sgn, nullptr, st, false, 32);
+    double E;
+    if (STASH) {   // the warp's dead columns as evaluate's [10][32] double2 stash
+      E = evaluate<double, 0, METRIC, false>(q, a.ctl, Aprime, pwd, rel, nullptr, 0, sgn, nullptr,
+                                             stash - 64 * (int)(threadIdx.x >> 5), false, 32);
+    } else {
+      Setup s;
+      make_setup(q, a.ctl.dt_ms, a.ctl.h, a.ctl.n_steps, Aprime, pwd, s);
+      Prop2<double> pr;
+      make_prop<double, false>(s, pr);
+      const double acc = run_propagator<double, METRIC, false, false, 1, true>(
+          pr, s.n_pulse, a.ctl.n_steps, rel, nullptr, 0, 0.0, 1.0, nullptr, 0);
+      E = finish_error<METRIC>(acc, a.ctl.n_steps + 1);
+    }
     if (bad) {
       if (a.err_out) a.err_out[sac * a.err_ld + i] = E;
       nf += E < INF ? 1 : 0;
@@ -652,8 +669,10 @@ __global__ void __launch_bounds__(TM ? SUPER_MAX_WARPS * 32 : 32) fit_super_kern
   double* lv = rel + ((ns + 1) & ~1);
   double* gt = lv + ((L + 1) & ~1);                 // level tables of the grid dimensions
   double* cols = gt + ((a.sup_gt_n + 1) & ~1);      // smem warps: [super_cols(ns)][32] each
-  double* rings = cols + super_cols(ns) * 32 * (size_t)(B / 32 - T);   // TMEM warps: [SUPER_RING] each
-  double* region = tm ? rings + (size_t)SUPER_RING * wid : cols + super_cols(ns) * 32 * (size_t)(wid - T);
+  const size_t wcols = super_cols(ns, TM) * 32;    // doubles per shared-memory warp
+  double* rings = cols + wcols * (size_t)(B / 32 - T);   // TMEM warps: [SUPER_RING] each
+  double* region = tm ? rings + (size_t)SUPER_RING * wid : cols + wcols * (size_t)(wid - T);
+  const int32_t urow = TM ? ns - 1 : ns;            // U's first row in a shared-memory region
   if (TM && T > 0) {
     if (wid == 0) {
       const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&s_tmem_base);
@@ -771,7 +790,7 @@ __global__ void __launch_bounds__(TM ? SUPER_MAX_WARPS * 32 : 32) fit_super_kern
         TmemSink sink{reinterpret_cast<double2*>(region) + lane, rel, taddr, a.ctl.n_steps, 0};
         run_propagator_bu(pb, pu, s.n_pulse, a.ctl.n_steps, sink, Sb, Su);
       } else {
-        SmemSink sink{region + lane, region + (size_t)ns * 32 + lane, rel};
+        SmemSink<TM> sink{region + lane, region + (size_t)urow * 32 + lane, rel};
         run_propagator_bu(pb, pu, s.n_pulse, a.ctl.n_steps, sink, Sb, Su);
       }
     }
@@ -791,25 +810,26 @@ __global__ void __launch_bounds__(TM ? SUPER_MAX_WARPS * 32 : 32) fit_super_kern
         }
       } else if (mine) {
         const double* Wc = region + lane;
-        const double* Uc = region + (size_t)ns * 32 + lane;
+        const double* Uc = region + (size_t)urow * 32 + lane;
         switch (a.sup_J) {   // the TMEM kernel uses J <= 20 (register budget of two loops)
-          case 8: super_levels<METRIC, 8>(Wc, Uc, lv, ns, L, ib, st, record); break;
-          case 12: super_levels<METRIC, 12>(Wc, Uc, lv, ns, L, ib, st, record); break;
-          case 16: super_levels<METRIC, 16>(Wc, Uc, lv, ns, L, ib, st, record); break;
-          case 20: super_levels<METRIC, 20>(Wc, Uc, lv, ns, L, ib, st, record); break;
-          case 24: if (!TM) { super_levels<METRIC, 24>(Wc, Uc, lv, ns, L, ib, st, record); break; }
-          case 28: if (!TM) { super_levels<METRIC, 28>(Wc, Uc, lv, ns, L, ib, st, record); break; }
+          case 8: super_levels<METRIC, 8, TM>(Wc, Uc, lv, ns, L, ib, st, record); break;
+          case 12: super_levels<METRIC, 12, TM>(Wc, Uc, lv, ns, L, ib, st, record); break;
+          case 16: super_levels<METRIC, 16, TM>(Wc, Uc, lv, ns, L, ib, st, record); break;
+          case 20: super_levels<METRIC, 20, TM>(Wc, Uc, lv, ns, L, ib, st, record); break;
+          case 24: if (!TM) { super_levels<METRIC, 24, TM>(Wc, Uc, lv, ns, L, ib, st, record); break; }
+          case 28: if (!TM) { super_levels<METRIC, 28, TM>(Wc, Uc, lv, ns, L, ib, st, record); break; }
           default:
-            if (TM) super_levels<METRIC, 20>(Wc, Uc, lv, ns, L, ib, st, record);
-            else super_levels<METRIC, 32>(Wc, Uc, lv, ns, L, ib, st, record);
+            if (TM) super_levels<METRIC, 20, TM>(Wc, Uc, lv, ns, L, ib, st, record);
+            else super_levels<METRIC, 32, TM>(Wc, Uc, lv, ns, L, ib, st, record);
             break;
         }
       }
     }
     const bool bad = valid && !ok;
     if (__any_sync(0xffffffffu, bad)) {
-      __syncwarp();   // the region is dead now: the evaluator's stash reuses it
-      super_direct<METRIC>(a, sac, ib, bad, Aprime, pwd, sgn, rel, region, best_e, best_i, nf);
+      // TMEM layout: no stash anywhere (its shared columns omit sample 0, and
+      // the rings are too small); plain layout: the warp's dead columns
+      super_direct<METRIC, !TM>(a, sac, ib, bad, Aprime, pwd, sgn, rel, region, best_e, best_i, nf);
     }
     __syncwarp();   // the next node overwrites the columns
   }
@@ -1362,7 +1382,7 @@ const void* fit_super_kernel_ptr(int metric, bool tmem) {
 
 size_t super_smem(int32_t ns, int32_t levels, int32_t gt_n, int smem_warps, int tm_warps) {
   return ((size_t)((ns + 1) & ~1) + (size_t)((levels + 1) & ~1) + (size_t)((gt_n + 1) & ~1) +
-          super_cols(ns) * 32 * (size_t)smem_warps + (size_t)SUPER_RING * tm_warps) *
+          super_cols(ns, tm_warps > 0) * 32 * (size_t)smem_warps + (size_t)SUPER_RING * tm_warps) *
          sizeof(double);
 }
 

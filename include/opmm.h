@@ -138,8 +138,9 @@ typedef struct {
                               levels): the trajectory is affine in it (RK4 of
                               the linear plant), so each grid node is integrated
                               twice and every level scored at 2 fp64 ops per
-                              sample.  Needs grid mode, the 18-parameter model,
-                              FP64, PROPAGATOR, no substeps, a physical space,
+                              sample (FP32: fp64 integration, fp32 level loop).
+                              Needs grid mode, the 18-parameter model,
+                              PROPAGATOR, no substeps, a physical space,
                               no certify, block_size = 0; else UNSUPPORTED.
                               Auto (0) picks it for such grids with >= 8
                               levels.  Errors equal variant 1's up to rounding

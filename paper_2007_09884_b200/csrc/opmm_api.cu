@@ -485,12 +485,14 @@ opmm_status enqueue_fit_super(opmm_handle* h, const double* rec_dev, const opmm_
   int64_t nb = 0, ne = nodes;
   if (shard) opmm_shard_range(nodes, h->rank, h->world, &nb, &ne);
   const int32_t ns = ctl->n_steps + 1;
-  const size_t lim = max_dyn_smem(opmm::fit_super_kernel_ptr(metric, false));
+  const int precision = opts ? opts->precision : OPMM_FP64;
+  const bool f32 = precision == OPMM_FP32;   // fp32 columns and level loop (plain layout)
+  const size_t lim = max_dyn_smem(opmm::fit_super_kernel_ptr(metric, false, f32));
   int32_t gt_n = 0;
   for (int d = 0; d < OPMM_NPARAM; ++d)
     if (d != sup_dim) gt_n += space->levels[d] > 1 ? space->levels[d] : 0;
   int32_t use_tab = 1;
-  if (gt_n > opmm::SUPER_MAX_GT || opmm::super_smem(ns, L, gt_n, 1, 0) > lim) {
+  if (gt_n > opmm::SUPER_MAX_GT || opmm::super_smem(ns, L, gt_n, 1, 0, f32) > lim) {
     gt_n = 0;   // generic generator per node
     use_tab = 0;
   }
@@ -500,18 +502,18 @@ opmm_status enqueue_fit_super(opmm_handle* h, const double* rec_dev, const opmm_
   // so one warp's latency-bound setup overlaps another's level loop).
   // Otherwise one warp per block, shared memory only (occupancy decides).
   int tm_warps = 0, smem_warps = 1;
-  if (ctl->n_steps <= opmm::SUPER_TMEM_MAX_STEPS && super_tmem_wanted(L)) {
+  if (!f32 && ctl->n_steps <= opmm::SUPER_TMEM_MAX_STEPS && super_tmem_wanted(L)) {
     // one block per SM: it may take all of the SM's shared memory
-    const size_t lim_tm = max_dyn_smem_uncapped(opmm::fit_super_kernel_ptr(metric, true));
+    const size_t lim_tm = max_dyn_smem_uncapped(opmm::fit_super_kernel_ptr(metric, true, false));
     size_t fixed = opmm::super_smem(ns, L, gt_n, 0, 4);
     int sw = 0;
     while (sw < opmm::SUPER_MAX_WARPS - 4 && opmm::super_smem(ns, L, gt_n, sw + 1, 4) <= lim_tm)
       ++sw;
     if (fixed <= lim_tm) { tm_warps = 4; smem_warps = sw; }
   }
-  const void* fn = opmm::fit_super_kernel_ptr(metric, tm_warps > 0);
+  const void* fn = opmm::fit_super_kernel_ptr(metric, tm_warps > 0, f32);
   const int block = 32 * (tm_warps + smem_warps);
-  size_t smem = opmm::super_smem(ns, L, gt_n, smem_warps, tm_warps);
+  size_t smem = opmm::super_smem(ns, L, gt_n, smem_warps, tm_warps, f32);
   // tensor memory is allocated whole (512 columns) per block: keep one block per SM
   // (two blocks need 2 x (smem + ~2 KB static/reserved) <= 228 KB of the SM)
   constexpr size_t kOneBlockSmem = 116 * 1024;
@@ -598,15 +600,15 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
     const int32_t la = space->levels[opmm::NSAC_AG], ln = space->levels[opmm::NSAC_ANT];
     if (la > 1 || ln > 1) sup_dim = la >= ln ? opmm::NSAC_AG : opmm::NSAC_ANT;
   }
-  const bool sup_ok = sup_dim >= 0 && precision == OPMM_FP64 && integ == OPMM_INTEG_PROPAGATOR &&
+  const bool sup_ok = sup_dim >= 0 && integ == OPMM_INTEG_PROPAGATOR &&
                       ctl->substeps <= 1 && space_dev.all_physical && !(opts && opts->certify) &&
                       !(opts && opts->block_size) && space->levels[sup_dim] <= opmm::SUPER_MAX_L &&
                       opmm::super_smem(ctl->n_steps + 1, space->levels[sup_dim], 0, 1, 0) <=
-                          max_dyn_smem(opmm::fit_super_kernel_ptr(metric, false));
+                          max_dyn_smem(opmm::fit_super_kernel_ptr(metric, false, false));
   if (kv_opt == 4 && !sup_ok)
     return fail(OPMM_ERR_UNSUPPORTED, "kernel_variant 4 needs a grid space (18-parameter model) "
                                       "with N_SAC_AG or N_SAC_ANT levels > 1 (<= %d), all "
-                                      "candidates physical, FP64, the propagator, no substeps, "
+                                      "candidates physical, the propagator, no substeps, "
                                       "no certify, the default block size and a trace that fits "
                                       "shared memory", opmm::SUPER_MAX_L);
   const bool superpose = kv_opt == 4 || (kv_opt == 0 && sup_ok && kAutoSuper &&
@@ -926,8 +928,9 @@ opmm_status opmm_create(opmm_handle** out, int device) {
         allow_dyn_smem(opmm::fit2_kernel_ptr(p, m));
         allow_dyn_smem(opmm::fit3_kernel_ptr(p, m));
         if (p == 0 && i == 0) {
-          allow_dyn_smem(opmm::fit_super_kernel_ptr(m, false));
-          const void* f = opmm::fit_super_kernel_ptr(m, true);
+          allow_dyn_smem(opmm::fit_super_kernel_ptr(m, false, false));
+          allow_dyn_smem(opmm::fit_super_kernel_ptr(m, false, true));
+          const void* f = opmm::fit_super_kernel_ptr(m, true, false);
           cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)max_dyn_smem_uncapped(f));
         }

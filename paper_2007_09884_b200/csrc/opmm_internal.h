@@ -160,11 +160,12 @@ int nm_group_problems_per_block();
 
 const void* fit_kernel_ptr(int precision, int integrator, int metric);
 // superposition over one pulse-height grid dimension (kernel_variant 4, fp64)
-const void* fit_super_kernel_ptr(int metric, bool tmem);
+const void* fit_super_kernel_ptr(int metric, bool tmem, bool fp32);
 constexpr int SUPER_MAX_WARPS = 8;   // per block: TMEM warps (<= 4, one per quadrant) + smem warps
 constexpr int SUPER_TMEM_MAX_STEPS = 120;   // 4 TMEM columns per sample, groups of 4, 512 columns
 constexpr int SUPER_MAX_L = 4096;    // levels of the superposed dimension
-size_t super_smem(int32_t n_samples, int32_t levels, int32_t gt_n, int smem_warps, int tm_warps);
+size_t super_smem(int32_t n_samples, int32_t levels, int32_t gt_n, int smem_warps, int tm_warps,
+                  bool fp32 = false);
 constexpr int32_t SUPER_MAX_GT = 2048;   // level-table entries kept in shared memory
 const void* fit2_kernel_ptr(int precision, int metric);   // 2 candidates/thread, 256 threads
 constexpr int FIT2_BLOCK = 256;

@@ -443,9 +443,11 @@ constexpr int SUPER_RING = 512;        // doubles per TMEM warp: the 8-sample st
 // the dead columns double as evaluate's [10] x double2 stash for blown-up
 // nodes), or samples 1..n only (TMEM layout, where 8 warps must fit: sample 0
 // is (0, 0) and its blown-up nodes need no stash).
-__host__ __device__ constexpr size_t super_cols(int32_t ns, bool tm_layout = false) {
+// (fp32 columns, `f32`: half the bytes; the region is counted in doubles.)
+__host__ __device__ constexpr size_t super_cols(int32_t ns, bool tm_layout = false,
+                                                bool f32 = false) {
   return tm_layout ? (size_t)(2 * (ns - 1) > 2 ? 2 * (ns - 1) : 2)
-                   : (size_t)(2 * ns > 20 ? 2 * ns : 20);
+                   : (f32 ? (size_t)(ns > 20 ? ns : 20) : (size_t)(2 * ns > 20 ? 2 * ns : 20));
 }
 
 // ---- Tensor memory (tcgen05, sm_100a).  A warp may address only its own
@@ -480,15 +482,15 @@ __device__ __forceinline__ void tmem_wait_st() {
 
 // Column sinks of run_propagator_bu.  Both store w_k = b_k - rel_k (the
 // level loop's addend, computed once per node) and u_k.
-template <bool SKIP0>
+template <bool SKIP0, typename TC>
 struct SmemSink {             // lane-strided columns in shared memory: sample k at row k
-  double* W;                  // (SKIP0: row k - 1, sample 0 = (0, 0) not stored)
-  double* U;
+  TC* W;                      // (SKIP0: row k - 1, sample 0 = (0, 0) not stored)
+  TC* U;                      // TC = float: the fp32 fit's columns (w rounded once from fp64)
   const double* rel;
   __device__ __forceinline__ void put(int32_t k, double bk, double uk) {
     if (SKIP0 && k == 0) return;
-    W[(k - SKIP0) * 32] = bk - rel[k];
-    U[(k - SKIP0) * 32] = uk;
+    W[(k - SKIP0) * 32] = (TC)(bk - rel[k]);
+    U[(k - SKIP0) * 32] = (TC)uk;
   }
   __device__ __forceinline__ void after_block(int32_t) {}
   __device__ __forceinline__ void finish() {}
@@ -536,26 +538,26 @@ struct TmemSink {             // 8-sample shared ring, flushed 4 samples at a ti
 // a compile-time constant so the inner loop is J unguarded (DFMA, DADD)
 // pairs per sample; a partial last chunk repeats level L-1 in its spare slots
 // and records only its own.
-template <int METRIC, int J, bool SKIP0, typename Rec>
-__device__ __forceinline__ void super_levels(const double* __restrict__ Wc,
-                                             const double* __restrict__ Uc,
+template <int METRIC, int J, bool SKIP0, typename TC, typename Rec>
+__device__ __forceinline__ void super_levels(const TC* __restrict__ Wc,
+                                             const TC* __restrict__ Uc,
                                              const double* __restrict__ lv, int32_t ns, int L,
                                              int64_t ib, int64_t st, Rec& record) {
   for (int j0 = 0; j0 < L; j0 += J) {
-    double av[J], acc[J];
+    TC av[J], acc[J];
 #pragma unroll
     for (int jj = 0; jj < J; ++jj) {
-      av[jj] = lv[min(j0 + jj, L - 1)];
-      acc[jj] = 0.0;
+      av[jj] = (TC)lv[min(j0 + jj, L - 1)];
+      acc[jj] = TC(0);
     }
     // sample 0 contributes |0 - rel_0| = 0 (fit_kernel starts at k = 1 too).
     // The next sample's (w, u) is loaded one iteration ahead, so the shared
     // memory latency hides behind the J pairs of this one.
-    const double* __restrict__ wp = Wc + (SKIP0 ? 0 : 32);   // sample 1
-    const double* __restrict__ up = Uc + (SKIP0 ? 0 : 32);
-    double wn = *wp, un = *up;
+    const TC* __restrict__ wp = Wc + (SKIP0 ? 0 : 32);   // sample 1
+    const TC* __restrict__ up = Uc + (SKIP0 ? 0 : 32);
+    TC wn = *wp, un = *up;
     for (int32_t k = 1; k < ns; ++k) {
-      const double w = wn, u = un;
+      const TC w = wn, u = un;
       wp += 32;
       up += 32;
       if (k + 1 < ns) {
@@ -654,8 +656,9 @@ __device__ __noinline__ void super_direct(const FitArgs& a, int64_t sac, int64_t
 // One block per SM when TMEM warps are used (host pads shared memory); up to
 // SUPER_MAX_WARPS warps: warps 0..T-1 keep their columns in their TMEM
 // quadrant, warps T.. in shared memory.
-template <int METRIC, bool TM>
+template <int METRIC, bool TM, typename TC>
 __global__ void __launch_bounds__(TM ? SUPER_MAX_WARPS * 32 : 32) fit_super_kernel(FitArgs a) {
+  static_assert(!TM || sizeof(TC) == 8, "the TMEM layout is fp64");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t s_tmem_base;
   const int32_t ns = a.ctl.n_steps + 1;
@@ -669,10 +672,11 @@ __global__ void __launch_bounds__(TM ? SUPER_MAX_WARPS * 32 : 32) fit_super_kern
   double* lv = rel + ((ns + 1) & ~1);
   double* gt = lv + ((L + 1) & ~1);                 // level tables of the grid dimensions
   double* cols = gt + ((a.sup_gt_n + 1) & ~1);      // smem warps: [super_cols(ns)][32] each
-  const size_t wcols = super_cols(ns, TM) * 32;    // doubles per shared-memory warp
+  const size_t wcols = super_cols(ns, TM, sizeof(TC) == 4) * 32;   // doubles per shared-memory warp
   double* rings = cols + wcols * (size_t)(B / 32 - T);   // TMEM warps: [SUPER_RING] each
   double* region = tm ? rings + (size_t)SUPER_RING * wid : cols + wcols * (size_t)(wid - T);
-  const int32_t urow = TM ? ns - 1 : ns;            // U's first row in a shared-memory region
+  const int32_t urow = TM ? ns - 1 : ns;            // U's first row (in TC) in a shared-memory region
+  TC* tcol = reinterpret_cast<TC*>(region);
   if (TM && T > 0) {
     if (wid == 0) {
       const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&s_tmem_base);
@@ -790,7 +794,7 @@ __global__ void __launch_bounds__(TM ? SUPER_MAX_WARPS * 32 : 32) fit_super_kern
         TmemSink sink{reinterpret_cast<double2*>(region) + lane, rel, taddr, a.ctl.n_steps, 0};
         run_propagator_bu(pb, pu, s.n_pulse, a.ctl.n_steps, sink, Sb, Su);
       } else {
-        SmemSink<TM> sink{region + lane, region + (size_t)urow * 32 + lane, rel};
+        SmemSink<TM, TC> sink{tcol + lane, tcol + (size_t)urow * 32 + lane, rel};
         run_propagator_bu(pb, pu, s.n_pulse, a.ctl.n_steps, sink, Sb, Su);
       }
     }
@@ -809,18 +813,18 @@ __global__ void __launch_bounds__(TM ? SUPER_MAX_WARPS * 32 : 32) fit_super_kern
           default: super_levels_tmem<METRIC, 20>(taddr, lv, a.ctl.n_steps, L, ib, st, rec); break;
         }
       } else if (mine) {
-        const double* Wc = region + lane;
-        const double* Uc = region + (size_t)urow * 32 + lane;
+        const TC* Wc = tcol + lane;
+        const TC* Uc = tcol + (size_t)urow * 32 + lane;
         switch (a.sup_J) {   // the TMEM kernel uses J <= 20 (register budget of two loops)
-          case 8: super_levels<METRIC, 8, TM>(Wc, Uc, lv, ns, L, ib, st, record); break;
-          case 12: super_levels<METRIC, 12, TM>(Wc, Uc, lv, ns, L, ib, st, record); break;
-          case 16: super_levels<METRIC, 16, TM>(Wc, Uc, lv, ns, L, ib, st, record); break;
-          case 20: super_levels<METRIC, 20, TM>(Wc, Uc, lv, ns, L, ib, st, record); break;
-          case 24: if (!TM) { super_levels<METRIC, 24, TM>(Wc, Uc, lv, ns, L, ib, st, record); break; }
-          case 28: if (!TM) { super_levels<METRIC, 28, TM>(Wc, Uc, lv, ns, L, ib, st, record); break; }
+          case 8: super_levels<METRIC, 8, TM, TC>(Wc, Uc, lv, ns, L, ib, st, record); break;
+          case 12: super_levels<METRIC, 12, TM, TC>(Wc, Uc, lv, ns, L, ib, st, record); break;
+          case 16: super_levels<METRIC, 16, TM, TC>(Wc, Uc, lv, ns, L, ib, st, record); break;
+          case 20: super_levels<METRIC, 20, TM, TC>(Wc, Uc, lv, ns, L, ib, st, record); break;
+          case 24: if (!TM) { super_levels<METRIC, 24, TM, TC>(Wc, Uc, lv, ns, L, ib, st, record); break; }
+          case 28: if (!TM) { super_levels<METRIC, 28, TM, TC>(Wc, Uc, lv, ns, L, ib, st, record); break; }
           default:
-            if (TM) super_levels<METRIC, 20, TM>(Wc, Uc, lv, ns, L, ib, st, record);
-            else super_levels<METRIC, 32, TM>(Wc, Uc, lv, ns, L, ib, st, record);
+            if (TM) super_levels<METRIC, 20, TM, TC>(Wc, Uc, lv, ns, L, ib, st, record);
+            else super_levels<METRIC, 32, TM, TC>(Wc, Uc, lv, ns, L, ib, st, record);
             break;
         }
       }
@@ -1372,18 +1376,22 @@ const void* fit_kernel_ptr(int precision, int integrator, int metric) {
   return metric == 0 ? fit_fn<float, 1, 0>() : fit_fn<float, 1, 1>();
 }
 
-const void* fit_super_kernel_ptr(int metric, bool tmem) {
+const void* fit_super_kernel_ptr(int metric, bool tmem, bool fp32) {
+  if (fp32)
+    return metric == 0 ? reinterpret_cast<const void*>(&fit_super_kernel<0, false, float>)
+                       : reinterpret_cast<const void*>(&fit_super_kernel<1, false, float>);
   if (tmem)
-    return metric == 0 ? reinterpret_cast<const void*>(&fit_super_kernel<0, true>)
-                       : reinterpret_cast<const void*>(&fit_super_kernel<1, true>);
-  return metric == 0 ? reinterpret_cast<const void*>(&fit_super_kernel<0, false>)
-                     : reinterpret_cast<const void*>(&fit_super_kernel<1, false>);
+    return metric == 0 ? reinterpret_cast<const void*>(&fit_super_kernel<0, true, double>)
+                       : reinterpret_cast<const void*>(&fit_super_kernel<1, true, double>);
+  return metric == 0 ? reinterpret_cast<const void*>(&fit_super_kernel<0, false, double>)
+                     : reinterpret_cast<const void*>(&fit_super_kernel<1, false, double>);
 }
 
-size_t super_smem(int32_t ns, int32_t levels, int32_t gt_n, int smem_warps, int tm_warps) {
+size_t super_smem(int32_t ns, int32_t levels, int32_t gt_n, int smem_warps, int tm_warps,
+                  bool fp32) {
   return ((size_t)((ns + 1) & ~1) + (size_t)((levels + 1) & ~1) + (size_t)((gt_n + 1) & ~1) +
-          super_cols(ns, tm_warps > 0) * 32 * (size_t)smem_warps + (size_t)SUPER_RING * tm_warps) *
-         sizeof(double);
+          super_cols(ns, tm_warps > 0, fp32) * 32 * (size_t)smem_warps +
+          (size_t)SUPER_RING * tm_warps) * sizeof(double);
 }
 
 cudaError_t launch_fit(const void* fn, const FitArgs& a, dim3 grid, int block, size_t smem,

@@ -184,9 +184,12 @@ def test_super_rejects_ineligible(opmm, h):
     with pytest.raises(opmm.OpmmError):
         opmm.opmm_fit(h, rec, ctl, sp, 1000, opmm.fit_options(kernel_variant=4))
     g = W.g4_space(per_dim=6)
-    with pytest.raises(opmm.OpmmError):   # fp32 is not superposed
+    with pytest.raises(opmm.OpmmError):   # the literal four-stage integrator is not superposed
         opmm.opmm_fit(h, rec, ctl, g, g.n_grid(),
-                      opmm.fit_options(precision=opmm.FP32, kernel_variant=4))
+                      opmm.fit_options(integrator=opmm.INTEG_RK4_STAGES, kernel_variant=4))
+    with pytest.raises(opmm.OpmmError):   # nor the certified fp32 fit (fit_kernel's top-8)
+        opmm.opmm_fit(h, rec, ctl, g, g.n_grid(),
+                      opmm.fit_options(precision=opmm.FP32, certify=1, kernel_variant=4))
 
 
 def test_super_generic_generator_path(opmm, h):
@@ -298,3 +301,36 @@ print("tmem-smem ok")
                        timeout=300)
     assert p.returncode == 0, p.stdout + p.stderr
     assert "tmem-smem ok" in p.stdout
+
+
+@pytest.mark.parametrize("metric", [0, 1])
+def test_super_fp32_columns_within_fp32_budget(opmm, h, metric):
+    """precision = FP32: b and u are integrated in fp64, stored as fp32
+    columns and scored in fp32.  North-star FP32 bar: errors
+    within 1e-4 relative of the fp64 oracle's, finite/+inf classification
+    identical, and the fp32 winner's fp64 error within 1e-4 of the best."""
+    ctl = W.Control()
+    rec = trace(ctl)
+    d = W.truth_opc()
+    sp = W.grid_space({
+        "K_SE_AG": (d[I["K_SE_AG"]] / 1.02 ** 2, d[I["K_SE_AG"]] * 1.02 ** 2, 5, True),
+        "B_AG": (d[I["B_AG"]] * 1e-3, d[I["B_AG"]] * 1.05 ** 2, 6, True),
+        "N_SAC_AG": (d[I["N_SAC_AG"]] / 1.01 ** 18, d[I["N_SAC_AG"]] * 1.01 ** 18, 37, True),
+        "PW": (30.0, 55.0, 6, False),
+    })
+    n = sp.n_grid()
+    err = torch.full((n,), -1.0, dtype=torch.float64, device="cuda")
+    r = opmm.opmm_fit(h, rec, ctl, sp, n, opmm.fit_options(precision=opmm.FP32, metric=metric,
+                                                           err_out=err, kernel_variant=4))
+    E = err.cpu().numpy()
+    o = oracle.fit(rec, ctl, sp, 0, n, metric=metric, want_err=True)
+    O = o["err"]
+    rel, _, _ = oracle.relativize(rec, ctl.amplitude_deg)
+    scale = np.abs(rel).sum() if metric == 0 else np.sqrt(np.mean(rel ** 2))
+    assert np.array_equal(np.isinf(E), np.isinf(O))
+    assert np.isinf(E).any()   # the stiff B_AG levels blow up (direct path)
+    f = np.isfinite(O)
+    assert (np.abs(E[f] - O[f]) / np.maximum(O[f], scale)).max() <= 1e-4
+    e64 = O[r["best_index"]]
+    assert e64 <= (1 + 1e-4) * o["best_err"] + 1e-4 * scale
+    assert r["n_finite"] == o["n_finite"]

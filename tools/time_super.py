@@ -33,8 +33,8 @@ with opmm.opmm_create(0) as h:
     for name, sp in grids:
         n = sp.n_grid()
         res = {}
-        for kv in (1, 4):
-            o = opmm.fit_options(cpu_check=0, kernel_variant=kv)
+        for kv, prec in ((1, opmm.FP64), (4, opmm.FP64), (-1, opmm.FP32), (-4, opmm.FP32)):
+            o = opmm.fit_options(cpu_check=0, kernel_variant=abs(kv), precision=prec)
             for _ in range(2):
                 opmm.opmm_fit_async(h, rec, ctl, sp, n, out, o)
             ms = []
@@ -47,4 +47,5 @@ with opmm.opmm_create(0) as h:
         print(f"{name:26s} N={n:.3e}: direct {res[1][0]:8.3f} ms  super {res[4][0]:8.3f} ms  "
               f"x{res[1][0] / res[4][0]:5.2f}  {n / res[4][0] * 1e3:.3e} cand/s  "
               f"same best {res[1][1] == res[4][1]} ({res[4][1]}, {res[4][2]:.6g} vs {res[1][2]:.6g})"
-              f"  nf {res[1][3]} {res[4][3]}", flush=True)
+              f"  nf {res[1][3]} {res[4][3]} | fp32: direct {res[-1][0]:7.3f} ms  super {res[-4][0]:7.3f} ms"
+              f" x{res[-1][0] / res[-4][0]:5.2f} best {res[-4][1]}", flush=True)

@@ -4,6 +4,10 @@
 //   fit_kernel         generate -> setup -> integrate+score -> argmin, fused;
 //                      warp shuffle -> shared -> per-block partial -> the last
 //                      block reduces the partials.
+//   fit_super_kernel   grid spaces with pulse-height levels: two integrations
+//                      per grid node (b, u), every level scored from
+//                      Delta-theta = b + a u; shared-memory
+//                      or tensor-memory (tcgen05) columns; fp64 or fp32 loop.
 //   merge_kernel       world > 1: lexicographic min of the gathered per-rank
 //                      partials + winner regeneration (a8).
 //   simscore_kernel    explicit OPC batch -> E per candidate (no trajectories).

@@ -101,16 +101,13 @@ constexpr int kAutoVariant = 1;
 constexpr bool kAutoSuper = true;
 constexpr int32_t kSuperMinLevels = 8;
 // The superposition kernel's tensor-memory layout (4 warps keep their
-// columns in TMEM, 7 warps per SM instead of 4) overlaps the per-node setup
-// with the level loop: faster below this many levels, slower above (3 of the
-// 4 schedulers then carry 2 level-loop warps).  Env
-// OPMM_SUPER_TMEM=0/1 forces it off/on (A/B timing, tests).
-constexpr int32_t kSuperTmemMaxLevels = 64;
-bool super_tmem_wanted(int32_t levels) {
+// columns in TMEM, 8 warps per SM instead of 4) overlaps one warp's
+// latency-bound per-node setup with another's level loop: faster than the
+// shared-memory layout at every level count measured.  Env
+// OPMM_SUPER_TMEM=0 forces the shared-memory layout (A/B timing, tests).
+bool super_tmem_wanted(int32_t /*levels*/) {
   const char* e = getenv("OPMM_SUPER_TMEM");
-  if (e && e[0] == '0') return false;
-  if (e && e[0] == '1') return true;
-  return levels < kSuperTmemMaxLevels;
+  return !(e && e[0] == '0');
 }
 
 }  // namespace

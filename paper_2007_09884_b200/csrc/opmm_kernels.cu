@@ -568,8 +568,14 @@ __device__ __forceinline__ void super_levels(const TC* __restrict__ Wc,
         wn = *wp;
         un = *up;
       }
+      // all J products first, then the J dependent accumulations (same
+      // operations per level as one fused statement; the scheduler sees J
+      // independent FMAs before the first add that waits on one)
+      TC d[J];
 #pragma unroll
-      for (int jj = 0; jj < J; ++jj) accumulate<METRIC>(acc[jj], fma(av[jj], u, w));
+      for (int jj = 0; jj < J; ++jj) d[jj] = fma(av[jj], u, w);
+#pragma unroll
+      for (int jj = 0; jj < J; ++jj) accumulate<METRIC>(acc[jj], d[jj]);
     }
     const int jn = min(J, L - j0);
 #pragma unroll
@@ -603,8 +609,11 @@ __device__ __forceinline__ void super_levels_tmem(uint32_t taddr, const double* 
         if (k0 + j <= n_steps) {
           const double w = __hiloint2double((int)cur[4 * j + 1], (int)cur[4 * j + 0]);
           const double u = __hiloint2double((int)cur[4 * j + 3], (int)cur[4 * j + 2]);
+          double d[J];   // products first, as in super_levels
 #pragma unroll
-          for (int jj = 0; jj < J; ++jj) accumulate<METRIC>(acc[jj], fma(av[jj], u, w));
+          for (int jj = 0; jj < J; ++jj) d[jj] = fma(av[jj], u, w);
+#pragma unroll
+          for (int jj = 0; jj < J; ++jj) accumulate<METRIC>(acc[jj], d[jj]);
         }
       }
       if (more) {

@@ -70,6 +70,12 @@ def ncu_traffic_bytes():
         return None
 
 
+def workload_config(per_gpu, world):
+    """The workload keys both arms' `config` share (configs[1])."""
+    return {"workload": workload_name(per_gpu, world), "n_candidates": per_gpu * world,
+            "per_gpu": per_gpu, "n_steps": N_STEPS, "dt_ms": 1.0, "metric": "L1"}
+
+
 def workload_name(per_gpu, world):
     return (f"configs[1]: single synthetic 10 deg horizontal saccade, 1 kHz, 100 ms, "
             f"{per_gpu:.0e} random OPC candidates per GPU over S_paper (x{world} GPUs)")
@@ -182,7 +188,8 @@ def run_reference(args):
             "unit": "candidate sims/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_name(PER_GPU, args.gpus),
+            "config": {**workload_config(args.per_gpu, args.gpus),
+                       "integrator": "rk4-classical (oracle)",
                        "reference_step": f"{sample} candidates of the workload per step (bounded sample)"},
             "cpu_baseline": {"value": value, "unit": "candidate sims/s", "cores": cores,
                              "kind": "oracle",
@@ -482,9 +489,8 @@ def run_gpu(args):
         "unit": "candidate sims/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms64, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_name(args.per_gpu, world), "n_candidates": n_total,
-                   "per_gpu": args.per_gpu, "n_steps": N_STEPS, "dt_ms": 1.0,
-                   "integrator": "rk4-propagator", "metric": "L1",
+        "config": {**workload_config(args.per_gpu, world),
+                   "integrator": "rk4-propagator",
                    "l2": "flushed between timed steps (512 MiB write, outside the events)",
                    "parallelism": f"candidates sharded x{world}, 1 ncclAllGather of 32 B/rank"},
         "clocks": clocks,

@@ -79,6 +79,9 @@ def lib():
         L.orc_expand_9param.argtypes = [dp]
         L.orc_expand_9param.restype = None
         L.orc_fit.restype = C.c_int64
+        L.orc_objective_batch.argtypes = [dp, C.c_int64, C.c_int64, dp, C.c_int32, C.c_double, C.c_int32,
+                                          C.c_double, C.c_double, C.c_int, C.c_int, dp]
+        L.orc_objective_batch.restype = None
         L.orc_max_threads.argtypes = []
         L.orc_max_threads.restype = C.c_int
         ip = C.POINTER(C.c_int)
@@ -243,6 +246,21 @@ def fit(rec, ctl, space, begin: int, end: int, metric: int = 0, saccade: int = 0
     if want_err:
         out["err"] = err
     return out
+
+
+def objective_batch(opc_soa, rec, ctl, metric: int = 0, nthreads: int = 1) -> np.ndarray:
+    """E of every column of an explicit SoA batch opc_soa [18, n] (e.g. a
+    generator dump): the per-candidate step of fit() on supplied inputs."""
+    o = np.ascontiguousarray(opc_soa, dtype=np.float64)
+    assert o.shape[0] == NPARAM
+    n = o.shape[1]
+    r, pr = _d(rec)
+    assert len(r) == ctl.n_steps + 1
+    err = np.zeros(n)
+    lib().orc_objective_batch(o.ctypes.data_as(C.POINTER(C.c_double)), n, n, pr, ctl.n_steps, ctl.dt_ms,
+                              _sub(ctl), ctl.amplitude_deg, ctl.pw_default_ms, metric, nthreads,
+                              err.ctypes.data_as(C.POINTER(C.c_double)))
+    return err
 
 
 def max_threads() -> int:

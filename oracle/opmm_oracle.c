@@ -425,6 +425,42 @@ int64_t orc_fit(const double* rec, int32_t n_steps, double dt_ms, int32_t subste
   return n_finite;
 }
 
+/* ------------------------------------------------------------------------ */
+/* Objective of an explicit batch of OPC vectors (SoA opc[d * ld + i]) against */
+/* one recorded trace: err_out[i] = orc_objective_sub(opc_i) -- the same      */
+/* definition as orc_fit's per-candidate step, with the  */
+/* candidates supplied instead of generated (e.g. a generator dump, so that   */
+/* both sides score bit-identical inputs).  No reduction.                     */
+/* ------------------------------------------------------------------------ */
+void orc_objective_batch(const double* opc, int64_t n, int64_t ld, const double* rec,
+                         int32_t n_steps, double dt_ms, int32_t substeps, double amplitude,
+                         double pw_default_ms, int metric, int nthreads, double* err_out) {
+  int32_t ns = n_steps + 1;
+  double* rel = (double*)malloc(sizeof(double) * (size_t)ns);
+  double s, Aprime;
+  int64_t i;
+  orc_relativize(rec, ns, amplitude, rel, &s, &Aprime);
+  if (nthreads < 1) nthreads = 1;
+#ifdef _OPENMP
+#pragma omp parallel num_threads(nthreads)
+#endif
+  {
+    double* buf = (double*)malloc(sizeof(double) * (size_t)ns);
+    double p[ORC_NP];
+    int d;
+#ifdef _OPENMP
+#pragma omp for schedule(static)
+#endif
+    for (i = 0; i < n; ++i) {
+      for (d = 0; d < ORC_NP; ++d) p[d] = opc[(int64_t)d * ld + i];
+      err_out[i] = orc_objective_sub(p, rel, n_steps, dt_ms, substeps, Aprime, pw_default_ms,
+                                     metric, buf);
+    }
+    free(buf);
+  }
+  free(rel);
+}
+
 int orc_max_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();

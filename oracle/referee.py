@@ -37,8 +37,12 @@ def rk4_spectral_radius(p, dt_ms: float, substeps: int = 1) -> float:
     return r
 
 
-def objective_longdouble(p, rec, ctl, metric: int = 0) -> float:
-    """E of one OPC, every operation in long double (same steps as the oracle)."""
+def objective_longdouble(p, rec, ctl, metric: int = 0, perturb=None) -> float:
+    """E of one OPC, every operation in long double (same steps as the oracle).
+    perturb (a numpy Generator): after every RK4 step each state component is
+    multiplied by (1 + r u), r ~ U[-1, 1], u = 2^-53 -- the effect of rounding
+    the state to fp64 once per step, on top of the long-double arithmetic
+    (stochastic-rounding estimate of what fp64 can resolve; fp64_spread)."""
     P = [L(x) for x in p]
     Kag, Kant, Lag, Lant, Bag, Bant, Bp, Ncag, Ncant, J = P[:10]
     F = P[14]
@@ -78,8 +82,29 @@ def objective_longdouble(p, rec, ctl, metric: int = 0) -> float:
             k3 = f(y + h / 2 * k2, *args)
             k4 = f(y + h * k3, *args)
             y = y + h / 6 * (k1 + 2 * k2 + 2 * k3 + k4)
+            if perturb is not None:
+                y = y * (L(1) + L(2.0 ** -53) * np.array(perturb.uniform(-1.0, 1.0, 6), dtype=L))
         d = (y[0] - th_s) - L(rel[k + 1])
         acc += abs(d) if metric == 0 else d * d
     if not acc < L(1e20):
         return float("inf")
     return float(acc) if metric == 0 else float(np.sqrt(acc / L(ctl.n_steps + 1)))
+
+
+def fp64_spread(p, rec, ctl, metric: int = 0, samples: int = 8, seed: int = 0) -> float:
+    """What an fp64 evaluation of this candidate's error can resolve: the
+    largest |E_k - E| over `samples` long-double evaluations whose state is
+    perturbed at fp64's unit roundoff after every step (objective_longdouble
+    with perturb), relative to max(E, s) with s the trace's error scale
+    (sum |rel| for L1, RMS(rel) for RMS).  For RK4-unstable candidates (spectral
+    radius > 1) the step map amplifies these perturbations geometrically; this
+    is the measured fp64 resolution that DESIGN.md reading Q22 uses as the
+    parity bar where it exceeds 1e-9."""
+    rel, _, _ = oracle.relativize(rec, ctl.amplitude_deg)
+    scale = float(np.abs(rel).sum()) if metric == 0 else float(np.sqrt(np.mean(rel ** 2)))
+    ref = objective_longdouble(p, rec, ctl, metric)
+    if not np.isfinite(ref):
+        return float("inf")
+    g = np.random.default_rng(seed)
+    d = [abs(objective_longdouble(p, rec, ctl, metric, perturb=g) - ref) for _ in range(samples)]
+    return max(d) / max(ref, scale)

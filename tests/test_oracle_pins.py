@@ -418,6 +418,38 @@ def test_penalty_spec_example():
     assert oracle.physical_penalty(q) == 1e10
 
 
+def test_penalty_g_clause_no_static_balance():
+    """Reading Q13's G > 0 clause: with N_C + K_LT = 0 on both muscles every
+    bound holds (those four are >= 0, not > 0) but the static gain G =
+    g_AG (N_C_AG + K_LT_AG) + g_ANT (N_C_ANT + K_LT_ANT) is 0, so the
+    fixation balance G theta = g_AG n_AG - g_ANT n_ANT has no unique solution
+    (hand-derived statics): penalty 1e10 (1 + 0).  Any
+    positive restoring term on either muscle restores G > 0."""
+    q = W.truth_opc()
+    for name in ("N_C_AG", "K_LT_AG", "N_C_ANT", "K_LT_ANT"):
+        q[I[name]] = 0.0
+    assert oracle.physical_penalty(q) == 1e10
+    assert oracle.objective(q, np.zeros(101), W.Control()) == 1e10
+    for name in ("N_C_AG", "K_LT_AG", "N_C_ANT", "K_LT_ANT"):
+        r = q.copy()
+        r[I[name]] = 1e-3
+        assert oracle.physical_penalty(r) == 0.0, name
+
+
+def test_objective_batch_equals_fit_errors():
+    """orc_objective_batch on supplied candidates (the generator's own values)
+    returns exactly fit()'s per-candidate errors, for any thread count."""
+    ctl = W.Control()
+    rec = oracle.positions(W.truth_opc(), ctl) + W.noise(101)
+    sp = W.paper_space()
+    N = 1500
+    full = oracle.fit(rec, ctl, sp, 7, 7 + N, want_err=True)
+    soa = oracle.generate_batch(sp, 7, N).T
+    for nt in (1, 4):
+        E = oracle.objective_batch(soa, rec, ctl, nthreads=nt)
+        assert np.array_equal(E, full["err"])
+
+
 def test_pulse_window_discretisation():
     g = read_golden_kv("spec_worked_examples.txt")
     assert 46.0 - 6.0 == g["pw_placeholder_46ms"]
@@ -640,6 +672,32 @@ def test_referee_longdouble_agrees_with_oracle_on_stable_candidates():
     # TRUTH on its own clean output: both ~0
     rec0 = oracle.positions(W.truth_opc(), ctl)
     assert referee.objective_longdouble(W.truth_opc(), rec0, ctl) < 1e-10
+
+
+def test_referee_fp64_spread_brackets_the_oracle():
+    """fp64_spread (long double with the state rounded stochastically at
+    fp64's unit roundoff each step) measures what fp64 can resolve: on a
+    stable candidate it is at the 1e-16 level (and the fp64 oracle sits inside
+    a small multiple of it); on the RK4-unstable 10^8-tail candidates of
+    DESIGN.md section 6 it is orders of magnitude larger, and the plain fp64
+    oracle's own deviation from the exact value is of the same order."""
+    from oracle import referee
+    ctl = W.Control()
+    rec = oracle.positions(W.truth_opc(), ctl) + W.noise(101)
+    rel, _, _ = oracle.relativize(rec, ctl.amplitude_deg)
+    scale = np.abs(rel).sum()
+    p = W.truth_opc()
+    s_stable = referee.fp64_spread(p, rec, ctl)
+    assert s_stable < 1e-14
+    sp = W.paper_space()
+    for i in (31760573, 79953948):   # rho ~ 1.33 / 1.78, errors ~1e5 / 1e14
+        q = oracle.generate(sp, i)
+        assert referee.rk4_spectral_radius(q, ctl.dt_ms) > 1.0
+        s = referee.fp64_spread(q, rec, ctl)
+        ref = referee.objective_longdouble(q, rec, ctl)
+        o = abs(oracle.objective(q, rec, ctl) - ref) / max(ref, scale)
+        assert s > 1e3 * s_stable and s > 1e-9
+        assert o <= 3 * s, (i, o, s)
 
 
 # --------------------------------------------------------------------------- 9-parameter model

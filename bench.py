@@ -425,10 +425,10 @@ def run_gpu(args):
     torch.cuda.synchronize()
 
     def device_leg(precision):
-        # fp32 runs with certification (top-8 re-scored in fp64)
-        # (certification is single-GPU: on N > 1 the fp32 leg is the plain fp32 sweep)
+        # fp32 runs with certification: the exact top-32 by fp32 error, merged
+        # over the ranks and re-scored in fp64
         opts = opmm.fit_options(precision=precision, cpu_check=0,
-                                certify=1 if (precision == opmm.FP32 and world == 1) else 0)
+                                certify=1 if precision == opmm.FP32 else 0)
         for _ in range(args.warmup):
             opmm.opmm_fit_async(h, rec_dev, ctl, sp, n_total, out_dev, opts)
         stream.synchronize()
@@ -509,9 +509,9 @@ def run_gpu(args):
                      / (kms64 * 1e-3) / (SMS * FP64_LANES * SM_MAX_MHZ * 1e6)},
         "fp32": {"value": n_total / (ms32 * 1e-3), "ms_per_step": ms32, "kernel_ms": kms32,
                  "best_index": res32["best_index"], "certified": res32["certified"],
-                 ("opt_err_fp64" if world == 1 else "opt_err_fp32"): res32["opt_err"],
-                 "mode": ("fp32 integrate+score, fp64 setup, top-8 certified by fp64 re-score"
-                          if world == 1 else "fp32 integrate+score, fp64 setup (uncertified on N > 1)")},
+                 "opt_err_fp64": res32["opt_err"],
+                 "mode": "fp32 integrate+score, fp64 setup, exact top-32 by fp32 error (merged "
+                         "over the ranks) re-scored in fp64 and certified"},
         "result": {"best_index": res64["best_index"], "opt_err": res64["opt_err"],
                    "n_finite": res64["n_finite"], "cpu_check": r["cpu_check"]},
     }

@@ -3,7 +3,10 @@
  * Fits a synthetic 10-degree saccade (a hand-written pulse-step-like ramp,
  * host memory) over 10^5 random OPC candidates of the paper's bounds
  * (log-uniform [0.1x, 10x] of Table 1; PW in [1, 100] ms),
- * prints the winner, and exercises the error path.  Build:
+ * prints the winner and its exact top-5, then runs the asynchronous entry
+ * points on HOST buffers (generate -> simulate -> score, and the fused
+ * simulate_score; the library stages them on the device and waits), checks
+ * that the two scores agree, and exercises the error path.  Build:
  *   gcc -O2 -I include examples/fit_c_abi.c -L paper_2007_09884_b200 -lopmm \
  *       -Wl,-rpath,'$ORIGIN/../paper_2007_09884_b200' -o build/fit_c_abi -lm
  */
@@ -58,6 +61,36 @@ int main(void) {
          (long long)r.n_evaluated);
   printf("K_SE_AG %.6f J %.8f PW %.4f\n", r.opc[OPMM_P_KSE_AG], r.opc[OPMM_P_J], r.opc[OPMM_P_PW]);
   if (!(fabs(r.cpu_check - r.opt_err) <= 1e-9 * r.opt_err)) return 4;
+  /* the exact top-5 (E, index) pairs of the same fit */
+  opts.top_k = 5;
+  opmm_fit_result r5;
+  st = opmm_fit(h, rec, &ctl, &sp, 100000, &opts, &r5);
+  if (st != OPMM_OK || r5.top_k != 5 || r5.topk_index[0] != r.best_index) return 6;
+  for (int k = 1; k < 5; ++k)
+    if (!(r5.topk_err[k - 1] < r5.topk_err[k] ||
+          (r5.topk_err[k - 1] == r5.topk_err[k] && r5.topk_index[k - 1] < r5.topk_index[k])))
+      return 7;
+  printf("top-5:");
+  for (int k = 0; k < 5; ++k) printf(" %lld (%.6f)", (long long)r5.topk_index[k], r5.topk_err[k]);
+  printf("\n");
+  /* host buffers through the asynchronous entry points */
+  enum { NC = 64 };
+  static double opc[OPMM_NPARAM * NC], traj[101 * NC], e_score[NC], e_fused[NC];
+  static uint8_t status[NC];
+  if ((st = opmm_generate(h, &sp, 0, 0, NC, opc, NC, NULL)) != OPMM_OK) return 8;
+  if ((st = opmm_simulate(h, opc, NC, NC, &ctl, OPMM_FP64, OPMM_INTEG_PROPAGATOR, traj, NC, status,
+                          NULL)) != OPMM_OK) return 9;
+  if ((st = opmm_score(h, traj, NC, NC, 101, rec, OPMM_FP64, OPMM_METRIC_L1, e_score, NULL)) != OPMM_OK)
+    return 10;
+  if ((st = opmm_simulate_score(h, opc, NC, NC, &ctl, rec, OPMM_FP64, OPMM_METRIC_L1,
+                                OPMM_INTEG_PROPAGATOR, e_fused, NULL)) != OPMM_OK) return 11;
+  int n_ok = 0;
+  for (int i = 0; i < NC; ++i) {
+    if (isinf(e_fused[i]) != isinf(e_score[i]) || (status[i] == 2) != (isinf(e_fused[i]) != 0)) return 12;
+    if (!isinf(e_fused[i]) && !(fabs(e_fused[i] - e_score[i]) <= 1e-12 * e_fused[i])) return 13;
+    n_ok += status[i] == 0;
+  }
+  printf("host buffers: %d candidates simulated + scored, %d finite, scores agree\n", NC, n_ok);
   /* invalid argument: error status + message, nothing launched */
   ctl.dt_ms = -1.0;
   st = opmm_fit(h, rec, &ctl, &sp, 10, &opts, &r);

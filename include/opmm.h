@@ -26,11 +26,19 @@
  *    it in opmm_destroy.  A handle is not thread-safe: calls on one handle are
  *    serialised on its stream.
  *  - "device" pointers must be CUDA device (or managed) memory on the handle's
- *    device; "host" pointers are ordinary host memory.  Asynchronous entry
- *    points (suffix _async, and simulate/score/simulate_score/generate) only
- *    enqueue work on `stream` (NULL = the handle's own stream, which is a
- *    non-blocking stream; pass cudaStreamLegacy, (void*)1, to order the work
- *    with the legacy default stream) and return.
+ *    device; "host" pointers are ordinary host memory; "host or device"
+ *    pointers are told apart with cudaPointerGetAttributes.
+ *    The entry points opmm_generate / simulate / simulate_batch / score /
+ *    simulate_score are asynchronous on `stream` (NULL = the handle's own
+ *    stream, which is a non-blocking stream; pass cudaStreamLegacy, (void*)1,
+ *    to order the work with the legacy default stream) when every buffer is
+ *    device memory: they enqueue and return.  A host input is copied into a
+ *    handle-owned device buffer on that stream; a host output is produced in
+ *    one (its current contents copied in first, so entries the call does not
+ *    write come back unchanged) and copied back, and the call then waits for
+ *    its stream, so host results are complete on return.  Staging buffers
+ *    are per handle: calls with host buffers on different streams of one
+ *    handle must be ordered by the caller.  opmm_fit_async is device-only.
  *  - Per-candidate numerical failure is data, not an error:
  *      non-physical OPC  -> E = 1e10 * (1 + sum of violations)  (D8)
  *      non-finite or E >= 1e20 accumulated -> E = +inf          (reading Q10)
@@ -141,32 +149,60 @@ typedef struct {
                               sample (FP32: fp64 integration, fp32 level loop).
                               Needs grid mode, the 18-parameter model,
                               PROPAGATOR, no substeps, a physical space,
-                              no certify, block_size = 0; else UNSUPPORTED.
-                              Auto (0) picks it for such grids with >= 8
-                              levels.  Errors equal variant 1's up to rounding
-                              (DESIGN.md section 7b).                           */
-  int32_t certify;      /* FP32 only: keep the 8 best candidates by fp32 error among
-                           every thread's best two, re-score them in fp64 and return
-                           the fp64-best; result.certified = 1 when the fp32 error
-                           budget (1e-4 relative) cannot have hidden the fp64 winner
-                           (single fit, one GPU, kernel_variant 0/1)    */
+                              no certify, no top_k, block_size = 0; else
+                              UNSUPPORTED.  Auto (0) picks it for such grids
+                              with >= 8 levels.  Errors equal variant 1's up to
+                              rounding (<= 1e-11 relative measured, DESIGN.md
+                              section 7b), so where two candidates' errors tie
+                              to within that rounding the returned index may
+                              differ from variant 1's; exact ties still go to
+                              the lowest index.                                 */
+  int32_t certify;      /* FP32 only ("solutions are sorted for accuracy",
+                           PAPER.md:251): keep the exact top-K by fp32 error
+                           (K = top_k, or 8 when top_k = 0), re-score those K in
+                           fp64 and return the fp64-best; result.certified says
+                           whether the list provably holds the fp64 winner
+                           (DESIGN.md section 6).  Works on one GPU and across the
+                           ranks of an NCCL handle (the ranks' lists are merged
+                           before the re-score); kernel_variant 0/1 only.        */
+  int32_t top_k;        /* 0 or 1..OPMM_MAX_TOPK: also return the K best (E, index)
+                           pairs of the fit, exact and in lexicographic order
+                           (reading Q12), over all candidates and ranks.
+                           kernel_variant 0/1 (auto never superposes then).     */
+  uint32_t flags;       /* OPMM_FIT_FLAG_* (measurement / test switches)          */
   double* err_out;      /* optional DEVICE [n]: E_i of every candidate (validation) */
 } opmm_fit_options;
 
+#define OPMM_MAX_TOPK 32
+/* opmm_fit_options.flags.  None changes any result; they select between
+ * equivalent code paths for measurement and for the tests that prove the
+ * equivalence. */
+#define OPMM_FIT_FLAG_NO_LANE_SORT   1u  /* fit_kernel: no pulse-end sort pre-pass    */
+#define OPMM_FIT_FLAG_SUPER_SMEM     2u  /* superposition: shared-memory columns only */
+#define OPMM_FIT_FLAG_NO_GRAPH       4u  /* opmm_fit: plain launches, no CUDA graph   */
+
 typedef struct {
   int64_t best_index;            /* global candidate index; -1 if no finite E     */
-  double opt_err;                /* E of the winner as computed by the kernel      */
+  double opt_err;                /* E of the winner as computed by the kernel
+                                    (certify: its fp64 re-score)                  */
   double cpu_check;              /* serial host fp64 re-score (Fig. 4 CPU_check)   */
   double opc[OPMM_NPARAM];       /* winner's OPC, exactly as evaluated on device   */
   int64_t n_finite;              /* candidates with finite E (all ranks)           */
   int64_t n_evaluated;           /* candidates evaluated (all ranks)               */
-  int32_t top_k;                 /* certify: 8 (entries below), else 0             */
-  int32_t certified;             /* certify: 1 if the fp64 winner is provably among
-                                    the fp32 top-8           */
-  int64_t topk_index[8];         /* certify: kept indices in (fp32 E, index) order;
-                                    -1 = unused.  Contains every candidate within
-                                    the certificate's T* when certified = 1      */
-  double topk_err[8];            /* certify: their fp64 errors                     */
+  int32_t top_k;                 /* entries used below (top_k, or the certify K)   */
+  int32_t certified;             /* certify: 1 if (a) every candidate whose fp32
+                                    error is <= T* = E32[0] + 2 delta is in the
+                                    list (delta = 1e-4 max(E32[0], s), s = sum|rel|
+                                    or RMS(rel)) and (b) every listed candidate's
+                                    fp32 and fp64 errors agree within delta.  Then
+                                    the fp64 winner is in the list -- and returned
+                                    -- unless its own fp32 error misses the budget
+                                    (possible only for RK4-unstable candidates,
+                                    whose rounding grows with the step; DESIGN.md
+                                    section 6 bounds it for stable ones)           */
+  int64_t topk_index[OPMM_MAX_TOPK]; /* kept indices in (E, index) order (certify:
+                                    fp32 E); -1 = unused                           */
+  double topk_err[OPMM_MAX_TOPK];    /* their errors (certify: fp64 re-scores)     */
 } opmm_fit_result;
 
 typedef struct opmm_handle opmm_handle;
@@ -180,8 +216,11 @@ opmm_status opmm_create(opmm_handle** h, int device);
 /* Multi-GPU: one process per GPU.  `nccl_id` is OPMM_NCCL_ID_BYTES produced by
  * opmm_nccl_unique_id on rank 0 and broadcast by the caller (e.g. through
  * torch.distributed).  Candidates are sharded disjointly per rank and the
- * per-rank (E, index) pairs are merged with one ncclAllGather of 24 bytes per
- * rank.  NCCL is loaded at run time (libnccl.so.2). */
+ * per-rank results are merged with one ncclAllGather per fit: 32 bytes per
+ * rank (E, index, n_finite, n_evaluated), 544 with top_k / certify (the
+ * rank's top-32 list).  world = 1 still creates a
+ * one-rank communicator, so the gather + merge path also runs on one GPU.
+ * NCCL is loaded at run time (libnccl.so.2). */
 opmm_status opmm_nccl_unique_id(uint8_t* nccl_id /* host, 128 B */);
 opmm_status opmm_create_nccl(opmm_handle** h, int device, const uint8_t* nccl_id,
                              int rank, int world);
@@ -200,28 +239,44 @@ opmm_status opmm_shard_range(int64_t n, int rank, int world, int64_t* begin, int
  * idx -1 entries are ignored; +inf never beats a finite E (reading Q12). */
 opmm_status opmm_merge_argmin(const double* err, const int64_t* idx, int count,
                               double* best_err, int64_t* best_idx);
+/* Merge `lists` sorted (E, index) lists of K entries each (list l at
+ * err/idx + l * K; index -1 marks unused entries) into the K lexicographically
+ * smallest pairs out_err/out_idx [K] (-1 / +inf where fewer exist).  The same
+ * function the merge kernel applies to the ranks' top-K lists (reading Q12). */
+opmm_status opmm_merge_topk(const double* err, const int64_t* idx, int lists, int K,
+                            double* out_err, int64_t* out_idx);
+/* The fp32 certificate (opmm_fit_result.certified) of one
+ * merged list: e32 [K] its fp32 errors (sorted), e64 [K] their fp64
+ * re-scores, idx [K] (-1 unused), scale s = sum |rel| (L1) or RMS(rel) (RMS).
+ * Returns certified and the fp64-best entry (lowest index on ties). */
+opmm_status opmm_certify_topk(const double* e32, const double* e64, const int64_t* idx, int K,
+                              double scale, int32_t* certified, int64_t* best_index,
+                              double* best_err);
 /* Validate a control / search space (the same checks every entry point runs). */
 opmm_status opmm_validate(const opmm_control* ctl, const opmm_search_space* space,
                           int64_t n_candidates);
 
 /* ---- hot path ------------------------------------------------------------- */
 /* Candidates [begin, begin+count) of `space` for saccade `saccade`, written
- * SoA to DEVICE opc_out[18][ld].  Bit-identical to what the fit kernel
- * evaluates for the same indices. */
+ * SoA to host-or-device opc_out[18][ld].  Bit-identical to what the fit
+ * kernel evaluates for the same indices. */
 opmm_status opmm_generate(opmm_handle* h, const opmm_search_space* space, uint32_t saccade,
                           int64_t begin, int64_t count, double* opc_out, int64_t ld,
                           void* stream);
 
-/* Simulate n explicit OPC vectors (DEVICE SoA opc[18][ld]) under `ctl`:
- * DEVICE traj[(n_steps+1) x ld_out] of `precision` (double or float) receives
- * absolute positions theta0 + s * Delta-theta_k (s = sign(A), D6 mirroring);
- * optional DEVICE status[n]: 0 ok, 1 non-physical (trajectory NaN), 2 diverged
- * (non-finite sample).  SPEC simulate. */
+/* Simulate n explicit OPC vectors (host-or-device SoA opc[18][ld]) under
+ * `ctl`: host-or-device traj[(n_steps+1) x ld_out] of `precision` (double or
+ * float) receives absolute positions theta0 + s * Delta-theta_k (s = sign(A),
+ * D6 mirroring); optional host-or-device status[n]: 0 ok, 1 non-physical
+ * (trajectory NaN), 2 diverged (non-finite sample).  SPEC simulate
+ * (SPEC.md:108-116); the model is opmm_simulate(opc_batch, control, dt,
+ * n_steps) -> trajectories of BASELINE.json's north_star. */
 opmm_status opmm_simulate(opmm_handle* h, const double* opc, int64_t n, int64_t ld,
                           const opmm_control* ctl, int32_t precision, int32_t integrator,
                           void* traj, int64_t ld_out, uint8_t* status, void* stream);
 
-/* opmm_simulate with one control per candidate: candidate i (column i) is
+/* opmm_simulate with one control per candidate (host-or-device opc, traj,
+ * status as opmm_simulate): candidate i (column i) is
  * simulated under HOST ctl[i] -- its own amplitude_deg, theta0_deg and
  * pw_default_ms; dt_ms and n_steps must be equal for all i (INVALID_ARG
  * otherwise).  Identical outputs to n single-candidate opmm_simulate calls;
@@ -232,17 +287,19 @@ opmm_status opmm_simulate_batch(opmm_handle* h, const double* opc, int64_t n, in
                                 const opmm_control* ctl, int32_t precision, int32_t integrator,
                                 void* traj, int64_t ld_out, uint8_t* status, void* stream);
 
-/* Score n stored trajectories (DEVICE traj[n_samples x ld] of `precision`)
- * against DEVICE recorded[n_samples] (fp64):  E_i = sum_k |traj_k,i - rec_k|
- * (L1) or sqrt(mean d^2) (RMS); accumulated >= 1e20 or non-finite -> +inf.
- * DEVICE err[n] (fp64).  The only HBM-bound entry point. */
+/* Score n stored trajectories (host-or-device traj[n_samples x ld] of
+ * `precision`) against host-or-device recorded[n_samples] (fp64):  E_i =
+ * sum_k |traj_k,i - rec_k| (L1, "absolute difference") or
+ * sqrt(mean d^2) (RMS); accumulated >= 1e20 or non-finite -> +inf.
+ * host-or-device err[n] (fp64).  The only HBM-bound entry point. */
 opmm_status opmm_score(opmm_handle* h, const void* traj, int64_t n, int64_t ld,
                        int32_t n_samples, const double* recorded, int32_t precision,
                        int32_t metric, double* err, void* stream);
 
-/* Fused simulate + score of n explicit OPC vectors against DEVICE
- * recorded[n_steps+1]; no trajectory reaches HBM.  E_i as in opmm_fit
- * (penalty for non-physical).  DEVICE err[n] (fp64). */
+/* Fused simulate + score of n explicit OPC vectors (host-or-device opc)
+ * against host-or-device recorded[n_steps+1] (a host trace must be finite:
+ * INVALID_ARG otherwise); no trajectory reaches HBM.  E_i as in opmm_fit
+ * (penalty for non-physical).  host-or-device err[n] (fp64). */
 opmm_status opmm_simulate_score(opmm_handle* h, const double* opc, int64_t n, int64_t ld,
                                 const opmm_control* ctl, const double* recorded,
                                 int32_t precision, int32_t metric, int32_t integrator,

@@ -24,9 +24,10 @@ using opmm::Partial;
 // ABI layout (mirrored by the ctypes binding; checked by tests/test_abi.py)
 static_assert(sizeof(opmm_control) == 40, "opmm_control layout");
 static_assert(sizeof(opmm_search_space) == 400, "opmm_search_space layout");
-static_assert(sizeof(opmm_fit_options) == 40, "opmm_fit_options layout");
-static_assert(sizeof(opmm_fit_result) == 320, "opmm_fit_result layout");
+static_assert(sizeof(opmm_fit_options) == 48, "opmm_fit_options layout");
+static_assert(sizeof(opmm_fit_result) == 704, "opmm_fit_result layout");
 static_assert(sizeof(Partial) == 32, "Partial layout");
+static_assert(sizeof(opmm::RankPartial) == 544, "RankPartial layout");
 static_assert(sizeof(opmm_nm_options) == 48, "opmm_nm_options layout");
 static_assert(sizeof(opmm_nm_result) == 176, "opmm_nm_result layout");
 
@@ -100,14 +101,15 @@ constexpr int kAutoVariant = 1;
 // grids with at least this many pulse-height levels
 constexpr bool kAutoSuper = true;
 constexpr int32_t kSuperMinLevels = 8;
+// certify's list length when top_k = 0
+constexpr int kCertifyK = 8;
 // The superposition kernel's tensor-memory layout (4 warps keep their
 // columns in TMEM, 8 warps per SM instead of 4) overlaps one warp's
 // latency-bound per-node setup with another's level loop: faster than the
-// shared-memory layout at every level count measured.  Env
-// OPMM_SUPER_TMEM=0 forces the shared-memory layout (A/B timing, tests).
-bool super_tmem_wanted(int32_t /*levels*/) {
-  const char* e = getenv("OPMM_SUPER_TMEM");
-  return !(e && e[0] == '0');
+// shared-memory layout at every level count measured.
+// OPMM_FIT_FLAG_SUPER_SMEM forces the shared-memory layout (A/B timing, tests).
+bool super_tmem_wanted(const opmm_fit_options* opts) {
+  return !(opts && (opts->flags & OPMM_FIT_FLAG_SUPER_SMEM));
 }
 
 }  // namespace
@@ -142,12 +144,20 @@ struct opmm_handle {
   int occ_block = 0;
   size_t occ_smem = 0;
   int occ_per_sm = 0;
-  Partial* rank_part = nullptr;
+  opmm::RankPartial* rank_part = nullptr;   // world > 1: this rank's result per saccade
   size_t rank_part_cap = 0;
-  Partial* gathered = nullptr;
+  opmm::RankPartial* gathered = nullptr;    // all ranks' results (packed, 32 or 544 B each)
   size_t gathered_cap = 0;
-  opmm::CertPartial* cert_parts = nullptr;
-  size_t cert_parts_cap = 0;
+  void* stage[4] = {nullptr, nullptr, nullptr, nullptr};   // host-pointer staging (Staging)
+  size_t stage_cap[4] = {0, 0, 0, 0};
+  double* tk_e = nullptr;                   // top-K: per-block lists [S][grid][32]
+  size_t tk_e_cap = 0;
+  int64_t* tk_i = nullptr;
+  size_t tk_i_cap = 0;
+  unsigned int* tk_counters = nullptr;      // top-K: topk_kernel tickets + fill counts [2][S]
+  size_t tk_counters_cap = 0;
+  double* tk_err = nullptr;                 // top-K: the fit's errors when err_out is not given
+  size_t tk_err_cap = 0;
   opmm_fit_result* result = nullptr;
   size_t result_cap = 0;
   opmm_fit_result* result_host = nullptr;  // pinned
@@ -370,6 +380,57 @@ bool is_device_ptr(const void* p) {
   return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+// Host-or-device buffers of the asynchronous entry points (SURVEY 8(b):
+// "pointers may be host or device; the library detects which with
+// cudaPointerGetAttributes").  A device (or managed) pointer is used in place.
+// A host input is copied into a handle-owned device buffer on the call's
+// stream; a host output is staged the same way (its current contents copied
+// in first, so entries the kernel does not write -- padding columns, skipped
+// statuses -- come back unchanged) and copied back after the kernel, and the
+// call then synchronises the stream so the results are in the caller's memory
+// when it returns.  One staging slot per argument position.
+struct Staging {
+  opmm_handle* h;
+  cudaStream_t st;
+  struct Out { void* host; void* dev; size_t bytes; };
+  Out outs[3];
+  int n_out = 0;
+  Staging(opmm_handle* hh, cudaStream_t s) : h(hh), st(s) {}
+  opmm_status slot(int k, size_t bytes) {
+    if (bytes <= h->stage_cap[k]) return OPMM_OK;
+    if (h->stage[k]) {
+      CK(cudaStreamSynchronize(st));   // the old buffer may still be in use
+      cudaFree(h->stage[k]);
+    }
+    h->stage[k] = nullptr;
+    h->stage_cap[k] = 0;
+    CK(cudaMalloc(&h->stage[k], bytes));
+    h->stage_cap[k] = bytes;
+    return OPMM_OK;
+  }
+  template <typename P>
+  opmm_status in(P* p, size_t bytes, int k, P** dev) {
+    *dev = p;
+    if (p == nullptr || bytes == 0 || is_device_ptr(p)) return OPMM_OK;
+    CKS(slot(k, bytes));
+    CK(cudaMemcpyAsync(h->stage[k], p, bytes, cudaMemcpyHostToDevice, st));
+    *dev = static_cast<P*>(h->stage[k]);
+    return OPMM_OK;
+  }
+  template <typename P>
+  opmm_status out(P* p, size_t bytes, int k, P** dev) {
+    CKS(in(p, bytes, k, dev));
+    if (*dev != p) outs[n_out++] = Out{(void*)p, (void*)*dev, bytes};
+    return OPMM_OK;
+  }
+  opmm_status finish() {
+    for (int j = 0; j < n_out; ++j)
+      CK(cudaMemcpyAsync(outs[j].host, outs[j].dev, outs[j].bytes, cudaMemcpyDeviceToHost, st));
+    if (n_out > 0) CK(cudaStreamSynchronize(st));
+    return OPMM_OK;
+  }
+};
+
 int check_precision(int32_t p) { return p == OPMM_FP64 || p == OPMM_FP32; }
 
 size_t sim_smem(int precision, int32_t n_samples, int block, bool with_rel) {
@@ -440,8 +501,18 @@ struct FitLaunch {
   opmm::FitArgs a;
 };
 
+// topk_kernel blocks per saccade: enough 256-thread blocks to stream the
+// errors at HBM speed (a few batches of 32 per warp), at most one per SM for
+// a single fit (the last block stages every block's list in shared memory)
+int topk_blocks(opmm_handle* h, int64_t n, int64_t S) {
+  const int64_t want = (n + 8 * opmm::TOPK_BLOCK - 1) / (8 * opmm::TOPK_BLOCK);
+  const int64_t cap = S > 1 ? 16 : h->num_sms;
+  return (int)(want < 1 ? 1 : (want > cap ? cap : want));
+}
+
 // Shared tail of every fit enqueue: the launch(es), then for world > 1 the
-// 32-byte all-gather and the merge kernel.
+// all-gather of the rank results (32 bytes each, 544 with top-K lists) and
+// the merge kernel.
 opmm_status launch_fit_and_merge(opmm_handle* h, const void* fn, opmm::FitArgs& a, int grid,
                                  int block, size_t smem, int64_t s_begin, int64_t S, bool multi,
                                  opmm_fit_result* out_dev) {
@@ -451,16 +522,28 @@ opmm_status launch_fit_and_merge(opmm_handle* h, const void* fn, opmm::FitArgs& 
     a.sac_begin = s_begin + s0;
     CK(opmm::launch_fit(fn, a, dim3(grid, (unsigned)sn), block, smem, h->stream));
   }
+  if (a.topk) {   // exact top-K (+ certificate) from the errors the fit wrote
+    a.sac_begin = s_begin;
+    a.fit_grid = grid;
+    const int tb = topk_blocks(h, a.end - a.begin, S);
+    CK(opmm::launch_topk(a, tb, (int)S, opmm::topk_smem(tb), (int)a.metric_, h->stream));
+    if (a.certify && !multi)
+      CK(opmm::launch_cert(a, (int)S, opmm::cert_scratch_bytes(a.ctl.n_steps + 1), (int)a.metric_,
+                           h->stream));
+  }
   CKS(record_stop(h, h->stream));
   if (multi) {
-    // one exchange step: 32-byte (E, index, n_finite, n_evaluated) per rank
+    // the one exchange step per saccade
     NcclApi& api = nccl();
+    const size_t bytes = a.topk ? sizeof(opmm::RankPartial) : sizeof(Partial);
+    const int metric = (int)a.metric_;
+    const size_t msmem = a.certify ? opmm::cert_scratch_bytes(a.ctl.n_steps + 1) : 0;
     for (int64_t s = 0; s < S; ++s) {
-      ncclResult_t r = api.allGather(h->rank_part + s_begin + s, h->gathered, sizeof(Partial),
-                                     ncclUint8, h->comm, h->stream);
+      ncclResult_t r = api.allGather(h->rank_part + s_begin + s, h->gathered, bytes, ncclUint8,
+                                     h->comm, h->stream);
       if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather");
-      CK(opmm::launch_merge(h->gathered, h->world, a.space, (uint32_t)(s_begin + s), out_dev + s,
-                            h->exp_tab, h->stream));
+      CK(opmm::launch_merge(a, h->gathered, h->world, bytes, s_begin + s, out_dev + s, metric, msmem,
+                            h->stream));
     }
   }
   return OPMM_OK;
@@ -499,7 +582,7 @@ opmm_status enqueue_fit_super(opmm_handle* h, const double* rec_dev, const opmm_
   // so one warp's latency-bound setup overlaps another's level loop).
   // Otherwise one warp per block, shared memory only (occupancy decides).
   int tm_warps = 0, smem_warps = 1;
-  if (!f32 && ctl->n_steps <= opmm::SUPER_TMEM_MAX_STEPS && super_tmem_wanted(L)) {
+  if (!f32 && ctl->n_steps <= opmm::SUPER_TMEM_MAX_STEPS && super_tmem_wanted(opts)) {
     // one block per SM: it may take all of the SM's shared memory
     const size_t lim_tm = max_dyn_smem_uncapped(opmm::fit_super_kernel_ptr(metric, true, false));
     size_t fixed = opmm::super_smem(ns, L, gt_n, 0, 4);
@@ -531,6 +614,7 @@ opmm_status enqueue_fit_super(opmm_handle* h, const double* rec_dev, const opmm_
   }
   opmm::FitArgs a;
   std::memset(&a, 0, sizeof(a));
+  a.metric_ = metric;
   a.rec = rec_dev;
   a.exp_tab = h->exp_tab;
   a.ctl = make_ctl(ctl);
@@ -543,6 +627,7 @@ opmm_status enqueue_fit_super(opmm_handle* h, const double* rec_dev, const opmm_
   a.end = (ne - nb) * (int64_t)L;
   a.err_out = opts ? opts->err_out : nullptr;
   a.err_ld = n_candidates;
+  a.err_base = 0;
   a.partials = h->partials;
   a.counters = h->counters;
   a.rank_out = multi ? h->rank_part : nullptr;
@@ -585,10 +670,17 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
   const int metric = opts ? opts->metric : OPMM_METRIC_L1;
   const int integ = opts ? opts->integrator : OPMM_INTEG_PROPAGATOR;
   const int kv_opt = opts ? opts->kernel_variant : 0;
+  const int top_k = opts ? opts->top_k : 0;
   if (!check_precision(precision)) return fail(OPMM_ERR_INVALID_ARG, "bad precision %d", precision);
   if (metric != 0 && metric != 1) return fail(OPMM_ERR_INVALID_ARG, "bad metric %d", metric);
   if (integ != 0 && integ != 1) return fail(OPMM_ERR_INVALID_ARG, "bad integrator %d", integ);
   if (kv_opt < 0 || kv_opt > 4) return fail(OPMM_ERR_INVALID_ARG, "kernel_variant must be 0..4");
+  if (top_k < 0 || top_k > OPMM_MAX_TOPK)
+    return fail(OPMM_ERR_INVALID_ARG, "top_k must be in [0, %d] (got %d)", OPMM_MAX_TOPK, top_k);
+  // FP32 certification: the exact top-K by fp32 error (K = top_k, or 32),
+  // re-scored in fp64 by the finishing block (or, world > 1, the merge kernel)
+  const bool certify = opts && opts->certify && precision == OPMM_FP32;
+  const int K = certify ? (top_k > 0 ? top_k : kCertifyK) : top_k;
   const opmm::SpaceDev space_dev = make_space(space);
   // variant 4: superposition over the grid levels of a pulse height (fp64
   // propagator, 18-parameter grid, physical space)
@@ -598,7 +690,7 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
     if (la > 1 || ln > 1) sup_dim = la >= ln ? opmm::NSAC_AG : opmm::NSAC_ANT;
   }
   const bool sup_ok = sup_dim >= 0 && integ == OPMM_INTEG_PROPAGATOR &&
-                      ctl->substeps <= 1 && space_dev.all_physical && !(opts && opts->certify) &&
+                      ctl->substeps <= 1 && space_dev.all_physical && !certify && K == 0 &&
                       !(opts && opts->block_size) && space->levels[sup_dim] <= opmm::SUPER_MAX_L &&
                       opmm::super_smem(ctl->n_steps + 1, space->levels[sup_dim], 0, 1, 0) <=
                           max_dyn_smem(opmm::fit_super_kernel_ptr(metric, false, false));
@@ -606,8 +698,8 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
     return fail(OPMM_ERR_UNSUPPORTED, "kernel_variant 4 needs a grid space (18-parameter model) "
                                       "with N_SAC_AG or N_SAC_ANT levels > 1 (<= %d), all "
                                       "candidates physical, the propagator, no substeps, "
-                                      "no certify, the default block size and a trace that fits "
-                                      "shared memory", opmm::SUPER_MAX_L);
+                                      "no certify or top_k, the default block size and a trace "
+                                      "that fits shared memory", opmm::SUPER_MAX_L);
   const bool superpose = kv_opt == 4 || (kv_opt == 0 && sup_ok && kAutoSuper &&
                                          space->levels[sup_dim] >= kSuperMinLevels);
   if (superpose)
@@ -623,28 +715,24 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
                                       "substeps", kv_opt);
   const int kv = kv_opt == 0 ? (special_ok ? kAutoVariant : 1) : kv_opt;
   const bool two = kv == 2, three = kv == 3;
+  if ((two || three) && K > 0)
+    return fail(OPMM_ERR_UNSUPPORTED, "top_k / certify need kernel_variant 0 or 1");
   const int block = three ? opmm::FIT3_BLOCK : two ? opmm::FIT2_BLOCK
                         : ((opts && opts->block_size) ? opts->block_size : kDefaultBlock);
   CKS(check_block(block));
   int64_t b = 0, e = n_candidates;
   if (shard) opmm_shard_range(n_candidates, h->rank, h->world, &b, &e);
   const int32_t ns = ctl->n_steps + 1;
-  // FP32 certification (top-8 + fp64 re-score): single fit on one GPU, fit1
-  const bool certify = opts && opts->certify && precision == OPMM_FP32;
-  constexpr int kCertMaxGrid = 256;
-  if (certify && (two || three || S != 1 || (shard && h->comm != nullptr)))
-    return fail(OPMM_ERR_UNSUPPORTED, "certify needs a single fit on one GPU with kernel_variant 0/1");
   size_t smem = three ? opmm::fit3_smem(precision, ns) : fit_smem(precision, ns, block, two ? 2 : 1);
-  if (certify) smem += opmm::cert_scratch_bytes(block, kCertMaxGrid, ns);
   if (smem > kMaxDynSmem) return fail(OPMM_ERR_INVALID_ARG, "trace too long for shared memory");
   const void* fn = three ? opmm::fit3_kernel_ptr(precision, metric)
                          : two ? opmm::fit2_kernel_ptr(precision, metric)
                                : opmm::fit_kernel_ptr(precision, kernel_integ(integ, ctl), metric);
   const bool one = !two && !three;
-  const size_t perm_off = (smem + 15) & ~(size_t)15;   // fit_kernel's super-tile arrays follow
-  // fit_kernel: the pre-pass key/rank scratch aliases the coefficient stash
-  // (at stash_off) when the stash holds it, else it follows the permutation
-  // fit_kernel layout: rel, exp table, stash (opmm_kernels.cu)
+  // fit_kernel dynamic shared memory: rel, exp table, stash (opmm_kernels.cu),
+  // then the super-tile permutation and the pre-pass key/rank scratch
+  // (aliased onto the stash when it fits there)
+  const size_t perm_off = (smem + 15) & ~(size_t)15;
   const size_t stash_off = (precision == OPMM_FP64 ? opmm::rel_bytes<double>(ns)
                                                    : opmm::rel_bytes<float>(ns)) +
                            opmm::exp_tab_bytes();
@@ -675,7 +763,6 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
     grid = (int)(tiles < 65535 ? (tiles > 0 ? tiles : 1) : 65535);
   }
   if (e <= b) grid = 1;  // empty shard: one block reports "no candidate"
-  if (certify && grid > kCertMaxGrid) grid = kCertMaxGrid;  // bounds the last block's smem staging
   // fit_kernel super-tile: an equal share of the range per block, multiple of
   // 32, at most SUPER_MAX (larger ranges take several persistent passes)
   int64_t super = 32;
@@ -686,15 +773,37 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
     if (super > super_cap) super = super_cap;
     smem = fit_dyn(super);
   }
-  const bool multi = shard && h->comm != nullptr;   // world > 1 (or a 1-rank test comm)
+  const bool multi = shard && h->comm != nullptr;   // world > 1 (or a 1-rank communicator)
   CKS(ensure(h->partials, h->partials_cap, (size_t)grid * (size_t)(s_begin + S)));
   CKS(ensure(h->counters, h->counters_cap, (size_t)(s_begin + S), true));
+  // top-K / certify: the fit writes every error (the caller's err_out, or a
+  // handle workspace of 8 bytes per candidate of this rank), topk_kernel
+  // selects from it
+  double* err_buf = opts ? opts->err_out : nullptr;
+  int64_t err_ld = n_candidates, err_base = 0;
+  if (K > 0) {
+    const int tb = topk_blocks(h, e - b, S);
+    CKS(ensure(h->tk_e, h->tk_e_cap, (size_t)tb * (size_t)(s_begin + S) * opmm::TOPK));
+    CKS(ensure(h->tk_i, h->tk_i_cap, (size_t)tb * (size_t)(s_begin + S) * opmm::TOPK));
+    CKS(ensure(h->tk_counters, h->tk_counters_cap, 2 * (size_t)(s_begin + S), true));
+    if (certify && opmm::cert_scratch_bytes(ns) > max_dyn_smem(opmm::cert_kernel_ptr(metric)))
+      return fail(OPMM_ERR_INVALID_ARG, "trace too long for certify");
+    if (!err_buf) {
+      err_ld = e - b > 0 ? e - b : 1;
+      err_base = b;
+      CKS(ensure(h->tk_err, h->tk_err_cap, (size_t)err_ld * (size_t)(s_begin + S)));
+      err_buf = h->tk_err;
+    }
+  }
   if (multi) {
     CKS(ensure(h->rank_part, h->rank_part_cap, (size_t)(s_begin + S)));
     CKS(ensure(h->gathered, h->gathered_cap, (size_t)h->world));
+    if (certify && opmm::cert_scratch_bytes(ns) > max_dyn_smem(opmm::merge_kernel_ptr(metric)))
+      return fail(OPMM_ERR_INVALID_ARG, "trace too long for certify");
   }
   opmm::FitArgs a;
   std::memset(&a, 0, sizeof(a));
+  a.metric_ = metric;
   a.rec = rec_dev;
   a.exp_tab = h->exp_tab;
   a.ctl = make_ctl(ctl);
@@ -705,24 +814,26 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
   a.sac_begin = s_begin;
   a.begin = b;
   a.end = e;
-  a.err_out = opts ? opts->err_out : nullptr;
-  a.err_ld = n_candidates;
-  a.sort_lanes = getenv("OPMM_NO_LANE_SORT") ? 0 : 1;   // env switch for A/B timing only
+  a.err_out = err_buf;
+  a.err_ld = err_ld;
+  a.err_base = err_base;
+  a.sort_lanes = (opts && (opts->flags & OPMM_FIT_FLAG_NO_LANE_SORT)) ? 0 : 1;
   a.super_tile = super;
   a.perm_off = (int64_t)perm_off;
   a.tmp_off = (int64_t)(opmm::tmp_bytes(super) <= stash_sz ? stash_off
                                                           : perm_off + opmm::perm_bytes(super));
-  if (certify) {
-    CKS(ensure(h->cert_parts, h->cert_parts_cap, (size_t)grid * (size_t)(s_begin + S)));
-    a.certify = 1;
-    a.cert_partials = h->cert_parts;
-  }
+  a.topk = K;
+  a.certify = certify ? 1 : 0;
+  a.tk_e = h->tk_e;
+  a.tk_i = h->tk_i;
+  a.tk_counters = h->tk_counters;
+  a.tk_fill_off = (int64_t)(h->tk_counters_cap / 2);
   a.partials = h->partials;
   a.counters = h->counters;
   a.rank_out = multi ? h->rank_part : nullptr;
   a.final_out = multi ? nullptr : out_dev;
   a.out_base = s_begin;
-  if (prepare_only && !multi && S == 1) {   // the caller launches it (graph)
+  if (prepare_only && !multi && S == 1 && K == 0) {   // the caller launches it (graph)
     prepare_only->fn = fn;
     prepare_only->grid = grid;
     prepare_only->block = block;
@@ -932,6 +1043,11 @@ opmm_status opmm_create(opmm_handle** out, int device) {
                                (int)max_dyn_smem_uncapped(f));
         }
         allow_dyn_smem(opmm::simulate_kernel_ptr(p, i));
+        if (p == 0 && i == 0) {
+          allow_dyn_smem(opmm::merge_kernel_ptr(m));
+          allow_dyn_smem(opmm::topk_kernel_ptr(m));
+          allow_dyn_smem(opmm::cert_kernel_ptr(m));
+        }
         allow_dyn_smem(opmm::score_kernel_ptr(p, m));
         for (int obj = 0; obj < 5; ++obj)
           for (int g = 0; g < 2; ++g) {
@@ -984,9 +1100,9 @@ opmm_status opmm_create_nccl(opmm_handle** out, int device, const uint8_t* id, i
   opmm_handle* h = *out;
   h->rank = rank;
   h->world = world;
-  // A single-rank communicator is also created when OPMM_NCCL_SINGLE_RANK is
-  // set, so the one-GPU tests exercise the all-gather + merge path for real.
-  if (world > 1 || getenv("OPMM_NCCL_SINGLE_RANK")) {
+  // world = 1 also gets a (one-rank) communicator: the caller asked for the
+  // NCCL path, so the all-gather + merge runs for real on one GPU too.
+  {
     NcclApi& api = nccl();
     if (!api.loaded) {
       opmm_destroy(h);
@@ -1018,7 +1134,11 @@ opmm_status opmm_destroy(opmm_handle* h) {
   cudaFree(h->nm_rel);
   cudaFree(h->rank_part);
   cudaFree(h->gathered);
-  cudaFree(h->cert_parts);
+  cudaFree(h->tk_e);
+  cudaFree(h->tk_i);
+  cudaFree(h->tk_counters);
+  cudaFree(h->tk_err);
+  for (int k = 0; k < 4; ++k) cudaFree(h->stage[k]);
   cudaFree(h->result);
   cudaFree(h->exp_tab);
   cudaFree(h->nm_x0);
@@ -1078,6 +1198,65 @@ opmm_status opmm_merge_argmin(const double* err, const int64_t* idx, int count, 
   return bi < 0 ? OPMM_ERR_NO_FINITE : OPMM_OK;
 }
 
+opmm_status opmm_merge_topk(const double* err, const int64_t* idx, int lists, int K,
+                            double* out_err, int64_t* out_idx) {
+  if (K < 1 || K > OPMM_MAX_TOPK || lists < 0 || !out_err || !out_idx ||
+      (lists > 0 && (!err || !idx)))
+    return fail(OPMM_ERR_INVALID_ARG, "bad merge_topk arguments");
+  // K-way selection by repeated lexicographic minimum over the list heads
+  // (the lists are sorted; index -1 ends a list)
+  std::string ptr_buf((size_t)(lists > 0 ? lists : 1) * sizeof(int), '\0');
+  int* ptr = reinterpret_cast<int*>(&ptr_buf[0]);
+  for (int l = 0; l < lists; ++l) ptr[l] = 0;
+  for (int k = 0; k < K; ++k) {
+    int bl = -1;
+    for (int l = 0; l < lists; ++l) {
+      if (ptr[l] >= K) continue;
+      const int64_t j = (int64_t)l * K + ptr[l];
+      if (idx[j] < 0) continue;
+      const int64_t bj = bl < 0 ? 0 : (int64_t)bl * K + ptr[bl];
+      if (bl < 0 || err[j] < err[bj] || (err[j] == err[bj] && idx[j] < idx[bj])) bl = l;
+    }
+    if (bl < 0) {
+      out_err[k] = INFINITY;
+      out_idx[k] = -1;
+      continue;
+    }
+    const int64_t j = (int64_t)bl * K + ptr[bl]++;
+    out_err[k] = err[j];
+    out_idx[k] = idx[j];
+  }
+  return OPMM_OK;
+}
+
+opmm_status opmm_certify_topk(const double* e32, const double* e64, const int64_t* idx, int K,
+                              double scale, int32_t* certified, int64_t* best_index,
+                              double* best_err) {
+  if (K < 1 || K > OPMM_MAX_TOPK || !e32 || !e64 || !idx || !certified || !best_index || !best_err)
+    return fail(OPMM_ERR_INVALID_ARG, "bad certify_topk arguments");
+  // delta = 1e-4 max(E32[0], s), T* = E32[0] + 2 delta;
+  // certified iff E32[K-1] > T* and every listed candidate's |E64 - E32| <= delta
+  const bool have0 = idx[0] >= 0 && e32[0] < INFINITY;
+  const double delta = 1e-4 * std::fmax(e32[0], scale);
+  const double tstar = e32[0] + 2.0 * delta;
+  const double eK = idx[K - 1] >= 0 ? e32[K - 1] : INFINITY;
+  bool budget = true;
+  double be = INFINITY;
+  int64_t bi = -1;
+  for (int k = 0; k < K; ++k) {
+    if (idx[k] < 0 || !(e32[k] < INFINITY)) continue;
+    budget = budget && std::fabs(e64[k] - e32[k]) <= delta;
+    if (bi < 0 || e64[k] < be || (e64[k] == be && idx[k] < bi)) {
+      be = e64[k];
+      bi = idx[k];
+    }
+  }
+  *certified = (have0 && eK > tstar && budget) ? 1 : 0;
+  *best_index = bi;
+  *best_err = be;
+  return OPMM_OK;
+}
+
 opmm_status opmm_validate(const opmm_control* ctl, const opmm_search_space* space,
                           int64_t n_candidates) {
   if (n_candidates < 0) return fail(OPMM_ERR_INVALID_ARG, "n_candidates < 0");
@@ -1096,9 +1275,11 @@ opmm_status opmm_generate(opmm_handle* h, const opmm_search_space* space, uint32
   cudaStream_t st = stream ? (cudaStream_t)stream : h->stream;
   int grid = (int)((count + 255) / 256);
   if (grid > h->num_sms * 8) grid = h->num_sms * 8;
-  CK(opmm::launch_generate(make_space(space), saccade, begin, count, opc_out, ld, h->exp_tab, grid,
-                           st));
-  return OPMM_OK;
+  Staging sg(h, st);
+  double* out = nullptr;
+  CKS(sg.out(opc_out, (size_t)(17 * ld + count) * sizeof(double), 0, &out));
+  CK(opmm::launch_generate(make_space(space), saccade, begin, count, out, ld, h->exp_tab, grid, st));
+  return sg.finish();
 }
 
 namespace {
@@ -1158,6 +1339,11 @@ opmm_status simulate_impl(opmm_handle* h, const double* opc, int64_t n, int64_t 
   const void* fn = opmm::simulate_kernel_ptr(precision, kernel_integ(integrator, ctl));
   int grid = 1;
   CKS(grid_for(h, fn, block, smem, n, 0, &grid));
+  const size_t esz = precision == OPMM_FP64 ? sizeof(double) : sizeof(float);
+  Staging sg(h, st);
+  CKS(sg.in(opc, (size_t)(17 * ld + n) * sizeof(double), 0, &opc));
+  CKS(sg.out(traj, (size_t)((int64_t)ctl->n_steps * ld_out + n) * esz, 1, &traj));
+  CKS(sg.out(status, (size_t)n, 2, &status));
   opmm::ExplicitArgs a;
   std::memset(&a, 0, sizeof(a));
   a.opc = opc;
@@ -1173,7 +1359,7 @@ opmm_status simulate_impl(opmm_handle* h, const double* opc, int64_t n, int64_t 
   CKS(record_start(h, st));
   CK(opmm::launch_explicit(fn, a, dim3(grid), block, smem, st));
   CKS(record_stop(h, st));
-  return OPMM_OK;
+  return sg.finish();
 }
 }
 
@@ -1192,11 +1378,16 @@ opmm_status opmm_score(opmm_handle* h, const void* traj, int64_t n, int64_t ld, 
   const size_t smem = (size_t)n_samples * sizeof(double);
   int grid = 1;
   CKS(grid_for(h, opmm::score_kernel_ptr(precision, metric), block, smem, n, 0, &grid));
+  const size_t esz = precision == OPMM_FP64 ? sizeof(double) : sizeof(float);
+  Staging sg(h, st);
+  CKS(sg.in(traj, (size_t)((int64_t)(n_samples - 1) * ld + n) * esz, 0, &traj));
+  CKS(sg.in(recorded, (size_t)n_samples * sizeof(double), 1, &recorded));
+  CKS(sg.out(err, (size_t)n * sizeof(double), 2, &err));
   opmm::ScoreArgs a{traj, n, ld, n_samples, recorded, err};
   CKS(record_start(h, st));
   CK(opmm::launch_score(a, precision, metric, dim3(grid), block, smem, st));
   CKS(record_stop(h, st));
-  return OPMM_OK;
+  return sg.finish();
 }
 
 opmm_status opmm_simulate_score(opmm_handle* h, const double* opc, int64_t n, int64_t ld,
@@ -1217,6 +1408,15 @@ opmm_status opmm_simulate_score(opmm_handle* h, const double* opc, int64_t n, in
   const void* fn = opmm::simscore_kernel_ptr(precision, kernel_integ(integrator, ctl), metric);
   int grid = 1;
   CKS(grid_for(h, fn, block, smem, n, 0, &grid));
+  const size_t ns = (size_t)ctl->n_steps + 1;
+  if (!is_device_ptr(recorded))
+    for (size_t k = 0; k < ns; ++k)
+      if (!is_finite(recorded[k]))
+        return fail(OPMM_ERR_INVALID_ARG, "recorded sample %zu is not finite", k);
+  Staging sg(h, st);
+  CKS(sg.in(opc, (size_t)(17 * ld + n) * sizeof(double), 0, &opc));
+  CKS(sg.in(recorded, ns * sizeof(double), 1, &recorded));
+  CKS(sg.out(err, (size_t)n * sizeof(double), 2, &err));
   opmm::ExplicitArgs a;
   std::memset(&a, 0, sizeof(a));
   a.opc = opc;
@@ -1230,7 +1430,7 @@ opmm_status opmm_simulate_score(opmm_handle* h, const double* opc, int64_t n, in
   CKS(record_start(h, st));
   CK(opmm::launch_explicit(fn, a, dim3(grid), block, smem, st));
   CKS(record_stop(h, st));
-  return OPMM_OK;
+  return sg.finish();
 }
 
 opmm_status opmm_fit_async(opmm_handle* h, const double* recorded_dev, const opmm_control* ctl,
@@ -1257,7 +1457,7 @@ opmm_status opmm_fit(opmm_handle* h, const double* recorded, const opmm_control*
   const bool host_rec = !is_device_ptr(recorded);
   // (host traces only: a device trace's pointer is part of the launch, and
   // callers that keep traces on the device use opmm_fit_async anyway)
-  if (h->comm == nullptr && host_rec && !getenv("OPMM_NO_FIT_GRAPH")) {
+  if (h->comm == nullptr && host_rec && !(opts && (opts->flags & OPMM_FIT_FLAG_NO_GRAPH))) {
     // Graph path: the trace is copied into pinned staging on the host, and
     // one graph launch does H2D + kernel + D2H (re-captured when the launch
     // changes).  The previous call synchronised, so the staging is free.

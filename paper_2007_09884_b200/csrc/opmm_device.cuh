@@ -98,35 +98,6 @@ __device__ __forceinline__ double exp_tab(double x, const double2* __restrict__ 
   return e.x + fma(e.x, q, e.y);
 }
 
-// exp(x) for 0 <= x < 700 without memory: x = k ln2 + r (Cody-Waite, |r| <=
-// ln2/2), degree-13 Taylor polynomial (truncation < 6e-18 relative), scaled
-// by 2^k through the exponent field; ~1 ulp.
-__device__ __forceinline__ double exp_poly(double x) {
-  const double k = rint(x * 1.4426950408889634);
-  double r = fma(k, -6.93147180369123816490e-01, x);
-  r = fma(k, -1.90821492927058770002e-10, r);
-  double q = 1.0 / 6227020800.0;
-  q = fma(q, r, 1.0 / 479001600.0);
-  q = fma(q, r, 1.0 / 39916800.0);
-  q = fma(q, r, 1.0 / 3628800.0);
-  q = fma(q, r, 1.0 / 362880.0);
-  q = fma(q, r, 1.0 / 40320.0);
-  q = fma(q, r, 1.0 / 5040.0);
-  q = fma(q, r, 1.0 / 720.0);
-  q = fma(q, r, 1.0 / 120.0);
-  q = fma(q, r, 1.0 / 24.0);
-  q = fma(q, r, 1.0 / 6.0);
-  q = fma(q, r, 0.5);
-  q = fma(q, r, 1.0);
-  q = fma(q, r, 1.0);
-  const double two_k = __hiloint2double(((int)k + 1023) << 20, 0);
-  return q * two_k;
-}
-
-#ifndef OPMM_EXP_MODE
-#define OPMM_EXP_MODE 0   // 0: double-double table, 1: polynomial, 2: libm exp
-#endif
-
 // General-range exp for log dimensions whose argument can reach 8 or more
 // (kind 3): out of line, so the 17 inlined maps carry one call, not 17
 // copies of libm's exp.
@@ -146,13 +117,7 @@ __device__ __forceinline__ double map_word(const SpaceDev& sp, int d, uint32_t w
   const double x = sp.exact_u ? __dmul_rn(__dmul_rn(w5, 2.3283064365386962890625e-10), sp.span[d])
                               : __dmul_rn(w5, sp.span32[d]);
   if (sp.kind[d] == 1) return __dadd_rn(sp.lo[d], x);
-#if OPMM_EXP_MODE == 0
   return __dmul_rn(sp.lo[d], sp.kind[d] == 2 ? exp_tab(x, tab) : exp_libm(x));
-#elif OPMM_EXP_MODE == 1
-  return __dmul_rn(sp.lo[d], sp.kind[d] == 2 ? exp_poly(x) : exp_libm(x));
-#else
-  return __dmul_rn(sp.lo[d], exp(x));
-#endif
 }
 
 // 9-parameter OPMM (Table 2) in the 18-vector, SPEC D7
@@ -1246,32 +1211,6 @@ __device__ __forceinline__ double evaluate(const double p[NP], const CtlDev& c, 
   T acc;
   if (INTEG == 0 || INTEG == 2) {
     Prop2<T> pr;
-#ifdef OPMM_EXP_NOPROP   // timing experiment only: skip the propagator build
-    {
-      const double b0 = s.m.z10 * 1e-6, b1 = s.ph[0].zd_ag * 1e-3, b2 = s.ph[1].zd_ant * 1e-3;
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) pr.P2[r][j] = (T)(r == j ? 0.9 + b0 : b0);
-        pr.P0[r] = (T)(0.1 * b1);
-        pr.z1[r] = (T)b2;
-#pragma unroll
-        for (int ph = 0; ph < 2; ++ph) {
-          pr.ph[ph].X2[r][0] = (T)b1; pr.ph[ph].X2[r][1] = (T)b2; pr.ph[ph].c2[r] = (T)(b1 * b2);
-        }
-      }
-#pragma unroll
-      for (int ph = 0; ph < 2; ++ph) {
-        pr.ph[ph].pf2[0] = (T)(0.5 + b1); pr.ph[ph].pf2[1] = (T)(0.5 + b2);
-        pr.ph[ph].qf2[0] = (T)b2; pr.ph[ph].qf2[1] = (T)b1;
-        pr.ph[ph].X0[0] = (T)b0; pr.ph[ph].X0[1] = (T)b1; pr.ph[ph].c0 = (T)b2;
-      }
-      pr.f1[0] = (T)b0; pr.f1[1] = (T)b1;
-    }
-    acc = run_propagator<T, METRIC, TRAJ>(pr, s.n_pulse, c.n_steps, rel, traj, ld_out,
-                                          (T)c.theta0, (T)sgn, stash,
-                                          stash_ld < 0 ? (int)blockDim.x : stash_ld);
-#else
     const int ld = stash_ld < 0 ? (int)blockDim.x : stash_ld;
     typename Vec2<T>::type* st2 = reinterpret_cast<typename Vec2<T>::type*>(stash) + threadIdx.x;
     if (INTEG == 2) {   // sample map = one-substep map ^ substeps (own instantiation)
@@ -1281,7 +1220,6 @@ __device__ __forceinline__ double evaluate(const double p[NP], const CtlDev& c, 
     }
     acc = run_propagator<T, METRIC, TRAJ, true, RL>(pr, s.n_pulse, c.n_steps, rel, traj, ld_out,
                                                 (T)c.theta0, (T)sgn, stash, ld);
-#endif
   } else {
     acc = run_rk4_stages<T, METRIC, TRAJ, RL>(s, c.n_steps, rel, traj, ld_out, (T)c.theta0, (T)sgn,
                                           c.substeps);

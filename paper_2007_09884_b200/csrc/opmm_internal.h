@@ -31,7 +31,6 @@ struct Partial {
   int64_t neval;  // evaluated candidates (rank partials only)
 };
 
-// FP32 certification: one block's (or rank's) top-8 by fp32 error
 // fit_kernel launch bounds: 384 threads x 168 registers, one block per SM
 // (3 warps per scheduler); the default block size of the fit entry points
 #ifndef OPMM_FIT_LB_THREADS
@@ -41,7 +40,6 @@ struct Partial {
 #define OPMM_FIT_LB_BLOCKS 1
 #endif
 
-constexpr int CERT_KK = 8;
 // fit_kernel super-tile: a block sorts up to SUPER_MAX candidates at once
 // (per candidate in shared memory: permutation uint16 for the whole pass,
 // key/rank uint32 during the pre-pass only -- aliased onto the coefficient
@@ -49,22 +47,22 @@ constexpr int CERT_KK = 8;
 constexpr int SUPER_MAX = 8192;
 __host__ __device__ constexpr size_t perm_bytes(int64_t s) { return (size_t)((s * 2 + 15) / 16 * 16); }
 __host__ __device__ constexpr size_t tmp_bytes(int64_t s) { return (size_t)((s * 4 + 15) / 16 * 16); }
-// certify scratch (one region, reused by stage): per-thread best two (E, idx)
-// + per-warp lists; in the last block, every block's list + chunk lists, then
-// the fp64 trace and stash of the re-score.  grid <= 256.
-__host__ __device__ constexpr size_t cert_max3(size_t x, size_t y, size_t z) {
-  return x > y ? (x > z ? x : z) : (y > z ? y : z);
+
+// Exact top-K lists (top_k / certify): one sorted list of TOPK (E, index)
+// pairs per warp, lane l = rank l (K <= TOPK used).
+constexpr int TOPK = OPMM_MAX_TOPK;
+// certify scratch of the finishing block: the fp64 trace and a [10][32]
+// double2 stash for the one-warp fp64 re-score
+__host__ __device__ constexpr size_t cert_scratch_bytes(int32_t n_samples) {
+  return (((size_t)n_samples + 1) & ~(size_t)1) * 8 + (size_t)20 * 32 * 8;
 }
-__host__ __device__ constexpr size_t cert_scratch_bytes(int block, int grid, int32_t n_samples) {
-  return cert_max3((size_t)2 * block * 16 + (size_t)8 * ((block + 31) / 32) * 16,
-                   (size_t)8 * grid * 16 + (size_t)8 * ((grid + 31) / 32) * 16,
-                   (((size_t)n_samples + 1) & ~(size_t)1) * 8 + (size_t)20 * 32 * 8);
-}
-struct CertPartial {
-  double e[8];
-  int64_t i[8];
-  int64_t nf;
-  double m2;   // min over the block's threads of their second-best fp32 error
+// Per-rank result (world > 1): the rank's (E, index, n_finite, n_evaluated)
+// and, with top_k / certify, its top-32 list.  The all-gather moves the first
+// 32 bytes, or all 544 with a list.
+struct RankPartial {
+  Partial p;
+  double e[TOPK];
+  int64_t i[TOPK];
 };
 
 struct FitArgs {
@@ -77,17 +75,25 @@ struct FitArgs {
   const double* sac_ctl;    // batch: device [S][2] = (amplitude, pw_default); else nullptr
   int64_t sac_begin;        // first saccade of this launch (blockIdx.y offset)
   int64_t begin, end;       // candidate range of this rank
-  double* err_out;          // optional device, indexed [sac * err_ld + i]
+  double* err_out;          // optional device, candidate i at [sac * err_ld + i - err_base]
   int64_t err_ld;
+  int64_t err_base;
   int32_t sort_lanes;       // counting-sort tiles by pulse end (see fit_kernel)
-  int32_t certify;          // fp32: top-8 + fp64 re-score (fit_kernel only)
+  int32_t certify;          // fp32: top-K by fp32 E + fp64 re-score (fit_kernel only)
+  int32_t topk;             // K of the exact top-K (0 = none; certify sets it): topk_kernel
+  int32_t metric_;          // opmm_metric (host side: the merge kernel's instantiation)
+  int32_t fit_grid;         // topk_kernel: the fit kernel's gridDim.x (its Partials per saccade)
+  int32_t pad1_;
+  double* tk_e;             // topk_kernel: [S][gridDim.x * TOPK] key buffer
+  int64_t* tk_i;
+  unsigned int* tk_counters;   // topk_kernel: tickets [S] + fill counts at tk_fill_off, zero at rest
+  int64_t tk_fill_off;
   int64_t super_tile;       // fit_kernel: candidates per block pass (multiple of 32, <= SUPER_MAX)
   int64_t perm_off;         // fit_kernel: byte offset of the super-tile permutation in smem
   int64_t tmp_off;          // fit_kernel: byte offset of the pre-pass key/rank scratch
-  CertPartial* cert_partials;  // [S][gridDim.x] when certify
   Partial* partials;        // [S][gridDim.x]
   unsigned int* counters;   // [S], zero between launches
-  Partial* rank_out;        // optional [S]: per-rank result (world > 1)
+  RankPartial* rank_out;    // optional [S]: per-rank result (world > 1)
   opmm_fit_result* final_out;  // optional: final result of saccade s at [s - out_base]
   int64_t out_base;
   // kernel_variant 4 (fit_super_kernel): superposition over the grid levels of
@@ -178,8 +184,24 @@ const void* score_kernel_ptr(int precision, int metric);
 
 cudaError_t launch_fit(const void* fn, const FitArgs& a, dim3 grid, int block, size_t smem,
                        cudaStream_t st);
-cudaError_t launch_merge(const Partial* gathered, int world, const SpaceDev& sp, uint32_t saccade,
-                         opmm_fit_result* out, const double2* tab, cudaStream_t st);
+// world > 1: merge the gathered rank results of saccade `sac` (rank r's at
+// gathered + r * stride bytes; the lists only when a.topk) and write its final
+// result; certify re-scores the merged list in fp64 (dynamic smem: the
+// certify scratch)
+cudaError_t launch_merge(const FitArgs& a, const void* gathered, int world, size_t stride,
+                         int64_t sac, opmm_fit_result* out, int metric, size_t smem,
+                         cudaStream_t st);
+const void* merge_kernel_ptr(int metric);
+// exact top-K of a fit from its err_out (after the fit kernel, same stream):
+// grid (blocks, S), dynamic smem topk_smem(blocks, n_samples, certify)
+constexpr int TOPK_BLOCK = 256;
+const void* topk_kernel_ptr(int metric);
+__host__ __device__ constexpr size_t topk_smem(int) { return (size_t)512 * 16; }   // TOPK_MAXFG minima
+cudaError_t launch_topk(const FitArgs& a, int blocks, int S, size_t smem, int metric, cudaStream_t st);
+// fp32 certification after topk_kernel (one rank): one warp per saccade,
+// dynamic smem cert_scratch_bytes(n_samples)
+const void* cert_kernel_ptr(int metric);
+cudaError_t launch_cert(const FitArgs& a, int S, size_t smem, int metric, cudaStream_t st);
 cudaError_t launch_explicit(const void* fn, const ExplicitArgs& a, dim3 grid, int block, size_t smem,
                             cudaStream_t st);
 cudaError_t launch_score(const ScoreArgs& a, int precision, int metric, dim3 grid, int block,

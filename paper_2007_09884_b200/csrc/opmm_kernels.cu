@@ -46,13 +46,16 @@ __device__ __forceinline__ void block_argmin(double& e, int64_t& i, int64_t& nf)
   }
 }
 
+constexpr unsigned FULL = 0xffffffffu;
+__device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000000000000LL); }
+
 // Write the final result struct (one thread) and the winner's OPC.
 __device__ void write_result(const SpaceDev& sp, uint32_t saccade, double e, int64_t i,
                              int64_t nf, int64_t neval, opmm_fit_result* out,
                              const double2* tab) {
-  const bool ok = i != INT64_MAX && e < __longlong_as_double(0x7ff0000000000000LL);
+  const bool ok = i != INT64_MAX && e < dinf();
   out->best_index = ok ? i : -1;
-  out->opt_err = ok ? e : __longlong_as_double(0x7ff0000000000000LL);
+  out->opt_err = ok ? e : dinf();
   out->cpu_check = __longlong_as_double(0x7ff8000000000000LL);
   out->n_finite = nf;
   out->n_evaluated = neval;
@@ -71,8 +74,6 @@ __device__ void write_result(const SpaceDev& sp, uint32_t saccade, double e, int
 __device__ __forceinline__ void fit_epilogue(const FitArgs& a, int64_t sac, double best_e,
                                              int64_t best_i, int64_t nf) {
   block_argmin(best_e, best_i, nf);
-
-  // per-block partial, then the last block of this saccade reduces them
   __shared__ bool is_last;
   Partial* parts = a.partials + sac * (int64_t)gridDim.x;
   if (threadIdx.x == 0) {
@@ -84,7 +85,7 @@ __device__ __forceinline__ void fit_epilogue(const FitArgs& a, int64_t sac, doub
   __syncthreads();
   if (!is_last) return;
   __threadfence();
-  double e = __longlong_as_double(0x7ff0000000000000LL);
+  double e = dinf();
   int64_t i = INT64_MAX, n = 0;
   for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
     // L2-coherent loads: the partials were written by other blocks
@@ -99,170 +100,326 @@ __device__ __forceinline__ void fit_epilogue(const FitArgs& a, int64_t sac, doub
   if (threadIdx.x == 0) {
     a.counters[sac] = 0;  // re-arm for the next launch (graph-replay safe)
     const int64_t neval = a.end - a.begin;
-    if (a.rank_out) a.rank_out[sac] = Partial{e, i, n, neval};
-    if (a.final_out)
-      write_result(a.space, (uint32_t)sac, e, i, n, neval, a.final_out + (sac - a.out_base),
-                   a.exp_tab);
-  }}
-
-// ---------------------------------------------------------------------------
-// FP32 certification (opmm_fit_options.certify, fit1 / fp32 only).  Every
-// thread keeps its two best (E32, index) pairs in registers; warps, blocks
-// and finally the last block merge them into the global top-8 by fp32 error
-// (8 rounds of warp argmin over sorted list heads -- no block barriers per
-// round), and the minimum over all threads of their SECOND-best error, m2,
-// is reduced alongside.  Warp 0 of the last block re-scores the 8 in fp64
-// (the fp64 fit's evaluator) and the fit returns the fp64-best of them.
-// Certificate: with T* = E32[0] + 2 delta, delta =
-// 1e-4 max(E32[0], sum |rel|) the fp32 error budget, every candidate within
-// T* is in the list iff m2 > T* (no thread dropped one) and E32[7] > T* (no
-// merge stage dropped one) -- or fewer than 8 finite candidates exist.
-// ---------------------------------------------------------------------------
-constexpr int CERT_K = CERT_KK;
-
-// 8 rounds of warp argmin over per-lane sorted lists: lane l holds cnt
-// entries at (le[k * ld], li[k * ld]), k < cnt; results in out_e/out_i (lane 0).
-__device__ __forceinline__ void warp_topk(const double* le, const int64_t* li, int ld, int cnt,
-                                          double* out_e, int64_t* out_i) {
-  int ptr = 0;
-  for (int r = 0; r < CERT_K; ++r) {
-    double e = ptr < cnt ? le[ptr * ld] : __longlong_as_double(0x7ff0000000000000LL);
-    int64_t i = ptr < cnt ? li[ptr * ld] : INT64_MAX;
-    const double me = e;
-    const int64_t mi = i;
-    warp_argmin(e, i);
-    if (me == e && mi == i && mi != INT64_MAX) ++ptr;
-    if ((threadIdx.x & 31) == 0) { out_e[r] = e; out_i[r] = i; }
+    if (a.rank_out) a.rank_out[sac].p = Partial{e, i, n, neval};
+    if (a.final_out) {
+      opmm_fit_result* out = a.final_out + (sac - a.out_base);
+      write_result(a.space, (uint32_t)sac, e, i, n, neval, out, a.exp_tab);
+      for (int k = 0; k < OPMM_MAX_TOPK; ++k) {   // no list unless topk_kernel writes one
+        out->topk_index[k] = -1;
+        out->topk_err[k] = dinf();
+      }
+    }
   }
 }
 
-template <typename T, int METRIC>
-__device__ void cert_epilogue(const FitArgs& a, int64_t sac, double e1, int64_t i1, double e2,
-                              int64_t i2, int64_t nf, double sgn, double Aprime, double pwd,
-                              unsigned char* scratch) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
-  const double INF = __longlong_as_double(0x7ff0000000000000LL);
-  // scratch layout: thread lists [2][block], warp lists [nw][8], then reused
-  double* te = reinterpret_cast<double*>(scratch);
-  int64_t* ti = reinterpret_cast<int64_t*>(te + 2 * blockDim.x);
-  double* we = reinterpret_cast<double*>(ti + 2 * blockDim.x);
-  int64_t* wi = reinterpret_cast<int64_t*>(we + 8 * nw);
-  __shared__ double s_m2;
-  __shared__ int64_t s_nf;
-  __shared__ double b_e[CERT_K];
-  __shared__ int64_t b_i[CERT_K];
-  __shared__ bool is_last;
-  te[threadIdx.x] = e1; ti[threadIdx.x] = i1;
-  te[blockDim.x + threadIdx.x] = e2; ti[blockDim.x + threadIdx.x] = i2;
-  // block n_finite and min second-best (argmin-reduce on (e2, i2) gives the min)
-  {
-    double m = e2;
-    int64_t mi = i2, n = nf;
-    block_argmin(m, mi, n);
-    if (threadIdx.x == 0) { s_m2 = m; s_nf = n; }
+// ---------------------------------------------------------------------------
+// Exact top-K of (E, index), K <= 32, lexicographic (reading Q12; "solutions
+// are sorted for accuracy").  A warp holds one sorted list,
+// lane l = rank l; ranks >= K hold the pad (+inf, INT64_MAX).  A batch of 32
+// keys (one per lane) enters by a bitonic sort of the batch (15
+// compare-exchange steps), the lane-wise minimum of the list and the reversed
+// batch -- the 32 smallest keys of the union, as a bitonic sequence -- and a
+// bitonic merge (5 steps); a batch with only a few qualifying keys inserts
+// them one at a time instead.  Keys are unique (distinct indices) except pads.
+//
+// The comparisons run on the integer pipe: for E >= 0 (errors, penalties,
+// +inf) the fp64 bit patterns order exactly as the values.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool kbetter(double e1, int64_t i1, double e2, int64_t i2) {
+  const unsigned long long a = (unsigned long long)__double_as_longlong(e1);
+  const unsigned long long b = (unsigned long long)__double_as_longlong(e2);
+  return a < b || (a == b && i1 < i2);
+}
+
+__device__ __forceinline__ void tk_cx(double& e, int64_t& i, int j, bool keep_min) {
+  const double oe = __shfl_xor_sync(FULL, e, j);
+  const int64_t oi = __shfl_xor_sync(FULL, i, j);
+  if (keep_min ? kbetter(oe, oi, e, i) : kbetter(e, i, oe, oi)) { e = oe; i = oi; }
+}
+
+__device__ __forceinline__ void tk_sort32(double& e, int64_t& i) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) tk_cx(e, i, j, ((lane & j) == 0) == ((lane & k) == 0));
+}
+
+// (e, i): sorted list; (ve, vi): sorted batch -> the K smallest of both, sorted
+__device__ __forceinline__ void tk_merge32(double& e, int64_t& i, double ve, int64_t vi, int K) {
+  const int lane = threadIdx.x & 31;
+  const double re = __shfl_sync(FULL, ve, 31 - lane);
+  const int64_t ri = __shfl_sync(FULL, vi, 31 - lane);
+  if (kbetter(re, ri, e, i)) { e = re; i = ri; }
+#pragma unroll
+  for (int j = 16; j > 0; j >>= 1) tk_cx(e, i, j, (lane & j) == 0);
+  if (lane >= K) { e = dinf(); i = INT64_MAX; }
+}
+
+// merge another sorted list unless its head cannot enter (warp-uniform)
+__device__ __forceinline__ void tk_merge_list(double& e, int64_t& i, double ve, int64_t vi, int K) {
+  const double he = __shfl_sync(FULL, ve, 0), te = __shfl_sync(FULL, e, K - 1);
+  const int64_t hi = __shfl_sync(FULL, vi, 0), ti = __shfl_sync(FULL, i, K - 1);
+  if (kbetter(he, hi, te, ti)) tk_merge32(e, i, ve, vi, K);
+}
+
+// One batch of keys (lane's E, i; c = the key beats the list's K-th) into the
+// warp's list (le, li): one at a time when few qualify, else sort + merge.
+__device__ __forceinline__ void tk_insert(double& le, int64_t& li, double E, int64_t i, bool c,
+                                          int K) {
+  const int lane = threadIdx.x & 31;
+  const unsigned m = __ballot_sync(FULL, c);
+  if (m == 0) return;
+  if (__popc(m) <= 4) {
+    // the list entries ahead of key x form a prefix (the list is sorted), so
+    // x's rank is the popcount of their ballot; later entries shift up a lane
+    for (unsigned rest = m; rest != 0; rest &= rest - 1) {
+      const int src = __ffs(rest) - 1;
+      const double xe = __shfl_sync(FULL, E, src);
+      const int64_t xi = __shfl_sync(FULL, i, src);
+      const int r = __popc(__ballot_sync(FULL, kbetter(le, li, xe, xi)));
+      const double pe = __shfl_up_sync(FULL, le, 1);
+      const int64_t pi = __shfl_up_sync(FULL, li, 1);
+      if (lane > r) { le = pe; li = pi; }
+      if (lane == r) { le = xe; li = xi; }
+      if (lane >= K) { le = dinf(); li = INT64_MAX; }
+    }
+  } else {
+    double ve = c ? E : dinf();
+    int64_t vi = c ? i : INT64_MAX;
+    tk_sort32(ve, vi);
+    tk_merge32(le, li, ve, vi, K);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Final top-K of saccade `sac`, by one warp (all 32 lanes), from the merged
+// list (le, li): the K entries and, with fp32 certification
+// (opmm_fit_options.certify), the certificate and the
+// fp64-best of the list as the fit's winner.  The K listed candidates are
+// re-scored in fp64 (one per lane, the fp64 fit's evaluator; rel64 / st64 =
+// the block's fp64 trace and [10][32] stash); with delta = 1e-4 max(E32[0],
+// s) (s = sum |rel| for L1, RMS(rel) for RMS) and T* = E32[0] + 2 delta the
+// list is certified iff E32[K-1] > T* (the exact top-K then holds every
+// candidate whose fp32 error is <= T*, and the fp64 winner's fp32 error is
+// <= T* whenever its own budget holds) and every listed candidate's |E64 -
+// E32| <= delta (the budget, checked where it can be).  nf / neval: the
+// fit's counts.  Without certify the fit's own winner (the list head) stays.
+// ---------------------------------------------------------------------------
+template <int METRIC, bool CERT>
+__device__ void finalize_topk(const FitArgs& a, int64_t sac, double le, int64_t li, int64_t nf,
+                              int64_t neval, opmm_fit_result* out, const double* rel64,
+                              double* st64, double sgn, double Aprime, double pwd) {
+  const int lane = threadIdx.x & 31;
+  const int K = a.topk;
+  const double INF = dinf();
+  double oe = le;
+  bool certified = false;
+  if (CERT && a.certify) {
+    const int32_t ns = a.ctl.n_steps + 1;
+    const bool have = lane < K && li != INT64_MAX && le < INF;
+    double p[NP];
+    generate_opc(a.space, (uint32_t)sac, have ? li : 0, p, a.exp_tab);
+    double E64 = evaluate<double, 0, METRIC, false>(p, a.ctl, Aprime, pwd, rel64, nullptr, 0, sgn,
+                                                    nullptr, st64, !a.space.all_physical, 32);
+    if (!have) E64 = INF;
+    double srel = 0.0;
+    for (int k = lane; k < ns; k += 32) srel += METRIC == 0 ? fabs(rel64[k]) : rel64[k] * rel64[k];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) srel += __shfl_xor_sync(FULL, srel, off);
+    if (METRIC != 0) srel = sqrt(srel / (double)ns);
+    const double e0 = __shfl_sync(FULL, le, 0), eK = __shfl_sync(FULL, le, K - 1);
+    const double delta = 1e-4 * fmax(e0, srel);
+    const double tstar = e0 + 2.0 * delta;
+    const bool budget = !have || fabs(E64 - le) <= delta;
+    certified = __all_sync(FULL, budget) && e0 < INF && eK > tstar;
+    double we = E64;
+    int64_t wi = have ? li : INT64_MAX;
+    warp_argmin(we, wi);
+    if (lane == 0) write_result(a.space, (uint32_t)sac, we, wi, nf, neval, out, a.exp_tab);
+    oe = E64;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    out->top_k = K;
+    out->certified = certified ? 1 : 0;
+  }
+  const bool used = lane < K && li != INT64_MAX;
+  out->topk_index[lane] = used ? li : -1;
+  out->topk_err[lane] = used ? oe : INF;
+}
+
+// ---------------------------------------------------------------------------
+// Exact top-K of a fit (top_k / certify) from the per-candidate errors the
+// fit kernel wrote (a.err_out[sac * err_ld + i - err_base], i in [begin,
+// end)).  Kept out of the fit kernel: list upkeep inside its loop costs
+// issue slots and registers of the fp64-bound integration (measured: +40 us
+// per 10^6 candidates at K = 32).
+//   1. Threshold: the K-th smallest of the fit's per-block minima (ranked in
+//      parallel by every block) -- with ~150 fit blocks it sits within a few
+//      dozen candidates of the exact K-th, so almost every error is rejected
+//      by one compare.
+//   2. Every warp streams its errors (8 batches of 32 in flight) and keeps
+//      the survivors in a sorted list in registers; the block's warps merge
+//      theirs and append the block's entries to the saccade's key buffer.
+//   3. The last block of a saccade (ticket) merges the buffer (usually a few
+//      dozen keys) and writes the rank lists (world > 1) or the result's
+//      top-K (finalize_topk; certify then runs cert_kernel).
+// 8 bytes read per candidate, a few microseconds per 10^6.
+// ---------------------------------------------------------------------------
+constexpr int TOPK_THREADS = 256;
+constexpr int TOPK_MAXFG = 512;   // fit blocks per saccade the threshold step ranks (smem 16 B each)
+
+template <int METRIC>
+__global__ void __launch_bounds__(TOPK_THREADS) topk_kernel(FitArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = TOPK_THREADS / 32;
+  const int K = a.topk;
+  const int G = gridDim.x;
+  const int64_t sac = (int64_t)blockIdx.y + a.sac_begin;
+  const int64_t n = a.end - a.begin;
+  // 1. the threshold: the K-th smallest of the fit's block minima (its
+  // Partials), by ranks -- each minimum counts the minima ahead of it, the
+  // one with K-1 ahead is the threshold.  K distinct candidates lie at or
+  // below it, so no candidate above it can be in the top-K (and it may be
+  // one of them: keys <= it are kept).  None when fewer than K fit blocks
+  // hold a candidate, or more than TOPK_MAXFG.
+  __shared__ double s_te;
+  __shared__ int64_t s_ti;
+  const int FG = a.fit_grid;
+  if (threadIdx.x == 0) { s_te = dinf(); s_ti = INT64_MAX; }
+  if (FG <= TOPK_MAXFG) {
+    double* pe = reinterpret_cast<double*>(smem_raw);   // [FG] block minima
+    int64_t* pi = reinterpret_cast<int64_t*>(pe + TOPK_MAXFG);
+    const Partial* parts = a.partials + sac * (int64_t)FG;
+    for (int b = threadIdx.x; b < FG; b += TOPK_THREADS) {
+      pe[b] = __ldcg(&parts[b].e);
+      pi[b] = (int64_t)__ldcg(reinterpret_cast<const long long*>(&parts[b].i));
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < FG; b += TOPK_THREADS) {
+      const double eb = pe[b];
+      const int64_t ib = pi[b];
+      int r = 0;
+#pragma unroll 8
+      for (int j = 0; j < FG; ++j) r += kbetter(pe[j], pi[j], eb, ib) ? 1 : 0;
+      if (r == K - 1 && ib != INT64_MAX) { s_te = eb; s_ti = ib + 1; }
+    }
   }
   __syncthreads();
-  // warp top-8 of the warp's 32 x 2 entries, then warp 0 merges the nw lists
-  warp_topk(te + threadIdx.x, ti + threadIdx.x, blockDim.x, 2, we + 8 * wid, wi + 8 * wid);
+  double le = dinf(), te = s_te;
+  int64_t li = INT64_MAX, ti = s_ti;
+  // 2. stream the errors
+  const double* err = a.err_out + sac * a.err_ld + (a.begin - a.err_base);
+  const int64_t step = (int64_t)G * nw * 32;
+  for (int64_t j0 = ((int64_t)blockIdx.x * nw + wid) * 32; j0 < n; j0 += 8 * step) {
+    double Ev[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t j = j0 + u * step + lane;
+      Ev[u] = j < n ? __ldcs(err + j) : dinf();
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t j = j0 + u * step + lane;
+      const int64_t i = a.begin + j;
+      if (__any_sync(FULL, j < n && kbetter(Ev[u], i, te, ti))) {
+        tk_insert(le, li, Ev[u], i, j < n && kbetter(Ev[u], i, te, ti), K);
+        // the filter: the list's K-th once it is below the threshold
+        const double le_k = __shfl_sync(FULL, le, K - 1);
+        const int64_t li_k = __shfl_sync(FULL, li, K - 1);
+        if (kbetter(le_k, li_k, te, ti)) { te = le_k; ti = li_k; }
+      }
+    }
+  }
+  // the block's list (warp 0 merges the warps'), then its entries are
+  // appended to the saccade's key buffer (a.tk_e / a.tk_i, fill count
+  // a.tk_counters[S_total + sac]); the last block (ticket) merges the buffer
+  __shared__ double se[TOPK_THREADS];
+  __shared__ int64_t si[TOPK_THREADS];
+  se[wid * TOPK + lane] = le;
+  si[wid * TOPK + lane] = li;
   __syncthreads();
+  unsigned int* fill = a.tk_counters + a.tk_fill_off + sac;
+  double* be = a.tk_e + sac * (int64_t)G * TOPK;
+  int64_t* bi = a.tk_i + sac * (int64_t)G * TOPK;
   if (wid == 0) {
-    // lane l < nw holds warp l's sorted list (8 entries)
-    warp_topk(we + 8 * lane, wi + 8 * lane, 1, lane < nw ? 8 : 0, b_e, b_i);
-  }
-  __syncthreads();
-  CertPartial* parts = a.cert_partials + sac * (int64_t)gridDim.x;
-  if (threadIdx.x == 0) {
-    CertPartial q;
-    for (int k = 0; k < CERT_K; ++k) { q.e[k] = b_e[k]; q.i[k] = b_i[k]; }
-    q.nf = s_nf;
-    q.m2 = s_m2;
-    parts[blockIdx.x] = q;
+    for (int w = 1; w < nw; ++w) tk_merge_list(le, li, se[w * TOPK + lane], si[w * TOPK + lane], K);
+    const bool has = li != INT64_MAX;
+    const unsigned m = __ballot_sync(FULL, has);
+    unsigned base = 0;
+    if (lane == 0 && m) base = atomicAdd(fill, (unsigned)__popc(m));
+    base = __shfl_sync(FULL, base, 0);
+    if (has) {   // sorted, so the entries are lanes 0 .. popc(m) - 1
+      be[base + lane] = le;
+      bi[base + lane] = li;
+    }
     __threadfence();
-    const unsigned int t = atomicAdd(a.counters + sac, 1u);
+  }
+  __shared__ bool is_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int t = atomicAdd(a.tk_counters + sac, 1u);
     is_last = (t == gridDim.x - 1);
   }
   __syncthreads();
   if (!is_last) return;
   __threadfence();
-  // last block: stage every block's list in smem (coalesced L2 loads), then
-  // the same two-level warp merge: chunks of 32 lists -> [nchunk][8] -> top-8
-  const int G = gridDim.x, nchunk = (G + 31) >> 5;   // G <= 256 (host cap)
-  double* pe = reinterpret_cast<double*>(scratch);   // [G][8]
-  int64_t* pi = reinterpret_cast<int64_t*>(pe + 8 * G);
-  double* ce = reinterpret_cast<double*>(pi + 8 * G); // [nchunk][8]
-  int64_t* ci = reinterpret_cast<int64_t*>(ce + 8 * nchunk);
-  for (int t = threadIdx.x; t < 8 * G; t += blockDim.x) {
-    pe[t] = __ldcg(&parts[t >> 3].e[t & 7]);
-    pi[t] = __ldcg(reinterpret_cast<const long long*>(&parts[t >> 3].i[t & 7]));
+  // 3. the last block: warps merge strides of the buffered keys (usually a
+  // few dozen after the threshold), warp 0 merges the warps' lists
+  const int cnt = (int)__ldcg(fill);
+  le = dinf();
+  li = INT64_MAX;
+  te = dinf();
+  ti = INT64_MAX;
+  for (int k0 = wid * 32; k0 < cnt; k0 += TOPK_THREADS) {
+    const int k = k0 + lane;
+    const double E = k < cnt ? __ldcg(be + k) : dinf();
+    const int64_t i = k < cnt ? (int64_t)__ldcg(reinterpret_cast<const long long*>(bi + k)) : INT64_MAX;
+    tk_insert(le, li, E, i, k < cnt && kbetter(E, i, te, ti), K);
+    te = __shfl_sync(FULL, le, K - 1);
+    ti = __shfl_sync(FULL, li, K - 1);
   }
-  {
-    double m = INF;
-    int64_t mi = 0, n = 0;
-    for (int b = threadIdx.x; b < G; b += blockDim.x) {
-      m = fmin(m, __ldcg(&parts[b].m2));
-      n += __ldcg(reinterpret_cast<const long long*>(&parts[b].nf));
+  __syncthreads();
+  se[wid * TOPK + lane] = le;
+  si[wid * TOPK + lane] = li;
+  __syncthreads();
+  if (wid == 0) {
+    for (int w = 1; w < nw; ++w) tk_merge_list(le, li, se[w * TOPK + lane], si[w * TOPK + lane], K);
+    if (a.rank_out) {
+      a.rank_out[sac].e[lane] = le;
+      a.rank_out[sac].i[lane] = li;
+    } else if (a.final_out) {
+      opmm_fit_result* out = a.final_out + (sac - a.out_base);
+      finalize_topk<METRIC, false>(a, sac, le, li, 0, 0, out, nullptr, nullptr, 1.0, 0.0, 0.0);
     }
-    __syncthreads();
-    block_argmin(m, mi, n);
-    if (threadIdx.x == 0) { s_m2 = m; s_nf = n; }
   }
-  __syncthreads();
-  for (int c = wid; c < nchunk; c += nw) {
-    const int l = 32 * c + lane;
-    warp_topk(pe + 8 * l, pi + 8 * l, 1, l < G ? 8 : 0, ce + 8 * c, ci + 8 * c);
-  }
-  __syncthreads();
-  if (wid == 0) warp_topk(ce + 8 * lane, ci + 8 * lane, 1, lane < nchunk ? 8 : 0, b_e, b_i);
-  __syncthreads();
-  const int32_t ns = a.ctl.n_steps + 1;
-  double* rel64 = reinterpret_cast<double*>(scratch);            // reuse the scratch
-  double* st64 = rel64 + ((ns + 1) & ~1);                        // fp64 stash [10][32] double2
-  const double* rec = a.rec + sac * (int64_t)ns;
-  for (int k = threadIdx.x; k < ns; k += blockDim.x) rel64[k] = sgn * (rec[k] - rec[0]);
-  __syncthreads();
-  if (wid != 0) return;
-  const int64_t nft = s_nf;
-  const double m2 = s_m2;
-  double ge[CERT_K];
-  int64_t gi[CERT_K];
-#pragma unroll
-  for (int r = 0; r < CERT_K; ++r) { ge[r] = b_e[r]; gi[r] = b_i[r]; }
-  // fp64 re-score of the 8 (all 32 lanes run the evaluator)
-  const int kk = lane < CERT_K ? lane : 0;
-  const int64_t idx = b_i[kk];
-  const double e32 = b_e[kk];
-  double p[NP];
-  generate_opc(a.space, (uint32_t)sac, idx == INT64_MAX ? 0 : idx, p, a.exp_tab);
-#ifdef OPMM_CERT_NOFP64   // timing experiment only: skip the fp64 re-score
-  double E64 = e32 + p[0] * 0.0;
-#else
-  double E64 = evaluate<double, 0, METRIC, false>(p, a.ctl, Aprime, pwd, rel64, nullptr, 0, sgn,
-                                                  nullptr, st64, !a.space.all_physical, 32);
-#endif
-  if (idx == INT64_MAX || !(e32 < INF)) E64 = INF;
-  double e = lane < CERT_K ? E64 : INF;
-  int64_t i = lane < CERT_K ? idx : INT64_MAX;
-  warp_argmin(e, i);
-  opmm_fit_result* out = a.final_out + (sac - a.out_base);
-  if (lane == 0) {
-    a.counters[sac] = 0;   // re-arm (graph-replay safe)
-    write_result(a.space, (uint32_t)sac, e, i, nft, a.end - a.begin, out, a.exp_tab);
-    // error scale of the trace in the fit's metric: sum |rel| (L1), or the
-    // RMS of rel (RMS) -- the fp32 budget's floor
-    double srel = 0.0;
-    for (int k = 0; k < ns; ++k) srel += METRIC == 0 ? fabs(rel64[k]) : rel64[k] * rel64[k];
-    if (METRIC != 0) srel = sqrt(srel / (double)ns);
-    const double tstar = ge[0] + 2.0 * (1e-4 * fmax(ge[0], srel));
-    out->top_k = CERT_K;
-    out->certified = (nft < CERT_K || (m2 > tstar && ge[CERT_K - 1] > tstar)) ? 1 : 0;
-  }
-  __syncwarp();
-  if (lane < CERT_K) {
-    out->topk_index[lane] = idx == INT64_MAX ? -1 : idx;
-    out->topk_err[lane] = E64;
-  }
+  if (threadIdx.x == 0) *fill = 0;
+  if (threadIdx.x == 0) a.tk_counters[sac] = 0;   // re-arm (graph-replay safe)
 }
 
+// FP32 certification of saccade sac on one rank (after topk_kernel): one
+// warp re-scores the result's list in fp64 (finalize_topk with CERT).
+template <int METRIC>
+__global__ void __launch_bounds__(32) cert_kernel(FitArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int64_t sac = (int64_t)blockIdx.x + a.sac_begin;
+  opmm_fit_result* out = a.final_out + (sac - a.out_base);
+  const int64_t li0 = out->topk_index[lane];
+  const double le = li0 >= 0 ? out->topk_err[lane] : dinf();
+  const int64_t li = li0 >= 0 ? li0 : INT64_MAX;
+  const int64_t nf = out->n_finite, neval = out->n_evaluated;
+  const int32_t ns = a.ctl.n_steps + 1;
+  double* rel64 = reinterpret_cast<double*>(smem_raw);
+  double* st64 = rel64 + ((ns + 1) & ~1);
+  const double amp = a.sac_ctl ? a.sac_ctl[2 * sac] : a.amplitude;
+  const double pwd = a.sac_ctl ? a.sac_ctl[2 * sac + 1] : a.pw_default;
+  double sgn, Aprime;
+  stage_trace<double>(a.rec + sac * (int64_t)ns, ns, amp, rel64, sgn, Aprime);
+  __syncwarp();
+  finalize_topk<METRIC, true>(a, sac, le, li, nf, neval, out, rel64, st64, sgn, Aprime, pwd);
+}
 
 // ---------------------------------------------------------------------------
 // The fused fit kernel.  gridDim.y = saccades of this launch (1 for a single
@@ -278,13 +435,6 @@ __global__ void __launch_bounds__(OPMM_FIT_LB_THREADS, OPMM_FIT_LB_BLOCKS) fit_k
   T* rel = reinterpret_cast<T*>(smem_raw);
   double2* tab = reinterpret_cast<double2*>(smem_raw + rel_bytes<T>(ns));
   T* stash = reinterpret_cast<T*>(smem_raw + rel_bytes<T>(ns) + exp_tab_bytes());  // [10][block] vec2
-  // certification scratch follows the stash (fp32 + a.certify only)
-  unsigned char* cert_raw = smem_raw + rel_bytes<T>(ns) + exp_tab_bytes() + stash_bytes<T>(blockDim.x);
-  const bool certify = sizeof(T) == 4 && a.certify;
-  // second-best (E, idx) per thread lives in the certify scratch, not in registers
-  double* sec_e = reinterpret_cast<double*>(cert_raw) + blockDim.x + threadIdx.x;
-  int64_t* sec_i = reinterpret_cast<int64_t*>(cert_raw) + 3 * blockDim.x + threadIdx.x;
-  if (certify) { *sec_e = __longlong_as_double(0x7ff0000000000000LL); *sec_i = INT64_MAX; }
   for (int j = threadIdx.x; j < EXP_TAB_N; j += blockDim.x) tab[j] = a.exp_tab[j];
   const int64_t sac = (int64_t)blockIdx.y + a.sac_begin;
   const double amp = a.sac_ctl ? a.sac_ctl[2 * sac] : a.amplitude;
@@ -317,10 +467,6 @@ __global__ void __launch_bounds__(OPMM_FIT_LB_THREADS, OPMM_FIT_LB_BLOCKS) fit_k
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int nbins = blockDim.x < 256 ? (int)blockDim.x : 256;   // multiple of 32
   const int64_t sstride = (int64_t)gridDim.x * a.super_tile;
-#ifdef OPMM_EXP_BLOCKTIME   // timing experiment only: per-block start/end in err_out
-  unsigned long long t_start;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
-#endif
   for (int64_t sb = a.begin + (int64_t)blockIdx.x * a.super_tile; sb < a.end; sb += sstride) {
     const int cnt = (int)min(a.super_tile, a.end - sb);
     if (tid < nbins) s_hist[tid] = 0;
@@ -382,42 +528,16 @@ __global__ void __launch_bounds__(OPMM_FIT_LB_THREADS, OPMM_FIT_LB_BLOCKS) fit_k
       const int off = a.sort_lanes ? (int)s_perm[sl] : sl;
       const int64_t i = sb + off;
       double p[NP];
-#ifdef OPMM_EXP_NOGEN   // timing experiment only: cheap stand-in candidates
-#pragma unroll
-      for (int d = 0; d < NP; ++d)
-        p[d] = a.space.lo[d] * (1.0 + (double)(((uint64_t)i * 7 + d) & 1023) * 1e-3);
-      p[PW_] = generate_pw(a.space, (uint32_t)sac, i, tab);   // same pulse ends -> same sort
-#else
       generate_opc(a.space, (uint32_t)sac, i, p, tab);
-#endif
       const double E = evaluate<T, INTEG, METRIC, false>(p, a.ctl, Aprime, pwd, rel, nullptr, 0,
                                                          sgn, nullptr, stash, !a.space.all_physical);
       if (valid) {
-#ifndef OPMM_EXP_BLOCKTIME
-        if (a.err_out) a.err_out[sac * a.err_ld + i] = E;
-#endif
+        if (a.err_out) a.err_out[sac * a.err_ld + i - a.err_base] = E;
         nf += E < __longlong_as_double(0x7ff0000000000000LL) ? 1 : 0;
-        if (better(E, i, best_e, best_i)) {
-          if (certify) { *sec_e = best_e; *sec_i = best_i; }
-          best_e = E; best_i = i;
-        } else if (certify && better(E, i, *sec_e, *sec_i)) {
-          *sec_e = E; *sec_i = i;
-        }
+        if (better(E, i, best_e, best_i)) { best_e = E; best_i = i; }
       }
     }
     __syncthreads();   // s_hist / s_perm / s_next are reused by the next pass
-  }
-#ifdef OPMM_EXP_BLOCKTIME
-  if (threadIdx.x == 0 && a.err_out) {
-    unsigned long long t_end;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
-    a.err_out[2 * blockIdx.x] = (double)t_start;
-    a.err_out[2 * blockIdx.x + 1] = (double)t_end;
-  }
-#endif
-  if (sizeof(T) == 4 && a.certify) {
-    cert_epilogue<T, METRIC>(a, sac, best_e, best_i, *sec_e, *sec_i, nf, sgn, Aprime, pwd, cert_raw);
-    return;
   }
   fit_epilogue(a, sac, best_e, best_i, nf);
 }
@@ -659,7 +779,7 @@ __device__ __noinline__ void super_direct(const FitArgs& a, int64_t sac, int64_t
       E = finish_error<METRIC>(acc, a.ctl.n_steps + 1);
     }
     if (bad) {
-      if (a.err_out) a.err_out[sac * a.err_ld + i] = E;
+      if (a.err_out) a.err_out[sac * a.err_ld + i - a.err_base] = E;
       nf += E < INF ? 1 : 0;
       if (better(E, i, best_e, best_i)) { best_e = E; best_i = i; }
     }
@@ -745,7 +865,7 @@ __global__ void __launch_bounds__(TM ? SUPER_MAX_WARPS * 32 : 32) fit_super_kern
   int64_t best_i = INT64_MAX;
   int64_t nf = 0;
   auto record = [&](double E, int64_t i) {
-    if (a.err_out) a.err_out[sac * a.err_ld + i] = E;
+    if (a.err_out) a.err_out[sac * a.err_ld + i - a.err_base] = E;
     nf += E < INF ? 1 : 0;
     if (better(E, i, best_e, best_i)) { best_e = E; best_i = i; }
   };
@@ -963,7 +1083,7 @@ __global__ void __launch_bounds__(FIT2_THREADS, 1) fit2_kernel(FitArgs a) {
     for (int c = 0; c < 2; ++c) {
       const double E = finish_error<METRIC>(acc[c], ns);
       if (valid[c]) {
-        if (a.err_out) a.err_out[sac * a.err_ld + ic[c]] = E;
+        if (a.err_out) a.err_out[sac * a.err_ld + ic[c] - a.err_base] = E;
         nf += E < __longlong_as_double(0x7ff0000000000000LL) ? 1 : 0;
         if (better(E, ic[c], best_e, best_i)) { best_e = E; best_i = ic[c]; }
       }
@@ -1220,7 +1340,7 @@ __global__ void __launch_bounds__(FIT3_THREADS, 1) fit3_kernel(FitArgs a) {
                                                      T(1), stash, blockDim.x);
       const double E = finish_error<METRIC>(acc, ns);
       if (i0 < a.end) {
-        if (a.err_out) a.err_out[sac * a.err_ld + i0] = E;
+        if (a.err_out) a.err_out[sac * a.err_ld + i0 - a.err_base] = E;
         nf += E < __longlong_as_double(0x7ff0000000000000LL) ? 1 : 0;
         if (better(E, i0, best_e, best_i)) { best_e = E; best_i = i0; }
       }
@@ -1248,15 +1368,22 @@ size_t fit3_smem(int precision, int32_t n_samples) {
 }
 
 // ---------------------------------------------------------------------------
-// world > 1: merge the gathered per-rank partials (lexicographic) and write
-// the final result with the regenerated winner OPC.  One warp.
+// world > 1: merge the gathered per-rank results of saccade `sac` (rank r's
+// RankPartial at gathered + r * stride; the lists only when a.topk) --
+// lexicographic (E, index), n_finite and n_evaluated summed, the rank lists
+// merged into the global exact top-K -- and write the final result with the
+// regenerated winner OPC.  certify: the merged fp32 list is re-scored in fp64
+// here, so every rank returns the same certified winner.  One warp.
 // ---------------------------------------------------------------------------
-__global__ void merge_kernel(const Partial* gathered, int world, SpaceDev sp, uint32_t saccade,
-                             opmm_fit_result* out, const double2* tab) {
-  double e = __longlong_as_double(0x7ff0000000000000LL);
+template <int METRIC>
+__global__ void __launch_bounds__(32) merge_kernel(FitArgs a, const unsigned char* gathered,
+                                                   int world, int64_t stride, int64_t sac) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  double e = dinf();
   int64_t i = INT64_MAX, n = 0, ne = 0;
-  for (int r = threadIdx.x; r < world; r += 32) {
-    const Partial q = gathered[r];
+  for (int r = lane; r < world; r += 32) {
+    const Partial q = reinterpret_cast<const RankPartial*>(gathered + (int64_t)r * stride)->p;
     if (better(q.e, q.i, e, i)) { e = q.e; i = q.i; }
     n += q.nf;
     ne += q.neval;
@@ -1264,10 +1391,34 @@ __global__ void merge_kernel(const Partial* gathered, int world, SpaceDev sp, ui
   warp_argmin(e, i);
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
-    n += __shfl_xor_sync(0xffffffffu, n, off);
-    ne += __shfl_xor_sync(0xffffffffu, ne, off);
+    n += __shfl_xor_sync(FULL, n, off);
+    ne += __shfl_xor_sync(FULL, ne, off);
   }
-  if (threadIdx.x == 0) write_result(sp, saccade, e, i, n, ne, out, tab);
+  opmm_fit_result* out = a.final_out + (sac - a.out_base);
+  if (lane == 0) write_result(a.space, (uint32_t)sac, e, i, n, ne, out, a.exp_tab);
+  __syncwarp();
+  if (!a.topk) {
+    out->topk_index[lane] = -1;
+    out->topk_err[lane] = dinf();
+    return;
+  }
+  double le = dinf();
+  int64_t li = INT64_MAX;
+  for (int r = 0; r < world; ++r) {
+    const RankPartial* q = reinterpret_cast<const RankPartial*>(gathered + (int64_t)r * stride);
+    tk_merge_list(le, li, q->e[lane], q->i[lane], a.topk);
+  }
+  const double pwd = a.sac_ctl ? a.sac_ctl[2 * sac + 1] : a.pw_default;
+  const int32_t ns = a.ctl.n_steps + 1;
+  double* rel64 = reinterpret_cast<double*>(smem_raw);
+  double* st64 = rel64 + ((ns + 1) & ~1);
+  double sgn = 1.0, Aprime = 0.0;
+  if (a.certify) {
+    const double amp = a.sac_ctl ? a.sac_ctl[2 * sac] : a.amplitude;
+    stage_trace<double>(a.rec + sac * (int64_t)ns, ns, amp, rel64, sgn, Aprime);
+    __syncwarp();
+  }
+  finalize_topk<METRIC, true>(a, sac, le, li, n, ne, out, rel64, st64, sgn, Aprime, pwd);
 }
 
 // ---------------------------------------------------------------------------
@@ -1413,10 +1564,57 @@ cudaError_t launch_fit(const void* fn, const FitArgs& a, dim3 grid, int block, s
   return cudaLaunchKernel(fn, grid, dim3(block), args, smem, st);
 }
 
-cudaError_t launch_merge(const Partial* gathered, int world, const SpaceDev& sp, uint32_t saccade,
-                         opmm_fit_result* out, const double2* tab, cudaStream_t st) {
-  merge_kernel<<<1, 32, 0, st>>>(gathered, world, sp, saccade, out, tab);
+cudaError_t launch_merge(const FitArgs& a, const void* gathered, int world, size_t stride,
+                         int64_t sac, opmm_fit_result* out, int metric, size_t smem,
+                         cudaStream_t st) {
+  FitArgs b = a;
+  b.final_out = out;   // finalize_result writes final_out + (sac - out_base)
+  b.out_base = sac;
+  const unsigned char* g = static_cast<const unsigned char*>(gathered);
+  if (metric == 0) merge_kernel<0><<<1, 32, smem, st>>>(b, g, world, (int64_t)stride, sac);
+  else merge_kernel<1><<<1, 32, smem, st>>>(b, g, world, (int64_t)stride, sac);
   return cudaGetLastError();
+}
+
+const void* topk_kernel_ptr(int metric) {
+  return metric == 0 ? reinterpret_cast<const void*>(&topk_kernel<0>)
+                     : reinterpret_cast<const void*>(&topk_kernel<1>);
+}
+
+cudaError_t launch_topk(const FitArgs& a, int blocks, int S, size_t smem, int metric,
+                        cudaStream_t st) {
+  for (int s0 = 0; s0 < S; s0 += 65535) {
+    FitArgs b = a;
+    b.sac_begin = a.sac_begin + s0;
+    void* bargs[] = {&b};
+    const int sn = S - s0 < 65535 ? S - s0 : 65535;
+    const cudaError_t e = cudaLaunchKernel(topk_kernel_ptr(metric), dim3(blocks, sn), dim3(TOPK_BLOCK),
+                                           bargs, smem, st);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+const void* cert_kernel_ptr(int metric) {
+  return metric == 0 ? reinterpret_cast<const void*>(&cert_kernel<0>)
+                     : reinterpret_cast<const void*>(&cert_kernel<1>);
+}
+
+cudaError_t launch_cert(const FitArgs& a, int S, size_t smem, int metric, cudaStream_t st) {
+  for (int s0 = 0; s0 < S; s0 += 65535) {
+    FitArgs b = a;
+    b.sac_begin = a.sac_begin + s0;
+    void* bargs[] = {&b};
+    const int sn = S - s0 < 65535 ? S - s0 : 65535;
+    const cudaError_t e = cudaLaunchKernel(cert_kernel_ptr(metric), dim3(sn), dim3(32), bargs, smem, st);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+const void* merge_kernel_ptr(int metric) {
+  return metric == 0 ? reinterpret_cast<const void*>(&merge_kernel<0>)
+                     : reinterpret_cast<const void*>(&merge_kernel<1>);
 }
 
 template <typename T, int INTEG, int METRIC>

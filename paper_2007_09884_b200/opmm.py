@@ -49,17 +49,22 @@ class SearchSpace(C.Structure):
                 ("levels", C.c_int32 * NPARAM)]
 
 
+MAX_TOPK = 32
+FIT_FLAG_NO_LANE_SORT, FIT_FLAG_SUPER_SMEM, FIT_FLAG_NO_GRAPH = 1, 2, 4
+
+
 class FitOptions(C.Structure):
     _fields_ = [("precision", C.c_int32), ("metric", C.c_int32), ("integrator", C.c_int32),
                 ("block_size", C.c_int32), ("grid_blocks", C.c_int32), ("cpu_check", C.c_int32),
-                ("kernel_variant", C.c_int32), ("certify", C.c_int32), ("err_out", C.c_void_p)]
+                ("kernel_variant", C.c_int32), ("certify", C.c_int32), ("top_k", C.c_int32),
+                ("flags", C.c_uint32), ("err_out", C.c_void_p)]
 
 
 class FitResult(C.Structure):
     _fields_ = [("best_index", C.c_int64), ("opt_err", C.c_double), ("cpu_check", C.c_double),
                 ("opc", C.c_double * NPARAM), ("n_finite", C.c_int64), ("n_evaluated", C.c_int64),
-                ("top_k", C.c_int32), ("certified", C.c_int32), ("topk_index", C.c_int64 * 8),
-                ("topk_err", C.c_double * 8)]
+                ("top_k", C.c_int32), ("certified", C.c_int32), ("topk_index", C.c_int64 * MAX_TOPK),
+                ("topk_err", C.c_double * MAX_TOPK)]
 
     def as_dict(self) -> dict:
         return {"best_index": self.best_index, "opt_err": self.opt_err, "cpu_check": self.cpu_check,
@@ -110,6 +115,9 @@ def _load():
         "opmm_shard_range": ([i64, C.c_int, C.c_int, C.POINTER(i64), C.POINTER(i64)], st),
         "opmm_merge_argmin": ([dp, C.POINTER(i64), C.c_int, dp, C.POINTER(i64)], st),
         "opmm_validate": ([C.POINTER(Control), C.POINTER(SearchSpace), i64], st),
+        "opmm_merge_topk": ([dp, C.POINTER(i64), C.c_int, C.c_int, dp, C.POINTER(i64)], st),
+        "opmm_certify_topk": ([dp, dp, C.POINTER(i64), C.c_int, C.c_double, C.POINTER(i32),
+                               C.POINTER(i64), dp], st),
         "opmm_generate": ([vp, C.POINTER(SearchSpace), C.c_uint32, i64, i64, vp, i64, vp], st),
         "opmm_simulate": ([vp, vp, i64, i64, C.POINTER(Control), i32, i32, vp, i64, vp, vp], st),
         "opmm_simulate_batch": ([vp, vp, i64, i64, C.POINTER(Control), i32, i32, vp, i64, vp, vp], st),
@@ -135,7 +143,8 @@ def _load():
 _lib = _load()
 EXPORTED = ("opmm_version", "opmm_last_error", "opmm_create", "opmm_nccl_unique_id",
             "opmm_create_nccl", "opmm_destroy", "opmm_get_stream", "opmm_last_kernel_ms",
-            "opmm_shard_range", "opmm_merge_argmin", "opmm_validate", "opmm_generate",
+            "opmm_shard_range", "opmm_merge_argmin", "opmm_merge_topk", "opmm_certify_topk",
+            "opmm_validate", "opmm_generate",
             "opmm_simulate", "opmm_simulate_batch", "opmm_score", "opmm_simulate_score", "opmm_fit", "opmm_fit_async",
             "opmm_fit_batch", "opmm_estimate_batch", "opmm_nm_minimize_test")
 
@@ -178,9 +187,11 @@ def search_space(s) -> SearchSpace:
 
 
 def fit_options(precision=FP64, metric=METRIC_L1, integrator=INTEG_PROPAGATOR, block_size=0,
-                grid_blocks=0, cpu_check=1, err_out=None, kernel_variant=0, certify=0) -> FitOptions:
+                grid_blocks=0, cpu_check=1, err_out=None, kernel_variant=0, certify=0, top_k=0,
+                flags=0) -> FitOptions:
     return FitOptions(precision, metric, integrator, block_size, grid_blocks, cpu_check,
-                      kernel_variant, certify, _ptr(err_out) if err_out is not None else None)
+                      kernel_variant, certify, top_k, flags,
+                      _ptr(err_out) if err_out is not None else None)
 
 
 def _ptr(x):
@@ -292,6 +303,31 @@ def opmm_merge_argmin(errs, idxs) -> tuple[float, int]:
     if st not in (OK, ERR_NO_FINITE):
         _check(st, "opmm_merge_argmin")
     return be.value, bi.value
+
+
+def opmm_merge_topk(errs, idxs, K: int) -> tuple[np.ndarray, np.ndarray]:
+    """errs/idxs: [lists, K] sorted lists -> the merged K smallest (err, idx)."""
+    e = np.ascontiguousarray(errs, dtype=np.float64).reshape(-1, K)
+    i = np.ascontiguousarray(idxs, dtype=np.int64).reshape(-1, K)
+    oe, oi = np.zeros(K), np.zeros(K, dtype=np.int64)
+    _check(_lib.opmm_merge_topk(e.ctypes.data_as(C.POINTER(C.c_double)),
+                                i.ctypes.data_as(C.POINTER(C.c_int64)), e.shape[0], K,
+                                oe.ctypes.data_as(C.POINTER(C.c_double)),
+                                oi.ctypes.data_as(C.POINTER(C.c_int64))), "opmm_merge_topk")
+    return oe, oi
+
+
+def opmm_certify_topk(e32, e64, idx, scale: float) -> tuple[int, int, float]:
+    """(certified, best_index, best_err) of one merged fp32 list."""
+    a = np.ascontiguousarray(e32, dtype=np.float64)
+    b = np.ascontiguousarray(e64, dtype=np.float64)
+    i = np.ascontiguousarray(idx, dtype=np.int64)
+    c, bi, be = C.c_int32(), C.c_int64(), C.c_double()
+    _check(_lib.opmm_certify_topk(a.ctypes.data_as(C.POINTER(C.c_double)),
+                                  b.ctypes.data_as(C.POINTER(C.c_double)),
+                                  i.ctypes.data_as(C.POINTER(C.c_int64)), len(a), scale,
+                                  C.byref(c), C.byref(bi), C.byref(be)), "opmm_certify_topk")
+    return c.value, bi.value, be.value
 
 
 def opmm_validate(ctl=None, space=None, n_candidates: int = 0) -> None:

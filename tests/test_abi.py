@@ -51,8 +51,8 @@ def test_struct_layouts_match_header(opmm):
     # the C side static_asserts the same sizes (opmm_api.cu)
     assert ctypes.sizeof(opmm.Control) == 40
     assert ctypes.sizeof(opmm.SearchSpace) == 400
-    assert ctypes.sizeof(opmm.FitOptions) == 40
-    assert ctypes.sizeof(opmm.FitResult) == 320
+    assert ctypes.sizeof(opmm.FitOptions) == 48
+    assert ctypes.sizeof(opmm.FitResult) == 704
     assert ctypes.sizeof(opmm.NmOptions) == 48
     assert ctypes.sizeof(opmm.NmResult) == 176
     assert opmm.SearchSpace.levels.offset == 400 - 72

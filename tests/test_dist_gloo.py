@@ -160,3 +160,99 @@ def test_world2_super_node_shards_partition_the_grid():
     full = oracle.fit(rec, ctl, sp, 0, n)
     for rank, be, bi, _, _ in results:
         assert (be, bi) == (full["best_err"], full["best_index"])
+
+
+def _topk_rank_main(rank, world, port, q):
+    """One rank of the fp32-certified multi-GPU fit, on CPU: the rank's exact
+    top-K by (fp32 error, index) over its shard -- fp32 errors stood in by the
+    oracle's fp64 errors rounded to float32 -- all-gathered, merged with
+    opmm_merge_topk, re-scored in fp64 (oracle) and certified with
+    opmm_certify_topk, as the merge kernel does on the device."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import numpy as np
+        from paper_2007_09884_b200 import opmm
+        ctl = W.Control()
+        rec = oracle.positions(W.truth_opc(), ctl) + W.noise(ctl.n_steps + 1)
+        sp = W.paper_space()
+        N, K = 5000, 16
+        b, e = opmm.opmm_shard_range(N, rank, world)
+        E = oracle.fit(rec, ctl, sp, b, e, want_err=True)["err"]
+        e32 = E.astype(np.float32).astype(np.float64)
+        order = np.lexsort((np.arange(b, e), e32))[:K]
+        le = np.full(K, np.inf)
+        li = np.full(K, -1, dtype=np.int64)
+        le[:len(order)] = e32[order]
+        li[:len(order)] = order + b
+        ge = [torch.zeros(K, dtype=torch.float64) for _ in range(world)]
+        gi = [torch.zeros(K, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(ge, torch.from_numpy(le))
+        dist.all_gather(gi, torch.from_numpy(li))
+        me, mi = opmm.opmm_merge_topk(torch.stack(ge).numpy(), torch.stack(gi).numpy(), K)
+        e64 = np.array([oracle.objective(oracle.generate(sp, int(i)), rec, ctl) if i >= 0 else np.inf
+                        for i in mi])
+        rel, _, _ = oracle.relativize(rec, ctl.amplitude_deg)
+        cert = opmm.opmm_certify_topk(me, e64, mi, float(np.abs(rel).sum()))
+        q.put((rank, mi.tolist(), me.tolist(), cert))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_world2_topk_merge_and_fp32_certificate():
+    """Multi-GPU fp32 certification (the ranks' (E, index) lists
+    are gathered and merged; "solutions are sorted for accuracy",
+    PAPER.md:251): the merged list equals the unsharded exact top-K, every rank
+    returns the same certified winner, and it is the fp64 argmin of all N."""
+    import numpy as np
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_topk_rank_main, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = sorted(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ctl = W.Control()
+    rec = oracle.positions(W.truth_opc(), ctl) + W.noise(ctl.n_steps + 1)
+    sp = W.paper_space()
+    full = oracle.fit(rec, ctl, sp, 0, 5000, want_err=True)
+    e32 = full["err"].astype(np.float32).astype(np.float64)
+    order = np.lexsort((np.arange(5000), e32))[:16]
+    for rank, mi, me, cert in results:
+        assert mi == order.tolist() and me == e32[order].tolist()
+        assert cert == (1, full["best_index"], full["best_err"])
+    assert results[0][1:] == results[1][1:]
+
+
+def test_merge_topk_and_certificate_edge_cases():
+    """Host helpers: pads (-1) end a list, exact ties go to the lower index,
+    fewer entries than K pad the output; the certificate is refused when the
+    K-th fp32 error lies within T* or a listed candidate breaks the budget."""
+    import numpy as np
+    from paper_2007_09884_b200 import opmm
+    inf = np.inf
+    e = np.array([[1.0, 2.0, 2.0, inf], [0.5, 2.0, inf, inf]])
+    i = np.array([[10, 3, 7, -1], [4, 2, -1, -1]], dtype=np.int64)
+    me, mi = opmm.opmm_merge_topk(e, i, 4)
+    assert mi.tolist() == [4, 10, 2, 3] and me.tolist() == [0.5, 1.0, 2.0, 2.0]
+    me, mi = opmm.opmm_merge_topk(e[:1, :], i[:1, :], 4)
+    assert mi.tolist() == [10, 3, 7, -1] and me[3] == inf
+    idx = np.array([5, 9, 1, 2], dtype=np.int64)
+    e32 = np.array([10.0, 20.0, 30.0, 40.0])
+    assert opmm.opmm_certify_topk(e32, e32 + 1e-6, idx, 100.0) == (1, 5, 10.0 + 1e-6)
+    # K-th error inside T* = 10 + 2e-2: refused
+    assert opmm.opmm_certify_topk(np.array([10.0, 10.01, 10.015, 10.02]), np.full(4, 10.0), idx,
+                                  100.0)[0] == 0
+    # budget broken by a listed candidate (|E64 - E32| = 0.1 > delta = 1e-2): refused
+    e64 = e32.copy()
+    e64[2] = 29.9
+    c = opmm.opmm_certify_topk(e32, e64, idx, 100.0)
+    assert c[0] == 0 and c[1] == 5
+    # fewer finite candidates than K: certified, winner the fp64-best
+    c = opmm.opmm_certify_topk(np.array([3.0, inf, inf, inf]), np.array([2.9999, inf, inf, inf]),
+                               np.array([8, -1, -1, -1], dtype=np.int64), 1.0)
+    assert c == (1, 8, 2.9999)

@@ -241,7 +241,6 @@ def test_super_nccl_single_rank_node_sharding(opmm, h):
     code = r'''
 import os, sys, numpy as np
 sys.path.insert(0, os.getcwd())
-os.environ["OPMM_NCCL_SINGLE_RANK"] = "1"
 import torch, oracle, workloads as W
 from paper_2007_09884_b200 import opmm
 ctl = W.Control()
@@ -271,36 +270,19 @@ def test_super_tmem_and_smem_layouts_agree_bitwise(opmm, h):
     """The tensor-memory column layout (TMEM warps + shared-memory warps, one
     block per SM) and the shared-memory-only layout compute every error with
     the same operations in the same order: bit-identical err_out and result.
-    Forced through OPMM_SUPER_TMEM in subprocesses (read per call)."""
-    import os
-    import subprocess
-    import sys
-    code = r'''
-import os, sys, numpy as np
-sys.path.insert(0, os.getcwd())
-import torch, oracle, workloads as W
-from paper_2007_09884_b200 import opmm
-ctl = W.Control()
-rec = oracle.positions(W.truth_opc(), ctl) + W.noise(101)
-out = {}
-with opmm.opmm_create(0) as h:
-    for name, sp in (("g4_12", W.g4_space(12)), ("g4_40", W.g4_space(40))):
+    The shared-memory layout is forced with OPMM_FIT_FLAG_SUPER_SMEM."""
+    ctl = W.Control()
+    rec = oracle.positions(W.truth_opc(), ctl) + W.noise(101)
+    for sp in (W.g4_space(12), W.g4_space(40)):
         n = sp.n_grid()
-        for mode in ("0", "1"):
-            os.environ["OPMM_SUPER_TMEM"] = mode
+        out = []
+        for flags in (opmm.FIT_FLAG_SUPER_SMEM, 0):
             err = torch.empty(n, dtype=torch.float64, device="cuda")
-            r = opmm.opmm_fit(h, rec, ctl, sp, n, opmm.fit_options(kernel_variant=4, err_out=err))
-            out[(name, mode)] = (r["best_index"], r["opt_err"], r["n_finite"], err.cpu().numpy())
-        a, b = out[(name, "0")], out[(name, "1")]
-        assert a[:3] == b[:3], (name, a[:3], b[:3])
-        assert np.array_equal(a[3], b[3]), name
-print("tmem-smem ok")
-'''
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    p = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
-                       timeout=300)
-    assert p.returncode == 0, p.stdout + p.stderr
-    assert "tmem-smem ok" in p.stdout
+            r = opmm.opmm_fit(h, rec, ctl, sp, n, opmm.fit_options(kernel_variant=4, err_out=err,
+                                                                   flags=flags))
+            out.append((r["best_index"], r["opt_err"], r["n_finite"], err.cpu().numpy()))
+        assert out[0][:3] == out[1][:3]
+        assert np.array_equal(out[0][3], out[1][3])
 
 
 @pytest.mark.parametrize("metric", [0, 1])

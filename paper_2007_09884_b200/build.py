@@ -49,28 +49,6 @@ def _compile(src: str) -> tuple[str, str]:
     return obj, p.stderr
 
 
-def build_variant(name: str, defines: list[str]) -> str:
-    """Build an experimental variant build/variants/libopmm_<name>.so with extra
-    -D flags (performance experiments only; the product is `build()`)."""
-    out_dir = os.path.join(BUILD, "variants", name)
-    os.makedirs(out_dir, exist_ok=True)
-    lib = os.path.join(BUILD, "variants", f"libopmm_{name}.so")
-
-    def comp(src):
-        obj = os.path.join(out_dir, src + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, src), "-o", obj]
-        p = subprocess.run(cmd, capture_output=True, text=True)
-        if p.returncode != 0:
-            raise RuntimeError(f"nvcc failed for {src} ({name}):\n{p.stderr}")
-        return obj
-    with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
-        objs = list(ex.map(comp, SOURCES))
-    p = subprocess.run([NVCC, *ARCH, "-shared", "-o", lib, *objs, "-ldl"], capture_output=True, text=True)
-    if p.returncode != 0:
-        raise RuntimeError(f"link failed ({name}):\n{p.stderr}")
-    return lib
-
-
 def build(force: bool = False, verbose: bool = False) -> str:
     digest = _digest()
     if not force and os.path.exists(LIB) and os.path.exists(STAMP) and open(STAMP).read() == digest:

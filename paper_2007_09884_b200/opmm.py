@@ -16,8 +16,7 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-# OPMM_LIB overrides the library path (used only by tools/ to time build variants)
-LIB_PATH = os.environ.get("OPMM_LIB", os.path.join(_PKG, "libopmm.so"))
+LIB_PATH = os.path.join(_PKG, "libopmm.so")
 
 NPARAM = 18
 MAX_STEPS = 16384

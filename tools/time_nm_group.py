@@ -1,5 +1,4 @@
-"""Group-schedule NM kernel time at a few sizes (A/B of build variants via
-OPMM_LIB; GPU box).   python tools/time_nm_group.py [S ...]"""
+"""Group-schedule NM kernel time at a few sizes (GPU box).   python tools/time_nm_group.py [S ...]"""
 import os
 import sys
 

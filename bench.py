@@ -49,25 +49,47 @@ FLOP_PER_STEP = 34
 FLOP_SETUP = 1285
 FP64_INST_PER_STEP = 18    # fp64-pipe instructions per step (loop)
 FP64_INST_SETUP = 797      # fp64-pipe instructions per candidate outside the loop (ncu)
-SMS, FP64_LANES, SM_MAX_MHZ = 148, 64, 1965.0
+SMS, FP64_LANES, FP32_LANES, SM_MAX_MHZ = 148, 64, 128, 1965.0
 FP64_PEAK_TFLOPS = SMS * FP64_LANES * 2 * SM_MAX_MHZ * 1e6 / 1e12   # 37.23
+FP32_PEAK_TFLOPS = SMS * FP32_LANES * 2 * SM_MAX_MHZ * 1e6 / 1e12   # 74.45
 FP64_MEASURED_TFLOPS = 33.90   # profiles/r01_fma_peak.txt (DFMA microbenchmark)
 
 
-def ncu_traffic_bytes():
-    """dram__bytes_read.sum + dram__bytes_write.sum of the fit kernel from the
+def ncu_traffic_bytes(kernel="fit_kernel<double, 0, 0>"):
+    """dram__bytes_read.sum + dram__bytes_write.sum of a fit kernel from the
     committed `ncu --set full` capture summary (profiles/), per launch."""
     units = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-    path = os.path.join(ROOT, "profiles", "r01_fit_kernel_fp64_ncu_full.txt")
+    path = os.path.join(ROOT, "profiles", "r02_fit_kernels_ncu_full.txt")
     try:
-        tot = 0.0
+        tot, on = 0.0, False
         for line in open(path):
+            if line.startswith("kernel:"):
+                on = kernel in line
+                continue
             parts = line.split()
-            if parts and parts[0] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            if on and parts and parts[0] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
                 tot += float(parts[1]) * units[parts[2]]
         return tot or None
     except OSError:
         return None
+
+
+def fp32_roofline(per_gpu, kernel_ms):
+    """The fp32 fit kernel (uncertified, the kernel the fp32 leg's time is
+    spent in) against both pipes it uses: the fp32 loop's executed flops
+    (34 per step) vs the nominal FP32 peak, and the fp64
+    generation + setup flops (1285 per candidate) vs the nominal FP64 peak.
+    The two pipes share the warp schedulers' issue slots, so frac = the sum
+    of the two fractions; ncu's issue utilisation is in profiles/."""
+    t = kernel_ms * 1e-3
+    f32 = FLOP_PER_STEP * N_STEPS * per_gpu / t / 1e12
+    f64 = FLOP_SETUP * per_gpu / t / 1e12
+    return {"bound": "alu", "unit": "TFLOP/s", "kernel": "fit_kernel<float, propagator, L1>",
+            "kernel_ms": kernel_ms, "achieved": f32, "peak": FP32_PEAK_TFLOPS,
+            "fp32_frac": f32 / FP32_PEAK_TFLOPS, "fp64_setup_tflops": f64,
+            "fp64_frac": f64 / FP64_PEAK_TFLOPS, "frac": f32 / FP32_PEAK_TFLOPS + f64 / FP64_PEAK_TFLOPS,
+            "traffic": ncu_traffic_bytes("fit_kernel<float, 0, 0>"),
+            "peak_basis": "148 SM x 128 FP32 / 64 FP64 lanes x 2 x 1965 MHz (nominal)"}
 
 
 def workload_config(per_gpu, world):
@@ -144,14 +166,35 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_baseline(target_s=12.0, sample_cap=3 * 10**6):
-    """The oracle as it stands, all host cores (OpenMP), on a bounded sample
-    of the same workload (same trace, same candidate stream)."""
+def host_info():
+    """CPU model and the oracle's compiler, for the cpu_baseline record."""
+    model = None
+    try:
+        for line in subprocess.run(["lscpu"], capture_output=True, text=True).stdout.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    try:
+        cc = subprocess.run(["gcc", "--version"], capture_output=True, text=True).stdout.splitlines()[0]
+    except (OSError, IndexError):
+        cc = "gcc"
+    import oracle
+    return {"cpu_model": model, "compiler": f"{cc}; {' '.join(oracle.CFLAGS)}"}
+
+
+def cpu_baseline(target_s=12.0, sample_cap=3 * 10**6, single_n=20000):
+    """The oracle as it stands on the host: one thread on a 2*10^4-candidate
+    sample, then all cores (OpenMP) on a bounded sample of the same workload
+    (same trace, same candidate stream)."""
     import oracle
     ctl = W.Control()
     rec = make_trace()
     sp = W.paper_space()
     cores = len(os.sched_getaffinity(0))
+    t0 = time.perf_counter()
+    oracle.fit(rec, ctl, sp, 0, single_n, nthreads=1)
+    single = single_n / (time.perf_counter() - t0)
     t0 = time.perf_counter()
     oracle.fit(rec, ctl, sp, 0, 20000, nthreads=cores)
     rate0 = 20000 / (time.perf_counter() - t0)
@@ -159,9 +202,11 @@ def cpu_baseline(target_s=12.0, sample_cap=3 * 10**6):
     t0 = time.perf_counter()
     oracle.fit(rec, ctl, sp, 0, n, nthreads=cores)
     dt = time.perf_counter() - t0
-    return {"value": n / dt, "unit": "candidate sims/s", "cores": cores, "kind": "oracle",
-            "sample": f"candidates [0, {n}) of the bench workload (same trace and Philox stream), "
-                      f"{dt:.1f} s, OpenMP static chunks, gcc -O2 -ffp-contract=off"}
+    return {"value": n / dt, "unit": "candidate sims/s", "cores": cores, "threads": cores,
+            "kind": "oracle", "single_thread_value": single,
+            "sample": f"all cores: candidates [0, {n}) of the bench workload (same trace and Philox "
+                      f"stream), {dt:.1f} s, OpenMP static chunks; single thread: [0, {single_n})",
+            **host_info()}
 
 
 def run_reference(args):
@@ -173,12 +218,17 @@ def run_reference(args):
     rec = make_trace()
     sp = W.paper_space()
     cores = len(os.sched_getaffinity(0))
-    sample = 200000
+    n_total = args.per_gpu * args.gpus
+    sample = min(200000, n_total)
+    # step s scores candidates [b, b + sample) of the workload's [0, n_total),
+    # wrapping around: every sample lies inside the workload the config names
+    starts = [((k * sample) % n_total) if (k * sample) % n_total + sample <= n_total else 0
+              for k in range(args.warmup + args.steps)]
     for s in range(args.warmup):
-        oracle.fit(rec, ctl, sp, s * sample, (s + 1) * sample, nthreads=cores)
+        oracle.fit(rec, ctl, sp, starts[s], starts[s] + sample, nthreads=cores)
     times = []
     for s in range(args.steps):
-        b = (args.warmup + s) * sample
+        b = starts[args.warmup + s]
         t0 = time.perf_counter()
         oracle.fit(rec, ctl, sp, b, b + sample, nthreads=cores)
         times.append(time.perf_counter() - t0)
@@ -190,10 +240,14 @@ def run_reference(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {**workload_config(args.per_gpu, args.gpus),
                        "integrator": "rk4-classical (oracle)",
-                       "reference_step": f"{sample} candidates of the workload per step (bounded sample)"},
+                       "n_candidates_timed": sample * args.steps,
+                       "reference_step": f"{sample} candidates of the workload per step (bounded sample), "
+                                         f"index ranges {sorted(set(starts[args.warmup:]))} + {sample}, "
+                                         f"inside [0, {n_total})"},
             "cpu_baseline": {"value": value, "unit": "candidate sims/s", "cores": cores,
-                             "kind": "oracle",
-                             "sample": f"{sample} candidates per step x {args.steps} steps"},
+                             "threads": cores, "kind": "oracle",
+                             "sample": f"{sample} candidates per step x {args.steps} steps",
+                             **host_info()},
             "e2e": {"value": value, "unit": "candidate sims/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -424,11 +478,11 @@ def run_gpu(args):
     flush = torch.empty(512 * 2**20, dtype=torch.uint8, device="cuda")
     torch.cuda.synchronize()
 
-    def device_leg(precision):
-        # fp32 runs with certification: the exact top-32 by fp32 error, merged
+    def device_leg(precision, certify=True):
+        # fp32 runs with certification: the exact top-K by fp32 error, merged
         # over the ranks and re-scored in fp64
         opts = opmm.fit_options(precision=precision, cpu_check=0,
-                                certify=1 if precision == opmm.FP32 else 0)
+                                certify=1 if (precision == opmm.FP32 and certify) else 0)
         for _ in range(args.warmup):
             opmm.opmm_fit_async(h, rec_dev, ctl, sp, n_total, out_dev, opts)
         stream.synchronize()
@@ -455,6 +509,8 @@ def run_gpu(args):
         ms64, kms64, res64 = device_leg(opmm.FP64)
     clocks = clk.summary()
     ms32, kms32, res32 = device_leg(opmm.FP32)
+    # the fp32 fit kernel alone (uncertified): its pipes' roofline
+    _, kms32_plain, _ = device_leg(opmm.FP32, certify=False)
 
     # e2e: synchronous public call, trace in pinned host memory
     rec_host = torch.as_tensor(rec, dtype=torch.float64).pin_memory()
@@ -508,9 +564,10 @@ def run_gpu(args):
                      "fp64_issue_frac": (FP64_INST_PER_STEP * N_STEPS + FP64_INST_SETUP) * args.per_gpu
                      / (kms64 * 1e-3) / (SMS * FP64_LANES * SM_MAX_MHZ * 1e6)},
         "fp32": {"value": n_total / (ms32 * 1e-3), "ms_per_step": ms32, "kernel_ms": kms32,
+                 "roofline": fp32_roofline(args.per_gpu, kms32_plain),
                  "best_index": res32["best_index"], "certified": res32["certified"],
                  "opt_err_fp64": res32["opt_err"],
-                 "mode": "fp32 integrate+score, fp64 setup, exact top-32 by fp32 error (merged "
+                 "mode": "fp32 integrate+score, fp64 setup, exact top-8 by fp32 error (merged "
                          "over the ranks) re-scored in fp64 and certified"},
         "result": {"best_index": res64["best_index"], "opt_err": res64["opt_err"],
                    "n_finite": res64["n_finite"], "cpu_check": r["cpu_check"]},

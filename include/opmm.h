@@ -338,7 +338,8 @@ opmm_status opmm_fit_batch(opmm_handle* h, const double* recorded, int64_t S,
  * transformations evaluated simultaneously, the simplex sorted
  * every iteration, exit when BOTH the max coordinate distance
  * to the best vertex <= tol_x AND the max |f_i - f_best| <= tol_f
- * (PAPER.md:252-255), or after max_iter iterations.  Coefficients rho = 1,
+ * (PAPER.md:252-255), or after max_iter iterations, or at the time boundary
+ * (opmm_nm_options.time_budget_ms).  Coefficients rho = 1,
  * chi = 2, gamma = 0.5, sigma = 0.5 (SPEC D10); initial simplex: each
  * coordinate scaled by (1 + init_scale), zero coordinates set to
  * init_scale * 0.00025 (SPEC D9); stable sort (SPEC D14).  Scheduled one
@@ -382,6 +383,13 @@ typedef struct {
   double init_scale;     /* 0 = 0.05 (SPEC D9)                                      */
   int32_t cpu_check;     /* 1 = fill cpu_check (plant objectives)                  */
   int32_t schedule;      /* opmm_nm_schedule (0 = auto)                             */
+  double time_budget_ms; /* the paper's time boundary (SPEC D13
+                            time_budget): a problem stops once its own wall
+                            clock, from its start on the GPU (%globaltimer),
+                            exceeds this; exit_reason 2.  0 = none.  Checked
+                            once per iteration, after the tolerance test, so a
+                            converged problem still reports 0; max_iter is the
+                            deterministic equivalent                        */
 } opmm_nm_options;
 
 typedef struct {
@@ -393,7 +401,7 @@ typedef struct {
   int32_t gpu_evals;     /* evaluations performed (LOCKSTEP: n + 4 per iteration;
                             LANE: the serial algorithm's own, = func_evals;
                             GROUP: 4 per iteration, n per shrink)                 */
-  int32_t exit_reason;   /* 0 = tolerances met, 1 = max_iter                        */
+  int32_t exit_reason;   /* 0 = tolerances met, 1 = max_iter, 2 = time budget      */
 } opmm_nm_result;
 
 /* Estimate the 18-parameter OPC of S saccades independently (SPEC

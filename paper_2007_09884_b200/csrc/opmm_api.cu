@@ -28,7 +28,7 @@ static_assert(sizeof(opmm_fit_options) == 48, "opmm_fit_options layout");
 static_assert(sizeof(opmm_fit_result) == 704, "opmm_fit_result layout");
 static_assert(sizeof(Partial) == 32, "Partial layout");
 static_assert(sizeof(opmm::RankPartial) == 544, "RankPartial layout");
-static_assert(sizeof(opmm_nm_options) == 48, "opmm_nm_options layout");
+static_assert(sizeof(opmm_nm_options) == 56, "opmm_nm_options layout");
 static_assert(sizeof(opmm_nm_result) == 176, "opmm_nm_result layout");
 
 namespace {
@@ -591,13 +591,33 @@ opmm_status enqueue_fit_super(opmm_handle* h, const double* rec_dev, const opmm_
       ++sw;
     if (fixed <= lim_tm) { tm_warps = 4; smem_warps = sw; }
   }
+  // tensor memory: every TMEM warp keeps 4 columns per sample in its lane
+  // quadrant; the block allocates the next power of two >= 4 (n_steps + 4)
+  // columns (the flushes write whole groups of 4 samples).  tcgen05.alloc
+  // blocks while another block on the SM holds the columns, so the TMEM
+  // layout is used only when shared memory provably limits the SM to ONE
+  // block of this kernel (padding it if needed); otherwise the plain layout.
+  int32_t tm_cols = 32;
+  while (tm_cols < 4 * (ctl->n_steps + 4)) tm_cols *= 2;
+  if (tm_warps > 0) {
+    constexpr size_t kOneBlockSmem = 116 * 1024;   // 2 x (116 KB + static) > 228 KB per SM
+    const void* tf = opmm::fit_super_kernel_ptr(metric, true, false);
+    size_t sm = opmm::super_smem(ns, L, gt_n, smem_warps, tm_warps, f32);
+    if (sm < kOneBlockSmem) sm = kOneBlockSmem;
+    int per_sm = 0;
+    if (tm_cols > 512 ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tf, 32 * (tm_warps + smem_warps), sm) !=
+            cudaSuccess ||
+        per_sm != 1) {
+      cudaGetLastError();
+      tm_warps = 0;   // fall back to the shared-memory layout
+      smem_warps = 1;
+    }
+  }
   const void* fn = opmm::fit_super_kernel_ptr(metric, tm_warps > 0, f32);
   const int block = 32 * (tm_warps + smem_warps);
   size_t smem = opmm::super_smem(ns, L, gt_n, smem_warps, tm_warps, f32);
-  // tensor memory is allocated whole (512 columns) per block: keep one block per SM
-  // (two blocks need 2 x (smem + ~2 KB static/reserved) <= 228 KB of the SM)
-  constexpr size_t kOneBlockSmem = 116 * 1024;
-  if (tm_warps > 0 && smem < kOneBlockSmem) smem = kOneBlockSmem;
+  if (tm_warps > 0 && smem < 116 * 1024) smem = 116 * 1024;
   int grid = 1;
   CKS(grid_for(h, fn, block, smem, ne - nb, opts ? opts->grid_blocks : 0, &grid));
   if (S > 1 && !(opts && opts->grid_blocks)) {
@@ -646,6 +666,7 @@ opmm_status enqueue_fit_super(opmm_handle* h, const double* rec_dev, const opmm_
   a.sup_gt_n = gt_n;
   a.sup_tab = use_tab;
   a.sup_tm_warps = tm_warps;
+  a.sup_tm_cols = tm_cols;
   a.sup_st = st;
   a.node_begin = nb;
   a.node_end = ne;
@@ -867,7 +888,7 @@ const double kTable1Defaults[OPMM_NPARAM] = {2.5,  2.5, 1.2, 1.2,  0.046, 0.022,
 
 struct NmConfig {
   int obj, precision, metric, max_iter, cpu_check, schedule;
-  double tol_x, tol_f, init_scale;
+  double tol_x, tol_f, init_scale, time_budget_ms;
 };
 
 // OPMM_NM_SCHEDULE_AUTO: the group schedule from this many problems on (one
@@ -887,6 +908,9 @@ opmm_status nm_config(const opmm_nm_options* o, int dim, bool plant, NmConfig* c
   c->init_scale = (o && o->init_scale != 0.0) ? o->init_scale : 0.05;
   c->cpu_check = o ? o->cpu_check : 1;
   c->schedule = o ? o->schedule : OPMM_NM_SCHEDULE_AUTO;
+  c->time_budget_ms = o ? o->time_budget_ms : 0.0;
+  if (!(c->time_budget_ms >= 0.0) || !is_finite(c->time_budget_ms))
+    return fail(OPMM_ERR_INVALID_ARG, "time_budget_ms must be finite and >= 0");
   if (c->schedule < OPMM_NM_SCHEDULE_AUTO || c->schedule > OPMM_NM_SCHEDULE_GROUP)
     return fail(OPMM_ERR_INVALID_ARG, "bad NM schedule %d", c->schedule);
   if (plant && (c->obj < 0 || c->obj > 2)) return fail(OPMM_ERR_INVALID_ARG, "bad NM objective");
@@ -951,6 +975,10 @@ opmm_status nm_launch(opmm_handle* h, const NmConfig& c, const double* rec_dev,
   a.tol_x = c.tol_x;
   a.tol_f = c.tol_f;
   a.init_scale = c.init_scale;
+  // (a positive budget below 1 ns still stops at the first check)
+  a.time_budget_ns = c.time_budget_ms > 0.0
+                         ? (unsigned long long)std::fmax(1.0, std::fmin(c.time_budget_ms * 1e6, 9e18))
+                         : 0ull;
   const int64_t grid = n_blocks;
   if (grid == 0) return OPMM_OK;
   if (grid > 0x7fffffff) return fail(OPMM_ERR_INVALID_ARG, "too many problems");

@@ -723,6 +723,43 @@ __device__ __forceinline__ void make_prop_sub(const Setup& s, int nsub, Prop2<T>
 // Trace staging (D5/D6, reading Q7/Q8): s = sign(A) (+1 for A = 0),
 // A' = |A|, rel_k = s (rec_k - rec_0), into shared memory in the loop's type.
 // ----------------------------------------------------------------------------
+// Long fp64 traces (>= TMA_TRACE_BYTES, north_star: "staged once per block
+// into shared memory, or via TMA when long") arrive by one bulk copy
+// (cp.async.bulk, the TMA engine, completion counted on an mbarrier) and are
+// then relativized in place; shorter ones, fp32 traces and 16-byte-misaligned
+// sources take coalesced loads.  Every thread of the block must call it.
+constexpr int TMA_TRACE_BYTES = 48 * 1024;
+
+__device__ __forceinline__ bool stage_trace_bulk(const double* __restrict__ rec, int32_t n_samples,
+                                                 double* rel) {
+  const uint32_t bytes = (uint32_t)n_samples * 8u;
+  if (bytes < (uint32_t)TMA_TRACE_BYTES || (reinterpret_cast<uintptr_t>(rec) & 15u) ||
+      (reinterpret_cast<uintptr_t>(rel) & 15u))
+    return false;
+  __shared__ __align__(8) uint64_t bar;
+  const uint32_t b = (uint32_t)__cvta_generic_to_shared(&bar);
+  const uint32_t bulk = bytes & ~15u;   // the bulk unit is 16 bytes; a last odd sample by hand
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(b) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(b), "r"(bulk) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 :: "r"((uint32_t)__cvta_generic_to_shared(rel)), "l"(rec), "r"(bulk), "r"(b)
+                 : "memory");
+  }
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "TMA_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n\t"
+      "@!P1 bra TMA_WAIT_%=;\n}" :: "r"(b) : "memory");
+  if (threadIdx.x == 0 && bulk < bytes) rel[n_samples - 1] = rec[n_samples - 1];
+  __syncthreads();   // the hand-copied sample, and every thread past the wait
+  return true;
+}
+
 template <typename T>
 __device__ __forceinline__ void stage_trace(const double* __restrict__ rec, int32_t n_samples,
                                             double amplitude, T* rel, double& sgn,
@@ -731,6 +768,10 @@ __device__ __forceinline__ void stage_trace(const double* __restrict__ rec, int3
   const double A = isnan(amplitude) ? rec[n_samples - 1] - r0 : amplitude;
   sgn = A < 0.0 ? -1.0 : 1.0;
   Aprime = fabs(A);
+  if (sizeof(T) == 8 && stage_trace_bulk(rec, n_samples, reinterpret_cast<double*>(rel))) {
+    for (int k = threadIdx.x; k < n_samples; k += blockDim.x) rel[k] = (T)(sgn * ((double)rel[k] - r0));
+    return;
+  }
   for (int k = threadIdx.x; k < n_samples; k += blockDim.x) rel[k] = (T)(sgn * (rec[k] - r0));
 }
 

@@ -104,6 +104,8 @@ struct FitArgs {
   int32_t sup_gt_n;         // entries of the per-dimension level tables
   int32_t sup_tab;          // 1: nodes from the tables; 0: generic generator (too many levels)
   int32_t sup_tm_warps;     // warps 0..T-1 keep their columns in tensor memory (0: none)
+  int32_t sup_tm_cols;      // TMEM columns the block allocates (power of two, 32..512)
+  int32_t pad2_;
   int64_t sup_st;           // its mixed-radix stride (product of the lower levels)
   int64_t node_begin, node_end;   // this rank's nodes
 };
@@ -147,6 +149,7 @@ struct NmArgs {
   int64_t prob_begin, prob_end;
   int32_t dim, fn_id, max_iter, pad_;
   double tol_x, tol_f, init_scale;
+  unsigned long long time_budget_ns;   // per-problem wall-clock limit (0 = none)
   void* rel_global;         // long traces: device [S][n_steps+1] of the loop type; else null
 };
 

@@ -813,8 +813,8 @@ __global__ void __launch_bounds__(TM ? SUPER_MAX_WARPS * 32 : 32) fit_super_kern
   if (TM && T > 0) {
     if (wid == 0) {
       const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&s_tmem_base);
-      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" :: "r"(dst)
-                   : "memory");
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                   :: "r"(dst), "r"(a.sup_tm_cols) : "memory");
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -974,8 +974,8 @@ __global__ void __launch_bounds__(TM ? SUPER_MAX_WARPS * 32 : 32) fit_super_kern
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (wid == 0)
-      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" :: "r"(s_tmem_base)
-                   : "memory");
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;"
+                   :: "r"(s_tmem_base), "r"(a.sup_tm_cols) : "memory");
   }
   fit_epilogue(a, sac, best_e, best_i, nf);
 }

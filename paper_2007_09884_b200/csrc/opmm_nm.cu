@@ -32,6 +32,16 @@
 
 namespace opmm {
 
+// The paper's time-boundary exit (SPEC D13 time_budget): a
+// problem stops iterating once its own wall clock (from its start, read from
+// %globaltimer in ns) exceeds NmArgs::time_budget_ns (0 = none); exit_reason 2.
+__device__ __forceinline__ unsigned long long nm_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+
 #define Mr(a, b) __dmul_rn((a), (b))
 #define Ar(a, b) __dadd_rn((a), (b))
 #define Sr(a, b) __dsub_rn((a), (b))
@@ -205,6 +215,7 @@ __device__ __forceinline__ void nm_run(const NmArgs& a, unsigned char* smem_raw)
   T* stash = reinterpret_cast<T*>(smem_raw + NM_WARPS * sizeof(NmWarpSmem) +
                                   (GREL ? 0 : NM_WARPS * rel_bytes<T>(a.ctl.n_steps + 1)));
   if (prob >= a.prob_end) return;   // whole warp
+  const unsigned long long t0 = __shfl_sync(0xffffffffu, nm_now(), 0);
   const int n = OBJ == 3 ? a.dim : NP;   // plant objectives: always the 18-vector
   const int32_t ns = a.ctl.n_steps + 1;
   double sgn = 1.0, Aprime = 0.0, pwd = 0.0;
@@ -288,6 +299,8 @@ __device__ __forceinline__ void nm_run(const NmArgs& a, unsigned char* smem_raw)
       for (int i = 1; i <= n; ++i) ok = ok && fabs(W->S[ord[i]][lane] - v0) <= a.tol_x;
     }
     if (__all_sync(0xffffffffu, ok)) { reason = 0; break; }
+    if (a.time_budget_ns &&
+        __shfl_sync(0xffffffffu, nm_now(), 0) - t0 >= a.time_budget_ns) { reason = 2; break; }
     // centroid of the n best vertices (summed in vertex order, then / n)
     if (lane < n) {
       double sum = 0.0;
@@ -467,6 +480,7 @@ __global__ void __launch_bounds__(32, 1) nm_lane_kernel(NmArgs a) {
   const int64_t prob_raw = (int64_t)blockIdx.x * 32 + lane + a.prob_begin;
   const bool live = prob_raw < a.prob_end;
   const int64_t prob = live ? prob_raw : a.prob_end - 1;   // pad lanes mirror the last problem
+  const unsigned long long t0 = nm_now();
   const int n = OBJ == 3 ? a.dim : NP;
   double sgn = 1.0, Aprime = 0.0, pwd = 0.0;
   if (OBJ != 3) {
@@ -545,6 +559,7 @@ __global__ void __launch_bounds__(32, 1) nm_lane_kernel(NmArgs a) {
       }
     }
     if (ok) { st = NML_DONE; reason = 0; return; }
+    if (a.time_budget_ns && nm_now() - t0 >= a.time_budget_ns) { st = NML_DONE; reason = 2; return; }
     {
       // centroid of the n best, summed per coordinate in vertex order
       double sum[NM_NMAX];
@@ -722,6 +737,8 @@ __global__ void __launch_bounds__(32) nm_group_kernel(NmArgs a) {
   const int64_t prob_raw = (int64_t)blockIdx.x * NMQ_P + g + a.prob_begin;
   const bool live = prob_raw < a.prob_end;
   const int64_t prob = live ? prob_raw : a.prob_end - 1;   // pad groups mirror the last problem
+  // group-uniform clock: the group's first lane reads it
+  const unsigned long long t0 = __shfl_sync(0xffffffffu, nm_now(), 4 * g);
   const int n = OBJ == 3 ? a.dim : NP;
   double sgn = 1.0, Aprime = 0.0, pwd = 0.0;
   if (OBJ != 3) {
@@ -791,6 +808,8 @@ __global__ void __launch_bounds__(32) nm_group_kernel(NmArgs a) {
       }
       if (__all_sync(gmask, ok)) { st = NMQ_DONE; reason = 0; return; }
     }
+    if (a.time_budget_ns &&
+        __shfl_sync(gmask, nm_now(), 4 * g) - t0 >= a.time_budget_ns) { st = NMQ_DONE; reason = 2; return; }
 #pragma unroll
     for (int jj = 0; jj < (NM_NMAX + NMQ_G - 1) / NMQ_G; ++jj) {   // centroid, in vertex order
       const int j = q + NMQ_G * jj;

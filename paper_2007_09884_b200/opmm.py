@@ -76,7 +76,8 @@ class FitResult(C.Structure):
 class NmOptions(C.Structure):
     _fields_ = [("precision", C.c_int32), ("objective", C.c_int32), ("metric", C.c_int32),
                 ("max_iter", C.c_int32), ("tol_x", C.c_double), ("tol_f", C.c_double),
-                ("init_scale", C.c_double), ("cpu_check", C.c_int32), ("schedule", C.c_int32)]
+                ("init_scale", C.c_double), ("cpu_check", C.c_int32), ("schedule", C.c_int32),
+                ("time_budget_ms", C.c_double)]
 
 
 class NmResult(C.Structure):
@@ -429,10 +430,11 @@ def opmm_fit_batch(h: Handle, recorded, ctls, space, n_per: int,
 
 # ---------------------------------------------------------------------- Nelder-Mead
 def nm_options(precision=FP64, objective=NM_OBJ_PROPAGATOR, metric=METRIC_L1, max_iter=0, tol_x=0.0,
-               tol_f=0.0, init_scale=0.0, cpu_check=1, schedule=0) -> NmOptions:
-    """schedule: NM_SCHEDULE_AUTO / _LOCKSTEP / _LANE / _GROUP (opmm.h)."""
+               tol_f=0.0, init_scale=0.0, cpu_check=1, schedule=0, time_budget_ms=0.0) -> NmOptions:
+    """schedule: NM_SCHEDULE_AUTO / _LOCKSTEP / _LANE / _GROUP (opmm.h);
+    time_budget_ms: the paper's per-problem time boundary (0 = none)."""
     return NmOptions(precision, objective, metric, max_iter, tol_x, tol_f, init_scale, cpu_check,
-                     schedule)
+                     schedule, time_budget_ms)
 
 
 def opmm_estimate_batch(h: Handle, recorded, ctls, x0=None, options: NmOptions | None = None) -> list:

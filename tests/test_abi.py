@@ -53,7 +53,7 @@ def test_struct_layouts_match_header(opmm):
     assert ctypes.sizeof(opmm.SearchSpace) == 400
     assert ctypes.sizeof(opmm.FitOptions) == 48
     assert ctypes.sizeof(opmm.FitResult) == 704
-    assert ctypes.sizeof(opmm.NmOptions) == 48
+    assert ctypes.sizeof(opmm.NmOptions) == 56
     assert ctypes.sizeof(opmm.NmResult) == 176
     assert opmm.SearchSpace.levels.offset == 400 - 72
     assert opmm.FitResult.n_finite.offset == 168

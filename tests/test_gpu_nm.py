@@ -185,3 +185,31 @@ def test_long_trace_uses_global_trace_workspace(opmm, h, schedule):
     fast = opmm.opmm_estimate_batch(h, rec[None, :], [ctl],
                                     options=opmm.nm_options(max_iter=15, cpu_check=1, schedule=schedule))
     assert abs(fast[0]["cpu_check"] - fast[0]["f"]) <= 1e-9 * fast[0]["f"]
+
+
+@SCHEDULES
+def test_time_budget_exit(opmm, h, schedule):
+    """The paper's time boundary (SPEC D13 time_budget): a
+    budget shorter than any iteration stops every problem at its first check
+    (iteration 1, after the initial simplex) with exit_reason 2 -- bit-equal
+    to the oracle's run cut off by max_iter = 1 -- and a budget no run reaches
+    changes nothing."""
+    S = 12
+    amp, pw, truths = W.population(S)
+    ctls = [W.Control(n_steps=150, amplitude_deg=float(amp[s]), pw_default_ms=float(pw[s]))
+            for s in range(S)]
+    recs = np.array([oracle.positions(truths[s], ctls[s]) + W.noise(151, seed=1000 + s)
+                     for s in range(S)])
+    base = dict(objective=opmm.NM_OBJ_REFERENCE, max_iter=40, cpu_check=0, schedule=schedule)
+    tiny = opmm.opmm_estimate_batch(h, recs, ctls, options=opmm.nm_options(time_budget_ms=1e-9, **base))
+    o1 = oracle.estimate_batch(recs, ctls, max_iter=1)
+    for s in range(S):
+        assert (tiny[s]["iterations"], tiny[s]["exit_reason"]) == (1, 2), s
+        assert tiny[s]["x"].tolist() == o1["x"][s].tolist() and tiny[s]["f"] == float(o1["f"][s])
+    ref = opmm.opmm_estimate_batch(h, recs, ctls, options=opmm.nm_options(**base))
+    big = opmm.opmm_estimate_batch(h, recs, ctls, options=opmm.nm_options(time_budget_ms=1e5, **base))
+    for a, b in zip(ref, big):
+        assert (a["iterations"], a["exit_reason"], a["f"]) == (b["iterations"], b["exit_reason"], b["f"])
+        assert a["x"].tolist() == b["x"].tolist()
+    with pytest.raises(opmm.OpmmError):
+        opmm.opmm_estimate_batch(h, recs, ctls, options=opmm.nm_options(time_budget_ms=-1.0))

@@ -647,6 +647,60 @@ __device__ __forceinline__ void make_prop(const Setup& s, Prop2<T>& pr,
 }
 
 // ----------------------------------------------------------------------------
+// Superposition pair (fit_super_kernel): the b and u recurrences of one node
+// share every map (P, X, pf: they depend on the plant and the time constants
+// only) and differ in the forcing.  u is a unit pulse of one channel with no
+// other drive, so its post-pulse forcing is exactly zero and only its pulse
+// phase needs c, qf (and the two-step c2, qf2, c[0], the odd-start z1, f1).
+// Built once: the maps and b's forcing as make_prop builds them, u's pulse
+// forcing with the same one_step_phase / two_step_phase arithmetic -- so both
+// are bit-identical to two make_prop calls, at about half the work and
+// register peak (a second full Prop2 is never live).
+// ----------------------------------------------------------------------------
+struct UnitForcing {   // u's pulse-phase forcing terms (post-pulse: all zero)
+  double c2[4], qf2[2], c0;
+  double z1[4], f1[2];
+};
+
+__device__ __forceinline__ void make_prop_bu(const Setup& sb, const Phase& upulse,
+                                             Prop2<double>& pb, UnitForcing& pu) {
+  const Mech& m = sb.m;
+  double P[4][4];
+  one_step_P<double>(m, P);
+  double u[2][4][4];
+  coupling_u<double>(m, u);
+#pragma unroll
+  for (int phi = 0; phi < 2; ++phi) {
+    const int ph = 1 - phi;   // post-pulse first, as make_prop<STASH>
+    double X[4][2], c[4], pf[2], qf[2];
+    one_step_phase<double>(sb.ph[ph], u, X, c, pf, qf);
+    two_step_phase<double, double>(P, X, c, pf, qf, pb.ph[ph]);
+    if (ph == 0) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) pb.z1[r] = c[r];
+      pb.f1[0] = qf[0];
+      pb.f1[1] = qf[1];
+      // u: same zd (so the same X, pf), its own drive
+      double Xu[4][2], cu[4], pfu[2], qfu[2];
+      one_step_phase<double>(upulse, u, Xu, cu, pfu, qfu);
+      PhaseProp2<double> q;
+      two_step_phase<double, double>(P, Xu, cu, pfu, qfu, q);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        pu.c2[r] = q.c2[r];
+        pu.z1[r] = cu[r];
+      }
+      pu.qf2[0] = q.qf2[0];
+      pu.qf2[1] = q.qf2[1];
+      pu.c0 = q.c0;
+      pu.f1[0] = qfu[0];
+      pu.f1[1] = qfu[1];
+    }
+  }
+  square_P<double, double>(P, pb);
+}
+
+// ----------------------------------------------------------------------------
 // Integer substeps (reading Q25): the sample-to-sample map of a phase is the
 // one-substep map (h/s) to the power s, by binary exponentiation of the
 // affine map (z, f) -> (P z + X f + c, pf f + qf) -- the loop is unchanged
@@ -945,7 +999,7 @@ __device__ __forceinline__ T run_propagator(const Prop2<T>& pr, int32_t n_pulse,
 // sink.finish() at the end.  Returns sum |b_k| and sum |u_k|.
 // ----------------------------------------------------------------------------
 template <typename Sink>
-__device__ __forceinline__ void run_propagator_bu(const Prop2<double>& pb, const Prop2<double>& pu,
+__device__ __forceinline__ void run_propagator_bu(const Prop2<double>& pb, const UnitForcing& pu,
                                                   int32_t n_pulse, int32_t n_steps, Sink& sink,
                                                   double& Sb, double& Su) {
   const PhaseProp2<double>& q0 = pb.ph[0];
@@ -956,9 +1010,8 @@ __device__ __forceinline__ void run_propagator_bu(const Prop2<double>& pb, const
   // forcing of b and of u
   double c0 = q0.c2[0], c1 = q0.c2[1], c2 = q0.c2[2], c3 = q0.c2[3];
   double qa = q0.qf2[0], qn = q0.qf2[1], d0 = q0.c0;
-  const PhaseProp2<double>& r0 = pu.ph[0];
-  double e0 = r0.c2[0], e1 = r0.c2[1], e2 = r0.c2[2], e3 = r0.c2[3];
-  double ra = r0.qf2[0], rn = r0.qf2[1], g0 = r0.c0;
+  double e0 = pu.c2[0], e1 = pu.c2[1], e2 = pu.c2[2], e3 = pu.c2[3];
+  double ra = pu.qf2[0], rn = pu.qf2[1], g0 = pu.c0;
   const double Q00 = pb.P2[0][0], Q01 = pb.P2[0][1], Q02 = pb.P2[0][2], Q03 = pb.P2[0][3];
   const double Q10 = pb.P2[1][0], Q11 = pb.P2[1][1], Q12 = pb.P2[1][2], Q13 = pb.P2[1][3];
   const double Q20 = pb.P2[2][0], Q21 = pb.P2[2][1], Q22 = pb.P2[2][2], Q23 = pb.P2[2][3];
@@ -972,9 +1025,8 @@ __device__ __forceinline__ void run_propagator_bu(const Prop2<double>& pb, const
     x0a = q1.X0[0]; x0n = q1.X0[1];
     c0 = q1.c2[0]; c1 = q1.c2[1]; c2 = q1.c2[2]; c3 = q1.c2[3];
     qa = q1.qf2[0]; qn = q1.qf2[1]; d0 = q1.c0;
-    const PhaseProp2<double>& r1 = pu.ph[1];
-    e0 = r1.c2[0]; e1 = r1.c2[1]; e2 = r1.c2[2]; e3 = r1.c2[3];
-    ra = r1.qf2[0]; rn = r1.qf2[1]; g0 = r1.c0;
+    e0 = 0.0; e1 = 0.0; e2 = 0.0; e3 = 0.0;   // u: no post-pulse drive
+    ra = 0.0; rn = 0.0; g0 = 0.0;
   };
   const bool switches = n_pulse > 0 && n_pulse <= n_steps;
   const int32_t o = switches ? (n_pulse & 1) : 0;

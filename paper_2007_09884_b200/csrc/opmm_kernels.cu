@@ -790,7 +790,8 @@ __device__ __noinline__ void super_direct(const FitArgs& a, int64_t sac, int64_t
 // SUPER_MAX_WARPS warps: warps 0..T-1 keep their columns in their TMEM
 // quadrant, warps T.. in shared memory.
 template <int METRIC, bool TM, typename TC>
-__global__ void __launch_bounds__(TM ? SUPER_MAX_WARPS * 32 : 32) fit_super_kernel(FitArgs a) {
+__global__ void __launch_bounds__(TM ? SUPER_MAX_WARPS * 32 : 32)
+    fit_super_kernel(const __grid_constant__ FitArgs a) {
   static_assert(!TM || sizeof(TC) == 8, "the TMEM layout is fp64");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t s_tmem_base;
@@ -912,17 +913,16 @@ __global__ void __launch_bounds__(TM ? SUPER_MAX_WARPS * 32 : 32) fit_super_kern
     const double F = p[NC_FIX];
     double Sb, Su;
     {
-      Setup sb = s, su = s;
+      Setup sb = s;
       // b: N_SAC_d = 0 (n~ = 0 - F during the pulse)
       if (ag) sb.ph[0].nt_ag = -F; else sb.ph[0].nt_ant = -F;
-      // u: unit pulse on channel d, nothing else
-      su.ph[0].nt_ag = ag ? 1.0 : 0.0;
-      su.ph[0].nt_ant = ag ? 0.0 : 1.0;
-      su.ph[1].nt_ag = 0.0;
-      su.ph[1].nt_ant = 0.0;
-      Prop2<double> pb, pu;
-      make_prop<double, false>(sb, pb);
-      make_prop<double, false>(su, pu);
+      // u: unit pulse on channel d, nothing else (no post-pulse drive)
+      Phase up = s.ph[0];
+      up.nt_ag = ag ? 1.0 : 0.0;
+      up.nt_ant = ag ? 0.0 : 1.0;
+      Prop2<double> pb;
+      UnitForcing pu;
+      make_prop_bu(sb, up, pb, pu);
       if (TM && tm) {
         TmemSink sink{reinterpret_cast<double2*>(region) + lane, rel, taddr, a.ctl.n_steps, 0};
         run_propagator_bu(pb, pu, s.n_pulse, a.ctl.n_steps, sink, Sb, Su);

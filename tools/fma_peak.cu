@@ -16,6 +16,43 @@ __global__ void thr(T* out, int iters, T a, T b) {
   for (int c = 0; c < CH; ++c) s += x[c];
   if (s == (T)12345.678) out[0] = s;
 }
+// the fit loop's form: every operand a distinct register (coefficients held
+// in registers per chain, as fma(A, f, c) in run_propagator)
+template <typename T, int CH>
+__global__ void thr_reg(T* out, const T* coef, int iters) {
+  T x[CH], a[CH], b[CH];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    x[c] = (T)(threadIdx.x + c) * (T)1e-3;
+    a[c] = coef[c];
+    b[c] = coef[CH + c];
+  }
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < CH; ++c) x[c] = fma(x[c], a[c], b[c]);
+  }
+  T s = 0;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) s += x[c];
+  if (s == (T)12345.678) out[0] = s;
+}
+template <typename T, int CH>
+void run_thr_reg(const char* name, int blocks, int threads, int iters) {
+  T* d; cudaMalloc(&d, 64);
+  T hc[2 * CH];
+  for (int c = 0; c < 2 * CH; ++c) hc[c] = c < CH ? (T)(0.999999 - 1e-7 * c) : (T)(1e-7 * (c + 1));
+  T* dc; cudaMalloc(&dc, sizeof(hc)); cudaMemcpy(dc, hc, sizeof(hc), cudaMemcpyHostToDevice);
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  thr_reg<T, CH><<<blocks, threads>>>(d, dc, iters);
+  cudaEventRecord(e0);
+  for (int r = 0; r < 5; ++r) thr_reg<T, CH><<<blocks, threads>>>(d, dc, iters);
+  cudaEventRecord(e1); cudaEventSynchronize(e1);
+  float ms; cudaEventElapsedTime(&ms, e0, e1);
+  double fma = 5.0 * blocks * threads * (double)iters * CH;
+  printf("%s 3-reg blocks=%d threads=%d chains=%d: %.3f TFMA/s = %.2f TFLOP/s (%.3f ms)\n", name, blocks,
+         threads, CH, fma / (ms * 1e-3) / 1e12, 2 * fma / (ms * 1e-3) / 1e12, ms);
+  cudaFree(d); cudaFree(dc);
+}
 template <typename T>
 __global__ void lat(T* out, long long* cyc, int iters, T a, T b) {
   T x = (T)threadIdx.x;
@@ -60,5 +97,7 @@ int main() {
   run_thr<double, 4>("DFMA", sm * 4, 128, 20000);
   run_thr<double, 2>("DFMA", sm * 8, 128, 20000);
   for (int w : {4, 8, 16, 32}) run_thr<float, 8>("FFMA", sm * (w / 4), 128, 40000);
+  for (int w : {8, 16, 32}) run_thr_reg<float, 8>("FFMA", sm * (w / 4), 128, 40000);
+  for (int w : {8, 16, 32}) run_thr_reg<double, 8>("DFMA", sm * (w / 4), 128, 20000);
   return 0;
 }

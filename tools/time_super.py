@@ -33,8 +33,10 @@ with opmm.opmm_create(0) as h:
     for name, sp in grids:
         n = sp.n_grid()
         res = {}
-        for kv, prec in ((1, opmm.FP64), (4, opmm.FP64), (-1, opmm.FP32), (-4, opmm.FP32)):
-            o = opmm.fit_options(cpu_check=0, kernel_variant=abs(kv), precision=prec)
+        for kv, prec in ((1, opmm.FP64), (4, opmm.FP64), (5, opmm.FP64), (-1, opmm.FP32), (-4, opmm.FP32)):
+            # 5: the superposition kernel forced onto its shared-memory layout
+            o = opmm.fit_options(cpu_check=0, kernel_variant=min(abs(kv), 4), precision=prec,
+                                 flags=opmm.FIT_FLAG_SUPER_SMEM if kv == 5 else 0)
             for _ in range(2):
                 opmm.opmm_fit_async(h, rec, ctl, sp, n, out, o)
             ms = []
@@ -45,7 +47,7 @@ with opmm.opmm_create(0) as h:
             r = opmm.decode_result(bytes(out.cpu().numpy()))
             res[kv] = (float(np.median(ms)), r["best_index"], r["opt_err"], r["n_finite"])
         print(f"{name:26s} N={n:.3e}: direct {res[1][0]:8.3f} ms  super {res[4][0]:8.3f} ms  "
-              f"x{res[1][0] / res[4][0]:5.2f}  {n / res[4][0] * 1e3:.3e} cand/s  "
+              f"x{res[1][0] / res[4][0]:5.2f}  {n / res[4][0] * 1e3:.3e} cand/s  smem-layout {res[5][0]:7.3f} ms  "
               f"same best {res[1][1] == res[4][1]} ({res[4][1]}, {res[4][2]:.6g} vs {res[1][2]:.6g})"
               f"  nf {res[1][3]} {res[4][3]} | fp32: direct {res[-1][0]:7.3f} ms  super {res[-4][0]:7.3f} ms"
               f" x{res[-1][0] / res[-4][0]:5.2f} best {res[-4][1]}", flush=True)

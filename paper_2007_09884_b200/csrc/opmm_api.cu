@@ -156,6 +156,8 @@ struct opmm_handle {
   size_t tk_i_cap = 0;
   unsigned int* tk_counters = nullptr;      // top-K: topk_kernel tickets + fill counts [2][S]
   size_t tk_counters_cap = 0;
+  unsigned long long* sup_next = nullptr;   // superposition: node-group counters [S]
+  size_t sup_next_cap = 0;
   double* tk_err = nullptr;                 // top-K: the fit's errors when err_out is not given
   size_t tk_err_cap = 0;
   opmm_fit_result* result = nullptr;
@@ -670,6 +672,8 @@ opmm_status enqueue_fit_super(opmm_handle* h, const double* rec_dev, const opmm_
   a.sup_st = st;
   a.node_begin = nb;
   a.node_end = ne;
+  CKS(ensure(h->sup_next, h->sup_next_cap, (size_t)(s_begin + S), true));
+  a.sup_next = h->sup_next;
   if (prepare_only && !multi && S == 1) {
     prepare_only->fn = fn;
     prepare_only->grid = grid;
@@ -1166,6 +1170,7 @@ opmm_status opmm_destroy(opmm_handle* h) {
   cudaFree(h->tk_i);
   cudaFree(h->tk_counters);
   cudaFree(h->tk_err);
+  cudaFree(h->sup_next);
   for (int k = 0; k < 4; ++k) cudaFree(h->stage[k]);
   cudaFree(h->result);
   cudaFree(h->exp_tab);

@@ -108,6 +108,7 @@ struct FitArgs {
   int32_t pad2_;
   int64_t sup_st;           // its mixed-radix stride (product of the lower levels)
   int64_t node_begin, node_end;   // this rank's nodes
+  unsigned long long* sup_next;   // [S]: next 32-node group to take (zero at rest)
 };
 
 struct ExplicitArgs {

@@ -99,6 +99,7 @@ __device__ __forceinline__ void fit_epilogue(const FitArgs& a, int64_t sac, doub
   block_argmin(e, i, n);
   if (threadIdx.x == 0) {
     a.counters[sac] = 0;  // re-arm for the next launch (graph-replay safe)
+    if (a.sup_next) a.sup_next[sac] = 0;
     const int64_t neval = a.end - a.begin;
     if (a.rank_out) a.rank_out[sac].p = Partial{e, i, n, neval};
     if (a.final_out) {
@@ -871,7 +872,16 @@ __global__ void __launch_bounds__(TM ? SUPER_MAX_WARPS * 32 : 32)
     if (better(E, i, best_e, best_i)) { best_e = E; best_i = i; }
   };
   // uniform trip count per warp: lanes past the end redo the last node and drop it
-  for (int64_t t0 = (int64_t)blockIdx.x * B; t0 < nn; t0 += (int64_t)gridDim.x * B) {
+  // Warps take groups of 32 nodes from the saccade's global counter
+  // (a.sup_next, zero at rest; the finishing block re-arms it): TMEM and
+  // shared-memory warps run at different speeds, and a static split left the
+  // faster ones idle at the end.
+  for (;;) {
+    unsigned long long g = 0;
+    if (lane == 0) g = atomicAdd(a.sup_next + sac, 1ull);
+    const int64_t gs = (int64_t)__shfl_sync(0xffffffffu, g, 0) * 32;   // the group's first node
+    if (gs >= nn) break;
+    const int64_t t0 = gs - (tid - lane);   // so that t0 + tid = gs + lane
     const bool valid = t0 + tid < nn;
     const int64_t node = a.node_begin + (valid ? t0 + tid : nn - 1);
     const int64_t ib = node / st * stL + node % st;   // index of the node's level 0

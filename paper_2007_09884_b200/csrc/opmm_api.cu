@@ -1090,10 +1090,10 @@ opmm_status opmm_create(opmm_handle** out, int device) {
       }
   cudaGetLastError();
   {
-    // exp(j/64), j < EXP_TAB_N, as double-double from 80-bit expl
+    // exp(j/128), j < EXP_TAB_N, as double-double from 80-bit expl
     double2 tab[opmm::EXP_TAB_N];
     for (int j = 0; j < opmm::EXP_TAB_N; ++j) {
-      const long double v = expl((long double)j / 64.0L);
+      const long double v = expl((long double)j / 128.0L);
       tab[j].x = (double)v;
       tab[j].y = (double)(v - (long double)tab[j].x);
     }

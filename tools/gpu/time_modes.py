@@ -26,7 +26,8 @@ modes = [("fp64", dict(precision=0)), ("fp32", dict(precision=1)),
 if new_api:
     modes += [("fp64 top1", dict(precision=0, top_k=1)), ("fp64 top8", dict(precision=0, top_k=8)),
               ("fp64 top32", dict(precision=0, top_k=32)), ("fp32 certify K=32", dict(precision=1, certify=1, top_k=32)),
-              ("fp64 nosort", dict(precision=0, flags=1))]
+              ("fp64 nosort", dict(precision=0, flags=1)), ("fp64 block 192", dict(precision=0, block_size=192)),
+              ("fp64 block 128", dict(precision=0, block_size=128))]
 with opmm.opmm_create(0) as h:
     recd = torch.as_tensor(rec, device="cuda")
     out = torch.zeros(ctypes.sizeof(opmm.FitResult), dtype=torch.uint8, device="cuda")

@@ -609,7 +609,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-nm", action="store_true")
     ap.add_argument("--no-latency", action="store_true")
-    ap.add_argument("--nm-saccades", type=int, default=4096)
+    ap.add_argument("--nm-saccades", type=int, default=16384)
     ap.add_argument("--no-pop", action="store_true")
     ap.add_argument("--pop-saccades", type=int, default=10000)
     ap.add_argument("--pop-candidates", type=int, default=100000)

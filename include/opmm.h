@@ -363,6 +363,9 @@ typedef enum {
  *   GROUP: 4 lanes per problem evaluate the reflection, expansion and both
  *     contractions at once (shrink and initial points 4 at a time): one
  *     evaluation of latency per iteration at 8 problems per warp.
+ *     With more problems than one wave of resident blocks, the grid is one
+ *     wave and a group whose problem has finished takes the next one (refill),
+ *     so slots are not held idle until the slowest problem of their block ends.
  *   AUTO: GROUP from 1024 problems (per rank) on, LOCKSTEP below (measured on
  *     one B200: GROUP is the fastest from ~1000 problems on, LOCKSTEP below;
  *     LANE does the least work but has the longest latency per iteration). */

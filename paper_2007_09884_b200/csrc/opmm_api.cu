@@ -174,6 +174,8 @@ struct opmm_handle {
   size_t nm_xbest_cap = 0;
   opmm::NmOut* nm_out = nullptr;
   size_t nm_out_cap = 0;
+  unsigned long long* nm_next = nullptr;    // NM group schedule: refill counter
+  size_t nm_next_cap = 0;
 };
 
 namespace {
@@ -983,9 +985,24 @@ opmm_status nm_launch(opmm_handle* h, const NmConfig& c, const double* rec_dev,
   a.time_budget_ns = c.time_budget_ms > 0.0
                          ? (unsigned long long)std::fmax(1.0, std::fmin(c.time_budget_ms * 1e6, 9e18))
                          : 0ull;
-  const int64_t grid = n_blocks;
+  int64_t grid = n_blocks;
   if (grid == 0) return OPMM_OK;
   if (grid > 0x7fffffff) return fail(OPMM_ERR_INVALID_ARG, "too many problems");
+  if (group) {
+    // more problems than one wave of resident blocks: launch one wave and let
+    // finished groups take the next problem (nm_group_kernel's refill)
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel_for(rel_global), 32, smem));
+    const int64_t wave = (int64_t)h->num_sms * (per_sm > 0 ? per_sm : 1);
+    if (grid > wave) {
+      grid = wave;
+      CKS(ensure(h->nm_next, h->nm_next_cap, 1));
+      const unsigned long long first = (unsigned long long)(pb + grid * per);
+      CK(cudaMemcpyAsync(h->nm_next, &first, sizeof(first), cudaMemcpyHostToDevice, h->stream));
+      CK(cudaStreamSynchronize(h->stream));   // `first` lives on this stack frame
+      a.nm_next = h->nm_next;
+    }
+  }
   CKS(record_start(h, h->stream));
   if (lane || group)   // 32-thread blocks
     CK(opmm::launch_nm_lane(kernel_for(rel_global), a, (int)grid, smem, h->stream));
@@ -1177,6 +1194,7 @@ opmm_status opmm_destroy(opmm_handle* h) {
   cudaFree(h->nm_x0);
   cudaFree(h->nm_xbest);
   cudaFree(h->nm_out);
+  cudaFree(h->nm_next);
   if (h->result_host) cudaFreeHost(h->result_host);
   if (h->fit_graph) cudaGraphExecDestroy(h->fit_graph);
   if (h->rec_stage) cudaFreeHost(h->rec_stage);

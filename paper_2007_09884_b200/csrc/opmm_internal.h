@@ -151,6 +151,7 @@ struct NmArgs {
   int32_t dim, fn_id, max_iter, pad_;
   double tol_x, tol_f, init_scale;
   unsigned long long time_budget_ns;   // per-problem wall-clock limit (0 = none)
+  unsigned long long* nm_next;        // group schedule: next unassigned problem (refill; null = off)
   void* rel_global;         // long traces: device [S][n_steps+1] of the loop type; else null
 };
 

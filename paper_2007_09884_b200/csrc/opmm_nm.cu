@@ -734,24 +734,35 @@ __global__ void __launch_bounds__(32) nm_group_kernel(NmArgs a) {
 #define FS(slot) FSv[(slot) * NMQ_P + g]
 #define XB(j) XBv[(j) * NMQ_P + g]
 #define ORD(p) ORDv[(p) * NMQ_P + g]
-  const int64_t prob_raw = (int64_t)blockIdx.x * NMQ_P + g + a.prob_begin;
-  const bool live = prob_raw < a.prob_end;
-  const int64_t prob = live ? prob_raw : a.prob_end - 1;   // pad groups mirror the last problem
-  // group-uniform clock: the group's first lane reads it
-  const unsigned long long t0 = __shfl_sync(0xffffffffu, nm_now(), 4 * g);
+  // Problem refill (a.nm_next != nullptr): the grid is one wave of resident
+  // blocks, and a group whose problem is done takes the next unassigned one
+  // from the global counter, so problems that stop early no longer leave
+  // their slots idle until the whole wave ends.  Each problem's run is the
+  // same whichever slot runs it.
+  int64_t prob_raw = (int64_t)blockIdx.x * NMQ_P + g + a.prob_begin;
+  bool live = prob_raw < a.prob_end;
+  int64_t prob = live ? prob_raw : a.prob_end - 1;   // pad groups mirror the last problem
+  unsigned long long t0 = 0;
   const int n = OBJ == 3 ? a.dim : NP;
   double sgn = 1.0, Aprime = 0.0, pwd = 0.0;
-  if (OBJ != 3) {
-    const double amp = a.sac_ctl[2 * prob];
-    pwd = a.sac_ctl[2 * prob + 1];
-    const double* rec = a.rec + prob * (int64_t)ns;
-    const double r0 = rec[0];
-    const double A = isnan(amp) ? rec[ns - 1] - r0 : amp;
-    sgn = A < 0.0 ? -1.0 : 1.0;
-    Aprime = fabs(A);
-    for (int k = q; k < ns; k += NMQ_G) rel[(int64_t)k * NMQ_P] = (RT)(sgn * (rec[k] - r0));
-  }
-  const double* x0 = a.x0 + prob * (int64_t)a.x0_ld;
+  const double* x0 = nullptr;
+  // stage problem `prob`: its relativized trace in the group's slot, the
+  // start vector, and the group-uniform start of its clock
+  auto load_problem = [&]() {
+    t0 = __shfl_sync(gmask, nm_now(), 4 * g);
+    if (OBJ != 3) {
+      const double amp = a.sac_ctl[2 * prob];
+      pwd = a.sac_ctl[2 * prob + 1];
+      const double* rec = a.rec + prob * (int64_t)ns;
+      const double r0 = rec[0];
+      const double A = isnan(amp) ? rec[ns - 1] - r0 : amp;
+      sgn = A < 0.0 ? -1.0 : 1.0;
+      Aprime = fabs(A);
+      for (int k = q; k < ns; k += NMQ_G) rel[(int64_t)k * NMQ_P] = (RT)(sgn * (rec[k] - r0));
+    }
+    x0 = a.x0 + prob * (int64_t)a.x0_ld;
+  };
+  load_problem();
   const double rho = 1.0, chi = 2.0, psi = 0.5, sigma = 0.5;
   auto coefs = [&](int t, double& ca, double& cb) {   // t: 0 xr, 1 xe, 2 xc, 3 xcc
     if (t == 0) { ca = Ar(1.0, rho); cb = -rho; }
@@ -769,6 +780,41 @@ __global__ void __launch_bounds__(32) nm_group_kernel(NmArgs a) {
   int st = NMQ_INIT, k = 0, sn = 0, s0 = 0;
   int32_t it = 1, evals = n + 1, gpu_evals = 0, reason = 1;
   double f0 = 0.0, fn1 = 0.0, fnn = 0.0;
+  // the finished problem's result, written as soon as it is known
+  auto retire = [&]() {
+    __syncwarp(gmask);
+    const int sb = ORD(0);
+    for (int j = q; j < n; j += NMQ_G) a.x_best[prob * (int64_t)a.x_ld + j] = SV(sb, j);
+    if (q == 0) {
+      NmOut o;
+      o.f_best = FS(sb);
+      o.iterations = it;
+      o.func_evals = evals;
+      o.gpu_evals = gpu_evals;
+      o.exit_reason = reason;
+      a.out[prob] = o;
+    }
+    live = false;
+  };
+  // refill: the next unassigned problem, if any (group-uniform)
+  bool drained = a.nm_next == nullptr;
+  auto take_next = [&]() {
+    unsigned long long nx = 0;
+    if (q == 0) nx = atomicAdd(a.nm_next, 1ull);
+    nx = __shfl_sync(gmask, nx, 4 * g);
+    if ((int64_t)nx >= a.prob_end) { drained = true; return; }
+    prob = (int64_t)nx;
+    live = true;
+    __syncwarp(gmask);
+    load_problem();
+    __syncwarp(gmask);
+    st = NMQ_INIT;
+    k = 0;
+    it = 1;
+    evals = n + 1;
+    gpu_evals = 0;
+    reason = 1;
+  };
   auto sort_all = [&]() {   // lane q = 0; stable insertion sort of positions 0..n by f
     for (int p = 1; p <= n; ++p) {
       const int key = ORD(p);
@@ -836,7 +882,12 @@ __global__ void __launch_bounds__(32) nm_group_kernel(NmArgs a) {
     st = NMQ_DONE;
   }
   __syncwarp();
-  while (!__all_sync(0xffffffffu, st == NMQ_DONE)) {
+  for (;;) {
+    if (st == NMQ_DONE) {   // group-uniform
+      if (live) retire();
+      if (!drained) take_next();
+    }
+    if (__all_sync(0xffffffffu, st == NMQ_DONE)) break;
     double f;
     {
       // this lane's point: vertex / transformation / shrink point / best vertex
@@ -968,20 +1019,6 @@ __global__ void __launch_bounds__(32) nm_group_kernel(NmArgs a) {
     }
     ++it;
     begin_iteration();
-  }
-  __syncwarp();
-  if (live) {
-    const int sb = ORD(0);
-    for (int j = q; j < n; j += NMQ_G) a.x_best[prob * (int64_t)a.x_ld + j] = SV(sb, j);
-    if (q == 0) {
-      NmOut o;
-      o.f_best = FS(sb);
-      o.iterations = it;
-      o.func_evals = evals;
-      o.gpu_evals = gpu_evals;
-      o.exit_reason = reason;
-      a.out[prob] = o;
-    }
   }
 #undef SV
 #undef FS

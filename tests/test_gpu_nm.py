@@ -213,3 +213,20 @@ def test_time_budget_exit(opmm, h, schedule):
         assert a["x"].tolist() == b["x"].tolist()
     with pytest.raises(opmm.OpmmError):
         opmm.opmm_estimate_batch(h, recs, ctls, options=opmm.nm_options(time_budget_ms=-1.0))
+
+
+def test_group_schedule_refill_bit_identical(opmm, h):
+    """More problems than one wave of group-schedule blocks: the grid is one
+    wave and finished groups take the next problem.  Every run must still be
+    the oracle's serial run, bit for bit (Rosenbrock, dim 4, seeded starts)."""
+    S = 24000
+    rng = np.random.default_rng(17)
+    x0 = rng.uniform(-2.0, 2.0, size=(S, 4))
+    res = opmm.opmm_nm_minimize_test(h, opmm.NM_ROSENBROCK, x0,
+                                     opmm.nm_options(schedule=3, max_iter=300))
+    for s in range(S):
+        o = oracle.nm_test(oracle.NM_ROSENBROCK, x0[s], max_iter=300)
+        r = res[s]
+        assert (r["iterations"], r["func_evals"], r["exit_reason"]) == \
+               (o["iterations"], o["func_evals"], o["exit_reason"]), s
+        assert r["x"].tolist() == o["x"].tolist() and r["f"] == o["f"], s

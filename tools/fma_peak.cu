@@ -53,6 +53,44 @@ void run_thr_reg(const char* name, int blocks, int threads, int iters) {
          threads, CH, fma / (ms * 1e-3) / 1e12, 2 * fma / (ms * 1e-3) / 1e12, ms);
   cudaFree(d); cudaFree(dc);
 }
+// FFMA2 (sm_100: two fp32 FMAs per instruction), the fit loop's packed form:
+// x2 = fma2(A2, (s, s), x2) with the multiplier broadcast from one register
+template <int CH>
+__global__ void thr_ffma2(float2* out, const float* coef, int iters) {
+  float2 x[CH], a[CH];
+  float s[CH];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    x[c] = make_float2((threadIdx.x + c) * 1e-3f, (threadIdx.x + c) * 2e-3f);
+    a[c] = make_float2(coef[c], coef[CH + c]);
+    s[c] = coef[2 * CH + c];
+  }
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < CH; ++c) x[c] = __ffma2_rn(a[c], make_float2(s[c], s[c]), x[c]);
+  }
+  float t = 0.f;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) t += x[c].x + x[c].y;
+  if (t == 12345.678f) out[0] = x[0];
+}
+template <int CH>
+void run_ffma2(int blocks, int threads, int iters) {
+  float2* d; cudaMalloc(&d, 64);
+  float hc[3 * CH];
+  for (int c = 0; c < 3 * CH; ++c) hc[c] = c < 2 * CH ? 0.999999f - 1e-7f * c : 1e-7f * (c + 1);
+  float* dc; cudaMalloc(&dc, sizeof(hc)); cudaMemcpy(dc, hc, sizeof(hc), cudaMemcpyHostToDevice);
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  thr_ffma2<CH><<<blocks, threads>>>(d, dc, iters);
+  cudaEventRecord(e0);
+  for (int r = 0; r < 5; ++r) thr_ffma2<CH><<<blocks, threads>>>(d, dc, iters);
+  cudaEventRecord(e1); cudaEventSynchronize(e1);
+  float ms; cudaEventElapsedTime(&ms, e0, e1);
+  double fma = 5.0 * blocks * threads * (double)iters * CH * 2;
+  printf("FFMA2 (broadcast, 3-reg) blocks=%d threads=%d chains=%d: %.3f TFMA/s = %.2f TFLOP/s (%.3f ms)\n",
+         blocks, threads, CH, fma / (ms * 1e-3) / 1e12, 2 * fma / (ms * 1e-3) / 1e12, ms);
+  cudaFree(d); cudaFree(dc);
+}
 template <typename T>
 __global__ void lat(T* out, long long* cyc, int iters, T a, T b) {
   T x = (T)threadIdx.x;
@@ -99,5 +137,6 @@ int main() {
   for (int w : {4, 8, 16, 32}) run_thr<float, 8>("FFMA", sm * (w / 4), 128, 40000);
   for (int w : {8, 16, 32}) run_thr_reg<float, 8>("FFMA", sm * (w / 4), 128, 40000);
   for (int w : {8, 16, 32}) run_thr_reg<double, 8>("DFMA", sm * (w / 4), 128, 20000);
+  for (int w : {8, 16, 32}) run_ffma2<8>(sm * (w / 4), 128, 40000);
   return 0;
 }

@@ -156,7 +156,12 @@ typedef struct {
                               section 7b), so where two candidates' errors tie
                               to within that rounding the returned index may
                               differ from variant 1's; exact ties still go to
-                              the lowest index.                                 */
+                              the lowest index.
+                              5 = lane refill: a lane whose error
+                              has passed CAP (reading Q10: +inf) stops; once 16
+                              lanes of a warp are free they take new candidates.
+                              Same needs as 2/3, no certify / top_k.  Errors bit-identical to 1;
+                              measured slower.          */
   int32_t certify;      /* FP32 only ("solutions are sorted for accuracy",
                            PAPER.md:251): keep the exact top-K by fp32 error
                            (K = top_k, or 8 when top_k = 0), re-score those K in

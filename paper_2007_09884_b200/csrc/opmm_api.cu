@@ -701,7 +701,7 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
   if (!check_precision(precision)) return fail(OPMM_ERR_INVALID_ARG, "bad precision %d", precision);
   if (metric != 0 && metric != 1) return fail(OPMM_ERR_INVALID_ARG, "bad metric %d", metric);
   if (integ != 0 && integ != 1) return fail(OPMM_ERR_INVALID_ARG, "bad integrator %d", integ);
-  if (kv_opt < 0 || kv_opt > 4) return fail(OPMM_ERR_INVALID_ARG, "kernel_variant must be 0..4");
+  if (kv_opt < 0 || kv_opt > 5) return fail(OPMM_ERR_INVALID_ARG, "kernel_variant must be 0..5");
   if (top_k < 0 || top_k > OPMM_MAX_TOPK)
     return fail(OPMM_ERR_INVALID_ARG, "top_k must be in [0, %d] (got %d)", OPMM_MAX_TOPK, top_k);
   // FP32 certification: the exact top-K by fp32 error (K = top_k, or 32),
@@ -732,7 +732,7 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
   if (superpose)
     return enqueue_fit_super(h, rec_dev, ctl, sacctl_dev, s_begin, S, space, space_dev, sup_dim,
                              n_candidates, opts, out_dev, shard, prepare_only);
-  // variants 2/3 need the propagator integrator and a search space whose
+  // variants 2/3/5 need the propagator integrator and a search space whose
   // candidates are all physical (no per-candidate penalty path)
   const bool special_ok = integ == OPMM_INTEG_PROPAGATOR && space_dev.all_physical &&
                           !(opts && opts->block_size) && ctl->substeps <= 1;
@@ -741,8 +741,8 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
                                       "physical search space, the default block size and no "
                                       "substeps", kv_opt);
   const int kv = kv_opt == 0 ? (special_ok ? kAutoVariant : 1) : kv_opt;
-  const bool two = kv == 2, three = kv == 3;
-  if ((two || three) && K > 0)
+  const bool two = kv == 2, three = kv == 3, refill = kv == 5;
+  if ((two || three || refill) && K > 0)
     return fail(OPMM_ERR_UNSUPPORTED, "top_k / certify need kernel_variant 0 or 1");
   const int block = three ? opmm::FIT3_BLOCK : two ? opmm::FIT2_BLOCK
                         : ((opts && opts->block_size) ? opts->block_size : kDefaultBlock);
@@ -753,9 +753,10 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
   size_t smem = three ? opmm::fit3_smem(precision, ns) : fit_smem(precision, ns, block, two ? 2 : 1);
   if (smem > kMaxDynSmem) return fail(OPMM_ERR_INVALID_ARG, "trace too long for shared memory");
   const void* fn = three ? opmm::fit3_kernel_ptr(precision, metric)
-                         : two ? opmm::fit2_kernel_ptr(precision, metric)
-                               : opmm::fit_kernel_ptr(precision, kernel_integ(integ, ctl), metric);
-  const bool one = !two && !three;
+                   : two ? opmm::fit2_kernel_ptr(precision, metric)
+                   : refill ? opmm::fit_refill_kernel_ptr(precision, metric)
+                            : opmm::fit_kernel_ptr(precision, kernel_integ(integ, ctl), metric);
+  const bool one = !two && !three && !refill;
   // fit_kernel dynamic shared memory: rel, exp table, stash (opmm_kernels.cu),
   // then the super-tile permutation and the pre-pass key/rank scratch
   // (aliased onto the stash when it fits there)
@@ -1084,6 +1085,7 @@ opmm_status opmm_create(opmm_handle** out, int device) {
         allow_dyn_smem(opmm::simscore_kernel_ptr(p, i, m));
         allow_dyn_smem(opmm::fit2_kernel_ptr(p, m));
         allow_dyn_smem(opmm::fit3_kernel_ptr(p, m));
+        allow_dyn_smem(opmm::fit_refill_kernel_ptr(p, m));
         if (p == 0 && i == 0) {
           allow_dyn_smem(opmm::fit_super_kernel_ptr(m, false, false));
           allow_dyn_smem(opmm::fit_super_kernel_ptr(m, false, true));

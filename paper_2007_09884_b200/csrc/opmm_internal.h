@@ -180,6 +180,7 @@ size_t super_smem(int32_t n_samples, int32_t levels, int32_t gt_n, int smem_warp
 constexpr int32_t SUPER_MAX_GT = 2048;   // level-table entries kept in shared memory
 const void* fit2_kernel_ptr(int precision, int metric);   // 2 candidates/thread, 256 threads
 constexpr int FIT2_BLOCK = 256;
+const void* fit_refill_kernel_ptr(int precision, int metric);   // lane refill (f2), default block
 const void* fit3_kernel_ptr(int precision, int metric);   // warp-specialised, 384 threads
 constexpr int FIT3_BLOCK = 384;
 size_t fit3_smem(int precision, int32_t n_samples);

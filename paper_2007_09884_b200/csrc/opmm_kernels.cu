@@ -1103,6 +1103,191 @@ __global__ void __launch_bounds__(FIT2_THREADS, 1) fit2_kernel(FitArgs a) {
   fit_epilogue(a, sac, best_e, best_i, nf);
 }
 
+// ---------------------------------------------------------------------------
+// Lane refill (kernel_variant 5).  A candidate
+// whose accumulated error reaches CAP ends at +inf (reading Q10; the sum only
+// grows), so its remaining steps are wasted work -- 53% of S_paper candidates
+// do this, half of them by step 20.  Here a lane stops at the first check
+// (every REFILL_SEG two-step blocks) after its accumulator passes CAP, and
+// once REFILL_MIN lanes of the warp are free they take the block's next
+// candidates (shared counter over the block's static range), generate and
+// set them up -- only those lanes, divergent -- and the warp continues with
+// every lane at its own step, phase and trace offset.  Each candidate's
+// arithmetic is run_propagator's, block for block (same FMA order), so every
+// finite error is bit-identical to variant 1's; an early-stopped one is +inf
+// exactly as variant 1's finish_error makes it.  Needs a physical space (no
+// penalty path).  Measured slower than variant 1: setup is
+// warp-wide work however few lanes need it.
+// ---------------------------------------------------------------------------
+constexpr int32_t REFILL_SEG = 8;   // two-step blocks between divergence checks
+constexpr int REFILL_MIN = 16;      // free lanes that trigger a refill
+
+template <typename T, int METRIC>
+__global__ void __launch_bounds__(OPMM_FIT_LB_THREADS, OPMM_FIT_LB_BLOCKS) fit_refill_kernel(FitArgs a) {
+  using V2 = typename Vec2<T>::type;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int32_t n = a.ctl.n_steps, ns = n + 1;
+  T* rel = reinterpret_cast<T*>(smem_raw);
+  double2* tab = reinterpret_cast<double2*>(smem_raw + rel_bytes<T>(ns));
+  T* stash = reinterpret_cast<T*>(smem_raw + rel_bytes<T>(ns) + exp_tab_bytes());  // [10][block] vec2
+  for (int j = threadIdx.x; j < EXP_TAB_N; j += blockDim.x) tab[j] = a.exp_tab[j];
+  const int64_t sac = (int64_t)blockIdx.y + a.sac_begin;
+  const double amp = a.sac_ctl ? a.sac_ctl[2 * sac] : a.amplitude;
+  const double pwd = a.sac_ctl ? a.sac_ctl[2 * sac + 1] : a.pw_default;
+  double sgn, Aprime;
+  __shared__ unsigned long long s_next;
+  if (threadIdx.x == 0) s_next = 0;
+  stage_trace<T>(a.rec + sac * (int64_t)ns, ns, amp, rel, sgn, Aprime);
+  __syncthreads();
+  // the block's static share of the range
+  const int64_t span = a.end - a.begin;
+  const int64_t per = (span + gridDim.x - 1) / gridDim.x;
+  const int64_t lo = a.begin + min(span, per * (int64_t)blockIdx.x);
+  const int64_t hi = a.begin + min(span, per * (int64_t)(blockIdx.x + 1));
+  const int lane = threadIdx.x & 31;
+  const unsigned FULL = 0xffffffffu;
+  V2* st2 = reinterpret_cast<V2*>(stash) + threadIdx.x;
+  const int ld = (int)blockDim.x;
+  const int32_t nb = (n + 1) / 2;
+  double best_e = dinf();
+  int64_t best_i = INT64_MAX;
+  int64_t nf = 0;
+  T Q00 = 0, Q01 = 0, Q02 = 0, Q03 = 0, Q10 = 0, Q11 = 0, Q12 = 0, Q13 = 0;
+  T Q20 = 0, Q21 = 0, Q22 = 0, Q23 = 0, Q30 = 0, Q31 = 0, Q32 = 0, Q33 = 0;
+  T R0 = 0, R1 = 0, R2 = 0, R3 = 0;
+  T A00 = 0, A01 = 0, A10 = 0, A11 = 0, A20 = 0, A21 = 0, A30 = 0, A31 = 0;
+  T c0 = 0, c1 = 0, c2 = 0, c3 = 0, pa = 0, pn = 0, qa = 0, qn = 0, x0a = 0, x0n = 0, d0 = 0;
+  T th = 0, om = 0, xa = 0, xn = 0, fa = 0, fn = 0, acc = 0;
+  int32_t b = 0, bs = 0, o = 0;
+  int64_t ci = 0;
+  bool act = false, more = lo < hi;
+  auto swap_in = [&]() {
+    V2 v;
+    v = st2[0 * ld]; A00 = v.x; A01 = v.y;
+    v = st2[1 * ld]; A10 = v.x; A11 = v.y;
+    v = st2[2 * ld]; A20 = v.x; A21 = v.y;
+    v = st2[3 * ld]; A30 = v.x; A31 = v.y;
+    v = st2[4 * ld]; c0 = v.x; c1 = v.y;
+    v = st2[5 * ld]; c2 = v.x; c3 = v.y;
+    v = st2[6 * ld]; pa = v.x; pn = v.y;
+    v = st2[7 * ld]; qa = v.x; qn = v.y;
+    v = st2[8 * ld]; x0a = v.x; x0n = v.y;
+    v = st2[9 * ld]; d0 = v.x;
+  };
+  auto retire = [&](double E) {
+    if (a.err_out) a.err_out[sac * a.err_ld + ci - a.err_base] = E;
+    nf += E < dinf() ? 1 : 0;
+    if (better(E, ci, best_e, best_i)) { best_e = E; best_i = ci; }
+    act = false;
+    b = 0;   // a free lane keeps running the block body on in-range samples
+    o = 0;
+    bs = -1;
+  };
+  for (;;) {
+    const unsigned need = __ballot_sync(FULL, !act);
+    if (more && (need == FULL || __popc(need) >= REFILL_MIN)) {
+      const int k = __popc(need);
+      unsigned long long base = 0;
+      if (lane == 0) base = atomicAdd(&s_next, (unsigned long long)k);
+      base = __shfl_sync(FULL, base, 0);
+      if ((int64_t)base + k >= hi - lo) more = false;
+      const int64_t j = lo + (int64_t)base + __popc(need & ((1u << lane) - 1u));
+      if (!act && j < hi) {
+        act = true;
+        ci = j;
+        double p[NP];
+        generate_opc(a.space, (uint32_t)sac, ci, p, tab);
+        Setup su;
+        make_setup(p, a.ctl.dt_ms, a.ctl.h, n, Aprime, pwd, su);
+        Prop2<T> pr;
+        make_prop<T, true>(su, pr, st2, ld);   // phase 1 -> the lane's stash
+        const PhaseProp2<T>& q0 = pr.ph[0];
+        A00 = q0.X2[0][0]; A01 = q0.X2[0][1]; A10 = q0.X2[1][0]; A11 = q0.X2[1][1];
+        A20 = q0.X2[2][0]; A21 = q0.X2[2][1]; A30 = q0.X2[3][0]; A31 = q0.X2[3][1];
+        c0 = q0.c2[0]; c1 = q0.c2[1]; c2 = q0.c2[2]; c3 = q0.c2[3];
+        pa = q0.pf2[0]; pn = q0.pf2[1]; qa = q0.qf2[0]; qn = q0.qf2[1];
+        x0a = q0.X0[0]; x0n = q0.X0[1]; d0 = q0.c0;
+        Q00 = pr.P2[0][0]; Q01 = pr.P2[0][1]; Q02 = pr.P2[0][2]; Q03 = pr.P2[0][3];
+        Q10 = pr.P2[1][0]; Q11 = pr.P2[1][1]; Q12 = pr.P2[1][2]; Q13 = pr.P2[1][3];
+        Q20 = pr.P2[2][0]; Q21 = pr.P2[2][1]; Q22 = pr.P2[2][2]; Q23 = pr.P2[2][3];
+        Q30 = pr.P2[3][0]; Q31 = pr.P2[3][1]; Q32 = pr.P2[3][2]; Q33 = pr.P2[3][3];
+        R0 = pr.P0[0]; R1 = pr.P0[1]; R2 = pr.P0[2]; R3 = pr.P0[3];
+        // run_propagator's start: lane parity, switch block, odd first step
+        const int32_t np = su.n_pulse;
+        const bool sw = np > 0 && np <= n;
+        o = sw ? (np & 1) : 0;
+        bs = sw ? (np - o) / 2 : nb;
+        b = 0;
+        th = T(0); om = T(0); xa = T(0); xn = T(0); fa = T(0); fn = T(0);
+        acc = T(0);
+        if (np == 0) swap_in();
+        if (o) {
+          th = pr.z1[0]; om = pr.z1[1]; xa = pr.z1[2]; xn = pr.z1[3];
+          fa = pr.f1[0]; fn = pr.f1[1];
+          accumulate<METRIC>(acc, th - rel[1]);
+        }
+        if (!sw) bs = -1;   // sw && bs == 0: swapped before the first block, in the loop
+      }
+    }
+    // a lane at its last block (steps o + 2b + 1, + 2, either may lie past n)
+    if (act && b >= nb - 1) {
+      if (b == bs) swap_in();
+      if (nb >= 1) {
+        const int32_t k1 = o + 2 * b + 1;
+        const T t1 = fma(R0, th, fma(R1, om, fma(R2, xa, fma(R3, xn, fma(x0a, fa, fma(x0n, fn, d0))))));
+        const T t2 = fma(Q00, th, fma(Q01, om, fma(Q02, xa, fma(Q03, xn, fma(A00, fa, fma(A01, fn, c0))))));
+        if (k1 <= n) accumulate<METRIC>(acc, t1 - rel[k1]);
+        if (k1 + 1 <= n) accumulate<METRIC>(acc, t2 - rel[k1 + 1]);
+      }
+      retire(finish_error<METRIC>(acc, ns));
+    }
+    if (!__any_sync(FULL, act)) {
+      if (!more) break;
+      continue;
+    }
+    // uniform segment: up to every active lane's next divergence check or its
+    // last block.  Lanes sit at different steps, so each switches phase inside
+    // the segment (before its block bs, as run_propagator does between
+    // segments) instead of splitting it.
+    const int32_t ev = act ? min(nb - 1, b + REFILL_SEG) - b : INT32_MAX;
+    const int32_t len = __reduce_min_sync(FULL, ev);
+    const T* __restrict__ rl = rel + o;
+    const int32_t inc = act ? 1 : 0;
+    for (int32_t t = 0; t < len; ++t) {
+      if (b == bs) swap_in();
+      T t1 = fma(x0n, fn, d0), nth = fma(A01, fn, c0), nom = fma(A11, fn, c1);
+      T nxa = fma(A21, fn, c2), nxn = fma(A31, fn, c3);
+      t1 = fma(x0a, fa, t1); nth = fma(A00, fa, nth); nom = fma(A10, fa, nom);
+      nxa = fma(A20, fa, nxa); nxn = fma(A30, fa, nxn);
+      fa = fma(pa, fa, qa);
+      fn = fma(pn, fn, qn);
+      t1 = fma(R3, xn, t1); nth = fma(Q03, xn, nth); nom = fma(Q13, xn, nom);
+      nxa = fma(Q23, xn, nxa); nxn = fma(Q33, xn, nxn);
+      t1 = fma(R2, xa, t1); nth = fma(Q02, xa, nth); nom = fma(Q12, xa, nom);
+      nxa = fma(Q22, xa, nxa); nxn = fma(Q32, xa, nxn);
+      t1 = fma(R1, om, t1); nth = fma(Q01, om, nth); nom = fma(Q11, om, nom);
+      nxa = fma(Q21, om, nxa); nxn = fma(Q31, om, nxn);
+      t1 = fma(R0, th, t1); nth = fma(Q00, th, nth); nom = fma(Q10, th, nom);
+      nxa = fma(Q20, th, nxa); nxn = fma(Q30, th, nxn);
+      th = nth; om = nom; xa = nxa; xn = nxn;
+      accumulate<METRIC>(acc, t1 - rl[2 * b + 1]);
+      accumulate<METRIC>(acc, th - rl[2 * b + 2]);
+      b += inc;
+    }
+    // stopped early: the accumulator only grows, so the error is +inf (Q10)
+    if (act && b < nb - 1 && !((double)acc < CAP)) retire(dinf());
+  }
+  fit_epilogue(a, sac, best_e, best_i, nf);
+}
+
+template <typename T, int METRIC>
+static const void* refill_fn() { return reinterpret_cast<const void*>(&fit_refill_kernel<T, METRIC>); }
+
+const void* fit_refill_kernel_ptr(int precision, int metric) {
+  if (precision == 0) return metric == 0 ? refill_fn<double, 0>() : refill_fn<double, 1>();
+  return metric == 0 ? refill_fn<float, 0>() : refill_fn<float, 1>();
+}
+
 template <typename T, int METRIC>
 static const void* fit2_fn() { return reinterpret_cast<const void*>(&fit2_kernel<T, METRIC>); }
 

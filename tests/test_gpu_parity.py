@@ -499,11 +499,12 @@ def test_fit_launch_config_invariance(opmm, h):
 
 
 @pytest.mark.parametrize("precision", [0, 1])
-@pytest.mark.parametrize("variant", [2, 3])
+@pytest.mark.parametrize("variant", [2, 3, 5])
 def test_fit_kernel_variants_identical(opmm, h, precision, variant):
-    """fit2 (two interleaved candidates per thread) and fit3 (warp-specialised
-    producer/consumer) give bit-identical per-candidate errors and argmin to
-    the default one-candidate-per-thread kernel (ragged N, several rounds)."""
+    """fit2 (two interleaved candidates per thread), fit3 (warp-specialised
+    producer/consumer) and lane refill (5: diverged lanes stop at CAP and take
+    new candidates) give bit-identical per-candidate errors and argmin to the
+    default one-candidate-per-thread kernel (ragged N, several rounds)."""
     ctl = W.Control()
     rec = trace(ctl)
     sp = W.paper_space()
@@ -514,6 +515,50 @@ def test_fit_kernel_variants_identical(opmm, h, precision, variant):
     assert np.array_equal(E1, E2)
     with pytest.raises(opmm.OpmmError) as ei:   # variants 2/3 need the propagator
         _fit(opmm, h, rec, ctl, sp, 10, kernel_variant=variant, integrator=opmm.INTEG_RK4_STAGES)
+    assert ei.value.status == opmm.ERR_UNSUPPORTED
+
+
+@pytest.mark.parametrize("metric", [0, 1])
+def test_fit_refill_edges(opmm, h, metric):
+    """Lane refill (kernel_variant 5): bit-identical to variant 1
+    on short and odd traces (n = 1, 2, 3, 7: last-block and odd-start paths),
+    pulses of one step and pulses ending past the trace, ragged and tiny counts, forced
+    one-block grids (every lane refilled many times) and the population batch;
+    and element-wise against the oracle on the bench trace."""
+    for n_steps in (1, 2, 3, 7, 100):
+        ctl = W.Control(n_steps=n_steps)
+        rec = trace(ctl)
+        sp = W.paper_space(n_steps=n_steps)
+        sp.lo[17], sp.hi[17] = 0.01, 2.0 * n_steps + 3.0   # PW from one step to past the trace
+        for n, gb in ((1, 0), (31, 0), (33, 1), (5000, 0), (20011, 1), (20011, 3)):
+            r1, E1 = _fit(opmm, h, rec, ctl, sp, n, metric=metric, kernel_variant=1, grid_blocks=gb)
+            r5, E5 = _fit(opmm, h, rec, ctl, sp, n, metric=metric, kernel_variant=5, grid_blocks=gb)
+            assert (r1["best_index"], r1["opt_err"], r1["n_finite"]) == \
+                   (r5["best_index"], r5["opt_err"], r5["n_finite"]), (n_steps, n, gb)
+            assert np.array_equal(E1, E5), (n_steps, n, gb)
+    ctl = W.Control()
+    rec = trace(ctl)
+    sp = W.paper_space()
+    r5, E5 = _fit(opmm, h, rec, ctl, sp, 3000, metric=metric, kernel_variant=5)
+    o = oracle.fit(rec, ctl, sp, 0, 3000, metric=metric, want_err=True)
+    rel, _, _ = oracle.relativize(rec, ctl.amplitude_deg)
+    scale = np.abs(rel).sum() if metric == 0 else np.sqrt(np.mean(rel ** 2))
+    assert_fp64_errors(E5, o["err"], lambda i: oracle.generate(sp, i), rec, ctl, scale, metric)
+    assert r5["best_index"] == o["best_index"]
+    assert np.isinf(E5).sum() > 1000   # the S_paper mix: many lanes stop early
+    # population: gridDim.y = saccades, one block-sized slice per block
+    S = 6
+    amp, pw, truths = W.population(S)
+    ctls = [W.Control(n_steps=150, amplitude_deg=amp[k], pw_default_ms=pw[k]) for k in range(S)]
+    recs = np.array([oracle.positions(truths[k], ctls[k]) + W.noise(151, seed=7 + k) for k in range(S)])
+    spp = W.paper_space(n_steps=150)
+    b1 = opmm.opmm_fit_batch(h, recs, ctls, spp, 4001, opmm.fit_options(metric=metric, kernel_variant=1))
+    b5 = opmm.opmm_fit_batch(h, recs, ctls, spp, 4001, opmm.fit_options(metric=metric, kernel_variant=5))
+    for k in range(S):
+        assert (b1[k]["best_index"], b1[k]["opt_err"], b1[k]["n_finite"]) == \
+               (b5[k]["best_index"], b5[k]["opt_err"], b5[k]["n_finite"]), k
+    with pytest.raises(opmm.OpmmError) as ei:
+        _fit(opmm, h, rec, ctl, sp, 100, kernel_variant=5, top_k=4)
     assert ei.value.status == opmm.ERR_UNSUPPORTED
 
 

@@ -332,7 +332,9 @@ opmm_status opmm_fit_async(opmm_handle* h, const double* recorded_dev, const opm
  * dt for all, from ctl[0]); ctl: HOST [S] (per-saccade amplitude /
  * pw_default); out: HOST [S].  On an NCCL handle rank r fits only saccades
  * [floor(rS/R), floor((r+1)S/R)) and fills only those entries of out: the
- * saccades are independent problems, so there is no collective. */
+ * saccades are independent problems, so there is no collective.
+ * opts->err_out (optional): DEVICE [S][n_per], row s = saccade s's errors
+ * (on an NCCL handle only this rank's rows are written). */
 opmm_status opmm_fit_batch(opmm_handle* h, const double* recorded, int64_t S,
                            const opmm_control* ctl, const opmm_search_space* space,
                            int64_t n_per, const opmm_fit_options* opts, opmm_fit_result* out);

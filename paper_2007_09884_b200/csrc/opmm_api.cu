@@ -1605,8 +1605,6 @@ opmm_status opmm_fit_batch(opmm_handle* h, const double* recorded, int64_t S,
       return fail(OPMM_ERR_INVALID_ARG, "all saccades of a batch share dt_ms, n_steps and substeps");
   }
   CKS(validate_space(space, n_per));
-  if (opts && opts->err_out)
-    return fail(OPMM_ERR_UNSUPPORTED, "err_out is not supported by opmm_fit_batch");
   // saccades are independent problems: rank r takes its contiguous share
   int64_t sb = 0, se = S;
   opmm_shard_range(S, h->rank, h->world, &sb, &se);

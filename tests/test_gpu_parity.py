@@ -647,9 +647,14 @@ def test_fit_batch_population(opmm, h):
     recs = np.array(recs)
     sp = W.paper_space(n_steps=n_steps)
     n_per = 3000
-    res = opmm.opmm_fit_batch(h, recs, ctls, sp, n_per)
+    err = torch.full((S, n_per), -1.0, dtype=torch.float64, device="cuda")
+    res = opmm.opmm_fit_batch(h, recs, ctls, sp, n_per, opmm.fit_options(err_out=err))
+    E = err.cpu().numpy()
     for s in (0, 1, 17, 47):
-        o = oracle.fit(recs[s], ctls[s], sp, 0, n_per, saccade=s)
+        o = oracle.fit(recs[s], ctls[s], sp, 0, n_per, saccade=s, want_err=True)
+        rel, _, _ = oracle.relativize(recs[s], ctls[s].amplitude_deg)
+        assert_fp64_errors(E[s], o["err"], lambda i, s=s: oracle.generate(sp, i, saccade=s), recs[s], ctls[s],
+                           np.abs(rel).sum())
         assert res[s]["best_index"] == o["best_index"], s
         assert abs(res[s]["opt_err"] - o["best_err"]) <= 1e-9 * max(o["best_err"], 1.0)
         assert abs(res[s]["cpu_check"] - res[s]["opt_err"]) <= 1e-9 * res[s]["opt_err"]

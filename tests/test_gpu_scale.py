@@ -177,3 +177,48 @@ def test_fit_random_5e9_indices_beyond_2_32(opmm, h):
     O = np.array([oracle.objective(oracle.generate(sp, int(i)), rec, ctl) for i in idx])
     assert np.all(O[np.isfinite(O)] > r["opt_err"] * (1 - 1e-9))
     print(f"\n5e9: best {r['best_index']} E {r['opt_err']:.9f}, n_finite {r['n_finite']}")
+
+
+def test_population_bench_scale(opmm, h):
+    """configs[4] at the bench's population size: 10^4 saccades x 10^5 S_paper
+    candidates, n = 150, through opmm_fit_batch (Philox counter word 2 =
+    saccade).  Traces are the bench recipe (workloads.population, simulated
+    here by the oracle, + N(0, 0.02 deg)).  Every saccade's reduction is
+    checked on the device against its full error row (min, lowest index of
+    the min, n_finite); every winner is re-scored by the oracle; 8 sampled
+    saccades get a full oracle sweep (all 10^5 errors, argmin, n_finite)."""
+    S, n_per, n_steps = 10**4, 10**5, 150
+    amp, pw, truths = W.population(S)
+    ctls = [W.Control(n_steps=n_steps, amplitude_deg=float(a), pw_default_ms=float(p))
+            for a, p in zip(amp, pw)]
+    recs = np.stack([oracle.positions(truths[k], ctls[k]) for k in range(S)])
+    recs += np.random.default_rng(W.SEED_NOISE).normal(0.0, 0.02, size=recs.shape)
+    sp = W.paper_space(n_steps=n_steps)
+    err = torch.empty((S, n_per), dtype=torch.float64, device="cuda")
+    res = opmm.opmm_fit_batch(h, recs, ctls, sp, n_per, opmm.fit_options(err_out=err, cpu_check=0))
+    torch.cuda.synchronize()
+    fin = torch.isfinite(err)
+    nf = fin.sum(1).cpu().numpy()
+    emin = torch.where(fin, err, torch.full_like(err, float("inf"))).min(1).values
+    first = (err == emin[:, None]).to(torch.int8).argmax(1).cpu().numpy()
+    emin = emin.cpu().numpy()
+    for k in range(S):
+        r = res[k]
+        assert r["n_finite"] == nf[k], k
+        assert r["opt_err"] == emin[k] and r["best_index"] == first[k], k
+        w = oracle.objective(oracle.generate(sp, r["best_index"], saccade=k), recs[k], ctls[k])
+        assert abs(w - r["opt_err"]) <= 1e-9 * max(w, 1.0), k
+    rng = np.random.default_rng(4)
+    stats_all = {}
+    for k in sorted(rng.choice(S, 8, replace=False)):
+        o = oracle.fit(recs[k], ctls[k], sp, 0, n_per, saccade=int(k), nthreads=oracle.max_threads(),
+                       want_err=True)
+        assert (res[k]["best_index"], res[k]["n_finite"]) == (o["best_index"], o["n_finite"]), k
+        rel, _, _ = oracle.relativize(recs[k], ctls[k].amplitude_deg)
+        st = {}
+        assert_fp64_errors(err[k].cpu().numpy(), o["err"], lambda i, k=k: oracle.generate(sp, i, saccade=int(k)),
+                           recs[k], ctls[k], np.abs(rel).sum(), 0, stats=st)
+        for key, v in st.items():
+            if isinstance(v, (int, np.integer)):
+                stats_all[key] = stats_all.get(key, 0) + int(v)
+    print(f"\npopulation 1e4 x 1e5: all winners re-scored, 8 full sweeps, {stats_all}")

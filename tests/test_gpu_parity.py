@@ -778,6 +778,24 @@ def test_fp32_certified_fit(opmm, h):
     assert ei.value.status == opmm.ERR_UNSUPPORTED
 
 
+def test_fp32_certified_population(opmm, h):
+    """FP32 certification per saccade of opmm_fit_batch: each saccade keeps
+    its own exact fp32 top-8 and re-scores it in fp64; every saccade is
+    certified and returns the fp64 batch's winner and error."""
+    S = 24
+    amp, pw, truths = W.population(S)
+    ctls = [W.Control(n_steps=150, amplitude_deg=float(amp[k]), pw_default_ms=float(pw[k])) for k in range(S)]
+    recs = np.array([oracle.positions(truths[k], ctls[k]) + W.noise(151, seed=300 + k) for k in range(S)])
+    sp = W.paper_space(n_steps=150)
+    n_per = 20000
+    b64 = opmm.opmm_fit_batch(h, recs, ctls, sp, n_per, opmm.fit_options(precision=opmm.FP64))
+    b32 = opmm.opmm_fit_batch(h, recs, ctls, sp, n_per, opmm.fit_options(precision=opmm.FP32, certify=1))
+    for k in range(S):
+        assert b32[k]["certified"] == 1 and b32[k]["top_k"] == 8, k
+        assert (b32[k]["best_index"], b32[k]["opt_err"]) == (b64[k]["best_index"], b64[k]["opt_err"]), k
+        assert b32[k]["n_finite"] == b64[k]["n_finite"], k
+
+
 def test_fp32_certificate_refused_on_near_ties(opmm, h):
     """The certificate is not a formality: 64 candidates whose errors agree to
     ~1e-9 relative (K_LT_ANT varied by 1e-9) all lie within T*, so no list of

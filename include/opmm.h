@@ -185,6 +185,8 @@ typedef struct {
 #define OPMM_FIT_FLAG_NO_LANE_SORT   1u  /* fit_kernel: no pulse-end sort pre-pass    */
 #define OPMM_FIT_FLAG_SUPER_SMEM     2u  /* superposition: shared-memory columns only */
 #define OPMM_FIT_FLAG_NO_GRAPH       4u  /* opmm_fit: plain launches, no CUDA graph   */
+#define OPMM_FIT_FLAG_NO_GRID_TABLES 8u  /* grid fits: the generic grid generator, not
+                                            the shared-memory level tables           */
 
 typedef struct {
   int64_t best_index;            /* global candidate index; -1 if no finite E     */

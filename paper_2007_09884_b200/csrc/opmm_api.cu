@@ -752,11 +752,20 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
   const int32_t ns = ctl->n_steps + 1;
   size_t smem = three ? opmm::fit3_smem(precision, ns) : fit_smem(precision, ns, block, two ? 2 : 1);
   if (smem > kMaxDynSmem) return fail(OPMM_ERR_INVALID_ARG, "trace too long for shared memory");
+  const bool one = !two && !three && !refill;
+  // grid spaces: per-dimension level tables in shared memory (fit_kernel<GT>)
+  // when they fit, the propagator integrates and the flag does not forbid it
+  int64_t gt_n = 0;
+  for (int d = 0; d < OPMM_NPARAM; ++d) gt_n += space->levels[d] > 1 ? space->levels[d] : 0;
+  const bool grid_tables = one && space->mode == 1 && kernel_integ(integ, ctl) == 0 &&
+                           gt_n <= opmm::SUPER_MAX_GT &&
+                           !(opts && (opts->flags & OPMM_FIT_FLAG_NO_GRID_TABLES));
+  const size_t gt_bytes = grid_tables ? (size_t)gt_n * sizeof(double) : 0;
   const void* fn = three ? opmm::fit3_kernel_ptr(precision, metric)
                    : two ? opmm::fit2_kernel_ptr(precision, metric)
                    : refill ? opmm::fit_refill_kernel_ptr(precision, metric)
-                            : opmm::fit_kernel_ptr(precision, kernel_integ(integ, ctl), metric);
-  const bool one = !two && !three && !refill;
+                            : opmm::fit_kernel_ptr(precision, kernel_integ(integ, ctl), metric,
+                                                   grid_tables);
   // fit_kernel dynamic shared memory: rel, exp table, stash (opmm_kernels.cu),
   // then the super-tile permutation and the pre-pass key/rank scratch
   // (aliased onto the stash when it fits there)
@@ -766,10 +775,13 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
                            opmm::exp_tab_bytes();
   const size_t stash_sz = precision == OPMM_FP64 ? opmm::stash_bytes<double>(block)
                                                  : opmm::stash_bytes<float>(block);
-  auto fit_dyn = [&](int64_t sup) {
+  auto fit_dyn_nogt = [&](int64_t sup) {
     const size_t end = perm_off + opmm::perm_bytes(sup);
     return opmm::tmp_bytes(sup) <= stash_sz ? end : end + opmm::tmp_bytes(sup);
   };
+  // the level tables (if any) follow, 8-byte aligned
+  auto gt_at = [&](int64_t sup) { return (fit_dyn_nogt(sup) + 7) & ~(size_t)7; };
+  auto fit_dyn = [&](int64_t sup) { return gt_at(sup) + gt_bytes; };
   // largest super-tile the kernel's shared memory allows (long traces leave less room)
   int64_t super_cap = opmm::SUPER_MAX;
   if (one) {
@@ -850,6 +862,7 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
   a.perm_off = (int64_t)perm_off;
   a.tmp_off = (int64_t)(opmm::tmp_bytes(super) <= stash_sz ? stash_off
                                                           : perm_off + opmm::perm_bytes(super));
+  a.gt_off = grid_tables ? (int64_t)gt_at(super) : 0;
   a.topk = K;
   a.certify = certify ? 1 : 0;
   a.tk_e = h->tk_e;
@@ -1082,6 +1095,7 @@ opmm_status opmm_create(opmm_handle** out, int device) {
     for (int i = 0; i < 3; ++i)
       for (int m = 0; m < 2; ++m) {
         allow_dyn_smem(opmm::fit_kernel_ptr(p, i, m));
+        if (i == 0) allow_dyn_smem(opmm::fit_kernel_ptr(p, i, m, true));
         allow_dyn_smem(opmm::simscore_kernel_ptr(p, i, m));
         allow_dyn_smem(opmm::fit2_kernel_ptr(p, m));
         allow_dyn_smem(opmm::fit3_kernel_ptr(p, m));

@@ -142,6 +142,16 @@ __device__ __forceinline__ void expand_9param(double p[NP]) {
 // generator is ~20% of a candidate's instructions).  Grid mode (int64 div/mod
 // per dimension) stays rolled to keep the kernel's code footprint small.
 // Grid mode of generate_opc (mixed-radix digits, dimension 0 fastest).
+// Value of grid dimension d at level `digit` (lo, lo + j span, or lo exp(j span)).
+__device__ __forceinline__ double grid_value(const SpaceDev& sp, int d, uint64_t digit,
+                                            const double2* __restrict__ tab) {
+  const uint64_t L = (uint64_t)sp.levels[d];
+  if (sp.kind[d] == 0 || L <= 1) return sp.lo[d];
+  if (sp.kind[d] == 1) return __dadd_rn(sp.lo[d], __dmul_rn((double)digit, sp.span[d]));
+  const double x = __dmul_rn((double)digit, sp.span[d]);
+  return __dmul_rn(sp.lo[d], sp.kind[d] == 2 ? exp_tab(x, tab) : exp_libm(x));
+}
+
 __device__ __forceinline__ void generate_grid_opc(const SpaceDev& sp, int64_t idx, double p[NP],
                                                   const double2* __restrict__ tab) {
   uint64_t rem = (uint64_t)idx;
@@ -153,7 +163,7 @@ __device__ __forceinline__ void generate_grid_opc(const SpaceDev& sp, int64_t id
       digit = rem % L;
       rem = rem / L;
     }
-    double v;
+    double v;   // grid_value(sp, d, digit, tab), written out (register allocation of fit_kernel)
     if (sp.kind[d] == 0 || L <= 1) v = sp.lo[d];
     else if (sp.kind[d] == 1) v = __dadd_rn(sp.lo[d], __dmul_rn((double)digit, sp.span[d]));
     else {
@@ -206,6 +216,50 @@ __device__ __forceinline__ void generate_opc(const SpaceDev& sp, uint32_t saccad
 
 // PW of candidate idx alone (for the lane sort key): Philox block j = 4,
 // word 1 is dimension 17; grid mode takes the PW digit directly.
+// Grid spaces from per-dimension level tables (fit_kernel, GT): gt holds
+// grid_value(d, j) for every dimension with levels > 1, concatenated in
+// dimension order (build_grid_tables).  Digits of idx by mixed radix
+// (dimension 0 fastest; 32-bit division while the remainder fits), then one
+// shared-memory load per grid dimension -- bit-identical to
+// generate_grid_opc, whose values the tables are.
+__device__ __forceinline__ void build_grid_tables(const SpaceDev& sp, double* gt,
+                                                  const double2* __restrict__ tab) {
+  int off = 0;
+  for (int d = 0; d < NP; ++d) {
+    const int64_t L = sp.levels[d];
+    if (L <= 1) continue;
+    for (int j = threadIdx.x; j < (int)L; j += blockDim.x) gt[off + j] = grid_value(sp, d, (uint64_t)j, tab);
+    off += (int)L;
+  }
+}
+
+__device__ __forceinline__ void grid_opc_from_tables(const SpaceDev& sp, int64_t idx,
+                                                     const double* __restrict__ gt, double p[NP]) {
+  uint64_t rem = (uint64_t)idx;
+  int off = 0;
+#pragma unroll
+  for (int d = 0; d < NP; ++d) {
+    const int64_t L = sp.levels[d];
+    if (L > 1) {
+      uint64_t digit;
+      if ((rem >> 32) == 0) {
+        const uint32_t r32 = (uint32_t)rem, q32 = r32 / (uint32_t)L;
+        digit = r32 - q32 * (uint32_t)L;
+        rem = q32;
+      } else {
+        const uint64_t q = rem / (uint64_t)L;
+        digit = rem - q * (uint64_t)L;
+        rem = q;
+      }
+      p[d] = gt[off + (int)digit];
+      off += (int)L;
+    } else {
+      p[d] = sp.lo[d];
+    }
+  }
+  if (sp.model == 1) expand_9param(p);
+}
+
 __device__ __forceinline__ double generate_pw(const SpaceDev& sp, uint32_t saccade, int64_t idx,
                                               const double2* __restrict__ tab) {
   if (sp.mode == 0) {

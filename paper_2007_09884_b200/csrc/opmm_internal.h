@@ -91,6 +91,7 @@ struct FitArgs {
   int64_t super_tile;       // fit_kernel: candidates per block pass (multiple of 32, <= SUPER_MAX)
   int64_t perm_off;         // fit_kernel: byte offset of the super-tile permutation in smem
   int64_t tmp_off;          // fit_kernel: byte offset of the pre-pass key/rank scratch
+  int64_t gt_off;           // fit_kernel<GT>: byte offset of the grid level tables in smem
   Partial* partials;        // [S][gridDim.x]
   unsigned int* counters;   // [S], zero between launches
   RankPartial* rank_out;    // optional [S]: per-rank result (world > 1)
@@ -169,7 +170,7 @@ const void* nm_group_kernel_ptr(int precision, int obj, int metric, bool rel_glo
 size_t nm_group_smem(int precision, int obj, int32_t n_samples, bool rel_in_smem);
 int nm_group_problems_per_block();
 
-const void* fit_kernel_ptr(int precision, int integrator, int metric);
+const void* fit_kernel_ptr(int precision, int integrator, int metric, bool grid_tables = false);
 // superposition over one pulse-height grid dimension (kernel_variant 4, fp64)
 const void* fit_super_kernel_ptr(int metric, bool tmem, bool fp32);
 constexpr int SUPER_MAX_WARPS = 8;   // per block: TMEM warps (<= 4, one per quadrant) + smem warps
@@ -177,7 +178,7 @@ constexpr int SUPER_TMEM_MAX_STEPS = 120;   // 4 TMEM columns per sample, groups
 constexpr int SUPER_MAX_L = 4096;    // levels of the superposed dimension
 size_t super_smem(int32_t n_samples, int32_t levels, int32_t gt_n, int smem_warps, int tm_warps,
                   bool fp32 = false);
-constexpr int32_t SUPER_MAX_GT = 2048;   // level-table entries kept in shared memory
+constexpr int32_t SUPER_MAX_GT = 2048;   // level-table entries kept in shared memory (also fit_kernel<GT>)
 const void* fit2_kernel_ptr(int precision, int metric);   // 2 candidates/thread, 256 threads
 constexpr int FIT2_BLOCK = 256;
 const void* fit_refill_kernel_ptr(int precision, int metric);   // lane refill (f2), default block

@@ -429,14 +429,22 @@ __global__ void __launch_bounds__(32) cert_kernel(FitArgs a) {
 // registers), 3 warps per scheduler: measured best among 128/168/238-register
 // budgets.
 // ---------------------------------------------------------------------------
-template <typename T, int INTEG, int METRIC>
+// GT: a grid space whose level tables fit shared memory (a.gt_off): every
+// candidate's OPC is digits + table loads (grid_opc_from_tables) instead of
+// generate_grid_opc's 64-bit divisions and exps -- the same values.
+template <typename T, int INTEG, int METRIC, bool GT>
 __global__ void __launch_bounds__(OPMM_FIT_LB_THREADS, OPMM_FIT_LB_BLOCKS) fit_kernel(FitArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int32_t ns = a.ctl.n_steps + 1;
   T* rel = reinterpret_cast<T*>(smem_raw);
   double2* tab = reinterpret_cast<double2*>(smem_raw + rel_bytes<T>(ns));
   T* stash = reinterpret_cast<T*>(smem_raw + rel_bytes<T>(ns) + exp_tab_bytes());  // [10][block] vec2
+  double* gt = GT ? reinterpret_cast<double*>(smem_raw + a.gt_off) : nullptr;
   for (int j = threadIdx.x; j < EXP_TAB_N; j += blockDim.x) tab[j] = a.exp_tab[j];
+  if (GT) {
+    __syncthreads();   // grid_value reads the exp table
+    build_grid_tables(a.space, gt, tab);
+  }
   const int64_t sac = (int64_t)blockIdx.y + a.sac_begin;
   const double amp = a.sac_ctl ? a.sac_ctl[2 * sac] : a.amplitude;
   const double pwd = a.sac_ctl ? a.sac_ctl[2 * sac + 1] : a.pw_default;
@@ -529,7 +537,8 @@ __global__ void __launch_bounds__(OPMM_FIT_LB_THREADS, OPMM_FIT_LB_BLOCKS) fit_k
       const int off = a.sort_lanes ? (int)s_perm[sl] : sl;
       const int64_t i = sb + off;
       double p[NP];
-      generate_opc(a.space, (uint32_t)sac, i, p, tab);
+      if (GT) grid_opc_from_tables(a.space, i, gt, p);
+      else generate_opc(a.space, (uint32_t)sac, i, p, tab);
       const double E = evaluate<T, INTEG, METRIC, false>(p, a.ctl, Aprime, pwd, rel, nullptr, 0,
                                                          sgn, nullptr, stash, !a.space.all_physical);
       if (valid) {
@@ -1718,13 +1727,17 @@ __global__ void generate_kernel(SpaceDev sp, uint32_t saccade, int64_t begin, in
 // ---------------------------------------------------------------------------
 // Launchers.
 // ---------------------------------------------------------------------------
-template <typename T, int INTEG, int METRIC>
-static const void* fit_fn() { return reinterpret_cast<const void*>(&fit_kernel<T, INTEG, METRIC>); }
+template <typename T, int INTEG, int METRIC, bool GT = false>
+static const void* fit_fn() { return reinterpret_cast<const void*>(&fit_kernel<T, INTEG, METRIC, GT>); }
 
 // integrator 2 = the propagator with substeps (internal; the host picks it
 // when opmm_control.substeps > 1) -- its own instantiation, so the out-of-line
 // substep power never touches the plain propagator kernels' register budget
-const void* fit_kernel_ptr(int precision, int integrator, int metric) {
+const void* fit_kernel_ptr(int precision, int integrator, int metric, bool grid_tables) {
+  if (grid_tables && integrator == 0) {   // the propagator only
+    if (precision == 0) return metric == 0 ? fit_fn<double, 0, 0, true>() : fit_fn<double, 0, 1, true>();
+    return metric == 0 ? fit_fn<float, 0, 0, true>() : fit_fn<float, 0, 1, true>();
+  }
   if (precision == 0) {
     if (integrator == 0) return metric == 0 ? fit_fn<double, 0, 0>() : fit_fn<double, 0, 1>();
     if (integrator == 2) return metric == 0 ? fit_fn<double, 2, 0>() : fit_fn<double, 2, 1>();

@@ -49,7 +49,7 @@ class SearchSpace(C.Structure):
 
 
 MAX_TOPK = 32
-FIT_FLAG_NO_LANE_SORT, FIT_FLAG_SUPER_SMEM, FIT_FLAG_NO_GRAPH = 1, 2, 4
+FIT_FLAG_NO_LANE_SORT, FIT_FLAG_SUPER_SMEM, FIT_FLAG_NO_GRAPH, FIT_FLAG_NO_GRID_TABLES = 1, 2, 4, 8
 
 
 class FitOptions(C.Structure):

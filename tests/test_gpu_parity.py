@@ -562,6 +562,96 @@ def test_fit_refill_edges(opmm, h, metric):
     assert ei.value.status == opmm.ERR_UNSUPPORTED
 
 
+def _grid_spaces():
+    d = W.truth_opc()
+    mixed = W.grid_space({"K_SE_AG": (d[I["K_SE_AG"]] * 0.5, d[I["K_SE_AG"]] * 2.0, 7, True),
+                          "J": (d[I["J"]] * 1e-3, d[I["J"]] * 1e3, 5, True),       # x up to 13.8: libm exp
+                          "B_ANT": (d[I["B_ANT"]] * 0.5, d[I["B_ANT"]] * 1.5, 3, False),
+                          "PW": (5.0, 80.0, 16, False)})
+    lo, hi = np.ones(18), np.ones(18)
+    logs, lv = np.zeros(18, dtype=np.uint8), np.ones(18, dtype=np.int32)
+    for name, dv in zip(W.NINE_SLOTS, W.TABLE2_DEFAULTS):
+        lo[I[name]] = hi[I[name]] = dv
+    for name, n in (("K_SE_AG", 9), ("B_AG", 6), ("J", 5), ("N_C_FIX", 4)):
+        dv = W.TABLE2_DEFAULTS[W.NINE_SLOTS.index(name)]
+        lo[I[name]], hi[I[name]], logs[I[name]], lv[I[name]] = 0.3 * dv, 3.0 * dv, 1, n
+    nine = W.SearchSpace(1, 0, lo, hi, logs, lv, model=1)
+    return [("g4", W.g4_space(32)), ("mixed", mixed), ("nine", nine)]
+
+
+@pytest.mark.parametrize("precision", [0, 1])
+@pytest.mark.parametrize("metric", [0, 1])
+def test_grid_level_tables_bit_identical(opmm, h, precision, metric):
+    """Grid fits take each OPC from per-dimension level tables in shared
+    memory (fit_kernel<GT>): mixed-radix digits + one load per grid
+    dimension.  Every error is bit-identical to the generic grid generator's
+    (OPMM_FIT_FLAG_NO_GRID_TABLES) on G4 at 32^4 nodes, a grid with
+    linear, table-exp and libm-exp (argument >= 8) dimensions, and a
+    9-parameter-model grid (D7 expansion after the lookup); and the 9-param
+    grid against the oracle."""
+    ctl = W.Control()
+    rec = trace(ctl)
+    for name, sp in _grid_spaces():
+        n = sp.n_grid()
+        r1, E1 = _fit(opmm, h, rec, ctl, sp, n, precision=precision, metric=metric, kernel_variant=1)
+        r0, E0 = _fit(opmm, h, rec, ctl, sp, n, precision=precision, metric=metric, kernel_variant=1,
+                      flags=opmm.FIT_FLAG_NO_GRID_TABLES)
+        assert (r1["best_index"], r1["opt_err"], r1["n_finite"]) == \
+               (r0["best_index"], r0["opt_err"], r0["n_finite"]), name
+        assert np.array_equal(E1, E0, equal_nan=True), name
+        if name == "nine" and precision == 0:
+            o = oracle.fit(rec, ctl, sp, 0, n, metric=metric, want_err=True)
+            rel, _, _ = oracle.relativize(rec, ctl.amplitude_deg)
+            scale = np.abs(rel).sum() if metric == 0 else np.sqrt(np.mean(rel ** 2))
+            assert_fp64_errors(E1, o["err"], lambda i: oracle.generate(sp, i), rec, ctl, scale, metric)
+            assert r1["best_index"] == o["best_index"]
+
+
+def test_grid_level_tables_beyond_2_32_and_population(opmm, h):
+    """The table path's 64-bit digit step (indices >= 2^32) and the
+    population batch: same results as the generic grid generator."""
+    ctl = W.Control()
+    rec = trace(ctl)
+    d = W.truth_opc()
+    dims = {k: (d[I[k]] * 0.8, d[I[k]] * 1.25, 100, True) for k in ("K_SE_AG", "B_AG", "N_SAC_AG", "B_ANT")}
+    dims["PW"] = (1.0, 85.0, 43, False)
+    sp = W.grid_space(dims)
+    n = sp.n_grid()   # 4.3e9 > 2^32 nodes
+    assert n > 2**32
+    o = opmm.fit_options(kernel_variant=1, cpu_check=0)
+    r1 = opmm.opmm_fit(h, rec, ctl, sp, n, o)
+    r0 = opmm.opmm_fit(h, rec, ctl, sp, n, opmm.fit_options(kernel_variant=1, cpu_check=0,
+                                                           flags=opmm.FIT_FLAG_NO_GRID_TABLES))
+    assert (r1["best_index"], r1["opt_err"], r1["n_finite"]) == (r0["best_index"], r0["opt_err"], r0["n_finite"])
+    # the tail past 2^32 alone, element-wise
+    tail = 4 * 10**6
+    e1 = torch.empty(n, dtype=torch.float64, device="cuda")
+    e0 = torch.empty(n, dtype=torch.float64, device="cuda")
+    opmm.opmm_fit(h, rec, ctl, sp, n, opmm.fit_options(kernel_variant=1, cpu_check=0, err_out=e1))
+    opmm.opmm_fit(h, rec, ctl, sp, n, opmm.fit_options(kernel_variant=1, cpu_check=0, err_out=e0,
+                                                      flags=opmm.FIT_FLAG_NO_GRID_TABLES))
+    torch.cuda.synchronize()
+    assert torch.equal(e1[-tail:].isnan(), e0[-tail:].isnan())
+    assert bool((e1[-tail:] == e0[-tail:]).logical_or(e1[-tail:].isnan()).all())
+    del e1, e0
+    S = 4
+    amp, pw, truths = W.population(S)
+    ctls = [W.Control(n_steps=150, amplitude_deg=float(amp[k]), pw_default_ms=float(pw[k])) for k in range(S)]
+    recs = np.array([oracle.positions(truths[k], ctls[k]) + W.noise(151, seed=40 + k) for k in range(S)])
+    spg = _grid_spaces()[1][1]
+    npg = spg.n_grid()
+    for fl in (0, opmm.FIT_FLAG_NO_GRID_TABLES):
+        err = torch.empty((S, npg), dtype=torch.float64, device="cuda")
+        res = opmm.opmm_fit_batch(h, recs, ctls, spg, npg, opmm.fit_options(kernel_variant=1, err_out=err, flags=fl))
+        torch.cuda.synchronize()
+        if fl == 0:
+            ref_res, ref_err = res, err.cpu().numpy()
+        else:
+            assert np.array_equal(err.cpu().numpy(), ref_err, equal_nan=True)
+            for k in range(S):
+                assert (res[k]["best_index"], res[k]["opt_err"]) == (ref_res[k]["best_index"], ref_res[k]["opt_err"])
+
+
 def test_fit_async_matches_sync(opmm, h):
     import ctypes
     ctl = W.Control()

@@ -1,5 +1,7 @@
-"""Fit kernel time on the G4 planted grid (10^8, grid-mode generation) vs the
-random S_paper space at the same N (GPU box).   python tools/time_grid.py"""
+"""Direct fit kernel (kernel_variant 1) on the G4 planted grid (10^8) with
+the shared-memory level tables (default) and with the generic grid generator
+(OPMM_FIT_FLAG_NO_GRID_TABLES), fp64 and fp32, against the random S_paper
+space at the same N (GPU box).   python tools/time_grid.py"""
 import ctypes
 import os
 import sys
@@ -15,10 +17,17 @@ from paper_2007_09884_b200 import opmm  # noqa: E402
 
 ctl = W.Control()
 rec = torch.as_tensor(oracle.positions(W.truth_opc(), ctl), device="cuda")
+n = 10**8
+cases = [("G4 tables fp64", W.g4_space(100), dict(kernel_variant=1)),
+         ("G4 generic fp64", W.g4_space(100), dict(kernel_variant=1, flags=opmm.FIT_FLAG_NO_GRID_TABLES)),
+         ("G4 tables fp32", W.g4_space(100), dict(kernel_variant=1, precision=1)),
+         ("G4 generic fp32", W.g4_space(100), dict(kernel_variant=1, precision=1, flags=opmm.FIT_FLAG_NO_GRID_TABLES)),
+         ("S_paper fp64", W.paper_space(), dict()),
+         ("S_paper fp32", W.paper_space(), dict(precision=1))]
 with opmm.opmm_create(0) as h:
     out = torch.zeros(ctypes.sizeof(opmm.FitResult), dtype=torch.uint8, device="cuda")
-    for name, sp, n in (("G4 grid", W.g4_space(100), 10**8), ("S_paper random", W.paper_space(), 10**8)):
-        o = opmm.fit_options(cpu_check=0)
+    for name, sp, kw in cases:
+        o = opmm.fit_options(cpu_check=0, **kw)
         for _ in range(2):
             opmm.opmm_fit_async(h, rec, ctl, sp, n, out, o)
         ms = []
@@ -27,4 +36,4 @@ with opmm.opmm_create(0) as h:
             ms.append(opmm.opmm_last_kernel_ms(h))
         torch.cuda.ExternalStream(h.stream).synchronize()
         r = opmm.decode_result(bytes(out.cpu().numpy()))
-        print(f"{name:15s} N={n:.0e}: {np.median(ms):7.2f} ms  best {r['best_index']}", flush=True)
+        print(f"{name:16s} N={n:.0e}: {np.median(ms):7.2f} ms  best {r['best_index']}", flush=True)

@@ -214,8 +214,6 @@ __device__ __forceinline__ void generate_opc(const SpaceDev& sp, uint32_t saccad
   }
 }
 
-// PW of candidate idx alone (for the lane sort key): Philox block j = 4,
-// word 1 is dimension 17; grid mode takes the PW digit directly.
 // Grid spaces from per-dimension level tables (fit_kernel, GT): gt holds
 // grid_value(d, j) for every dimension with levels > 1, concatenated in
 // dimension order (build_grid_tables).  Digits of idx by mixed radix
@@ -260,6 +258,8 @@ __device__ __forceinline__ void grid_opc_from_tables(const SpaceDev& sp, int64_t
   if (sp.model == 1) expand_9param(p);
 }
 
+// PW of candidate idx alone (for the lane sort key): Philox block j = 4,
+// word 1 is dimension 17; grid mode takes the PW digit directly.
 __device__ __forceinline__ double generate_pw(const SpaceDev& sp, uint32_t saccade, int64_t idx,
                                               const double2* __restrict__ tab) {
   if (sp.mode == 0) {

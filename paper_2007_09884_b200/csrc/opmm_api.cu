@@ -757,10 +757,10 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
   // when they fit, the propagator integrates and the flag does not forbid it
   int64_t gt_n = 0;
   for (int d = 0; d < OPMM_NPARAM; ++d) gt_n += space->levels[d] > 1 ? space->levels[d] : 0;
-  const bool grid_tables = one && space->mode == 1 && kernel_integ(integ, ctl) == 0 &&
-                           gt_n <= opmm::SUPER_MAX_GT &&
-                           !(opts && (opts->flags & OPMM_FIT_FLAG_NO_GRID_TABLES));
-  const size_t gt_bytes = grid_tables ? (size_t)gt_n * sizeof(double) : 0;
+  bool grid_tables = one && space->mode == 1 && kernel_integ(integ, ctl) == 0 &&
+                     gt_n <= opmm::SUPER_MAX_GT &&
+                     !(opts && (opts->flags & OPMM_FIT_FLAG_NO_GRID_TABLES));
+  size_t gt_bytes = grid_tables ? (size_t)gt_n * sizeof(double) : 0;
   const void* fn = three ? opmm::fit3_kernel_ptr(precision, metric)
                    : two ? opmm::fit2_kernel_ptr(precision, metric)
                    : refill ? opmm::fit_refill_kernel_ptr(precision, metric)
@@ -782,6 +782,13 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
   // the level tables (if any) follow, 8-byte aligned
   auto gt_at = [&](int64_t sup) { return (fit_dyn_nogt(sup) + 7) & ~(size_t)7; };
   auto fit_dyn = [&](int64_t sup) { return gt_at(sup) + gt_bytes; };
+  // the tables must leave room for the smallest super-tile (very long
+  // traces), else the generic grid generator
+  if (grid_tables && fit_dyn(32) > max_dyn_smem(fn)) {
+    grid_tables = false;
+    gt_bytes = 0;
+    fn = opmm::fit_kernel_ptr(precision, kernel_integ(integ, ctl), metric, false);
+  }
   // largest super-tile the kernel's shared memory allows (long traces leave less room)
   int64_t super_cap = opmm::SUPER_MAX;
   if (one) {

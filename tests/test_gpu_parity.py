@@ -608,8 +608,9 @@ def test_grid_level_tables_bit_identical(opmm, h, precision, metric):
 
 
 def test_grid_level_tables_beyond_2_32_and_population(opmm, h):
-    """The table path's 64-bit digit step (indices >= 2^32) and the
-    population batch: same results as the generic grid generator."""
+    """The table path's 64-bit digit step (indices >= 2^32), a 16000-step
+    trace with 1900 table entries, and the population batch: same results as
+    the generic grid generator."""
     ctl = W.Control()
     rec = trace(ctl)
     d = W.truth_opc()
@@ -634,6 +635,18 @@ def test_grid_level_tables_beyond_2_32_and_population(opmm, h):
     assert torch.equal(e1[-tail:].isnan(), e0[-tail:].isnan())
     assert bool((e1[-tail:] == e0[-tail:]).logical_or(e1[-tail:].isnan()).all())
     del e1, e0
+    # a long trace (fp64 rel 128 KB in shared memory) with large tables (1900 entries)
+    cl = W.Control(n_steps=16000)
+    rl = trace(cl)
+    spl = W.grid_space({"N_SAC_AG": (d[I["N_SAC_AG"]] * 0.5, d[I["N_SAC_AG"]] * 1.5, 900, False),
+                        "PW": (1.0, 16000.0, 1000, False)})
+    sub = 9 * 10**5
+    for prec in (0, 1):
+        a1, A1 = _fit(opmm, h, rl, cl, spl, spl.n_grid(), precision=prec, kernel_variant=1)
+        a0, A0 = _fit(opmm, h, rl, cl, spl, spl.n_grid(), precision=prec, kernel_variant=1,
+                      flags=opmm.FIT_FLAG_NO_GRID_TABLES)
+        assert (a1["best_index"], a1["opt_err"], a1["n_finite"]) == (a0["best_index"], a0["opt_err"], a0["n_finite"])
+        assert np.array_equal(A1[:sub], A0[:sub], equal_nan=True)
     S = 4
     amp, pw, truths = W.population(S)
     ctls = [W.Control(n_steps=150, amplitude_deg=float(amp[k]), pw_default_ms=float(pw[k])) for k in range(S)]

@@ -175,7 +175,8 @@ typedef struct {
                            (reading Q12), over all candidates and ranks.
                            kernel_variant 0/1 (auto never superposes then).     */
   uint32_t flags;       /* OPMM_FIT_FLAG_* (measurement / test switches)          */
-  double* err_out;      /* optional DEVICE [n]: E_i of every candidate (validation) */
+  double* err_out;      /* optional DEVICE [n]: E_i of every candidate (validation);
+                           a host pointer is refused (OPMM_ERR_INVALID_ARG)      */
 } opmm_fit_options;
 
 #define OPMM_MAX_TOPK 32

@@ -384,6 +384,18 @@ bool is_device_ptr(const void* p) {
   return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+// a kernel may write through p: device or managed memory, or mapped pinned
+// host memory whose device address is p itself (UVA)
+bool is_device_accessible(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged ||
+         (a.type == cudaMemoryTypeHost && a.devicePointer == p);
+}
+
 // Host-or-device buffers of the asynchronous entry points (SURVEY 8(b):
 // "pointers may be host or device; the library detects which with
 // cudaPointerGetAttributes").  A device (or managed) pointer is used in place.
@@ -704,6 +716,8 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
   if (kv_opt < 0 || kv_opt > 5) return fail(OPMM_ERR_INVALID_ARG, "kernel_variant must be 0..5");
   if (top_k < 0 || top_k > OPMM_MAX_TOPK)
     return fail(OPMM_ERR_INVALID_ARG, "top_k must be in [0, %d] (got %d)", OPMM_MAX_TOPK, top_k);
+  if (opts && opts->err_out && !is_device_accessible(opts->err_out))
+    return fail(OPMM_ERR_INVALID_ARG, "err_out must be device (or mapped) memory");
   // FP32 certification: the exact top-K by fp32 error (K = top_k, or 32),
   // re-scored in fp64 by the finishing block (or, world > 1, the merge kernel)
   const bool certify = opts && opts->certify && precision == OPMM_FP32;

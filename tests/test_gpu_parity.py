@@ -560,6 +560,10 @@ def test_fit_refill_edges(opmm, h, metric):
     with pytest.raises(opmm.OpmmError) as ei:
         _fit(opmm, h, rec, ctl, sp, 100, kernel_variant=5, top_k=4)
     assert ei.value.status == opmm.ERR_UNSUPPORTED
+    host_err = np.zeros(100)
+    with pytest.raises(opmm.OpmmError) as ei:   # err_out must be device memory
+        opmm.opmm_fit(h, rec, ctl, sp, 100, opmm.fit_options(err_out=host_err))
+    assert ei.value.status == opmm.ERR_INVALID_ARG
 
 
 def _grid_spaces():

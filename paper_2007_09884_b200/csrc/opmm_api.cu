@@ -1529,6 +1529,8 @@ opmm_status opmm_fit_async(opmm_handle* h, const double* recorded_dev, const opm
   if (n_candidates < 0) return fail(OPMM_ERR_INVALID_ARG, "n_candidates < 0");
   CKS(validate_space(space, n_candidates));
   if (!recorded_dev || !out_dev) return fail(OPMM_ERR_INVALID_ARG, "NULL recorded/out");
+  if (!is_device_accessible(recorded_dev) || !is_device_accessible(out_dev))
+    return fail(OPMM_ERR_INVALID_ARG, "opmm_fit_async takes device buffers (use opmm_fit for host ones)");
   return enqueue_fit(h, recorded_dev, ctl, nullptr, 0, 1, space, n_candidates, opts, out_dev, true);
 }
 

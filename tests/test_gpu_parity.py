@@ -564,6 +564,11 @@ def test_fit_refill_edges(opmm, h, metric):
     with pytest.raises(opmm.OpmmError) as ei:   # err_out must be device memory
         opmm.opmm_fit(h, rec, ctl, sp, 100, opmm.fit_options(err_out=host_err))
     assert ei.value.status == opmm.ERR_INVALID_ARG
+    import ctypes
+    out_host = np.zeros(ctypes.sizeof(opmm.FitResult), dtype=np.uint8)
+    with pytest.raises(opmm.OpmmError) as ei:   # the async entry point takes device buffers
+        opmm.opmm_fit_async(h, dev(rec), ctl, sp, 100, out_host)
+    assert ei.value.status == opmm.ERR_INVALID_ARG
 
 
 def _grid_spaces():

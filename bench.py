@@ -61,7 +61,7 @@ FP64_MEASURED_TFLOPS = 36.90
 FP32_MEASURED_TFLOPS = 45.64
 
 
-def ncu_traffic_bytes(kernel="fit_kernel<double, 0, 0>"):
+def ncu_traffic_bytes(kernel="fit_kernel<double, 0, 0, 0>"):
     """dram__bytes_read.sum + dram__bytes_write.sum of a fit kernel from the
     committed `ncu --set full` capture summary (profiles/), per launch."""
     units = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
@@ -95,7 +95,7 @@ def fp32_roofline(per_gpu, kernel_ms):
             "fp32_frac": f32 / FP32_MEASURED_TFLOPS, "fp32_frac_of_nominal": f32 / FP32_PEAK_TFLOPS,
             "fp64_setup_tflops": f64, "fp64_frac": f64 / FP64_PEAK_TFLOPS,
             "frac": f32 / FP32_MEASURED_TFLOPS + f64 / FP64_PEAK_TFLOPS,
-            "traffic": ncu_traffic_bytes("fit_kernel<float, 0, 0>"),
+            "traffic": ncu_traffic_bytes("fit_kernel<float, 0, 0, 0>"),
             "peak_basis": "measured all-register FFMA rate (profiles/r02_fma_peak.txt); nominal "
                           "148 SM x 128 FP32 lanes x 2 x 1965 MHz = 74.4 for context; fp64 setup "
                           "vs nominal 37.2"}

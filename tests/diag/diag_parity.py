@@ -3,7 +3,7 @@
 Prints the candidates with the largest relative |E_gpu - E_orc| together
 with their RK4 spectral radius, and for the worst few an 80-bit long-double
 RK4 reference (numpy longdouble) to show which side is closer to the exact
-RK4 value.   python tools/diag_parity.py [N]
+RK4 value.   python tests/diag/diag_parity.py [N]
 """
 import os
 import sys
@@ -11,7 +11,7 @@ import sys
 import numpy as np
 import torch
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 import oracle  # noqa: E402
 import workloads as W  # noqa: E402

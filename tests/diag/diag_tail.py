@@ -2,7 +2,7 @@
 whose GPU error differs from the oracle's by more than 1e-10 relative, with
 its RK4 spectral radius and both sides' distance to the 80-bit referee.
 
-    python tools/gpu/diag_tail.py [n] > gpurun_out/tail.txt
+    python tests/diag/diag_tail.py [n] > gpurun_out/tail.txt
 """
 import os
 import sys

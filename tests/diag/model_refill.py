@@ -2,13 +2,13 @@
 distribution of diverged S_paper candidates (oracle trajectories) and the
 throughput of refilling dead lanes in batches of R, with the measured costs
 (setup ~80 step-equivalents per warp-wide batch: 100 us of setup against
-1.26 us per step per 10^6 candidates).   python tools/model_refill.py"""
+1.26 us per step per 10^6 candidates).   python tests/diag/model_refill.py"""
 import os
 import sys
 
 import numpy as np
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 import oracle  # noqa: E402  (test infrastructure: trajectories for the model's input)
 import workloads as W  # noqa: E402

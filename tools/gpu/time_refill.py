@@ -15,16 +15,17 @@ pkg = sys.argv[1] if len(sys.argv) > 1 else ROOT
 sys.path.insert(0, ROOT)
 sys.path.insert(0, pkg)
 import torch  # noqa: E402
-import oracle  # noqa: E402  (test trace only)
 import workloads as W  # noqa: E402
 from paper_2007_09884_b200 import opmm  # noqa: E402
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+from synth_trace import truth_trace  # noqa: E402
 
 tag = os.path.basename(pkg.rstrip("/")) if pkg != ROOT else "repo"
 n = 10**6
 with opmm.opmm_create(0) as h:
     for n_steps in (100, 150, 300):
         ctl = W.Control(n_steps=n_steps)
-        rec = oracle.positions(W.truth_opc(), ctl) + W.noise(n_steps + 1)
+        rec = truth_trace(opmm, h, ctl)
         sp = W.paper_space(n_steps=n_steps)
         recd = torch.as_tensor(rec, device="cuda")
         out = torch.zeros(ctypes.sizeof(opmm.FitResult), dtype=torch.uint8, device="cuda")

@@ -6,14 +6,16 @@ ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)
 pkg = sys.argv[1] if len(sys.argv) > 1 and sys.argv[1] != "-" else ROOT
 sys.path.insert(0, ROOT)
 sys.path.insert(0, pkg)
-import torch, oracle, workloads as W
+import torch, workloads as W
 from paper_2007_09884_b200 import opmm
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+from synth_trace import truth_trace
 tag = os.path.basename(pkg.rstrip("/")) if pkg != ROOT else "repo"
 with opmm.opmm_create(0) as h:
     out = torch.zeros(ctypes.sizeof(opmm.FitResult), dtype=torch.uint8, device="cuda")
     for n_steps in (int(x) for x in sys.argv[2:]):
         ctl = W.Control(n_steps=n_steps)
-        rec = torch.as_tensor(oracle.positions(W.truth_opc(), ctl) + W.noise(n_steps + 1), device="cuda")
+        rec = torch.as_tensor(truth_trace(opmm, h, ctl), device="cuda")
         sp = W.paper_space(n_steps=n_steps)
         line = []
         for prec in (0, 1):

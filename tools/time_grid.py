@@ -11,12 +11,12 @@ import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-import oracle  # noqa: E402  (the trace only)
 import workloads as W  # noqa: E402
 from paper_2007_09884_b200 import opmm  # noqa: E402
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from synth_trace import truth_trace  # noqa: E402
 
 ctl = W.Control()
-rec = torch.as_tensor(oracle.positions(W.truth_opc(), ctl), device="cuda")
 n = 10**8
 cases = [("G4 tables fp64", W.g4_space(100), dict(kernel_variant=1)),
          ("G4 generic fp64", W.g4_space(100), dict(kernel_variant=1, flags=opmm.FIT_FLAG_NO_GRID_TABLES)),
@@ -25,6 +25,7 @@ cases = [("G4 tables fp64", W.g4_space(100), dict(kernel_variant=1)),
          ("S_paper fp64", W.paper_space(), dict()),
          ("S_paper fp32", W.paper_space(), dict(precision=1))]
 with opmm.opmm_create(0) as h:
+    rec = torch.as_tensor(truth_trace(opmm, h, ctl, noisy=False), device="cuda")
     out = torch.zeros(ctypes.sizeof(opmm.FitResult), dtype=torch.uint8, device="cuda")
     for name, sp, kw in cases:
         o = opmm.fit_options(cpu_check=0, **kw)

@@ -10,12 +10,12 @@ import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-import oracle  # noqa: E402  (the trace only)
 import workloads as W  # noqa: E402
 from paper_2007_09884_b200 import opmm  # noqa: E402
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from synth_trace import truth_trace  # noqa: E402
 
 ctl = W.Control()
-rec = torch.as_tensor(oracle.positions(W.truth_opc(), ctl) + W.noise(101), device="cuda")
 d = W.truth_opc()
 I = W.IDX
 grids = [("G4 100^4", W.g4_space(100))]
@@ -29,6 +29,7 @@ for L in (10, 32, 100, 400):
         "N_SAC_AG": (d[I["N_SAC_AG"]] * 0.5, d[I["N_SAC_AG"]] * 2.0, L, True),
         "PW": (1.0, 100.0, npw, False)})))
 with opmm.opmm_create(0) as h:
+    rec = torch.as_tensor(truth_trace(opmm, h, ctl), device="cuda")
     out = torch.zeros(ctypes.sizeof(opmm.FitResult), dtype=torch.uint8, device="cuda")
     for name, sp in grids:
         n = sp.n_grid()

@@ -136,6 +136,26 @@ def test_product_does_not_import_the_oracle():
             assert "from paper_2007_09884_b200" not in txt and "libopmm.so" not in txt, f
 
 
+def test_only_tests_smoke_and_bench_touch_the_oracle():
+    """Outside tests/ and oracle/ itself, only __graft_entry__.py (smoke),
+    bench.py (its CPU-baseline and reference legs) and scripts/ (the committed
+    writers of tests/golden/ fixtures, which call only oracle/) may import
+    oracle/; tools/, workloads/, examples/ and the package never do."""
+    allowed = {os.path.join(ROOT, "__graft_entry__.py"), os.path.join(ROOT, "bench.py")}
+    for dirpath, dirs, files in os.walk(ROOT):
+        rel = os.path.relpath(dirpath, ROOT)
+        top = rel.split(os.sep)[0]
+        if top in ("tests", "oracle", "scripts", ".git", "gpurun_out", "baseline") or "/scratch" in dirpath \
+                or "/var" in dirpath:
+            dirs[:] = []
+            continue
+        for f in files:
+            path = os.path.join(dirpath, f)
+            if f.endswith(".py") and path not in allowed:
+                txt = open(path).read()
+                assert "import oracle" not in txt and "from oracle" not in txt, path
+
+
 def test_stream_marshalling():
     """torch's default stream is the legacy NULL stream; the C ABI reads NULL
     as "the handle's own (non-blocking) stream", so the binding must pass

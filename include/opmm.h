@@ -329,6 +329,23 @@ opmm_status opmm_fit_async(opmm_handle* h, const double* recorded_dev, const opm
                            const opmm_search_space* space, int64_t n_candidates,
                            const opmm_fit_options* opts, opmm_fit_result* out_dev);
 
+/* One rank's share of a fit, on a PLAIN handle, for callers that launch the
+ * ranks themselves (their own launcher or communicator) and merge on the
+ * host: the same evaluation as opmm_fit for rank `rank` of `world` (SURVEY
+ * 8(e)) -- candidates [floor(rN/R), floor((r+1)N/R)), or, when the
+ * superposition kernel is chosen, that range of grid nodes with all their
+ * levels -- with out (HOST) describing the shard: its lexicographic best
+ * (global index), n_finite, n_evaluated, its exact top-K when asked, CPU_check
+ * of its winner.  The shards partition the candidates, so the fit's winner is
+ * opmm_merge_argmin over the shards' (opt_err, best_index), its n_finite the
+ * sum, its top-K opmm_merge_topk over their lists; with FP32 certify each
+ * shard re-scores its own list in fp64, and the merged winner is certified
+ * when every shard is (each certified shard returns its fp64-best).  An
+ * NCCL handle is refused (it shards by itself). */
+opmm_status opmm_fit_shard(opmm_handle* h, const double* recorded, const opmm_control* ctl,
+                           const opmm_search_space* space, int64_t n_candidates, int rank,
+                           int world, const opmm_fit_options* opts, opmm_fit_result* out);
+
 /* Population batch: S independent saccades, each
  * fitted over candidates [0, n_per) of `space` with Philox counter word 2 =
  * saccade index.  recorded: HOST or DEVICE [S][n_steps+1] (same n_steps and

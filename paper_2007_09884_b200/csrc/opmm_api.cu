@@ -696,7 +696,10 @@ opmm_status enqueue_fit_super(opmm_handle* h, const double* rec_dev, const opmm_
     prepare_only->a = a;
     return OPMM_OK;
   }
-  if (prepare_only) prepare_only->fn = nullptr;
+  if (prepare_only) {   // not graph-eligible: nothing launched, the caller enqueues it plainly
+    prepare_only->fn = nullptr;
+    return OPMM_OK;
+  }
   return launch_fit_and_merge(h, fn, a, grid, block, smem, s_begin, S, multi, out_dev);
 }
 
@@ -903,7 +906,10 @@ opmm_status enqueue_fit(opmm_handle* h, const double* rec_dev, const opmm_contro
     prepare_only->a = a;
     return OPMM_OK;
   }
-  if (prepare_only) prepare_only->fn = nullptr;   // not graph-eligible: launched here
+  if (prepare_only) {   // not graph-eligible: nothing launched, the caller enqueues it plainly
+    prepare_only->fn = nullptr;
+    return OPMM_OK;
+  }
   return launch_fit_and_merge(h, fn, a, grid, block, smem, s_begin, S, multi, out_dev);
 }
 
@@ -1600,7 +1606,10 @@ opmm_status opmm_fit(opmm_handle* h, const double* recorded, const opmm_control*
       }
       CK(cudaGraphLaunch(h->fit_graph, h->stream));
       h->timed = true;
-    } else {   // launched directly by enqueue_fit
+    } else {   // not graph-eligible (top-K / certify): this call's trace, then plain launches
+      CK(cudaMemcpyAsync(h->rec, h->rec_stage, ns * sizeof(double), cudaMemcpyHostToDevice,
+                         h->stream));
+      CKS(enqueue_fit(h, rec_dev, ctl, nullptr, 0, 1, space, n_candidates, opts, h->result, true));
       CK(cudaMemcpyAsync(h->result_host, h->result, sizeof(opmm_fit_result),
                          cudaMemcpyDeviceToHost, h->stream));
     }
@@ -1626,6 +1635,34 @@ opmm_status opmm_fit(opmm_handle* h, const double* recorded, const opmm_control*
   }
   if (out->best_index < 0) return fail(OPMM_ERR_NO_FINITE, "no candidate has a finite error");
   return OPMM_OK;
+}
+
+// One rank's share of a fit on a plain handle, for callers that bring their
+// own launcher and merge on the host (opmm.h): the handle's rank/world
+// select the shard for this call only; everything else is opmm_fit.
+opmm_status opmm_fit_shard(opmm_handle* h, const double* recorded, const opmm_control* ctl,
+                           const opmm_search_space* space, int64_t n_candidates, int rank,
+                           int world, const opmm_fit_options* opts, opmm_fit_result* out) {
+  CKS(check_handle(h));
+  if (h->comm != nullptr)
+    return fail(OPMM_ERR_INVALID_ARG, "opmm_fit_shard takes a plain handle (an NCCL handle shards itself)");
+  if (world < 1 || rank < 0 || rank >= world)
+    return fail(OPMM_ERR_INVALID_ARG, "rank %d / world %d", rank, world);
+  opmm_fit_options o;
+  if (opts) {
+    o = *opts;
+  } else {   // opmm_fit's defaults for a NULL opts
+    std::memset(&o, 0, sizeof(o));
+    o.cpu_check = 1;
+  }
+  o.flags |= OPMM_FIT_FLAG_NO_GRAPH;   // shards differ in their launch bytes
+  const int r0 = h->rank, w0 = h->world;
+  h->rank = rank;
+  h->world = world;
+  const opmm_status st = opmm_fit(h, recorded, ctl, space, n_candidates, &o, out);
+  h->rank = r0;
+  h->world = w0;
+  return st;
 }
 
 opmm_status opmm_fit_batch(opmm_handle* h, const double* recorded, int64_t S,

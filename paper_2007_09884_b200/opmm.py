@@ -127,6 +127,8 @@ def _load():
                       C.POINTER(FitOptions), C.POINTER(FitResult)], st),
         "opmm_fit_async": ([vp, vp, C.POINTER(Control), C.POINTER(SearchSpace), i64,
                             C.POINTER(FitOptions), vp], st),
+        "opmm_fit_shard": ([vp, vp, C.POINTER(Control), C.POINTER(SearchSpace), i64, C.c_int, C.c_int,
+                            C.POINTER(FitOptions), C.POINTER(FitResult)], st),
         "opmm_fit_batch": ([vp, vp, i64, C.POINTER(Control), C.POINTER(SearchSpace), i64,
                             C.POINTER(FitOptions), C.POINTER(FitResult)], st),
         "opmm_estimate_batch": ([vp, vp, i64, C.POINTER(Control), vp, C.POINTER(NmOptions),
@@ -146,7 +148,7 @@ EXPORTED = ("opmm_version", "opmm_last_error", "opmm_create", "opmm_nccl_unique_
             "opmm_shard_range", "opmm_merge_argmin", "opmm_merge_topk", "opmm_certify_topk",
             "opmm_validate", "opmm_generate",
             "opmm_simulate", "opmm_simulate_batch", "opmm_score", "opmm_simulate_score", "opmm_fit", "opmm_fit_async",
-            "opmm_fit_batch", "opmm_estimate_batch", "opmm_nm_minimize_test")
+            "opmm_fit_shard", "opmm_fit_batch", "opmm_estimate_batch", "opmm_nm_minimize_test")
 
 
 def lib():
@@ -411,6 +413,19 @@ def opmm_fit_async(h: Handle, recorded_dev, ctl, space, n_candidates: int, out_d
 
 def decode_result(raw: bytes) -> dict:
     return FitResult.from_buffer_copy(raw).as_dict()
+
+
+def opmm_fit_shard(h: Handle, recorded, ctl, space, n_candidates: int, rank: int, world: int,
+                   options: FitOptions | None = None) -> dict:
+    """Rank `rank` of `world`'s share of a fit on a plain handle (opmm.h)."""
+    out = FitResult()
+    rec = recorded
+    if isinstance(recorded, np.ndarray):
+        rec = np.ascontiguousarray(recorded, dtype=np.float64)
+    opts = options if options is not None else fit_options()
+    _check(_lib.opmm_fit_shard(h.ptr, _ptr(rec), C.byref(_ctl(ctl)), C.byref(_space(space)),
+                               n_candidates, rank, world, C.byref(opts), C.byref(out)), "opmm_fit_shard")
+    return out.as_dict()
 
 
 def opmm_fit_batch(h: Handle, recorded, ctls, space, n_per: int,

@@ -674,6 +674,93 @@ def test_grid_level_tables_beyond_2_32_and_population(opmm, h):
                 assert (res[k]["best_index"], res[k]["opt_err"]) == (ref_res[k]["best_index"], ref_res[k]["opt_err"])
 
 
+def test_sync_fit_with_topk_uses_this_calls_trace(opmm):
+    """Regression: opmm_fit with a host trace and top_k / certify (the
+    non-graph path) must stage THIS call's trace -- on a fresh handle, and
+    after a graph-path fit of a different trace."""
+    ctl = W.Control()
+    a = trace(ctl)
+    b = oracle.positions(W.truth_opc(pw_ms=30.0), ctl) + W.noise(101, seed=77)
+    sp = W.paper_space()
+    n = 50000
+    with opmm.opmm_create(0) as hh:
+        outs = {}
+        for name, r in (("a", a), ("b", b)):
+            out = torch.zeros(ctypes_sizeof_fitresult(opmm), dtype=torch.uint8, device="cuda")
+            opmm.opmm_fit_async(hh, dev(r), ctl, sp, n, out, opmm.fit_options(top_k=8))
+            torch.cuda.synchronize()
+            outs[name] = opmm.decode_result(bytes(out.cpu().numpy()))
+    with opmm.opmm_create(0) as hh:
+        r1 = opmm.opmm_fit(hh, b, ctl, sp, n, opmm.fit_options(top_k=8))        # fresh handle
+        assert (r1["best_index"], r1["opt_err"], r1["topk_index"]) == \
+               (outs["b"]["best_index"], outs["b"]["opt_err"], outs["b"]["topk_index"])
+        opmm.opmm_fit(hh, a, ctl, sp, n)                                          # graph path, trace a
+        r2 = opmm.opmm_fit(hh, b, ctl, sp, n, opmm.fit_options(top_k=8))        # then b with top-K
+        assert (r2["best_index"], r2["opt_err"], r2["topk_index"]) == \
+               (outs["b"]["best_index"], outs["b"]["opt_err"], outs["b"]["topk_index"])
+        r3 = opmm.opmm_fit(hh, a, ctl, sp, n, opmm.fit_options(precision=opmm.FP32, certify=1))
+        assert r3["certified"] == 1 and r3["best_index"] == outs["a"]["best_index"]
+
+
+def ctypes_sizeof_fitresult(opmm):
+    import ctypes
+    return ctypes.sizeof(opmm.FitResult)
+
+
+def _merge_shards(opmm, parts, K=0):
+    be, bi = opmm.opmm_merge_argmin([p["opt_err"] if p["best_index"] >= 0 else np.inf for p in parts],
+                                    [p["best_index"] for p in parts])
+    out = {"best_index": bi, "opt_err": be, "n_finite": sum(p["n_finite"] for p in parts),
+           "n_evaluated": sum(p["n_evaluated"] for p in parts)}
+    if K:
+        oe, oi = opmm.opmm_merge_topk([p["topk_err"][:K] for p in parts], [p["topk_index"][:K] for p in parts], K)
+        out["topk_err"], out["topk_index"] = oe.tolist(), oi.tolist()
+    return out
+
+
+def test_fit_shard_partitions_and_merges(opmm, h):
+    """opmm_fit_shard (SURVEY 8(e) on a plain handle, host merge): the
+    per-rank kernels of a sharded fit -- candidate ranges starting past 0,
+    each rank's partial, its top-K list -- merged on the host equal the single
+    fit, for several world sizes; FP32 certification per shard composes to
+    the certified single-GPU winner; the superposition kernel shards grid
+    nodes and merges to the same winner."""
+    ctl = W.Control()
+    rec = trace(ctl)
+    sp = W.paper_space()
+    n = 300001
+    K = 8
+    full = opmm.opmm_fit(h, rec, ctl, sp, n, opmm.fit_options(top_k=K))
+    for world in (2, 3, 7):
+        parts = [opmm.opmm_fit_shard(h, rec, ctl, sp, n, r, world, opmm.fit_options(top_k=K))
+                 for r in range(world)]
+        for r, p in enumerate(parts):
+            lo, hi = opmm.opmm_shard_range(n, r, world)
+            assert p["n_evaluated"] == hi - lo
+            assert p["best_index"] < 0 or lo <= p["best_index"] < hi
+        m = _merge_shards(opmm, parts, K)
+        assert (m["best_index"], m["opt_err"], m["n_finite"], m["n_evaluated"]) == \
+               (full["best_index"], full["opt_err"], full["n_finite"], n), world
+        assert m["topk_index"] == full["topk_index"][:K] and m["topk_err"] == full["topk_err"][:K], world
+    # fp32 certified: every shard certified, merged winner = the certified single fit's
+    c = opmm.opmm_fit(h, rec, ctl, sp, n, opmm.fit_options(precision=opmm.FP32, certify=1))
+    parts = [opmm.opmm_fit_shard(h, rec, ctl, sp, n, r, 4, opmm.fit_options(precision=opmm.FP32, certify=1))
+             for r in range(4)]
+    assert all(p["certified"] == 1 for p in parts)
+    m = _merge_shards(opmm, parts)
+    assert c["certified"] == 1 and (m["best_index"], m["opt_err"]) == (c["best_index"], c["opt_err"])
+    # the superposition kernel (auto on this grid) shards nodes
+    g = W.g4_space(20)
+    fg = opmm.opmm_fit(h, rec, ctl, g, g.n_grid())
+    parts = [opmm.opmm_fit_shard(h, rec, ctl, g, g.n_grid(), r, 3) for r in range(3)]
+    m = _merge_shards(opmm, parts)
+    assert (m["best_index"], m["opt_err"], m["n_finite"], m["n_evaluated"]) == \
+           (fg["best_index"], fg["opt_err"], fg["n_finite"], g.n_grid())
+    with pytest.raises(opmm.OpmmError) as ei:
+        opmm.opmm_fit_shard(h, rec, ctl, sp, n, 3, 3)
+    assert ei.value.status == opmm.ERR_INVALID_ARG
+
+
 def test_fit_async_matches_sync(opmm, h):
     import ctypes
     ctl = W.Control()

@@ -73,6 +73,29 @@ int main(void) {
   printf("top-5:");
   for (int k = 0; k < 5; ++k) printf(" %lld (%.6f)", (long long)r5.topk_index[k], r5.topk_err[k]);
   printf("\n");
+  /* the same fit as three ranks' shares (opmm_fit_shard), merged on the host */
+  {
+    enum { R = 3 };
+    opmm_fit_result part[R];
+    double pe[R], le[R * 5];
+    int64_t pi[R], li[R * 5];
+    for (int k = 0; k < R; ++k) {
+      if ((st = opmm_fit_shard(h, rec, &ctl, &sp, 100000, k, R, &opts, &part[k])) != OPMM_OK) return 14;
+      pe[k] = part[k].opt_err;
+      pi[k] = part[k].best_index;
+      for (int j = 0; j < 5; ++j) {
+        le[k * 5 + j] = part[k].topk_err[j];
+        li[k * 5 + j] = part[k].topk_index[j];
+      }
+    }
+    double be, me[5];
+    int64_t bi, mi[5];
+    if (opmm_merge_argmin(pe, pi, R, &be, &bi) != OPMM_OK || bi != r.best_index || be != r.opt_err) return 15;
+    if (opmm_merge_topk(le, li, R, 5, me, mi) != OPMM_OK) return 16;
+    for (int j = 0; j < 5; ++j)
+      if (mi[j] != r5.topk_index[j] || me[j] != r5.topk_err[j]) return 17;
+    printf("3 shards merged on the host: best %lld, top-5 identical\n", (long long)bi);
+  }
   /* host buffers through the asynchronous entry points */
   enum { NC = 64 };
   static double opc[OPMM_NPARAM * NC], traj[101 * NC], e_score[NC], e_fused[NC];

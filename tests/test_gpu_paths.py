@@ -1,0 +1,110 @@
+"""Equivalence of the library's call paths (-m gpu).
+
+One fit can reach the kernels through several host paths: the synchronous
+opmm_fit (CUDA-graph replay for plain fits, plain launches for top-K /
+certified fits), opmm_fit_async on device buffers, opmm_fit_batch
+(gridDim.y = saccades), and opmm_fit_shard (one rank's share).  The kernels
+are the same, so every path must give the same result for the same inputs,
+whatever the handle did before.  These tests sweep the option combinations
+(precision, metric, top_k, certify, kernel variant, grid tables) over fresh
+handles and over handles that just fitted a different trace -- the kind of
+cross-call state that hid a stale-trace bug in the plain-launch path of
+opmm_fit until round 2.
+"""
+import ctypes
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def opmm():
+    if not torch.cuda.is_available():
+        pytest.fail("no CUDA device: the -m gpu suite must run on a B200")
+    from paper_2007_09884_b200 import build
+    build.build()
+    from paper_2007_09884_b200 import opmm as m
+    return m
+
+
+def traces(ctl):
+    a = oracle.positions(W.truth_opc(), ctl) + W.noise(ctl.n_steps + 1)
+    b = oracle.positions(W.truth_opc(pw_ms=31.0), ctl) + W.noise(ctl.n_steps + 1, seed=99)
+    return a, b
+
+
+def key(r):
+    return (r["best_index"], r["opt_err"], r["n_finite"], r["n_evaluated"], r["top_k"], r["certified"],
+            tuple(r["topk_index"]), tuple(r["topk_err"]))
+
+
+def via_async(opmm, h, rec, ctl, sp, n, o):
+    out = torch.zeros(ctypes.sizeof(opmm.FitResult), dtype=torch.uint8, device="cuda")
+    opmm.opmm_fit_async(h, torch.as_tensor(rec, device="cuda"), ctl, sp, n, out, o)
+    torch.cuda.synchronize()
+    return opmm.decode_result(bytes(out.cpu().numpy()))
+
+
+CASES = [
+    ("fp64", "paper", dict()),
+    ("fp64 rms", "paper", dict(metric=1)),
+    ("fp64 top7", "paper", dict(top_k=7)),
+    ("fp32", "paper", dict(precision=1)),
+    ("fp32 certify", "paper", dict(precision=1, certify=1)),
+    ("fp32 certify rms top12", "paper", dict(precision=1, certify=1, metric=1, top_k=12)),
+    ("refill", "paper", dict(kernel_variant=5)),
+    ("grid tables", "grid", dict(kernel_variant=1)),
+    ("grid tables top3", "grid", dict(kernel_variant=1, top_k=3)),
+    ("superposition", "grid", dict()),
+    ("superposition fp32", "grid", dict(precision=1)),
+]
+
+
+@pytest.mark.parametrize("name,space,kw", CASES, ids=[c[0] for c in CASES])
+def test_sync_async_and_history_agree(opmm, name, space, kw):
+    """opmm_fit on a fresh handle, opmm_fit right after a fit of another
+    trace, opmm_fit_async on device buffers, and opmm_fit without the CUDA
+    graph: identical results (winner, counts, top-K list, certificate)."""
+    ctl = W.Control()
+    a, b = traces(ctl)
+    sp = W.paper_space() if space == "paper" else W.g4_space(16)
+    n = 60001 if space == "paper" else sp.n_grid()
+    o = opmm.fit_options(cpu_check=0, **kw)
+    with opmm.opmm_create(0) as h:
+        ref = via_async(opmm, h, b, ctl, sp, n, o)
+    with opmm.opmm_create(0) as h:
+        fresh = opmm.opmm_fit(h, b, ctl, sp, n, o)
+    with opmm.opmm_create(0) as h:
+        opmm.opmm_fit(h, a, ctl, sp, n, opmm.fit_options(cpu_check=0))              # graph path, trace a
+        opmm.opmm_fit(h, a, ctl, sp, n, opmm.fit_options(cpu_check=0, top_k=4))     # plain path, trace a
+        after = opmm.opmm_fit(h, b, ctl, sp, n, o)
+        nograph = opmm.opmm_fit(h, b, ctl, sp, n, opmm.fit_options(cpu_check=0, flags=opmm.FIT_FLAG_NO_GRAPH,
+                                                                    **kw))
+        again = via_async(opmm, h, b, ctl, sp, n, o)
+    for r in (fresh, after, nograph, again):
+        assert key(r) == key(ref), name
+
+
+@pytest.mark.parametrize("kw", [dict(), dict(top_k=6), dict(precision=1, certify=1)],
+                         ids=["plain", "top6", "fp32-certify"])
+def test_batch_saccade0_equals_single_fit(opmm, kw):
+    """Saccade 0 of opmm_fit_batch (Philox counter word 2 = 0, per-saccade
+    amplitude and pw_default from the batch's control table, one slice per
+    block) equals opmm_fit of the same trace and control."""
+    ctl0 = W.Control(amplitude_deg=12.0, pw_default_ms=35.0)
+    a, b = traces(ctl0)
+    sp = W.paper_space()
+    n = 40000
+    ctls = [ctl0, W.Control(amplitude_deg=7.0, pw_default_ms=25.0), W.Control(amplitude_deg=20.0)]
+    recs = np.stack([a, b, a])
+    o = opmm.fit_options(cpu_check=0, **kw)
+    with opmm.opmm_create(0) as h:
+        res = opmm.opmm_fit_batch(h, recs, ctls, sp, n, o)
+        single = opmm.opmm_fit(h, a, ctl0, sp, n, o)
+    assert key(res[0]) == key(single)

@@ -11,6 +11,8 @@
 #include <cstring>
 #include <dlfcn.h>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include <cuda_runtime.h>
 #include <nccl.h>
@@ -1082,6 +1084,30 @@ opmm_status nm_collect(opmm_handle* h, int64_t pb, int64_t pe, int dim, opmm_nm_
 // ===========================================================================
 // C ABI
 // ===========================================================================
+// The paper's CPU_check for a batch: one serial fp64 re-score per saccade,
+// independent, so they run on the host's cores (up to 32 threads, shared
+// among the ranks of an NCCL handle; the calling thread takes a share).
+// Below `grain` saccades per thread it stays on the calling thread.
+template <typename F>
+void host_parallel_for(int64_t n, int world, F&& f, int64_t grain = 32) {
+  const unsigned hw = std::thread::hardware_concurrency();
+  int64_t T = hw ? (int64_t)hw / (world > 0 ? world : 1) : 1;
+  if (T > 32) T = 32;
+  if (T > n / grain) T = n / grain;
+  if (T <= 1) {
+    for (int64_t i = 0; i < n; ++i) f(i);
+    return;
+  }
+  auto run = [&](int64_t t) {
+    for (int64_t i = n * t / T; i < n * (t + 1) / T; ++i) f(i);
+  };
+  std::vector<std::thread> th;
+  th.reserve((size_t)(T - 1));
+  for (int64_t t = 1; t < T; ++t) th.emplace_back(run, t);
+  run(0);
+  for (auto& x : th) x.join();
+}
+
 extern "C" {
 
 const char* opmm_version(void) { return "libopmm 0.1.0 (sm_100a)"; }
@@ -1720,13 +1746,13 @@ opmm_status opmm_fit_batch(opmm_handle* h, const double* recorded, int64_t S,
     CK(cudaMemcpy(&tmp[0], recorded, (size_t)S * ns * sizeof(double), cudaMemcpyDeviceToHost));
     rec_host = reinterpret_cast<const double*>(tmp.data());
   }
-  for (int64_t j = 0; j < Sl; ++j) {
+  const int metric = opts ? opts->metric : 0;
+  host_parallel_for(Sl, h->world, [&](int64_t j) {
     opmm_fit_result r = h->result_host[j];
     if (want_check && r.best_index >= 0)
-      r.cpu_check = opmm::cpu_check_score(r.opc, rec_host + (size_t)(sb + j) * ns, ctl + sb + j,
-                                           opts ? opts->metric : 0);
+      r.cpu_check = opmm::cpu_check_score(r.opc, rec_host + (size_t)(sb + j) * ns, ctl + sb + j, metric);
     out[sb + j] = r;
-  }
+  });
   return OPMM_OK;
 }
 
@@ -1788,8 +1814,10 @@ opmm_status opmm_estimate_batch(opmm_handle* h, const double* recorded, int64_t 
       CK(cudaMemcpy(&tmp[0], recorded, tmp.size(), cudaMemcpyDeviceToHost));
       rec_host = reinterpret_cast<const double*>(tmp.data());
     }
-    for (int64_t s = sb; s < se; ++s)
+    host_parallel_for(se - sb, h->world, [&](int64_t j) {
+      const int64_t s = sb + j;
       out[s].cpu_check = opmm::cpu_check_score(out[s].x, rec_host + (size_t)s * ns, ctl + s, c.metric);
+    });
   }
   return OPMM_OK;
 }

@@ -344,6 +344,58 @@ def _ctl(c):
     return c if isinstance(c, Control) else control(c)
 
 
+def _ctl_array(ctls):
+    """[S] Control array for the batch entry points, filled column-wise
+    (the same conversions as control())."""
+    S = len(ctls)
+    arr = (Control * S)()
+    a = np.frombuffer(arr, dtype=np.dtype(Control))
+    if all(isinstance(c, Control) for c in ctls):
+        for k in range(S):
+            arr[k] = ctls[k]
+        return arr
+    a["dt_ms"] = [float(c.dt_ms) for c in ctls]
+    a["n_steps"] = [int(c.n_steps) for c in ctls]
+    a["substeps"] = [int(getattr(c, "substeps", 0)) for c in ctls]
+    a["amplitude_deg"] = [float(c.amplitude_deg) for c in ctls]
+    a["theta0_deg"] = [float(c.theta0_deg) for c in ctls]
+    a["pw_default_ms"] = [float(c.pw_default_ms) for c in ctls]
+    return arr
+
+
+def _fit_results(out, lo: int, hi: int) -> list:
+    """[S] FitResult -> list of FitResult.as_dict() for entries [lo, hi), None
+    elsewhere (other ranks' saccades), converted column-wise."""
+    S = len(out)
+    a = np.frombuffer(out, dtype=np.dtype(FitResult))[lo:hi]
+    P = np.array(a["opc"])
+    TI, TE = a["topk_index"], a["topk_err"]
+    cols = zip(a["best_index"].tolist(), a["opt_err"].tolist(), a["cpu_check"].tolist(),
+               a["n_finite"].tolist(), a["n_evaluated"].tolist(), a["top_k"].tolist(),
+               a["certified"].tolist())
+    res = [None] * S
+    for k, (bi, oe, cc, nf, ne, tk, ce) in enumerate(cols):
+        res[lo + k] = {"best_index": bi, "opt_err": oe, "cpu_check": cc, "opc": P[k], "n_finite": nf,
+                       "n_evaluated": ne, "top_k": tk, "certified": ce,
+                       "topk_index": TI[k, :tk].tolist() if tk else [],
+                       "topk_err": TE[k, :tk].tolist() if tk else []}
+    return res
+
+
+def _nm_results(out, lo: int, hi: int) -> list:
+    """[S] NmResult -> list of NmResult.as_dict() for [lo, hi), None elsewhere."""
+    S = len(out)
+    a = np.frombuffer(out, dtype=np.dtype(NmResult))[lo:hi]
+    X = np.array(a["x"])
+    cols = zip(a["f_best"].tolist(), a["cpu_check"].tolist(), a["iterations"].tolist(),
+               a["func_evals"].tolist(), a["gpu_evals"].tolist(), a["exit_reason"].tolist())
+    res = [None] * S
+    for k, (f, cc, it, fe, ge, er) in enumerate(cols):
+        res[lo + k] = {"x": X[k], "f": f, "cpu_check": cc, "iterations": it, "func_evals": fe,
+                       "gpu_evals": ge, "exit_reason": er}
+    return res
+
+
 def _space(s):
     return s if isinstance(s, SearchSpace) else search_space(s)
 
@@ -431,7 +483,7 @@ def opmm_fit_shard(h: Handle, recorded, ctl, space, n_candidates: int, rank: int
 def opmm_fit_batch(h: Handle, recorded, ctls, space, n_per: int,
                    options: FitOptions | None = None) -> list[dict]:
     S = len(ctls)
-    arr = (Control * S)(*[_ctl(c) for c in ctls])
+    arr = _ctl_array(ctls)
     out = (FitResult * S)()
     rec = recorded
     if isinstance(recorded, np.ndarray):
@@ -440,7 +492,7 @@ def opmm_fit_batch(h: Handle, recorded, ctls, space, n_per: int,
     _check(_lib.opmm_fit_batch(h.ptr, _ptr(rec), S, arr, C.byref(_space(space)), n_per,
                                C.byref(opts), out), "opmm_fit_batch")
     lo, hi = opmm_shard_range(S, h.rank, h.world)
-    return [out[s].as_dict() if lo <= s < hi else None for s in range(S)]
+    return _fit_results(out, lo, hi)
 
 
 # ---------------------------------------------------------------------- Nelder-Mead
@@ -455,7 +507,7 @@ def nm_options(precision=FP64, objective=NM_OBJ_PROPAGATOR, metric=METRIC_L1, ma
 def opmm_estimate_batch(h: Handle, recorded, ctls, x0=None, options: NmOptions | None = None) -> list:
     """Nelder-Mead OPC estimation of S saccades (recorded [S, n_steps+1])."""
     S = len(ctls)
-    arr = (Control * S)(*[_ctl(c) for c in ctls])
+    arr = _ctl_array(ctls)
     out = (NmResult * S)()
     rec = recorded
     if isinstance(recorded, np.ndarray):
@@ -465,7 +517,7 @@ def opmm_estimate_batch(h: Handle, recorded, ctls, x0=None, options: NmOptions |
                                     C.byref(options if options is not None else nm_options()), out),
            "opmm_estimate_batch")
     lo, hi = opmm_shard_range(S, h.rank, h.world)
-    return [out[s].as_dict() if lo <= s < hi else None for s in range(S)]
+    return _nm_results(out, lo, hi)
 
 
 def opmm_nm_minimize_test(h: Handle, fn_id: int, x0, options: NmOptions | None = None) -> list:

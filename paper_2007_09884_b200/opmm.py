@@ -66,11 +66,12 @@ class FitResult(C.Structure):
                 ("topk_err", C.c_double * MAX_TOPK)]
 
     def as_dict(self) -> dict:
+        tk = self.top_k
         return {"best_index": self.best_index, "opt_err": self.opt_err, "cpu_check": self.cpu_check,
-                "opc": np.array(self.opc[:]), "n_finite": self.n_finite,
-                "n_evaluated": self.n_evaluated, "top_k": self.top_k, "certified": self.certified,
-                "topk_index": list(self.topk_index[:self.top_k]),
-                "topk_err": list(self.topk_err[:self.top_k])}
+                "opc": np.frombuffer(self.opc, dtype=np.float64).copy(), "n_finite": self.n_finite,
+                "n_evaluated": self.n_evaluated, "top_k": tk, "certified": self.certified,
+                "topk_index": self.topk_index[:tk] if tk else [],
+                "topk_err": self.topk_err[:tk] if tk else []}
 
 
 class NmOptions(C.Structure):

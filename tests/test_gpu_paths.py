@@ -108,3 +108,23 @@ def test_batch_saccade0_equals_single_fit(opmm, kw):
         res = opmm.opmm_fit_batch(h, recs, ctls, sp, n, o)
         single = opmm.opmm_fit(h, a, ctl0, sp, n, o)
     assert key(res[0]) == key(single)
+
+
+def test_workspace_growth_and_reuse(opmm):
+    """One handle through fits of growing and shrinking size and changing
+    options (its workspaces -- partials, counters, top-K buffers, error
+    workspace, staging -- grow and are reused) gives each fit the result a
+    fresh handle gives."""
+    ctl = W.Control()
+    a, b = traces(ctl)
+    sp = W.paper_space()
+    seq = [(a, 1000, dict()), (b, 200001, dict(top_k=32)), (a, 37, dict(top_k=5)),
+           (b, 1000003, dict(precision=1, certify=1)), (a, 1000, dict(top_k=9, metric=1)),
+           (b, 5, dict(precision=1, certify=1, top_k=3)), (a, 300000, dict(kernel_variant=5)),
+           (b, 1000, dict())]
+    with opmm.opmm_create(0) as h:
+        got = [opmm.opmm_fit(h, r, ctl, sp, n, opmm.fit_options(cpu_check=0, **kw)) for r, n, kw in seq]
+    for (r, n, kw), g in zip(seq, got):
+        with opmm.opmm_create(0) as hf:
+            ref = opmm.opmm_fit(hf, r, ctl, sp, n, opmm.fit_options(cpu_check=0, **kw))
+        assert key(g) == key(ref), (n, kw)

@@ -128,3 +128,56 @@ def test_workspace_growth_and_reuse(opmm):
         with opmm.opmm_create(0) as hf:
             ref = opmm.opmm_fit(hf, r, ctl, sp, n, opmm.fit_options(cpu_check=0, **kw))
         assert key(g) == key(ref), (n, kw)
+
+
+def test_explicit_entry_points_host_equals_device(opmm):
+    """opmm_generate / opmm_simulate / opmm_score / opmm_simulate_score with
+    host (numpy) buffers give exactly the device-buffer results; a host
+    output with a leading dimension larger than n keeps the entries the call
+    does not write; opmm_fit_batch and opmm_estimate_batch take device traces
+    with the same results as host ones."""
+    ctl = W.Control()
+    a, b = traces(ctl)
+    sp = W.paper_space()
+    n, ld = 300, 311
+    with opmm.opmm_create(0) as h:
+        s = torch.cuda.current_stream()
+        opc_d = torch.zeros((18, ld), dtype=torch.float64, device="cuda")
+        opmm.opmm_generate(h, sp, 1000, n, opc_d, ld=ld, stream=s)
+        opc_h = np.full((18, ld), 7.0)
+        opmm.opmm_generate(h, sp, 1000, n, opc_h, ld=ld)
+        torch.cuda.synchronize()
+        assert np.array_equal(opc_h[:, :n], opc_d.cpu().numpy()[:, :n]) and np.all(opc_h[:, n:] == 7.0)
+        tr_d = torch.zeros((101, n), dtype=torch.float64, device="cuda")
+        st_d = torch.zeros(n, dtype=torch.uint8, device="cuda")
+        opmm.opmm_simulate(h, opc_d, n, ctl, tr_d, ld=ld, status=st_d, stream=s)
+        tr_h, st_h = np.zeros((101, n)), np.zeros(n, dtype=np.uint8)
+        opmm.opmm_simulate(h, opc_h, n, ctl, tr_h, ld=ld, status=st_h)
+        torch.cuda.synchronize()
+        assert np.array_equal(tr_h, tr_d.cpu().numpy(), equal_nan=True)
+        assert np.array_equal(st_h, st_d.cpu().numpy())
+        for metric in (0, 1):
+            e_d = torch.zeros(n, dtype=torch.float64, device="cuda")
+            opmm.opmm_score(h, tr_d, n, 101, torch.as_tensor(b, device="cuda"), e_d, metric=metric, stream=s)
+            e_h = np.zeros(n)
+            opmm.opmm_score(h, tr_h, n, 101, b, e_h, metric=metric)
+            f_d = torch.zeros(n, dtype=torch.float64, device="cuda")
+            opmm.opmm_simulate_score(h, opc_d, n, ctl, torch.as_tensor(b, device="cuda"), f_d, metric=metric,
+                                     ld=ld, stream=s)
+            f_h = np.zeros(n)
+            opmm.opmm_simulate_score(h, opc_h, n, ctl, b, f_h, metric=metric, ld=ld)
+            torch.cuda.synchronize()
+            assert np.array_equal(e_h, e_d.cpu().numpy(), equal_nan=True)
+            assert np.array_equal(f_h, f_d.cpu().numpy(), equal_nan=True)
+        recs = np.stack([a, b, b, a])
+        ctls = [W.Control(amplitude_deg=10.0 + k) for k in range(4)]
+        fh = opmm.opmm_fit_batch(h, recs, ctls, sp, 3000, opmm.fit_options(cpu_check=1))
+        fd = opmm.opmm_fit_batch(h, torch.as_tensor(recs, device="cuda"), ctls, sp, 3000,
+                                 opmm.fit_options(cpu_check=1))
+        assert [key(x) + (x["cpu_check"],) for x in fh] == [key(x) + (x["cpu_check"],) for x in fd]
+        o = opmm.nm_options(max_iter=300)
+        nh = opmm.opmm_estimate_batch(h, recs, ctls, options=o)
+        nd = opmm.opmm_estimate_batch(h, torch.as_tensor(recs, device="cuda"), ctls, options=o)
+        for x, y in zip(nh, nd):
+            assert np.array_equal(x["x"], y["x"]) and (x["f"], x["iterations"], x["cpu_check"]) == \
+                   (y["f"], y["iterations"], y["cpu_check"])

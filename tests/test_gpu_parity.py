@@ -795,6 +795,43 @@ def test_edge_empty_single_ragged(opmm, h):
         assert np.array_equal(np.isinf(E), np.isinf(o["err"]))
 
 
+@pytest.mark.parametrize("precision", [0, 1])
+def test_fit_space_with_nonphysical_candidates(opmm, h, precision):
+    """A search space whose candidates are not all physical (B_AG and N_C_AG
+    ranges crossing zero): the fit kernel runs the per-candidate physical
+    check (SPEC D8, reading Q13) and scores violators with the penalty
+    1e10 (1 + sum of violations) exactly as the oracle does; the argmin is
+    unaffected.  Random and grid (level tables) spaces; variants that need a
+    physical space refuse it."""
+    ctl = W.Control()
+    rec = trace(ctl)
+    d = W.truth_opc()
+    sp = W.paper_space()
+    sp.log_scale[I["B_AG"]] = 0
+    sp.lo[I["B_AG"]], sp.hi[I["B_AG"]] = -0.2 * d[I["B_AG"]], 3.0 * d[I["B_AG"]]
+    sp.log_scale[I["N_C_AG"]] = 0
+    sp.lo[I["N_C_AG"]], sp.hi[I["N_C_AG"]] = -0.5 * d[I["N_C_AG"]], 2.0 * d[I["N_C_AG"]]
+    g = W.grid_space({"B_AG": (-0.2 * d[I["B_AG"]], 3.0 * d[I["B_AG"]], 40, False),
+                      "PW": (10.0, 60.0, 26, False)})
+    for space, n in ((sp, 20000), (g, g.n_grid())):
+        r, E = _fit(opmm, h, rec, ctl, space, n, precision=precision)
+        o = oracle.fit(rec, ctl, space, 0, n, want_err=True)
+        O = o["err"]
+        pen = np.array([oracle.physical_penalty(oracle.generate(space, i)) for i in range(n)])
+        assert (pen > 0).sum() > n // 20                          # the check is exercised
+        assert np.array_equal(E[pen > 0], O[pen > 0])             # penalties exact
+        assert r["best_index"] == o["best_index"]
+        if precision == 0:
+            rel, _, _ = oracle.relativize(rec, ctl.amplitude_deg)
+            f = pen == 0
+            assert_fp64_errors(E[f], O[f], lambda i, f=np.flatnonzero(f): oracle.generate(space, int(f[i])),
+                               rec, ctl, np.abs(rel).sum())
+    for kv in (2, 3, 5):
+        with pytest.raises(opmm.OpmmError) as ei:
+            _fit(opmm, h, rec, ctl, sp, 1000, kernel_variant=kv)
+        assert ei.value.status == opmm.ERR_UNSUPPORTED
+
+
 def test_edge_all_diverged(opmm, h):
     ctl = W.Control()
     rec = trace(ctl, noisy=False)

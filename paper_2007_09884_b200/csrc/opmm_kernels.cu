@@ -271,9 +271,18 @@ __device__ void finalize_topk(const FitArgs& a, int64_t sac, double le, int64_t 
 constexpr int TOPK_THREADS = 256;
 constexpr int TOPK_MAXFG = 512;   // fit blocks per saccade the threshold step ranks (smem 16 B each)
 
+// Launched with programmatic dependent launch (launch_pdl): the grid may be
+// scheduled while the fit kernel drains; griddepcontrol.wait holds every
+// thread until the fit grid has completed and its writes are visible (a no-op
+// when launched plainly).
+__device__ __forceinline__ void wait_for_producer_grid() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 template <int METRIC>
 __global__ void __launch_bounds__(TOPK_THREADS) topk_kernel(FitArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  wait_for_producer_grid();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = TOPK_THREADS / 32;
   const int K = a.topk;
   const int G = gridDim.x;
@@ -404,6 +413,7 @@ __global__ void __launch_bounds__(TOPK_THREADS) topk_kernel(FitArgs a) {
 template <int METRIC>
 __global__ void __launch_bounds__(32) cert_kernel(FitArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  wait_for_producer_grid();
   const int lane = threadIdx.x & 31;
   const int64_t sac = (int64_t)blockIdx.x + a.sac_begin;
   opmm_fit_result* out = a.final_out + (sac - a.out_base);
@@ -1789,6 +1799,24 @@ const void* topk_kernel_ptr(int metric) {
                      : reinterpret_cast<const void*>(&topk_kernel<1>);
 }
 
+// Programmatic dependent launch: the kernel may start while the previous
+// kernel on the stream finishes; it waits for it in-kernel
+// (wait_for_producer_grid), which hides the launch gap between the two.
+static cudaError_t launch_pdl(const void* fn, dim3 grid, dim3 block, void** args, size_t smem,
+                              cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelExC(&cfg, fn, args);
+}
+
 cudaError_t launch_topk(const FitArgs& a, int blocks, int S, size_t smem, int metric,
                         cudaStream_t st) {
   for (int s0 = 0; s0 < S; s0 += 65535) {
@@ -1796,8 +1824,8 @@ cudaError_t launch_topk(const FitArgs& a, int blocks, int S, size_t smem, int me
     b.sac_begin = a.sac_begin + s0;
     void* bargs[] = {&b};
     const int sn = S - s0 < 65535 ? S - s0 : 65535;
-    const cudaError_t e = cudaLaunchKernel(topk_kernel_ptr(metric), dim3(blocks, sn), dim3(TOPK_BLOCK),
-                                           bargs, smem, st);
+    const cudaError_t e = launch_pdl(topk_kernel_ptr(metric), dim3(blocks, sn), dim3(TOPK_BLOCK),
+                                     bargs, smem, st);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
@@ -1814,7 +1842,7 @@ cudaError_t launch_cert(const FitArgs& a, int S, size_t smem, int metric, cudaSt
     b.sac_begin = a.sac_begin + s0;
     void* bargs[] = {&b};
     const int sn = S - s0 < 65535 ? S - s0 : 65535;
-    const cudaError_t e = cudaLaunchKernel(cert_kernel_ptr(metric), dim3(sn), dim3(32), bargs, smem, st);
+    const cudaError_t e = launch_pdl(cert_kernel_ptr(metric), dim3(sn), dim3(32), bargs, smem, st);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;

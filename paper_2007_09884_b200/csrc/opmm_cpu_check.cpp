@@ -22,17 +22,18 @@ struct Plant {
 
 // D1: T_m = K_SE_m (x_m - s_m theta); B_m x_m' = f_m - N_C_m s_m theta - K_LT_m x_m - T_m;
 // f_m' = (n_m - f_m)/tau_m; J omega' = T_AG - T_ANT - B_P omega; theta' = omega.
-void deriv(const Plant& P, const double y[6], const double n[2], const double inv_tau_s[2],
-           double dy[6]) {
-  const double sgn[2] = {1.0, -1.0};
-  double T[2];
-  for (int m = 0; m < 2; ++m) T[m] = P.kse[m] * (y[2 + m] - sgn[m] * y[0]);
+// (s_AG = +1, s_ANT = -1; written out per muscle so the compiler keeps the
+// state in registers)
+inline void deriv(const Plant& P, const double y[6], const double n[2], const double inv_tau_s[2],
+                  double dy[6]) {
+  const double t0 = P.kse[0] * (y[2] - y[0]);
+  const double t1 = P.kse[1] * (y[3] + y[0]);
   dy[0] = y[1];
-  dy[1] = (T[0] - T[1] - P.bp * y[1]) * P.inv_J;
-  for (int m = 0; m < 2; ++m) {
-    dy[2 + m] = (y[4 + m] - P.nc[m] * sgn[m] * y[0] - P.klt[m] * y[2 + m] - T[m]) * P.inv_b[m];
-    dy[4 + m] = (n[m] - y[4 + m]) * inv_tau_s[m];
-  }
+  dy[1] = (t0 - t1 - P.bp * y[1]) * P.inv_J;
+  dy[2] = (y[4] - P.nc[0] * y[0] - P.klt[0] * y[2] - t0) * P.inv_b[0];
+  dy[3] = (y[5] + P.nc[1] * y[0] - P.klt[1] * y[3] - t1) * P.inv_b[1];
+  dy[4] = (n[0] - y[4]) * inv_tau_s[0];
+  dy[5] = (n[1] - y[5]) * inv_tau_s[1];
 }
 
 }  // namespace

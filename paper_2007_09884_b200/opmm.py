@@ -206,6 +206,8 @@ def _ptr(x):
     if hasattr(x, "data_ptr"):
         return x.data_ptr()
     if isinstance(x, np.ndarray):
+        if x.flags.c_contiguous and x.flags.writeable and x.size:
+            return C.addressof(C.c_char.from_buffer(x))   # ~1 us cheaper than .ctypes.data
         return x.ctypes.data
     raise TypeError(f"cannot take a pointer of {type(x)}")
 

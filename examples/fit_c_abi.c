@@ -114,6 +114,28 @@ int main(void) {
     n_ok += status[i] == 0;
   }
   printf("host buffers: %d candidates simulated + scored, %d finite, scores agree\n", NC, n_ok);
+  /* the paper's own estimator: batched Nelder-Mead on 4 copies of the trace
+   * (Table 1 defaults as the start, 60 iterations at most) */
+  {
+    enum { S = 4 };
+    static double recs[S * 101];
+    opmm_control ctls[S];
+    opmm_nm_result nm[S];
+    for (int k = 0; k < S; ++k) {
+      memcpy(recs + k * 101, rec, sizeof(double) * 101);
+      ctls[k] = ctl;
+    }
+    opmm_nm_options no;
+    memset(&no, 0, sizeof(no));
+    no.max_iter = 60;
+    no.cpu_check = 1;
+    if ((st = opmm_estimate_batch(h, recs, S, ctls, NULL, &no, nm)) != OPMM_OK) return 18;
+    for (int k = 1; k < S; ++k)
+      if (nm[k].f_best != nm[0].f_best || nm[k].iterations != nm[0].iterations) return 19;
+    if (!(fabs(nm[0].cpu_check - nm[0].f_best) <= 1e-9 * nm[0].f_best)) return 20;
+    printf("Nelder-Mead: f %.6f after %d iterations (exit %d), CPU_check agrees\n", nm[0].f_best,
+           nm[0].iterations, nm[0].exit_reason);
+  }
   /* invalid argument: error status + message, nothing launched */
   ctl.dt_ms = -1.0;
   st = opmm_fit(h, rec, &ctl, &sp, 10, &opts, &r);

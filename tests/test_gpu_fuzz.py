@@ -1,0 +1,127 @@
+"""Seeded random configurations against the oracle (-m gpu).
+
+Each case draws a search space (random or grid; every dimension fixed,
+linear or log with random bounds around Table 1, some crossing into the
+non-physical region), a control (dt, n_steps, amplitude given or from the
+trace, theta0, pw_default, substeps), a metric and the fit options
+(precision, top_k, certify, kernel variant), then checks the fit against the
+oracle's exhaustive evaluation of the same candidates: FP64 errors within the
+parity rule, the argmin and n_finite identical, the
+top-K list the exact lexicographic top-K of the errors; FP32 with the same
+classification and, when certified, the FP64 winner.  Small sizes so the
+oracle finishes in a second per case.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+from test_gpu_parity import assert_fp64_errors, rk4_stable
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+I = W.IDX
+
+
+@pytest.fixture(scope="module")
+def opmm():
+    if not torch.cuda.is_available():
+        pytest.fail("no CUDA device: the -m gpu suite must run on a B200")
+    from paper_2007_09884_b200 import build
+    build.build()
+    from paper_2007_09884_b200 import opmm as m
+    return m
+
+
+@pytest.fixture(scope="module")
+def h(opmm):
+    with opmm.opmm_create(0) as handle:
+        yield handle
+
+
+def draw_case(seed):
+    rng = np.random.default_rng(seed)
+    d = np.array(W.TABLE1_DEFAULTS, dtype=np.float64)
+    d[I["PW"]] = 40.0
+    dt = float(rng.choice([0.5, 1.0, 2.0]))
+    n_steps = int(rng.choice([1, 2, 7, 50, 100, 151, 300]))
+    ctl = W.Control(dt_ms=dt, n_steps=n_steps,
+                    amplitude_deg=float(rng.choice([10.0, -7.5, 25.0, np.nan])),
+                    theta0_deg=float(rng.uniform(-5, 5)), pw_default_ms=float(rng.uniform(5, 60)),
+                    substeps=int(rng.choice([0, 0, 0, 2])))
+    grid = rng.random() < 0.4
+    lo, hi = d.copy(), d.copy()
+    logs = np.zeros(18, dtype=np.uint8)
+    levels = np.ones(18, dtype=np.int32)
+    dims = rng.choice(18, size=int(rng.integers(1, 6 if grid else 18)), replace=False)
+    for k in dims:
+        kind = rng.choice(["log", "lin", "lin_cross"])
+        if kind == "log":
+            lo[k], hi[k], logs[k] = d[k] * rng.uniform(0.1, 0.9), d[k] * rng.uniform(1.1, 10), 1
+        elif kind == "lin":
+            lo[k], hi[k] = d[k] * rng.uniform(0.2, 0.9), d[k] * rng.uniform(1.1, 3)
+        else:   # may cross zero: non-physical candidates
+            lo[k], hi[k] = -0.3 * d[k], d[k] * rng.uniform(1.1, 3)
+        if k == I["PW"]:
+            lo[k] = dt * rng.uniform(0.5, 2)
+            hi[k], logs[k] = max(dt * n_steps * rng.uniform(0.5, 1.5), 1.5 * lo[k]), 0
+    if grid:
+        for k in dims:
+            levels[k] = int(rng.integers(2, 9))
+        sp = W.SearchSpace(1, 0, lo, hi, logs, levels)
+        n = int(np.prod(levels.astype(np.int64)))
+    else:
+        sp = W.SearchSpace(0, int(rng.integers(0, 2**40)), lo, hi, logs, levels)
+        n = int(rng.choice([1, 33, 999, 4000]))
+    metric = int(rng.integers(0, 2))
+    precision = int(rng.integers(0, 2))
+    top_k = int(rng.choice([0, 0, 1, 5, 32]))
+    certify = int(precision == 1 and rng.random() < 0.5)
+    kv = int(rng.choice([0, 0, 1, 5]))
+    return ctl, sp, n, metric, precision, top_k, certify, kv
+
+
+@pytest.mark.parametrize("seed", range(80))
+def test_random_configuration(opmm, h, seed):
+    ctl, sp, n, metric, precision, top_k, certify, kv = draw_case(seed)
+    rng = np.random.default_rng(1000 + seed)
+    truth = np.array(W.TABLE1_DEFAULTS, dtype=np.float64)
+    truth[I["PW"]] = 0.4 * ctl.n_steps * ctl.dt_ms + ctl.dt_ms
+    c0 = W.Control(dt_ms=ctl.dt_ms, n_steps=ctl.n_steps,
+                   amplitude_deg=10.0 if np.isnan(ctl.amplitude_deg) else ctl.amplitude_deg,
+                   theta0_deg=ctl.theta0_deg, pw_default_ms=ctl.pw_default_ms, substeps=ctl.substeps)
+    rec = oracle.positions(truth, c0) + rng.normal(0.0, 0.02, ctl.n_steps + 1)
+    err = torch.full((n,), -1.0, dtype=torch.float64, device="cuda")
+    o = opmm.fit_options(precision=precision, metric=metric, top_k=top_k, certify=certify, kernel_variant=kv,
+                         err_out=err)
+    try:
+        r = opmm.opmm_fit(h, rec, ctl, sp, n, o)
+    except opmm.OpmmError as e:
+        # the only refusals: variants that need a physical space / the propagator / no top-K
+        assert e.status == opmm.ERR_UNSUPPORTED and kv == 5, (seed, e)
+        return
+    E = err.cpu().numpy()
+    orc = oracle.fit(rec, ctl, sp, 0, n, metric=metric, want_err=True)
+    O = orc["err"]
+    assert r["n_evaluated"] == n
+    assert np.array_equal(np.isinf(E), np.isinf(O)), seed
+    assert r["n_finite"] == orc["n_finite"], seed
+    rel, _, _ = oracle.relativize(rec, ctl.amplitude_deg)
+    scale = np.abs(rel).sum() if metric == 0 else np.sqrt(np.mean(rel ** 2))
+    if precision == 0:
+        assert_fp64_errors(E, O, lambda i: oracle.generate(sp, i), rec, ctl, scale, metric)
+        assert r["best_index"] == orc["best_index"], seed
+    else:
+        # FP32 scope: RK4-stable candidates
+        f = np.flatnonzero(np.isfinite(O))
+        st = np.array([rk4_stable(oracle.generate(sp, int(i)), ctl) for i in f], dtype=bool)
+        g = f[st] if f.size else f
+        assert np.all(np.abs(E[g] - O[g]) <= 1e-4 * np.maximum(O[g], scale)), seed
+        if certify and r["certified"] == 1:
+            assert r["best_index"] == orc["best_index"], seed
+    K = top_k if top_k else (8 if certify else 0)
+    if K:
+        m = min(K, n)
+        order = np.lexsort((np.arange(n), E))[:m].tolist()
+        assert r["top_k"] == K and r["topk_index"][:m] == order, seed

@@ -125,3 +125,39 @@ def test_random_configuration(opmm, h, seed):
         m = min(K, n)
         order = np.lexsort((np.arange(n), E))[:m].tolist()
         assert r["top_k"] == K and r["topk_index"][:m] == order, seed
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_random_population_batch(opmm, h, seed):
+    """opmm_fit_batch on random configurations: S saccades with their own
+    amplitude / pw_default (Philox counter word 2 = saccade), every
+    saccade's errors, argmin and n_finite against the oracle's fit of that
+    saccade."""
+    ctl, sp, n, metric, precision, top_k, certify, kv = draw_case(500 + seed)
+    rng = np.random.default_rng(2000 + seed)
+    S = int(rng.integers(1, 5))
+    ctls, recs = [], []
+    for s in range(S):
+        c = W.Control(dt_ms=ctl.dt_ms, n_steps=ctl.n_steps, amplitude_deg=float(rng.uniform(5, 30)),
+                      theta0_deg=ctl.theta0_deg, pw_default_ms=float(rng.uniform(5, 60)), substeps=ctl.substeps)
+        truth = np.array(W.TABLE1_DEFAULTS, dtype=np.float64)
+        truth[I["PW"]] = rng.uniform(0.2, 0.6) * ctl.n_steps * ctl.dt_ms + ctl.dt_ms
+        ctls.append(c)
+        recs.append(oracle.positions(truth, c) + rng.normal(0.0, 0.02, ctl.n_steps + 1))
+    recs = np.array(recs)
+    err = torch.full((S, n), -1.0, dtype=torch.float64, device="cuda")
+    o = opmm.fit_options(precision=0, metric=metric, top_k=top_k, err_out=err,
+                         kernel_variant=kv if kv != 5 else 1)
+    res = opmm.opmm_fit_batch(h, recs, ctls, sp, n, o)
+    E = err.cpu().numpy()
+    for s in range(S):
+        orc = oracle.fit(recs[s], ctls[s], sp, 0, n, metric=metric, saccade=s, want_err=True)
+        rel, _, _ = oracle.relativize(recs[s], ctls[s].amplitude_deg)
+        scale = np.abs(rel).sum() if metric == 0 else np.sqrt(np.mean(rel ** 2))
+        assert np.array_equal(np.isinf(E[s]), np.isinf(orc["err"])), (seed, s)
+        assert_fp64_errors(E[s], orc["err"], lambda i, s=s: oracle.generate(sp, i, saccade=s), recs[s], ctls[s],
+                           scale, metric)
+        assert (res[s]["best_index"], res[s]["n_finite"]) == (orc["best_index"], orc["n_finite"]), (seed, s)
+        if top_k:
+            m = min(top_k, n)
+            assert res[s]["topk_index"][:m] == np.lexsort((np.arange(n), E[s]))[:m].tolist(), (seed, s)

@@ -161,3 +161,42 @@ def test_random_population_batch(opmm, h, seed):
         if top_k:
             m = min(top_k, n)
             assert res[s]["topk_index"][:m] == np.lexsort((np.arange(n), E[s]))[:m].tolist(), (seed, s)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_nelder_mead_reference_bit_exact(opmm, h, seed):
+    """Batched Nelder-Mead with the reference-order objective on random
+    controls, start vectors, metrics, tolerances and initial scales, in all
+    three schedules: every run bit-identical to the oracle's serial
+    Lagarias run (x, f, iterations, evaluations, exit reason)."""
+    rng = np.random.default_rng(3000 + seed)
+    n_steps = int(rng.choice([20, 60, 150]))
+    dt = float(rng.choice([0.5, 1.0]))
+    S = int(rng.integers(1, 6))
+    ctls, recs = [], []
+    for s in range(S):
+        c = W.Control(dt_ms=dt, n_steps=n_steps, amplitude_deg=float(rng.uniform(5, 30)),
+                      pw_default_ms=float(rng.uniform(0.2, 0.6) * n_steps * dt + dt))
+        truth = np.array(W.TABLE1_DEFAULTS, dtype=np.float64)
+        truth *= np.exp(rng.uniform(-0.2, 0.2, 18))
+        truth[I["PW"]] = c.pw_default_ms
+        ctls.append(c)
+        recs.append(oracle.positions(truth, c) + rng.normal(0.0, 0.02, n_steps + 1))
+    recs = np.array(recs)
+    x0 = np.array(W.TABLE1_DEFAULTS, dtype=np.float64) * np.exp(rng.uniform(-0.3, 0.3, 18))
+    x0[I["PW"]] = np.nan
+    metric = int(rng.integers(0, 2))
+    tol = float(rng.choice([1e-4, 1e-6]))
+    scale = float(rng.choice([0.05, 0.1]))
+    max_iter = int(rng.choice([30, 120]))
+    o = oracle.estimate_batch(recs, ctls, x0=x0, metric=metric, init_scale=scale, tol_x=tol, tol_f=tol,
+                              max_iter=max_iter)
+    for schedule in (1, 2, 3):
+        opts = opmm.nm_options(objective=opmm.NM_OBJ_REFERENCE, metric=metric, max_iter=max_iter, tol_x=tol,
+                               tol_f=tol, init_scale=scale, schedule=schedule, cpu_check=0)
+        res = opmm.opmm_estimate_batch(h, recs, ctls, x0=x0, options=opts)
+        for s in range(S):
+            r = res[s]
+            assert r["x"].tolist() == o["x"][s].tolist(), (seed, schedule, s)
+            assert r["f"] == o["f"][s] and (r["iterations"], r["func_evals"], r["exit_reason"]) == \
+                   (o["iterations"][s], o["func_evals"][s], o["exit_reason"][s]), (seed, schedule, s)

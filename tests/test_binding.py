@@ -3,9 +3,17 @@ opmm_fit_batch / opmm_estimate_batch give exactly the per-struct dicts."""
 import math
 
 import numpy as np
+import pytest
 
 import workloads as W
-from paper_2007_09884_b200 import opmm
+
+
+@pytest.fixture(scope="module")
+def opmm():
+    from paper_2007_09884_b200 import build
+    build.build()   # the binding loads libopmm.so at import
+    from paper_2007_09884_b200 import opmm as m
+    return m
 
 
 def _same(d1, d2):
@@ -20,7 +28,7 @@ def _same(d1, d2):
             assert a == b and type(a) is type(b), (k, a, b)
 
 
-def test_fit_results_match_as_dict():
+def test_fit_results_match_as_dict(opmm):
     rng = np.random.default_rng(3)
     S = 7
     out = (opmm.FitResult * S)()
@@ -42,7 +50,7 @@ def test_fit_results_match_as_dict():
                 assert res[k] is None
 
 
-def test_nm_results_match_as_dict():
+def test_nm_results_match_as_dict(opmm):
     rng = np.random.default_rng(4)
     S = 5
     out = (opmm.NmResult * S)()
@@ -60,7 +68,7 @@ def test_nm_results_match_as_dict():
             assert res[k] is None
 
 
-def test_control_array_matches_per_struct():
+def test_control_array_matches_per_struct(opmm):
     ctls = [W.Control(n_steps=150, amplitude_deg=5.0 + k, pw_default_ms=30.0 + k, substeps=k % 3)
             for k in range(9)]
     ref = (opmm.Control * 9)(*[opmm.control(c) for c in ctls])

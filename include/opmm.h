@@ -235,9 +235,15 @@ opmm_status opmm_create_nccl(opmm_handle** h, int device, const uint8_t* nccl_id
 opmm_status opmm_destroy(opmm_handle* h);
 /* The handle's own stream (cudaStream_t), for callers that want to order work. */
 opmm_status opmm_get_stream(opmm_handle* h, void** stream);
+/* Kernel timing, off by default: when on, every launch through the handle is
+ * bracketed by a pair of CUDA events on its stream (~6 us of stream time per
+ * call on a B200), and opmm_last_kernel_ms reads them. */
+opmm_status opmm_set_kernel_timing(opmm_handle* h, int32_t on);
 /* Device time (ms, CUDA events on the launching stream) of the most recent
- * fit/simulate kernel launched through this handle (synchronises the handle's
- * stream). */
+ * launch through this handle while timing was on: the kernels of one fit /
+ * simulate / score / estimate call (a synchronous opmm_fit: its H2D copy and
+ * kernel).  Synchronises with that launch.  INVALID_ARG when timing is off or
+ * nothing has been launched since it was turned on. */
 opmm_status opmm_last_kernel_ms(opmm_handle* h, float* ms);
 
 /* ---- host-only helpers (no GPU needed) ----------------------------------- */

@@ -113,6 +113,7 @@ def _load():
         "opmm_destroy": ([vp], st),
         "opmm_get_stream": ([vp, C.POINTER(vp)], st),
         "opmm_last_kernel_ms": ([vp, C.POINTER(C.c_float)], st),
+        "opmm_set_kernel_timing": ([vp, C.c_int32], st),
         "opmm_shard_range": ([i64, C.c_int, C.c_int, C.POINTER(i64), C.POINTER(i64)], st),
         "opmm_merge_argmin": ([dp, C.POINTER(i64), C.c_int, dp, C.POINTER(i64)], st),
         "opmm_validate": ([C.POINTER(Control), C.POINTER(SearchSpace), i64], st),
@@ -145,7 +146,7 @@ def _load():
 
 _lib = _load()
 EXPORTED = ("opmm_version", "opmm_last_error", "opmm_create", "opmm_nccl_unique_id",
-            "opmm_create_nccl", "opmm_destroy", "opmm_get_stream", "opmm_last_kernel_ms",
+            "opmm_create_nccl", "opmm_destroy", "opmm_get_stream", "opmm_last_kernel_ms", "opmm_set_kernel_timing",
             "opmm_shard_range", "opmm_merge_argmin", "opmm_merge_topk", "opmm_certify_topk",
             "opmm_validate", "opmm_generate",
             "opmm_simulate", "opmm_simulate_batch", "opmm_score", "opmm_simulate_score", "opmm_fit", "opmm_fit_async",
@@ -268,8 +269,17 @@ def opmm_version() -> str:
     return _lib.opmm_version().decode()
 
 
-def opmm_create(device: int = 0) -> Handle:
-    return Handle(device)
+def opmm_create(device: int = 0, kernel_timing: bool = False) -> Handle:
+    """kernel_timing: bracket every launch with CUDA events so that
+    opmm_last_kernel_ms can report it (costs ~6 us of stream time per call)."""
+    h = Handle(device)
+    if kernel_timing:
+        opmm_set_kernel_timing(h, True)
+    return h
+
+
+def opmm_set_kernel_timing(h, on: bool = True):
+    _check(_lib.opmm_set_kernel_timing(h.ptr, 1 if on else 0), "opmm_set_kernel_timing")
 
 
 def opmm_nccl_unique_id() -> bytes:

@@ -181,3 +181,29 @@ def test_explicit_entry_points_host_equals_device(opmm):
         for x, y in zip(nh, nd):
             assert np.array_equal(x["x"], y["x"]) and (x["f"], x["iterations"], x["cpu_check"]) == \
                    (y["f"], y["iterations"], y["cpu_check"])
+
+
+def test_kernel_timing_is_opt_in(opmm):
+    """opmm_last_kernel_ms needs opmm_set_kernel_timing: off by default (no
+    timing events on the stream), then every entry point's launch is timed,
+    the synchronous graph path included; turning it off again drops it."""
+    ctl = W.Control()
+    a, _ = traces(ctl)
+    sp = W.paper_space()
+    with opmm.opmm_create(0) as h:
+        opmm.opmm_fit(h, a, ctl, sp, 20000)
+        with pytest.raises(opmm.OpmmError) as ei:
+            opmm.opmm_last_kernel_ms(h)
+        assert ei.value.status == opmm.ERR_INVALID_ARG
+        opmm.opmm_set_kernel_timing(h, True)
+        for o in (opmm.fit_options(), opmm.fit_options(top_k=4), opmm.fit_options(precision=1, certify=1)):
+            r = opmm.opmm_fit(h, a, ctl, sp, 20000, o)
+            assert opmm.opmm_last_kernel_ms(h) > 0.0 and r["best_index"] >= 0
+        via_async(opmm, h, a, ctl, sp, 20000, opmm.fit_options())
+        assert opmm.opmm_last_kernel_ms(h) > 0.0
+        opmm.opmm_set_kernel_timing(h, False)
+        with pytest.raises(opmm.OpmmError):
+            opmm.opmm_last_kernel_ms(h)
+    with opmm.opmm_create(0, kernel_timing=True) as h:
+        opmm.opmm_fit(h, a, ctl, sp, 20000)
+        assert opmm.opmm_last_kernel_ms(h) > 0.0

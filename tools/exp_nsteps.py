@@ -15,7 +15,7 @@ from paper_2007_09884_b200 import opmm  # noqa: E402
 
 prec = int(sys.argv[1]) if len(sys.argv) > 1 else 0
 N = 10**6
-with opmm.opmm_create(0) as h:
+with opmm.opmm_create(0, kernel_timing=True) as h:
     out = torch.zeros(ctypes.sizeof(opmm.FitResult), dtype=torch.uint8, device="cuda")
     s = torch.cuda.ExternalStream(h.stream)
     res = []

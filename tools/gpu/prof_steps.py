@@ -10,7 +10,7 @@ import torch, workloads as W
 from paper_2007_09884_b200 import opmm
 sys.path.insert(0, os.path.join(ROOT, "tools"))
 from synth_trace import truth_trace
-with opmm.opmm_create(0) as h:
+with opmm.opmm_create(0, kernel_timing=True) as h:
     out = torch.zeros(ctypes.sizeof(opmm.FitResult), dtype=torch.uint8, device="cuda")
     for n_steps in (int(x) for x in sys.argv[1:]):
         ctl = W.Control(n_steps=n_steps)

@@ -28,7 +28,7 @@ if new_api:
               ("fp64 top32", dict(precision=0, top_k=32)), ("fp32 certify K=32", dict(precision=1, certify=1, top_k=32)),
               ("fp64 nosort", dict(precision=0, flags=1)), ("fp64 block 192", dict(precision=0, block_size=192)),
               ("fp64 block 128", dict(precision=0, block_size=128))]
-with opmm.opmm_create(0) as h:
+with opmm.opmm_create(0, kernel_timing=True) as h:
     recd = torch.as_tensor(rec, device="cuda")
     out = torch.zeros(ctypes.sizeof(opmm.FitResult), dtype=torch.uint8, device="cuda")
     for name, kw in modes:

@@ -22,7 +22,7 @@ from synth_trace import truth_trace  # noqa: E402
 
 tag = os.path.basename(pkg.rstrip("/")) if pkg != ROOT else "repo"
 n = 10**6
-with opmm.opmm_create(0) as h:
+with opmm.opmm_create(0, kernel_timing=True) as h:
     for n_steps in (100, 150, 300):
         ctl = W.Control(n_steps=n_steps)
         rec = truth_trace(opmm, h, ctl)

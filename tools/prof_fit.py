@@ -16,7 +16,7 @@ prec = int(sys.argv[1]) if len(sys.argv) > 1 else 0
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 10**6
 rec = np.loadtxt(os.path.join(ROOT, "tests", "golden", "trace_truth_A10_dt1_n100.txt")) + W.noise(101)
 ctl, sp = W.Control(), W.paper_space()
-with opmm.opmm_create(0) as h:
+with opmm.opmm_create(0, kernel_timing=True) as h:
     recd = torch.as_tensor(rec, device="cuda")
     out = torch.zeros(ctypes.sizeof(opmm.FitResult), dtype=torch.uint8, device="cuda")
     torch.cuda.synchronize()

@@ -26,7 +26,7 @@ if L:
         "N_SAC_AG": (d[I["N_SAC_AG"]] * 0.5, d[I["N_SAC_AG"]] * 2.0, L, True),
         "PW": (1.0, 100.0, 100, False)})
 n = sp.n_grid()
-with opmm.opmm_create(0) as h:
+with opmm.opmm_create(0, kernel_timing=True) as h:
     recd = torch.as_tensor(rec, device="cuda")
     out = torch.zeros(ctypes.sizeof(opmm.FitResult), dtype=torch.uint8, device="cuda")
     torch.cuda.synchronize()

@@ -7,7 +7,7 @@ import workloads as W
 from paper_2007_09884_b200 import opmm
 rec = np.loadtxt(os.path.join(ROOT, "tests/golden/trace_truth_A10_dt1_n100.txt")) + W.noise(101)
 ctl, sp = W.Control(), W.paper_space()
-with opmm.opmm_create(0) as h:
+with opmm.opmm_create(0, kernel_timing=True) as h:
     recd = torch.as_tensor(rec, device="cuda")
     out = torch.zeros(ctypes.sizeof(opmm.FitResult), dtype=torch.uint8, device="cuda")
     for N in (56832, 200000, 1000000):

@@ -16,7 +16,7 @@ from paper_2007_09884_b200 import opmm  # noqa: E402
 rec = np.loadtxt(os.path.join(ROOT, "tests/golden/trace_truth_A10_dt1_n100.txt")) + W.noise(101)
 rec = torch.as_tensor(rec).pin_memory().numpy()
 ctl, sp = W.Control(), W.paper_space()
-with opmm.opmm_create(0) as h:
+with opmm.opmm_create(0, kernel_timing=True) as h:
     for n in (1000, 10**6):
         for chk in (0, 1):
             o = opmm.fit_options(cpu_check=chk)

@@ -18,7 +18,7 @@ rec = torch.as_tensor(np.loadtxt(os.path.join(ROOT, "tests/golden/trace_truth_A1
                       + W.noise(101)).pin_memory().numpy()
 ctl, sp = opmm.control(W.Control()), opmm.search_space(W.paper_space())
 lib = opmm.lib()
-with opmm.opmm_create(0) as h:
+with opmm.opmm_create(0, kernel_timing=True) as h:
     for n in (1000, 10**6):
         for chk in (0, 1):
             o = opmm.fit_options(cpu_check=chk)

@@ -24,7 +24,7 @@ cases = [("G4 tables fp64", W.g4_space(100), dict(kernel_variant=1)),
          ("G4 generic fp32", W.g4_space(100), dict(kernel_variant=1, precision=1, flags=opmm.FIT_FLAG_NO_GRID_TABLES)),
          ("S_paper fp64", W.paper_space(), dict()),
          ("S_paper fp32", W.paper_space(), dict(precision=1))]
-with opmm.opmm_create(0) as h:
+with opmm.opmm_create(0, kernel_timing=True) as h:
     rec = torch.as_tensor(truth_trace(opmm, h, ctl, noisy=False), device="cuda")
     out = torch.zeros(ctypes.sizeof(opmm.FitResult), dtype=torch.uint8, device="cuda")
     for name, sp, kw in cases:

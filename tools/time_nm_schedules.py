@@ -14,7 +14,7 @@ import bench  # noqa: E402
 from paper_2007_09884_b200 import opmm  # noqa: E402
 
 sizes = [int(a) for a in sys.argv[1:]] or [16, 64, 256, 1024, 4096, 16384]
-with opmm.opmm_create(0) as h:
+with opmm.opmm_create(0, kernel_timing=True) as h:
     ctls, recs = bench.population_traces(h, opmm, torch, max(sizes), 150)
     for S in sizes:
         row, runs = [], []

@@ -14,7 +14,7 @@ from paper_2007_09884_b200 import opmm  # noqa: E402
 
 peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
 ns = 101
-with opmm.opmm_create(0) as h:
+with opmm.opmm_create(0, kernel_timing=True) as h:
     for prec, dt in ((0, torch.float64), (1, torch.float32)):
         for n in (10**6, 4 * 10**6):
             traj = torch.randn((ns, n), dtype=dt, device="cuda")

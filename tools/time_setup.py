@@ -13,7 +13,7 @@ import workloads as W  # noqa: E402
 from paper_2007_09884_b200 import opmm  # noqa: E402
 
 N = 10**6
-with opmm.opmm_create(0) as h:
+with opmm.opmm_create(0, kernel_timing=True) as h:
     out = torch.zeros(ctypes.sizeof(opmm.FitResult), dtype=torch.uint8, device="cuda")
     line = []
     for prec in (0, 1):

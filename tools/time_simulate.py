@@ -12,7 +12,7 @@ import workloads as W  # noqa: E402
 from paper_2007_09884_b200 import opmm  # noqa: E402
 
 n, ns = 10**6, 101
-with opmm.opmm_create(0) as h:
+with opmm.opmm_create(0, kernel_timing=True) as h:
     opc = torch.empty((18, n), dtype=torch.float64, device="cuda")
     st = torch.cuda.current_stream()
     opmm.opmm_generate(h, W.paper_space(), 0, n, opc, stream=st)

@@ -4,7 +4,7 @@ import torch
 sys.path.insert(0, os.environ.get("GRAFT_REPO_ROOT", "/root/repo"))
 import workloads as W
 from paper_2007_09884_b200 import opmm
-with opmm.opmm_create(0) as h:
+with opmm.opmm_create(0, kernel_timing=True) as h:
     out = torch.zeros(ctypes.sizeof(opmm.FitResult), dtype=torch.uint8, device="cuda")
     rec = torch.linspace(0, 10, 101, dtype=torch.float64, device="cuda")
     for s in (0, 2, 4, 16, 64):

@@ -28,7 +28,7 @@ for L in (10, 32, 100, 400):
         "B_AG": (d[I["B_AG"]] * 0.7, d[I["B_AG"]] * 1.5, others // k, True),
         "N_SAC_AG": (d[I["N_SAC_AG"]] * 0.5, d[I["N_SAC_AG"]] * 2.0, L, True),
         "PW": (1.0, 100.0, npw, False)})))
-with opmm.opmm_create(0) as h:
+with opmm.opmm_create(0, kernel_timing=True) as h:
     rec = torch.as_tensor(truth_trace(opmm, h, ctl), device="cuda")
     out = torch.zeros(ctypes.sizeof(opmm.FitResult), dtype=torch.uint8, device="cuda")
     for name, sp in grids:

@@ -78,7 +78,19 @@ def draw_case(seed):
     precision = int(rng.integers(0, 2))
     top_k = int(rng.choice([0, 0, 1, 5, 32]))
     certify = int(precision == 1 and rng.random() < 0.5)
-    kv = int(rng.choice([0, 0, 1, 5]))
+    kv = int(rng.choice([0, 0, 1, 5] + ([4, 4] if grid else [])))
+    if grid and kv == 4 and rng.random() < 0.7:   # make superposition eligible most of the time
+        k = I["N_SAC_AG"] if rng.random() < 0.5 else I["N_SAC_ANT"]
+        lo[k], hi[k], logs[k] = d[k] * 0.5, d[k] * 2.0, 1
+        levels[k] = int(rng.integers(8, 40))
+        for j in range(18):
+            if lo[j] < 0:
+                lo[j] = 0.1 * max(hi[j], 1e-9)
+        if I["PW"] in dims:
+            lo[I["PW"]] = max(lo[I["PW"]], 1e-3)
+        sp = W.SearchSpace(1, 0, lo, hi, logs, levels)
+        n = int(np.prod(levels.astype(np.int64)))
+        top_k, certify = 0, 0
     return ctl, sp, n, metric, precision, top_k, certify, kv
 
 
@@ -98,8 +110,9 @@ def test_random_configuration(opmm, h, seed):
     try:
         r = opmm.opmm_fit(h, rec, ctl, sp, n, o)
     except opmm.OpmmError as e:
-        # the only refusals: variants that need a physical space / the propagator / no top-K
-        assert e.status == opmm.ERR_UNSUPPORTED and kv == 5, (seed, e)
+        # the only refusals: variants that need a physical space / the propagator /
+        # no top-K (5), or a grid with a superposable pulse height (4)
+        assert e.status == opmm.ERR_UNSUPPORTED and kv in (4, 5), (seed, e)
         return
     E = err.cpu().numpy()
     orc = oracle.fit(rec, ctl, sp, 0, n, metric=metric, want_err=True)
@@ -147,7 +160,7 @@ def test_random_population_batch(opmm, h, seed):
     recs = np.array(recs)
     err = torch.full((S, n), -1.0, dtype=torch.float64, device="cuda")
     o = opmm.fit_options(precision=0, metric=metric, top_k=top_k, err_out=err,
-                         kernel_variant=kv if kv != 5 else 1)
+                         kernel_variant=kv if kv in (0, 1) else 0)
     res = opmm.opmm_fit_batch(h, recs, ctls, sp, n, o)
     E = err.cpu().numpy()
     for s in range(S):

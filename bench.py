@@ -428,10 +428,14 @@ def nm_leg(h, opmm, torch, args, max_over_ranks=lambda x: x, sum_over_ranks=lamb
     S, n_steps = args.nm_saccades, 150
     ctls, recs = population_traces(h, opmm, torch, S, n_steps)
     opts = opmm.nm_options(cpu_check=0)
-    opmm.opmm_estimate_batch(h, recs[:64], ctls[:64], options=opts)   # warm-up
-    t0 = time.perf_counter()
-    res = opmm.opmm_estimate_batch(h, recs, ctls, options=opts)
-    e2e_s = time.perf_counter() - t0
+    # warm-up at the full size (the handle's workspaces are sized on first use), then two timed calls
+    opmm.opmm_estimate_batch(h, recs, ctls, options=opts)
+    walls = []
+    for _ in range(2):
+        t0 = time.perf_counter()
+        res = opmm.opmm_estimate_batch(h, recs, ctls, options=opts)
+        walls.append(time.perf_counter() - t0)
+    e2e_s = min(walls)
     # N > 1: saccades are sharded over the ranks (opmm_estimate_batch); the
     # statistics below are this rank's share, the times the max over ranks
     kern_ms = max_over_ranks(opmm.opmm_last_kernel_ms(h))
